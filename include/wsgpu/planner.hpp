@@ -1,0 +1,381 @@
+// planner.hpp — host-side C++ drop-in for the reference planner interface.
+//
+// Mirrors the value types of the reference planner API
+//   WorkloadSpec/ModuleDecl/TaskDecl/InputSize   workload.hpp:16-69
+//   CurvePiece/ProfilePoint/ScalingCurve          scaling.hpp:16-164
+//   ClusterTopology                               topology.hpp:15-53
+//   MetaOp/MetaGraph/ComputationGraph             graph.hpp:13-58
+//   AslTuple/TuplePair/AllocationPlan/Options     allocation.hpp:17-46
+//   Wave/WaveEntry/WavefrontSchedule              schedule.hpp:15-35
+//   Flow/PlacementOptions                         placement.hpp:42-109
+//   PlanEntity/ExecutionPlan                      plan_io.hpp:21-51
+//   PlannerOptions/PlannerResult/plan_workload    planner.hpp:21-38,156
+// with the same field names and meaning, so callers switch by namespace.
+// plan_workload() here encodes the inputs into the ws_abi.h batch format,
+// runs the sm_100a kernels through the C-ABI and decodes the result; errors
+// are rethrown as the same exception classes with the same what() text.
+#pragma once
+
+#include <cstdint>
+#include <map>
+#include <memory>
+#include <optional>
+#include <set>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "wsgpu/ws_abi.h"
+
+namespace wsgpu {
+
+// ---- exception taxonomy (common.hpp:20-60) --------------------------------
+struct Error : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+struct ParseError : Error {
+    using Error::Error;
+};
+struct InfeasibleError : Error {
+    using Error::Error;
+};
+struct InvariantError : Error {
+    using Error::Error;
+};
+struct CyclicWorkload : ParseError {
+    using ParseError::ParseError;
+};
+struct UnknownModule : ParseError {
+    using ParseError::ParseError;
+};
+struct EmptyWorkload : ParseError {
+    using ParseError::ParseError;
+};
+struct InsufficientProfile : ParseError {
+    using ParseError::ParseError;
+};
+struct DegenerateFit : InfeasibleError {
+    using InfeasibleError::InfeasibleError;
+};
+struct OutOfRange : InvariantError {
+    using InvariantError::InvariantError;
+};
+struct NoValidAllocation : InfeasibleError {
+    using InfeasibleError::InfeasibleError;
+};
+struct EmptyLevel : InvariantError {
+    using InvariantError::InvariantError;
+};
+struct PlacementInfeasible : InfeasibleError {
+    using InfeasibleError::InfeasibleError;
+};
+// Input outside the device limits of this build (ws_abi.h WS_MAX_*).
+struct LimitExceeded : Error {
+    using Error::Error;
+};
+
+std::string fmt_g(double v, int precision = 9);
+inline std::string fmt_exact(double v) { return fmt_g(v, 17); }
+
+// ---- curves ------------------------------------------------------------------
+struct ProfilePoint {
+    int n = 1;
+    double time = 0.0;
+    std::string parallel_config = "dp";
+};
+
+struct CurvePiece {
+    double n_lo = 1.0;
+    double n_hi = 1.0;
+    double alpha = 0.0;
+    double beta_c = 0.0;
+    double beta_w = 0.0;
+};
+
+// Piecewise alpha-beta curve T(n) = alpha + beta_c*c + beta_w*w/n.
+class ScalingCurve {
+public:
+    ScalingCurve() = default;
+    static ScalingCurve from_pieces(std::vector<CurvePiece> pieces, double c, double w);
+    double n_max() const { return n_max_; }
+    int n_max_int() const;
+    double c() const { return c_; }
+    double w() const { return w_; }
+    const std::vector<CurvePiece>& pieces() const { return pieces_; }
+    double eval(double n) const;
+    double inverse_exact(double target) const;
+    std::string dump() const;
+
+private:
+    std::vector<CurvePiece> pieces_;
+    double c_ = 0.0;
+    double w_ = 1.0;
+    double n_max_ = 1.0;
+};
+
+// ---- workload & topology -------------------------------------------------------
+struct InputSize {
+    std::int64_t batch = 1;
+    std::int64_t seq = 1;
+    std::int64_t hidden = 1;
+    bool operator==(const InputSize& o) const {
+        return batch == o.batch && seq == o.seq && hidden == o.hidden;
+    }
+};
+
+struct ModuleDecl {
+    std::string kind;
+    int layers = 1;
+    InputSize input;
+    int tp_degree = 1;
+    std::string param_group;
+    std::uint64_t param_bytes = 0;
+    double flops_proxy = 1.0;
+    double comm_proxy = 0.0;
+    std::uint64_t act_bytes = 0;
+    std::uint64_t out_bytes = 0;
+    std::uint64_t edge_bytes() const { return out_bytes == 0 ? act_bytes : out_bytes; }
+};
+
+using FlowBranch = std::vector<std::string>;
+using FlowStep = std::vector<FlowBranch>;
+
+struct TaskDecl {
+    std::string id;
+    std::vector<FlowStep> flow;
+    std::string flow_text;
+};
+
+struct WorkloadSpec {
+    std::map<std::string, ModuleDecl> modules;
+    std::vector<TaskDecl> tasks;
+    std::map<std::string, std::vector<CurvePiece>> truth;
+    std::map<std::string, std::vector<ProfilePoint>> profiles;
+    std::map<std::string, std::vector<int>> breakpoints;
+    const ModuleDecl& module(const std::string& kind) const;
+};
+
+struct ClusterTopology {
+    std::vector<int> devices;
+    std::vector<std::vector<int>> islands;
+    std::map<int, int> island_of;
+    double intra_bw = 1.0;
+    double inter_bw = 1.0;
+    std::uint64_t mem_capacity = 0;
+    void finalize();
+};
+
+ClusterTopology make_topology(int num_devices, int island_size, double intra_bw, double inter_bw,
+                              std::uint64_t mem_capacity);
+
+std::vector<FlowStep> parse_flow(const std::string& text, const std::string& ctx);
+std::string flow_to_text(const std::vector<FlowStep>& flow);
+void validate_workload(const WorkloadSpec& spec);
+WorkloadSpec parse_workload(const std::string& text);
+std::string dump_workload(const WorkloadSpec& spec);
+ClusterTopology parse_topology(const std::string& text);
+std::string dump_topology(const ClusterTopology& topo);
+
+// ---- graph ---------------------------------------------------------------------
+struct Operator {
+    std::string id;
+    std::string kind;
+    std::set<std::string> task_ids;
+    InputSize input;
+    int tp_degree = 1;
+    std::string param_group;
+};
+
+struct ComputationGraph {
+    std::map<std::string, Operator> operators;
+    std::set<std::pair<std::string, std::string>> edges;
+};
+
+struct MetaOp {
+    std::string id;
+    std::vector<std::string> member_ops;
+    int length = 0;
+    std::string kind;
+    InputSize input;
+    std::int64_t global_batch = 1;
+    int tp_degree = 1;
+    int level = -1;
+    std::string param_group;
+    std::set<std::string> task_ids;
+};
+
+struct MetaGraph {
+    std::map<std::string, MetaOp> metaops;
+    std::set<std::pair<std::string, std::string>> edges;
+    std::vector<std::vector<std::string>> levels;
+};
+
+std::string dump_metagraph(const MetaGraph& meta);
+
+// ---- allocation / schedule / placement ----------------------------------------------
+struct AslTuple {
+    std::string metaop_id;
+    int n = 0;
+    double start = -1.0;
+    int layers = 0;
+};
+
+struct TuplePair {
+    AslTuple upper;
+    std::optional<AslTuple> lower;
+};
+
+struct AllocationPlan {
+    int level = 0;
+    double c_star = 0.0;
+    std::map<std::string, TuplePair> tuples;
+};
+
+struct AllocatorOptions {
+    double eps = 1e-7;
+    int max_iters = 200;
+    double drop_floor = 0.0;
+};
+
+std::string dump_allocation(const AllocationPlan& plan);
+
+struct WaveEntry {
+    std::string metaop_id;
+    int n = 0;
+    int layers = 0;
+    double span = 0.0;
+};
+
+struct Wave {
+    int index = 0;
+    int level = 0;
+    double start = 0.0;
+    double duration = 0.0;
+    std::vector<WaveEntry> entries;
+};
+
+struct WavefrontSchedule {
+    std::vector<Wave> waves;
+    double end_time = 0.0;
+    std::vector<int> level_boundaries;
+};
+
+std::string dump_schedule(const WavefrontSchedule& sched);
+
+struct Flow {
+    int from_wave = 0;
+    std::string from_id;
+    int to_wave = 0;
+    std::string to_id;
+    std::uint64_t volume = 0;
+    std::string mode;
+};
+
+struct PlacementOptions {
+    bool sequential = false;
+    int backtrack_depth = 2;
+    int backtrack_branching = 3;
+};
+
+// ---- plan artifact ----------------------------------------------------------------------
+struct PlanEntity {
+    std::string id;
+    std::string kind;
+    int length = 1;
+    int level = 0;
+    int tp_degree = 1;
+    std::int64_t global_batch = 1;
+    double batch_fraction = 1.0;
+    std::string param_group;
+    std::uint64_t param_bytes = 0;
+    std::uint64_t act_bytes = 0;
+    std::uint64_t out_bytes = 0;
+    double w = 1.0;
+    double c = 0.0;
+    std::set<std::string> task_ids;
+};
+
+struct ExecutionPlan {
+    std::string strategy = "wavefront";
+    ClusterTopology topo;
+    std::map<std::string, PlanEntity> entities;
+    std::map<std::string, ScalingCurve> curves;
+    std::set<std::pair<std::string, std::string>> deps;
+    WavefrontSchedule schedule;
+    std::map<std::pair<int, std::string>, std::vector<int>> devices;
+    std::vector<Flow> flows;
+    double lower_bound = 0.0;
+    double grad_opt_multiplier = 3.0;
+};
+
+std::string write_plan(const ExecutionPlan& plan);
+
+// ---- planner API (planner.hpp:21-38,156) ------------------------------------------------------
+struct PlannerOptions {
+    AllocatorOptions alloc;
+    PlacementOptions placement;
+    double grad_opt_multiplier = 3.0;
+    double synth_noise = 0.0;
+    std::uint64_t synth_seed = 0;
+};
+
+struct PlannerResult {
+    ComputationGraph graph;
+    MetaGraph meta;
+    std::map<std::string, ScalingCurve> curves;
+    std::vector<AllocationPlan> level_plans;
+    WavefrontSchedule schedule;
+    ExecutionPlan plan;
+    double lower_bound = 0.0;
+    double predicted_makespan = 0.0;
+};
+
+// Drop-in for wavesched::plan_workload: same arguments, same result, same
+// exceptions.  Runs on the process-wide default context (CUDA device 0, or
+// $WSGPU_DEVICE).  Throws if the CUDA planner cannot run (no fallback).
+PlannerResult plan_workload(const WorkloadSpec& spec, const ClusterTopology& topo,
+                            const PlannerOptions& opt = {});
+
+// ---- batch encoding (host side of the C-ABI) ---------------------------------------------
+// One planning problem of a batch.
+struct Problem {
+    const WorkloadSpec* spec = nullptr;
+    const ClusterTopology* topo = nullptr;
+    PlannerOptions opt;
+};
+
+// Owns the memory behind a ws_batch (one contiguous, optionally pinned,
+// block = ws_batch.blob).  Host-side validation (validate_workload) runs while
+// encoding; a failing problem is recorded in host_error_* and encoded with no
+// modules so the batch stays aligned.
+class EncodedBatch {
+public:
+    ws_batch view{};
+    std::vector<std::string> host_error_class;  // per plan; empty = encoded
+    std::vector<std::string> host_error_msg;
+    std::shared_ptr<std::uint8_t> buffer;
+    std::size_t nbytes = 0;
+    bool pinned = false;
+};
+
+EncodedBatch encode_batch(const std::vector<Problem>& problems, bool pinned = false);
+
+// Decoded plan (strings rebuilt).  Throws the reference exception for a failed plan.
+PlannerResult decode_result(const Problem& prob, const ws_plan_result& res, const std::uint8_t* arena,
+                            bool build_graph = true);
+// write_plan() text of a decoded result, or "error <Class>: <what>" for a failure.
+std::string plan_text_or_error(const Problem& prob, const ws_plan_result& res, const std::uint8_t* arena);
+[[noreturn]] void throw_result_error(const Problem& prob, const ws_plan_result& res);
+
+// Deterministic scenario generator (scenarios.hpp restated): the measurement
+// input source.  Returns workload + topology built directly (no text pass).
+struct Scenario {
+    WorkloadSpec spec;
+    ClusterTopology topo;
+};
+Scenario generate_scenario(const std::string& name, int tasks, int devices, std::uint64_t seed);
+// SURVEY §8(d) sweep mixture i.
+Scenario sweep_mixture(std::int64_t i);
+
+}  // namespace wsgpu

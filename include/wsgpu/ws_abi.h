@@ -1,0 +1,260 @@
+/*
+ * ws_abi.h — C-ABI of the B200 wavefront planner (drop-in for
+ * wavesched::plan_workload, /root/reference/proj/include/wavesched/planner.hpp:156-212).
+ *
+ * Plain C: fixed-width integers, plain pointers and sizes, no torch or C++
+ * types.  A *batch* holds many independent planning problems ("plans") as
+ * structure-of-arrays sections; the planner fills one ws_plan_result per plan
+ * plus a byte arena holding each plan's variable-length output record.
+ *
+ * Every declaration below names the reference interface it replaces.
+ * The host-side C++ mirror (include/wsgpu/planner.hpp) encodes
+ * WorkloadSpec/ClusterTopology/PlannerOptions into this format and decodes the
+ * results back into PlannerResult/ExecutionPlan.
+ */
+#ifndef WSGPU_WS_ABI_H
+#define WSGPU_WS_ABI_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define WS_ABI_VERSION 1
+
+/* Device-side limits of this build (per plan).  A plan exceeding one returns
+ * WS_STATUS_LIMIT with err_code naming the limit; nothing falls back to CPU. */
+#define WS_MAX_DEVICES 64   /* device sets are u64 masks                       */
+#define WS_MAX_MODULES 64   /* module DAG adjacency is u64 masks               */
+#define WS_MAX_TASKS 64     /* task sets are u64 masks                         */
+#define WS_MAX_PIECES 64    /* fitted pieces per curve (isotonic: nmax-1)      */
+#define WS_MAX_TUPLES 128   /* pending ASL tuples per level                    */
+#define WS_MAX_WAVES 256    /* waves per plan                                  */
+#define WS_MAX_ENTRIES 1024 /* wave entries per plan                           */
+#define WS_MAX_FLOWS 4096   /* flows per plan                                  */
+
+/* ---- status (maps the exception taxonomy, common.hpp:20-60, cli.hpp:330-344) */
+enum ws_status {
+    WS_STATUS_OK = 0,
+    WS_STATUS_PARSE = 2,      /* ParseError and subclasses       -> exit 2 */
+    WS_STATUS_INFEASIBLE = 3, /* InfeasibleError and subclasses  -> exit 3 */
+    WS_STATUS_INVARIANT = 4,  /* InvariantError and subclasses   -> exit 4 */
+    WS_STATUS_LIMIT = 5,      /* input exceeds a WS_MAX_* limit of this build */
+    WS_STATUS_INTERNAL = 6    /* arena overflow or CUDA error */
+};
+
+/* ---- leaf error codes; err_a/err_b/err_x/err_y carry the message arguments */
+enum ws_err {
+    WS_E_NONE = 0,
+    WS_E_CYCLIC_WORKLOAD = 1,   /* CyclicWorkload "workload data flows form a cycle" (graph.hpp:145)      */
+    WS_E_TRUTH_RANGE = 2,       /* ParseError "truth curve does not cover the device range" (planner.hpp:50) */
+    WS_E_CURVE_START = 3,       /* InvariantError "ScalingCurve: pieces must start at n=1" (scaling.hpp:48) */
+    WS_E_CURVE_CONTIG = 4,      /* InvariantError "ScalingCurve: pieces must be contiguous" (scaling.hpp:51) */
+    WS_E_NO_SOURCE = 5,         /* ParseError "module '<a>' has neither profile points nor a truth curve" */
+    WS_E_FIT_NO_POINTS = 6,     /* InsufficientProfile "fit: no profile points" (scaling.hpp:231)         */
+    WS_E_FIT_BAD_N = 7,         /* InsufficientProfile "fit: device count must be >= 1"                  */
+    WS_E_FIT_BAD_TIME = 8,      /* InsufficientProfile "fit: non-positive time sample"                   */
+    WS_E_FIT_BREAKPOINT = 9,    /* ParseError "fit: breakpoint <a> outside point span" (scaling.hpp:243)  */
+    WS_E_FIT_PIECE_POINTS = 10, /* InsufficientProfile "fit: piece [<a>, <b>] needs points at >= 2 distinct n" */
+    WS_E_FIT_DEGENERATE_X = 11, /* InsufficientProfile "fit: points do not span distinct n" (scaling.hpp:186) */
+    WS_E_FIT_NONPOSITIVE = 12,  /* DegenerateFit "fit: non-positive T(<a>)" (scaling.hpp:319)            */
+    WS_E_TP_EXCEEDS = 13,       /* NoValidAllocation "metaop 'm<a>': tp degree <b> exceeds device count <N>" */
+    WS_E_EVAL_RANGE = 14,       /* OutOfRange "eval_time: n=<x> outside [1, <y>]" (scaling.hpp:68)        */
+    WS_E_NO_SCHEDULABLE = 15,   /* InvariantError "schedule_level: no schedulable tuple"                 */
+    WS_E_NO_PROGRESS = 16,      /* InvariantError "schedule_level: wave made no progress"                */
+    WS_E_BT_BUDGET = 17,        /* PlacementInfeasible "placement backtrack budget exhausted at wave <a>" */
+    WS_E_NO_PLACEMENT_W0 = 18,  /* PlacementInfeasible "no feasible placement for wave 0"                */
+    WS_E_HOST_PRESET = 19,      /* error detected by the host encoder; message kept host-side           */
+    WS_E_LIMIT_DEVICES = 40,
+    WS_E_LIMIT_MODULES = 41,
+    WS_E_LIMIT_TASKS = 42,
+    WS_E_LIMIT_PIECES = 43,
+    WS_E_LIMIT_TUPLES = 44,
+    WS_E_LIMIT_WAVES = 45,
+    WS_E_LIMIT_ENTRIES = 46,
+    WS_E_LIMIT_FLOWS = 47,
+    WS_E_ARENA_OVERFLOW = 60,
+    WS_E_CUDA = 61
+};
+
+/* Flow token encoding (workload.hpp:71-87 grammar "a>b+c,d"):
+ *   >= 0           module index local to the plan ('>' chains consecutive modules)
+ *   WS_TOK_BRANCH  '+'   WS_TOK_STEP ','                                         */
+#define WS_TOK_BRANCH (-1)
+#define WS_TOK_STEP (-2)
+
+/* One planning problem: a WorkloadSpec + ClusterTopology + PlannerOptions. */
+typedef struct ws_plan_rec {
+    int32_t mod_begin, n_mod;    /* modules, sorted by kind (std::map order)           */
+    int32_t task_begin, n_tasks; /* tasks in spec order; see ws_batch.task_*           */
+    int32_t dev_begin, n_dev;    /* devices in ascending id order; island per device   */
+    int32_t n_islands;           /* islands in declaration order                        */
+    int32_t n_groups;            /* distinct param_group strings (ids 0..n_groups-1)    */
+    int32_t max_iters;           /* AllocatorOptions::max_iters (allocation.hpp:44)     */
+    int32_t sequential;          /* PlacementOptions::sequential (placement.hpp:106)    */
+    int32_t bt_depth;            /* PlacementOptions::backtrack_depth                   */
+    int32_t bt_branching;        /* PlacementOptions::backtrack_branching               */
+    uint64_t mem_capacity;       /* ClusterTopology::mem_capacity                       */
+    double eps;                  /* AllocatorOptions::eps                               */
+    double drop_floor;           /* AllocatorOptions::drop_floor                        */
+    double grad_mult;            /* PlannerOptions::grad_opt_multiplier                 */
+} ws_plan_rec;
+
+/* Structure-of-arrays batch.  All pointers address the same memory space
+ * (host for the oracle and the *_host entry points, device inside the ctx). */
+typedef struct ws_batch {
+    int32_t n_plans;
+    int32_t n_modules;     /* total modules over all plans        */
+    int32_t n_task_total;  /* total tasks                         */
+    int32_t n_tokens;      /* total flow tokens                   */
+    int32_t n_devices;     /* total devices                       */
+    int32_t n_pieces;      /* total declared truth pieces         */
+    int32_t n_points;      /* total profile points                */
+    int32_t n_bps;         /* total breakpoint values             */
+    int32_t n_name_bytes;  /* total kind-name bytes               */
+    int32_t pad0;
+    /* Optional: if non-NULL every section below lies inside [blob, blob +
+     * blob_bytes) and the planner moves the batch with one copy. */
+    const void* blob;
+    uint64_t blob_bytes;
+    const ws_plan_rec* plans; /* [n_plans] */
+    /* modules (ModuleDecl workload.hpp:27-40 + per-kind curve sources) [n_modules] */
+    const int32_t* mod_plan;     /* owning plan                                   */
+    const int32_t* mod_layers;   /* layers                                        */
+    const int32_t* mod_tp;       /* tp_degree                                     */
+    const int32_t* mod_group;    /* param_group id, -1 = empty                    */
+    const int32_t* mod_alias;    /* param_group spelled "m<k>": k, else -1        */
+    const int64_t* mod_batch;    /* input.batch                                   */
+    const uint64_t* mod_param;   /* param_bytes                                   */
+    const uint64_t* mod_act;     /* act_bytes                                     */
+    const uint64_t* mod_out;     /* out_bytes                                     */
+    const double* mod_w;         /* flops_proxy                                   */
+    const double* mod_c;         /* comm_proxy                                    */
+    const int32_t* mod_name_off; /* kind bytes in names[]                         */
+    const int32_t* mod_name_len;
+    const int32_t* mod_truth_off; /* declared truth pieces (spec.truth)           */
+    const int32_t* mod_truth_n;   /* -1: no truth entry                           */
+    const int32_t* mod_prof_off;  /* profile points (spec.profiles)               */
+    const int32_t* mod_prof_n;    /* -1: no profile entry                         */
+    const int32_t* mod_bp_off;    /* breakpoints (spec.breakpoints)               */
+    const int32_t* mod_bp_n;      /* -1: no breakpoints entry                     */
+    const int32_t* mod_pre_err;   /* host-detected fit-stage error (ws_err), 0    */
+    /* tasks [n_task_total]: token range and rank of the id among the plan's ids */
+    const int32_t* task_tok_off;
+    const int32_t* task_tok_n;
+    const int32_t* task_rank;
+    const int32_t* tokens;        /* [n_tokens]                                    */
+    const int32_t* dev_island;    /* [n_devices] island index of device i          */
+    const double* truth;          /* [n_pieces*5]: n_lo n_hi alpha beta_c beta_w   */
+    const int32_t* prof_n;        /* [n_points]                                    */
+    const double* prof_t;         /* [n_points]                                    */
+    const int32_t* bps;           /* [n_bps]                                       */
+    const uint8_t* names;         /* [n_name_bytes]                                */
+} ws_batch;
+
+/* ---- per-plan result header ------------------------------------------------ */
+typedef struct ws_plan_result {
+    int32_t status;    /* ws_status                                             */
+    int32_t err_code;  /* ws_err                                                */
+    int64_t err_a, err_b;
+    double err_x, err_y;
+    int32_t n_metaops, n_edges, n_levels, n_waves;
+    int32_t n_entries, n_flows, n_pieces, pad;
+    double lower_bound; /* PlannerResult::lower_bound (planner.hpp:189)          */
+    double end_time;    /* predicted_makespan = schedule.end_time (:193-194)      */
+    uint64_t offset;    /* byte offset of this plan's record in the arena        */
+    uint64_t size;      /* record bytes                                          */
+} ws_plan_result;
+
+/* Arena record of one plan: the sections below, in this order, each 8-byte
+ * aligned.  MetaOps are indexed by their number k (id "m<k>", graph.hpp:175). */
+typedef struct ws_out_metaop {
+    int32_t module;      /* local module index (kind)                          */
+    int32_t level;       /* MetaOp::level (graph.hpp:207-226)                  */
+    int32_t first_layer; /* first member operator layer                        */
+    int32_t length;      /* L_m                                                */
+    int32_t piece_begin; /* into the pieces section                            */
+    int32_t piece_count;
+    int32_t upper_n, upper_l; /* TuplePair::upper (allocation.hpp:31-34)       */
+    int32_t lower_n, lower_l; /* lower tuple; lower_l == 0: absent             */
+} ws_out_metaop;
+
+typedef struct ws_out_level {
+    double c_star;        /* AllocationPlan::c_star                             */
+    int32_t first_wave;   /* WavefrontSchedule::level_boundaries                 */
+    int32_t n_waves;
+} ws_out_level;
+
+typedef struct ws_out_piece {
+    double n_lo, n_hi, alpha, beta_c, beta_w; /* CurvePiece (scaling.hpp:25-31) */
+} ws_out_piece;
+
+typedef struct ws_out_edge {
+    int32_t from, to; /* MetaGraph::edges, std::set<pair<string,string>> order */
+} ws_out_edge;
+
+typedef struct ws_out_wave {
+    double start, duration; /* Wave (schedule.hpp:22-28) after merge_levels     */
+    int32_t level, entry_begin, n_entries, pad;
+} ws_out_wave;
+
+typedef struct ws_out_entry {
+    double span;         /* layers * T(n)                                        */
+    uint64_t devmask;    /* placement device set (bit i = i-th device id)         */
+    int32_t metaop, n, layers;
+    int32_t rot;         /* device-list start index (sequential ablation order)  */
+} ws_out_entry;
+
+enum ws_flow_mode { WS_FLOW_COPY = 0, WS_FLOW_INTRA = 1, WS_FLOW_INTER = 2 };
+
+typedef struct ws_out_flow {
+    uint64_t volume;
+    int32_t from_wave, from_metaop, to_wave, to_metaop;
+    int32_t mode, pad;
+} ws_out_flow;
+
+/* ---- context & planning --------------------------------------------------- */
+typedef struct ws_ctx ws_ctx;
+
+/* Creates a planning context bound to CUDA device `device`.  Returns 0 on
+ * success; the ctx owns device buffers and a stream. */
+int ws_ctx_create(int device, ws_ctx** out);
+void ws_ctx_destroy(ws_ctx* ctx);
+/* Text of the last error on this ctx (CUDA failures, bad arguments). */
+const char* ws_ctx_last_error(const ws_ctx* ctx);
+
+/* Replaces wavesched::plan_workload over a whole batch (planner.hpp:156-212).
+ * `in` points to HOST memory; results and arena are written to HOST memory.
+ * The H2D copy, all kernels and the D2H copies run on the ctx stream (or on
+ * `stream` if non-NULL, a cudaStream_t).  Never throws; per-plan failures are
+ * reported in results[i].status.  Returns 0 unless the call itself failed. */
+int ws_plan_batch_host(ws_ctx* ctx, const ws_batch* in, ws_plan_result* results, uint8_t* arena,
+                       uint64_t arena_cap, uint64_t* arena_used, void* stream);
+
+/* Device-resident variant for throughput measurement: ws_stage_batch copies a
+ * host batch into ctx-owned device memory once; ws_plan_staged then plans it
+ * entirely on the device (results stay in device memory until ws_fetch_results). */
+int ws_stage_batch(ws_ctx* ctx, const ws_batch* in, void* stream);
+int ws_plan_staged(ws_ctx* ctx, void* stream);
+int ws_fetch_results(ws_ctx* ctx, ws_plan_result* results, uint8_t* arena, uint64_t arena_cap,
+                     uint64_t* arena_used, void* stream);
+/* Number of kernel launches issued by the last ws_plan_staged / ws_plan_batch_host. */
+int ws_last_launch_count(const ws_ctx* ctx);
+/* Device time (ms) of each planner kernel in the last planning call, measured
+ * with CUDA events on the launching stream: out[0]=fit, out[1]=plan. */
+int ws_last_kernel_ms(const ws_ctx* ctx, double* out, int n);
+
+/* Global best candidate: on-device argmin of key over the staged
+ * batch, key = end_time / lower_bound (mode 0) or end_time (mode 1); infeasible
+ * plans count as +inf; ties go to the smaller index.  Writes {key, index}. */
+int ws_best_staged(ws_ctx* ctx, int mode, double* key, int64_t* index, void* stream);
+
+/* Arena capacity sufficient for any batch whose plans stay within the limits. */
+uint64_t ws_arena_bound(const ws_batch* in);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* WSGPU_WS_ABI_H */

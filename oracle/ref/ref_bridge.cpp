@@ -1,0 +1,212 @@
+// ref_bridge.cpp — compiled ONLY in the build container against the reference
+// headers (/root/reference/proj/include, read in place, never copied) into
+// oracle/_ref/libwsref.so.  Test infrastructure: it runs the reference planner
+// itself so the oracle restatement and the CUDA planner can be pinned to it,
+// and it is the "reference" CPU baseline of bench.py (kind "reference").
+#include <atomic>
+#include <chrono>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "wavesched/planner.hpp"
+#include "wavesched/scenarios.hpp"
+
+// The acceptance suite is compiled in place (not copied) so its fuzz
+// generator (acceptance.cpp:284-323) and tiny instances are reused verbatim.
+#define main wsref_acceptance_main
+#include "tests/acceptance.cpp"
+#undef main
+
+using namespace wavesched;
+
+extern "C" {
+typedef struct wsref_opts {
+    double eps;
+    int max_iters;
+    double drop_floor;
+    int sequential;
+    int bt_depth;
+    int bt_branching;
+    double grad_mult;
+    double synth_noise;
+    unsigned long long synth_seed;
+} wsref_opts;
+}
+
+namespace {
+
+char* dup(const std::string& s) {
+    char* p = static_cast<char*>(std::malloc(s.size() + 1));
+    std::memcpy(p, s.c_str(), s.size() + 1);
+    return p;
+}
+
+PlannerOptions to_opts(const wsref_opts* o) {
+    PlannerOptions opt;
+    if (!o) return opt;
+    opt.alloc.eps = o->eps;
+    opt.alloc.max_iters = o->max_iters;
+    opt.alloc.drop_floor = o->drop_floor;
+    opt.placement.sequential = o->sequential != 0;
+    opt.placement.backtrack_depth = o->bt_depth;
+    opt.placement.backtrack_branching = o->bt_branching;
+    opt.grad_opt_multiplier = o->grad_mult;
+    opt.synth_noise = o->synth_noise;
+    opt.synth_seed = o->synth_seed;
+    return opt;
+}
+
+// Reference outcome as text: the plan file, or "error <Class>: <what>".
+std::string outcome(const WorkloadSpec& spec, const ClusterTopology& topo, const PlannerOptions& opt) {
+    try {
+        return write_plan(plan_workload(spec, topo, opt).plan);
+    } catch (const CyclicWorkload& e) {
+        return std::string("error CyclicWorkload: ") + e.what() + "\n";
+    } catch (const UnknownModule& e) {
+        return std::string("error UnknownModule: ") + e.what() + "\n";
+    } catch (const EmptyWorkload& e) {
+        return std::string("error EmptyWorkload: ") + e.what() + "\n";
+    } catch (const InsufficientProfile& e) {
+        return std::string("error InsufficientProfile: ") + e.what() + "\n";
+    } catch (const ParseError& e) {
+        return std::string("error ParseError: ") + e.what() + "\n";
+    } catch (const DegenerateFit& e) {
+        return std::string("error DegenerateFit: ") + e.what() + "\n";
+    } catch (const NoValidAllocation& e) {
+        return std::string("error NoValidAllocation: ") + e.what() + "\n";
+    } catch (const PlacementInfeasible& e) {
+        return std::string("error PlacementInfeasible: ") + e.what() + "\n";
+    } catch (const OutOfRange& e) {
+        return std::string("error OutOfRange: ") + e.what() + "\n";
+    } catch (const EmptyLevel& e) {
+        return std::string("error EmptyLevel: ") + e.what() + "\n";
+    } catch (const InvariantError& e) {
+        return std::string("error InvariantError: ") + e.what() + "\n";
+    } catch (const Error& e) {
+        return std::string("error Error: ") + e.what() + "\n";
+    }
+}
+
+Scenario sweep(long i) {
+    static const char* fam[3] = {"clip-like", "ofasys-like", "qwen-val-like"};
+    static const int devs[4] = {8, 16, 32, 64};
+    return generate_scenario(fam[i % 3], 2 + static_cast<int>((i / 3) % 15), devs[(i / 45) % 4],
+                             static_cast<std::uint64_t>(i));
+}
+
+}  // namespace
+
+extern "C" {
+
+void wsref_free(char* p) { std::free(p); }
+
+// Reference plan text for workload/topology texts (parsed by the reference).
+char* wsref_plan_text(const char* workload, const char* topology, const wsref_opts* o) {
+    try {
+        WorkloadSpec spec = parse_workload(workload);
+        ClusterTopology topo = parse_topology(topology);
+        return dup(outcome(spec, topo, to_opts(o)));
+    } catch (const Error& e) {
+        return dup(std::string("error Parse: ") + e.what() + "\n");
+    }
+}
+
+// generate_scenario texts (scenarios.hpp:292-299).
+int wsref_scenario(const char* name, int tasks, int devices, unsigned long long seed, char** workload,
+                   char** topology) {
+    try {
+        Scenario sc = generate_scenario(name, tasks, devices, seed);
+        *workload = dup(sc.workload_text);
+        *topology = dup(sc.topology_text);
+        return 0;
+    } catch (const Error& e) {
+        *workload = dup(e.what());
+        *topology = nullptr;
+        return 1;
+    }
+}
+
+// The acceptance fuzz sequence (Rng(2024), acceptance.cpp:451-456): workload i
+// as dump_workload text plus its topology text.
+int wsref_fuzz(int count, char*** workloads, char*** topologies) {
+    Rng rng(2024);
+    *workloads = static_cast<char**>(std::malloc(sizeof(char*) * count));
+    *topologies = static_cast<char**>(std::malloc(sizeof(char*) * count));
+    for (int i = 0; i < count; ++i) {
+        WorkloadSpec spec = fuzz_workload(rng);
+        const int devices = 2 << rng.next_int(0, 3);
+        ClusterTopology topo = make_topology(devices, std::max(2, devices / 2), 100e9, 20e9, 1ull << 50);
+        (*workloads)[i] = dup(dump_workload(spec));
+        (*topologies)[i] = dup(dump_topology(topo));
+    }
+    return 0;
+}
+
+void wsref_free_list(char** list, int count) {
+    for (int i = 0; i < count; ++i) std::free(list[i]);
+    std::free(list);
+}
+
+// Reference plan text of sweep mixture i, default options.
+char* wsref_sweep_plan(long i) {
+    Scenario sc = sweep(i);
+    return dup(outcome(parse_workload(sc.workload_text), parse_topology(sc.topology_text), PlannerOptions{}));
+}
+
+char* wsref_sweep_workload(long i, char** topology) {
+    Scenario sc = sweep(i);
+    *topology = dup(sc.topology_text);
+    return dup(sc.workload_text);
+}
+
+// CPU baseline: reference plan_workload over sweep mixtures [start, start+count)
+// (inputs pre-parsed outside the timed region) on `threads` std::threads.
+// Returns plans/s; writes the number of infeasible plans.
+double wsref_sweep_bench(long start, long count, int threads, long* infeasible) {
+    std::vector<WorkloadSpec> specs(count);
+    std::vector<ClusterTopology> topos(count);
+    for (long i = 0; i < count; ++i) {
+        Scenario sc = sweep(start + i);
+        specs[i] = parse_workload(sc.workload_text);
+        topos[i] = parse_topology(sc.topology_text);
+    }
+    std::atomic<long> next{0}, bad{0};
+    auto worker = [&] {
+        for (long i; (i = next.fetch_add(1)) < count;) {
+            try {
+                PlannerResult r = plan_workload(specs[i], topos[i]);
+                (void)r;
+            } catch (const Error&) {
+                bad.fetch_add(1);
+            }
+        }
+    };
+    const auto t0 = std::chrono::steady_clock::now();
+    std::vector<std::thread> pool;
+    for (int t = 0; t < threads; ++t) pool.emplace_back(worker);
+    for (auto& th : pool) th.join();
+    const double sec = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    if (infeasible) *infeasible = bad.load();
+    return static_cast<double>(count) / sec;
+}
+
+// Single-plan latency of the reference planner (median of `reps`, ms).
+double wsref_latency_ms(const char* name, int tasks, int devices, int reps) {
+    Scenario sc = generate_scenario(name, tasks, devices, 0);
+    WorkloadSpec spec = parse_workload(sc.workload_text);
+    ClusterTopology topo = parse_topology(sc.topology_text);
+    std::vector<double> ms;
+    for (int r = 0; r < reps; ++r) {
+        const auto t0 = std::chrono::steady_clock::now();
+        PlannerResult res = plan_workload(spec, topo);
+        (void)res;
+        ms.push_back(std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+    }
+    std::sort(ms.begin(), ms.end());
+    return ms[ms.size() / 2];
+}
+
+}  // extern "C"

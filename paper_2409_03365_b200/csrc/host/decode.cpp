@@ -1,0 +1,298 @@
+// decode.cpp — ws_plan_result + arena record -> PlannerResult / ExecutionPlan.
+//
+// Rebuilds the reference's string-keyed result objects (planner.hpp:29-38,
+// 196-210; build_entities :99-122) from the device's index-based output, and
+// maps error codes back to the reference exception classes and messages.
+#include <algorithm>
+#include <cstring>
+
+#include "wsgpu/planner.hpp"
+
+namespace wsgpu {
+namespace {
+
+std::size_t al8(std::size_t v) { return (v + 7) & ~std::size_t(7); }
+
+struct Sections {
+    const ws_out_metaop* mo;
+    const ws_out_level* lv;
+    const ws_out_piece* pc;
+    const ws_out_edge* ed;
+    const ws_out_wave* wv;
+    const ws_out_entry* en;
+    const ws_out_flow* fl;
+};
+
+Sections sections_of(const ws_plan_result& r, const std::uint8_t* arena) {
+    const std::uint8_t* base = arena + r.offset;
+    std::size_t off = 0;
+    Sections s{};
+    s.mo = reinterpret_cast<const ws_out_metaop*>(base + off);
+    off += al8(sizeof(ws_out_metaop) * r.n_metaops);
+    s.lv = reinterpret_cast<const ws_out_level*>(base + off);
+    off += al8(sizeof(ws_out_level) * r.n_levels);
+    s.pc = reinterpret_cast<const ws_out_piece*>(base + off);
+    off += al8(sizeof(ws_out_piece) * r.n_pieces);
+    s.ed = reinterpret_cast<const ws_out_edge*>(base + off);
+    off += al8(sizeof(ws_out_edge) * r.n_edges);
+    s.wv = reinterpret_cast<const ws_out_wave*>(base + off);
+    off += al8(sizeof(ws_out_wave) * r.n_waves);
+    s.en = reinterpret_cast<const ws_out_entry*>(base + off);
+    off += al8(sizeof(ws_out_entry) * r.n_entries);
+    s.fl = reinterpret_cast<const ws_out_flow*>(base + off);
+    return s;
+}
+
+const char* class_of(int code) {
+    switch (code) {
+        case WS_E_CYCLIC_WORKLOAD: return "CyclicWorkload";
+        case WS_E_TRUTH_RANGE:
+        case WS_E_NO_SOURCE:
+        case WS_E_FIT_BREAKPOINT: return "ParseError";
+        case WS_E_CURVE_START:
+        case WS_E_CURVE_CONTIG:
+        case WS_E_NO_SCHEDULABLE:
+        case WS_E_NO_PROGRESS: return "InvariantError";
+        case WS_E_FIT_NO_POINTS:
+        case WS_E_FIT_BAD_N:
+        case WS_E_FIT_BAD_TIME:
+        case WS_E_FIT_PIECE_POINTS:
+        case WS_E_FIT_DEGENERATE_X: return "InsufficientProfile";
+        case WS_E_FIT_NONPOSITIVE: return "DegenerateFit";
+        case WS_E_TP_EXCEEDS: return "NoValidAllocation";
+        case WS_E_EVAL_RANGE: return "OutOfRange";
+        case WS_E_BT_BUDGET:
+        case WS_E_NO_PLACEMENT_W0: return "PlacementInfeasible";
+        default: return code >= 40 && code < 60 ? "LimitExceeded" : "Error";
+    }
+}
+
+std::string module_kind(const WorkloadSpec& spec, std::int64_t index) {
+    auto it = spec.modules.begin();
+    std::advance(it, index);
+    return it->first;
+}
+
+std::vector<int> device_list(const Problem& prob, const ws_out_entry& e) {
+    const auto& devs = prob.topo->devices;
+    const int N = static_cast<int>(devs.size());
+    std::vector<int> out;
+    if (prob.opt.placement.sequential) {  // rolling cursor order (placement.hpp:351-357)
+        for (int i = 0; i < e.n; ++i) out.push_back(devs[(e.rot + i) % N]);
+    } else {
+        for (int d = 0; d < N; ++d)
+            if (e.devmask >> d & 1ull) out.push_back(devs[d]);
+    }
+    return out;
+}
+
+}  // namespace
+
+[[noreturn]] void throw_result_error(const Problem& prob, const ws_plan_result& r) {
+    const int N = static_cast<int>(prob.topo->devices.size());
+    switch (r.err_code) {
+        case WS_E_CYCLIC_WORKLOAD: throw CyclicWorkload("workload data flows form a cycle");
+        case WS_E_TRUTH_RANGE: throw ParseError("truth curve does not cover the device range");
+        case WS_E_CURVE_START: throw InvariantError("ScalingCurve: pieces must start at n=1");
+        case WS_E_CURVE_CONTIG: throw InvariantError("ScalingCurve: pieces must be contiguous");
+        case WS_E_NO_SOURCE:
+            throw ParseError("module '" + module_kind(*prob.spec, r.err_a) +
+                             "' has neither profile points nor a truth curve");
+        case WS_E_FIT_NO_POINTS: throw InsufficientProfile("fit: no profile points");
+        case WS_E_FIT_BAD_N: throw InsufficientProfile("fit: device count must be >= 1");
+        case WS_E_FIT_BAD_TIME: throw InsufficientProfile("fit: non-positive time sample");
+        case WS_E_FIT_BREAKPOINT:
+            throw ParseError("fit: breakpoint " + std::to_string(r.err_a) + " outside point span");
+        case WS_E_FIT_PIECE_POINTS:
+            throw InsufficientProfile("fit: piece [" + std::to_string(r.err_a) + ", " + std::to_string(r.err_b) +
+                                      "] needs points at >= 2 distinct n");
+        case WS_E_FIT_DEGENERATE_X: throw InsufficientProfile("fit: points do not span distinct n");
+        case WS_E_FIT_NONPOSITIVE: throw DegenerateFit("fit: non-positive T(" + std::to_string(r.err_a) + ")");
+        case WS_E_TP_EXCEEDS:
+            throw NoValidAllocation("metaop 'm" + std::to_string(r.err_a) + "': tp degree " +
+                                    std::to_string(r.err_b) + " exceeds device count " + std::to_string(N));
+        case WS_E_EVAL_RANGE:
+            throw OutOfRange("eval_time: n=" + fmt_g(r.err_x) + " outside [1, " + fmt_g(r.err_y) + "]");
+        case WS_E_NO_SCHEDULABLE: throw InvariantError("schedule_level: no schedulable tuple");
+        case WS_E_NO_PROGRESS: throw InvariantError("schedule_level: wave made no progress");
+        case WS_E_BT_BUDGET:
+            throw PlacementInfeasible("placement backtrack budget exhausted at wave " + std::to_string(r.err_a));
+        case WS_E_NO_PLACEMENT_W0: throw PlacementInfeasible("no feasible placement for wave 0");
+        case WS_E_HOST_PRESET: {
+            // re-run host validation to raise the original exception
+            validate_workload(*prob.spec);
+            if (N > WS_MAX_DEVICES) throw LimitExceeded("device count " + std::to_string(N) + " exceeds WS_MAX_DEVICES");
+            if (prob.spec->modules.size() > WS_MAX_MODULES) throw LimitExceeded("module count exceeds WS_MAX_MODULES");
+            throw LimitExceeded("task count exceeds WS_MAX_TASKS");
+        }
+        default:
+            if (r.err_code >= 40 && r.err_code < 60)
+                throw LimitExceeded("plan exceeds device limit (code " + std::to_string(r.err_code) + ")");
+            throw Error("planner internal error (code " + std::to_string(r.err_code) + ")");
+    }
+}
+
+PlannerResult decode_result(const Problem& prob, const ws_plan_result& r, const std::uint8_t* arena,
+                            bool build_graph) {
+    if (r.status != WS_STATUS_OK) throw_result_error(prob, r);
+    const WorkloadSpec& spec = *prob.spec;
+    const Sections s = sections_of(r, arena);
+    std::vector<const ModuleDecl*> mods;
+    for (const auto& kv : spec.modules) mods.push_back(&kv.second);
+    const int K = r.n_metaops;
+    auto mid = [](int k) { return "m" + std::to_string(k); };
+
+    // tasks routing through each module (graph.hpp:101-121)
+    std::map<std::string, std::set<std::string>> tasks_of;
+    for (const TaskDecl& t : spec.tasks)
+        for (const FlowStep& st : t.flow)
+            for (const FlowBranch& br : st)
+                for (const std::string& m : br) tasks_of[m].insert(t.id);
+
+    PlannerResult res;
+    for (int k = 0; k < K; ++k) {
+        const ws_out_metaop& o = s.mo[k];
+        const ModuleDecl& md = *mods[o.module];
+        MetaOp m;
+        m.id = mid(k);
+        for (int l = 0; l < o.length; ++l) m.member_ops.push_back(md.kind + "." + std::to_string(o.first_layer + l));
+        m.length = o.length;
+        m.kind = md.kind;
+        m.input = md.input;
+        m.global_batch = md.input.batch;
+        m.tp_degree = md.tp_degree;
+        m.level = o.level;
+        m.param_group = md.param_group;
+        m.task_ids = tasks_of[md.kind];
+        std::vector<CurvePiece> pieces;
+        for (int i = 0; i < o.piece_count; ++i) {
+            const ws_out_piece& p = s.pc[o.piece_begin + i];
+            pieces.push_back({p.n_lo, p.n_hi, p.alpha, p.beta_c, p.beta_w});
+        }
+        res.curves[m.id] = ScalingCurve::from_pieces(pieces, md.comm_proxy, md.flops_proxy);
+        res.meta.metaops.emplace(m.id, std::move(m));
+    }
+    for (int e = 0; e < r.n_edges; ++e) res.meta.edges.insert({mid(s.ed[e].from), mid(s.ed[e].to)});
+    res.meta.levels.assign(r.n_levels, {});
+    for (const auto& [id, m] : res.meta.metaops) res.meta.levels[m.level].push_back(id);
+
+    if (build_graph) {
+        for (const auto& [id, m] : res.meta.metaops) {
+            for (const std::string& op : m.member_ops) {
+                Operator o;
+                o.id = op;
+                o.kind = m.kind;
+                o.task_ids = m.task_ids;
+                o.input = m.input;
+                o.tp_degree = m.tp_degree;
+                o.param_group = m.param_group;
+                res.graph.operators.emplace(op, std::move(o));
+            }
+            for (std::size_t i = 1; i < m.member_ops.size(); ++i)
+                res.graph.edges.insert({m.member_ops[i - 1], m.member_ops[i]});
+        }
+        for (const auto& [a, b] : res.meta.edges)
+            res.graph.edges.insert({res.meta.metaops.at(a).member_ops.back(), res.meta.metaops.at(b).member_ops.front()});
+    }
+
+    for (int l = 0; l < r.n_levels; ++l) {
+        AllocationPlan ap;
+        ap.level = l;
+        ap.c_star = s.lv[l].c_star;
+        for (const std::string& id : res.meta.levels[l]) {
+            const ws_out_metaop& o = s.mo[std::stoi(id.substr(1))];
+            TuplePair tp;
+            tp.upper = {id, o.upper_n, -1.0, o.upper_l};
+            if (o.lower_l > 0) tp.lower = AslTuple{id, o.lower_n, -1.0, o.lower_l};
+            ap.tuples.emplace(id, tp);
+        }
+        res.level_plans.push_back(std::move(ap));
+        res.schedule.level_boundaries.push_back(s.lv[l].first_wave);
+    }
+    ExecutionPlan& plan = res.plan;
+    for (int w = 0; w < r.n_waves; ++w) {
+        Wave wave;
+        wave.index = w;
+        wave.level = s.wv[w].level;
+        wave.start = s.wv[w].start;
+        wave.duration = s.wv[w].duration;
+        for (int i = 0; i < s.wv[w].n_entries; ++i) {
+            const ws_out_entry& e = s.en[s.wv[w].entry_begin + i];
+            wave.entries.push_back({mid(e.metaop), e.n, e.layers, e.span});
+            plan.devices[{w, mid(e.metaop)}] = device_list(prob, e);
+        }
+        res.schedule.waves.push_back(std::move(wave));
+    }
+    res.schedule.end_time = r.end_time;
+    res.lower_bound = r.lower_bound;
+    res.predicted_makespan = r.end_time;
+
+    plan.strategy = "wavefront";
+    plan.topo = *prob.topo;
+    for (const auto& [id, m] : res.meta.metaops) {  // build_entities (planner.hpp:99-122)
+        const ModuleDecl& md = spec.module(m.kind);
+        PlanEntity e;
+        e.id = id;
+        e.kind = m.kind;
+        e.length = m.length;
+        e.level = m.level;
+        e.tp_degree = m.tp_degree;
+        e.global_batch = m.global_batch;
+        e.batch_fraction = 1.0;
+        e.param_group = m.length == md.layers ? md.param_group : "";
+        e.param_bytes = static_cast<std::uint64_t>(static_cast<double>(md.param_bytes) * m.length / md.layers);
+        e.act_bytes = md.act_bytes;
+        e.out_bytes = md.out_bytes;
+        e.w = md.flops_proxy;
+        e.c = md.comm_proxy;
+        e.task_ids = m.task_ids;
+        plan.entities[id] = std::move(e);
+    }
+    plan.curves = res.curves;
+    plan.deps = res.meta.edges;
+    plan.schedule = res.schedule;
+    plan.lower_bound = res.lower_bound;
+    plan.grad_opt_multiplier = prob.opt.grad_opt_multiplier;
+    static const char* kModes[3] = {"copy", "intra-island", "inter-island"};
+    for (int f = 0; f < r.n_flows; ++f) {
+        const ws_out_flow& x = s.fl[f];
+        plan.flows.push_back({x.from_wave, mid(x.from_metaop), x.to_wave, mid(x.to_metaop), x.volume, kModes[x.mode]});
+    }
+    return res;
+}
+
+std::string plan_text_or_error(const Problem& prob, const ws_plan_result& r, const std::uint8_t* arena) {
+    if (r.status != WS_STATUS_OK) {
+        try {
+            throw_result_error(prob, r);
+        } catch (const std::exception& e) {
+            const char* cls = class_of(r.err_code);
+            if (r.err_code == WS_E_HOST_PRESET) {
+                if (dynamic_cast<const CyclicWorkload*>(&e)) cls = "CyclicWorkload";
+                else if (dynamic_cast<const UnknownModule*>(&e)) cls = "UnknownModule";
+                else if (dynamic_cast<const EmptyWorkload*>(&e)) cls = "EmptyWorkload";
+                else if (dynamic_cast<const ParseError*>(&e)) cls = "ParseError";
+                else cls = "LimitExceeded";
+            }
+            return std::string("error ") + cls + ": " + e.what() + "\n";
+        }
+    }
+    return write_plan(decode_result(prob, r, arena, false).plan);
+}
+
+}  // namespace wsgpu
+
+// Arena bytes for a batch: a per-plan estimate generous for the reference's
+// workload families (metaops, 2 tuples and 2 curve pieces per MetaOp, dense
+// waves/flows); a plan exceeding its share is reported WS_E_ARENA_OVERFLOW and
+// re-planned alone by the host wrapper with ws_arena_bound of that one plan.
+extern "C" uint64_t ws_arena_bound(const ws_batch* in) {
+    uint64_t total = 0;
+    for (int p = 0; p < in->n_plans; ++p) {
+        const uint64_t M = static_cast<uint64_t>(in->plans[p].n_mod);
+        total += 64 + sizeof(ws_out_metaop) * M + sizeof(ws_out_level) * M + sizeof(ws_out_piece) * 4 * M +
+                 sizeof(ws_out_edge) * M * M + sizeof(ws_out_wave) * 4 * M + sizeof(ws_out_entry) * 8 * M +
+                 sizeof(ws_out_flow) * 16 * M;
+    }
+    return total + 4096;
+}
