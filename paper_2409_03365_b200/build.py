@@ -1,0 +1,73 @@
+"""In-tree build of the B200 planner library (paper_2409_03365_b200/lib/libwsgpu.so).
+
+Device code: nvcc for sm_100a only (``-gencode arch=compute_100a,code=sm_100a``),
+``-fmad=false`` so every double matches the reference bit for bit,
+``-lineinfo`` for ncu source attribution.  Host C++: g++ with
+``-ffp-contract=off``.  nvcc cross-compiles without a GPU, so this runs in the
+build container; the resulting .so travels to the GPU box in-tree.
+"""
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+from pathlib import Path
+
+PKG = Path(__file__).resolve().parent
+ROOT = PKG.parent
+CSRC = PKG / "csrc"
+LIB = PKG / "lib"
+BUILD = PKG / "lib" / "obj"
+CUDA = Path(os.environ.get("CUDA_HOME", "/usr/local/cuda"))
+NVCC = str(CUDA / "bin" / "nvcc")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+NVCC_FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-fmad=false", "--expt-relaxed-constexpr",
+              "-Xcompiler", "-fPIC", "-Xcompiler", "-ffp-contract=off", "-I", str(ROOT / "include")] + ARCH
+CXX_FLAGS = ["-O2", "-std=c++17", "-fPIC", "-ffp-contract=off", "-Wall", "-Wno-sign-compare",
+             "-I", str(ROOT / "include"), "-I", str(CUDA / "include")]
+
+LIBNAME = LIB / "libwsgpu.so"
+
+
+def _run(cmd: list[str], verbose: bool) -> None:
+    if verbose:
+        print(" ".join(cmd), flush=True)
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        sys.stderr.write(r.stdout + r.stderr)
+        raise RuntimeError(f"build step failed: {' '.join(cmd[:3])} ...")
+    if verbose and (r.stdout or r.stderr):
+        sys.stderr.write(r.stdout + r.stderr)
+
+
+def _stale(target: Path, deps: list[Path]) -> bool:
+    if not target.exists():
+        return True
+    t = target.stat().st_mtime
+    return any(d.stat().st_mtime > t for d in deps)
+
+
+def build(verbose: bool = False, force: bool = False) -> Path:
+    """Compile host + device sources and link libwsgpu.so; returns its path."""
+    BUILD.mkdir(parents=True, exist_ok=True)
+    headers = list((ROOT / "include").rglob("*.h*")) + list((CSRC / "device").glob("*.cuh"))
+    objs = []
+    for src in sorted((CSRC / "host").glob("*.cpp")):
+        obj = BUILD / (src.stem + ".o")
+        if force or _stale(obj, [src] + headers):
+            _run(["g++", *CXX_FLAGS, "-c", str(src), "-o", str(obj)], verbose)
+        objs.append(obj)
+    for src in sorted((CSRC / "device").glob("*.cu")):
+        obj = BUILD / (src.stem + ".cu.o")
+        if force or _stale(obj, [src] + headers):
+            _run([NVCC, *NVCC_FLAGS, "-Xptxas", "-v" if verbose else "-O3", "-c", str(src), "-o", str(obj)], verbose)
+        objs.append(obj)
+    if force or _stale(LIBNAME, objs):
+        _run([NVCC, *ARCH, "-shared", "-o", str(LIBNAME), *map(str, objs), "-cudart", "static",
+              "-Xlinker", "--no-undefined", "-lpthread", "-ldl", "-lrt"], verbose)
+    return LIBNAME
+
+
+if __name__ == "__main__":
+    build(verbose="-v" in sys.argv, force="-f" in sys.argv)
+    print(LIBNAME)
