@@ -1,0 +1,355 @@
+"""bench.py — batched planning throughput of the B200 planner.
+
+Workload (default): BASELINE config 5, the synthetic sweep of 100k task mixtures
+(2-16 tasks, clip/ofasys/qwen families, 8-64 device cluster specs), sharded
+across ranks (strided; strong scaling: the 100k total is fixed).  A "step" plans
+every mixture of the rank's shard once.
+
+  value  plans/s with the encoded batch already resident in HBM (device-timed,
+         CUDA events on the planner stream, max over ranks)
+  e2e    plans/s through the C-ABI host call ws_plan_batch_host: pinned host
+         batch -> H2D -> kernels -> D2H of the result headers + arena
+  roofline   dominant kernel k_plan vs the measured HBM copy bandwidth
+  cpu_baseline  the reference planner (oracle/_ref, compiled from the
+         reference sources) on all host cores over a bounded sweep sample
+
+usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+       [--mixtures M] [--workload sweep|clip10x64|...]
+Under torchrun (N>1) every rank plans its shard; rank 0 prints one JSON line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+sys.path.insert(0, str(ROOT / "oracle"))
+
+METRIC = "candidate plans evaluated/s and plan latency (ms) vs CPU ref; HBM GB/s fraction"
+CONFIGS = {  # BASELINE.json configs[0..3] (single-plan latency lines)
+    "clip4x8": ("clip-like", 4, 8),
+    "clip10x64": ("clip-like", 10, 64),
+    "ofasys7x32": ("ofasys-like", 7, 32),
+    "qwen3x64": ("qwen-val-like", 3, 64),
+}
+FALLBACK_HBM_GBS = 6650.0  # /opt/skills/guides/B200_PROFILING.md fallback
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def measured_peak():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        try:
+            return float(json.loads(p.read_text())["hbm_gbs"]), "measured"
+        except Exception:
+            pass
+    return FALLBACK_HBM_GBS, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    def __init__(self, index: int):
+        self.proc = None
+        self.path = ROOT / "gpurun_out" / f"clocks_rank{index}.csv"
+        try:
+            self.path.parent.mkdir(exist_ok=True)
+            self.f = open(self.path, "w")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={index}", "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "100"], stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self) -> dict:
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        self.proc.wait()
+        self.f.close()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.path.read_text().splitlines():
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def cpu_baseline(n_sample: int, threads: int) -> dict:
+    """Reference planner (compiled from the reference sources) on host cores."""
+    import pyoracle as po
+    if po.ref_available():
+        rate, bad = po.ref_sweep_bench(0, n_sample, threads)
+        return {"value": rate, "unit": "plans/s", "cores": threads, "kind": "reference",
+                "sample": f"sweep mixtures 0..{n_sample - 1}, reference plan_workload, inputs pre-parsed, "
+                          f"{threads} std::threads ({bad} infeasible)"}
+    import paper_2409_03365_b200 as ws
+    ps = ws.ProblemSet()
+    ps.add_sweep(0, n_sample)
+    ps.encode()
+    t0 = time.perf_counter()
+    po.plan_batch(ps)
+    dt = time.perf_counter() - t0
+    return {"value": n_sample / dt, "unit": "plans/s", "cores": 1, "kind": "port",
+            "sample": f"sweep mixtures 0..{n_sample - 1}, oracle restatement, 1 thread"}
+
+
+def run_reference(args) -> None:
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    import pyoracle as po
+    threads = os.cpu_count() or 1
+    n = args.ref_sample
+    if not po.ref_available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libwsref.so not built (needs /root/reference)"}))
+        return
+    for _ in range(args.warmup):
+        po.ref_sweep_bench(0, min(n, 200), threads)
+    rates = []
+    t_total = 0.0
+    for s in range(args.steps):
+        t0 = time.perf_counter()
+        rate, _ = po.ref_sweep_bench(s * n, n, threads)
+        t_total += time.perf_counter() - t0
+        rates.append(rate)
+    value = statistics.median(rates)
+    line = {
+        "metric": METRIC, "value": value, "unit": "plans/s", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1000.0 * n / value, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"sweep-{args.mixtures} (bounded sample of {n} mixtures per step)",
+                   "parallelism": f"{threads} host threads"},
+        "impl": "reference",
+        "cpu_baseline": {"value": value, "unit": "plans/s", "cores": threads, "kind": "reference",
+                         "sample": f"{n} sweep mixtures per step, reference plan_workload compiled from the "
+                                   f"reference headers (-O2 -ffp-contract=off)"},
+        "e2e": {"value": value, "unit": "plans/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main() -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--mixtures", type=int, default=100000)
+    ap.add_argument("--ref-sample", type=int, default=4000)
+    ap.add_argument("--cpu-sample", type=int, default=6000)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--latency-reps", type=int, default=50)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    if args.impl == "reference":
+        run_reference(args)
+        return
+
+    import torch
+    import paper_2409_03365_b200 as ws
+    from paper_2409_03365_b200 import parallel
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+
+    # ---- inputs (untimed): this rank's shard of the sweep, encoded + pinned ----
+    idx = list(parallel.shard(args.mixtures, rank, world))
+    ps = ws.ProblemSet()
+    for i in idx:
+        ps.add_sweep(i, 1)
+    ps.encode(pinned=True)
+    in_bytes_blob = ps.encoded_bytes
+    planner = ws.Planner(local)
+    stream = torch.cuda.Stream(device=dev)
+    sptr = stream.cuda_stream
+
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
+
+    def barrier():
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            torch.distributed.barrier()
+
+    # ---- device-resident throughput ----
+    planner.stage(ps, sptr)
+    for _ in range(args.warmup):
+        planner.plan_staged(sptr)
+    torch.cuda.synchronize(dev)
+    res = planner.fetch(ps, sptr)
+    kernel_ms = planner.kernel_ms()
+    launches_per_step = planner.launch_count
+    clocks = ClockSampler(local)
+    barrier()
+    step_ms, plan_kernel_ms = [], []
+    for _ in range(args.steps):
+        flush.zero_()  # L2 flush between timed steps (outside the events)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        planner.plan_staged(sptr)
+        e1.record(stream)
+        e1.synchronize()
+        step_ms.append(e0.elapsed_time(e1))
+        plan_kernel_ms.append(planner.kernel_ms())
+    barrier()
+    clk = clocks.stop()
+    t_local = sum(step_ms) / 1000.0
+    t = torch.tensor([t_local], dtype=torch.float64, device=dev)
+    if world > 1:
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    t_max = float(t.item())
+    value = args.mixtures * args.steps / t_max
+
+    # ---- correctness + global best (min-loc over ranks) ----
+    planner.stage(ps, sptr)
+    planner.plan_staged(sptr)
+    res = planner.fetch(ps, sptr)
+    key, li = planner.best(0, sptr)
+    gi = parallel.local_to_global(li, rank, world) if li >= 0 else -1
+    best_key, best_idx = parallel.global_best(key if li >= 0 else float("inf"), gi, dev)
+    n_ok = sum(1 for i in range(len(ps)) if res.results[i].status == 0)
+    infeasible = torch.tensor([len(ps) - n_ok], dtype=torch.int64, device=dev)
+    if world > 1:
+        torch.distributed.all_reduce(infeasible)
+    alg_in, alg_out = ps.algorithmic_bytes(res)
+    d2h_bytes = len(ps) * ctypes_sizeof_result() + int(res.arena_used.value)
+
+    # ---- end to end through the C-ABI host call ----
+    for _ in range(2):
+        planner.plan(ps, sptr)
+    barrier()
+    e2e_ms = []
+    for _ in range(args.steps):
+        flush.zero_()
+        torch.cuda.synchronize(dev)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        r2 = planner.plan(ps, sptr)
+        e1.record(stream)
+        e1.synchronize()
+        e2e_ms.append(e0.elapsed_time(e1))
+    barrier()
+    te = torch.tensor([sum(e2e_ms) / 1000.0], dtype=torch.float64, device=dev)
+    if world > 1:
+        torch.distributed.all_reduce(te, op=torch.distributed.ReduceOp.MAX)
+    e2e_value = args.mixtures * args.steps / float(te.item())
+    d2h_step = len(ps) * ctypes_sizeof_result() + int(r2.arena_used.value)
+
+    if rank != 0:
+        if world > 1:
+            torch.distributed.destroy_process_group()
+        return
+
+    # ---- roofline of the dominant kernel (k_plan) ----
+    peak, peak_src = measured_peak()
+    kplan_ms = statistics.median(k[1] for k in plan_kernel_ms)
+    kfit_ms = statistics.median(k[0] for k in plan_kernel_ms)
+    kplan_bytes = alg_in + alg_out  # SURVEY §8(d) compulsory in+out of the rank's plans
+    achieved = kplan_bytes / (kplan_ms / 1000.0) / 1e9
+    traffic = None
+    tp = ROOT / "profiles" / "kplan_traffic.json"
+    if tp.exists():
+        try:
+            traffic = json.loads(tp.read_text()).get("bytes_per_launch")
+        except Exception:
+            traffic = None
+
+    # ---- single-plan latency of the BASELINE configs ----
+    latency = {}
+    for name, (fam, tasks, devices) in CONFIGS.items():
+        one = ws.ProblemSet()
+        one.add_scenario(fam, tasks, devices, 0)
+        one.encode(pinned=True)
+        for _ in range(5):
+            planner.plan(one, sptr)
+        samples = []
+        for _ in range(args.latency_reps):
+            t0 = time.perf_counter()
+            planner.plan(one, sptr)
+            samples.append((time.perf_counter() - t0) * 1000.0)
+        latency[name] = {"gpu_e2e_ms_median": statistics.median(samples)}
+
+    cpu = None
+    if not args.no_cpu_baseline:
+        cpu = cpu_baseline(args.cpu_sample, os.cpu_count() or 1)
+        try:
+            import pyoracle as po
+            if po.ref_available():
+                for name, (fam, tasks, devices) in CONFIGS.items():
+                    latency[name]["cpu_reference_ms_median"] = po.ref_latency_ms(fam, tasks, devices, 100)
+        except Exception:
+            pass
+
+    line = {
+        "metric": METRIC,
+        "value": value,
+        "unit": "plans/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": 1000.0 * t_max / args.steps,
+        "higher_is_better": True,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": f"sweep-{args.mixtures} (BASELINE config 5: 2-16 tasks, clip/ofasys/qwen, 8-64 devices)",
+                   "plans_per_rank": len(ps), "sharding": "strided i % world == rank",
+                   "l2": "256 MiB buffer written between timed steps (outside the timed events)",
+                   "parallelism": f"dp{world} (independent plans, one NCCL min-loc all_gather at the end)"},
+        "e2e": {"value": e2e_value, "unit": "plans/s", "h2d_bytes_per_step": in_bytes_blob,
+                "d2h_bytes_per_step": d2h_step, "path": "ws_plan_batch_host (pinned host in/out)"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic, "kernel": "k_plan",
+                     "algorithmic_bytes_per_launch": kplan_bytes, "kernel_ms": kplan_ms, "peak_source": peak_src,
+                     "k_fit_ms": kfit_ms},
+        "cpu_baseline": cpu,
+        "gpu_launches": launches_per_step * args.steps,
+        "clocks": clk,
+        "latency_ms": latency,
+        "parity": {"infeasible_plans": int(infeasible.item()), "best_gap": best_key, "best_index": best_idx},
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+def ctypes_sizeof_result() -> int:
+    import ctypes
+    from paper_2409_03365_b200 import PlanResult
+    return ctypes.sizeof(PlanResult)
+
+
+if __name__ == "__main__":
+    main()

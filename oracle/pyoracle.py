@@ -1,0 +1,121 @@
+"""ctypes binding of the CPU oracle (oracle/liboracle.so) and, when built, the
+reference bridge (oracle/_ref/libwsref.so).
+
+TEST INFRASTRUCTURE ONLY: imported by tests/, __graft_entry__.smoke() and
+bench.py's cpu_baseline / --impl reference legs, never by the product path.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from pathlib import Path
+
+HERE = Path(__file__).resolve().parent
+ORACLE_LIB = HERE / "liboracle.so"
+REF_LIB = HERE / "_ref" / "libwsref.so"
+
+_oracle = None
+_ref = None
+
+
+def oracle():
+    global _oracle
+    if _oracle is None:
+        if not ORACLE_LIB.exists():
+            raise ImportError(f"{ORACLE_LIB} missing (make -C oracle)")
+        lib = C.CDLL(str(ORACLE_LIB))
+        lib.wso_plan_batch.restype = C.c_int
+        lib.wso_plan_batch.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint64, C.POINTER(C.c_uint64)]
+        _oracle = lib
+    return _oracle
+
+
+def plan_batch(pset):
+    """Plan every problem of a ProblemSet on the CPU oracle; returns Results."""
+    from paper_2409_03365_b200 import Results
+    cap = pset.arena_bound()
+    out = Results(len(pset), cap)
+    oracle().wso_plan_batch(pset.batch, out.results, out.arena, cap, C.byref(out.arena_used))
+    return out
+
+
+class RefOpts(C.Structure):
+    _fields_ = [("eps", C.c_double), ("max_iters", C.c_int), ("drop_floor", C.c_double),
+                ("sequential", C.c_int), ("bt_depth", C.c_int), ("bt_branching", C.c_int),
+                ("grad_mult", C.c_double), ("synth_noise", C.c_double), ("synth_seed", C.c_ulonglong)]
+
+
+def ref_available() -> bool:
+    return REF_LIB.exists()
+
+
+def ref():
+    """The reference planner compiled from the reference headers (build container only)."""
+    global _ref
+    if _ref is None:
+        lib = C.CDLL(str(REF_LIB))
+        vp = C.c_void_p
+        lib.wsref_plan_text.restype = vp
+        lib.wsref_plan_text.argtypes = [C.c_char_p, C.c_char_p, C.POINTER(RefOpts)]
+        lib.wsref_free.argtypes = [vp]
+        lib.wsref_scenario.restype = C.c_int
+        lib.wsref_scenario.argtypes = [C.c_char_p, C.c_int, C.c_int, C.c_ulonglong, C.POINTER(vp), C.POINTER(vp)]
+        lib.wsref_fuzz.restype = C.c_int
+        lib.wsref_fuzz.argtypes = [C.c_int, C.POINTER(C.POINTER(vp)), C.POINTER(C.POINTER(vp))]
+        lib.wsref_free_list.argtypes = [C.POINTER(vp), C.c_int]
+        lib.wsref_sweep_plan.restype = vp
+        lib.wsref_sweep_plan.argtypes = [C.c_long]
+        lib.wsref_sweep_bench.restype = C.c_double
+        lib.wsref_sweep_bench.argtypes = [C.c_long, C.c_long, C.c_int, C.POINTER(C.c_long)]
+        lib.wsref_latency_ms.restype = C.c_double
+        lib.wsref_latency_ms.argtypes = [C.c_char_p, C.c_int, C.c_int, C.c_int]
+        _ref = lib
+    return _ref
+
+
+def _s(ptr) -> str:
+    try:
+        return C.string_at(ptr).decode()
+    finally:
+        ref().wsref_free(ptr)
+
+
+def ref_options(**kw) -> RefOpts:
+    o = RefOpts(1e-7, 200, 0.0, 0, 2, 3, 3.0, 0.0, 0)
+    for k, v in kw.items():
+        setattr(o, k, v)
+    return o
+
+
+def ref_plan_text(workload: str, topology: str, **opts) -> str:
+    return _s(ref().wsref_plan_text(workload.encode(), topology.encode(), C.byref(ref_options(**opts))))
+
+
+def ref_scenario(name: str, tasks: int, devices: int, seed: int = 0) -> tuple[str, str]:
+    w, t = C.c_void_p(), C.c_void_p()
+    rc = ref().wsref_scenario(name.encode(), tasks, devices, seed, C.byref(w), C.byref(t))
+    if rc != 0:
+        raise ValueError(_s(w))
+    return _s(w), _s(t)
+
+
+def ref_fuzz(count: int) -> list[tuple[str, str]]:
+    ws, ts = C.POINTER(C.c_void_p)(), C.POINTER(C.c_void_p)()
+    ref().wsref_fuzz(count, C.byref(ws), C.byref(ts))
+    out = [(C.string_at(ws[i]).decode(), C.string_at(ts[i]).decode()) for i in range(count)]
+    ref().wsref_free_list(ws, count)
+    ref().wsref_free_list(ts, count)
+    return out
+
+
+def ref_sweep_plan(i: int) -> str:
+    return _s(ref().wsref_sweep_plan(i))
+
+
+def ref_sweep_bench(start: int, count: int, threads: int) -> tuple[float, int]:
+    bad = C.c_long(0)
+    rate = ref().wsref_sweep_bench(start, count, threads, C.byref(bad))
+    return rate, bad.value
+
+
+def ref_latency_ms(name: str, tasks: int, devices: int, reps: int) -> float:
+    return ref().wsref_latency_ms(name.encode(), tasks, devices, reps)

@@ -1,0 +1,317 @@
+"""paper_2409_03365_b200 — B200-native execution planner of Spindle (arXiv 2409.03365).
+
+Python mirror of the reference planner interface
+(/root/reference/proj/include/wavesched/planner.hpp:156 ``plan_workload``) over
+the C-ABI in include/wsgpu/ws_abi.h and include/wsgpu/wsx.h.  All planning runs
+in the sm_100a kernels of lib/libwsgpu.so; importing fails loudly if that
+library is missing, and there is no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from pathlib import Path
+
+_PKG = Path(__file__).resolve().parent
+LIB_PATH = _PKG / "lib" / "libwsgpu.so"
+
+__all__ = [
+    "LIB_PATH", "Options", "PlanResult", "ProblemSet", "Planner", "plan_workload", "PlannerError",
+    "ParseError", "InfeasibleError", "InvariantError", "CyclicWorkload", "UnknownModule", "EmptyWorkload",
+    "InsufficientProfile", "DegenerateFit", "OutOfRange", "NoValidAllocation", "EmptyLevel",
+    "PlacementInfeasible", "LimitExceeded", "WS_STATUS", "raise_for_text",
+]
+
+
+# ---- exception taxonomy (common.hpp:20-60) ---------------------------------
+class PlannerError(RuntimeError):
+    """wavesched::Error"""
+
+
+class ParseError(PlannerError):
+    pass
+
+
+class InfeasibleError(PlannerError):
+    pass
+
+
+class InvariantError(PlannerError):
+    pass
+
+
+class CyclicWorkload(ParseError):
+    pass
+
+
+class UnknownModule(ParseError):
+    pass
+
+
+class EmptyWorkload(ParseError):
+    pass
+
+
+class InsufficientProfile(ParseError):
+    pass
+
+
+class DegenerateFit(InfeasibleError):
+    pass
+
+
+class OutOfRange(InvariantError):
+    pass
+
+
+class NoValidAllocation(InfeasibleError):
+    pass
+
+
+class EmptyLevel(InvariantError):
+    pass
+
+
+class PlacementInfeasible(InfeasibleError):
+    pass
+
+
+class LimitExceeded(PlannerError):
+    """Input beyond the WS_MAX_* limits of this build."""
+
+
+_ERRORS = {c.__name__: c for c in (
+    ParseError, InfeasibleError, InvariantError, CyclicWorkload, UnknownModule, EmptyWorkload,
+    InsufficientProfile, DegenerateFit, OutOfRange, NoValidAllocation, EmptyLevel, PlacementInfeasible,
+    LimitExceeded)}
+_ERRORS["Error"] = PlannerError
+
+WS_STATUS = {"ok": 0, "parse": 2, "infeasible": 3, "invariant": 4, "limit": 5, "internal": 6}
+
+
+def raise_for_text(text: str) -> str:
+    """Return plan text, or raise the exception an ``error <Class>: <what>`` line names."""
+    if text.startswith("error "):
+        head, _, what = text[len("error "):].rstrip("\n").partition(": ")
+        raise _ERRORS.get(head, PlannerError)(what)
+    return text
+
+
+# ---- C structures -------------------------------------------------------------
+class Options(C.Structure):
+    """PlannerOptions (planner.hpp:21-27) as ws_options (wsx.h)."""
+    _fields_ = [("eps", C.c_double), ("max_iters", C.c_int32), ("sequential", C.c_int32),
+                ("drop_floor", C.c_double), ("bt_depth", C.c_int32), ("bt_branching", C.c_int32),
+                ("grad_mult", C.c_double), ("synth_noise", C.c_double), ("synth_seed", C.c_uint64)]
+
+
+class PlanResult(C.Structure):
+    """ws_plan_result (ws_abi.h)."""
+    _fields_ = [("status", C.c_int32), ("err_code", C.c_int32), ("err_a", C.c_int64), ("err_b", C.c_int64),
+                ("err_x", C.c_double), ("err_y", C.c_double), ("n_metaops", C.c_int32), ("n_edges", C.c_int32),
+                ("n_levels", C.c_int32), ("n_waves", C.c_int32), ("n_entries", C.c_int32), ("n_flows", C.c_int32),
+                ("n_pieces", C.c_int32), ("pad", C.c_int32), ("lower_bound", C.c_double), ("end_time", C.c_double),
+                ("offset", C.c_uint64), ("size", C.c_uint64)]
+
+
+def _load() -> C.CDLL:
+    if not LIB_PATH.exists():
+        raise ImportError(f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'`")
+    lib = C.CDLL(str(LIB_PATH))
+    vp, i32, i64, u64 = C.c_void_p, C.c_int32, C.c_int64, C.c_uint64
+    sig = {
+        "ws_ctx_create": (C.c_int, [C.c_int, C.POINTER(vp)]),
+        "ws_ctx_destroy": (None, [vp]),
+        "ws_ctx_last_error": (C.c_char_p, [vp]),
+        "ws_plan_batch_host": (C.c_int, [vp, vp, vp, vp, u64, C.POINTER(u64), vp]),
+        "ws_stage_batch": (C.c_int, [vp, vp, vp]),
+        "ws_plan_staged": (C.c_int, [vp, vp]),
+        "ws_fetch_results": (C.c_int, [vp, vp, vp, u64, C.POINTER(u64), vp]),
+        "ws_last_launch_count": (C.c_int, [vp]),
+        "ws_last_kernel_ms": (C.c_int, [vp, C.POINTER(C.c_double), C.c_int]),
+        "ws_best_staged": (C.c_int, [vp, C.c_int, C.POINTER(C.c_double), C.POINTER(i64), vp]),
+        "ws_arena_bound": (u64, [vp]),
+        "wsx_default_options": (None, [C.POINTER(Options)]),
+        "wsx_set_new": (vp, []),
+        "wsx_set_free": (None, [vp]),
+        "wsx_set_size": (i32, [vp]),
+        "wsx_add_text": (i32, [vp, C.c_char_p, C.c_char_p, C.POINTER(Options)]),
+        "wsx_add_scenario": (i32, [vp, C.c_char_p, i32, i32, u64, C.POINTER(Options)]),
+        "wsx_add_sweep": (i32, [vp, i64, i64, C.POINTER(Options)]),
+        "wsx_set_error": (C.c_char_p, [vp]),
+        "wsx_encode": (vp, [vp, i32]),
+        "wsx_encoded_bytes": (u64, [vp]),
+        "wsx_result_text": (vp, [vp, i32, vp, vp]),
+        "wsx_dump_workload": (vp, [vp, i32]),
+        "wsx_dump_topology": (vp, [vp, i32]),
+        "wsx_free_str": (None, [vp]),
+        "wsx_plan_workload_text": (vp, [C.c_char_p, C.c_char_p, C.POINTER(Options)]),
+        "wsx_algorithmic_bytes": (None, [vp, vp, vp, C.POINTER(u64), C.POINTER(u64)]),
+    }
+    for name, (res, args) in sig.items():
+        f = getattr(lib, name)
+        f.restype = res
+        f.argtypes = args
+    return lib
+
+
+lib = _load()
+
+
+def _take_str(ptr: int) -> str:
+    try:
+        return C.string_at(ptr).decode()
+    finally:
+        lib.wsx_free_str(ptr)
+
+
+def make_options(**kw) -> Options:
+    """Options with the reference defaults, overridden by keyword (eps, max_iters,
+    sequential, drop_floor, bt_depth, bt_branching, grad_mult, synth_noise, synth_seed)."""
+    o = Options()
+    lib.wsx_default_options(C.byref(o))
+    for k, v in kw.items():
+        if not hasattr(o, k):
+            raise TypeError(f"unknown planner option {k!r}")
+        setattr(o, k, v)
+    return o
+
+
+class ProblemSet:
+    """A batch of planning problems (WorkloadSpec + ClusterTopology + options)."""
+
+    def __init__(self):
+        self._h = lib.wsx_set_new()
+        self._batch = None
+
+    def __del__(self):
+        h, self._h = getattr(self, "_h", None), None
+        if h:
+            lib.wsx_set_free(h)
+
+    def __len__(self) -> int:
+        return lib.wsx_set_size(self._h)
+
+    def _check(self, idx: int) -> int:
+        if idx < 0:
+            raise ParseError(lib.wsx_set_error(self._h).decode())
+        self._batch = None
+        return idx
+
+    def add_text(self, workload: str, topology: str, **opts) -> int:
+        return self._check(lib.wsx_add_text(self._h, workload.encode(), topology.encode(),
+                                            C.byref(make_options(**opts))))
+
+    def add_scenario(self, name: str, tasks: int, devices: int, seed: int = 0, **opts) -> int:
+        return self._check(lib.wsx_add_scenario(self._h, name.encode(), tasks, devices, seed,
+                                                C.byref(make_options(**opts))))
+
+    def add_sweep(self, start: int, count: int, **opts) -> int:
+        return self._check(lib.wsx_add_sweep(self._h, start, count, C.byref(make_options(**opts))))
+
+    def encode(self, pinned: bool = False) -> int:
+        """Encode into the ws_batch SoA format; returns the ws_batch pointer."""
+        self._batch = lib.wsx_encode(self._h, 1 if pinned else 0)
+        return self._batch
+
+    @property
+    def batch(self) -> int:
+        return self._batch if self._batch is not None else self.encode()
+
+    @property
+    def encoded_bytes(self) -> int:
+        return int(lib.wsx_encoded_bytes(self._h))
+
+    def arena_bound(self) -> int:
+        return int(lib.ws_arena_bound(self.batch))
+
+    def text(self, i: int, results, arena) -> str:
+        """write_plan() text (plan_io.hpp:53-110) of problem i, or 'error <Class>: <what>'."""
+        return _take_str(lib.wsx_result_text(self._h, i, C.cast(results, C.c_void_p),
+                                             C.cast(arena, C.c_void_p)))
+
+    def algorithmic_bytes(self, res: "Results") -> tuple[int, int]:
+        """SURVEY §8(d) compulsory (in, out) bytes of this set's plans."""
+        a, b = C.c_uint64(), C.c_uint64()
+        lib.wsx_algorithmic_bytes(self._h, res.results, res.arena, C.byref(a), C.byref(b))
+        return a.value, b.value
+
+    def dump_workload(self, i: int) -> str:
+        return _take_str(lib.wsx_dump_workload(self._h, i))
+
+    def dump_topology(self, i: int) -> str:
+        return _take_str(lib.wsx_dump_topology(self._h, i))
+
+
+class Results:
+    """Host copy of one planning call: ws_plan_result[] + arena bytes."""
+
+    def __init__(self, n: int, arena_cap: int):
+        self.results = (PlanResult * max(n, 1))()
+        self.arena = (C.c_uint8 * max(arena_cap, 8))()
+        self.arena_used = C.c_uint64(0)
+        self.n = n
+
+    def texts(self, pset: ProblemSet) -> list[str]:
+        return [pset.text(i, self.results, self.arena) for i in range(self.n)]
+
+
+class Planner:
+    """A ws_ctx bound to one CUDA device."""
+
+    def __init__(self, device: int = 0):
+        h = C.c_void_p()
+        if lib.ws_ctx_create(device, C.byref(h)) != 0:
+            raise PlannerError(f"CUDA planner unavailable on device {device}")
+        self._h = h
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib.ws_ctx_destroy(self._h)
+            self._h = None
+
+    __del__ = close
+
+    def _ok(self, rc: int):
+        if rc != 0:
+            raise PlannerError(lib.ws_ctx_last_error(self._h).decode())
+
+    def plan(self, pset: ProblemSet, stream: int | None = None) -> Results:
+        """Host batch in, host results out (H2D + kernels + D2H)."""
+        cap = pset.arena_bound()
+        out = Results(len(pset), cap)
+        self._ok(lib.ws_plan_batch_host(self._h, pset.batch, out.results, out.arena, cap,
+                                        C.byref(out.arena_used), stream))
+        return out
+
+    def stage(self, pset: ProblemSet, stream: int | None = None):
+        self._ok(lib.ws_stage_batch(self._h, pset.batch, stream))
+
+    def plan_staged(self, stream: int | None = None):
+        self._ok(lib.ws_plan_staged(self._h, stream))
+
+    def fetch(self, pset: ProblemSet, stream: int | None = None) -> Results:
+        cap = pset.arena_bound()
+        out = Results(len(pset), cap)
+        self._ok(lib.ws_fetch_results(self._h, out.results, out.arena, cap, C.byref(out.arena_used), stream))
+        return out
+
+    def best(self, mode: int = 0, stream: int | None = None) -> tuple[float, int]:
+        key, idx = C.c_double(), C.c_int64()
+        self._ok(lib.ws_best_staged(self._h, mode, C.byref(key), C.byref(idx), stream))
+        return key.value, idx.value
+
+    @property
+    def launch_count(self) -> int:
+        return lib.ws_last_launch_count(self._h)
+
+    def kernel_ms(self) -> tuple[float, float]:
+        buf = (C.c_double * 2)()
+        lib.ws_last_kernel_ms(self._h, buf, 2)
+        return buf[0], buf[1]
+
+
+def plan_workload(workload: str, topology: str, **opts) -> str:
+    """Drop-in for wavesched::plan_workload on reference text inputs: returns the
+    write_plan() text of the plan, or raises the reference's exception class."""
+    return raise_for_text(_take_str(lib.wsx_plan_workload_text(workload.encode(), topology.encode(),
+                                                               C.byref(make_options(**opts)))))

@@ -77,7 +77,7 @@ __device__ __forceinline__ bool dec_less(int a, int b) {
 // reference sorts with ties; serial, run by one lane.
 // ---------------------------------------------------------------------------
 template <typename Cmp>
-__device__ void ls_push_heap(int* a, int hole, int top, int value, Cmp& comp) {
+__host__ __device__ void ls_push_heap(int* a, int hole, int top, int value, Cmp& comp) {
     int parent = (hole - 1) / 2;
     while (hole > top && comp(a[parent], value)) {
         a[hole] = a[parent];
@@ -88,7 +88,7 @@ __device__ void ls_push_heap(int* a, int hole, int top, int value, Cmp& comp) {
 }
 
 template <typename Cmp>
-__device__ void ls_adjust_heap(int* a, int hole, int len, int value, Cmp& comp) {
+__host__ __device__ void ls_adjust_heap(int* a, int hole, int len, int value, Cmp& comp) {
     const int top = hole;
     int child = hole;
     while (child < (len - 1) / 2) {
@@ -106,7 +106,7 @@ __device__ void ls_adjust_heap(int* a, int hole, int len, int value, Cmp& comp) 
 }
 
 template <typename Cmp>
-__device__ void ls_heap_sort(int* a, int len, Cmp& comp) {  // __partial_sort(first, last, last)
+__host__ __device__ void ls_heap_sort(int* a, int len, Cmp& comp) {  // __partial_sort(first, last, last)
     if (len >= 2) {
         for (int parent = (len - 2) / 2;; --parent) {
             ls_adjust_heap(a, parent, len, a[parent], comp);
@@ -122,7 +122,7 @@ __device__ void ls_heap_sort(int* a, int len, Cmp& comp) {  // __partial_sort(fi
 }
 
 template <typename Cmp>
-__device__ void ls_insertion_sort(int* a, int lo, int hi, Cmp& comp) {
+__host__ __device__ void ls_insertion_sort(int* a, int lo, int hi, Cmp& comp) {
     if (lo == hi) return;
     for (int i = lo + 1; i < hi; ++i) {
         const int v = a[i];
@@ -141,9 +141,13 @@ __device__ void ls_insertion_sort(int* a, int lo, int hi, Cmp& comp) {
 }
 
 template <typename Cmp>
-__device__ void ls_sort(int* a, int n, Cmp& comp) {
+__host__ __device__ void ls_sort(int* a, int n, Cmp& comp) {
     if (n <= 1) return;
+#ifdef __CUDA_ARCH__
     int lg = 31 - __clz(n);
+#else
+    int lg = 31 - __builtin_clz(static_cast<unsigned>(n));
+#endif
     // explicit stack reproducing the recursion order of __introsort_loop
     int st_f[40], st_l[40], st_d[40];
     int sp = 0;

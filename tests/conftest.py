@@ -1,0 +1,46 @@
+"""Shared fixtures.  `-m "not gpu"` runs on CPU (oracle vs golden fixtures,
+host logic, C-ABI exports, gloo multi-process); `-m gpu` runs the parity
+tests of the CUDA planner on a B200."""
+from __future__ import annotations
+
+import gzip
+import json
+import sys
+from pathlib import Path
+
+import pytest
+
+ROOT = Path(__file__).resolve().parent.parent
+sys.path.insert(0, str(ROOT))
+sys.path.insert(0, str(ROOT / "oracle"))
+GOLDEN = ROOT / "tests" / "golden"
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs a B200 (CUDA planner parity tests)")
+
+
+@pytest.fixture(scope="session")
+def golden_cases():
+    with gzip.open(GOLDEN / "cases.json.gz", "rt") as f:
+        return json.load(f)
+
+
+@pytest.fixture(scope="session")
+def sweep_hashes():
+    with gzip.open(GOLDEN / "sweep_hashes.txt.gz", "rt") as f:
+        return f.read().split()
+
+
+def build_set(cases):
+    """ProblemSet of the parseable cases; returns (set, kept cases, parse-failed cases)."""
+    import paper_2409_03365_b200 as ws
+    ps = ws.ProblemSet()
+    kept, failed = [], []
+    for c in cases:
+        try:
+            ps.add_text(c["workload"], c["topology"], **c["options"])
+            kept.append(c)
+        except ws.ParseError as e:
+            failed.append((c, str(e)))
+    return ps, kept, failed

@@ -1,0 +1,138 @@
+"""GPU parity: the CUDA planner (through the C-ABI) against the reference's
+outputs (golden fixtures) and the CPU oracle, bit-exact.  Run with -m gpu."""
+import ctypes
+import hashlib
+
+import pytest
+
+from conftest import build_set
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def planner():
+    import paper_2409_03365_b200 as ws
+    return ws.Planner(0)
+
+
+def records(res, i):
+    """(header without arena offset, record bytes) of plan i."""
+    r = res.results[i]
+    hdr = bytes(r)
+    size = ctypes.sizeof(r)
+    hdr = bytearray(hdr)
+    off_field = type(r).offset.offset
+    hdr[off_field:off_field + 8] = b"\0" * 8
+    body = bytes(res.arena[r.offset:r.offset + r.size]) if r.status == 0 else b""
+    return bytes(hdr[:size]), body
+
+
+def test_gpu_matches_reference_golden_cases(planner, golden_cases):
+    ps, kept, _ = build_set(golden_cases)
+    ps.encode(pinned=True)
+    texts = planner.plan(ps).texts(ps)
+    bad = [c["name"] for c, t in zip(kept, texts) if t != c["expected"]]
+    assert not bad, bad[:10]
+    assert planner.launch_count >= 2
+
+
+def test_gpu_full_sweep_100k_matches_reference(planner, sweep_hashes):
+    """BASELINE config 5 at full size: every mixture's plan text hashes to the
+    reference planner's (217 PlacementInfeasible outcomes included)."""
+    import paper_2409_03365_b200 as ws
+    n = len(sweep_hashes)
+    assert n == 100000
+    ps = ws.ProblemSet()
+    ps.add_sweep(0, n)
+    ps.encode(pinned=True)
+    res = planner.plan(ps)
+    got = [hashlib.sha1(ps.text(i, res.results, res.arena).encode()).hexdigest()[:16] for i in range(n)]
+    mism = [i for i in range(n) if got[i] != sweep_hashes[i]]
+    assert not mism, mism[:20]
+    infeasible = sum(1 for i in range(n) if res.results[i].status != 0)
+    assert infeasible == 217
+
+
+def test_gpu_records_bit_identical_to_oracle(planner, golden_cases):
+    import paper_2409_03365_b200 as ws
+    import pyoracle
+    ps, kept, _ = build_set(golden_cases)
+    ps.add_sweep(0, 3000)
+    ps.encode(pinned=True)
+    g = planner.plan(ps)
+    o = pyoracle.plan_batch(ps)
+    bad = [i for i in range(len(ps)) if records(g, i) != records(o, i)]
+    assert not bad, bad[:10]
+
+
+def test_gpu_best_plan_minloc_matches_oracle(planner):
+    import paper_2409_03365_b200 as ws
+    import pyoracle
+    from paper_2409_03365_b200 import parallel
+    ps = ws.ProblemSet()
+    ps.add_sweep(0, 4000)
+    ps.encode(pinned=True)
+    planner.stage(ps)
+    planner.plan_staged()
+    key, idx = planner.best(0)
+    o = pyoracle.plan_batch(ps)
+    recs = [(o.results[i].end_time / o.results[i].lower_bound, i) for i in range(len(ps)) if o.results[i].status == 0]
+    assert (key, idx) == parallel.reduce_minloc(recs)
+    key1, idx1 = planner.best(1)
+    recs1 = [(o.results[i].end_time, i) for i in range(len(ps)) if o.results[i].status == 0]
+    assert (key1, idx1) == parallel.reduce_minloc(recs1)
+
+
+def test_gpu_empty_batch(planner):
+    import paper_2409_03365_b200 as ws
+    ps = ws.ProblemSet()
+    ps.encode(pinned=True)
+    res = planner.plan(ps)
+    assert res.n == 0
+
+
+def test_gpu_ragged_batch_and_determinism(planner, golden_cases):
+    """Mixed sizes (1..64 devices, 1..22 MetaOps, error outcomes) in one batch,
+    planned twice on the same context: identical records, all equal to the
+    reference."""
+    import paper_2409_03365_b200 as ws
+    picks = [c for c in golden_cases if c["name"].startswith(("edge/", "fuzz/1", "config/"))]
+    ps, kept, _ = build_set(picks[::-1])
+    ps.add_sweep(99000, 500)
+    ps.encode(pinned=True)
+    a = planner.plan(ps)
+    b = planner.plan(ps)
+    assert all(records(a, i) == records(b, i) for i in range(len(ps)))
+    texts = a.texts(ps)
+    assert all(t == c["expected"] for c, t in zip(kept, texts))
+
+
+def test_gpu_device_limit_is_loud(planner):
+    """More devices than the build supports is a reported LimitExceeded, not a fallback."""
+    import paper_2409_03365_b200 as ws
+    topo = "island 0: " + " ".join(str(i) for i in range(70)) + "\nbw intra=1e11 inter=1e10\nmem 100000000000\n"
+    ps = ws.ProblemSet()
+    ps.add_text("module a layers=2 B=48\ntruth a piece 1 1024 0.1 0 1\ntask t flow=a\n", topo)
+    ps.encode(pinned=True)
+    text = planner.plan(ps).texts(ps)[0]
+    assert text.startswith("error LimitExceeded")
+
+
+def test_gpu_dropin_plan_workload(golden_cases):
+    import paper_2409_03365_b200 as ws
+    c = next(c for c in golden_cases if c["name"] == "config/clip-like/10t/64d/default")
+    assert ws.plan_workload(c["workload"], c["topology"]) == c["expected"]
+    c = next(c for c in golden_cases if c["name"] == "edge/place/infeasible-memory")
+    with pytest.raises(ws.PlacementInfeasible, match="no feasible placement for wave 0"):
+        ws.plan_workload(c["workload"], c["topology"])
+
+
+def test_gpu_kernel_timing_reported(planner):
+    import paper_2409_03365_b200 as ws
+    ps = ws.ProblemSet()
+    ps.add_sweep(0, 2000)
+    ps.encode(pinned=True)
+    planner.plan(ps)
+    fit_ms, plan_ms = planner.kernel_ms()
+    assert fit_ms > 0 and plan_ms > 0
