@@ -56,6 +56,11 @@ void wsx_free_str(char* p);
 void wsx_algorithmic_bytes(const wsx_set* s, const ws_plan_result* results, const uint8_t* arena,
                            uint64_t* in_bytes, uint64_t* out_bytes);
 
+/* Page-locked host buffers for results/arena (cudaMallocHost; plain malloc
+ * when no CUDA device is present).  Not zero-initialized. */
+void* wsx_host_alloc(uint64_t bytes);
+void wsx_host_free(void* p);
+
 /* Drop-in single-plan call through the process default context:
  * plan text, or "error <Class>: <what>\n". */
 char* wsx_plan_workload_text(const char* workload, const char* topology, const ws_options* o);

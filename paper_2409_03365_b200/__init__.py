@@ -146,6 +146,8 @@ def _load() -> C.CDLL:
         "wsx_free_str": (None, [vp]),
         "wsx_plan_workload_text": (vp, [C.c_char_p, C.c_char_p, C.POINTER(Options)]),
         "wsx_algorithmic_bytes": (None, [vp, vp, vp, C.POINTER(u64), C.POINTER(u64)]),
+        "wsx_host_alloc": (vp, [u64]),
+        "wsx_host_free": (None, [vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -243,13 +245,29 @@ class ProblemSet:
 
 
 class Results:
-    """Host copy of one planning call: ws_plan_result[] + arena bytes."""
+    """Host copy of one planning call: ws_plan_result[] + arena bytes, in
+    page-locked host memory (wsx_host_alloc) so the D2H copies run at full
+    PCIe/C2C speed.  Reusable across calls of the same or smaller size."""
 
     def __init__(self, n: int, arena_cap: int):
-        self.results = (PlanResult * max(n, 1))()
-        self.arena = (C.c_uint8 * max(arena_cap, 8))()
+        self._res_ptr = lib.wsx_host_alloc(C.sizeof(PlanResult) * max(n, 1))
+        self._arena_ptr = lib.wsx_host_alloc(max(arena_cap, 8))
+        self.results = (PlanResult * max(n, 1)).from_address(self._res_ptr)
+        self.arena = (C.c_uint8 * max(arena_cap, 8)).from_address(self._arena_ptr)
         self.arena_used = C.c_uint64(0)
         self.n = n
+        self.cap_plans = max(n, 1)
+        self.cap_arena = max(arena_cap, 8)
+
+    def fits(self, n: int, arena_cap: int) -> bool:
+        return n <= self.cap_plans and arena_cap <= self.cap_arena
+
+    def __del__(self):
+        for name in ("_res_ptr", "_arena_ptr"):
+            ptr = getattr(self, name, None)
+            if ptr:
+                lib.wsx_host_free(ptr)
+                setattr(self, name, None)
 
     def texts(self, pset: ProblemSet) -> list[str]:
         return [pset.text(i, self.results, self.arena) for i in range(self.n)]
@@ -275,10 +293,17 @@ class Planner:
         if rc != 0:
             raise PlannerError(lib.ws_ctx_last_error(self._h).decode())
 
-    def plan(self, pset: ProblemSet, stream: int | None = None) -> Results:
-        """Host batch in, host results out (H2D + kernels + D2H)."""
+    def _out(self, pset: ProblemSet, out: Results | None) -> tuple[Results, int]:
         cap = pset.arena_bound()
-        out = Results(len(pset), cap)
+        if out is None or not out.fits(len(pset), cap):
+            out = Results(len(pset), cap)
+        out.n = len(pset)
+        return out, cap
+
+    def plan(self, pset: ProblemSet, stream: int | None = None, out: Results | None = None) -> Results:
+        """Host batch in, host results out (H2D + kernels + D2H); pass `out`
+        to reuse page-locked result buffers across calls."""
+        out, cap = self._out(pset, out)
         self._ok(lib.ws_plan_batch_host(self._h, pset.batch, out.results, out.arena, cap,
                                         C.byref(out.arena_used), stream))
         return out
@@ -289,9 +314,8 @@ class Planner:
     def plan_staged(self, stream: int | None = None):
         self._ok(lib.ws_plan_staged(self._h, stream))
 
-    def fetch(self, pset: ProblemSet, stream: int | None = None) -> Results:
-        cap = pset.arena_bound()
-        out = Results(len(pset), cap)
+    def fetch(self, pset: ProblemSet, stream: int | None = None, out: Results | None = None) -> Results:
+        out, cap = self._out(pset, out)
         self._ok(lib.ws_fetch_results(self._h, out.results, out.arena, cap, C.byref(out.arena_used), stream))
         return out
 

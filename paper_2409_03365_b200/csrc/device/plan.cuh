@@ -35,6 +35,7 @@ struct Ctl {  // per-warp control block in shared memory
     int pad;
     long long a, b;
     double x, y;
+    double level_offset;  // merge_levels running offset (lane 0 -> warp)
     int i0, i1, i2, i3;
 };
 
@@ -1620,7 +1621,7 @@ __global__ void __launch_bounds__(32 * kPlanWarps) k_plan(PlanArgs A) {
                 }
                 ctl->i0 = nW;
                 ctl->i1 = nE;
-                ctl->x = offset;
+                ctl->level_offset = offset;
             }
             __syncwarp();
             if (ctl->err) {
@@ -1629,7 +1630,7 @@ __global__ void __launch_bounds__(32 * kPlanWarps) k_plan(PlanArgs A) {
             }
             nW = ctl->i0;
             nE = ctl->i1;
-            offset = ctl->x;
+            offset = ctl->level_offset;
         }
         end_time = offset;
         P.nW = nW;

@@ -1,5 +1,7 @@
 // api.cpp — the C++ drop-in plan_workload (planner.hpp:156-212) over the
 // C-ABI, and the wsx.h helper API used by FFI callers.
+#include <cuda_runtime_api.h>
+
 #include <cstdlib>
 #include <cstring>
 #include <deque>
@@ -225,6 +227,24 @@ void wsx_algorithmic_bytes(const wsx_set* s, const ws_plan_result* results, cons
     }
     *in_bytes = in;
     *out_bytes = out;
+}
+
+void* wsx_host_alloc(uint64_t bytes) {
+    void* p = nullptr;
+    if (cudaMallocHost(&p, bytes ? bytes : 8) == cudaSuccess) return p;
+    cudaGetLastError();
+    return std::malloc(bytes ? bytes : 8);
+}
+
+void wsx_host_free(void* p) {
+    if (!p) return;
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, p) == cudaSuccess && a.type == cudaMemoryTypeHost) {
+        cudaFreeHost(p);
+        return;
+    }
+    cudaGetLastError();
+    std::free(p);
 }
 
 char* wsx_plan_workload_text(const char* workload, const char* topology, const ws_options* o) {
