@@ -1,0 +1,249 @@
+// kcommon.cuh — pieces shared by the planner kernels k_sched and k_place:
+// the per-warp control block, read-only T-table/curve access, the
+// reference's numeric kernels (inverse_exact, shard_moves), placement scores
+// and warp reductions.
+#pragma once
+#include "common.cuh"
+#include "fit.cuh"
+
+namespace wsdev {
+
+struct Ctl {  // per-warp control block (shared memory)
+    int err;
+    int pad;
+    long long a, b;
+    double x, y;
+    int i0, i1, i2, i3;
+    double d0;
+};
+
+__device__ __forceinline__ bool set_err(Ctl* ctl, int code, long long a = 0, long long b = 0) {
+    if (!ctl->err) {
+        ctl->err = code;
+        ctl->a = a;
+        ctl->b = b;
+    }
+    return false;
+}
+
+__device__ __forceinline__ int status_of(int code) {
+    switch (code) {
+        case WS_E_FIT_NONPOSITIVE:
+        case WS_E_TP_EXCEEDS:
+        case WS_E_BT_BUDGET:
+        case WS_E_NO_PLACEMENT_W0: return WS_STATUS_INFEASIBLE;
+        case WS_E_CURVE_START:
+        case WS_E_CURVE_CONTIG:
+        case WS_E_EVAL_RANGE:
+        case WS_E_NO_SCHEDULABLE:
+        case WS_E_NO_PROGRESS: return WS_STATUS_INVARIANT;
+        default:
+            if (code >= 40 && code < 60) return WS_STATUS_LIMIT;
+            if (code >= 60) return WS_STATUS_INTERNAL;
+            return WS_STATUS_PARSE;
+    }
+}
+
+__device__ __forceinline__ void write_error(ws_plan_result* out, const Ctl* ctl) {
+    ws_plan_result r{};
+    r.err_code = ctl->err;
+    r.status = status_of(ctl->err);
+    r.err_a = ctl->a;
+    r.err_b = ctl->b;
+    r.err_x = ctl->x;
+    r.err_y = ctl->y;
+    *out = r;
+}
+
+// ScalingCurve::eval at integer n (scaling.hpp:66-70) through the T-table;
+// n above the curve's n_max is OutOfRange.  gm: global module index.
+__device__ __forceinline__ double t_at(const FitOut& F, int gm, int n) {
+    return __ldg(F.ttab + static_cast<int64_t>(gm) * F.tstride + (n - 1));
+}
+
+struct TErr {  // error-capturing lookup (first error wins)
+    const FitOut* F;
+    const int* gm_of;    // metaop -> global module (shared)
+    const int* nmax_of;  // metaop -> curve n_max (shared)
+    Ctl* ctl;
+    __device__ double operator()(int k, int n) const {
+        if (n > nmax_of[k]) {
+            if (!ctl->err) {
+                ctl->err = WS_E_EVAL_RANGE;
+                ctl->x = n;
+                ctl->y = nmax_of[k];
+            }
+            return 1.0;
+        }
+        return t_at(*F, gm_of[k], n);
+    }
+};
+
+// ScalingCurve::inverse_exact (scaling.hpp:118-137) over fitted pieces
+__device__ __forceinline__ double inverse_exact(const double* __restrict__ pc, int np, double c, double w,
+                                                double nmax, double target) {
+    auto val = [&](int i, double n) {
+        return __ldg(pc + 5 * i + 2) + __ldg(pc + 5 * i + 3) * c + __ldg(pc + 5 * i + 4) * w / n;
+    };
+    if (target <= val(np - 1, nmax)) return nmax;
+    for (int i = 0; i < np; ++i) {
+        const double lo = __ldg(pc + 5 * i + 0), hi = __ldg(pc + 5 * i + 1);
+        const double hi_val = val(i, lo);
+        const double lo_val = val(i, hi);
+        const double b = __ldg(pc + 5 * i + 4) * w;
+        const double base = __ldg(pc + 5 * i + 2) + __ldg(pc + 5 * i + 3) * c;
+        if (target > hi_val + 1e-15 * fabs(hi_val)) {
+            if (b <= 0.0) return 0.0;
+            return b / (target - base);
+        }
+        if (target >= lo_val) {
+            if (b <= 0.0) return lo;
+            if (target <= base) return hi;
+            const double v = b / (target - base);
+            return v < lo ? lo : (hi < v ? hi : v);  // std::clamp
+        }
+    }
+    return nmax;
+}
+
+// shard_moves (placement.hpp:74-103) on device-index bitmasks; isl = island id per device
+__device__ __forceinline__ void shard_moves(uint64_t from, uint64_t to, uint64_t full, const int* isl,
+                                            uint64_t& intra, uint64_t& inter) {
+    intra = inter = 0;
+    if (!from || !to) return;
+    const uint64_t shared = from & to;
+    uint64_t src = from & ~shared, dst = to & ~shared;
+    const int pf = popc64(from), pt = popc64(to);
+    const int units = pf > pt ? pf : pt;
+    const int moving = units - popc64(shared);
+    if (moving == 0) return;
+    if (!src) src = from;
+    if (!dst) dst = to;
+    const double unit_bytes = static_cast<double>(full) / static_cast<double>(units);
+    const uint64_t bytes = static_cast<uint64_t>(llround(unit_bytes));
+    uint64_t rs = src, rt = dst;
+    int same = 0;
+    for (int i = 0; i < moving; ++i) {
+        const int s = low_bit(rs);
+        rs &= rs - 1;
+        if (!rs) rs = src;
+        const int t = low_bit(rt);
+        rt &= rt - 1;
+        if (!rt) rt = dst;
+        same += isl[s] == isl[t];
+    }
+    intra = static_cast<uint64_t>(same) * bytes;
+    inter = static_cast<uint64_t>(moving - same) * bytes;
+}
+
+// Score (placement.hpp:265-283)
+struct Score {
+    int valid;
+    int feasible;
+    int islands;
+    int rot;
+    double inter, intra, displaced, peak;
+    uint64_t devs;
+};
+
+__device__ __forceinline__ bool score_less(const Score& a, const Score& b) {
+    if (a.feasible != b.feasible) return a.feasible;
+    if (a.inter != b.inter) return a.inter < b.inter;
+    if (a.intra != b.intra) return a.intra < b.intra;
+    if (a.displaced != b.displaced) return a.displaced < b.displaced;
+    if (a.islands != b.islands) return a.islands < b.islands;
+    if (a.peak != b.peak) return a.peak < b.peak;
+    const uint64_t diff = a.devs ^ b.devs;  // sorted device-list lexicographic order
+    if (!diff) return false;
+    return (a.devs & (diff & (~diff + 1))) != 0;
+}
+
+__device__ __forceinline__ Score shfl_xor_score(const Score& s, int m) {
+    Score o;
+    o.valid = __shfl_xor_sync(kFull, s.valid, m);
+    o.feasible = __shfl_xor_sync(kFull, s.feasible, m);
+    o.islands = __shfl_xor_sync(kFull, s.islands, m);
+    o.rot = __shfl_xor_sync(kFull, s.rot, m);
+    o.inter = __shfl_xor_sync(kFull, s.inter, m);
+    o.intra = __shfl_xor_sync(kFull, s.intra, m);
+    o.displaced = __shfl_xor_sync(kFull, s.displaced, m);
+    o.peak = __shfl_xor_sync(kFull, s.peak, m);
+    o.devs = __shfl_xor_sync(kFull, s.devs, m);
+    return o;
+}
+
+__device__ __forceinline__ Score warp_min_score(Score s) {
+    for (int off = 16; off; off >>= 1) {
+        const Score o = shfl_xor_score(s, off);
+        if (o.valid && (!s.valid || score_less(o, s))) s = o;
+    }
+    return s;
+}
+
+__device__ __forceinline__ int warp_sum(int v) {
+    for (int off = 16; off; off >>= 1) v += __shfl_xor_sync(kFull, v, off);
+    return v;
+}
+
+__device__ __forceinline__ int warp_min_i(int v) {
+    for (int off = 16; off; off >>= 1) {
+        const int o = __shfl_xor_sync(kFull, v, off);
+        v = o < v ? o : v;
+    }
+    return v;
+}
+
+__device__ __forceinline__ double warp_max_d(double v) {  // std::max fold, NaN-free inputs
+    for (int off = 16; off; off >>= 1) {
+        const double o = __shfl_xor_sync(kFull, v, off);
+        v = (v < o) ? o : v;
+    }
+    return v;
+}
+
+__device__ __forceinline__ double warp_min_d(double v) {
+    for (int off = 16; off; off >>= 1) {
+        const double o = __shfl_xor_sync(kFull, v, off);
+        v = (o < v) ? o : v;
+    }
+    return v;
+}
+
+// kind bytes of module gm followed by "." and optionally a layer number
+struct OpKey {
+    const uint8_t* name;
+    int len;
+    char tail[12];
+    int tlen;
+    __device__ int size() const { return len + tlen; }
+    __device__ char at(int i) const { return i < len ? static_cast<char>(name[i]) : tail[i - len]; }
+};
+
+__device__ __forceinline__ OpKey op_key(const ws_batch& B, int gm, int layer, bool with_layer) {
+    OpKey k;
+    k.name = B.names + B.mod_name_off[gm];
+    k.len = B.mod_name_len[gm];
+    k.tail[0] = '.';
+    k.tlen = 1;
+    if (with_layer) {
+        char t[11];
+        int n = 0, v = layer;
+        do { t[n++] = static_cast<char>('0' + v % 10); v /= 10; } while (v);
+        while (n) k.tail[k.tlen++] = t[--n];
+    }
+    return k;
+}
+
+__device__ __forceinline__ bool key_less(const OpKey& a, const OpKey& b) {  // std::string operator<
+    const int la = a.size(), lb = b.size();
+    const int l = la < lb ? la : lb;
+    for (int i = 0; i < l; ++i) {
+        const unsigned char ca = static_cast<unsigned char>(a.at(i)), cb = static_cast<unsigned char>(b.at(i));
+        if (ca != cb) return ca < cb;
+    }
+    return la < lb;
+}
+
+__device__ __forceinline__ uint64_t al8(uint64_t v) { return (v + 7) & ~7ull; }
+
+}  // namespace wsdev

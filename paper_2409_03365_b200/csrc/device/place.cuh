@@ -1,0 +1,739 @@
+// place.cuh — k_place: subsystem (4b) placement (placement.hpp:168-447,
+// planner.hpp:99-151) and the output record.  One warp per plan; MetaOp,
+// entry, device and group state in dynamic shared memory; lanes score the
+// candidate device sets and min-locate the best; the per-wave snapshots the
+// backtracking DFS restores from and the flow list live in global memory.
+#pragma once
+#include "kcommon.cuh"
+#include "sched.cuh"
+
+namespace wsdev {
+
+constexpr int kPlaceWarps = 4;
+
+struct PlaceCaps {
+    int M, N, W, E, F, G, IS;
+};
+
+struct PlSmLayout {
+    int by_rank, idrank, lastw, home, lastent, gkey, tp, mod_of;  // [M] i32
+    int pred_r, contb, edgeb, memact, parb;                       // [M] u64
+    int e_k, e_n, e_l, e_rot, e_prev, e_wave;                     // [E] i32
+    int e_mask;                                                   // [E] u64
+    int w_eb, w_ec, w_cursor, variant;                            // [W] i32
+    int mem;                                                      // [N] f64
+    int isl;                                                      // [N] i32
+    int islmask;                                                  // [IS] u64
+    int nwin;                                                     // [IS] i32
+    int chg;                                                      // [G] u64
+    int fin_src, fin_bytes;                                       // [M+1]
+    int disp_mask, disp_bytes, disp_cnt, eorder, va;              // [M]
+    int bytes;
+};
+
+__host__ __device__ inline PlSmLayout make_pl_layout(const PlaceCaps& c) {
+    PlSmLayout L{};
+    int o = 0;
+    auto take = [&](int b) {
+        const int at = o;
+        o = (o + b + 7) & ~7;
+        return at;
+    };
+    const int M = c.M, E = c.E, W = c.W, N = c.N;
+    L.by_rank = take(4 * M);
+    L.idrank = take(4 * M);
+    L.lastw = take(4 * M);
+    L.home = take(4 * M);
+    L.lastent = take(4 * M);
+    L.gkey = take(4 * M);
+    L.tp = take(4 * M);
+    L.mod_of = take(4 * M);
+    L.pred_r = take(8 * M);
+    L.contb = take(8 * M);
+    L.edgeb = take(8 * M);
+    L.memact = take(8 * M);
+    L.parb = take(8 * M);
+    L.e_k = take(4 * E);
+    L.e_n = take(4 * E);
+    L.e_l = take(4 * E);
+    L.e_rot = take(4 * E);
+    L.e_prev = take(4 * E);
+    L.e_wave = take(4 * E);
+    L.e_mask = take(8 * E);
+    L.w_eb = take(4 * W);
+    L.w_ec = take(4 * W);
+    L.w_cursor = take(4 * W);
+    L.variant = take(4 * W);
+    L.mem = take(8 * N);
+    L.isl = take(4 * N);
+    L.islmask = take(8 * c.IS);
+    L.nwin = take(4 * (c.IS + W + 1));  // island window counts, then flows-per-wave marks
+    L.chg = take(8 * c.G);
+    L.fin_src = take(4 * (M + 1));
+    L.fin_bytes = take(8 * (M + 1));
+    L.disp_mask = take(8 * M);
+    L.disp_bytes = take(8 * M);
+    L.disp_cnt = take(4 * M);
+    L.eorder = take(4 * M);
+    L.va = take(8 * M);
+    L.bytes = (o + 15) & ~15;
+    return L;
+}
+
+struct PlaceArgs {
+    ws_batch B;
+    FitOut fit;
+    PlaceCaps caps;
+    RecLayout RL;
+    PlSmLayout PL;
+    const char* recs;         // schedule records (k_sched)
+    uint64_t* flows;          // [n_launch][F][2]: volume, packed meta
+    const int32_t* plan_ids;
+    const int32_t* n_ids;
+    int n_launch;
+    int rec_by_slot;          // retry pass: records indexed by launch slot
+    ws_plan_result* results;
+    uint8_t* arena;
+    unsigned long long* arena_top;
+    unsigned long long arena_cap;
+};
+
+struct PCtx {
+    const ws_batch* B;
+    const ws_plan_rec* R;
+    const FitOut* F;
+    const PlSmLayout* L;
+    char* sm;
+    Ctl* ctl;
+    int lane, N, K, mbase, nW, nE, nF, Fcap, G, n_isl;
+    uint64_t all;
+    uint64_t* flows;  // this plan's flow list (2 words per flow)
+    template <typename T>
+    __device__ __forceinline__ T* at(int off) const {
+        return reinterpret_cast<T*>(sm + off);
+    }
+};
+
+// flow packing: word0 = volume; word1 = from_wave | from_k<<16 | to_wave<<32 | to_k<<48 ; mode kept
+// in bits 14..15 of the to_k field (k < 2^14)
+__device__ __forceinline__ uint64_t pack_flow(int fw, int fk, int tw, int tk, int mode) {
+    return static_cast<uint64_t>(fw & 0xffff) | (static_cast<uint64_t>(fk & 0x3fff) << 16) |
+           (static_cast<uint64_t>(mode & 3) << 30) | (static_cast<uint64_t>(tw & 0xffff) << 32) |
+           (static_cast<uint64_t>(tk & 0xffff) << 48);
+}
+
+// One wave: 1 placed, 0 infeasible (caller tries the next variant), -1 error.
+__device__ int p_wave(PCtx& C, int w, int variant) {
+    const PlSmLayout& L = *C.L;
+    const ws_plan_rec& R = *C.R;
+    const int lane = C.lane, N = C.N;
+    const int* w_eb = C.at<int>(L.w_eb);
+    const int* w_ec = C.at<int>(L.w_ec);
+    const int* e_k = C.at<int>(L.e_k);
+    const int* e_n = C.at<int>(L.e_n);
+    const int* e_l = C.at<int>(L.e_l);
+    uint64_t* e_mask = C.at<uint64_t>(L.e_mask);
+    int* e_rot = C.at<int>(L.e_rot);
+    const int* e_wave = C.at<int>(L.e_wave);
+    const int* home = C.at<int>(L.home);
+    const int* lastw = C.at<int>(L.lastw);
+    const int* by_rank = C.at<int>(L.by_rank);
+    const int* idrank = C.at<int>(L.idrank);
+    const uint64_t* pred_r = C.at<uint64_t>(L.pred_r);
+    const uint64_t* contb = C.at<uint64_t>(L.contb);
+    const uint64_t* edgeb = C.at<uint64_t>(L.edgeb);
+    const uint64_t* memact = C.at<uint64_t>(L.memact);
+    const uint64_t* parb = C.at<uint64_t>(L.parb);
+    const int* gkey = C.at<int>(L.gkey);
+    const int* tpk = C.at<int>(L.tp);
+    double* mem = C.at<double>(L.mem);
+    uint64_t* chg = C.at<uint64_t>(L.chg);
+    const int* isl = C.at<int>(L.isl);
+    const uint64_t* islmask = C.at<uint64_t>(L.islmask);
+    int* nwin = C.at<int>(L.nwin);
+    int* fin_src = C.at<int>(L.fin_src);
+    uint64_t* fin_bytes = C.at<uint64_t>(L.fin_bytes);
+    uint64_t* disp_mask = C.at<uint64_t>(L.disp_mask);
+    double* disp_bytes = C.at<double>(L.disp_bytes);
+    int* disp_cnt = C.at<int>(L.disp_cnt);
+    int* eorder = C.at<int>(L.eorder);
+    uint64_t* va = C.at<uint64_t>(L.va);
+    const int* w_cursor = C.at<int>(L.w_cursor);
+    const int eb = w_eb[w], ec = w_ec[w];
+
+    // incoming volume per entry (incoming_flows :188-206), entry order (:208-221)
+    for (int i = lane; i < ec; i += 32) {
+        const int k = e_k[eb + i];
+        uint64_t v = 0;
+        if (home[k] >= 0) {
+            v = contb[k];
+        } else {
+            for (uint64_t pr = pred_r[k]; pr; pr &= pr - 1) {
+                const int p = by_rank[low_bit(pr)];
+                if (home[p] >= 0) v += edgeb[p];
+            }
+        }
+        va[i] = v;
+    }
+    __syncwarp();
+    for (int i = lane; i < ec; i += 32) {
+        int pos = i;
+        if (!R.sequential) {
+            pos = 0;
+            const int ki = e_k[eb + i];
+            for (int j = 0; j < ec; ++j) {
+                if (j == i) continue;
+                const int kj = e_k[eb + j];
+                if (va[j] > va[i] || (va[j] == va[i] && idrank[kj] < idrank[ki])) ++pos;
+            }
+        }
+        eorder[pos] = i;
+    }
+    __syncwarp();
+    uint64_t free = C.all;
+    uint64_t placed_now = 0;
+    int cursor = R.sequential ? w_cursor[w] : 0;
+    for (int oi = 0; oi < ec; ++oi) {
+        const int e = eb + eorder[oi];
+        const int k = e_k[e], n = e_n[e], lay = e_l[e];
+        // flows_in: the entity's own previous placement, else producers in dep order
+        int nfin = 0;
+        if (home[k] >= 0) {
+            if (lane == 0) fin_src[0] = home[k], fin_bytes[0] = contb[k];
+            nfin = 1;
+        } else {
+            for (uint64_t pr = pred_r[k]; pr; pr &= pr - 1) {
+                const int p = by_rank[low_bit(pr)];
+                if (home[p] < 0) continue;
+                if (lane == 0) fin_src[nfin] = home[p], fin_bytes[nfin] = edgeb[p];
+                ++nfin;
+            }
+        }
+        // homes this entry could displace (score_candidate :293-305), in id order
+        int ndisp = 0;
+        for (int base = 0; base < C.K; base += 32) {
+            const int r = base + lane;
+            bool ok = false;
+            int e2 = -1;
+            if (r < C.K) {
+                e2 = by_rank[r];
+                ok = e2 != k && lastw[e2] >= w && !(placed_now >> e2 & 1ull) && home[e2] >= 0;
+            }
+            const unsigned b = __ballot_sync(kFull, ok);
+            if (ok) {
+                const int slot = ndisp + __popc(b & ((1u << lane) - 1u));
+                const uint64_t hm = e_mask[home[e2]];
+                disp_mask[slot] = hm;
+                disp_bytes[slot] = static_cast<double>(contb[e2]);
+                disp_cnt[slot] = popc64(hm);
+            }
+            ndisp += __popc(b);
+        }
+        // memory_delta constants (:132-140)
+        const double A = lay * (static_cast<double>(memact[k]) / n);
+        const double Pm = (1.0 + R.grad_mult) * static_cast<double>(parb[k]) / tpk[k];
+        const uint64_t charged = chg[gkey[k]];
+        const double cap = static_cast<double>(R.mem_capacity);
+        __syncwarp();
+
+        auto score_of = [&](uint64_t devs, int rot) {
+            Score s;
+            s.valid = 1;
+            s.devs = devs;
+            s.rot = rot;
+            s.islands = 0;
+            for (int i = 0; i < C.n_isl; ++i) s.islands += (devs & islmask[i]) != 0;
+            s.displaced = 0.0;
+            for (int j = 0; j < ndisp; ++j) {
+                const int ov = popc64(devs & disp_mask[j]);
+                if (ov == 0) continue;
+                s.displaced += disp_bytes[j] * static_cast<double>(ov) / static_cast<double>(disp_cnt[j]);
+            }
+            s.feasible = 1;
+            double peak = 0.0;
+            for (uint64_t d = devs; d; d &= d - 1) {
+                const int dv = low_bit(d);
+                double delta = A;
+                if (!(charged >> dv & 1ull)) delta += Pm;
+                const double used = mem[dv] + delta;
+                peak = (peak < used) ? used : peak;
+                if (used > cap) s.feasible = 0;
+            }
+            s.peak = peak;
+            s.inter = 0.0;
+            s.intra = 0.0;
+            for (int f = 0; f < nfin; ++f) {
+                uint64_t a, b;
+                shard_moves(e_mask[fin_src[f]], devs, fin_bytes[f], isl, a, b);
+                s.inter += static_cast<double>(b);
+                s.intra += static_cast<double>(a);
+            }
+            return s;
+        };
+
+        Score chosen;
+        chosen.valid = 0;
+        if (R.sequential) {
+            if (popc64(free) >= n) {  // rolling cursor block (:350-358)
+                uint64_t m = 0;
+                for (int i = 0; i < n; ++i) m |= 1ull << ((cursor + i) % N);
+                chosen = score_of(m, cursor);
+                cursor = (cursor + n) % N;
+            }
+        } else {
+            // candidate_sets (:223-263): predecessor reuse, island windows, global windows
+            const int nfree = popc64(free);
+            if (nfree >= n) {
+                int total = nfin;
+                for (int i = 0; i < C.n_isl; ++i) {
+                    const int c = popc64(free & islmask[i]);
+                    const int nw = c >= n ? c - n + 1 : 0;
+                    if (lane == 0) nwin[i] = nw;
+                    total += nw;
+                }
+                total += nfree - n + 1;
+                __syncwarp();
+                const int rounds = oi == 0 ? variant + 1 : 1;  // first entry takes scores[variant]
+                Score prev;
+                prev.valid = 0;
+                for (int rd = 0; rd < rounds; ++rd) {
+                    Score best;
+                    best.valid = 0;
+                    for (int j = lane; j < total; j += 32) {
+                        uint64_t m;
+                        if (j < nfin) {
+                            m = e_mask[fin_src[j]];
+                            if (popc64(m) != n || (m & ~free)) continue;
+                        } else {
+                            int r = j - nfin;
+                            int i = 0;
+                            for (; i < C.n_isl && r >= nwin[i]; ++i) r -= nwin[i];
+                            m = i < C.n_isl ? window_mask(free & islmask[i], r, n) : window_mask(free, r, n);
+                        }
+                        const Score s = score_of(m, 0);
+                        if (prev.valid && !score_less(prev, s)) continue;  // next distinct rank
+                        if (!best.valid || score_less(s, best)) best = s;
+                    }
+                    best = warp_min_score(best);
+                    if (!best.valid) break;  // fewer distinct candidates than variant+1
+                    prev = best;
+                    chosen = best;
+                }
+            }
+        }
+        if (!chosen.valid || !chosen.feasible) return 0;
+        // commit_memory (:142-149), lane per device
+        for (int dv = lane; dv < N; dv += 32) {
+            if (!(chosen.devs >> dv & 1ull)) continue;
+            double delta = A;
+            if (!(charged >> dv & 1ull)) delta += Pm;
+            mem[dv] += delta;
+        }
+        if (lane == 0) {
+            chg[gkey[k]] = charged | chosen.devs;
+            e_mask[e] = chosen.devs;
+            e_rot[e] = chosen.rot;
+        }
+        // flow records (:376-400), lane 0 appends in order
+        for (int f = 0; f < nfin; ++f) {
+            uint64_t a, b;
+            const int src = fin_src[f];
+            shard_moves(e_mask[src], chosen.devs, fin_bytes[f], isl, a, b);
+            const int need = (a + b == 0) ? 1 : (a > 0) + (b > 0);
+            if (C.nF + need > C.Fcap) {
+                if (lane == 0) set_err(C.ctl, WS_E_LIMIT_FLOWS);
+                __syncwarp();
+                return -1;
+            }
+            if (lane == 0) {
+                const int fw = e_wave[src], fk = e_k[src];
+                if (a + b == 0) {
+                    C.flows[2 * C.nF] = 0;
+                    C.flows[2 * C.nF + 1] = pack_flow(fw, fk, w, k, WS_FLOW_COPY);
+                } else {
+                    int q = C.nF;
+                    if (a > 0) C.flows[2 * q] = a, C.flows[2 * q + 1] = pack_flow(fw, fk, w, k, WS_FLOW_INTRA), ++q;
+                    if (b > 0) C.flows[2 * q] = b, C.flows[2 * q + 1] = pack_flow(fw, fk, w, k, WS_FLOW_INTER);
+                }
+            }
+            C.nF += need;
+        }
+        free &= ~chosen.devs;
+        placed_now |= 1ull << k;
+        __syncwarp();
+    }
+    return 1;
+}
+
+__device__ void p_emit(PCtx& C, int p, const char* rec, const RecLayout& RL, const SchedHdr& h, const PlaceArgs& A) {
+    const int lane = C.lane, K = C.K;
+    const ws_batch& B = *C.B;
+    const int* r_mod_of = reinterpret_cast<const int*>(rec + RL.mod_of);
+    const int* r_level = reinterpret_cast<const int*>(rec + RL.level);
+    const int* r_up_n = reinterpret_cast<const int*>(rec + RL.up_n);
+    const int* r_up_l = reinterpret_cast<const int*>(rec + RL.up_l);
+    const int* r_lo_n = reinterpret_cast<const int*>(rec + RL.lo_n);
+    const int* r_lo_l = reinterpret_cast<const int*>(rec + RL.lo_l);
+    const uint64_t* r_succ = reinterpret_cast<const uint64_t*>(rec + RL.succ_r);
+    const int* by_rank = C.at<int>(C.L->by_rank);
+    int npieces = 0, nedges = 0;
+    for (int k = lane; k < K; k += 32) {
+        npieces += C.F->npieces[C.mbase + r_mod_of[k]];
+        nedges += popc64(r_succ[k]);
+    }
+    npieces = warp_sum(npieces);
+    nedges = warp_sum(nedges);
+    const int nL = h.n_levels, nW = h.nW, nE = h.nE, nF = C.nF;
+    const uint64_t sz = al8(sizeof(ws_out_metaop) * K) + al8(sizeof(ws_out_level) * nL) +
+                        al8(sizeof(ws_out_piece) * npieces) + al8(sizeof(ws_out_edge) * nedges) +
+                        al8(sizeof(ws_out_wave) * nW) + al8(sizeof(ws_out_entry) * nE) + al8(sizeof(ws_out_flow) * nF);
+    unsigned long long off = 0;
+    if (lane == 0) off = atomicAdd(A.arena_top, static_cast<unsigned long long>(sz));
+    off = __shfl_sync(kFull, off, 0);
+    ws_plan_result* res = A.results + p;
+    if (off + sz > A.arena_cap) {
+        if (lane == 0) {
+            ws_plan_result r{};
+            r.status = WS_STATUS_INTERNAL;
+            r.err_code = WS_E_ARENA_OVERFLOW;
+            *res = r;
+        }
+        return;
+    }
+    uint8_t* base = A.arena + off;
+    uint64_t o = 0;
+    auto* mo = reinterpret_cast<ws_out_metaop*>(base + o);
+    o += al8(sizeof(ws_out_metaop) * K);
+    auto* lv = reinterpret_cast<ws_out_level*>(base + o);
+    o += al8(sizeof(ws_out_level) * nL);
+    auto* pc = reinterpret_cast<ws_out_piece*>(base + o);
+    o += al8(sizeof(ws_out_piece) * npieces);
+    auto* ed = reinterpret_cast<ws_out_edge*>(base + o);
+    o += al8(sizeof(ws_out_edge) * nedges);
+    auto* wv = reinterpret_cast<ws_out_wave*>(base + o);
+    o += al8(sizeof(ws_out_wave) * nW);
+    auto* en = reinterpret_cast<ws_out_entry*>(base + o);
+    o += al8(sizeof(ws_out_entry) * nE);
+    auto* fl = reinterpret_cast<ws_out_flow*>(base + o);
+    {
+        int pb = 0;
+        for (int k = 0; k < K; ++k) {
+            const int gm = C.mbase + r_mod_of[k];
+            const int np = C.F->npieces[gm];
+            if ((k & 31) == lane) {
+                ws_out_metaop x;
+                x.module = r_mod_of[k];
+                x.level = r_level[k];
+                x.first_layer = 0;
+                x.length = B.mod_layers[gm];
+                x.piece_begin = pb;
+                x.piece_count = np;
+                x.upper_n = r_up_n[k];
+                x.upper_l = r_up_l[k];
+                x.lower_n = r_lo_n[k];
+                x.lower_l = r_lo_l[k];
+                mo[k] = x;
+            }
+            const double* src = C.F->pieces + 5 * C.F->piece_off[gm];
+            for (int i = lane; i < np; i += 32)
+                pc[pb + i] = ws_out_piece{src[5 * i], src[5 * i + 1], src[5 * i + 2], src[5 * i + 3], src[5 * i + 4]};
+            pb += np;
+        }
+    }
+    const double* cstar = reinterpret_cast<const double*>(rec + RL.cstar);
+    const int* lfw = reinterpret_cast<const int*>(rec + RL.lvl_fw);
+    const int* lnw = reinterpret_cast<const int*>(rec + RL.lvl_nw);
+    for (int l = lane; l < nL; l += 32) lv[l] = ws_out_level{cstar[l], lfw[l], lnw[l]};
+    if (lane == 0) {  // MetaGraph edges in std::set<pair<string,string>> order
+        int ne = 0;
+        for (int ra = 0; ra < K; ++ra) {
+            const int a = by_rank[ra];
+            for (uint64_t s = r_succ[a]; s; s &= s - 1) ed[ne++] = ws_out_edge{a, by_rank[low_bit(s)]};
+        }
+    }
+    const double* w_start = reinterpret_cast<const double*>(rec + RL.w_start);
+    const double* w_dur = reinterpret_cast<const double*>(rec + RL.w_dur);
+    const int* w_level = reinterpret_cast<const int*>(rec + RL.w_level);
+    const int* w_eb = C.at<int>(C.L->w_eb);
+    const int* w_ec = C.at<int>(C.L->w_ec);
+    for (int w = lane; w < nW; w += 32) {
+        ws_out_wave x;
+        x.start = w_start[w];
+        x.duration = w_dur[w];
+        x.level = w_level[w];
+        x.entry_begin = w_eb[w];
+        x.n_entries = w_ec[w];
+        x.pad = 0;
+        wv[w] = x;
+    }
+    const int* e_k = C.at<int>(C.L->e_k);
+    const int* e_n = C.at<int>(C.L->e_n);
+    const int* e_l = C.at<int>(C.L->e_l);
+    const double* e_span = reinterpret_cast<const double*>(rec + RL.e_span);
+    const uint64_t* e_mask = C.at<uint64_t>(C.L->e_mask);
+    const int* e_rot = C.at<int>(C.L->e_rot);
+    for (int e = lane; e < nE; e += 32) {
+        ws_out_entry x;
+        x.span = e_span[e];
+        x.devmask = e_mask[e];
+        x.metaop = e_k[e];
+        x.n = e_n[e];
+        x.layers = e_l[e];
+        x.rot = e_rot[e];
+        en[e] = x;
+    }
+    for (int f = lane; f < nF; f += 32) {
+        const uint64_t meta = C.flows[2 * f + 1];
+        ws_out_flow x;
+        x.volume = C.flows[2 * f];
+        x.from_wave = static_cast<int>(meta & 0xffff);
+        x.from_metaop = static_cast<int>((meta >> 16) & 0x3fff);
+        x.mode = static_cast<int>((meta >> 30) & 3);
+        x.to_wave = static_cast<int>((meta >> 32) & 0xffff);
+        x.to_metaop = static_cast<int>((meta >> 48) & 0xffff);
+        x.pad = 0;
+        fl[f] = x;
+    }
+    if (lane == 0) {
+        ws_plan_result r{};
+        r.status = WS_STATUS_OK;
+        r.n_metaops = K;
+        r.n_edges = nedges;
+        r.n_levels = nL;
+        r.n_waves = nW;
+        r.n_entries = nE;
+        r.n_flows = nF;
+        r.n_pieces = npieces;
+        r.lower_bound = h.lower_bound;
+        r.end_time = h.end_time;
+        r.offset = off;
+        r.size = sz;
+        *res = r;
+    }
+}
+
+__global__ void __launch_bounds__(32 * kPlaceWarps) k_place(PlaceArgs A) {
+    extern __shared__ __align__(16) char smem_dyn[];
+    __shared__ Ctl ctl_s[kPlaceWarps];
+    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int slot = blockIdx.x * kPlaceWarps + wid;
+    if (slot >= A.n_launch) return;
+    if (A.n_ids && slot >= *A.n_ids) return;
+    const int p = A.plan_ids[slot];
+    const char* rec = A.recs + static_cast<int64_t>(A.rec_by_slot ? slot : p) * A.RL.bytes;
+    const SchedHdr h = *reinterpret_cast<const SchedHdr*>(rec + A.RL.hdr);
+    if (!h.ok) return;  // k_sched already wrote the error result
+    Ctl* ctl = &ctl_s[wid];
+    if (lane == 0) *ctl = Ctl{};
+    const ws_plan_rec& R = A.B.plans[p];
+    PCtx C;
+    C.B = &A.B;
+    C.R = &R;
+    C.F = &A.fit;
+    C.L = &A.PL;
+    C.sm = smem_dyn + wid * A.PL.bytes;
+    C.ctl = ctl;
+    C.lane = lane;
+    C.N = R.n_dev;
+    C.K = h.K;
+    C.mbase = R.mod_begin;
+    C.nW = h.nW;
+    C.nE = h.nE;
+    C.nF = 0;
+    C.Fcap = A.caps.F;
+    C.G = R.n_groups + h.K;
+    C.n_isl = R.n_islands;
+    C.all = C.N == 64 ? ~0ull : ((1ull << C.N) - 1ull);
+    C.flows = A.flows + static_cast<int64_t>(slot) * A.caps.F * 2;
+    const ws_batch& B = A.B;
+    const PlSmLayout& L = A.PL;
+    const int K = C.K, N = C.N, nW = C.nW, nE = C.nE, G = C.G;
+    if (C.G > A.caps.G || C.n_isl > A.caps.IS || nE > A.caps.E || nW > A.caps.W || K > A.caps.M) {
+        if (lane == 0) {
+            set_err(ctl, WS_E_LIMIT_MODULES);
+            write_error(A.results + p, ctl);
+        }
+        return;
+    }
+    // load the schedule and build the entity tables (planner.hpp:99-151)
+    const int* r_mod_of = reinterpret_cast<const int*>(rec + A.RL.mod_of);
+    const int* r_by_rank = reinterpret_cast<const int*>(rec + A.RL.by_rank);
+    const int* r_idrank = reinterpret_cast<const int*>(rec + A.RL.idrank);
+    const uint64_t* r_pred = reinterpret_cast<const uint64_t*>(rec + A.RL.pred_r);
+    int* by_rank = C.at<int>(L.by_rank);
+    int* idrank = C.at<int>(L.idrank);
+    int* lastw = C.at<int>(L.lastw);
+    int* home = C.at<int>(L.home);
+    int* lastent = C.at<int>(L.lastent);
+    int* gkey = C.at<int>(L.gkey);
+    int* tpk = C.at<int>(L.tp);
+    uint64_t* pred_r = C.at<uint64_t>(L.pred_r);
+    uint64_t* contb = C.at<uint64_t>(L.contb);
+    uint64_t* edgeb = C.at<uint64_t>(L.edgeb);
+    uint64_t* memact = C.at<uint64_t>(L.memact);
+    uint64_t* parb = C.at<uint64_t>(L.parb);
+    for (int k = lane; k < K; k += 32) {
+        by_rank[k] = r_by_rank[k];
+        idrank[k] = r_idrank[k];
+        pred_r[k] = r_pred[k];
+        const int gm = C.mbase + r_mod_of[k];
+        const int Lk = B.mod_layers[gm];  // one MetaOp per module: length == layers
+        parb[k] = static_cast<uint64_t>(static_cast<double>(B.mod_param[gm]) * Lk / B.mod_layers[gm]);
+        const uint64_t act = B.mod_act[gm];
+        memact[k] = static_cast<uint64_t>(static_cast<double>(act) * 1.0);
+        contb[k] = static_cast<uint64_t>(static_cast<double>(act) * 1.0);
+        const uint64_t edge = B.mod_out[gm] == 0 ? act : B.mod_out[gm];
+        edgeb[k] = static_cast<uint64_t>(static_cast<double>(edge) * 1.0);
+        const int grp = (Lk == B.mod_layers[gm]) ? B.mod_group[gm] : -1;
+        const int al = B.mod_alias[gm];
+        gkey[k] = grp < 0 ? R.n_groups + k : ((al >= 0 && al < K) ? R.n_groups + al : grp);
+        tpk[k] = B.mod_tp[gm];
+        home[k] = -1;
+        lastw[k] = -1;
+        lastent[k] = -1;
+    }
+    const int* r_w_eb = reinterpret_cast<const int*>(rec + A.RL.w_eb);
+    const int* r_w_ec = reinterpret_cast<const int*>(rec + A.RL.w_ec);
+    const int* r_e_k = reinterpret_cast<const int*>(rec + A.RL.e_k);
+    const int* r_e_n = reinterpret_cast<const int*>(rec + A.RL.e_n);
+    const int* r_e_l = reinterpret_cast<const int*>(rec + A.RL.e_l);
+    int* w_eb = C.at<int>(L.w_eb);
+    int* w_ec = C.at<int>(L.w_ec);
+    int* w_cursor = C.at<int>(L.w_cursor);
+    int* variant = C.at<int>(L.variant);
+    int* e_k = C.at<int>(L.e_k);
+    int* e_n = C.at<int>(L.e_n);
+    int* e_l = C.at<int>(L.e_l);
+    int* e_prev = C.at<int>(L.e_prev);
+    int* e_wave = C.at<int>(L.e_wave);
+    uint64_t* e_mask = C.at<uint64_t>(L.e_mask);
+    int* e_rot = C.at<int>(L.e_rot);
+    for (int w = lane; w < nW; w += 32) {
+        w_eb[w] = r_w_eb[w];
+        w_ec[w] = r_w_ec[w];
+        variant[w] = 0;
+    }
+    for (int e = lane; e < nE; e += 32) {
+        e_k[e] = r_e_k[e];
+        e_n[e] = r_e_n[e];
+        e_l[e] = r_e_l[e];
+        e_mask[e] = 0;
+        e_rot[e] = 0;
+    }
+    double* mem = C.at<double>(L.mem);
+    uint64_t* chg = C.at<uint64_t>(L.chg);
+    int* isl = C.at<int>(L.isl);
+    uint64_t* islmask = C.at<uint64_t>(L.islmask);
+    for (int d = lane; d < N; d += 32) {
+        isl[d] = B.dev_island[R.dev_begin + d];
+        mem[d] = 0.0;
+    }
+    for (int g = lane; g < G; g += 32) chg[g] = 0;
+    for (int i = lane; i < C.n_isl; i += 32) islmask[i] = 0;
+    __syncwarp();
+    if (lane == 0) {
+        for (int d = 0; d < N; ++d) islmask[isl[d]] |= 1ull << d;
+        int cur = 0;
+        for (int w = 0; w < nW; ++w) {
+            w_cursor[w] = cur;  // sequential-ablation cursor (:331-338)
+            for (int i = 0; i < w_ec[w]; ++i) {
+                const int e = w_eb[w] + i;
+                e_wave[e] = w;
+                e_prev[e] = lastent[e_k[e]];
+                lastent[e_k[e]] = e;
+                lastw[e_k[e]] = w;
+                cur = (cur + e_n[e]) % N;
+            }
+        }
+    }
+    __syncwarp();
+    // depth-first search over per-wave variants with a bounded attempt budget (:409-441).
+    // The reference copies the whole state per placed wave; here the state
+    // before wave k is rebuilt on demand by replaying the committed entries of
+    // waves 0..k-1 (their device masks are still in e_mask): entries of one wave
+    // use disjoint devices, so per device the additions happen in the same order
+    // and the doubles are identical.  Only the flow count is recorded per wave.
+    int* wave_nf = C.at<int>(L.nwin) + C.n_isl;  // [W+1] after the window counts
+    long long attempts = 0, budget = nW;
+    for (int d = 0; d < R.bt_depth; ++d) budget *= (R.bt_branching > 1 ? R.bt_branching : 1);
+    const int branching = R.sequential ? 1 : R.bt_branching;
+    int k = 0;
+    bool dirty = false;
+    if (lane == 0) wave_nf[0] = 0;
+    while (k < nW) {
+        if (++attempts > budget) {
+            if (lane == 0) {
+                set_err(ctl, WS_E_BT_BUDGET, k);
+                write_error(A.results + p, ctl);
+            }
+            return;
+        }
+        if (dirty) {  // rebuild the state before wave k
+            for (int d = lane; d < N; d += 32) mem[d] = 0.0;
+            for (int g = lane; g < G; g += 32) chg[g] = 0;
+            __syncwarp();
+            for (int w = 0; w < k; ++w) {
+                for (int i = 0; i < w_ec[w]; ++i) {
+                    const int e = w_eb[w] + i;
+                    const int ke = e_k[e];
+                    const double Ae = e_l[e] * (static_cast<double>(memact[ke]) / e_n[e]);
+                    const double Pe = (1.0 + R.grad_mult) * static_cast<double>(parb[ke]) / tpk[ke];
+                    const uint64_t charged = chg[gkey[ke]];
+                    for (int dv = lane; dv < N; dv += 32) {
+                        if (!(e_mask[e] >> dv & 1ull)) continue;
+                        double delta = Ae;
+                        if (!(charged >> dv & 1ull)) delta += Pe;
+                        mem[dv] += delta;
+                    }
+                    __syncwarp();
+                    if (lane == 0) chg[gkey[ke]] = charged | e_mask[e];
+                    __syncwarp();
+                }
+            }
+            C.nF = wave_nf[k];
+            dirty = false;
+            __syncwarp();
+        }
+        if (variant[k] >= branching) {
+            __syncwarp();
+            if (lane == 0) variant[k] = 0;
+            if (k == 0) {
+                if (lane == 0) {
+                    set_err(ctl, WS_E_NO_PLACEMENT_W0);
+                    write_error(A.results + p, ctl);
+                }
+                return;
+            }
+            --k;
+            for (int i = lane; i < w_ec[k]; i += 32) {  // home[] back to "before wave k"
+                const int e = w_eb[k] + i;
+                home[e_k[e]] = e_prev[e];
+            }
+            if (lane == 0) variant[k]++;
+            dirty = true;
+            __syncwarp();
+            continue;
+        }
+        const int r = p_wave(C, k, variant[k]);
+        __syncwarp();
+        if (r < 0) {
+            if (lane == 0) write_error(A.results + p, ctl);
+            return;
+        }
+        if (r > 0) {
+            if (lane == 0) wave_nf[k + 1] = C.nF;  // flows recorded before wave k+1
+            for (int i = lane; i < w_ec[k]; i += 32) {
+                const int e = w_eb[k] + i;
+                home[e_k[e]] = e;
+            }
+            ++k;
+        } else {
+            if (lane == 0) variant[k]++;
+            dirty = true;
+        }
+        __syncwarp();
+    }
+    p_emit(C, p, rec, A.RL, h, A);
+}
+
+}  // namespace wsdev

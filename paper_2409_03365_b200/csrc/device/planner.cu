@@ -1,30 +1,36 @@
 // planner.cu — C-ABI implementation: planning context, device buffers and the
 // launch sequence of the sm_100a planner kernels.
 //
-//   k_fit   (K2)           one thread per declared module
-//   k_plan  (K1,K3,K4,K5)  one warp per plan; soft-cap overflows re-run in a
-//                          device-driven retry launch with the hard caps
-//   k_best                 global-best candidate (min-loc) over the batch
+//   k_fit    (subsystem 2)        one thread per declared module
+//   k_sched  (subsystems 1, 3, 4a) one warp per plan, working set in shared memory
+//   k_place  (subsystem 4b + out)  one warp per plan, working set in shared memory
+//   retry    plans that overflow the soft record caps re-run with the hard
+//            caps; the list is built and counted on the device (no host sync)
+//   k_best   global-best candidate (min-loc) over the batch
 //
+// Plans are launched in descending estimated cost (longest-processing-time
+// order) so the long plans start first and the tail of each launch is short.
 // Replaces wavesched::plan_workload (planner.hpp:156-212) for whole batches.
 #include <cuda_runtime.h>
 
 #include <algorithm>
 #include <cstdio>
 #include <cstring>
+#include <numeric>
 #include <string>
 #include <vector>
 
 #include "fit.cuh"
-#include "plan.cuh"
+#include "place.cuh"
+#include "sched.cuh"
 
 using namespace wsdev;
 
 namespace {
 
-constexpr int kRetryMax = 2048;               // plans re-run with hard caps per call
+constexpr int kRetryMax = 1024;               // plans re-run with hard caps per call
 constexpr int64_t kOverflowPieces = 1 << 18;  // isotonic/long curves
-constexpr size_t kScratchBudget = size_t(6) << 30;
+constexpr int kSmemLimit = 227 * 1024;
 
 struct DevBuf {
     void* p = nullptr;
@@ -47,8 +53,7 @@ struct DevBuf {
     }
 };
 
-// k_soft_collect: plans whose soft scratch caps overflowed (waves/entries/flows
-// or arena) get queued for the retry launch.
+// plans whose soft record caps overflowed get queued for the retry launch
 __global__ void k_soft_collect(const ws_plan_result* res, int n, int32_t* ids, int32_t* count) {
     const int p = blockIdx.x * blockDim.x + threadIdx.x;
     if (p >= n) return;
@@ -96,6 +101,45 @@ __global__ void k_best(const ws_plan_result* res, int n, int mode, double* out_k
     }
 }
 
+struct LaunchCaps {
+    RecCaps rec;
+    PlaceCaps pl;
+    int M;
+};
+
+LaunchCaps batch_caps(const std::vector<ws_plan_rec>& plans, bool hard) {
+    int M = 1, N = 1, IS = 1, gmax = 0;
+    for (const ws_plan_rec& r : plans) {
+        M = std::max(M, r.n_mod);
+        N = std::max(N, r.n_dev);
+        IS = std::max(IS, r.n_islands);
+        gmax = std::max(gmax, r.n_groups);
+    }
+    M = std::min(M, WS_MAX_MODULES);
+    N = std::min(N, WS_MAX_DEVICES);
+    IS = std::min(IS, N);
+    const int W = std::min(WS_MAX_WAVES, 2 * M + 1);  // each wave drains a tuple
+    int E, F;
+    if (hard) {
+        E = std::min(WS_MAX_ENTRIES, std::max(64, 2 * M * M));
+        F = WS_MAX_FLOWS;
+    } else {
+        E = std::max(32, 4 * M);
+        F = std::max(64, 8 * M);
+    }
+    LaunchCaps c;
+    c.M = M;
+    c.rec = RecCaps{M, W, E};
+    c.pl = PlaceCaps{M, N, W, E, F, gmax + M, IS};
+    return c;
+}
+
+int warps_for(int bytes_per_warp, int want) {
+    int w = want;
+    while (w > 1 && w * bytes_per_warp > kSmemLimit) --w;
+    return w;
+}
+
 }  // namespace
 
 struct ws_ctx {
@@ -103,14 +147,14 @@ struct ws_ctx {
     cudaStream_t stream = nullptr;
     std::string err;
     // staged batch
-    DevBuf blob;
+    DevBuf blob, order;
     ws_batch dview{};
     std::vector<ws_plan_rec> host_plans;
-    Caps caps{}, caps_hard{};
+    LaunchCaps caps{}, caps_hard{};
     // K2 outputs
     DevBuf fit_err, fit_a, fit_b, fit_np, fit_nmax, fit_off, fit_pieces, ttab;
-    // K1/K3/K4/K5
-    DevBuf scratch, results, arena, counters, retry_ids, best;
+    // records, flows, results
+    DevBuf recs, flows, recs_r, flows_r, results, arena, counters, retry_ids, best;
     uint64_t arena_cap = 0;
     int launches = 0;
     cudaEvent_t ev[4] = {};
@@ -125,34 +169,11 @@ int fail(ws_ctx* c, const std::string& what, cudaError_t e = cudaSuccess) {
     return 1;
 }
 
-#define CK(call)                                               \
-    do {                                                       \
-        cudaError_t e_ = (call);                               \
-        if (e_ != cudaSuccess) return fail(ctx, #call, e_);    \
+#define CK(call)                                            \
+    do {                                                    \
+        cudaError_t e_ = (call);                            \
+        if (e_ != cudaSuccess) return fail(ctx, #call, e_); \
     } while (0)
-
-Caps batch_caps(const std::vector<ws_plan_rec>& plans, bool hard) {
-    Caps c{1, 1, 1, 1, 1, 1, 1};
-    int gmax = 0;
-    for (const ws_plan_rec& r : plans) {
-        c.M = std::max(c.M, r.n_mod);
-        c.N = std::max(c.N, r.n_dev);
-        c.IS = std::max(c.IS, r.n_islands);
-        gmax = std::max(gmax, r.n_groups);
-    }
-    c.M = std::min(c.M, WS_MAX_MODULES);
-    c.N = std::min(c.N, WS_MAX_DEVICES);
-    c.G = gmax + c.M;
-    c.W = std::min(WS_MAX_WAVES, 2 * c.M + 1);  // each wave drains a tuple
-    if (hard) {
-        c.E = std::min(WS_MAX_ENTRIES, std::max(64, 2 * c.M * c.M));
-        c.F = WS_MAX_FLOWS;
-    } else {
-        c.E = std::max(32, 4 * c.M);
-        c.F = std::max(64, 8 * c.M);
-    }
-    return c;
-}
 
 // rebase every section pointer of a host batch into device memory at `dbase`
 ws_batch rebase(const ws_batch& h, const void* hbase, char* dbase) {
@@ -197,6 +218,53 @@ ws_batch rebase(const ws_batch& h, const void* hbase, char* dbase) {
     return d;
 }
 
+// launch k_sched + k_place over `n` slots (plan ids from `ids`, count optionally on device)
+int launch_pair(ws_ctx* ctx, cudaStream_t st, const LaunchCaps& lc, const FitOut& fo, const int32_t* ids,
+                const int32_t* n_ids, int n, bool by_slot, char* recs, uint64_t* flows) {
+    if (n <= 0) return 0;
+    const ws_batch& B = ctx->dview;
+    SchedArgs S{};
+    S.B = B;
+    S.fit = fo;
+    S.caps = lc.rec;
+    S.RL = make_rec_layout(lc.rec);
+    S.SL = make_sm_layout(lc.M);
+    S.recs = recs;
+    S.plan_ids = ids;
+    S.n_ids = n_ids;
+    S.n_launch = n;
+    S.rec_by_slot = by_slot ? 1 : 0;
+    S.M_cap = lc.M;
+    S.results = ctx->results.as<ws_plan_result>();
+    const int sw = warps_for(S.SL.bytes, kSchedWarps);
+    if (sw * S.SL.bytes > kSmemLimit) return fail(ctx, "k_sched working set exceeds shared memory");
+    CK(cudaFuncSetAttribute(k_sched, cudaFuncAttributeMaxDynamicSharedMemorySize, kSchedWarps * S.SL.bytes));
+    k_sched<<<(n + kSchedWarps - 1) / kSchedWarps, 32 * kSchedWarps, kSchedWarps * S.SL.bytes, st>>>(S);
+    ctx->launches++;
+
+    PlaceArgs P{};
+    P.B = B;
+    P.fit = fo;
+    P.caps = lc.pl;
+    P.RL = S.RL;
+    P.PL = make_pl_layout(lc.pl);
+    P.recs = recs;
+    P.flows = flows;
+    P.plan_ids = ids;
+    P.n_ids = n_ids;
+    P.n_launch = n;
+    P.rec_by_slot = by_slot ? 1 : 0;
+    P.results = ctx->results.as<ws_plan_result>();
+    P.arena = ctx->arena.as<uint8_t>();
+    P.arena_top = ctx->counters.as<unsigned long long>();
+    P.arena_cap = ctx->arena_cap;
+    if (kPlaceWarps * P.PL.bytes > kSmemLimit) return fail(ctx, "k_place working set exceeds shared memory");
+    CK(cudaFuncSetAttribute(k_place, cudaFuncAttributeMaxDynamicSharedMemorySize, kPlaceWarps * P.PL.bytes));
+    k_place<<<(n + kPlaceWarps - 1) / kPlaceWarps, 32 * kPlaceWarps, kPlaceWarps * P.PL.bytes, st>>>(P);
+    ctx->launches++;
+    return 0;
+}
+
 }  // namespace
 
 extern "C" {
@@ -238,13 +306,26 @@ int ws_stage_batch(ws_ctx* ctx, const ws_batch* in, void* stream) {
     cudaSetDevice(ctx->device);
     cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
     if (!in->blob) return fail(ctx, "ws_stage_batch: batch must be contiguous (ws_batch.blob)");
-    if (!ctx->blob.ensure(in->blob_bytes + 256)) return fail(ctx, "cudaMalloc batch");
+    const int P = in->n_plans;
+    if (!ctx->blob.ensure(in->blob_bytes + 256) || !ctx->order.ensure(4ull * std::max(P, 1)))
+        return fail(ctx, "cudaMalloc batch");
     CK(cudaMemcpyAsync(ctx->blob.p, in->blob, in->blob_bytes, cudaMemcpyHostToDevice, st));
     ctx->dview = rebase(*in, in->blob, ctx->blob.as<char>());
-    ctx->host_plans.assign(in->plans, in->plans + in->n_plans);
+    ctx->host_plans.assign(in->plans, in->plans + P);
     ctx->caps = batch_caps(ctx->host_plans, false);
     ctx->caps_hard = batch_caps(ctx->host_plans, true);
     ctx->arena_cap = ws_arena_bound(in);
+    // longest-processing-time launch order: descending modules x devices
+    static thread_local std::vector<int32_t> order;
+    order.resize(P);
+    std::iota(order.begin(), order.end(), 0);
+    std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t b) {
+        const ws_plan_rec& x = ctx->host_plans[a];
+        const ws_plan_rec& y = ctx->host_plans[b];
+        return x.n_mod * (x.n_dev + 8) > y.n_mod * (y.n_dev + 8);
+    });
+    if (P) CK(cudaMemcpyAsync(ctx->order.p, order.data(), 4ull * P, cudaMemcpyHostToDevice, st));
+    CK(cudaStreamSynchronize(st));  // `order` is reused by the next stage call
     return 0;
 }
 
@@ -253,18 +334,23 @@ int ws_plan_staged(ws_ctx* ctx, void* stream) {
     cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
     const ws_batch& B = ctx->dview;
     const int P = B.n_plans, NM = std::max(B.n_modules, 1);
-    const Caps& caps = ctx->caps;
+    const LaunchCaps& lc = ctx->caps;
+    const LaunchCaps& lh = ctx->caps_hard;
     ctx->launches = 0;
-    // K2 buffers
-    const int tstride = caps.N;
+    const int tstride = lc.pl.N;
     if (!ctx->fit_err.ensure(4ull * NM) || !ctx->fit_a.ensure(4ull * NM) || !ctx->fit_b.ensure(4ull * NM) ||
         !ctx->fit_np.ensure(4ull * NM) || !ctx->fit_nmax.ensure(4ull * NM) || !ctx->fit_off.ensure(8ull * NM) ||
         !ctx->fit_pieces.ensure(40ull * (static_cast<uint64_t>(NM) * kInlinePieces + kOverflowPieces)) ||
         !ctx->ttab.ensure(8ull * NM * tstride))
         return fail(ctx, "cudaMalloc fit buffers");
+    const RecLayout RL = make_rec_layout(lc.rec), RLh = make_rec_layout(lh.rec);
     if (!ctx->counters.ensure(64) || !ctx->results.ensure(sizeof(ws_plan_result) * std::max(P, 1)) ||
-        !ctx->arena.ensure(ctx->arena_cap) || !ctx->retry_ids.ensure(4 * kRetryMax) || !ctx->best.ensure(64))
-        return fail(ctx, "cudaMalloc result buffers");
+        !ctx->arena.ensure(ctx->arena_cap) || !ctx->retry_ids.ensure(4 * kRetryMax) || !ctx->best.ensure(64) ||
+        !ctx->recs.ensure(static_cast<size_t>(RL.bytes) * std::max(P, 1)) ||
+        !ctx->flows.ensure(16ull * lc.pl.F * std::max(P, 1)) ||
+        !ctx->recs_r.ensure(static_cast<size_t>(RLh.bytes) * kRetryMax) ||
+        !ctx->flows_r.ensure(16ull * lh.pl.F * kRetryMax))
+        return fail(ctx, "cudaMalloc planner buffers");
     auto* counters = ctx->counters.as<unsigned long long>();  // [0] arena top [1] overflow top [2] retry count
     CK(cudaMemsetAsync(counters, 0, 64, st));
     FitOut fo;
@@ -287,50 +373,19 @@ int ws_plan_staged(ws_ctx* ctx, void* stream) {
         ctx->launches++;
     }
     CK(cudaEventRecord(ctx->ev[1], st));
-
-    PlanArgs A{};
-    A.B = B;
-    A.fit = fo;
-    A.results = ctx->results.as<ws_plan_result>();
-    A.arena = ctx->arena.as<uint8_t>();
-    A.arena_top = counters;
-    A.arena_cap = ctx->arena_cap;
-    // main pass (soft caps), chunked by scratch budget
-    A.caps = caps;
-    A.L = make_layout(caps);
-    const size_t per = static_cast<size_t>(A.L.bytes);
-    const int chunk = static_cast<int>(std::max<size_t>(1, std::min<size_t>(P, kScratchBudget / per)));
-    if (!ctx->scratch.ensure(per * std::max(chunk, 1))) return fail(ctx, "cudaMalloc scratch");
-    A.scratch = ctx->scratch.as<char>();
-    for (int base = 0; base < P; base += chunk) {
-        A.plan_base = base;
-        A.n_launch = std::min(chunk, P - base);
-        const int blocks = (A.n_launch + kPlanWarps - 1) / kPlanWarps;
-        k_plan<<<blocks, 32 * kPlanWarps, 0, st>>>(A);
-        ctx->launches++;
-    }
+    if (launch_pair(ctx, st, lc, fo, ctx->order.as<int32_t>(), nullptr, P, false, ctx->recs.as<char>(),
+                    ctx->flows.as<uint64_t>()))
+        return 1;
     // retry pass: soft-cap overflows with the hard caps, count read on device
     auto* rcount = reinterpret_cast<int32_t*>(counters + 2);
     if (P > 0) {
-        k_soft_collect<<<(P + 255) / 256, 256, 0, st>>>(A.results, P, ctx->retry_ids.as<int32_t>(), rcount);
+        k_soft_collect<<<(P + 255) / 256, 256, 0, st>>>(ctx->results.as<ws_plan_result>(), P,
+                                                         ctx->retry_ids.as<int32_t>(), rcount);
         k_clamp_count<<<1, 1, 0, st>>>(rcount);
         ctx->launches += 2;
-        PlanArgs Rr = A;
-        Rr.caps = ctx->caps_hard;
-        Rr.L = make_layout(Rr.caps);
-        const size_t per_h = static_cast<size_t>(Rr.L.bytes);
-        const int rchunk = static_cast<int>(std::min<size_t>(kRetryMax, std::max<size_t>(1, kScratchBudget / per_h)));
-        if (per_h * rchunk > ctx->scratch.n) {
-            // reuse the main scratch when large enough, else grow
-            if (!ctx->scratch.ensure(per_h * rchunk)) return fail(ctx, "cudaMalloc retry scratch");
-        }
-        Rr.scratch = ctx->scratch.as<char>();
-        Rr.plan_ids = ctx->retry_ids.as<int32_t>();
-        Rr.n_ids = rcount;
-        Rr.plan_base = 0;
-        Rr.n_launch = rchunk;
-        k_plan<<<(rchunk + kPlanWarps - 1) / kPlanWarps, 32 * kPlanWarps, 0, st>>>(Rr);
-        ctx->launches++;
+        if (launch_pair(ctx, st, lh, fo, ctx->retry_ids.as<int32_t>(), rcount, kRetryMax, true,
+                        ctx->recs_r.as<char>(), ctx->flows_r.as<uint64_t>()))
+            return 1;
     }
     CK(cudaEventRecord(ctx->ev[2], st));
     CK(cudaGetLastError());
@@ -343,7 +398,7 @@ int ws_fetch_results(ws_ctx* ctx, ws_plan_result* results, uint8_t* arena, uint6
     cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
     const int P = ctx->dview.n_plans;
     unsigned long long top = 0;
-    CK(cudaMemcpyAsync(results, ctx->results.p, sizeof(ws_plan_result) * P, cudaMemcpyDeviceToHost, st));
+    if (P) CK(cudaMemcpyAsync(results, ctx->results.p, sizeof(ws_plan_result) * P, cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(&top, ctx->counters.p, sizeof(top), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     float ms = 0;

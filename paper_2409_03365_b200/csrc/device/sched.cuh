@@ -1,0 +1,1219 @@
+// sched.cuh — k_sched: subsystems (1) graph/contraction/levels, (3) allocation
+// and (4a) wavefront scheduling.  One warp per plan; the per-plan working set
+// lives in dynamic shared memory; the schedule is handed to k_place through a
+// per-plan record in global memory.
+#pragma once
+#include "kcommon.cuh"
+
+namespace wsdev {
+
+constexpr int kSchedWarps = 4;
+
+// ---- per-plan schedule record (global), written by k_sched, read by k_place
+struct SchedHdr {
+    int ok, K, n_levels, nW;
+    int nE, pad0, pad1, pad2;
+    double lower_bound, end_time;
+};
+
+struct RecCaps {
+    int M, W, E;
+};
+
+struct RecLayout {
+    int hdr, mod_of, level, up_n, up_l, lo_n, lo_l, by_rank, idrank, pred_r, succ_r, cstar, lvl_fw, lvl_nw;
+    int w_level, w_eb, w_ec, w_start, w_dur, e_k, e_n, e_l, e_span;
+    int bytes;
+};
+
+__host__ __device__ inline int al16(int v) { return (v + 15) & ~15; }
+
+__host__ __device__ inline RecLayout make_rec_layout(const RecCaps& c) {
+    RecLayout L{};
+    int o = 0;
+    auto take = [&](int b) {
+        const int at = o;
+        o = al16(o + b);
+        return at;
+    };
+    L.hdr = take(sizeof(SchedHdr));
+    L.mod_of = take(4 * c.M);
+    L.level = take(4 * c.M);
+    L.up_n = take(4 * c.M);
+    L.up_l = take(4 * c.M);
+    L.lo_n = take(4 * c.M);
+    L.lo_l = take(4 * c.M);
+    L.by_rank = take(4 * c.M);
+    L.idrank = take(4 * c.M);
+    L.pred_r = take(8 * c.M);
+    L.succ_r = take(8 * c.M);
+    L.cstar = take(8 * c.M);
+    L.lvl_fw = take(4 * c.M);
+    L.lvl_nw = take(4 * c.M);
+    L.w_level = take(4 * c.W);
+    L.w_eb = take(4 * c.W);
+    L.w_ec = take(4 * c.W);
+    L.w_start = take(8 * c.W);
+    L.w_dur = take(8 * c.W);
+    L.e_k = take(4 * c.E);
+    L.e_n = take(4 * c.E);
+    L.e_l = take(4 * c.E);
+    L.e_span = take(8 * c.E);
+    L.bytes = o;
+    return L;
+}
+
+// ---- k_sched shared working set (per warp)
+struct SmLayout {
+    int adj, tmask, predk, pred_r, succ_r, valid, credit;                   // [M] 8 B
+    int indeg, keyrank, modat, kofm, mod_of, idrank, by_rank, level;         // [M] 4 B
+    int up_n, up_l, lo_n, lo_l, sumlay, lvl_mem, gm_of, nmax_of, Lk, absorb;  // [M] 4 B
+    int lvl_begin;                                                           // [M+1]
+    int tk, tn, tl, tn2, sel, best, pool, klay;                              // [2M]
+    int ord;                                                                 // [3*2M]
+    int bytes;
+};
+
+__host__ __device__ inline SmLayout make_sm_layout(int M) {
+    SmLayout L{};
+    int o = 0;
+    auto take = [&](int b) {
+        const int at = o;
+        o = (o + b + 7) & ~7;
+        return at;
+    };
+    const int T = 2 * M;
+    L.adj = take(8 * M);
+    L.tmask = take(8 * M);
+    L.predk = take(8 * M);
+    L.pred_r = take(8 * M);
+    L.succ_r = take(8 * M);
+    L.valid = take(8 * M);
+    L.credit = take(8 * M);
+    L.indeg = take(4 * M);
+    L.keyrank = take(4 * M);
+    L.modat = take(4 * M);
+    L.kofm = take(4 * M);
+    L.mod_of = take(4 * M);
+    L.idrank = take(4 * M);
+    L.by_rank = take(4 * M);
+    L.level = take(4 * M);
+    L.up_n = take(4 * M);
+    L.up_l = take(4 * M);
+    L.lo_n = take(4 * M);
+    L.lo_l = take(4 * M);
+    L.sumlay = take(4 * M);
+    L.lvl_mem = take(4 * M);
+    L.gm_of = take(4 * M);
+    L.nmax_of = take(4 * M);
+    L.Lk = take(4 * M);
+    L.absorb = take(4 * M);
+    L.lvl_begin = take(4 * (M + 1));
+    L.tk = take(4 * T);
+    L.tn = take(4 * T);
+    L.tl = take(4 * T);
+    L.tn2 = take(4 * T);
+    L.sel = take(4 * T);
+    L.best = take(4 * T);
+    L.pool = take(4 * T);
+    L.klay = take(4 * T);
+    L.ord = take(4 * 3 * T);
+    L.bytes = (o + 15) & ~15;
+    return L;
+}
+
+struct SchedArgs {
+    ws_batch B;
+    FitOut fit;
+    RecCaps caps;
+    RecLayout RL;
+    SmLayout SL;
+    char* recs;              // [n_plans * RL.bytes]
+    const int32_t* plan_ids; // launch order (cost-sorted) or retry list
+    const int32_t* n_ids;    // device count of plan_ids (retry pass) or null
+    int n_launch;
+    int rec_by_slot;         // retry pass: records indexed by launch slot
+    int M_cap;               // modules per plan this launch supports
+    ws_plan_result* results;
+};
+
+struct SCtx {
+    const ws_batch* B;
+    const ws_plan_rec* R;
+    const FitOut* F;
+    const SmLayout* L;
+    char* sm;
+    Ctl* ctl;
+    int lane, N, M, K, mbase;
+    template <typename T>
+    __device__ __forceinline__ T* at(int off) const {
+        return reinterpret_cast<T*>(sm + off);
+    }
+};
+
+// ---------------------------------------------------------------------------
+// (1) module DAG from the flows (graph.hpp:97-147), lexicographic Kahn and
+// contraction numbering (:66-90, :153-202), MetaGraph edges, levels (:207-226)
+// ---------------------------------------------------------------------------
+__device__ bool s_graph(SCtx& C) {
+    const ws_batch& B = *C.B;
+    const ws_plan_rec& R = *C.R;
+    const int M = C.M, lane = C.lane;
+    uint64_t* adj = C.at<uint64_t>(C.L->adj);
+    uint64_t* tmask = C.at<uint64_t>(C.L->tmask);
+    int* kofm = C.at<int>(C.L->kofm);
+    int* indeg = C.at<int>(C.L->indeg);
+    int* keyrank = C.at<int>(C.L->keyrank);
+    int* modat = C.at<int>(C.L->modat);
+    int* mod_of = C.at<int>(C.L->mod_of);
+    for (int m = lane; m < M; m += 32) {
+        adj[m] = 0;
+        tmask[m] = 0;
+        kofm[m] = -1;
+    }
+    __syncwarp();
+    // tasks in parallel: lane t walks the flow of task t
+    for (int t = lane; t < R.n_tasks; t += 32) {
+        const int tg = R.task_begin + t;
+        const int* tok = B.tokens + B.task_tok_off[tg];
+        const int ntok = B.task_tok_n[tg];
+        const uint64_t tbit = 1ull << B.task_rank[tg];
+        uint64_t prev_tails = 0, heads = 0, tails = 0;
+        int last = -1;
+        bool start = true;
+        for (int i = 0; i <= ntok; ++i) {
+            const int v = i < ntok ? __ldg(tok + i) : WS_TOK_STEP;
+            if (v >= 0) {
+                atomicOr(reinterpret_cast<unsigned long long*>(&tmask[v]), tbit);
+                if (start)
+                    heads |= 1ull << v;  // branch head (graph.hpp:130)
+                else
+                    atomicOr(reinterpret_cast<unsigned long long*>(&adj[last]), 1ull << v);  // chained (:131)
+                start = false;
+                last = v;
+            } else {
+                if (last >= 0) tails |= 1ull << last;
+                last = -1;
+                start = true;
+                if (v == WS_TOK_STEP) {  // every tail of step k feeds every head of step k+1 (:137-139)
+                    for (uint64_t f = prev_tails; f; f &= f - 1)
+                        atomicOr(reinterpret_cast<unsigned long long*>(&adj[low_bit(f)]), heads);
+                    prev_tails = tails;
+                    heads = tails = 0;
+                }
+            }
+        }
+    }
+    __syncwarp();
+    uint64_t used = 0;
+    for (int base = 0; base < M; base += 32) {
+        const int m = base + lane;
+        used |= static_cast<uint64_t>(__ballot_sync(kFull, m < M && tmask[m] != 0)) << base;
+    }
+    // in-degrees, rank of the key kind+"." and kinds prefixed by another kind+"."
+    int conflict = 0;
+    for (int m = lane; m < M; m += 32) {
+        int d = 0;
+        for (int a = 0; a < M; ++a) d += (adj[a] >> m) & 1ull;
+        indeg[m] = d;
+        if (!(used >> m & 1ull)) {
+            keyrank[m] = -1;
+            continue;
+        }
+        const OpKey km = op_key(B, C.mbase + m, 0, false);
+        int r = 0;
+        for (uint64_t o = used; o; o &= o - 1) {
+            const int q = low_bit(o);
+            if (q == m) continue;
+            const OpKey kq = op_key(B, C.mbase + q, 0, false);
+            if (key_less(kq, km)) ++r;
+            if (kq.len > km.len) {
+                bool pre = true;
+                for (int i = 0; i <= km.len && pre; ++i) pre = kq.at(i) == km.at(i);
+                if (pre) conflict = 1;
+            }
+        }
+        keyrank[m] = r;
+        modat[r] = m;
+    }
+    conflict = __any_sync(kFull, conflict);
+    __syncwarp();
+    const int nused = popc64(used);
+    if (lane == 0) {
+        int K = 0;
+        if (!conflict) {
+            // once kind.0 pops, its remaining layers pop consecutively,
+            // so the operator-level lexicographic Kahn is the module Kahn by kind+"."
+            uint64_t ready = 0;
+            for (uint64_t u = used; u; u &= u - 1) {
+                const int m = low_bit(u);
+                if (indeg[m] == 0) ready |= 1ull << keyrank[m];
+            }
+            while (ready) {
+                const int r = low_bit(ready);
+                ready &= ready - 1;
+                const int m = modat[r];
+                kofm[m] = K;
+                mod_of[K++] = m;
+                for (uint64_t s = adj[m]; s; s &= s - 1) {
+                    const int q = low_bit(s);
+                    if (--indeg[q] == 0) ready |= 1ull << keyrank[q];
+                }
+            }
+        } else {
+            // general operator-level lexicographic Kahn with per-module layer cursors
+            int* cursor = C.at<int>(C.L->sumlay);
+            for (int m = 0; m < M; ++m) cursor[m] = 0;
+            while (true) {
+                int best = -1;
+                OpKey bk;
+                for (uint64_t u = used; u; u &= u - 1) {
+                    const int m = low_bit(u);
+                    const int L = B.mod_layers[C.mbase + m];
+                    if (cursor[m] >= L || (cursor[m] == 0 && indeg[m] != 0)) continue;
+                    const OpKey k = op_key(B, C.mbase + m, cursor[m], true);
+                    if (best < 0 || key_less(k, bk)) {
+                        best = m;
+                        bk = k;
+                    }
+                }
+                if (best < 0) break;
+                if (cursor[best] == 0) {
+                    kofm[best] = K;
+                    mod_of[K++] = best;
+                }
+                if (++cursor[best] == B.mod_layers[C.mbase + best])
+                    for (uint64_t s = adj[best]; s; s &= s - 1) --indeg[low_bit(s)];
+            }
+        }
+        C.ctl->i0 = K;
+        if (K != nused) set_err(C.ctl, WS_E_CYCLIC_WORKLOAD);
+    }
+    __syncwarp();
+    if (C.ctl->err) return false;
+    const int K = C.ctl->i0;
+    C.K = K;
+    int* idrank = C.at<int>(C.L->idrank);
+    int* by_rank = C.at<int>(C.L->by_rank);
+    int* gm_of = C.at<int>(C.L->gm_of);
+    int* nmax_of = C.at<int>(C.L->nmax_of);
+    int* Lk = C.at<int>(C.L->Lk);
+    for (int k = lane; k < K; k += 32) {  // MetaOp ids "m<k>" in std::map order
+        int r = 0;
+        for (int j = 0; j < K; ++j) r += dec_less(j, k);
+        idrank[k] = r;
+        by_rank[r] = k;
+        const int gm = C.mbase + mod_of[k];
+        gm_of[k] = gm;
+        nmax_of[k] = C.F->nmax[gm];
+        Lk[k] = B.mod_layers[gm];
+    }
+    __syncwarp();
+    uint64_t* predk = C.at<uint64_t>(C.L->predk);
+    uint64_t* pred_r = C.at<uint64_t>(C.L->pred_r);
+    uint64_t* succ_r = C.at<uint64_t>(C.L->succ_r);
+    for (int k = lane; k < K; k += 32) {
+        const int m = mod_of[k];
+        uint64_t pk = 0, pr = 0, sr = 0;
+        for (int j = 0; j < K; ++j) {
+            if (j == k) continue;
+            const int q = mod_of[j];
+            if (adj[q] >> m & 1ull) pk |= 1ull << j, pr |= 1ull << idrank[j];
+            if (adj[m] >> q & 1ull) sr |= 1ull << idrank[j];
+        }
+        predk[k] = pk;
+        pred_r[k] = pr;
+        succ_r[k] = sr;
+    }
+    __syncwarp();
+    if (lane == 0) {  // longest-path levels; numbering order is topological
+        int* level = C.at<int>(C.L->level);
+        int maxl = 0;
+        for (int k = 0; k < K; ++k) {
+            int lv = 0;
+            for (uint64_t p = predk[k]; p; p &= p - 1) {
+                const int q = level[low_bit(p)] + 1;
+                lv = q > lv ? q : lv;
+            }
+            level[k] = lv;
+            maxl = lv > maxl ? lv : maxl;
+        }
+        int* lb = C.at<int>(C.L->lvl_begin);
+        int* lm = C.at<int>(C.L->lvl_mem);
+        int* fill = C.at<int>(C.L->absorb);
+        for (int l = 0; l <= maxl + 1; ++l) lb[l] = 0;
+        for (int k = 0; k < K; ++k) lb[level[k] + 1]++;
+        for (int l = 0; l <= maxl; ++l) lb[l + 1] += lb[l];
+        for (int l = 0; l <= maxl; ++l) fill[l] = lb[l];
+        for (int r = 0; r < K; ++r) {
+            const int k = by_rank[r];
+            lm[fill[level[k]]++] = k;
+        }
+        C.ctl->i1 = maxl + 1;
+    }
+    __syncwarp();
+    return true;
+}
+
+// (2) results of k_fit: the first module in kind order whose fit failed
+__device__ bool s_fit_status(SCtx& C) {
+    const int M = C.M;
+    for (int base = 0; base < M; base += 32) {
+        const int m = base + C.lane;
+        const int e = m < M ? C.F->err[C.mbase + m] : 0;
+        const unsigned b = __ballot_sync(kFull, e != 0);
+        if (b) {
+            const int first = base + __ffs(b) - 1;
+            if (C.lane == 0) {
+                const int gm = C.mbase + first;
+                const int code = C.F->err[gm];
+                set_err(C.ctl, code, code == WS_E_NO_SOURCE ? first : C.F->err_a[gm], C.F->err_b[gm]);
+            }
+            __syncwarp();
+            return false;
+        }
+    }
+    return true;
+}
+
+// (3a) valid allocation sets n = tp*r with r | B (allocation.hpp:51-63)
+__device__ bool s_valid(SCtx& C) {
+    const ws_batch& B = *C.B;
+    const int K = C.K, N = C.N, lane = C.lane;
+    const int* gm_of = C.at<int>(C.L->gm_of);
+    const int* by_rank = C.at<int>(C.L->by_rank);
+    uint64_t* valid = C.at<uint64_t>(C.L->valid);
+    for (int base = 0; base < K; base += 32) {  // tp > N in id order (planner.hpp:168-171)
+        const int r = base + lane;
+        const bool bad = r < K && B.mod_tp[gm_of[by_rank[r]]] > N;
+        const unsigned b = __ballot_sync(kFull, bad);
+        if (b) {
+            if (lane == 0) {
+                const int k = by_rank[base + __ffs(b) - 1];
+                set_err(C.ctl, WS_E_TP_EXCEEDS, k, B.mod_tp[gm_of[k]]);
+            }
+            __syncwarp();
+            return false;
+        }
+    }
+    for (int k = 0; k < K; ++k) {  // lanes = device counts n, one ballot per 32 n
+        const int gm = gm_of[k];
+        const int tp = B.mod_tp[gm];
+        const long long batch = B.mod_batch[gm];
+        uint64_t v = 0;
+        for (int base = 0; base < N; base += 32) {
+            const int n = base + lane + 1;
+            bool ok = n <= N && n % tp == 0;
+            if (ok) ok = batch % (n / tp) == 0;
+            v |= static_cast<uint64_t>(__ballot_sync(kFull, ok)) << base;
+        }
+        if (lane == 0) valid[k] = v;
+    }
+    __syncwarp();
+    return true;
+}
+
+__device__ __forceinline__ double ordered_sum(double v0, double v1, int w) {
+    double total = 0.0;  // reference order: ((0 + v_0) + v_1) + ...
+    for (int j = 0; j < 32 && j < w; ++j) total += shfl_d(v0, j);
+    for (int j = 0; j + 32 < w; ++j) total += shfl_d(v1, j);
+    return total;
+}
+
+// (3b) bisection on the capacity equation, bi-point discretization and
+// capacity repair for one level; lane i holds members i and i+32
+__device__ bool s_level_alloc(SCtx& C, int lvl, double& c_star_out) {
+    const ws_batch& B = *C.B;
+    const ws_plan_rec& R = *C.R;
+    const int N = C.N, lane = C.lane;
+    const int* lb = C.at<int>(C.L->lvl_begin);
+    const int* lm = C.at<int>(C.L->lvl_mem) + lb[lvl];
+    const int w = lb[lvl + 1] - lb[lvl];
+    const int* gm_of = C.at<int>(C.L->gm_of);
+    const int* nmax_of = C.at<int>(C.L->nmax_of);
+    const int* Lk = C.at<int>(C.L->Lk);
+    const uint64_t* valid = C.at<uint64_t>(C.L->valid);
+    int* up_n = C.at<int>(C.L->up_n);
+    int* up_l = C.at<int>(C.L->up_l);
+    int* lo_n = C.at<int>(C.L->lo_n);
+    int* lo_l = C.at<int>(C.L->lo_l);
+    const double nd = static_cast<double>(N);
+    const FitOut& F = *C.F;
+    struct Mem {
+        int k, gm, L, np;
+        const double* pc;
+        double c, w, nmax;
+    } mem[2];
+    for (int s = 0; s < 2; ++s) {
+        const int i = lane + 32 * s;
+        Mem& q = mem[s];
+        q.k = -1;
+        if (i < w) {
+            q.k = lm[i];
+            q.gm = gm_of[q.k];
+            q.L = Lk[q.k];
+            q.np = F.npieces[q.gm];
+            q.pc = F.pieces + 5 * F.piece_off[q.gm];
+            q.c = B.mod_c[q.gm];
+            q.w = B.mod_w[q.gm];
+            q.nmax = nmax_of[q.k];
+        }
+    }
+    // bracket [max T(min(N,nmax))*L, sum T(1)*L] (allocation.hpp:75-80)
+    double lo0 = 0.0, hi0[2] = {0.0, 0.0};
+    for (int s = 0; s < 2; ++s) {
+        const Mem& q = mem[s];
+        if (q.k < 0) continue;
+        const double ncap = (q.nmax < nd) ? q.nmax : nd;
+        const double v = t_at(F, q.gm, static_cast<int>(ncap)) * q.L;
+        lo0 = (lo0 < v) ? v : lo0;
+        hi0[s] = t_at(F, q.gm, 1) * q.L;
+    }
+    double c_lo = warp_max_d(lo0);
+    double c_hi = ordered_sum(hi0[0], hi0[1], w);
+    auto probe_term = [&](const Mem& q, double cc) {
+        const double v = inverse_exact(q.pc, q.np, q.c, q.w, q.nmax, cc / q.L);
+        return (nd < v) ? nd : v;  // std::min(v, N)
+    };
+    for (int it = 0; it < R.max_iters && (c_hi - c_lo) > R.eps * c_hi; ++it) {
+        const double mid = 0.5 * (c_lo + c_hi);
+        const double t0 = mem[0].k >= 0 ? probe_term(mem[0], mid) : 0.0;
+        const double t1 = mem[1].k >= 0 ? probe_term(mem[1], mid) : 0.0;
+        if (ordered_sum(t0, t1, w) < nd)
+            c_hi = mid;
+        else
+            c_lo = mid;
+    }
+    const double cs = 0.5 * (c_lo + c_hi);
+    c_star_out = cs;
+    // discretize (allocation.hpp:149-214)
+    int eidx0 = 0x7fffffff;
+    double ex0 = 0, ey0 = 0;
+    for (int s = 0; s < 2; ++s) {
+        const Mem& q = mem[s];
+        if (q.k < 0) continue;
+        const double nstar = probe_term(q, cs);
+        const uint64_t v = valid[q.k];
+        const int L = q.L;
+        int exact = -1, n_over = -1, n_under = -1;
+        for (uint64_t b = v; b; b &= b - 1) {
+            const int x = low_bit(b) + 1;
+            if (fabs(x - nstar) < 1e-9) {
+                exact = x;
+                break;
+            }
+        }
+        if (exact < 0)
+            for (uint64_t b = v; b; b &= b - 1) {
+                const int x = low_bit(b) + 1;
+                if (x < nstar) n_under = x;
+                if (x > nstar) {
+                    n_over = x;
+                    break;
+                }
+            }
+        int un = 0, ul = L, ln = 0, ll = 0;
+        if (exact >= 0) {
+            un = exact;
+        } else if (n_over == -1) {
+            un = 64 - __clzll(static_cast<long long>(v));
+        } else if (n_under == -1) {
+            un = low_bit(v) + 1;
+        } else {
+            if (n_over > q.nmax || n_under > q.nmax) {  // OutOfRange (eval(n_over) first)
+                const int idx = lane + 32 * s;
+                if (idx < eidx0) eidx0 = idx, ex0 = n_over > q.nmax ? n_over : n_under, ey0 = q.nmax;
+                continue;
+            }
+            const double t_over = t_at(F, q.gm, n_over);
+            const double t_under = t_at(F, q.gm, n_under);
+            if (t_under - t_over <= 0.0) {
+                un = n_under;
+            } else {
+                double lr = (cs - t_under * L) / (t_over - t_under);
+                lr = lr < 0.0 ? 0.0 : (static_cast<double>(L) < lr ? static_cast<double>(L) : lr);
+                int l_over = static_cast<int>(floor(lr + 0.5));
+                int l_under = L - l_over;
+                if (R.drop_floor > 0.0 && l_over > 0 && l_under > 0) {
+                    if (l_over * t_over < R.drop_floor * cs) {
+                        l_under += l_over;
+                        l_over = 0;
+                    } else if (l_under * t_under < R.drop_floor * cs) {
+                        l_over += l_under;
+                        l_under = 0;
+                    }
+                }
+                if (l_over == 0) {
+                    un = n_under;
+                } else if (l_under == 0) {
+                    un = n_over;
+                } else {
+                    un = n_over;
+                    ul = l_over;
+                    ln = n_under;
+                    ll = l_under;
+                }
+            }
+        }
+        up_n[q.k] = un;
+        up_l[q.k] = ul;
+        lo_n[q.k] = ln;
+        lo_l[q.k] = ll;
+    }
+    {
+        const int emin = warp_min_i(eidx0);
+        if (emin != 0x7fffffff) {
+            const int src = emin & 31;
+            const double xx = shfl_d(ex0, src), yy = shfl_d(ey0, src);
+            if (lane == 0) {
+                C.ctl->err = WS_E_EVAL_RANGE;
+                C.ctl->x = xx;
+                C.ctl->y = yy;
+            }
+            __syncwarp();
+            return false;
+        }
+    }
+    __syncwarp();
+    // repair_capacity (allocation.hpp:107-139)
+    while (true) {
+        int wid = 0;
+        for (int s = 0; s < 2; ++s) {
+            const Mem& q = mem[s];
+            if (q.k < 0) continue;
+            const int a = up_n[q.k], b = lo_l[q.k] ? lo_n[q.k] : 0;
+            wid += a > b ? a : b;
+        }
+        if (warp_sum(wid) <= N) break;
+        double best_pen = 0.0;
+        int best_i = 0x7fffffff, best_t = 0, eidx = 0x7fffffff;
+        double ex = 0, ey = 0;
+        for (int s = 0; s < 2; ++s) {
+            const Mem& q = mem[s];
+            if (q.k < 0) continue;
+            const int un = up_n[q.k];
+            const uint64_t below = valid[q.k] & ((1ull << (un - 1)) - 1ull);  // valid values < un
+            if (!below) continue;
+            const int target = 64 - __clzll(static_cast<long long>(below));
+            if (lo_l[q.k] && target <= lo_n[q.k]) continue;
+            const int idx = lane + 32 * s;
+            if (target > q.nmax || un > q.nmax) {  // eval(target) first, then eval(t.n)
+                if (idx < eidx) eidx = idx, ex = target > q.nmax ? target : un, ey = q.nmax;
+                continue;
+            }
+            const double pen = up_l[q.k] * (t_at(F, q.gm, target) - t_at(F, q.gm, un));
+            if (best_i == 0x7fffffff || pen < best_pen) best_pen = pen, best_i = idx, best_t = target;
+        }
+        const int emin = warp_min_i(eidx);
+        if (emin != 0x7fffffff) {
+            const int src = emin & 31;
+            const double xx = shfl_d(ex, src), yy = shfl_d(ey, src);
+            if (lane == 0) {
+                C.ctl->err = WS_E_EVAL_RANGE;
+                C.ctl->x = xx;
+                C.ctl->y = yy;
+            }
+            __syncwarp();
+            return false;
+        }
+        for (int off = 16; off; off >>= 1) {  // argmin over (penalty, member index)
+            const double op = __shfl_xor_sync(kFull, best_pen, off);
+            const int oi = __shfl_xor_sync(kFull, best_i, off);
+            const int ot = __shfl_xor_sync(kFull, best_t, off);
+            if (oi != 0x7fffffff && (best_i == 0x7fffffff || op < best_pen || (op == best_pen && oi < best_i)))
+                best_pen = op, best_i = oi, best_t = ot;
+        }
+        if (best_i == 0x7fffffff) break;
+        if (lane == 0) up_n[lm[best_i]] = best_t;
+        __syncwarp();
+    }
+    return true;
+}
+
+// ---------------------------------------------------------------------------
+// (4a) wave scheduling of one level (schedule.hpp:49-288)
+// ---------------------------------------------------------------------------
+struct SchedView {
+    int* tk;
+    int* tn;
+    int* tl;
+    int R;
+    const int* sumlay;
+    const int* idrank;
+    const uint64_t* valid;
+    int N;
+    TErr T;
+};
+
+struct CmpByN {  // schedule.hpp:98-104
+    const SchedView* s;
+    __device__ bool operator()(int a, int b) const {
+        if (s->tn[a] != s->tn[b]) return s->tn[a] > s->tn[b];
+        const double ra = s->tl[a] * s->T(s->tk[a], s->tn[a]);
+        const double rb = s->tl[b] * s->T(s->tk[b], s->tn[b]);
+        if (ra != rb) return ra > rb;
+        return s->idrank[s->tk[a]] < s->idrank[s->tk[b]];
+    }
+};
+struct CmpByTime {  // schedule.hpp:105-111
+    const SchedView* s;
+    __device__ bool operator()(int a, int b) const {
+        const double ra = s->sumlay[s->tk[a]] * s->T(s->tk[a], s->tn[a]);
+        const double rb = s->sumlay[s->tk[b]] * s->T(s->tk[b], s->tn[b]);
+        if (ra != rb) return ra > rb;
+        if (s->tn[a] != s->tn[b]) return s->tn[a] > s->tn[b];
+        return s->idrank[s->tk[a]] < s->idrank[s->tk[b]];
+    }
+};
+struct CmpByCheap {  // schedule.hpp:112-118
+    const SchedView* s;
+    __device__ bool operator()(int a, int b) const {
+        if (s->tn[a] != s->tn[b]) return s->tn[a] < s->tn[b];
+        const double ra = s->sumlay[s->tk[a]] * s->T(s->tk[a], s->tn[a]);
+        const double rb = s->sumlay[s->tk[b]] * s->T(s->tk[b], s->tn[b]);
+        if (ra != rb) return ra > rb;
+        return s->idrank[s->tk[a]] < s->idrank[s->tk[b]];
+    }
+};
+
+// serial path (lane 0): any tuple count, out-of-range-capable curves
+__device__ void ser_extend(const SchedView& S, int* n, const int* sel, int nsel) {  // schedule.hpp:144-173
+    while (true) {
+        int usedn = 0;
+        for (int i = 0; i < nsel; ++i) usedn += n[sel[i]];
+        const int idle = S.N - usedn;
+        if (idle <= 0) break;
+        int best = -1, best_next = 0;
+        double best_time = -1.0;
+        for (int i = 0; i < nsel; ++i) {
+            const int t = sel[i];
+            const int k = S.tk[t];
+            const uint64_t above = S.valid[k] & ~bits_upto(n[t] - 1);
+            if (!above) continue;
+            const int nx = low_bit(above) + 1;
+            if (nx - n[t] > idle) continue;
+            const double rem = S.sumlay[k] * S.T(k, n[t]);
+            if (S.T.ctl->err) return;
+            if (rem > best_time || (rem == best_time && best >= 0 && S.idrank[k] < S.idrank[S.tk[best]])) {
+                best = t;
+                best_time = rem;
+                best_next = nx;
+            }
+        }
+        if (best < 0) break;
+        n[best] = best_next;
+    }
+}
+
+__device__ int ser_greedy(const SchedView& S, const int* order, int* sel) {
+    int ns = 0, cap = S.N;
+    uint64_t taken = 0;
+    for (int i = 0; i < S.R; ++i) {
+        const int t = order[i];
+        if (S.tn[t] > cap) continue;
+        if (taken >> S.tk[t] & 1ull) continue;
+        sel[ns++] = t;
+        taken |= 1ull << S.tk[t];
+        cap -= S.tn[t];
+    }
+    return ns;
+}
+
+// One wave on lane 0: propose (3 exact std::sort emulations), extend, align.
+// Fills best[0..nbest) (selection order) and klay[]; returns nbest or -1.
+__device__ int ser_wave(SCtx& C, SchedView& S) {
+    int* n2 = C.at<int>(C.L->tn2);
+    int* sel = C.at<int>(C.L->sel);
+    int* best = C.at<int>(C.L->best);
+    int* pool = C.at<int>(C.L->pool);
+    int* klay = C.at<int>(C.L->klay);
+    double* credit = C.at<double>(C.L->credit);
+    const int cap2 = 2 * C.M;
+    int* o0 = C.at<int>(C.L->ord);
+    int* o1 = o0 + cap2;
+    int* o2 = o0 + 2 * cap2;
+    const int R = S.R;
+    for (int i = 0; i < R; ++i) o0[i] = o1[i] = o2[i] = i;
+    CmpByN c0{&S};
+    ls_sort(o0, R, c0);
+    CmpByTime c1{&S};
+    ls_sort(o1, R, c1);
+    CmpByCheap c2{&S};
+    ls_sort(o2, R, c2);
+    if (C.ctl->err) return -1;
+    int nbest = 0;
+    long long best_key = -1;
+    for (int o = 0; o < 3; ++o) {
+        const int* order = o == 0 ? o0 : (o == 1 ? o1 : o2);
+        const int ns = ser_greedy(S, order, sel);
+        for (int i = 0; i < R; ++i) n2[i] = S.tn[i];
+        ser_extend(S, n2, sel, ns);
+        if (C.ctl->err) return -1;
+        int usedn = 0;
+        for (int i = 0; i < ns; ++i) usedn += n2[sel[i]];
+        const long long key = static_cast<long long>(usedn) * 1000 + ns;
+        if (key > best_key) {  // strict: earlier orders win ties
+            best_key = key;
+            nbest = ns;
+            for (int i = 0; i < ns; ++i) best[i] = sel[i];
+        }
+    }
+    if (nbest == 0) {
+        set_err(C.ctl, WS_E_NO_SCHEDULABLE);
+        return -1;
+    }
+    ser_extend(S, S.tn, best, nbest);
+    if (C.ctl->err) return -1;
+    // align_time_span (schedule.hpp:190-227)
+    double t_wave = 0.0;
+    for (int i = 0; i < nbest; ++i) {
+        const int t = best[i];
+        pool[i] = S.sumlay[S.tk[t]];
+        const double span = pool[i] * S.T(S.tk[t], S.tn[t]);
+        if (i == 0 || span < t_wave) t_wave = span;
+    }
+    if (C.ctl->err) return -1;
+    for (int i = 0; i < nbest; ++i) {
+        const int t = best[i];
+        const int k = S.tk[t];
+        const double per = S.T(k, S.tn[t]);
+        int kk;
+        if (pool[i] * per <= t_wave * (1.0 + 1e-12)) {
+            kk = pool[i];
+            credit[k] = 0.0;
+        } else {
+            const double carried = credit[k];
+            const double budget = t_wave + ((per < carried) ? per : carried);
+            kk = static_cast<int>(floor(budget / per * (1.0 + 1e-12)));
+            kk = kk < 1 ? 1 : kk;
+            kk = kk < pool[i] ? kk : pool[i];
+            const double rest = budget - kk * per;
+            credit[k] = (0.0 < rest) ? rest : 0.0;
+        }
+        klay[i] = kk;
+    }
+    return C.ctl->err ? -1 : nbest;
+}
+
+// Fast path (R <= 16 tuples, every curve defined up to N): lanes = tuples.
+// Stable ranks reproduce std::sort exactly for <= 16 elements (insertion
+// sort); greedy runs warp-uniformly; extension/alignment are lane-parallel.
+__device__ int fast_wave(SCtx& C, SchedView& S) {
+    const int lane = C.lane, R = S.R, N = S.N;
+    const FitOut& F = *C.F;
+    const int* gm_of = C.at<int>(C.L->gm_of);
+    int* best = C.at<int>(C.L->best);
+    int* klay = C.at<int>(C.L->klay);
+    double* credit = C.at<double>(C.L->credit);
+    int* o0 = C.at<int>(C.L->ord);
+    const int cap2 = 2 * C.M;
+    const bool mine = lane < R;
+    const int k = mine ? S.tk[lane] : 0;
+    const int n0 = mine ? S.tn[lane] : 0;
+    const int tl = mine ? S.tl[lane] : 0;
+    const int sl = mine ? S.sumlay[k] : 0;
+    const int idr = mine ? S.idrank[k] : 0;
+    const uint64_t vmask = mine ? S.valid[k] : 0;
+    const int gm = mine ? gm_of[k] : 0;
+    const double T0 = mine ? t_at(F, gm, n0) : 0.0;
+    const double tt = tl * T0;  // tuple_time
+    const double rt = sl * T0;  // metaop_remaining_time at own n
+    // stable ranks under the three comparators
+    int p0 = 0, p1 = 0, p2 = 0;
+    for (int j = 0; j < R; ++j) {
+        const int nj = __shfl_sync(kFull, n0, j);
+        const double ttj = __shfl_sync(kFull, tt, j);
+        const double rtj = __shfl_sync(kFull, rt, j);
+        const int idj = __shfl_sync(kFull, idr, j);
+        if (!mine || j == lane) continue;
+        // comp(j, i) or (j < i and equivalent)
+        bool lt0, eq0, lt1, eq1, lt2, eq2;
+        if (nj != n0) lt0 = nj > n0, eq0 = false;
+        else if (ttj != tt) lt0 = ttj > tt, eq0 = false;
+        else lt0 = idj < idr, eq0 = idj == idr;
+        if (rtj != rt) lt1 = rtj > rt, eq1 = false;
+        else if (nj != n0) lt1 = nj > n0, eq1 = false;
+        else lt1 = idj < idr, eq1 = idj == idr;
+        if (nj != n0) lt2 = nj < n0, eq2 = false;
+        else if (rtj != rt) lt2 = rtj > rt, eq2 = false;
+        else lt2 = idj < idr, eq2 = idj == idr;
+        p0 += lt0 || (eq0 && j < lane);
+        p1 += lt1 || (eq1 && j < lane);
+        p2 += lt2 || (eq2 && j < lane);
+    }
+    if (mine) {
+        o0[p0] = lane;
+        o0[cap2 + p1] = lane;
+        o0[2 * cap2 + p2] = lane;
+    }
+    __syncwarp();
+    // three greedy selections (warp-uniform), scratch extension, keys
+    unsigned best_sel = 0;
+    int best_cnt = 0;
+    long long best_key = -1;
+    int my_best_pos = -1;
+    for (int o = 0; o < 3; ++o) {
+        const int* order = o0 + o * cap2;
+        unsigned sel = 0;
+        int cap = N, ns = 0, mypos = -1;
+        uint64_t taken = 0;
+        for (int i = 0; i < R; ++i) {
+            const int t = order[i];
+            const int nt = S.tn[t], kt = S.tk[t];
+            if (nt > cap || (taken >> kt & 1ull)) continue;
+            sel |= 1u << t;
+            taken |= 1ull << kt;
+            cap -= nt;
+            if (t == lane) mypos = ns;
+            ++ns;
+        }
+        // scratch extension (schedule.hpp:126-131): lane-parallel argmax loop
+        int n = n0;
+        const bool in = (sel >> lane) & 1u;
+        while (true) {
+            const int idle = N - warp_sum(in ? n : 0);
+            if (idle <= 0) break;
+            double rem = -1.0;
+            int cand = 0, nx = 0;
+            if (in) {
+                const uint64_t above = vmask & ~bits_upto(n - 1);
+                if (above) {
+                    nx = low_bit(above) + 1;
+                    if (nx - n <= idle) {
+                        cand = 1;
+                        rem = sl * t_at(F, gm, n);
+                    }
+                }
+            }
+            // argmax rem, ties -> smaller id
+            double br = rem;
+            int bi = cand ? idr : 0x7fffffff, bl = cand ? lane : -1;
+            for (int off = 16; off; off >>= 1) {
+                const double orr = __shfl_xor_sync(kFull, br, off);
+                const int oi = __shfl_xor_sync(kFull, bi, off);
+                const int ol = __shfl_xor_sync(kFull, bl, off);
+                if (ol >= 0 && (bl < 0 || orr > br || (orr == br && oi < bi))) br = orr, bi = oi, bl = ol;
+            }
+            if (bl < 0) break;
+            if (lane == bl) n = nx;
+        }
+        const int usedn = warp_sum(in ? n : 0);
+        const long long key = static_cast<long long>(usedn) * 1000 + ns;
+        if (key > best_key) {
+            best_key = key;
+            best_sel = sel;
+            best_cnt = ns;
+            my_best_pos = mypos;
+        }
+    }
+    if (best_cnt == 0) {
+        if (lane == 0) set_err(C.ctl, WS_E_NO_SCHEDULABLE);
+        __syncwarp();
+        return -1;
+    }
+    // real extension on the chosen set
+    const bool in = (best_sel >> lane) & 1u;
+    int n = n0;
+    while (true) {
+        const int idle = N - warp_sum(in ? n : 0);
+        if (idle <= 0) break;
+        double rem = -1.0;
+        int cand = 0, nx = 0;
+        if (in) {
+            const uint64_t above = vmask & ~bits_upto(n - 1);
+            if (above) {
+                nx = low_bit(above) + 1;
+                if (nx - n <= idle) {
+                    cand = 1;
+                    rem = sl * t_at(F, gm, n);
+                }
+            }
+        }
+        double br = rem;
+        int bi = cand ? idr : 0x7fffffff, bl = cand ? lane : -1;
+        for (int off = 16; off; off >>= 1) {
+            const double orr = __shfl_xor_sync(kFull, br, off);
+            const int oi = __shfl_xor_sync(kFull, bi, off);
+            const int ol = __shfl_xor_sync(kFull, bl, off);
+            if (ol >= 0 && (bl < 0 || orr > br || (orr == br && oi < bi))) br = orr, bi = oi, bl = ol;
+        }
+        if (bl < 0) break;
+        if (lane == bl) n = nx;
+    }
+    if (mine) S.tn[lane] = n;
+    // align_time_span: t_wave = min span over the chosen set
+    const double per = in ? t_at(F, gm, n) : 0.0;
+    const double span = in ? sl * per : 0.0;
+    const double t_wave = warp_min_d(in ? span : __longlong_as_double(0x7ff0000000000000ll));
+    if (in) {
+        int kk;
+        if (sl * per <= t_wave * (1.0 + 1e-12)) {
+            kk = sl;
+            credit[k] = 0.0;
+        } else {
+            const double carried = credit[k];
+            const double budget = t_wave + ((per < carried) ? per : carried);
+            kk = static_cast<int>(floor(budget / per * (1.0 + 1e-12)));
+            kk = kk < 1 ? 1 : kk;
+            kk = kk < sl ? kk : sl;
+            const double rest = budget - kk * per;
+            credit[k] = (0.0 < rest) ? rest : 0.0;
+        }
+        best[my_best_pos] = lane;
+        klay[my_best_pos] = kk;
+    }
+    __syncwarp();
+    return best_cnt;
+}
+
+// (4a) schedule_level + merge_levels offsets; appends waves/entries to the record
+__device__ bool s_schedule_level(SCtx& C, char* rec, const RecLayout& RL, int lvl, int& nW, int& nE,
+                                 double offset, double& level_end, int W_CAP, int E_CAP) {
+    const int lane = C.lane;
+    const int* lb = C.at<int>(C.L->lvl_begin);
+    const int* lm = C.at<int>(C.L->lvl_mem) + lb[lvl];
+    const int w = lb[lvl + 1] - lb[lvl];
+    const int* up_n = C.at<int>(C.L->up_n);
+    const int* up_l = C.at<int>(C.L->up_l);
+    const int* lo_n = C.at<int>(C.L->lo_n);
+    const int* lo_l = C.at<int>(C.L->lo_l);
+    const int* nmax_of = C.at<int>(C.L->nmax_of);
+    int* sumlay = C.at<int>(C.L->sumlay);
+    double* credit = C.at<double>(C.L->credit);
+    int* best = C.at<int>(C.L->best);
+    int* klay = C.at<int>(C.L->klay);
+    int* absorb = C.at<int>(C.L->absorb);
+    SchedView S;
+    S.tk = C.at<int>(C.L->tk);
+    S.tn = C.at<int>(C.L->tn);
+    S.tl = C.at<int>(C.L->tl);
+    S.sumlay = sumlay;
+    S.idrank = C.at<int>(C.L->idrank);
+    S.valid = C.at<uint64_t>(C.L->valid);
+    S.N = C.N;
+    S.T = TErr{C.F, C.at<int>(C.L->gm_of), nmax_of, C.ctl};
+    int* w_level = reinterpret_cast<int*>(rec + RL.w_level);
+    int* w_eb = reinterpret_cast<int*>(rec + RL.w_eb);
+    int* w_ec = reinterpret_cast<int*>(rec + RL.w_ec);
+    double* w_start = reinterpret_cast<double*>(rec + RL.w_start);
+    double* w_dur = reinterpret_cast<double*>(rec + RL.w_dur);
+    int* e_k = reinterpret_cast<int*>(rec + RL.e_k);
+    int* e_n = reinterpret_cast<int*>(rec + RL.e_n);
+    int* e_l = reinterpret_cast<int*>(rec + RL.e_l);
+    double* e_span = reinterpret_cast<double*>(rec + RL.e_span);
+    // remaining tuples in id order: upper then lower (schedule.hpp:236-240)
+    int R = 0;
+    bool all_defined = true;
+    if (lane == 0) {
+        for (int i = 0; i < w; ++i) {
+            const int k = lm[i];
+            S.tk[R] = k, S.tn[R] = up_n[k], S.tl[R] = up_l[k], ++R;
+            if (lo_l[k]) S.tk[R] = k, S.tn[R] = lo_n[k], S.tl[R] = lo_l[k], ++R;
+            credit[k] = 0.0;
+            absorb[k] = 0;
+        }
+        C.ctl->i2 = R;
+    }
+    for (int i = lane; i < w; i += 32) all_defined &= nmax_of[lm[i]] >= C.N;
+    all_defined = __all_sync(kFull, all_defined);
+    __syncwarp();
+    R = C.ctl->i2;
+    double now = 0.0;
+    while (R > 0) {
+        S.R = R;
+        // layers each MetaOp still owes (schedule.hpp:49-61)
+        if (lane == 0) {
+            for (int i = 0; i < R; ++i) sumlay[S.tk[i]] = 0;
+            for (int i = 0; i < R; ++i) sumlay[S.tk[i]] += S.tl[i];
+        }
+        __syncwarp();
+        int nbest;
+        if (all_defined && R <= 16) {
+            nbest = fast_wave(C, S);
+        } else {
+            if (lane == 0) C.ctl->i3 = ser_wave(C, S);
+            __syncwarp();
+            nbest = C.ctl->i3;
+        }
+        if (nbest < 0 || C.ctl->err) return false;
+        if (nW + 1 > W_CAP || nE + nbest > E_CAP) {
+            if (lane == 0) set_err(C.ctl, nW + 1 > W_CAP ? WS_E_LIMIT_WAVES : WS_E_LIMIT_ENTRIES);
+            __syncwarp();
+            return false;
+        }
+        // wave entries in selection order; duration = max span
+        double span = 0.0;
+        if (lane < nbest) {
+            const int t = best[lane];
+            const int k = S.tk[t];
+            const int kk = klay[lane];
+            span = kk * t_at(*C.F, S.T.gm_of[k], S.tn[t]);
+            e_k[nE + lane] = k;
+            e_n[nE + lane] = S.tn[t];
+            e_l[nE + lane] = kk;
+            e_span[nE + lane] = span;
+            // bookkeeping: own tuple pays its layers, the sibling covers the absorbed rest
+            int ab = kk - S.tl[t];
+            ab = ab > 0 ? ab : 0;
+            S.tl[t] -= kk - ab;
+            absorb[k] = ab;
+        }
+        const double dur = warp_max_d(span);
+        if (lane == 0) {
+            w_level[nW] = lvl;
+            w_eb[nW] = nE;
+            w_ec[nW] = nbest;
+            w_start[nW] = now + offset;  // merge_levels offset (schedule.hpp:292-309)
+            w_dur[nW] = dur;
+        }
+        ++nW;
+        nE += nbest;
+        now += dur;
+        __syncwarp();
+        // the sibling tuple (same MetaOp, not selected) gives up the absorbed layers
+        for (int j = lane; j < R; j += 32) {
+            const int kj = S.tk[j];
+            const int ab = absorb[kj];
+            bool selected = false;
+            for (int i = 0; i < nbest; ++i) selected |= best[i] == j;
+            if (ab > 0 && !selected) {
+                const int take = ab < S.tl[j] ? ab : S.tl[j];
+                S.tl[j] -= take;
+            }
+        }
+        __syncwarp();
+        for (int i = lane; i < nbest; i += 32) absorb[S.tk[best[i]]] = 0;
+        __syncwarp();
+        // compact the remaining tuples (order kept)
+        if (lane == 0) {
+            int R2 = 0;
+            for (int i = 0; i < R; ++i)
+                if (S.tl[i] > 0) S.tk[R2] = S.tk[i], S.tn[R2] = S.tn[i], S.tl[R2] = S.tl[i], ++R2;
+            if (R2 == R) set_err(C.ctl, WS_E_NO_PROGRESS);
+            C.ctl->i2 = R2;
+        }
+        __syncwarp();
+        if (C.ctl->err) return false;
+        R = C.ctl->i2;
+    }
+    // merge_levels: level end = max over its waves of start + duration
+    double le = offset;
+    for (int i = lane; i < nW; i += 32)
+        if (w_level[i] == lvl) {
+            const double e = w_start[i] + w_dur[i];
+            le = (le < e) ? e : le;
+        }
+    level_end = warp_max_d(le);
+    return true;
+}
+
+__global__ void __launch_bounds__(32 * kSchedWarps) k_sched(SchedArgs A) {
+    extern __shared__ __align__(16) char smem_dyn[];
+    __shared__ Ctl ctl_s[kSchedWarps];
+    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int slot = blockIdx.x * kSchedWarps + wid;
+    if (slot >= A.n_launch) return;
+    if (A.n_ids && slot >= *A.n_ids) return;
+    const int p = A.plan_ids[slot];
+    Ctl* ctl = &ctl_s[wid];
+    if (lane == 0) *ctl = Ctl{};
+    __syncwarp();
+    const ws_plan_rec& R = A.B.plans[p];
+    char* rec = A.recs + static_cast<int64_t>(A.rec_by_slot ? slot : p) * A.RL.bytes;
+    SchedHdr* hdr = reinterpret_cast<SchedHdr*>(rec + A.RL.hdr);
+    SCtx C;
+    C.B = &A.B;
+    C.R = &R;
+    C.F = &A.fit;
+    C.L = &A.SL;
+    C.sm = smem_dyn + wid * A.SL.bytes;
+    C.ctl = ctl;
+    C.lane = lane;
+    C.N = R.n_dev;
+    C.M = R.n_mod;
+    C.K = 0;
+    C.mbase = R.mod_begin;
+    bool ok = true;
+    if (R.n_mod == 0 && R.n_tasks == 0) {
+        ok = false;
+        if (lane == 0) ctl->err = WS_E_HOST_PRESET;
+    } else if (R.n_dev > WS_MAX_DEVICES) {
+        ok = false;
+        if (lane == 0) ctl->err = WS_E_LIMIT_DEVICES;
+    } else if (R.n_mod > A.M_cap) {
+        ok = false;
+        if (lane == 0) ctl->err = WS_E_LIMIT_MODULES;
+    }
+    __syncwarp();
+    if (ok) ok = s_graph(C);
+    if (ok) ok = s_fit_status(C);
+    if (ok) ok = s_valid(C);
+    int n_levels = 0, nW = 0, nE = 0;
+    double lower_bound = 0.0, offset = 0.0;
+    if (ok) {
+        n_levels = ctl->i1;
+        double* cstar = reinterpret_cast<double*>(rec + A.RL.cstar);
+        int* lfw = reinterpret_cast<int*>(rec + A.RL.lvl_fw);
+        int* lnw = reinterpret_cast<int*>(rec + A.RL.lvl_nw);
+        for (int l = 0; l < n_levels && ok; ++l) {
+            double cs = 0.0;
+            ok = s_level_alloc(C, l, cs);
+            if (!ok) break;
+            lower_bound += cs;  // planner.hpp:189
+            const int w0 = nW;
+            double level_end = offset;
+            ok = s_schedule_level(C, rec, A.RL, l, nW, nE, offset, level_end, A.caps.W, A.caps.E);
+            if (!ok) break;
+            if (lane == 0) {
+                cstar[l] = cs;
+                lfw[l] = w0;
+                lnw[l] = nW - w0;
+            }
+            offset = level_end;
+        }
+    }
+    if (!ok) {
+        if (lane == 0) {
+            write_error(A.results + p, ctl);
+            hdr->ok = 0;
+        }
+        return;
+    }
+    // hand the MetaOp tables to k_place / emit
+    const int K = C.K;
+    int* r_mod_of = reinterpret_cast<int*>(rec + A.RL.mod_of);
+    int* r_level = reinterpret_cast<int*>(rec + A.RL.level);
+    int* r_up_n = reinterpret_cast<int*>(rec + A.RL.up_n);
+    int* r_up_l = reinterpret_cast<int*>(rec + A.RL.up_l);
+    int* r_lo_n = reinterpret_cast<int*>(rec + A.RL.lo_n);
+    int* r_lo_l = reinterpret_cast<int*>(rec + A.RL.lo_l);
+    int* r_by_rank = reinterpret_cast<int*>(rec + A.RL.by_rank);
+    int* r_idrank = reinterpret_cast<int*>(rec + A.RL.idrank);
+    uint64_t* r_pred = reinterpret_cast<uint64_t*>(rec + A.RL.pred_r);
+    uint64_t* r_succ = reinterpret_cast<uint64_t*>(rec + A.RL.succ_r);
+    for (int k = lane; k < K; k += 32) {
+        r_mod_of[k] = C.at<int>(A.SL.mod_of)[k];
+        r_level[k] = C.at<int>(A.SL.level)[k];
+        r_up_n[k] = C.at<int>(A.SL.up_n)[k];
+        r_up_l[k] = C.at<int>(A.SL.up_l)[k];
+        r_lo_n[k] = C.at<int>(A.SL.lo_n)[k];
+        r_lo_l[k] = C.at<int>(A.SL.lo_l)[k];
+        r_by_rank[k] = C.at<int>(A.SL.by_rank)[k];
+        r_idrank[k] = C.at<int>(A.SL.idrank)[k];
+        r_pred[k] = C.at<uint64_t>(A.SL.pred_r)[k];
+        r_succ[k] = C.at<uint64_t>(A.SL.succ_r)[k];
+    }
+    if (lane == 0) {
+        SchedHdr h{};
+        h.ok = 1;
+        h.K = K;
+        h.n_levels = n_levels;
+        h.nW = nW;
+        h.nE = nE;
+        h.lower_bound = lower_bound;
+        h.end_time = offset;
+        *hdr = h;
+    }
+}
+
+}  // namespace wsdev
