@@ -243,7 +243,8 @@ int ws_fetch_results(ws_ctx* ctx, ws_plan_result* results, uint8_t* arena, uint6
 /* Number of kernel launches issued by the last ws_plan_staged / ws_plan_batch_host. */
 int ws_last_launch_count(const ws_ctx* ctx);
 /* Device time (ms) of each planner kernel in the last planning call, measured
- * with CUDA events on the launching stream: out[0]=fit, out[1]=plan. */
+ * with CUDA events on the launching stream: out[0]=k_fit, out[1]=k_sched,
+ * out[2]=k_place (including the soft-cap retry pass). */
 int ws_last_kernel_ms(const ws_ctx* ctx, double* out, int n);
 
 /* Global best candidate: on-device argmin of key over the staged

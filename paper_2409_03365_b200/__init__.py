@@ -12,7 +12,7 @@ import ctypes as C
 from pathlib import Path
 
 _PKG = Path(__file__).resolve().parent
-LIB_PATH = _PKG / "lib" / "libwsgpu.so"
+LIB_PATH = Path(__import__("os").environ.get("WSGPU_LIB", _PKG / "lib" / "libwsgpu.so"))
 
 __all__ = [
     "LIB_PATH", "Options", "PlanResult", "ProblemSet", "Planner", "plan_workload", "PlannerError",
@@ -328,10 +328,11 @@ class Planner:
     def launch_count(self) -> int:
         return lib.ws_last_launch_count(self._h)
 
-    def kernel_ms(self) -> tuple[float, float]:
-        buf = (C.c_double * 2)()
-        lib.ws_last_kernel_ms(self._h, buf, 2)
-        return buf[0], buf[1]
+    def kernel_ms(self) -> tuple[float, float, float]:
+        """Device ms of (k_fit, k_sched, k_place incl. retry) in the last call."""
+        buf = (C.c_double * 3)()
+        lib.ws_last_kernel_ms(self._h, buf, 3)
+        return buf[0], buf[1], buf[2]
 
 
 def plan_workload(workload: str, topology: str, **opts) -> str:

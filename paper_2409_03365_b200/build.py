@@ -47,25 +47,31 @@ def _stale(target: Path, deps: list[Path]) -> bool:
     return any(d.stat().st_mtime > t for d in deps)
 
 
-def build(verbose: bool = False, force: bool = False) -> Path:
-    """Compile host + device sources and link libwsgpu.so; returns its path."""
-    BUILD.mkdir(parents=True, exist_ok=True)
+def build(verbose: bool = False, force: bool = False, defines: list[str] | None = None,
+          name: str | None = None) -> Path:
+    """Compile host + device sources and link libwsgpu.so; returns its path.
+    `defines`/`name` build a tuning variant (e.g. ["WS_PLACE_MINB=6"], "libwsgpu_v6.so")
+    with its own object directory."""
+    libname = LIB / name if name else LIBNAME
+    build_dir = BUILD if not name else LIB / ("obj_" + Path(name).stem)
+    dflags = [f"-D{d}" for d in (defines or [])]
+    build_dir.mkdir(parents=True, exist_ok=True)
     headers = list((ROOT / "include").rglob("*.h*")) + list((CSRC / "device").glob("*.cuh"))
     objs = []
     for src in sorted((CSRC / "host").glob("*.cpp")):
-        obj = BUILD / (src.stem + ".o")
+        obj = build_dir / (src.stem + ".o")
         if force or _stale(obj, [src] + headers):
             _run(["g++", *CXX_FLAGS, "-c", str(src), "-o", str(obj)], verbose)
         objs.append(obj)
     for src in sorted((CSRC / "device").glob("*.cu")):
-        obj = BUILD / (src.stem + ".cu.o")
+        obj = build_dir / (src.stem + ".cu.o")
         if force or _stale(obj, [src] + headers):
-            _run([NVCC, *NVCC_FLAGS, "-Xptxas", "-v" if verbose else "-O3", "-c", str(src), "-o", str(obj)], verbose)
+            _run([NVCC, *NVCC_FLAGS, *dflags, "-Xptxas", "-v" if verbose else "-O3", "-c", str(src), "-o", str(obj)], verbose)
         objs.append(obj)
-    if force or _stale(LIBNAME, objs):
-        _run([NVCC, *ARCH, "-shared", "-o", str(LIBNAME), *map(str, objs), "-cudart", "static",
+    if force or _stale(libname, objs):
+        _run([NVCC, *ARCH, "-shared", "-o", str(libname), *map(str, objs), "-cudart", "static",
               "-Xlinker", "--no-undefined", "-lpthread", "-ldl", "-lrt"], verbose)
-    return LIBNAME
+    return libname
 
 
 if __name__ == "__main__":

@@ -512,7 +512,10 @@ __device__ void p_emit(PCtx& C, int p, const char* rec, const RecLayout& RL, con
     }
 }
 
-__global__ void __launch_bounds__(32 * kPlaceWarps) k_place(PlaceArgs A) {
+#ifndef WS_PLACE_MINB
+#define WS_PLACE_MINB 1  // measured: capping registers (spills) loses more than occupancy gains
+#endif
+__global__ void __launch_bounds__(32 * kPlaceWarps, WS_PLACE_MINB) k_place(PlaceArgs A) {
     extern __shared__ __align__(16) char smem_dyn[];
     __shared__ Ctl ctl_s[kPlaceWarps];
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;

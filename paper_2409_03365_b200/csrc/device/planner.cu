@@ -158,7 +158,7 @@ struct ws_ctx {
     uint64_t arena_cap = 0;
     int launches = 0;
     cudaEvent_t ev[4] = {};
-    double kernel_ms[2] = {0, 0};
+    double kernel_ms[3] = {0, 0, 0};  // k_fit, k_sched, k_place (+ retry pass)
 };
 
 namespace {
@@ -220,7 +220,8 @@ ws_batch rebase(const ws_batch& h, const void* hbase, char* dbase) {
 
 // launch k_sched + k_place over `n` slots (plan ids from `ids`, count optionally on device)
 int launch_pair(ws_ctx* ctx, cudaStream_t st, const LaunchCaps& lc, const FitOut& fo, const int32_t* ids,
-                const int32_t* n_ids, int n, bool by_slot, char* recs, uint64_t* flows) {
+                const int32_t* n_ids, int n, bool by_slot, char* recs, uint64_t* flows,
+                cudaEvent_t mid = nullptr) {
     if (n <= 0) return 0;
     const ws_batch& B = ctx->dview;
     SchedArgs S{};
@@ -241,6 +242,7 @@ int launch_pair(ws_ctx* ctx, cudaStream_t st, const LaunchCaps& lc, const FitOut
     CK(cudaFuncSetAttribute(k_sched, cudaFuncAttributeMaxDynamicSharedMemorySize, kSchedWarps * S.SL.bytes));
     k_sched<<<(n + kSchedWarps - 1) / kSchedWarps, 32 * kSchedWarps, kSchedWarps * S.SL.bytes, st>>>(S);
     ctx->launches++;
+    if (mid) CK(cudaEventRecord(mid, st));
 
     PlaceArgs P{};
     P.B = B;
@@ -298,7 +300,7 @@ int ws_last_launch_count(const ws_ctx* c) { return c ? c->launches : 0; }
 
 int ws_last_kernel_ms(const ws_ctx* c, double* out, int n) {
     if (!c) return 1;
-    for (int i = 0; i < n && i < 2; ++i) out[i] = c->kernel_ms[i];
+    for (int i = 0; i < n && i < 3; ++i) out[i] = c->kernel_ms[i];
     return 0;
 }
 
@@ -374,7 +376,7 @@ int ws_plan_staged(ws_ctx* ctx, void* stream) {
     }
     CK(cudaEventRecord(ctx->ev[1], st));
     if (launch_pair(ctx, st, lc, fo, ctx->order.as<int32_t>(), nullptr, P, false, ctx->recs.as<char>(),
-                    ctx->flows.as<uint64_t>()))
+                    ctx->flows.as<uint64_t>(), ctx->ev[3]))
         return 1;
     // retry pass: soft-cap overflows with the hard caps, count read on device
     auto* rcount = reinterpret_cast<int32_t*>(counters + 2);
@@ -402,8 +404,10 @@ int ws_fetch_results(ws_ctx* ctx, ws_plan_result* results, uint8_t* arena, uint6
     CK(cudaMemcpyAsync(&top, ctx->counters.p, sizeof(top), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     float ms = 0;
+    ctx->kernel_ms[1] = ctx->kernel_ms[2] = 0;
     if (cudaEventElapsedTime(&ms, ctx->ev[0], ctx->ev[1]) == cudaSuccess) ctx->kernel_ms[0] = ms;
-    if (cudaEventElapsedTime(&ms, ctx->ev[1], ctx->ev[2]) == cudaSuccess) ctx->kernel_ms[1] = ms;
+    if (P && cudaEventElapsedTime(&ms, ctx->ev[1], ctx->ev[3]) == cudaSuccess) ctx->kernel_ms[1] = ms;
+    if (P && cudaEventElapsedTime(&ms, ctx->ev[3], ctx->ev[2]) == cudaSuccess) ctx->kernel_ms[2] = ms;
     if (top > ctx->arena_cap) top = ctx->arena_cap;
     if (top > arena_cap) return fail(ctx, "ws_fetch_results: arena buffer too small");
     if (top) CK(cudaMemcpyAsync(arena, ctx->arena.p, top, cudaMemcpyDeviceToHost, st));

@@ -1107,7 +1107,10 @@ __device__ bool s_schedule_level(SCtx& C, char* rec, const RecLayout& RL, int lv
     return true;
 }
 
-__global__ void __launch_bounds__(32 * kSchedWarps) k_sched(SchedArgs A) {
+#ifndef WS_SCHED_MINB
+#define WS_SCHED_MINB 1  // measured: capping registers (spills) loses more than occupancy gains
+#endif
+__global__ void __launch_bounds__(32 * kSchedWarps, WS_SCHED_MINB) k_sched(SchedArgs A) {
     extern __shared__ __align__(16) char smem_dyn[];
     __shared__ Ctl ctl_s[kSchedWarps];
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;

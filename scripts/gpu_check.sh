@@ -14,11 +14,11 @@ if timeout 600 $NCU_CMD > $OUT/ncu_plain_$TAG.log 2>&1; then
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
       --log-file $OUT/launches_$TAG.csv $NCU_CMD > $OUT/ncu_launch_$TAG.log 2>&1
   echo "ncu launches rc=$?" | tee -a $OUT/summary_$TAG.txt
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_plan -s 4 -c 1 \
-      -o $OUT/kplan_$TAG $NCU_CMD > $OUT/ncu_full_$TAG.log 2>&1
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_place -s 4 -c 1 \
+      -o $OUT/kplace_$TAG $NCU_CMD > $OUT/ncu_full_$TAG.log 2>&1
   echo "ncu full rc=$?" | tee -a $OUT/summary_$TAG.txt
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_fit -s 4 -c 1 \
-      -o $OUT/kfit_$TAG $NCU_CMD > $OUT/ncu_fullfit_$TAG.log 2>&1
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_sched -s 4 -c 1 \
+      -o $OUT/ksched_$TAG $NCU_CMD > $OUT/ncu_fullfit_$TAG.log 2>&1
   echo "ncu fit rc=$?" | tee -a $OUT/summary_$TAG.txt
 fi
 tail -5 $OUT/pytest_gpu_$TAG.log
