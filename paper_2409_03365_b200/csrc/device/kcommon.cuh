@@ -106,7 +106,61 @@ __device__ __forceinline__ double inverse_exact(const double* __restrict__ pc, i
     return nmax;
 }
 
-// shard_moves (placement.hpp:74-103) on device-index bitmasks; isl = island id per device
+// inverse_exact with every target-independent term hoisted out of the
+// bisection loop (curves of <= 2 pieces kept in registers; longer curves use
+// the generic routine).  Same expressions, so the same doubles.
+struct InvPre {
+    int np;  // <= 0: generic path
+    const double* pc;
+    double c, w, nmax, last;
+    double lo[2], hi[2], lov[2], thr[2], b[2], base[2];
+    __device__ __forceinline__ void init(const double* pc_, int np_, double c_, double w_, double nmax_) {
+        pc = pc_;
+        c = c_;
+        w = w_;
+        nmax = nmax_;
+        if (np_ > 2) {
+            np = -np_;
+            return;
+        }
+        np = np_;
+        auto val = [&](int i, double n) {
+            return __ldg(pc + 5 * i + 2) + __ldg(pc + 5 * i + 3) * c + __ldg(pc + 5 * i + 4) * w / n;
+        };
+        last = val(np - 1, nmax);
+        for (int i = 0; i < np; ++i) {
+            lo[i] = __ldg(pc + 5 * i + 0);
+            hi[i] = __ldg(pc + 5 * i + 1);
+            const double hv = val(i, lo[i]);
+            thr[i] = hv + 1e-15 * fabs(hv);
+            lov[i] = val(i, hi[i]);
+            b[i] = __ldg(pc + 5 * i + 4) * w;
+            base[i] = __ldg(pc + 5 * i + 2) + __ldg(pc + 5 * i + 3) * c;
+        }
+    }
+    __device__ __forceinline__ double operator()(double target) const {
+        if (np <= 0) return inverse_exact(pc, -np, c, w, nmax, target);
+        if (target <= last) return nmax;
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+            if (i >= np) break;
+            if (target > thr[i]) {
+                if (b[i] <= 0.0) return 0.0;
+                return b[i] / (target - base[i]);
+            }
+            if (target >= lov[i]) {
+                if (b[i] <= 0.0) return lo[i];
+                if (target <= base[i]) return hi[i];
+                const double v = b[i] / (target - base[i]);
+                return v < lo[i] ? lo[i] : (hi[i] < v ? hi[i] : v);
+            }
+        }
+        return nmax;
+    }
+};
+
+// shard_moves (placement.hpp:74-103) on device-index bitmasks; isl = island id per device.
+// Unit i pairs sources[i % S] with targets[i % T] (both sorted by device id).
 __device__ __forceinline__ void shard_moves(uint64_t from, uint64_t to, uint64_t full, const int* isl,
                                             uint64_t& intra, uint64_t& inter) {
     intra = inter = 0;
@@ -121,8 +175,8 @@ __device__ __forceinline__ void shard_moves(uint64_t from, uint64_t to, uint64_t
     if (!dst) dst = to;
     const double unit_bytes = static_cast<double>(full) / static_cast<double>(units);
     const uint64_t bytes = static_cast<uint64_t>(llround(unit_bytes));
-    uint64_t rs = src, rt = dst;
     int same = 0;
+    uint64_t rs = src, rt = dst;
     for (int i = 0; i < moving; ++i) {
         const int s = low_bit(rs);
         rs &= rs - 1;

@@ -15,6 +15,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 #include <string>
@@ -31,6 +32,7 @@ namespace {
 constexpr int kRetryMax = 1024;               // plans re-run with hard caps per call
 constexpr int64_t kOverflowPieces = 1 << 18;  // isotonic/long curves
 constexpr int kSmemLimit = 227 * 1024;
+constexpr int kMaxChunks = 16;  // k_sched/k_place pipeline depth
 
 struct DevBuf {
     void* p = nullptr;
@@ -158,6 +160,9 @@ struct ws_ctx {
     uint64_t arena_cap = 0;
     int launches = 0;
     cudaEvent_t ev[4] = {};
+    cudaStream_t stream2 = nullptr;             // k_place side of the pipeline
+    cudaEvent_t cev[kMaxChunks + 2] = {};       // chunk hand-offs + fork/join
+    int chunks = 8;
     double kernel_ms[3] = {0, 0, 0};  // k_fit, k_sched, k_place (+ retry pass)
 };
 
@@ -218,10 +223,21 @@ ws_batch rebase(const ws_batch& h, const void* hbase, char* dbase) {
     return d;
 }
 
-// launch k_sched + k_place over `n` slots (plan ids from `ids`, count optionally on device)
+// launch k_sched + k_place over `n` slots (plan ids from `ids`, count optionally
+// on device).  With chunks > 1 the slots are split into consecutive chunks and
+// k_place(chunk c) on a second stream overlaps k_sched(chunk c+1): the two
+// kernels share the SMs, so each SM has more resident warps to hide latency.
 int launch_pair(ws_ctx* ctx, cudaStream_t st, const LaunchCaps& lc, const FitOut& fo, const int32_t* ids,
                 const int32_t* n_ids, int n, bool by_slot, char* recs, uint64_t* flows,
-                cudaEvent_t mid = nullptr) {
+                cudaEvent_t mid = nullptr, int chunks = 1);
+
+}  // namespace
+
+namespace {
+
+int launch_pair(ws_ctx* ctx, cudaStream_t st, const LaunchCaps& lc, const FitOut& fo, const int32_t* ids,
+                const int32_t* n_ids, int n, bool by_slot, char* recs, uint64_t* flows, cudaEvent_t mid,
+                int chunks) {
     if (n <= 0) return 0;
     const ws_batch& B = ctx->dview;
     SchedArgs S{};
@@ -231,18 +247,12 @@ int launch_pair(ws_ctx* ctx, cudaStream_t st, const LaunchCaps& lc, const FitOut
     S.RL = make_rec_layout(lc.rec);
     S.SL = make_sm_layout(lc.M);
     S.recs = recs;
-    S.plan_ids = ids;
     S.n_ids = n_ids;
-    S.n_launch = n;
     S.rec_by_slot = by_slot ? 1 : 0;
     S.M_cap = lc.M;
     S.results = ctx->results.as<ws_plan_result>();
-    const int sw = warps_for(S.SL.bytes, kSchedWarps);
-    if (sw * S.SL.bytes > kSmemLimit) return fail(ctx, "k_sched working set exceeds shared memory");
+    if (kSchedWarps * S.SL.bytes > kSmemLimit) return fail(ctx, "k_sched working set exceeds shared memory");
     CK(cudaFuncSetAttribute(k_sched, cudaFuncAttributeMaxDynamicSharedMemorySize, kSchedWarps * S.SL.bytes));
-    k_sched<<<(n + kSchedWarps - 1) / kSchedWarps, 32 * kSchedWarps, kSchedWarps * S.SL.bytes, st>>>(S);
-    ctx->launches++;
-    if (mid) CK(cudaEventRecord(mid, st));
 
     PlaceArgs P{};
     P.B = B;
@@ -252,9 +262,7 @@ int launch_pair(ws_ctx* ctx, cudaStream_t st, const LaunchCaps& lc, const FitOut
     P.PL = make_pl_layout(lc.pl);
     P.recs = recs;
     P.flows = flows;
-    P.plan_ids = ids;
     P.n_ids = n_ids;
-    P.n_launch = n;
     P.rec_by_slot = by_slot ? 1 : 0;
     P.results = ctx->results.as<ws_plan_result>();
     P.arena = ctx->arena.as<uint8_t>();
@@ -262,8 +270,39 @@ int launch_pair(ws_ctx* ctx, cudaStream_t st, const LaunchCaps& lc, const FitOut
     P.arena_cap = ctx->arena_cap;
     if (kPlaceWarps * P.PL.bytes > kSmemLimit) return fail(ctx, "k_place working set exceeds shared memory");
     CK(cudaFuncSetAttribute(k_place, cudaFuncAttributeMaxDynamicSharedMemorySize, kPlaceWarps * P.PL.bytes));
-    k_place<<<(n + kPlaceWarps - 1) / kPlaceWarps, 32 * kPlaceWarps, kPlaceWarps * P.PL.bytes, st>>>(P);
-    ctx->launches++;
+
+    chunks = std::max(1, std::min(chunks, kMaxChunks));
+    if (n_ids || n < 4096) chunks = 1;  // retry pass / small batches: no pipelining
+    const int cs = (n + chunks - 1) / chunks;
+    cudaStream_t sb = chunks > 1 ? ctx->stream2 : st;
+    if (chunks > 1) {
+        CK(cudaEventRecord(ctx->cev[kMaxChunks], st));
+        CK(cudaStreamWaitEvent(sb, ctx->cev[kMaxChunks], 0));
+    }
+    for (int c = 0; c < chunks; ++c) {
+        const int base = c * cs;
+        const int cnt = std::min(cs, n - base);
+        if (cnt <= 0) break;
+        S.plan_ids = ids + base;
+        S.n_launch = cnt;
+        k_sched<<<(cnt + kSchedWarps - 1) / kSchedWarps, 32 * kSchedWarps, kSchedWarps * S.SL.bytes, st>>>(S);
+        ctx->launches++;
+        if (chunks > 1) {
+            CK(cudaEventRecord(ctx->cev[c], st));
+            CK(cudaStreamWaitEvent(sb, ctx->cev[c], 0));
+        } else if (mid) {
+            CK(cudaEventRecord(mid, st));
+        }
+        P.plan_ids = ids + base;
+        P.n_launch = cnt;
+        k_place<<<(cnt + kPlaceWarps - 1) / kPlaceWarps, 32 * kPlaceWarps, kPlaceWarps * P.PL.bytes, sb>>>(P);
+        ctx->launches++;
+    }
+    if (chunks > 1) {
+        if (mid) CK(cudaEventRecord(mid, st));  // end of the last k_sched chunk
+        CK(cudaEventRecord(ctx->cev[kMaxChunks + 1], sb));
+        CK(cudaStreamWaitEvent(st, ctx->cev[kMaxChunks + 1], 0));
+    }
     return 0;
 }
 
@@ -281,6 +320,12 @@ int ws_ctx_create(int device, ws_ctx** out) {
         return 1;
     }
     for (auto& e : c->ev) cudaEventCreate(&e);
+    for (auto& e : c->cev) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+    if (cudaStreamCreateWithFlags(&c->stream2, cudaStreamNonBlocking) != cudaSuccess) {
+        delete c;
+        return 1;
+    }
+    if (const char* env = std::getenv("WSGPU_CHUNKS")) c->chunks = std::atoi(env);
     *out = c;
     return 0;
 }
@@ -290,7 +335,10 @@ void ws_ctx_destroy(ws_ctx* c) {
     cudaSetDevice(c->device);
     for (auto& e : c->ev)
         if (e) cudaEventDestroy(e);
+    for (auto& e : c->cev)
+        if (e) cudaEventDestroy(e);
     if (c->stream) cudaStreamDestroy(c->stream);
+    if (c->stream2) cudaStreamDestroy(c->stream2);
     delete c;
 }
 
@@ -376,7 +424,7 @@ int ws_plan_staged(ws_ctx* ctx, void* stream) {
     }
     CK(cudaEventRecord(ctx->ev[1], st));
     if (launch_pair(ctx, st, lc, fo, ctx->order.as<int32_t>(), nullptr, P, false, ctx->recs.as<char>(),
-                    ctx->flows.as<uint64_t>(), ctx->ev[3]))
+                    ctx->flows.as<uint64_t>(), ctx->ev[3], ctx->chunks))
         return 1;
     // retry pass: soft-cap overflows with the hard caps, count read on device
     auto* rcount = reinterpret_cast<int32_t*>(counters + 2);

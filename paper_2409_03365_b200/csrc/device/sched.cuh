@@ -404,7 +404,9 @@ __device__ bool s_valid(SCtx& C) {
         for (int base = 0; base < N; base += 32) {
             const int n = base + lane + 1;
             bool ok = n <= N && n % tp == 0;
-            if (ok) ok = batch % (n / tp) == 0;
+            if (ok)  // 32-bit remainder when the batch fits (same result, fewer instructions)
+                ok = batch <= 0xffffffffll ? (static_cast<unsigned>(batch) % static_cast<unsigned>(n / tp)) == 0u
+                                           : batch % (n / tp) == 0;
             v |= static_cast<uint64_t>(__ballot_sync(kFull, ok)) << base;
         }
         if (lane == 0) valid[k] = v;
@@ -440,9 +442,9 @@ __device__ bool s_level_alloc(SCtx& C, int lvl, double& c_star_out) {
     const double nd = static_cast<double>(N);
     const FitOut& F = *C.F;
     struct Mem {
-        int k, gm, L, np;
-        const double* pc;
-        double c, w, nmax;
+        int k, gm, L;
+        double nmax;
+        InvPre inv;
     } mem[2];
     for (int s = 0; s < 2; ++s) {
         const int i = lane + 32 * s;
@@ -452,11 +454,8 @@ __device__ bool s_level_alloc(SCtx& C, int lvl, double& c_star_out) {
             q.k = lm[i];
             q.gm = gm_of[q.k];
             q.L = Lk[q.k];
-            q.np = F.npieces[q.gm];
-            q.pc = F.pieces + 5 * F.piece_off[q.gm];
-            q.c = B.mod_c[q.gm];
-            q.w = B.mod_w[q.gm];
             q.nmax = nmax_of[q.k];
+            q.inv.init(F.pieces + 5 * F.piece_off[q.gm], F.npieces[q.gm], B.mod_c[q.gm], B.mod_w[q.gm], q.nmax);
         }
     }
     // bracket [max T(min(N,nmax))*L, sum T(1)*L] (allocation.hpp:75-80)
@@ -472,7 +471,7 @@ __device__ bool s_level_alloc(SCtx& C, int lvl, double& c_star_out) {
     double c_lo = warp_max_d(lo0);
     double c_hi = ordered_sum(hi0[0], hi0[1], w);
     auto probe_term = [&](const Mem& q, double cc) {
-        const double v = inverse_exact(q.pc, q.np, q.c, q.w, q.nmax, cc / q.L);
+        const double v = q.inv(cc / q.L);
         return (nd < v) ? nd : v;  // std::min(v, N)
     };
     for (int it = 0; it < R.max_iters && (c_hi - c_lo) > R.eps * c_hi; ++it) {
@@ -795,6 +794,50 @@ __device__ int ser_wave(SCtx& C, SchedView& S) {
     return C.ctl->err ? -1 : nbest;
 }
 
+// argmax over candidate lanes of (rem desc, id asc) with single-instruction
+// warp reductions: rem > 0, so its IEEE bits order like its value.
+__device__ __forceinline__ int warp_argmax_rem(bool cand, double rem, int idr) {
+    if (!__any_sync(kFull, cand)) return -1;
+    const uint64_t bits = static_cast<uint64_t>(__double_as_longlong(rem));
+    const unsigned hi = cand ? static_cast<unsigned>(bits >> 32) : 0u;
+    const unsigned mh = __reduce_max_sync(kFull, hi);
+    const bool e1 = cand && hi == mh;
+    const unsigned lo = static_cast<unsigned>(bits);
+    const unsigned ml = __reduce_max_sync(kFull, e1 ? lo : 0u);
+    const bool e2 = e1 && lo == ml;
+    const unsigned mi = __reduce_min_sync(kFull, e2 ? static_cast<unsigned>(idr) : 0xffffffffu);
+    return __ffs(__ballot_sync(kFull, e2 && static_cast<unsigned>(idr) == mi)) - 1;
+}
+
+// extend_resources_if_needed (schedule.hpp:144-173), lanes = selected tuples:
+// grow the tuple whose MetaOp has the most remaining time to its next valid
+// allocation while idle devices remain.
+__device__ __forceinline__ int ext_lanes(bool in, int n, int N, uint64_t vmask, int sl, int idr, const FitOut& F,
+                                         int gm) {
+    const int lane = threadIdx.x & 31;
+    while (true) {
+        const int idle = N - static_cast<int>(__reduce_add_sync(kFull, in ? static_cast<unsigned>(n) : 0u));
+        if (idle <= 0) break;
+        bool cand = false;
+        int nx = 0;
+        double rem = 0.0;
+        if (in) {
+            const uint64_t above = vmask & ~bits_upto(n - 1);
+            if (above) {
+                nx = low_bit(above) + 1;
+                if (nx - n <= idle) {
+                    cand = true;
+                    rem = sl * t_at(F, gm, n);
+                }
+            }
+        }
+        const int win = warp_argmax_rem(cand, rem, idr);
+        if (win < 0) break;
+        if (lane == win) n = nx;
+    }
+    return n;
+}
+
 // Fast path (R <= 16 tuples, every curve defined up to N): lanes = tuples.
 // Stable ranks reproduce std::sort exactly for <= 16 elements (insertion
 // sort); greedy runs warp-uniformly; extension/alignment are lane-parallel.
@@ -867,37 +910,10 @@ __device__ int fast_wave(SCtx& C, SchedView& S) {
             if (t == lane) mypos = ns;
             ++ns;
         }
-        // scratch extension (schedule.hpp:126-131): lane-parallel argmax loop
-        int n = n0;
+        // scratch extension (schedule.hpp:126-131)
         const bool in = (sel >> lane) & 1u;
-        while (true) {
-            const int idle = N - warp_sum(in ? n : 0);
-            if (idle <= 0) break;
-            double rem = -1.0;
-            int cand = 0, nx = 0;
-            if (in) {
-                const uint64_t above = vmask & ~bits_upto(n - 1);
-                if (above) {
-                    nx = low_bit(above) + 1;
-                    if (nx - n <= idle) {
-                        cand = 1;
-                        rem = sl * t_at(F, gm, n);
-                    }
-                }
-            }
-            // argmax rem, ties -> smaller id
-            double br = rem;
-            int bi = cand ? idr : 0x7fffffff, bl = cand ? lane : -1;
-            for (int off = 16; off; off >>= 1) {
-                const double orr = __shfl_xor_sync(kFull, br, off);
-                const int oi = __shfl_xor_sync(kFull, bi, off);
-                const int ol = __shfl_xor_sync(kFull, bl, off);
-                if (ol >= 0 && (bl < 0 || orr > br || (orr == br && oi < bi))) br = orr, bi = oi, bl = ol;
-            }
-            if (bl < 0) break;
-            if (lane == bl) n = nx;
-        }
-        const int usedn = warp_sum(in ? n : 0);
+        const int n = ext_lanes(in, n0, N, vmask, sl, idr, F, gm);
+        const int usedn = static_cast<int>(__reduce_add_sync(kFull, in ? static_cast<unsigned>(n) : 0u));
         const long long key = static_cast<long long>(usedn) * 1000 + ns;
         if (key > best_key) {
             best_key = key;
@@ -913,33 +929,7 @@ __device__ int fast_wave(SCtx& C, SchedView& S) {
     }
     // real extension on the chosen set
     const bool in = (best_sel >> lane) & 1u;
-    int n = n0;
-    while (true) {
-        const int idle = N - warp_sum(in ? n : 0);
-        if (idle <= 0) break;
-        double rem = -1.0;
-        int cand = 0, nx = 0;
-        if (in) {
-            const uint64_t above = vmask & ~bits_upto(n - 1);
-            if (above) {
-                nx = low_bit(above) + 1;
-                if (nx - n <= idle) {
-                    cand = 1;
-                    rem = sl * t_at(F, gm, n);
-                }
-            }
-        }
-        double br = rem;
-        int bi = cand ? idr : 0x7fffffff, bl = cand ? lane : -1;
-        for (int off = 16; off; off >>= 1) {
-            const double orr = __shfl_xor_sync(kFull, br, off);
-            const int oi = __shfl_xor_sync(kFull, bi, off);
-            const int ol = __shfl_xor_sync(kFull, bl, off);
-            if (ol >= 0 && (bl < 0 || orr > br || (orr == br && oi < bi))) br = orr, bi = oi, bl = ol;
-        }
-        if (bl < 0) break;
-        if (lane == bl) n = nx;
-    }
+    const int n = ext_lanes(in, n0, N, vmask, sl, idr, F, gm);
     if (mine) S.tn[lane] = n;
     // align_time_span: t_wave = min span over the chosen set
     const double per = in ? t_at(F, gm, n) : 0.0;
@@ -1107,10 +1097,12 @@ __device__ bool s_schedule_level(SCtx& C, char* rec, const RecLayout& RL, int lv
     return true;
 }
 
-#ifndef WS_SCHED_MINB
-#define WS_SCHED_MINB 1  // measured: capping registers (spills) loses more than occupancy gains
-#endif
+// WS_SCHED_MINB: optional resident-blocks target for register tuning builds
+#ifdef WS_SCHED_MINB
 __global__ void __launch_bounds__(32 * kSchedWarps, WS_SCHED_MINB) k_sched(SchedArgs A) {
+#else
+__global__ void __launch_bounds__(32 * kSchedWarps) k_sched(SchedArgs A) {
+#endif
     extern __shared__ __align__(16) char smem_dyn[];
     __shared__ Ctl ctl_s[kSchedWarps];
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
