@@ -162,7 +162,7 @@ struct ws_ctx {
     cudaEvent_t ev[4] = {};
     cudaStream_t stream2 = nullptr;             // k_place side of the pipeline
     cudaEvent_t cev[kMaxChunks + 2] = {};       // chunk hand-offs + fork/join
-    int chunks = 8;
+    int chunks = 1;  // measured: concurrent k_sched/k_place chunks share the I-cache and lose ($WSGPU_CHUNKS)
     double kernel_ms[3] = {0, 0, 0};  // k_fit, k_sched, k_place (+ retry pass)
 };
 
