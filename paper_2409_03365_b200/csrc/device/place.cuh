@@ -28,6 +28,7 @@ struct PlSmLayout {
     int chg;                                                      // [G] u64
     int fin_src, fin_bytes;                                       // [M+1]
     int disp_mask, disp_bytes, disp_cnt, eorder, va;              // [M]
+    int cmask;                                                    // [2N+M+1] candidate device sets
     int bytes;
 };
 
@@ -76,6 +77,7 @@ __host__ __device__ inline PlSmLayout make_pl_layout(const PlaceCaps& c) {
     L.disp_cnt = take(4 * M);
     L.eorder = take(4 * M);
     L.va = take(8 * M);
+    L.cmask = take(8 * (2 * N + M + 1));
     L.bytes = (o + 15) & ~15;
     return L;
 }
@@ -106,6 +108,7 @@ struct PCtx {
     char* sm;
     Ctl* ctl;
     int lane, N, K, mbase, nW, nE, nF, Fcap, G, n_isl;
+    int contig;  // every island is one contiguous run of device indices
     uint64_t all;
     uint64_t* flows;  // this plan's flow list (2 words per flow)
     template <typename T>
@@ -293,24 +296,46 @@ __device__ int p_wave(PCtx& C, int w, int variant) {
                 }
                 total += nfree - n + 1;
                 __syncwarp();
+                // compact the candidate list first (ballot + popc), so lanes score
+                // in lockstep: skipping inside the scoring loop would split the warp
+                uint64_t* cmask = C.at<uint64_t>(L.cmask);
+                int ncand = 0;
+                for (int base = 0; base < total; base += 32) {
+                    const int j = base + lane;
+                    uint64_t m = 0;
+                    bool keep = false;
+                    if (j < nfin) {
+                        m = e_mask[fin_src[j]];
+                        keep = popc64(m) == n && !(m & ~free);
+                    } else if (j < total) {
+                        int r = j - nfin;
+                        int i = 0;
+                        for (; i < C.n_isl && r >= nwin[i]; ++i) r -= nwin[i];
+                        keep = true;
+                        if (i < C.n_isl) {
+                            m = window_mask(free & islmask[i], r, n);
+                        } else {
+                            m = window_mask(free, r, n);
+                            // with contiguous islands a global window inside one island is
+                            // that island's window at the same offset: a duplicate (:232)
+#ifndef WS_NO_DEDUP
+                            keep = !(C.contig && !(m & ~islmask[isl[low_bit(m)]]));
+#endif
+                        }
+                    }
+                    const unsigned bal = __ballot_sync(kFull, keep);
+                    if (keep) cmask[ncand + __popc(bal & ((1u << lane) - 1u))] = m;
+                    ncand += __popc(bal);
+                }
+                __syncwarp();
                 const int rounds = oi == 0 ? variant + 1 : 1;  // first entry takes scores[variant]
                 Score prev;
                 prev.valid = 0;
                 for (int rd = 0; rd < rounds; ++rd) {
                     Score best;
                     best.valid = 0;
-                    for (int j = lane; j < total; j += 32) {
-                        uint64_t m;
-                        if (j < nfin) {
-                            m = e_mask[fin_src[j]];
-                            if (popc64(m) != n || (m & ~free)) continue;
-                        } else {
-                            int r = j - nfin;
-                            int i = 0;
-                            for (; i < C.n_isl && r >= nwin[i]; ++i) r -= nwin[i];
-                            m = i < C.n_isl ? window_mask(free & islmask[i], r, n) : window_mask(free, r, n);
-                        }
-                        const Score s = score_of(m, 0);
+                    for (int j = lane; j < ncand; j += 32) {
+                        const Score s = score_of(cmask[j], 0);
                         if (prev.valid && !score_less(prev, s)) continue;  // next distinct rank
                         if (!best.valid || score_less(s, best)) best = s;
                     }
@@ -648,8 +673,16 @@ __global__ void __launch_bounds__(32 * kPlaceWarps, WS_PLACE_MINB) k_place(Place
                 cur = (cur + e_n[e]) % N;
             }
         }
+        int contig = 1;
+        for (int i = 0; i < C.n_isl; ++i) {
+            const uint64_t m = islmask[i];
+            const uint64_t run = m ? m >> low_bit(m) : 0;
+            if (!m || (run & (run + 1))) contig = 0;
+        }
+        ctl->i0 = contig;
     }
     __syncwarp();
+    C.contig = ctl->i0;
     // depth-first search over per-wave variants with a bounded attempt budget (:409-441).
     // The reference copies the whole state per placed wave; here the state
     // before wave k is rebuilt on demand by replaying the committed entries of
