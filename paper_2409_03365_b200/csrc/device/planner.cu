@@ -109,9 +109,10 @@ struct LaunchCaps {
     int M;
 };
 
-LaunchCaps batch_caps(const std::vector<ws_plan_rec>& plans, bool hard) {
+LaunchCaps batch_caps(const ws_plan_rec* plans, int P, bool hard) {
     int M = 1, N = 1, IS = 1, gmax = 0;
-    for (const ws_plan_rec& r : plans) {
+    for (int p = 0; p < P; ++p) {
+        const ws_plan_rec& r = plans[p];
         M = std::max(M, r.n_mod);
         N = std::max(N, r.n_dev);
         IS = std::max(IS, r.n_islands);
@@ -151,7 +152,7 @@ struct ws_ctx {
     // staged batch
     DevBuf blob, order;
     ws_batch dview{};
-    std::vector<ws_plan_rec> host_plans;
+    std::vector<int32_t> order_host, key_count;  // launch order (pageable: copied before the call returns)
     LaunchCaps caps{}, caps_hard{};
     // K2 outputs
     DevBuf fit_err, fit_a, fit_b, fit_np, fit_nmax, fit_off, fit_pieces, ttab;
@@ -164,6 +165,14 @@ struct ws_ctx {
     cudaEvent_t cev[kMaxChunks + 2] = {};       // chunk hand-offs + fork/join
     int chunks = 1;  // measured: concurrent k_sched/k_place chunks share the I-cache and lose ($WSGPU_CHUNKS)
     double kernel_ms[3] = {0, 0, 0};  // k_fit, k_sched, k_place (+ retry pass)
+    // direct output: kernels write headers/records straight into the caller's
+    // page-locked host buffers (zero-copy), set only inside ws_plan_batch_host
+    ws_plan_result* d_results = nullptr;
+    uint8_t* d_arena = nullptr;
+    uint64_t d_cap = 0;
+    ws_plan_result* res_out() { return d_results ? d_results : results.as<ws_plan_result>(); }
+    uint8_t* arena_out() { return d_arena ? d_arena : arena.as<uint8_t>(); }
+    uint64_t cap_out() const { return d_arena ? d_cap : arena_cap; }
 };
 
 namespace {
@@ -250,7 +259,7 @@ int launch_pair(ws_ctx* ctx, cudaStream_t st, const LaunchCaps& lc, const FitOut
     S.n_ids = n_ids;
     S.rec_by_slot = by_slot ? 1 : 0;
     S.M_cap = lc.M;
-    S.results = ctx->results.as<ws_plan_result>();
+    S.results = ctx->res_out();
     if (kSchedWarps * S.SL.bytes > kSmemLimit) return fail(ctx, "k_sched working set exceeds shared memory");
     CK(cudaFuncSetAttribute(k_sched, cudaFuncAttributeMaxDynamicSharedMemorySize, kSchedWarps * S.SL.bytes));
 
@@ -264,10 +273,10 @@ int launch_pair(ws_ctx* ctx, cudaStream_t st, const LaunchCaps& lc, const FitOut
     P.flows = flows;
     P.n_ids = n_ids;
     P.rec_by_slot = by_slot ? 1 : 0;
-    P.results = ctx->results.as<ws_plan_result>();
-    P.arena = ctx->arena.as<uint8_t>();
+    P.results = ctx->res_out();
+    P.arena = ctx->arena_out();
     P.arena_top = ctx->counters.as<unsigned long long>();
-    P.arena_cap = ctx->arena_cap;
+    P.arena_cap = ctx->cap_out();
     if (kPlaceWarps * P.PL.bytes > kSmemLimit) return fail(ctx, "k_place working set exceeds shared memory");
     CK(cudaFuncSetAttribute(k_place, cudaFuncAttributeMaxDynamicSharedMemorySize, kPlaceWarps * P.PL.bytes));
 
@@ -361,21 +370,23 @@ int ws_stage_batch(ws_ctx* ctx, const ws_batch* in, void* stream) {
         return fail(ctx, "cudaMalloc batch");
     CK(cudaMemcpyAsync(ctx->blob.p, in->blob, in->blob_bytes, cudaMemcpyHostToDevice, st));
     ctx->dview = rebase(*in, in->blob, ctx->blob.as<char>());
-    ctx->host_plans.assign(in->plans, in->plans + P);
-    ctx->caps = batch_caps(ctx->host_plans, false);
-    ctx->caps_hard = batch_caps(ctx->host_plans, true);
+    ctx->caps = batch_caps(in->plans, P, false);
+    ctx->caps_hard = batch_caps(in->plans, P, true);
     ctx->arena_cap = ws_arena_bound(in);
-    // longest-processing-time launch order: descending modules x devices
-    static thread_local std::vector<int32_t> order;
-    order.resize(P);
-    std::iota(order.begin(), order.end(), 0);
-    std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t b) {
-        const ws_plan_rec& x = ctx->host_plans[a];
-        const ws_plan_rec& y = ctx->host_plans[b];
-        return x.n_mod * (x.n_dev + 8) > y.n_mod * (y.n_dev + 8);
-    });
-    if (P) CK(cudaMemcpyAsync(ctx->order.p, order.data(), 4ull * P, cudaMemcpyHostToDevice, st));
-    CK(cudaStreamSynchronize(st));  // `order` is reused by the next stage call
+    // longest-processing-time launch order: descending modules x devices, by a
+    // stable counting sort over the small key range (O(plans) on the host)
+    constexpr int kKeys = (WS_MAX_MODULES + 1) * (WS_MAX_DEVICES + 9);
+    auto key = [&](int p) {
+        const ws_plan_rec& r = in->plans[p];
+        const int m = std::min(std::max(r.n_mod, 0), WS_MAX_MODULES), d = std::min(std::max(r.n_dev, 0), WS_MAX_DEVICES);
+        return kKeys - 1 - m * (d + 8);
+    };
+    ctx->order_host.resize(P);
+    ctx->key_count.assign(kKeys + 1, 0);
+    for (int p = 0; p < P; ++p) ctx->key_count[key(p) + 1]++;
+    for (int k = 0; k < kKeys; ++k) ctx->key_count[k + 1] += ctx->key_count[k];
+    for (int p = 0; p < P; ++p) ctx->order_host[ctx->key_count[key(p)]++] = p;
+    if (P) CK(cudaMemcpyAsync(ctx->order.p, ctx->order_host.data(), 4ull * P, cudaMemcpyHostToDevice, st));
     return 0;
 }
 
@@ -429,7 +440,7 @@ int ws_plan_staged(ws_ctx* ctx, void* stream) {
     // retry pass: soft-cap overflows with the hard caps, count read on device
     auto* rcount = reinterpret_cast<int32_t*>(counters + 2);
     if (P > 0) {
-        k_soft_collect<<<(P + 255) / 256, 256, 0, st>>>(ctx->results.as<ws_plan_result>(), P,
+        k_soft_collect<<<(P + 255) / 256, 256, 0, st>>>(ctx->res_out(), P,
                                                          ctx->retry_ids.as<int32_t>(), rcount);
         k_clamp_count<<<1, 1, 0, st>>>(rcount);
         ctx->launches += 2;
@@ -464,11 +475,47 @@ int ws_fetch_results(ws_ctx* ctx, ws_plan_result* results, uint8_t* arena, uint6
     return 0;
 }
 
+namespace {
+void* mapped_device_ptr(void* host) {  // device alias of page-locked host memory, else null
+    cudaPointerAttributes a{};
+    if (!host || cudaPointerGetAttributes(&a, host) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    return a.type == cudaMemoryTypeHost ? a.devicePointer : nullptr;
+}
+}  // namespace
+
 int ws_plan_batch_host(ws_ctx* ctx, const ws_batch* in, ws_plan_result* results, uint8_t* arena,
                        uint64_t arena_cap, uint64_t* arena_used, void* stream) {
-    if (ws_stage_batch(ctx, in, stream)) return 1;
-    if (ws_plan_staged(ctx, stream)) return 1;
-    return ws_fetch_results(ctx, results, arena, arena_cap, arena_used, stream);
+    cudaSetDevice(ctx->device);
+    void* dres = mapped_device_ptr(results);
+    void* dar = mapped_device_ptr(arena);
+    if (!dres || !dar || in->n_plans == 0) {  // pageable buffers: stage, plan, copy back
+        if (ws_stage_batch(ctx, in, stream)) return 1;
+        if (ws_plan_staged(ctx, stream)) return 1;
+        return ws_fetch_results(ctx, results, arena, arena_cap, arena_used, stream);
+    }
+    // page-locked buffers: the kernels write headers and records straight to the
+    // host (PCIe/C2C writes overlap the planning), only the arena top comes back
+    cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
+    ctx->d_results = static_cast<ws_plan_result*>(dres);
+    ctx->d_arena = static_cast<uint8_t*>(dar);
+    ctx->d_cap = arena_cap;
+    int rc = ws_stage_batch(ctx, in, stream);
+    if (!rc) rc = ws_plan_staged(ctx, stream);
+    ctx->d_results = nullptr;
+    ctx->d_arena = nullptr;
+    if (rc) return rc;
+    unsigned long long top = 0;
+    CK(cudaMemcpyAsync(&top, ctx->counters.p, sizeof(top), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    float ms = 0;
+    if (cudaEventElapsedTime(&ms, ctx->ev[0], ctx->ev[1]) == cudaSuccess) ctx->kernel_ms[0] = ms;
+    if (cudaEventElapsedTime(&ms, ctx->ev[1], ctx->ev[3]) == cudaSuccess) ctx->kernel_ms[1] = ms;
+    if (cudaEventElapsedTime(&ms, ctx->ev[3], ctx->ev[2]) == cudaSuccess) ctx->kernel_ms[2] = ms;
+    *arena_used = top < arena_cap ? top : arena_cap;
+    return 0;
 }
 
 int ws_best_staged(ws_ctx* ctx, int mode, double* key, int64_t* index, void* stream) {
