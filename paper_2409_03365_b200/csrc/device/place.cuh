@@ -538,7 +538,7 @@ __device__ void p_emit(PCtx& C, int p, const char* rec, const RecLayout& RL, con
 }
 
 #ifndef WS_PLACE_MINB
-#define WS_PLACE_MINB 1  // measured: capping registers (spills) loses more than occupancy gains
+#define WS_PLACE_MINB 3  // measured sweep 1/2/3/4: 3 blocks (<=170 regs) is fastest
 #endif
 __global__ void __launch_bounds__(32 * kPlaceWarps, WS_PLACE_MINB) k_place(PlaceArgs A) {
     extern __shared__ __align__(16) char smem_dyn[];

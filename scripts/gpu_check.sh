@@ -9,9 +9,9 @@ nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > $O
 timeout 900 python -m pytest tests -m gpu -x -q > $OUT/pytest_gpu_$TAG.log 2>&1; echo "pytest gpu rc=$?" | tee -a $OUT/summary_$TAG.txt
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke_$TAG.log 2>&1; echo "smoke rc=$?" | tee -a $OUT/summary_$TAG.txt
 timeout 900 python bench.py --steps 10 --warmup 3 > $OUT/bench_$TAG.json 2> $OUT/bench_$TAG.err; echo "bench rc=$?" | tee -a $OUT/summary_$TAG.txt
-NCU_CMD="python bench.py --steps 2 --warmup 3 --mixtures 20000 --no-cpu-baseline --latency-reps 2"
+NCU_CMD="python bench.py --steps 1 --warmup 3 --no-cpu-baseline --latency-reps 1"
 if timeout 600 $NCU_CMD > $OUT/ncu_plain_$TAG.log 2>&1; then
-  timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
+  timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 60 --csv \
       --log-file $OUT/launches_$TAG.csv $NCU_CMD > $OUT/ncu_launch_$TAG.log 2>&1
   echo "ncu launches rc=$?" | tee -a $OUT/summary_$TAG.txt
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_place -s 4 -c 1 \

@@ -54,3 +54,22 @@ for rep in sorted(g.glob(f"*_{tag}.ncu-rep")):
     out.append("\n# source attribution (stall samples / executed warp instructions)\n" + lines_out)
     (out_dir / f"{tag}_{rep.stem.rsplit('_', 1)[0]}.txt").write_text("\n".join(out) + "\n")
 print(sorted(p.name for p in out_dir.glob(f"{tag}_*")))
+
+# per-launch DRAM traffic of the captured kernels -> profiles/traffic.json (read by bench.py)
+import json
+traffic = {"source": f"ncu --set full captures *_{tag}.ncu-rep (one launch each)"}
+for rep in sorted(g.glob(f"*_{tag}.ncu-rep")):
+    raw = subprocess.run(["ncu", "-i", str(rep), "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(raw.splitlines()))
+    if len(rows) < 3:
+        continue
+    hdr, units, data = rows[0], rows[1], rows[2]
+    def val(name):
+        i = hdr.index(name)
+        v = float(data[i].replace(",", ""))
+        u = units[i].lower()
+        return v * {"byte": 1, "kbyte": 1e3, "mbyte": 1e6, "gbyte": 1e9}.get(u, 1)
+    kname = data[hdr.index("Kernel Name")].split("(")[0].split("::")[-1]
+    traffic[kname] = val("dram__bytes_read.sum") + val("dram__bytes_write.sum")
+(out_dir / "traffic.json").write_text(json.dumps(traffic, indent=1) + "\n")
+print(traffic)
