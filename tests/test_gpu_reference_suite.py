@@ -1,0 +1,30 @@
+"""GPU: the reference's OWN test sources (unit tests under a Catch2 shim, and
+the acceptance suite), compiled in place in the build container with every
+plan_workload call redirected to the B200 planner (oracle/ref/gpu_prelude.hpp,
+include/wsgpu/wavesched_compat.hpp).  Binaries travel in oracle/_ref/."""
+import subprocess
+from pathlib import Path
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+REF = Path(__file__).resolve().parent.parent / "oracle" / "_ref"
+
+
+def _run(name, timeout):
+    exe = REF / name
+    if not exe.exists():
+        pytest.skip(f"{exe} not built (make -C oracle reftests needs the reference tree)")
+    return subprocess.run([str(exe)], cwd=REF, capture_output=True, text=True, timeout=timeout)
+
+
+def test_reference_unit_tests_pass_on_gpu_planner():
+    r = _run("unit_gpu", 900)
+    assert r.returncode == 0, r.stdout[-3000:]
+    assert "95 test cases, 0 failed" in r.stdout
+
+
+def test_reference_acceptance_suite_passes_on_gpu_planner():
+    r = _run("acceptance_gpu", 1200)
+    assert r.returncode == 0, r.stdout[-3000:]
+    assert r.stdout.count("[PASS] criterion") == 10
