@@ -29,6 +29,7 @@ struct PlSmLayout {
     int fin_src, fin_bytes;                                       // [M+1]
     int disp_mask, disp_bytes, disp_cnt, eorder, va;              // [M]
     int cmask;                                                    // [2N+M+1] candidate device sets
+    int used_if;                                                  // [N] f64
     int bytes;
 };
 
@@ -78,6 +79,7 @@ __host__ __device__ inline PlSmLayout make_pl_layout(const PlaceCaps& c) {
     L.eorder = take(4 * M);
     L.va = take(8 * M);
     L.cmask = take(8 * (2 * N + M + 1));
+    L.used_if = take(8 * N);
     L.bytes = (o + 15) & ~15;
     return L;
 }
@@ -237,6 +239,13 @@ __device__ int p_wave(PCtx& C, int w, int variant) {
         const double Pm = (1.0 + R.grad_mult) * static_cast<double>(parb[k]) / tpk[k];
         const uint64_t charged = chg[gkey[k]];
         const double cap = static_cast<double>(R.mem_capacity);
+        // device memory if this entry lands there (memory_delta), once per entry
+        double* used_if = C.at<double>(L.used_if);
+        for (int dv = lane; dv < N; dv += 32) {
+            double delta = A;
+            if (!(charged >> dv & 1ull)) delta += Pm;
+            used_if[dv] = mem[dv] + delta;
+        }
         __syncwarp();
 
         auto score_of = [&](uint64_t devs, int rot) {
@@ -255,13 +264,10 @@ __device__ int p_wave(PCtx& C, int w, int variant) {
             s.feasible = 1;
             double peak = 0.0;
             for (uint64_t d = devs; d; d &= d - 1) {
-                const int dv = low_bit(d);
-                double delta = A;
-                if (!(charged >> dv & 1ull)) delta += Pm;
-                const double used = mem[dv] + delta;
+                const double used = used_if[low_bit(d)];
                 peak = (peak < used) ? used : peak;
-                if (used > cap) s.feasible = 0;
             }
+            s.feasible = !(peak > cap);  // a device above capacity <=> the maximum is
             s.peak = peak;
             s.inter = 0.0;
             s.intra = 0.0;
