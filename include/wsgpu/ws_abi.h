@@ -252,6 +252,10 @@ int ws_last_kernel_ms(const ws_ctx* ctx, double* out, int n);
  * plans count as +inf; ties go to the smaller index.  Writes {key, index}. */
 int ws_best_staged(ws_ctx* ctx, int mode, double* key, int64_t* index, void* stream);
 
+/* Profiling aid: SM cycles per planner phase summed over warps since the last
+ * call (k_place 0-7, k_sched 10-14); all zero unless built with -DWS_PHASES. */
+int ws_debug_phase_cycles(unsigned long long* out, int n);
+
 /* Arena capacity sufficient for any batch whose plans stay within the limits. */
 uint64_t ws_arena_bound(const ws_batch* in);
 

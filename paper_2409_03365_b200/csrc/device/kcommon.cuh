@@ -300,4 +300,20 @@ __device__ __forceinline__ bool key_less(const OpKey& a, const OpKey& b) {  // s
 
 __device__ __forceinline__ uint64_t al8(uint64_t v) { return (v + 7) & ~7ull; }
 
+// Opt-in phase profiler (-DWS_PHASES builds only): SM cycles per planner phase,
+// summed over warps (lane 0), read back with ws_debug_phase_cycles().
+#ifdef WS_PHASES
+__device__ unsigned long long g_phase_cycles[32];
+#define WS_PH_START(t) long long t = clock64()
+#define WS_PH_STOP(t, idx)                                                                     \
+    do {                                                                                       \
+        if ((threadIdx.x & 31) == 0)                                                           \
+            atomicAdd(&g_phase_cycles[idx], static_cast<unsigned long long>(clock64() - (t))); \
+        t = clock64();                                                                         \
+    } while (0)
+#else
+#define WS_PH_START(t) (void)0
+#define WS_PH_STOP(t, idx) (void)0
+#endif
+
 }  // namespace wsdev

@@ -166,6 +166,7 @@ __device__ int p_wave(PCtx& C, int w, int variant) {
     const int* w_cursor = C.at<int>(L.w_cursor);
     const int eb = w_eb[w], ec = w_ec[w];
 
+    WS_PH_START(tw);
     // incoming volume per entry (incoming_flows :188-206), entry order (:208-221)
     for (int i = lane; i < ec; i += 32) {
         const int k = e_k[eb + i];
@@ -195,6 +196,7 @@ __device__ int p_wave(PCtx& C, int w, int variant) {
         eorder[pos] = i;
     }
     __syncwarp();
+    WS_PH_STOP(tw, 1);
     uint64_t free = C.all;
     uint64_t placed_now = 0;
     int cursor = R.sequential ? w_cursor[w] : 0;
@@ -234,6 +236,7 @@ __device__ int p_wave(PCtx& C, int w, int variant) {
             }
             ndisp += __popc(b);
         }
+        WS_PH_STOP(tw, 2);
         // memory_delta constants (:132-140)
         const double A = lay * (static_cast<double>(memact[k]) / n);
         const double Pm = (1.0 + R.grad_mult) * static_cast<double>(parb[k]) / tpk[k];
@@ -334,6 +337,7 @@ __device__ int p_wave(PCtx& C, int w, int variant) {
                     ncand += __popc(bal);
                 }
                 __syncwarp();
+                WS_PH_STOP(tw, 3);
                 const int rounds = oi == 0 ? variant + 1 : 1;  // first entry takes scores[variant]
                 Score prev;
                 prev.valid = 0;
@@ -352,6 +356,7 @@ __device__ int p_wave(PCtx& C, int w, int variant) {
                 }
             }
         }
+        WS_PH_STOP(tw, 4);
         if (!chosen.valid || !chosen.feasible) return 0;
         // commit_memory (:142-149), lane per device
         for (int dv = lane; dv < N; dv += 32) {
@@ -389,6 +394,7 @@ __device__ int p_wave(PCtx& C, int w, int variant) {
             }
             C.nF += need;
         }
+        WS_PH_STOP(tw, 5);
         free &= ~chosen.devs;
         placed_now |= 1ull << k;
         __syncwarp();
@@ -589,6 +595,7 @@ __global__ void __launch_bounds__(32 * kPlaceWarps, WS_PLACE_MINB) k_place(Place
         }
         return;
     }
+    WS_PH_START(tk);
     // load the schedule and build the entity tables (planner.hpp:99-151)
     const int* r_mod_of = reinterpret_cast<const int*>(rec + A.RL.mod_of);
     const int* r_by_rank = reinterpret_cast<const int*>(rec + A.RL.by_rank);
@@ -689,6 +696,7 @@ __global__ void __launch_bounds__(32 * kPlaceWarps, WS_PLACE_MINB) k_place(Place
     }
     __syncwarp();
     C.contig = ctl->i0;
+    WS_PH_STOP(tk, 0);
     // depth-first search over per-wave variants with a bounded attempt budget (:409-441).
     // The reference copies the whole state per placed wave; here the state
     // before wave k is rebuilt on demand by replaying the committed entries of
@@ -710,6 +718,7 @@ __global__ void __launch_bounds__(32 * kPlaceWarps, WS_PLACE_MINB) k_place(Place
             }
             return;
         }
+        WS_PH_START(tr);
         if (dirty) {  // rebuild the state before wave k
             for (int d = lane; d < N; d += 32) mem[d] = 0.0;
             for (int g = lane; g < G; g += 32) chg[g] = 0;
@@ -733,6 +742,7 @@ __global__ void __launch_bounds__(32 * kPlaceWarps, WS_PLACE_MINB) k_place(Place
                 }
             }
             C.nF = wave_nf[k];
+            WS_PH_STOP(tr, 6);
             dirty = false;
             __syncwarp();
         }
@@ -775,7 +785,9 @@ __global__ void __launch_bounds__(32 * kPlaceWarps, WS_PLACE_MINB) k_place(Place
         }
         __syncwarp();
     }
+    WS_PH_START(te);
     p_emit(C, p, rec, A.RL, h, A);
+    WS_PH_STOP(te, 7);
 }
 
 }  // namespace wsdev

@@ -518,6 +518,20 @@ int ws_plan_batch_host(ws_ctx* ctx, const ws_batch* in, ws_plan_result* results,
     return 0;
 }
 
+// Phase cycle counters of a -DWS_PHASES build (zeros otherwise); resets them.
+int ws_debug_phase_cycles(unsigned long long* out, int n) {
+#ifdef WS_PHASES
+    unsigned long long h[32] = {};
+    if (cudaMemcpyFromSymbol(h, g_phase_cycles, sizeof(h)) != cudaSuccess) return 1;
+    for (int i = 0; i < n && i < 32; ++i) out[i] = h[i];
+    const unsigned long long z[32] = {};
+    cudaMemcpyToSymbol(g_phase_cycles, z, sizeof(z));
+#else
+    for (int i = 0; i < n; ++i) out[i] = 0;
+#endif
+    return 0;
+}
+
 int ws_best_staged(ws_ctx* ctx, int mode, double* key, int64_t* index, void* stream) {
     cudaSetDevice(ctx->device);
     cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;

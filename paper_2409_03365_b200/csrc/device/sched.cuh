@@ -69,6 +69,7 @@ struct SmLayout {
     int indeg, keyrank, modat, kofm, mod_of, idrank, by_rank, level;         // [M] 4 B
     int up_n, up_l, lo_n, lo_l, sumlay, lvl_mem, gm_of, nmax_of, Lk, absorb;  // [M] 4 B
     int lvl_begin;                                                           // [M+1]
+    int cstar_sm, aerr_x, aerr_y, aerr;                                      // [M] per level
     int tk, tn, tl, tn2, sel, best, pool, klay;                              // [2M]
     int ord;                                                                 // [3*2M]
     int bytes;
@@ -109,6 +110,10 @@ __host__ __device__ inline SmLayout make_sm_layout(int M) {
     L.Lk = take(4 * M);
     L.absorb = take(4 * M);
     L.lvl_begin = take(4 * (M + 1));
+    L.cstar_sm = take(8 * M);
+    L.aerr_x = take(8 * M);
+    L.aerr_y = take(8 * M);
+    L.aerr = take(4 * M);
     L.tk = take(4 * T);
     L.tn = take(4 * T);
     L.tl = take(4 * T);
@@ -422,6 +427,139 @@ __device__ __forceinline__ double ordered_sum(double v0, double v1, int w) {
     return total;
 }
 
+// repair_capacity (allocation.hpp:107-139) for one level; lane i holds members i, i+32
+__device__ bool s_level_repair(SCtx& C, int lvl) {
+    const int N = C.N, lane = C.lane;
+    const int* lb = C.at<int>(C.L->lvl_begin);
+    const int* lm = C.at<int>(C.L->lvl_mem) + lb[lvl];
+    const int w = lb[lvl + 1] - lb[lvl];
+    const int* gm_of = C.at<int>(C.L->gm_of);
+    const int* nmax_of = C.at<int>(C.L->nmax_of);
+    const uint64_t* valid = C.at<uint64_t>(C.L->valid);
+    int* up_n = C.at<int>(C.L->up_n);
+    const int* up_l = C.at<int>(C.L->up_l);
+    const int* lo_n = C.at<int>(C.L->lo_n);
+    const int* lo_l = C.at<int>(C.L->lo_l);
+    const FitOut& F = *C.F;
+    while (true) {
+        int wid = 0;
+        for (int i = lane; i < w; i += 32) {
+            const int k = lm[i];
+            const int a = up_n[k], b = lo_l[k] ? lo_n[k] : 0;
+            wid += a > b ? a : b;
+        }
+        if (warp_sum(wid) <= N) break;
+        double best_pen = 0.0;
+        int best_i = 0x7fffffff, best_t = 0, eidx = 0x7fffffff;
+        double ex = 0, ey = 0;
+        for (int i = lane; i < w; i += 32) {
+            const int k = lm[i];
+            const int un = up_n[k];
+            const uint64_t below = valid[k] & ((1ull << (un - 1)) - 1ull);  // valid values < un
+            if (!below) continue;
+            const int target = 64 - __clzll(static_cast<long long>(below));
+            if (lo_l[k] && target <= lo_n[k]) continue;
+            const int nmax = nmax_of[k];
+            if (target > nmax || un > nmax) {  // eval(target) first, then eval(t.n)
+                if (i < eidx) eidx = i, ex = target > nmax ? target : un, ey = nmax;
+                continue;
+            }
+            const double pen = up_l[k] * (t_at(F, gm_of[k], target) - t_at(F, gm_of[k], un));
+            if (best_i == 0x7fffffff || pen < best_pen) best_pen = pen, best_i = i, best_t = target;
+        }
+        const int emin = warp_min_i(eidx);
+        if (emin != 0x7fffffff) {
+            const int src = emin & 31;
+            const double xx = shfl_d(ex, src), yy = shfl_d(ey, src);
+            if (lane == 0) {
+                C.ctl->err = WS_E_EVAL_RANGE;
+                C.ctl->x = xx;
+                C.ctl->y = yy;
+            }
+            __syncwarp();
+            return false;
+        }
+        for (int off = 16; off; off >>= 1) {  // argmin over (penalty, member index)
+            const double op = __shfl_xor_sync(kFull, best_pen, off);
+            const int oi = __shfl_xor_sync(kFull, best_i, off);
+            const int ot = __shfl_xor_sync(kFull, best_t, off);
+            if (oi != 0x7fffffff && (best_i == 0x7fffffff || op < best_pen || (op == best_pen && oi < best_i)))
+                best_pen = op, best_i = oi, best_t = ot;
+        }
+        if (best_i == 0x7fffffff) break;
+        if (lane == 0) up_n[lm[best_i]] = best_t;
+        __syncwarp();
+    }
+    return true;
+}
+
+// bi-point discretization of one MetaOp (allocation.hpp:149-214).  Returns
+// false on OutOfRange (x = n, y = n_max; eval(n_over) is evaluated first).
+__device__ __forceinline__ bool discretize_one(const FitOut& F, const ws_plan_rec& R, int gm, int L, double nmax,
+                                               uint64_t v, double nstar, double cs, int& un, int& ul, int& ln,
+                                               int& ll, double& ex) {
+    int exact = -1, n_over = -1, n_under = -1;
+    for (uint64_t b = v; b; b &= b - 1) {
+        const int x = low_bit(b) + 1;
+        if (fabs(x - nstar) < 1e-9) {
+            exact = x;
+            break;
+        }
+    }
+    if (exact < 0)
+        for (uint64_t b = v; b; b &= b - 1) {
+            const int x = low_bit(b) + 1;
+            if (x < nstar) n_under = x;
+            if (x > nstar) {
+                n_over = x;
+                break;
+            }
+        }
+    un = 0, ul = L, ln = 0, ll = 0;
+    if (exact >= 0) {
+        un = exact;
+    } else if (n_over == -1) {
+        un = 64 - __clzll(static_cast<long long>(v));
+    } else if (n_under == -1) {
+        un = low_bit(v) + 1;
+    } else {
+        if (n_over > nmax || n_under > nmax) {
+            ex = n_over > nmax ? n_over : n_under;
+            return false;
+        }
+        const double t_over = t_at(F, gm, n_over);
+        const double t_under = t_at(F, gm, n_under);
+        if (t_under - t_over <= 0.0) {
+            un = n_under;
+        } else {
+            double lr = (cs - t_under * L) / (t_over - t_under);
+            lr = lr < 0.0 ? 0.0 : (static_cast<double>(L) < lr ? static_cast<double>(L) : lr);
+            int l_over = static_cast<int>(floor(lr + 0.5));
+            int l_under = L - l_over;
+            if (R.drop_floor > 0.0 && l_over > 0 && l_under > 0) {
+                if (l_over * t_over < R.drop_floor * cs) {
+                    l_under += l_over;
+                    l_over = 0;
+                } else if (l_under * t_under < R.drop_floor * cs) {
+                    l_over += l_under;
+                    l_under = 0;
+                }
+            }
+            if (l_over == 0) {
+                un = n_under;
+            } else if (l_under == 0) {
+                un = n_over;
+            } else {
+                un = n_over;
+                ul = l_over;
+                ln = n_under;
+                ll = l_under;
+            }
+        }
+    }
+    return true;
+}
+
 // (3b) bisection on the capacity equation, bi-point discretization and
 // capacity repair for one level; lane i holds members i and i+32
 __device__ bool s_level_alloc(SCtx& C, int lvl, double& c_star_out) {
@@ -491,68 +629,12 @@ __device__ bool s_level_alloc(SCtx& C, int lvl, double& c_star_out) {
     for (int s = 0; s < 2; ++s) {
         const Mem& q = mem[s];
         if (q.k < 0) continue;
-        const double nstar = probe_term(q, cs);
-        const uint64_t v = valid[q.k];
-        const int L = q.L;
-        int exact = -1, n_over = -1, n_under = -1;
-        for (uint64_t b = v; b; b &= b - 1) {
-            const int x = low_bit(b) + 1;
-            if (fabs(x - nstar) < 1e-9) {
-                exact = x;
-                break;
-            }
-        }
-        if (exact < 0)
-            for (uint64_t b = v; b; b &= b - 1) {
-                const int x = low_bit(b) + 1;
-                if (x < nstar) n_under = x;
-                if (x > nstar) {
-                    n_over = x;
-                    break;
-                }
-            }
-        int un = 0, ul = L, ln = 0, ll = 0;
-        if (exact >= 0) {
-            un = exact;
-        } else if (n_over == -1) {
-            un = 64 - __clzll(static_cast<long long>(v));
-        } else if (n_under == -1) {
-            un = low_bit(v) + 1;
-        } else {
-            if (n_over > q.nmax || n_under > q.nmax) {  // OutOfRange (eval(n_over) first)
-                const int idx = lane + 32 * s;
-                if (idx < eidx0) eidx0 = idx, ex0 = n_over > q.nmax ? n_over : n_under, ey0 = q.nmax;
-                continue;
-            }
-            const double t_over = t_at(F, q.gm, n_over);
-            const double t_under = t_at(F, q.gm, n_under);
-            if (t_under - t_over <= 0.0) {
-                un = n_under;
-            } else {
-                double lr = (cs - t_under * L) / (t_over - t_under);
-                lr = lr < 0.0 ? 0.0 : (static_cast<double>(L) < lr ? static_cast<double>(L) : lr);
-                int l_over = static_cast<int>(floor(lr + 0.5));
-                int l_under = L - l_over;
-                if (R.drop_floor > 0.0 && l_over > 0 && l_under > 0) {
-                    if (l_over * t_over < R.drop_floor * cs) {
-                        l_under += l_over;
-                        l_over = 0;
-                    } else if (l_under * t_under < R.drop_floor * cs) {
-                        l_over += l_under;
-                        l_under = 0;
-                    }
-                }
-                if (l_over == 0) {
-                    un = n_under;
-                } else if (l_under == 0) {
-                    un = n_over;
-                } else {
-                    un = n_over;
-                    ul = l_over;
-                    ln = n_under;
-                    ll = l_under;
-                }
-            }
+        int un, ul, ln, ll;
+        double ex;
+        if (!discretize_one(F, R, q.gm, q.L, q.nmax, valid[q.k], probe_term(q, cs), cs, un, ul, ln, ll, ex)) {
+            const int idx = lane + 32 * s;
+            if (idx < eidx0) eidx0 = idx, ex0 = ex, ey0 = q.nmax;
+            continue;
         }
         up_n[q.k] = un;
         up_l[q.k] = ul;
@@ -574,59 +656,114 @@ __device__ bool s_level_alloc(SCtx& C, int lvl, double& c_star_out) {
         }
     }
     __syncwarp();
-    // repair_capacity (allocation.hpp:107-139)
-    while (true) {
-        int wid = 0;
-        for (int s = 0; s < 2; ++s) {
-            const Mem& q = mem[s];
-            if (q.k < 0) continue;
-            const int a = up_n[q.k], b = lo_l[q.k] ? lo_n[q.k] : 0;
-            wid += a > b ? a : b;
+    return s_level_repair(C, lvl);
+}
+
+
+// (3b) all levels at once (K <= 32): levels are independent, so lane i holds
+// the i-th MetaOp in level-major order and each level's bisection runs in its
+// own lane segment; segment-local ordered sums reproduce each level's
+// reference summation order exactly.  Per level: c* (cstar_sm) and the first
+// discretization OutOfRange (aerr_*), reported in level order by the caller.
+__device__ void s_alloc_concurrent(SCtx& C, int n_levels) {
+    const ws_batch& B = *C.B;
+    const ws_plan_rec& R = *C.R;
+    const int N = C.N, lane = C.lane, K = C.K;
+    const int* lb = C.at<int>(C.L->lvl_begin);
+    const int* lm = C.at<int>(C.L->lvl_mem);
+    const int* level = C.at<int>(C.L->level);
+    const int* gm_of = C.at<int>(C.L->gm_of);
+    const int* nmax_of = C.at<int>(C.L->nmax_of);
+    const int* Lk = C.at<int>(C.L->Lk);
+    const uint64_t* valid = C.at<uint64_t>(C.L->valid);
+    double* cstar_sm = C.at<double>(C.L->cstar_sm);
+    double* aerr_x = C.at<double>(C.L->aerr_x);
+    double* aerr_y = C.at<double>(C.L->aerr_y);
+    int* aerr = C.at<int>(C.L->aerr);
+    const double nd = static_cast<double>(N);
+    const FitOut& F = *C.F;
+    const bool has = lane < K;
+    const int k = has ? lm[lane] : 0;
+    const int lv = has ? level[k] : 0;
+    const int s0 = has ? lb[lv] : lane;
+    const int sw = has ? lb[lv + 1] - lb[lv] : 0;
+    int maxw = 0;
+    for (int l = 0; l < n_levels; ++l) maxw = lb[l + 1] - lb[l] > maxw ? lb[l + 1] - lb[l] : maxw;
+    const int gm = has ? gm_of[k] : 0;
+    const int L = has ? Lk[k] : 1;
+    const double nmax = has ? nmax_of[k] : 1.0;
+    InvPre inv;
+    if (has) inv.init(F.pieces + 5 * F.piece_off[gm], F.npieces[gm], B.mod_c[gm], B.mod_w[gm], nmax);
+    auto seg_sum = [&](double v) {  // ((0 + v_s) + v_s+1) + ... over this lane's segment
+        double total = 0.0;
+        for (int j = 0; j < maxw; ++j) {
+            const double x = __shfl_sync(kFull, v, s0 + (j < sw ? j : (sw ? sw - 1 : 0)));
+            if (j < sw) total += x;
         }
-        if (warp_sum(wid) <= N) break;
-        double best_pen = 0.0;
-        int best_i = 0x7fffffff, best_t = 0, eidx = 0x7fffffff;
-        double ex = 0, ey = 0;
-        for (int s = 0; s < 2; ++s) {
-            const Mem& q = mem[s];
-            if (q.k < 0) continue;
-            const int un = up_n[q.k];
-            const uint64_t below = valid[q.k] & ((1ull << (un - 1)) - 1ull);  // valid values < un
-            if (!below) continue;
-            const int target = 64 - __clzll(static_cast<long long>(below));
-            if (lo_l[q.k] && target <= lo_n[q.k]) continue;
-            const int idx = lane + 32 * s;
-            if (target > q.nmax || un > q.nmax) {  // eval(target) first, then eval(t.n)
-                if (idx < eidx) eidx = idx, ex = target > q.nmax ? target : un, ey = q.nmax;
-                continue;
-            }
-            const double pen = up_l[q.k] * (t_at(F, q.gm, target) - t_at(F, q.gm, un));
-            if (best_i == 0x7fffffff || pen < best_pen) best_pen = pen, best_i = idx, best_t = target;
+        return total;
+    };
+    auto seg_max = [&](double v) {
+        double m = 0.0;
+        for (int j = 0; j < maxw; ++j) {
+            const double x = __shfl_sync(kFull, v, s0 + (j < sw ? j : (sw ? sw - 1 : 0)));
+            if (j < sw) m = (m < x) ? x : m;
         }
-        const int emin = warp_min_i(eidx);
-        if (emin != 0x7fffffff) {
-            const int src = emin & 31;
-            const double xx = shfl_d(ex, src), yy = shfl_d(ey, src);
-            if (lane == 0) {
-                C.ctl->err = WS_E_EVAL_RANGE;
-                C.ctl->x = xx;
-                C.ctl->y = yy;
-            }
-            __syncwarp();
-            return false;
-        }
-        for (int off = 16; off; off >>= 1) {  // argmin over (penalty, member index)
-            const double op = __shfl_xor_sync(kFull, best_pen, off);
-            const int oi = __shfl_xor_sync(kFull, best_i, off);
-            const int ot = __shfl_xor_sync(kFull, best_t, off);
-            if (oi != 0x7fffffff && (best_i == 0x7fffffff || op < best_pen || (op == best_pen && oi < best_i)))
-                best_pen = op, best_i = oi, best_t = ot;
-        }
-        if (best_i == 0x7fffffff) break;
-        if (lane == 0) up_n[lm[best_i]] = best_t;
-        __syncwarp();
+        return m;
+    };
+    auto probe_term = [&](double cc) {
+        const double v = inv(cc / L);
+        return (nd < v) ? nd : v;  // std::min(v, N)
+    };
+    // bracket [max T(min(N,nmax))*L, sum T(1)*L] (allocation.hpp:75-80)
+    double lo_t = 0.0, hi_t = 0.0;
+    if (has) {
+        const double ncap = (nmax < nd) ? nmax : nd;
+        lo_t = t_at(F, gm, static_cast<int>(ncap)) * L;
+        hi_t = t_at(F, gm, 1) * L;
     }
-    return true;
+    double c_lo = seg_max(lo_t);
+    double c_hi = seg_sum(hi_t);
+    int it = 0;
+    bool active = has && it < R.max_iters && (c_hi - c_lo) > R.eps * c_hi;
+    while (__any_sync(kFull, active)) {  // allocation.hpp:87-93, every level in its segment
+        const double mid = 0.5 * (c_lo + c_hi);
+        const double total = seg_sum(has ? probe_term(mid) : 0.0);
+        if (active) {
+            if (total < nd)
+                c_hi = mid;
+            else
+                c_lo = mid;
+            ++it;
+        }
+        active = has && it < R.max_iters && (c_hi - c_lo) > R.eps * c_hi;
+    }
+    const double cs = 0.5 * (c_lo + c_hi);
+    bool bad = false;
+    double ex = 0.0;
+    if (has) {
+        int un, ul, ln, ll;
+        bad = !discretize_one(F, R, gm, L, nmax, valid[k], probe_term(cs), cs, un, ul, ln, ll, ex);
+        if (!bad) {
+            C.at<int>(C.L->up_n)[k] = un;
+            C.at<int>(C.L->up_l)[k] = ul;
+            C.at<int>(C.L->lo_n)[k] = ln;
+            C.at<int>(C.L->lo_l)[k] = ll;
+        }
+    }
+    // first failing member of each level (segment), recorded by the segment head
+    const unsigned eb = __ballot_sync(kFull, bad);
+    const unsigned segm = sw ? ((sw >= 32 ? 0xffffffffu : ((1u << sw) - 1u)) << s0) : 0u;
+    const unsigned mine = eb & segm;
+    const int src = mine ? __ffs(mine) - 1 : lane;
+    const double xx = __shfl_sync(kFull, ex, src);
+    const double yy = __shfl_sync(kFull, nmax, src);
+    if (has && lane == s0) {
+        cstar_sm[lv] = cs;
+        aerr[lv] = mine ? WS_E_EVAL_RANGE : 0;
+        aerr_x[lv] = xx;
+        aerr_y[lv] = yy;
+    }
+    __syncwarp();
 }
 
 // ---------------------------------------------------------------------------
@@ -1140,9 +1277,12 @@ __global__ void __launch_bounds__(32 * kSchedWarps) k_sched(SchedArgs A) {
         if (lane == 0) ctl->err = WS_E_LIMIT_MODULES;
     }
     __syncwarp();
+    WS_PH_START(tg);
     if (ok) ok = s_graph(C);
+    WS_PH_STOP(tg, 10);
     if (ok) ok = s_fit_status(C);
     if (ok) ok = s_valid(C);
+    WS_PH_STOP(tg, 11);
     int n_levels = 0, nW = 0, nE = 0;
     double lower_bound = 0.0, offset = 0.0;
     if (ok) {
@@ -1150,14 +1290,34 @@ __global__ void __launch_bounds__(32 * kSchedWarps) k_sched(SchedArgs A) {
         double* cstar = reinterpret_cast<double*>(rec + A.RL.cstar);
         int* lfw = reinterpret_cast<int*>(rec + A.RL.lvl_fw);
         int* lnw = reinterpret_cast<int*>(rec + A.RL.lvl_nw);
+        const bool conc = C.K <= 32;  // every level's bisection at once
+        if (conc) s_alloc_concurrent(C, n_levels);
         for (int l = 0; l < n_levels && ok; ++l) {
             double cs = 0.0;
-            ok = s_level_alloc(C, l, cs);
+            if (conc) {
+                const int* aerr = C.at<int>(C.L->aerr);
+                cs = C.at<double>(C.L->cstar_sm)[l];
+                if (aerr[l]) {
+                    if (C.lane == 0) {
+                        ctl->err = aerr[l];
+                        ctl->x = C.at<double>(C.L->aerr_x)[l];
+                        ctl->y = C.at<double>(C.L->aerr_y)[l];
+                    }
+                    __syncwarp();
+                    ok = false;
+                } else {
+                    ok = s_level_repair(C, l);
+                }
+            } else {
+                ok = s_level_alloc(C, l, cs);
+            }
+            WS_PH_STOP(tg, 12);
             if (!ok) break;
             lower_bound += cs;  // planner.hpp:189
             const int w0 = nW;
             double level_end = offset;
             ok = s_schedule_level(C, rec, A.RL, l, nW, nE, offset, level_end, A.caps.W, A.caps.E);
+            WS_PH_STOP(tg, 13);
             if (!ok) break;
             if (lane == 0) {
                 cstar[l] = cs;
@@ -1174,6 +1334,7 @@ __global__ void __launch_bounds__(32 * kSchedWarps) k_sched(SchedArgs A) {
         }
         return;
     }
+    WS_PH_START(tw);
     // hand the MetaOp tables to k_place / emit
     const int K = C.K;
     int* r_mod_of = reinterpret_cast<int*>(rec + A.RL.mod_of);
@@ -1209,6 +1370,7 @@ __global__ void __launch_bounds__(32 * kSchedWarps) k_sched(SchedArgs A) {
         h.end_time = offset;
         *hdr = h;
     }
+    WS_PH_STOP(tw, 14);
 }
 
 }  // namespace wsdev
