@@ -226,6 +226,7 @@ __device__ __forceinline__ Score shfl_xor_score(const Score& s, int m) {
     return o;
 }
 
+#ifdef WS_MINLOC_SHFL
 __device__ __forceinline__ Score warp_min_score(Score s) {
     for (int off = 16; off; off >>= 1) {
         const Score o = shfl_xor_score(s, off);
@@ -233,6 +234,42 @@ __device__ __forceinline__ Score warp_min_score(Score s) {
     }
     return s;
 }
+#else
+// Same order as score_less, as a field-by-field elimination over 32-bit words
+// with redux.sync: the doubles are all >= +0.0 (sums/maxima of non-negative
+// terms starting at 0.0), whose IEEE bit patterns order like the values; the
+// sorted device-list order is the unsigned order of ~brev(devs).  Stops as
+// soon as one lane is left; the winner's Score is then broadcast once.
+__device__ __forceinline__ Score warp_min_score(const Score& s) {
+    unsigned cand = __ballot_sync(kFull, s.valid);
+    if (!cand) return s;  // no lane holds a candidate (s.valid == 0 everywhere)
+    const int lane = threadIdx.x & 31;
+    auto stage = [&](unsigned v) {
+        const unsigned key = (cand >> lane & 1u) ? v : 0xffffffffu;
+        cand &= __ballot_sync(kFull, key == __reduce_min_sync(kFull, key));
+        return (cand & (cand - 1u)) == 0u;
+    };
+    auto hi = [](double d) { return static_cast<unsigned>(__double_as_longlong(d) >> 32); };
+    auto lo = [](double d) { return static_cast<unsigned>(__double_as_longlong(d)); };
+    const uint64_t rd = ~__brevll(s.devs);
+    (void)(stage(s.feasible ? 0u : 1u) || stage(hi(s.inter)) || stage(lo(s.inter)) || stage(hi(s.intra)) ||
+           stage(lo(s.intra)) || stage(hi(s.displaced)) || stage(lo(s.displaced)) ||
+           stage(static_cast<unsigned>(s.islands)) || stage(hi(s.peak)) || stage(lo(s.peak)) ||
+           stage(static_cast<unsigned>(rd >> 32)) || stage(static_cast<unsigned>(rd)));
+    const int src = __ffs(cand) - 1;  // equal devs => equal Scores
+    Score o;
+    o.valid = 1;
+    o.feasible = __shfl_sync(kFull, s.feasible, src);
+    o.islands = __shfl_sync(kFull, s.islands, src);
+    o.rot = __shfl_sync(kFull, s.rot, src);
+    o.inter = __shfl_sync(kFull, s.inter, src);
+    o.intra = __shfl_sync(kFull, s.intra, src);
+    o.displaced = __shfl_sync(kFull, s.displaced, src);
+    o.peak = __shfl_sync(kFull, s.peak, src);
+    o.devs = __shfl_sync(kFull, s.devs, src);
+    return o;
+}
+#endif
 
 __device__ __forceinline__ int warp_sum(int v) {
     for (int off = 16; off; off >>= 1) v += __shfl_xor_sync(kFull, v, off);
@@ -311,9 +348,12 @@ __device__ unsigned long long g_phase_cycles[32];
             atomicAdd(&g_phase_cycles[idx], static_cast<unsigned long long>(clock64() - (t))); \
         t = clock64();                                                                         \
     } while (0)
+#define WS_PH_COUNT(idx, v) \
+    if ((threadIdx.x & 31) == 0) atomicAdd(&g_phase_cycles[idx], static_cast<unsigned long long>(v))
 #else
 #define WS_PH_START(t) (void)0
 #define WS_PH_STOP(t, idx) (void)0
+#define WS_PH_COUNT(idx, v) (void)0
 #endif
 
 }  // namespace wsdev

@@ -338,6 +338,14 @@ __device__ int p_wave(PCtx& C, int w, int variant) {
                 }
                 __syncwarp();
                 WS_PH_STOP(tw, 3);
+                WS_PH_COUNT(20, 1);
+                WS_PH_COUNT(21, ncand);
+                WS_PH_COUNT(22, n);
+                WS_PH_COUNT(23, ndisp);
+                WS_PH_COUNT(24, nfin);
+                WS_PH_COUNT(25, C.n_isl);
+                WS_PH_COUNT(26, (ncand + 31) / 32);
+                WS_PH_COUNT(27, N);
                 const int rounds = oi == 0 ? variant + 1 : 1;  // first entry takes scores[variant]
                 Score prev;
                 prev.valid = 0;
@@ -349,7 +357,9 @@ __device__ int p_wave(PCtx& C, int w, int variant) {
                         if (prev.valid && !score_less(prev, s)) continue;  // next distinct rank
                         if (!best.valid || score_less(s, best)) best = s;
                     }
+                    WS_PH_STOP(tw, 4);
                     best = warp_min_score(best);
+                    WS_PH_STOP(tw, 8);
                     if (!best.valid) break;  // fewer distinct candidates than variant+1
                     prev = best;
                     chosen = best;

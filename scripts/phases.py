@@ -8,7 +8,7 @@ sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
 import paper_2409_03365_b200 as ws
 
 NAMES = {0: "place:prologue", 1: "place:wave order", 2: "place:flows_in+disp", 3: "place:candidates",
-         4: "place:score+minloc", 5: "place:commit+flows", 6: "place:restore", 7: "place:emit",
+         4: "place:score", 8: "place:minloc", 5: "place:commit+flows", 6: "place:restore", 7: "place:emit",
          10: "sched:graph", 11: "sched:fit+valid", 12: "sched:alloc", 13: "sched:schedule", 14: "sched:writeback"}
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 100000
 ps = ws.ProblemSet()
@@ -25,8 +25,12 @@ f(buf, 32)
 pl.plan_staged()
 pl.fetch(ps)
 f(buf, 32)
-tot_p = sum(buf[i] for i in range(0, 8)) or 1
+tot_p = sum(buf[i] for i in range(0, 10)) or 1
 tot_s = sum(buf[i] for i in range(10, 15)) or 1
 for i, name in NAMES.items():
     tot = tot_p if i < 10 else tot_s
     print(f"{name:24s} {buf[i] / n:12.0f} cycles/plan  {100 * buf[i] / tot:5.1f}%")
+ne = buf[20] or 1
+print(f"scored entries/plan {buf[20] / n:.1f}; per entry: ncand {buf[21] / ne:.1f}  n {buf[22] / ne:.1f}  "
+      f"ndisp {buf[23] / ne:.1f}  nfin {buf[24] / ne:.2f}  islands {buf[25] / ne:.1f}  "
+      f"lane-iters {buf[26] / ne:.2f}  N {buf[27] / ne:.1f}")
