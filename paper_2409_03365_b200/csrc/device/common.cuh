@@ -9,7 +9,11 @@ namespace wsdev {
 constexpr unsigned kFull = 0xffffffffu;
 
 __device__ __forceinline__ int popc64(uint64_t m) { return __popcll(m); }
-__device__ __forceinline__ int low_bit(uint64_t m) { return __ffsll(static_cast<long long>(m)) - 1; }
+// index of the lowest set bit; m != 0 (one BREV+FLO on the nonzero half: cheaper than __ffsll)
+__device__ __forceinline__ int low_bit(uint64_t m) {
+    const unsigned lo = static_cast<unsigned>(m);
+    return lo ? __ffs(lo) - 1 : 31 + __ffs(static_cast<unsigned>(m >> 32));
+}
 
 // Index of the k-th (0-based) set bit of m; m must hold more than k bits.
 __device__ __forceinline__ int select_bit(uint64_t m, int k) {
@@ -48,26 +52,21 @@ __device__ __forceinline__ uint64_t window_mask(uint64_t pool, int s, int cnt) {
 __device__ __forceinline__ double shfl_d(double v, int src) { return __shfl_sync(kFull, v, src); }
 __device__ __forceinline__ uint64_t shfl_u64(uint64_t v, int src) { return __shfl_sync(kFull, v, src); }
 
-// "m<a>" < "m<b>" as std::string: compare decimal spellings lexicographically.
-__device__ __forceinline__ bool dec_less(int a, int b) {
-    char sa[12], sb[12];
-    int la = 0, lb = 0;
-    {
-        char t[12];
-        int n = 0, v = a;
-        do { t[n++] = static_cast<char>('0' + v % 10); v /= 10; } while (v);
-        while (n) sa[la++] = t[--n];
-    }
-    {
-        char t[12];
-        int n = 0, v = b;
-        do { t[n++] = static_cast<char>('0' + v % 10); v /= 10; } while (v);
-        while (n) sb[lb++] = t[--n];
-    }
-    const int l = la < lb ? la : lb;
-    for (int i = 0; i < l; ++i)
-        if (sa[i] != sb[i]) return sa[i] < sb[i];
-    return la < lb;
+// "m<a>" < "m<b>" as std::string (a, b >= 0): compare the decimal spellings
+// lexicographically.  Equal lengths order numerically; otherwise compare the
+// shorter spelling with the same-length prefix of the longer one, and a proper
+// prefix sorts first.
+__host__ __device__ __forceinline__ int dec_digits(int v) {
+    int d = 1;
+    while (v >= 10) v /= 10, ++d;
+    return d;
+}
+__host__ __device__ __forceinline__ bool dec_less(int a, int b) {
+    const int da = dec_digits(a), db = dec_digits(b);
+    if (da == db) return a < b;
+    int p = 1;
+    for (int i = da < db ? db - da : da - db; i; --i) p *= 10;
+    return da < db ? a <= b / p : a / p < b;
 }
 
 // ---------------------------------------------------------------------------

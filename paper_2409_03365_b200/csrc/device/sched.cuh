@@ -215,6 +215,18 @@ __device__ bool s_graph(SCtx& C) {
         const int m = base + lane;
         used |= static_cast<uint64_t>(__ballot_sync(kFull, m < M && tmask[m] != 0)) << base;
     }
+    // keys kind+"." packed big-endian into their first 8 bytes (zero padded);
+    // `valid` is scratch here, s_valid fills it later
+    uint64_t* key8 = C.at<uint64_t>(C.L->valid);
+    for (int m = lane; m < M; m += 32) {
+        const uint8_t* nm = B.names + B.mod_name_off[C.mbase + m];
+        const int len = B.mod_name_len[C.mbase + m];
+        uint64_t k = 0;
+        for (int i = 0; i < 8 && i <= len; ++i)
+            k |= static_cast<uint64_t>(i < len ? nm[i] : static_cast<uint8_t>('.')) << (56 - 8 * i);
+        key8[m] = k;
+    }
+    __syncwarp();
     // in-degrees, rank of the key kind+"." and kinds prefixed by another kind+"."
     int conflict = 0;
     for (int m = lane; m < M; m += 32) {
@@ -225,16 +237,29 @@ __device__ bool s_graph(SCtx& C) {
             keyrank[m] = -1;
             continue;
         }
-        const OpKey km = op_key(B, C.mbase + m, 0, false);
+        const uint64_t k8 = key8[m];
+        const int lm_ = B.mod_name_len[C.mbase + m];
+        const uint64_t pmask = lm_ < 7 ? ~0ull << (56 - 8 * lm_) : ~0ull;  // bytes 0..len
         int r = 0;
         for (uint64_t o = used; o; o &= o - 1) {
             const int q = low_bit(o);
             if (q == m) continue;
-            const OpKey kq = op_key(B, C.mbase + q, 0, false);
-            if (key_less(kq, km)) ++r;
-            if (kq.len > km.len) {
-                bool pre = true;
-                for (int i = 0; i <= km.len && pre; ++i) pre = kq.at(i) == km.at(i);
+            const uint64_t q8 = key8[q];
+            const int lq = B.mod_name_len[C.mbase + q];
+            if (q8 != k8) {
+                r += q8 < k8;  // the first differing byte lies in the packed prefix
+            } else if (key_less(op_key(B, C.mbase + q, 0, false), op_key(B, C.mbase + m, 0, false))) {
+                ++r;
+            }
+            if (lq > lm_) {  // kq starts with km + "."
+                bool pre;
+                if (lm_ < 8) {
+                    pre = ((q8 ^ k8) & pmask) == 0;
+                } else {
+                    const OpKey km = op_key(B, C.mbase + m, 0, false), kq = op_key(B, C.mbase + q, 0, false);
+                    pre = true;
+                    for (int i = 0; i <= km.len && pre; ++i) pre = kq.at(i) == km.at(i);
+                }
                 if (pre) conflict = 1;
             }
         }
