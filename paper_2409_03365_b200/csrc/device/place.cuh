@@ -462,41 +462,54 @@ __device__ void p_emit(PCtx& C, int p, const char* rec, const RecLayout& RL, con
     auto* en = reinterpret_cast<ws_out_entry*>(base + o);
     o += al8(sizeof(ws_out_entry) * nE);
     auto* fl = reinterpret_cast<ws_out_flow*>(base + o);
-    {
-        int pb = 0;
-        for (int k = 0; k < K; ++k) {
-            const int gm = C.mbase + r_mod_of[k];
-            const int np = C.F->npieces[gm];
-            if ((k & 31) == lane) {
-                ws_out_metaop x;
-                x.module = r_mod_of[k];
-                x.level = r_level[k];
-                x.first_layer = 0;
-                x.length = B.mod_layers[gm];
-                x.piece_begin = pb;
-                x.piece_count = np;
-                x.upper_n = r_up_n[k];
-                x.upper_l = r_up_l[k];
-                x.lower_n = r_lo_n[k];
-                x.lower_l = r_lo_l[k];
-                mo[k] = x;
-            }
+    // lane per MetaOp; piece offsets by a warp prefix sum over piece counts
+    for (int base = 0, pb0 = 0; base < K; base += 32) {
+        const int k = base + lane;
+        const int gm = k < K ? C.mbase + r_mod_of[k] : 0;
+        const int np = k < K ? C.F->npieces[gm] : 0;
+        int incl = np;
+        for (int off = 1; off < 32; off <<= 1) {
+            const int v = __shfl_up_sync(kFull, incl, off);
+            if (lane >= off) incl += v;
+        }
+        const int pb = pb0 + incl - np;
+        pb0 += __shfl_sync(kFull, incl, 31);
+        if (k < K) {
+            ws_out_metaop x;
+            x.module = r_mod_of[k];
+            x.level = r_level[k];
+            x.first_layer = 0;
+            x.length = B.mod_layers[gm];
+            x.piece_begin = pb;
+            x.piece_count = np;
+            x.upper_n = r_up_n[k];
+            x.upper_l = r_up_l[k];
+            x.lower_n = r_lo_n[k];
+            x.lower_l = r_lo_l[k];
+            mo[k] = x;
             const double* src = C.F->pieces + 5 * C.F->piece_off[gm];
-            for (int i = lane; i < np; i += 32)
+            for (int i = 0; i < np; ++i)
                 pc[pb + i] = ws_out_piece{src[5 * i], src[5 * i + 1], src[5 * i + 2], src[5 * i + 3], src[5 * i + 4]};
-            pb += np;
         }
     }
     const double* cstar = reinterpret_cast<const double*>(rec + RL.cstar);
     const int* lfw = reinterpret_cast<const int*>(rec + RL.lvl_fw);
     const int* lnw = reinterpret_cast<const int*>(rec + RL.lvl_nw);
     for (int l = lane; l < nL; l += 32) lv[l] = ws_out_level{cstar[l], lfw[l], lnw[l]};
-    if (lane == 0) {  // MetaGraph edges in std::set<pair<string,string>> order
-        int ne = 0;
-        for (int ra = 0; ra < K; ++ra) {
-            const int a = by_rank[ra];
-            for (uint64_t s = r_succ[a]; s; s &= s - 1) ed[ne++] = ws_out_edge{a, by_rank[low_bit(s)]};
+    // MetaGraph edges in std::set<pair<string,string>> order: lane per source rank
+    for (int base = 0, ne0 = 0; base < K; base += 32) {
+        const int ra = base + lane;
+        const int a = ra < K ? by_rank[ra] : 0;
+        const uint64_t succ = ra < K ? r_succ[a] : 0;
+        const int cnt = popc64(succ);
+        int incl = cnt;
+        for (int off = 1; off < 32; off <<= 1) {
+            const int v = __shfl_up_sync(kFull, incl, off);
+            if (lane >= off) incl += v;
         }
+        int ne = ne0 + incl - cnt;
+        ne0 += __shfl_sync(kFull, incl, 31);
+        for (uint64_t s = succ; s; s &= s - 1) ed[ne++] = ws_out_edge{a, by_rank[low_bit(s)]};
     }
     const double* w_start = reinterpret_cast<const double*>(rec + RL.w_start);
     const double* w_dur = reinterpret_cast<const double*>(rec + RL.w_dur);
@@ -680,22 +693,41 @@ __global__ void __launch_bounds__(32 * kPlaceWarps, WS_PLACE_MINB) k_place(Place
         mem[d] = 0.0;
     }
     for (int g = lane; g < G; g += 32) chg[g] = 0;
-    for (int i = lane; i < C.n_isl; i += 32) islmask[i] = 0;
+    __syncwarp();
+    for (int i = 0; i < C.n_isl; ++i) {  // island masks, one ballot per 32 devices
+        uint64_t m = 0;
+        for (int base = 0; base < N; base += 32) {
+            const int d = base + lane;
+            m |= static_cast<uint64_t>(__ballot_sync(kFull, d < N && isl[d] == i)) << base;
+        }
+        if (lane == 0) islmask[i] = m;
+    }
+    for (int w = lane; w < nW; w += 32) {
+        int cur = 0;  // sequential-ablation cursor (:331-338): sum of earlier n, mod N
+        for (int e = 0; e < w_eb[w]; ++e) cur += e_n[e];
+        w_cursor[w] = cur % N;
+        for (int i = 0; i < w_ec[w]; ++i) e_wave[w_eb[w] + i] = w;
+    }
+    __syncwarp();
+    for (int e = lane; e < nE; e += 32) {  // previous entry of the same MetaOp
+        int pv = -1;
+        for (int j = e - 1; j >= 0; --j)
+            if (e_k[j] == e_k[e]) {
+                pv = j;
+                break;
+            }
+        e_prev[e] = pv;
+    }
+    for (int k = lane; k < K; k += 32) {  // last entry / wave of each MetaOp
+        for (int j = nE - 1; j >= 0; --j)
+            if (e_k[j] == k) {
+                lastent[k] = j;
+                lastw[k] = e_wave[j];
+                break;
+            }
+    }
     __syncwarp();
     if (lane == 0) {
-        for (int d = 0; d < N; ++d) islmask[isl[d]] |= 1ull << d;
-        int cur = 0;
-        for (int w = 0; w < nW; ++w) {
-            w_cursor[w] = cur;  // sequential-ablation cursor (:331-338)
-            for (int i = 0; i < w_ec[w]; ++i) {
-                const int e = w_eb[w] + i;
-                e_wave[e] = w;
-                e_prev[e] = lastent[e_k[e]];
-                lastent[e_k[e]] = e;
-                lastw[e_k[e]] = w;
-                cur = (cur + e_n[e]) % N;
-            }
-        }
         int contig = 1;
         for (int i = 0; i < C.n_isl; ++i) {
             const uint64_t m = islmask[i];
