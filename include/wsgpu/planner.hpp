@@ -366,6 +366,10 @@ PlannerResult decode_result(const Problem& prob, const ws_plan_result& res, cons
                             bool build_graph = true);
 // write_plan() text of a decoded result, or "error <Class>: <what>" for a failure.
 std::string plan_text_or_error(const Problem& prob, const ws_plan_result& res, const std::uint8_t* arena);
+// Canonical evaluation text (simulate_plan + validate_plan report) of one
+// evaluated plan, or the plan's error text; see csrc/host/sim_text.cpp.
+std::string sim_text(const Problem& prob, const ws_plan_result& res, const std::uint8_t* plan_arena,
+                     const ws_sim_result& sim, const std::uint8_t* sim_arena);
 [[noreturn]] void throw_result_error(const Problem& prob, const ws_plan_result& res);
 
 // Deterministic scenario generator (scenarios.hpp restated): the measurement

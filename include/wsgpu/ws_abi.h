@@ -100,6 +100,7 @@ typedef struct ws_plan_rec {
     double eps;                  /* AllocatorOptions::eps                               */
     double drop_floor;           /* AllocatorOptions::drop_floor                        */
     double grad_mult;            /* PlannerOptions::grad_opt_multiplier                 */
+    double intra_bw, inter_bw;   /* ClusterTopology bandwidths (simulator, flow_duration) */
 } ws_plan_rec;
 
 /* Structure-of-arrays batch.  All pointers address the same memory space
@@ -215,6 +216,54 @@ typedef struct ws_out_flow {
     int32_t mode, pad;
 } ws_out_flow;
 
+/* ---- plan evaluation: simulate_plan + validate_plan (simulate.hpp, validate.hpp)
+ * Evaluates planned records (ws_plan_result + arena, from the planner or any
+ * producer of the same layout) on the device. */
+typedef struct ws_sim_opts {   /* SimulatorOptions (simulate.hpp:69-73)                */
+    double backward_ratio;     /* backward compute as a multiple of forward (2.0)       */
+    int32_t zero_volumes;      /* free transmissions                                   */
+    int32_t skip_sync;         /* no parameter synchronization                         */
+} ws_sim_opts;
+
+typedef struct ws_sim_result {
+    int32_t status;         /* WS_STATUS_OK, or the plan's own status (not evaluated)  */
+    int32_t valid;          /* ValidationReport::ok (validate.hpp:58-188)              */
+    int32_t n_violations;   /* violations found (the first WS_SIM_MAX_VIOLATIONS kept)  */
+    int32_t timeline_items; /* SimulationReport::timeline.size()                       */
+    double makespan;        /* SimulationReport (simulate.hpp:53-67)                   */
+    double fwd_bwd_seconds, param_sync_seconds, send_recv_seconds;
+    double fwd_bwd_fraction, param_sync_fraction, send_recv_fraction;
+    double total_transferred_bytes, total_inter_island_bytes;
+    uint64_t offset;        /* this plan's record in the simulation arena:             */
+    uint64_t size;          /*   busy[N] f64, busy_mask u64, mem[N] f64, util[K] f64,   */
+                            /*   util_mask u64, ws_out_violation[min(n, MAX)]          */
+} ws_sim_result;
+
+#define WS_SIM_MAX_VIOLATIONS 16
+
+/* One ValidationReport::fail() call; the host rebuilds the reference message. */
+enum ws_violation {
+    WS_V_UNKNOWN_ENTITY = 1, /* "wave <w>: unknown entity m<a>"                               */
+    WS_V_DUPLICATE = 2,      /* "wave <w>: entity m<a> appears twice"                          */
+    WS_V_SPAN = 3,           /* "wave <w>: entity m<a> recorded span <x> != recomputed <y>"    */
+    WS_V_SPAN_DURATION = 4,  /* "wave <w>: entry span exceeds wave duration"                   */
+    WS_V_WAVE_DEVICES = 5,   /* "wave <w>: allocations exceed device count"                    */
+    WS_V_WORK = 6,           /* "entity m<a>: executed <b> of <x> layers"                      */
+    WS_V_CAPACITY = 7,       /* "capacity exceeded at t=<x>: <a> devices"                      */
+    WS_V_OVERLAP = 8,        /* "entity m<a>: overlapping execution intervals"                 */
+    WS_V_DEPENDENCY = 9,     /* "dependency m<a> -> m<b> violated: consumer starts at <x> ..." */
+    WS_V_UNPLACED = 10,      /* "wave <w>: entity m<a> unplaced"                               */
+    WS_V_DEVICE_COUNT = 11,  /* "wave <w>: entity m<a> placed on <b> devices, needs <x>"       */
+    WS_V_UNKNOWN_DEVICE = 12,/* "unknown device <a>" (a = device index)                        */
+    WS_V_DEVICE_TWICE = 13,  /* "wave <w>: device <a> assigned twice" (a = device index)       */
+    WS_V_MEMORY = 14         /* "device <a> memory <x> exceeds capacity <y as u64 bits>"       */
+};
+
+typedef struct ws_out_violation {
+    int32_t code, wave, a, b;
+    double x, y;
+} ws_out_violation;
+
 /* ---- context & planning --------------------------------------------------- */
 typedef struct ws_ctx ws_ctx;
 
@@ -248,7 +297,8 @@ int ws_last_launch_count(const ws_ctx* ctx);
 int ws_last_kernel_ms(const ws_ctx* ctx, double* out, int n);
 
 /* Global best candidate: on-device argmin of key over the staged
- * batch, key = end_time / lower_bound (mode 0) or end_time (mode 1); infeasible
+ * batch, key = end_time / lower_bound (mode 0), end_time (mode 1), or the
+ * simulated makespan of the last ws_simulate_staged (mode 2); infeasible
  * plans count as +inf; ties go to the smaller index.  Writes {key, index}. */
 int ws_best_staged(ws_ctx* ctx, int mode, double* key, int64_t* index, void* stream);
 
@@ -258,6 +308,25 @@ int ws_debug_phase_cycles(unsigned long long* out, int n);
 
 /* Arena capacity sufficient for any batch whose plans stay within the limits. */
 uint64_t ws_arena_bound(const ws_batch* in);
+
+/* Replaces wavesched::simulate_plan + validate_plan (simulate.hpp:322-324,
+ * validate.hpp:58-188) for every planned record of the last ws_plan_staged /
+ * ws_plan_batch_host call on this ctx, on the device (plans that failed keep
+ * their status and are not evaluated).  Results stay on the device until
+ * ws_fetch_sim. */
+int ws_simulate_staged(ws_ctx* ctx, const ws_sim_opts* opts, void* stream);
+int ws_fetch_sim(ws_ctx* ctx, ws_sim_result* out, uint8_t* arena, uint64_t arena_cap, uint64_t* arena_used,
+                 void* stream);
+/* Same over plan records supplied from HOST memory (any producer of the
+ * ws_plan_result + arena layout, e.g. an edited plan): stages `in` and the
+ * records, simulates + validates, and writes HOST results. */
+int ws_simulate_batch_host(ws_ctx* ctx, const ws_batch* in, const ws_plan_result* plans, const uint8_t* plan_arena,
+                           uint64_t plan_arena_bytes, const ws_sim_opts* opts, ws_sim_result* out, uint8_t* arena,
+                           uint64_t arena_cap, uint64_t* arena_used, void* stream);
+/* Simulation-arena capacity for a batch (every plan evaluated). */
+uint64_t ws_sim_arena_bound(const ws_batch* in);
+/* Device time (ms) of the last simulation launch. */
+double ws_last_sim_ms(const ws_ctx* ctx);
 
 #ifdef __cplusplus
 }

@@ -47,6 +47,10 @@ const ws_batch* wsx_encode(wsx_set* s, int32_t pinned);
 uint64_t wsx_encoded_bytes(const wsx_set* s);
 /* Plan text (write_plan) or "error <Class>: <what>\n" of problem i; free with wsx_free_str. */
 char* wsx_result_text(const wsx_set* s, int32_t i, const ws_plan_result* results, const uint8_t* arena);
+/* Canonical evaluation text (simulate_plan + validate_plan, see sim_text.cpp)
+ * of problem i, or its planner error text; free with wsx_free_str. */
+char* wsx_sim_text(const wsx_set* s, int32_t i, const ws_plan_result* results, const uint8_t* arena,
+                   const ws_sim_result* sims, const uint8_t* sim_arena);
 char* wsx_dump_workload(const wsx_set* s, int32_t i);
 char* wsx_dump_topology(const wsx_set* s, int32_t i);
 void wsx_free_str(char* p);

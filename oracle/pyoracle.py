@@ -25,6 +25,9 @@ def oracle():
         lib = C.CDLL(str(ORACLE_LIB))
         lib.wso_plan_batch.restype = C.c_int
         lib.wso_plan_batch.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint64, C.POINTER(C.c_uint64)]
+        lib.wso_simulate_batch.restype = C.c_int
+        lib.wso_simulate_batch.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                           C.c_void_p, C.c_uint64, C.POINTER(C.c_uint64)]
         _oracle = lib
     return _oracle
 
@@ -38,10 +41,48 @@ def plan_batch(pset):
     return out
 
 
+def simulate_batch(pset, res, **sim_opts):
+    """simulate_plan + validate_plan of planned records on the CPU oracle; returns SimResults."""
+    from paper_2409_03365_b200 import SimResults, make_sim_options
+    lib = oracle()
+    cap = pset.sim_arena_bound()
+    out = SimResults(len(pset), cap)
+    lib.wso_simulate_batch(pset.batch, res.results, res.arena, C.byref(make_sim_options(**sim_opts)),
+                           out.results, out.arena, cap, C.byref(out.arena_used))
+    return out
+
+
 class RefOpts(C.Structure):
     _fields_ = [("eps", C.c_double), ("max_iters", C.c_int), ("drop_floor", C.c_double),
                 ("sequential", C.c_int), ("bt_depth", C.c_int), ("bt_branching", C.c_int),
                 ("grad_mult", C.c_double), ("synth_noise", C.c_double), ("synth_seed", C.c_ulonglong)]
+
+
+class RefSimOpts(C.Structure):
+    _fields_ = [("backward_ratio", C.c_double), ("zero_volumes", C.c_int), ("skip_sync", C.c_int)]
+
+
+def ref_sim_options(backward_ratio=2.0, zero_volumes=False, skip_sync=False) -> RefSimOpts:
+    return RefSimOpts(backward_ratio, 1 if zero_volumes else 0, 1 if skip_sync else 0)
+
+
+def ref_sim_text(workload: str, topology: str, sim: dict | None = None, **opts) -> str:
+    """Reference plan_workload + simulate_plan + validate_plan: canonical evaluation text."""
+    return _s(ref().wsref_sim_text(workload.encode(), topology.encode(), C.byref(ref_options(**opts)),
+                                   C.byref(ref_sim_options(**(sim or {})))))
+
+
+def ref_sim_plan_text(plan_text: str, **sim) -> str:
+    """Reference simulate_plan + validate_plan of a plan file (parse_plan)."""
+    return _s(ref().wsref_sim_plan_text(plan_text.encode(), C.byref(ref_sim_options(**sim))))
+
+
+def ref_sweep_sim(i: int, **sim) -> str:
+    return _s(ref().wsref_sweep_sim(i, C.byref(ref_sim_options(**sim))))
+
+
+def ref_sweep_sim_bench(start: int, count: int, threads: int) -> float:
+    return ref().wsref_sweep_sim_bench(start, count, threads)
 
 
 def ref_available() -> bool:
@@ -66,6 +107,14 @@ def ref():
         lib.wsref_sweep_plan.argtypes = [C.c_long]
         lib.wsref_sweep_bench.restype = C.c_double
         lib.wsref_sweep_bench.argtypes = [C.c_long, C.c_long, C.c_int, C.POINTER(C.c_long)]
+        lib.wsref_sim_text.restype = vp
+        lib.wsref_sim_text.argtypes = [C.c_char_p, C.c_char_p, C.POINTER(RefOpts), C.POINTER(RefSimOpts)]
+        lib.wsref_sim_plan_text.restype = vp
+        lib.wsref_sim_plan_text.argtypes = [C.c_char_p, C.POINTER(RefSimOpts)]
+        lib.wsref_sweep_sim.restype = vp
+        lib.wsref_sweep_sim.argtypes = [C.c_long, C.POINTER(RefSimOpts)]
+        lib.wsref_sweep_sim_bench.restype = C.c_double
+        lib.wsref_sweep_sim_bench.argtypes = [C.c_long, C.c_long, C.c_int]
         lib.wsref_latency_ms.restype = C.c_double
         lib.wsref_latency_ms.argtypes = [C.c_char_p, C.c_int, C.c_int, C.c_int]
         _ref = lib

@@ -13,6 +13,8 @@
 
 #include "wavesched/planner.hpp"
 #include "wavesched/scenarios.hpp"
+#include "wavesched/simulate.hpp"
+#include "wavesched/validate.hpp"
 
 // The acceptance suite is compiled in place (not copied) so its fuzz
 // generator (acceptance.cpp:284-323) and tiny instances are reused verbatim.
@@ -34,6 +36,11 @@ typedef struct wsref_opts {
     double synth_noise;
     unsigned long long synth_seed;
 } wsref_opts;
+typedef struct wsref_sim_opts {
+    double backward_ratio;
+    int zero_volumes;
+    int skip_sync;
+} wsref_sim_opts;
 }
 
 namespace {
@@ -88,6 +95,37 @@ std::string outcome(const WorkloadSpec& spec, const ClusterTopology& topo, const
     } catch (const Error& e) {
         return std::string("error Error: ") + e.what() + "\n";
     }
+}
+
+// Canonical evaluation text of a plan (the parity format shared with the
+// oracle and the CUDA evaluator, see paper_2409_03365_b200/csrc/host/sim_text.cpp):
+// simulate_plan's report scalars and per-device / per-entity maps, then
+// validate_plan's verdict and its first 16 violation messages.
+std::string sim_text(const ExecutionPlan& plan, const wsref_sim_opts* so) {
+    SimulatorOptions opt;
+    if (so) {
+        opt.backward_ratio = so->backward_ratio;
+        opt.zero_volumes = so->zero_volumes != 0;
+        opt.skip_sync = so->skip_sync != 0;
+    }
+    const SimulationReport r = simulate_plan(plan, opt);
+    const ValidationReport v = validate_plan(plan);
+    std::string out = "sim makespan=" + fmt_exact(r.makespan) + " fwd_bwd=" + fmt_exact(r.fwd_bwd_seconds) +
+                      " param_sync=" + fmt_exact(r.param_sync_seconds) + " send_recv=" +
+                      fmt_exact(r.send_recv_seconds) + " fracs=" + fmt_exact(r.fwd_bwd_fraction) + "," +
+                      fmt_exact(r.param_sync_fraction) + "," + fmt_exact(r.send_recv_fraction) +
+                      " transferred=" + fmt_exact(r.total_transferred_bytes) +
+                      " inter=" + fmt_exact(r.total_inter_island_bytes) +
+                      " timeline=" + std::to_string(r.timeline.size()) + "\n";
+    out += "busy";
+    for (const auto& [d, b] : r.per_device_busy) out += " " + std::to_string(d) + "=" + fmt_exact(b);
+    out += "\nmem";
+    for (const auto& [d, b] : r.per_device_peak_memory) out += " " + std::to_string(d) + "=" + fmt_exact(b);
+    out += "\nutil";
+    for (const auto& [id, u] : r.per_entity_utilization) out += " " + id + "=" + fmt_exact(u);
+    out += "\nvalid " + std::to_string(v.ok ? 1 : 0) + " " + std::to_string(v.violations.size()) + "\n";
+    for (std::size_t i = 0; i < v.violations.size() && i < 16; ++i) out += "v " + v.violations[i] + "\n";
+    return out;
 }
 
 Scenario sweep(long i) {
@@ -191,6 +229,74 @@ double wsref_sweep_bench(long start, long count, int threads, long* infeasible) 
     const double sec = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     if (infeasible) *infeasible = bad.load();
     return static_cast<double>(count) / sec;
+}
+
+// Reference plan_workload + simulate_plan + validate_plan: the canonical
+// evaluation text (or the planner's "error ..." outcome).
+char* wsref_sim_text(const char* workload, const char* topology, const wsref_opts* o, const wsref_sim_opts* so) {
+    try {
+        WorkloadSpec spec = parse_workload(workload);
+        ClusterTopology topo = parse_topology(topology);
+        try {
+            return dup(sim_text(plan_workload(spec, topo, to_opts(o)).plan, so));
+        } catch (const Error&) {
+            return dup(outcome(spec, topo, to_opts(o)));
+        }
+    } catch (const Error& e) {
+        return dup(std::string("error Parse: ") + e.what() + "\n");
+    }
+}
+
+// simulate_plan + validate_plan of a plan file (parse_plan, plan_io.hpp:112-255).
+char* wsref_sim_plan_text(const char* plan_text, const wsref_sim_opts* so) {
+    try {
+        return dup(sim_text(parse_plan(plan_text), so));
+    } catch (const Error& e) {
+        return dup(std::string("error Parse: ") + e.what() + "\n");
+    }
+}
+
+// Evaluation text of sweep mixture i (default planner options).
+char* wsref_sweep_sim(long i, const wsref_sim_opts* so) {
+    Scenario sc = sweep(i);
+    const WorkloadSpec spec = parse_workload(sc.workload_text);
+    const ClusterTopology topo = parse_topology(sc.topology_text);
+    try {
+        return dup(sim_text(plan_workload(spec, topo).plan, so));
+    } catch (const Error&) {
+        return dup(outcome(spec, topo, PlannerOptions{}));
+    }
+}
+
+// CPU baseline of the evaluation path: plan_workload + simulate_plan +
+// validate_plan over sweep mixtures [start, start+count) on `threads` threads.
+double wsref_sweep_sim_bench(long start, long count, int threads) {
+    std::vector<WorkloadSpec> specs(count);
+    std::vector<ClusterTopology> topos(count);
+    for (long i = 0; i < count; ++i) {
+        Scenario sc = sweep(start + i);
+        specs[i] = parse_workload(sc.workload_text);
+        topos[i] = parse_topology(sc.topology_text);
+    }
+    std::atomic<long> next{0};
+    auto worker = [&] {
+        for (long i; (i = next.fetch_add(1)) < count;) {
+            try {
+                PlannerResult r = plan_workload(specs[i], topos[i]);
+                SimulationReport sr = simulate_plan(r.plan);
+                ValidationReport vr = validate_plan(r.plan);
+                (void)sr;
+                (void)vr;
+            } catch (const Error&) {
+            }
+        }
+    };
+    const auto t0 = std::chrono::steady_clock::now();
+    std::vector<std::thread> pool;
+    for (int t = 0; t < threads; ++t) pool.emplace_back(worker);
+    for (auto& th : pool) th.join();
+    return static_cast<double>(count) /
+           std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
 }
 
 // Single-plan latency of the reference planner (median of `reps`, ms).

@@ -18,7 +18,8 @@ __all__ = [
     "LIB_PATH", "Options", "PlanResult", "ProblemSet", "Planner", "plan_workload", "PlannerError",
     "ParseError", "InfeasibleError", "InvariantError", "CyclicWorkload", "UnknownModule", "EmptyWorkload",
     "InsufficientProfile", "DegenerateFit", "OutOfRange", "NoValidAllocation", "EmptyLevel",
-    "PlacementInfeasible", "LimitExceeded", "WS_STATUS", "raise_for_text",
+    "PlacementInfeasible", "LimitExceeded", "WS_STATUS", "raise_for_text", "SimOptions", "SimResult",
+    "SimResults", "make_sim_options",
 ]
 
 
@@ -113,6 +114,25 @@ class PlanResult(C.Structure):
                 ("offset", C.c_uint64), ("size", C.c_uint64)]
 
 
+class SimOptions(C.Structure):
+    """SimulatorOptions (simulate.hpp:69-73) as ws_sim_opts (ws_abi.h)."""
+    _fields_ = [("backward_ratio", C.c_double), ("zero_volumes", C.c_int32), ("skip_sync", C.c_int32)]
+
+
+def make_sim_options(backward_ratio: float = 2.0, zero_volumes: bool = False, skip_sync: bool = False) -> SimOptions:
+    return SimOptions(backward_ratio, 1 if zero_volumes else 0, 1 if skip_sync else 0)
+
+
+class SimResult(C.Structure):
+    """ws_sim_result (ws_abi.h): SimulationReport scalars + ValidationReport verdict."""
+    _fields_ = [("status", C.c_int32), ("valid", C.c_int32), ("n_violations", C.c_int32),
+                ("timeline_items", C.c_int32), ("makespan", C.c_double), ("fwd_bwd_seconds", C.c_double),
+                ("param_sync_seconds", C.c_double), ("send_recv_seconds", C.c_double),
+                ("fwd_bwd_fraction", C.c_double), ("param_sync_fraction", C.c_double),
+                ("send_recv_fraction", C.c_double), ("total_transferred_bytes", C.c_double),
+                ("total_inter_island_bytes", C.c_double), ("offset", C.c_uint64), ("size", C.c_uint64)]
+
+
 def _load() -> C.CDLL:
     if not LIB_PATH.exists():
         raise ImportError(f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'`")
@@ -147,6 +167,13 @@ def _load() -> C.CDLL:
         "wsx_plan_workload_text": (vp, [C.c_char_p, C.c_char_p, C.POINTER(Options)]),
         "wsx_algorithmic_bytes": (None, [vp, vp, vp, C.POINTER(u64), C.POINTER(u64)]),
         "wsx_host_alloc": (vp, [u64]),
+        "wsx_sim_text": (vp, [vp, i32, vp, vp, vp, vp]),
+        "ws_simulate_staged": (C.c_int, [vp, C.POINTER(SimOptions), vp]),
+        "ws_fetch_sim": (C.c_int, [vp, vp, vp, u64, C.POINTER(u64), vp]),
+        "ws_simulate_batch_host": (C.c_int, [vp, vp, vp, vp, u64, C.POINTER(SimOptions), vp, vp, u64,
+                                             C.POINTER(u64), vp]),
+        "ws_sim_arena_bound": (u64, [vp]),
+        "ws_last_sim_ms": (C.c_double, [vp]),
         "wsx_host_free": (None, [vp]),
     }
     for name, (res, args) in sig.items():
@@ -231,6 +258,16 @@ class ProblemSet:
         return _take_str(lib.wsx_result_text(self._h, i, C.cast(results, C.c_void_p),
                                              C.cast(arena, C.c_void_p)))
 
+    def sim_arena_bound(self) -> int:
+        return int(lib.ws_sim_arena_bound(self.batch))
+
+    def sim_text(self, i: int, results: "Results", sims: "SimResults") -> str:
+        """Canonical simulate_plan + validate_plan text of problem i (see
+        csrc/host/sim_text.cpp), or its planner error text."""
+        return _take_str(lib.wsx_sim_text(self._h, i, C.cast(results.results, C.c_void_p),
+                                          C.cast(results.arena, C.c_void_p), C.cast(sims.results, C.c_void_p),
+                                          C.cast(sims.arena, C.c_void_p)))
+
     def algorithmic_bytes(self, res: "Results") -> tuple[int, int]:
         """SURVEY §8(d) compulsory (in, out) bytes of this set's plans."""
         a, b = C.c_uint64(), C.c_uint64()
@@ -271,6 +308,29 @@ class Results:
 
     def texts(self, pset: ProblemSet) -> list[str]:
         return [pset.text(i, self.results, self.arena) for i in range(self.n)]
+
+
+class SimResults:
+    """Host copy of one evaluation call: ws_sim_result[] + simulation arena
+    (page-locked, reusable like Results)."""
+
+    def __init__(self, n: int, arena_cap: int):
+        self._res_ptr = lib.wsx_host_alloc(C.sizeof(SimResult) * max(n, 1))
+        self._arena_ptr = lib.wsx_host_alloc(max(arena_cap, 8))
+        self.results = (SimResult * max(n, 1)).from_address(self._res_ptr)
+        self.arena = (C.c_uint8 * max(arena_cap, 8)).from_address(self._arena_ptr)
+        self.arena_used = C.c_uint64(0)
+        self.n = n
+        self.cap_plans = max(n, 1)
+        self.cap_arena = max(arena_cap, 8)
+
+    def fits(self, n: int, arena_cap: int) -> bool:
+        return n <= self.cap_plans and arena_cap <= self.cap_arena
+
+    __del__ = Results.__del__
+
+    def texts(self, pset: ProblemSet, res: Results) -> list[str]:
+        return [pset.sim_text(i, res, self) for i in range(self.n)]
 
 
 class Planner:
@@ -323,6 +383,36 @@ class Planner:
         key, idx = C.c_double(), C.c_int64()
         self._ok(lib.ws_best_staged(self._h, mode, C.byref(key), C.byref(idx), stream))
         return key.value, idx.value
+
+    def _sim_out(self, pset: ProblemSet, out: SimResults | None) -> tuple[SimResults, int]:
+        cap = pset.sim_arena_bound()
+        if out is None or not out.fits(len(pset), cap):
+            out = SimResults(len(pset), cap)
+        out.n = len(pset)
+        return out, cap
+
+    def simulate_staged(self, stream: int | None = None, **sim_opts):
+        """simulate_plan + validate_plan of every record of the last plan_staged,
+        on the device (results stay there until fetch_sim)."""
+        self._ok(lib.ws_simulate_staged(self._h, C.byref(make_sim_options(**sim_opts)), stream))
+
+    def fetch_sim(self, pset: ProblemSet, stream: int | None = None, out: SimResults | None = None) -> SimResults:
+        out, cap = self._sim_out(pset, out)
+        self._ok(lib.ws_fetch_sim(self._h, out.results, out.arena, cap, C.byref(out.arena_used), stream))
+        return out
+
+    def simulate(self, pset: ProblemSet, res: Results, stream: int | None = None, out: SimResults | None = None,
+                 **sim_opts) -> SimResults:
+        """Evaluate host plan records (any producer of the ws_abi.h layout)."""
+        out, cap = self._sim_out(pset, out)
+        self._ok(lib.ws_simulate_batch_host(self._h, pset.batch, res.results, res.arena, res.arena_used.value,
+                                            C.byref(make_sim_options(**sim_opts)), out.results, out.arena, cap,
+                                            C.byref(out.arena_used), stream))
+        return out
+
+    def sim_ms(self) -> float:
+        """Device ms of the last k_sim launch."""
+        return float(lib.ws_last_sim_ms(self._h))
 
     @property
     def launch_count(self) -> int:

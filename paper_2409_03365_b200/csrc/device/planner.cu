@@ -24,6 +24,7 @@
 #include "fit.cuh"
 #include "place.cuh"
 #include "sched.cuh"
+#include "sim.cuh"
 
 using namespace wsdev;
 
@@ -71,15 +72,16 @@ __global__ void k_clamp_count(int32_t* count) {
 }
 
 // Global min-loc over plan keys; ties -> smaller index.
-__global__ void k_best(const ws_plan_result* res, int n, int mode, double* out_key, long long* out_idx) {
+__global__ void k_best(const ws_plan_result* res, const ws_sim_result* sim, int n, int mode, double* out_key,
+                       long long* out_idx) {
     __shared__ double sk[1024];
     __shared__ long long si[1024];
     double bk = __longlong_as_double(0x7ff0000000000000ll);  // +inf
     long long bi = -1;
     for (int p = threadIdx.x; p < n; p += blockDim.x) {
         const ws_plan_result& r = res[p];
-        if (r.status != WS_STATUS_OK) continue;
-        const double k = mode == 0 ? r.end_time / r.lower_bound : r.end_time;
+        if (r.status != WS_STATUS_OK || (mode == 2 && sim[p].status != WS_STATUS_OK)) continue;
+        const double k = mode == 0 ? r.end_time / r.lower_bound : (mode == 1 ? r.end_time : sim[p].makespan);
         if (bi < 0 || k < bk || (k == bk && p < bi)) bk = k, bi = p;
     }
     sk[threadIdx.x] = bk;
@@ -165,6 +167,13 @@ struct ws_ctx {
     cudaEvent_t cev[kMaxChunks + 2] = {};       // chunk hand-offs + fork/join
     int chunks = 1;  // measured: concurrent k_sched/k_place chunks share the I-cache and lose ($WSGPU_CHUNKS)
     double kernel_ms[3] = {0, 0, 0};  // k_fit, k_sched, k_place (+ retry pass)
+    // plan evaluation (k_sim)
+    DevBuf sim_res, sim_arena, sim_scratch, sim_top;
+    uint64_t sim_cap = 0;           // ws_sim_arena_bound of the staged batch
+    bool records_on_device = false; // the last planning call left its records in ctx memory
+    bool sim_valid = false;         // sim_res holds the evaluation of the staged records
+    cudaEvent_t sev[2] = {};
+    double sim_ms = 0;
     // direct output: kernels write headers/records straight into the caller's
     // page-locked host buffers (zero-copy), set only inside ws_plan_batch_host
     ws_plan_result* d_results = nullptr;
@@ -328,8 +337,11 @@ int ws_ctx_create(int device, ws_ctx** out) {
         delete c;
         return 1;
     }
+    for (auto& e : c->sev)
+        if (e) cudaEventDestroy(e);
     for (auto& e : c->ev) cudaEventCreate(&e);
     for (auto& e : c->cev) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+    for (auto& e : c->sev) cudaEventCreate(&e);
     if (cudaStreamCreateWithFlags(&c->stream2, cudaStreamNonBlocking) != cudaSuccess) {
         delete c;
         return 1;
@@ -373,6 +385,9 @@ int ws_stage_batch(ws_ctx* ctx, const ws_batch* in, void* stream) {
     ctx->caps = batch_caps(in->plans, P, false);
     ctx->caps_hard = batch_caps(in->plans, P, true);
     ctx->arena_cap = ws_arena_bound(in);
+    ctx->sim_cap = ws_sim_arena_bound(in);
+    ctx->records_on_device = false;
+    ctx->sim_valid = false;
     // longest-processing-time launch order: descending modules x devices, by a
     // stable counting sort over the small key range (O(plans) on the host)
     constexpr int kKeys = (WS_MAX_MODULES + 1) * (WS_MAX_DEVICES + 9);
@@ -450,6 +465,8 @@ int ws_plan_staged(ws_ctx* ctx, void* stream) {
     }
     CK(cudaEventRecord(ctx->ev[2], st));
     CK(cudaGetLastError());
+    ctx->records_on_device = ctx->d_arena == nullptr;
+    ctx->sim_valid = false;
     return 0;
 }
 
@@ -537,7 +554,9 @@ int ws_best_staged(ws_ctx* ctx, int mode, double* key, int64_t* index, void* str
     cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
     auto* kb = ctx->best.as<double>();
     auto* ib = reinterpret_cast<long long*>(kb + 1);
-    k_best<<<1, 1024, 0, st>>>(ctx->results.as<ws_plan_result>(), ctx->dview.n_plans, mode, kb, ib);
+    if (mode == 2 && !ctx->sim_valid) return fail(ctx, "ws_best_staged: mode 2 needs ws_simulate_staged first");
+    k_best<<<1, 1024, 0, st>>>(ctx->results.as<ws_plan_result>(), ctx->sim_res.as<ws_sim_result>(),
+                               ctx->dview.n_plans, mode, kb, ib);
     double hk = 0;
     long long hi = -1;
     CK(cudaMemcpyAsync(&hk, kb, sizeof(double), cudaMemcpyDeviceToHost, st));
@@ -547,5 +566,83 @@ int ws_best_staged(ws_ctx* ctx, int mode, double* key, int64_t* index, void* str
     *index = hi;
     return 0;
 }
+
+
+
+// ---- plan evaluation (simulate_plan + validate_plan) -------------------------
+int ws_simulate_staged(ws_ctx* ctx, const ws_sim_opts* opts, void* stream) {
+    cudaSetDevice(ctx->device);
+    cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
+    if (!ctx->records_on_device)
+        return fail(ctx, "ws_simulate_staged: no device-resident plan records (plan with ws_plan_staged, "
+                         "or evaluate host records with ws_simulate_batch_host)");
+    const int P = ctx->dview.n_plans;
+    const LaunchCaps& lh = ctx->caps_hard;
+    SimArgs A{};
+    A.B = ctx->dview;
+    A.plans = ctx->results.as<ws_plan_result>();
+    A.parena = ctx->arena.as<uint8_t>();
+    A.opt = opts ? *opts : ws_sim_opts{2.0, 0, 0};
+    A.caps = SimCaps{lh.pl.G, lh.rec.W, lh.pl.IS, lh.M, lh.rec.E};
+    A.SL = make_sim_layout(A.caps);
+    A.n_plans = P;
+    if (!ctx->sim_res.ensure(sizeof(ws_sim_result) * std::max(P, 1)) || !ctx->sim_arena.ensure(ctx->sim_cap) ||
+        !ctx->sim_scratch.ensure(std::max<uint64_t>(ctx->arena_cap, 8)) || !ctx->sim_top.ensure(64))
+        return fail(ctx, "cudaMalloc simulation buffers");
+    A.scratch = ctx->sim_scratch.as<uint8_t>();
+    A.out = ctx->sim_res.as<ws_sim_result>();
+    A.arena = ctx->sim_arena.as<uint8_t>();
+    A.arena_top = ctx->sim_top.as<unsigned long long>();
+    A.arena_cap = ctx->sim_cap;
+    const int smem = kSimWarps * A.SL.bytes;
+    if (smem > kSmemLimit) return fail(ctx, "ws_simulate_staged: per-warp working set exceeds shared memory");
+    CK(cudaFuncSetAttribute(k_sim, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    CK(cudaMemsetAsync(A.arena_top, 0, 8, st));
+    CK(cudaEventRecord(ctx->sev[0], st));
+    if (P > 0) k_sim<<<(P + kSimWarps - 1) / kSimWarps, 32 * kSimWarps, smem, st>>>(A);
+    CK(cudaEventRecord(ctx->sev[1], st));
+    CK(cudaGetLastError());
+    ctx->sim_valid = true;
+    return 0;
+}
+
+int ws_fetch_sim(ws_ctx* ctx, ws_sim_result* out, uint8_t* arena, uint64_t arena_cap, uint64_t* arena_used,
+                 void* stream) {
+    cudaSetDevice(ctx->device);
+    cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
+    if (!ctx->sim_valid) return fail(ctx, "ws_fetch_sim: nothing simulated");
+    const int P = ctx->dview.n_plans;
+    unsigned long long top = 0;
+    if (P) CK(cudaMemcpyAsync(out, ctx->sim_res.p, sizeof(ws_sim_result) * P, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(&top, ctx->sim_top.p, sizeof(top), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    float ms = 0;
+    if (cudaEventElapsedTime(&ms, ctx->sev[0], ctx->sev[1]) == cudaSuccess) ctx->sim_ms = ms;
+    if (top > ctx->sim_cap) top = ctx->sim_cap;
+    if (top > arena_cap) return fail(ctx, "ws_fetch_sim: arena buffer too small");
+    if (top) CK(cudaMemcpyAsync(arena, ctx->sim_arena.p, top, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    *arena_used = top;
+    return 0;
+}
+
+int ws_simulate_batch_host(ws_ctx* ctx, const ws_batch* in, const ws_plan_result* plans, const uint8_t* plan_arena,
+                           uint64_t plan_arena_bytes, const ws_sim_opts* opts, ws_sim_result* out, uint8_t* arena,
+                           uint64_t arena_cap, uint64_t* arena_used, void* stream) {
+    cudaSetDevice(ctx->device);
+    cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
+    if (ws_stage_batch(ctx, in, stream)) return 1;
+    const int P = in->n_plans;
+    ctx->arena_cap = std::max<uint64_t>(plan_arena_bytes, 8);
+    if (!ctx->results.ensure(sizeof(ws_plan_result) * std::max(P, 1)) || !ctx->arena.ensure(ctx->arena_cap))
+        return fail(ctx, "cudaMalloc plan records");
+    if (P) CK(cudaMemcpyAsync(ctx->results.p, plans, sizeof(ws_plan_result) * P, cudaMemcpyHostToDevice, st));
+    if (plan_arena_bytes) CK(cudaMemcpyAsync(ctx->arena.p, plan_arena, plan_arena_bytes, cudaMemcpyHostToDevice, st));
+    ctx->records_on_device = true;
+    if (ws_simulate_staged(ctx, opts, stream)) return 1;
+    return ws_fetch_sim(ctx, out, arena, arena_cap, arena_used, stream);
+}
+
+double ws_last_sim_ms(const ws_ctx* ctx) { return ctx ? ctx->sim_ms : 0.0; }
 
 }  // extern "C"

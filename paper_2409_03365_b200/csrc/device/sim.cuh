@@ -1,0 +1,683 @@
+// sim.cuh — k_sim: plan evaluation on the device, one warp per planned record.
+//
+// Replaces wavesched::simulate_plan (simulate.hpp:127-324: build_param_groups +
+// the event-driven replay) and validate_plan (validate.hpp:27-188, including
+// compute_device_memory) for a whole batch of plans.  Lanes own devices
+// (lane, lane+32): per-device availability clocks, compute seconds and
+// resident bytes live in registers; gang barriers and the global frontier are
+// warp max-reductions; flows and waves are walked in the reference's order so
+// every double is produced by the same operations in the same order.
+// Validation (a verdict plus the first WS_SIM_MAX_VIOLATIONS violation records)
+// runs on the same warp; the host rebuilds the reference messages.
+#pragma once
+#include "kcommon.cuh"
+
+namespace wsdev {
+
+struct SimCaps {
+    int G, W, IS, K, E;  // groups (param groups + entities), waves, islands, MetaOps, entries
+};
+
+struct SimSmLayout {
+    int isl;     // [IS] u64 island device masks
+    int chg;     // [G]  u64 devices charged per group (compute_device_memory)
+    int gmask;   // [G]  u64 devices per group (build_param_groups)
+    int gbytes;  // [G]  u64 gradient bytes per group
+    int pbytes;  // [G]  u64 pooled bytes per representative group
+    int pord;    // [G]  i32 pool representatives in device-list order
+    int ord;     // [W]  i32 wave replay order
+    int exec;    // [K]  i32 executed layers per MetaOp
+    int by_rank; // [K]  i32 MetaOps in id-string order
+    int gk;      // [K]  i32 group key per MetaOp
+    int lst;     // [E]  i32 one entity's intervals (validate)
+    int vio;     // [WS_SIM_MAX_VIOLATIONS] ws_out_violation
+    int bytes;
+};
+
+__host__ __device__ inline SimSmLayout make_sim_layout(const SimCaps& c) {
+    SimSmLayout L{};
+    int o = 0;
+    auto take = [&](int b) {
+        const int at = o;
+        o = (o + b + 7) & ~7;
+        return at;
+    };
+    L.isl = take(8 * c.IS);
+    L.chg = take(8 * c.G);
+    L.gmask = take(8 * c.G);
+    L.gbytes = take(8 * c.G);
+    L.pbytes = take(8 * c.G);
+    L.pord = take(4 * c.G);
+    L.ord = take(4 * c.W);
+    L.exec = take(4 * c.K);
+    L.by_rank = take(4 * c.K);
+    L.gk = take(4 * c.K);
+    L.lst = take(4 * c.E);
+    L.vio = take(static_cast<int>(sizeof(ws_out_violation)) * WS_SIM_MAX_VIOLATIONS);
+    L.bytes = o;
+    return L;
+}
+
+struct SimArgs {
+    ws_batch B;
+    const ws_plan_result* plans;  // planned records (device)
+    const uint8_t* parena;
+    uint8_t* scratch;             // per-entry scratch, mirrors the plan arena offsets
+    ws_sim_opts opt;
+    SimCaps caps;
+    SimSmLayout SL;
+    ws_sim_result* out;
+    uint8_t* arena;
+    unsigned long long* arena_top;
+    unsigned long long arena_cap;
+    int n_plans;
+};
+
+constexpr int kSimWarps = 4;
+
+// ScalingCurve::eval_batch_fraction (scaling.hpp:83-86) over a record's pieces
+__device__ __forceinline__ double eval_bf(const ws_out_piece* pc, int np, double c, double w, double n,
+                                          double frac) {
+    const ws_out_piece* p = pc;
+    if (!(n < 1.0)) {
+        const double nmax = pc[np - 1].n_hi;
+        const double x = n < nmax ? n : nmax;  // std::min(n, n_max_)
+        p = pc + np - 1;
+        for (int i = 0; i < np; ++i)  // locate (scaling.hpp:149-154)
+            if (x <= pc[i].n_hi + 1e-9) {
+                p = pc + i;
+                break;
+            }
+    }
+    return p->alpha + p->beta_c * c + p->beta_w * w * frac / n;
+}
+
+// sorted-device-list order of two device masks (std::vector<int> operator<)
+__device__ __forceinline__ bool devlist_less(uint64_t a, uint64_t b) {
+    const uint64_t diff = a ^ b;
+    if (!diff) return false;
+    const uint64_t d = diff & (~diff + 1);
+    const uint64_t above = ~(d | (d - 1));  // bits strictly above d
+    return (a & d) ? (b & above) != 0 : !(a & above);
+}
+
+struct SimRec {
+    const ws_out_metaop* mo;
+    const ws_out_piece* pc;
+    const ws_out_edge* ed;
+    const ws_out_wave* wv;
+    const ws_out_entry* en;
+    const ws_out_flow* fl;
+    uint64_t en_off;  // entries section offset inside the record
+};
+
+__device__ __forceinline__ SimRec sim_rec(const ws_plan_result& r, const uint8_t* base) {
+    SimRec v;
+    uint64_t o = 0;
+    v.mo = reinterpret_cast<const ws_out_metaop*>(base + o);
+    o += al8(sizeof(ws_out_metaop) * r.n_metaops);
+    o += al8(sizeof(ws_out_level) * r.n_levels);
+    v.pc = reinterpret_cast<const ws_out_piece*>(base + o);
+    o += al8(sizeof(ws_out_piece) * r.n_pieces);
+    v.ed = reinterpret_cast<const ws_out_edge*>(base + o);
+    o += al8(sizeof(ws_out_edge) * r.n_edges);
+    v.wv = reinterpret_cast<const ws_out_wave*>(base + o);
+    o += al8(sizeof(ws_out_wave) * r.n_waves);
+    v.en = reinterpret_cast<const ws_out_entry*>(base + o);
+    v.en_off = o;
+    o += al8(sizeof(ws_out_entry) * r.n_entries);
+    v.fl = reinterpret_cast<const ws_out_flow*>(base + o);
+    return v;
+}
+
+// plan.devices.find({w, k}): device mask of the last entry of wave w with
+// MetaOp k and a nonzero placement, 0 when absent (warp-uniform result)
+__device__ __forceinline__ uint64_t sim_find(const SimRec& V, int nW, int lane, int w, int k) {
+    if (w < 0 || w >= nW) return 0;
+    const ws_out_wave& wv = V.wv[w];
+    uint64_t m = 0;
+    for (int base = 0; base < wv.n_entries; base += 32) {
+        const int i = base + lane;
+        uint64_t dm = 0;
+        bool hit = false;
+        if (i < wv.n_entries) {
+            const ws_out_entry& e = V.en[wv.entry_begin + i];
+            dm = e.devmask;
+            hit = e.metaop == k && dm != 0;
+        }
+        const unsigned b = __ballot_sync(kFull, hit);
+        if (b) m = __shfl_sync(kFull, dm, 31 - __clz(b));
+    }
+    return m;
+}
+
+// the same lookup on one thread
+__device__ __forceinline__ uint64_t sim_find1(const SimRec& V, int nW, int w, int k) {
+    if (w < 0 || w >= nW) return 0;
+    uint64_t m = 0;
+    for (int i = 0; i < V.wv[w].n_entries; ++i) {
+        const ws_out_entry& e = V.en[V.wv[w].entry_begin + i];
+        if (e.metaop == k && e.devmask) m = e.devmask;
+    }
+    return m;
+}
+
+// max over the devices of `mask` of a per-lane pair (d = lane, lane + 32), from 0.0
+__device__ __forceinline__ double lane_max2(uint64_t mask, int lane, double a0, double a1) {
+    double t = 0.0;
+    if (mask >> lane & 1ull) t = a0;
+    if (mask >> (lane + 32) & 1ull) t = (t < a1) ? a1 : t;
+    return warp_max_d(t);
+}
+
+__global__ void __launch_bounds__(32 * kSimWarps) k_sim(SimArgs A) {
+    extern __shared__ __align__(16) char sim_smem[];
+    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int p = blockIdx.x * kSimWarps + wid;
+    if (p >= A.n_plans) return;
+    const ws_plan_result& R = A.plans[p];
+    ws_sim_result* res = A.out + p;
+    if (R.status != WS_STATUS_OK) {
+        if (lane == 0) {
+            ws_sim_result r{};
+            r.status = R.status;
+            *res = r;
+        }
+        return;
+    }
+    char* sm = sim_smem + wid * A.SL.bytes;
+    const ws_batch& B = A.B;
+    const ws_plan_rec& P = B.plans[p];
+    const SimRec V = sim_rec(R, A.parena + R.offset);
+    const int N = P.n_dev, K = R.n_metaops, nW = R.n_waves, nE = R.n_entries, nF = R.n_flows;
+    const int G = P.n_groups + K, mbase = P.mod_begin;
+    const uint64_t all = N == 64 ? ~0ull : ((1ull << N) - 1ull);
+    // per-entry scratch (one 32-byte slot per entry): [0] interval end, [1] start
+    double* s_iv = reinterpret_cast<double*>(A.scratch + R.offset + V.en_off);
+    if (G > A.caps.G || G > 128 || nW > A.caps.W || P.n_islands > A.caps.IS || K > A.caps.K || nE > A.caps.E) {
+        if (lane == 0) {
+            ws_sim_result r{};
+            r.status = WS_STATUS_LIMIT;
+            *res = r;
+        }
+        return;
+    }
+    uint64_t* islm = reinterpret_cast<uint64_t*>(sm + A.SL.isl);
+    uint64_t* chg = reinterpret_cast<uint64_t*>(sm + A.SL.chg);
+    uint64_t* gmask = reinterpret_cast<uint64_t*>(sm + A.SL.gmask);
+    uint64_t* gbytes = reinterpret_cast<uint64_t*>(sm + A.SL.gbytes);
+    uint64_t* pbytes = reinterpret_cast<uint64_t*>(sm + A.SL.pbytes);
+    int* pord = reinterpret_cast<int*>(sm + A.SL.pord);
+    int* ord = reinterpret_cast<int*>(sm + A.SL.ord);
+    int* exec = reinterpret_cast<int*>(sm + A.SL.exec);
+    int* by_rank = reinterpret_cast<int*>(sm + A.SL.by_rank);
+    int* gk = reinterpret_cast<int*>(sm + A.SL.gk);
+    int* lst = reinterpret_cast<int*>(sm + A.SL.lst);
+    ws_out_violation* vio = reinterpret_cast<ws_out_violation*>(sm + A.SL.vio);
+
+    // ---- per-plan tables ------------------------------------------------
+    for (int i = 0; i < P.n_islands; ++i) {
+        uint64_t m = 0;
+        for (int base = 0; base < N; base += 32) {
+            const int d = base + lane;
+            m |= static_cast<uint64_t>(__ballot_sync(kFull, d < N && B.dev_island[P.dev_begin + d] == i)) << base;
+        }
+        if (lane == 0) islm[i] = m;
+    }
+    for (int g = lane; g < G; g += 32) {
+        chg[g] = 0;
+        gmask[g] = 0;
+        gbytes[g] = 0;
+    }
+    for (int k = lane; k < K; k += 32) {
+        const int gm = mbase + V.mo[k].module;
+        const int grp = V.mo[k].length == B.mod_layers[gm] ? B.mod_group[gm] : -1;
+        const int al = B.mod_alias[gm];
+        gk[k] = grp < 0 ? P.n_groups + k : ((al >= 0 && al < K) ? P.n_groups + al : grp);
+        exec[k] = 0;
+        int r = 0;
+        for (int j = 0; j < K; ++j) r += dec_less(j, k);
+        by_rank[r] = k;
+    }
+    // replay order: waves by (start, index) (simulate.hpp:208-212)
+    bool sorted = true;
+    for (int w = lane + 1; w < nW; w += 32) sorted &= !(V.wv[w].start < V.wv[w - 1].start);
+    sorted = __all_sync(kFull, sorted);
+    for (int w = lane; w < nW; w += 32) {
+        int pos = w;
+        if (!sorted) {
+            pos = 0;
+            const double sw = V.wv[w].start;
+            for (int j = 0; j < nW; ++j) pos += V.wv[j].start < sw || (V.wv[j].start == sw && j < w);
+        }
+        ord[pos] = w;
+    }
+    __syncwarp();
+
+    // ---- simulate (simulate.hpp:171-280) ---------------------------------
+    const ws_sim_opts& opt = A.opt;
+    double av0 = 0.0, av1 = 0.0;  // availability clocks of devices lane, lane+32
+    double bc0 = 0.0, bc1 = 0.0;  // compute seconds (per_device_busy)
+    uint64_t touched = 0;         // devices present in per_device_busy
+    double frontier = 0.0, fwd_bwd = 0.0, send_recv = 0.0, param_sync = 0.0;
+    double transferred = 0.0, inter_bytes = 0.0;
+    int timeline = 0;
+    auto busy_mask = [&](uint64_t m, double t0, double dur) {  // busy(d, t0, dur) for every d in m
+        const bool b0 = m >> lane & 1ull, b1 = m >> (lane + 32) & 1ull;
+        if (dur <= 0.0) {
+            if (b0) av0 = (av0 < t0) ? t0 : av0;
+            if (b1) av1 = (av1 < t0) ? t0 : av1;
+        } else {
+            if (b0) av0 = t0 + dur;
+            if (b1) av1 = t0 + dur;
+            timeline += popc64(m);
+        }
+    };
+    auto attribute = [&](double& bucket) {
+        const double f = lane_max2(all, lane, av0, av1);
+        bucket += f - frontier;
+        frontier = f;
+    };
+    auto run_flow = [&](const ws_out_flow& f) {
+        double dur = 0.0;  // flow_duration (simulate.hpp:96-100)
+        if (!opt.zero_volumes && f.volume != 0 && f.mode != WS_FLOW_COPY)
+            dur = static_cast<double>(f.volume) / (f.mode == WS_FLOW_INTER ? P.inter_bw : P.intra_bw);
+        const uint64_t ma = sim_find(V, nW, lane, f.from_wave, f.from_metaop);
+        const uint64_t mb = sim_find(V, nW, lane, f.to_wave, f.to_metaop);
+        if (!ma || !mb) return;
+        const uint64_t parties = ma | mb;
+        const double t0 = lane_max2(parties, lane, av0, av1);
+        busy_mask(parties, t0, dur);
+        if (!opt.zero_volumes) {
+            transferred += static_cast<double>(f.volume);
+            if (f.mode == WS_FLOW_INTER) inter_bytes += static_cast<double>(f.volume);
+        }
+    };
+    auto run_wave = [&](int w, bool backward) {
+        const double scale = backward ? opt.backward_ratio : 1.0;
+        const ws_out_wave& wv = V.wv[w];
+        uint64_t parts = 0;
+        for (int i = 0; i < wv.n_entries; ++i) parts |= sim_find(V, nW, lane, w, V.en[wv.entry_begin + i].metaop);
+        const double t0 = lane_max2(parts, lane, av0, av1);
+        for (int i = 0; i < wv.n_entries; ++i) {
+            const ws_out_entry& e = V.en[wv.entry_begin + i];
+            const uint64_t m = sim_find(V, nW, lane, w, e.metaop);
+            if (!m) continue;
+            const double dur = e.span * scale;
+            busy_mask(m, t0, dur);
+            if (m >> lane & 1ull) bc0 += dur;
+            if (m >> (lane + 32) & 1ull) bc1 += dur;
+            touched |= m;
+        }
+        const double rel = t0 + wv.duration * scale;  // the wave releases its devices together
+        if (parts >> lane & 1ull) av0 = (av0 < rel) ? rel : av0;
+        if (parts >> (lane + 32) & 1ull) av1 = (av1 < rel) ? rel : av1;
+    };
+    auto flows_where = [&](bool into, int w) {  // flows_into / flows_out_of, in flow order
+        for (int base = 0; base < nF; base += 32) {
+            const int f = base + lane;
+            const bool hit = f < nF && (into ? V.fl[f].to_wave : V.fl[f].from_wave) == w;
+            for (unsigned b = __ballot_sync(kFull, hit); b; b &= b - 1) run_flow(V.fl[base + __ffs(b) - 1]);
+        }
+    };
+    for (int j = 0; j < nW; ++j) {  // forward: transmissions arrive before their consumer wave
+        const int w = ord[j];
+        flows_where(true, w);
+        attribute(send_recv);
+        run_wave(w, false);
+        attribute(fwd_bwd);
+    }
+    for (int j = nW - 1; j >= 0; --j) {  // backward: reverse order, gradients mirror the flows
+        const int w = ord[j];
+        run_wave(w, true);
+        attribute(fwd_bwd);
+        flows_where(false, w);
+        attribute(send_recv);
+    }
+    if (!opt.skip_sync) {  // build_param_groups (simulate.hpp:127-165), group-wise sync (:268-276)
+        if (lane == 0) {
+            for (int w = 0; w < nW; ++w)
+                for (int i = 0; i < V.wv[w].n_entries; ++i) {
+                    const int k = V.en[V.wv[w].entry_begin + i].metaop;
+                    const uint64_t m = sim_find1(V, nW, w, k);
+                    if (!m || k < 0 || k >= K) continue;
+                    const int gm = mbase + V.mo[k].module;
+                    const uint64_t pb = static_cast<uint64_t>(static_cast<double>(B.mod_param[gm]) *
+                                                              V.mo[k].length / B.mod_layers[gm]);
+                    const uint64_t gb = 2ull * pb / static_cast<uint64_t>(B.mod_tp[gm]);
+                    gmask[gk[k]] |= m;
+                    gbytes[gk[k]] = gbytes[gk[k]] < gb ? gb : gbytes[gk[k]];
+                }
+        }
+        __syncwarp();
+        // pool entries: one per distinct device set (first group holding it), bytes summed
+        int npool = 0;
+        for (int base = 0; base < G; base += 32) {
+            const int g = base + lane;
+            bool rep = g < G && gmask[g] != 0;
+            uint64_t sum = 0;
+            if (rep) {
+                for (int h = 0; h < G; ++h)
+                    if (gmask[h] == gmask[g]) {
+                        if (h < g) rep = false;
+                        sum += gbytes[h];
+                    }
+            }
+            if (rep) pbytes[g] = sum;
+            npool += __popc(__ballot_sync(kFull, rep));
+            if (g < G) pord[g] = rep ? 1 : 0;  // representative flags
+        }
+        __syncwarp();
+        int rk[4];  // rank of each representative among the distinct sets (G <= 128)
+        for (int s = 0; s < 4; ++s) {
+            const int g = s * 32 + lane;
+            rk[s] = -1;
+            if (g < G && pord[g] == 1) {
+                int r = 0;
+                for (int h = 0; h < G; ++h) r += pord[h] == 1 && devlist_less(gmask[h], gmask[g]);
+                rk[s] = r;
+            }
+        }
+        __syncwarp();
+        for (int s = 0; s < 4; ++s)
+            if (rk[s] >= 0) pord[rk[s]] = s * 32 + lane;  // pord reused: rank -> group
+        __syncwarp();
+        for (int r = 0; r < npool; ++r) {
+            const int g = pord[r];
+            const uint64_t m = gmask[g];
+            const int size = popc64(m);
+            double dur = 0.0;
+            if (size >= 2) {
+                int widest = 0, islands = 0;
+                for (int base = 0; base < P.n_islands; base += 32) {
+                    const int i = base + lane;
+                    const int c = i < P.n_islands ? popc64(m & islm[i]) : 0;
+                    widest = max(widest, static_cast<int>(__reduce_max_sync(kFull, static_cast<unsigned>(c))));
+                    islands += __popc(__ballot_sync(kFull, c > 0));
+                }
+                const double bytes = static_cast<double>(pbytes[g]);
+                if (widest >= 2)
+                    dur += 2.0 * (static_cast<double>(widest) - 1.0) / static_cast<double>(widest) * bytes / P.intra_bw;
+                if (islands >= 2)
+                    dur += 2.0 * (static_cast<double>(islands) - 1.0) / static_cast<double>(islands) * bytes /
+                           P.inter_bw;
+            }
+            if (dur <= 0.0) continue;
+            const double t0 = lane_max2(m, lane, av0, av1);
+            busy_mask(m, t0, dur);
+        }
+        attribute(param_sync);
+    }
+    const double makespan = lane_max2(all, lane, av0, av1);
+
+    // ---- compute_device_memory (validate.hpp:27-50) -----------------------
+    double mem0 = 0.0, mem1 = 0.0;
+    for (int w = 0; w < nW; ++w) {
+        const ws_out_wave& wv = V.wv[w];
+        for (int i = 0; i < wv.n_entries; ++i) {
+            const ws_out_entry& e = V.en[wv.entry_begin + i];
+            const int k = e.metaop;
+            const uint64_t m = sim_find(V, nW, lane, w, k);
+            if (!m || k < 0 || k >= K) continue;
+            const int gm = mbase + V.mo[k].module;
+            const uint64_t pb = static_cast<uint64_t>(static_cast<double>(B.mod_param[gm]) * V.mo[k].length /
+                                                      B.mod_layers[gm]);
+            const uint64_t charged = chg[gk[k]];
+            const double pstate = (1.0 + P.grad_mult) * static_cast<double>(pb) / B.mod_tp[gm];
+            const double act = e.layers * (static_cast<double>(B.mod_act[gm]) * 1.0 / e.n);
+            if (m >> lane & 1ull) {
+                if (!(charged >> lane & 1ull)) mem0 += pstate;
+                mem0 += act;
+            }
+            if (m >> (lane + 32) & 1ull) {
+                if (!(charged >> (lane + 32) & 1ull)) mem1 += pstate;
+                mem1 += act;
+            }
+            __syncwarp();
+            if (lane == 0) chg[gk[k]] = charged | m;
+            __syncwarp();
+        }
+    }
+
+    // ---- utilization proxy (simulate.hpp:283-300), lanes = MetaOps --------
+    double ls[2] = {0.0, 0.0}, ds[2] = {0.0, 0.0}, rate = 0.0;
+    bool seen_k[2] = {false, false};
+    for (int s = 0; s < 2; ++s) {
+        const int k = lane + 32 * s;
+        if (k >= K) continue;
+        const int gm = mbase + V.mo[k].module;
+        const double wk = B.mod_w[gm];
+        for (int w = 0; w < nW; ++w)
+            for (int i = 0; i < V.wv[w].n_entries; ++i) {
+                const ws_out_entry& e = V.en[V.wv[w].entry_begin + i];
+                if (e.metaop != k) continue;
+                ls[s] += wk * 1.0 * e.layers;
+                ds[s] += e.span * e.n;
+                seen_k[s] = true;
+            }
+        const double t1 = eval_bf(V.pc + V.mo[k].piece_begin, V.mo[k].piece_count, B.mod_c[gm], wk, 1.0, 1.0);
+        if (t1 > 0.0) {
+            const double r = wk * 1.0 / t1;
+            rate = (rate < r) ? r : rate;
+        }
+    }
+    const double peak_rate = warp_max_d(rate);
+    const uint64_t util_mask = (static_cast<uint64_t>(__ballot_sync(kFull, seen_k[1])) << 32) |
+                               __ballot_sync(kFull, seen_k[0]);
+
+    // ---- validate_plan (validate.hpp:58-188) ------------------------------
+    int nv = 0;  // lane 0 holds the count
+    auto fail = [&](int code, int wave, int a, int b, double x, double y) {
+        if (nv < WS_SIM_MAX_VIOLATIONS) vio[nv] = ws_out_violation{code, wave, a, b, x, y};
+        ++nv;
+    };
+    const double horizon = R.end_time > 1.0 ? R.end_time : 1.0;  // std::max(1.0, end_time)
+    const double tol = 1e-6 * horizon;
+    if (lane == 0) {  // per-wave entry checks, recomputed spans, executed layers
+        for (int w = 0; w < nW; ++w) {
+            const ws_out_wave& wv = V.wv[w];
+            uint64_t seen = 0;
+            int used = 0;
+            for (int i = 0; i < wv.n_entries; ++i) {
+                const int ei = wv.entry_begin + i;
+                const ws_out_entry& e = V.en[ei];
+                const int k = e.metaop;
+                if (k < 0 || k >= K) {
+                    fail(WS_V_UNKNOWN_ENTITY, w, k, 0, 0, 0);
+                    continue;
+                }
+                if (seen >> k & 1ull) fail(WS_V_DUPLICATE, w, k, 0, 0, 0);
+                seen |= 1ull << k;
+                const int gm = mbase + V.mo[k].module;
+                const double per_layer = eval_bf(V.pc + V.mo[k].piece_begin, V.mo[k].piece_count, B.mod_c[gm],
+                                                 B.mod_w[gm], static_cast<double>(e.n), 1.0);
+                const double span = e.layers * per_layer;
+                if (fabs(span - e.span) > tol + 1e-9 * fabs(span)) fail(WS_V_SPAN, w, k, 0, e.span, span);
+                if (e.span > wv.duration + tol) fail(WS_V_SPAN_DURATION, w, 0, 0, 0, 0);
+                s_iv[4 * ei] = wv.start + span;
+                s_iv[4 * ei + 1] = wv.start;
+                exec[k] += e.layers;
+                used += e.n;
+            }
+            if (used > N) fail(WS_V_WAVE_DEVICES, w, 0, 0, 0, 0);
+        }
+        for (int r = 0; r < K; ++r) {  // work completion, entities in id order
+            const int k = by_rank[r];
+            if (exec[k] != V.mo[k].length) fail(WS_V_WORK, -1, k, exec[k], V.mo[k].length, 0);
+        }
+    }
+    __syncwarp();
+    // entry -> (start, end, n) of its interval; known MetaOps only
+    auto iv_of = [&](int ei, double& s, double& e, int& n) {
+        if (V.en[ei].metaop < 0 || V.en[ei].metaop >= K) return false;
+        e = s_iv[4 * ei];
+        s = s_iv[4 * ei + 1];
+        n = V.en[ei].n;
+        return true;
+    };
+    {  // instantaneous capacity: the first addition event after which active > N
+        double bt = 0.0;
+        int bn = 0, bi = 0x7fffffff, bact = 0;
+        for (int i = lane; i < nE; i += 32) {
+            double si, ei_, sj, ej;
+            int ni, nj;
+            if (!iv_of(i, si, ei_, ni)) continue;
+            int act = 0;
+            for (int j = 0; j < nE; ++j) {
+                if (!iv_of(j, sj, ej, nj)) continue;
+                if (sj < si || (sj == si && (nj < ni || (nj == ni && j <= i)))) act += nj;
+                const double rem = sj > ej - tol ? sj : ej - tol;  // std::max(start, end - tol)
+                if (rem <= si) act -= nj;
+            }
+            if (act > N && (bi == 0x7fffffff || si < bt || (si == bt && (ni < bn || (ni == bn && i < bi)))))
+                bt = si, bn = ni, bi = i, bact = act;
+        }
+        for (int off = 16; off; off >>= 1) {
+            const double ot = __shfl_xor_sync(kFull, bt, off);
+            const int on = __shfl_xor_sync(kFull, bn, off), oi = __shfl_xor_sync(kFull, bi, off),
+                      oa = __shfl_xor_sync(kFull, bact, off);
+            if (oi != 0x7fffffff &&
+                (bi == 0x7fffffff || ot < bt || (ot == bt && (on < bn || (on == bn && oi < bi)))))
+                bt = ot, bn = on, bi = oi, bact = oa;
+        }
+        if (lane == 0 && bi != 0x7fffffff) fail(WS_V_CAPACITY, -1, bact, 0, bt, 0);
+    }
+    if (lane == 0) {  // same-entity intervals pairwise disjoint, entities in id order
+        for (int r = 0; r < K; ++r) {
+            const int k = by_rank[r];
+            int cnt = 0;
+            for (int w = 0; w < nW; ++w)  // by_entity lists keep wave / entry order
+                for (int i = 0; i < V.wv[w].n_entries; ++i)
+                    if (V.en[V.wv[w].entry_begin + i].metaop == k) lst[cnt++] = V.wv[w].entry_begin + i;
+            struct ByStart {  // std::sort by interval start (exact libstdc++ emulation)
+                const double* iv;
+                __device__ bool operator()(int a, int b) const { return iv[4 * a + 1] < iv[4 * b + 1]; }
+            } cmp{s_iv};
+            ls_sort(lst, cnt, cmp);
+            for (int i = 0; i + 1 < cnt; ++i)
+                if (s_iv[4 * lst[i]] > s_iv[4 * lst[i + 1] + 1] + tol) {
+                    fail(WS_V_OVERLAP, -1, k, 0, 0, 0);
+                    break;
+                }
+        }
+    }
+    __syncwarp();
+    for (int q = 0; q < R.n_edges; ++q) {  // dependencies, in MetaGraph edge order
+        const int from = V.ed[q].from, to = V.ed[q].to;
+        double fe = 0.0, ts = horizon * 2;
+        bool hf = false, ht = false;
+        for (int i = lane; i < nE; i += 32) {
+            double s, e;
+            int n;
+            if (!iv_of(i, s, e, n)) continue;
+            if (V.en[i].metaop == from) hf = true, fe = (fe < e) ? e : fe;
+            if (V.en[i].metaop == to) ht = true, ts = (s < ts) ? s : ts;
+        }
+        hf = __any_sync(kFull, hf);
+        ht = __any_sync(kFull, ht);
+        fe = warp_max_d(fe);
+        ts = warp_min_d(ts);
+        if (lane == 0 && hf && ht && ts + tol < fe) fail(WS_V_DEPENDENCY, -1, from, to, ts, fe);
+    }
+    bool any_placed = false;
+    for (int i = lane; i < nE; i += 32) any_placed |= V.en[i].devmask != 0;
+    if (__any_sync(kFull, any_placed)) {
+        if (lane == 0) {  // per wave: placed, sized, disjoint (device-list order)
+            for (int w = 0; w < nW; ++w) {
+                uint64_t taken = 0;
+                for (int i = 0; i < V.wv[w].n_entries; ++i) {
+                    const ws_out_entry& e = V.en[V.wv[w].entry_begin + i];
+                    const uint64_t m = sim_find1(V, nW, w, e.metaop);
+                    if (!m) {
+                        fail(WS_V_UNPLACED, w, e.metaop, 0, 0, 0);
+                        continue;
+                    }
+                    // the placed entry's rot orders its device list
+                    int rot = 0;
+                    for (int j = 0; j < V.wv[w].n_entries; ++j) {
+                        const ws_out_entry& x = V.en[V.wv[w].entry_begin + j];
+                        if (x.metaop == e.metaop && x.devmask) rot = x.rot;
+                    }
+                    if (popc64(m) != e.n) fail(WS_V_DEVICE_COUNT, w, e.metaop, popc64(m), e.n, 0);
+                    const uint64_t order[2] = {m & ~((rot >= 64 ? ~0ull : (1ull << rot)) - 1ull),
+                                               m & ((rot >= 64 ? ~0ull : (1ull << rot)) - 1ull)};
+                    for (int h = 0; h < 2; ++h)
+                        for (uint64_t b = order[h]; b; b &= b - 1) {
+                            const int d = low_bit(b);
+                            if (d >= N)
+                                fail(WS_V_UNKNOWN_DEVICE, -1, d, 0, 0, 0);
+                            else if (taken >> d & 1ull)
+                                fail(WS_V_DEVICE_TWICE, w, d, 0, 0, 0);
+                            else
+                                taken |= 1ull << d;
+                        }
+                }
+            }
+        }
+        const double cap = static_cast<double>(P.mem_capacity) * (1.0 + 1e-9);
+        for (int h = 0; h < 2; ++h) {  // memory capacity, devices in id order
+            const double mv = h ? mem1 : mem0;
+            const int d = lane + 32 * h;
+            const unsigned b = __ballot_sync(kFull, d < N && mv > cap);
+            for (unsigned q = b; q; q &= q - 1) {
+                const int src = __ffs(q) - 1;
+                const double x = __shfl_sync(kFull, mv, src);
+                if (lane == 0) fail(WS_V_MEMORY, -1, 32 * h + src, 0, x, __longlong_as_double(static_cast<long long>(P.mem_capacity)));
+            }
+        }
+    }
+    __syncwarp();
+
+    // ---- write the record ---------------------------------------------------
+    nv = __shfl_sync(kFull, nv, 0);
+    const int keep = nv < WS_SIM_MAX_VIOLATIONS ? nv : WS_SIM_MAX_VIOLATIONS;
+    const uint64_t sz = 16ull * N + 16 + 8ull * K + sizeof(ws_out_violation) * keep;
+    unsigned long long off = 0;
+    if (lane == 0) off = atomicAdd(A.arena_top, static_cast<unsigned long long>(sz));
+    off = __shfl_sync(kFull, off, 0);
+    if (off + sz > A.arena_cap) {
+        if (lane == 0) {
+            ws_sim_result r{};
+            r.status = WS_STATUS_INTERNAL;
+            *res = r;
+        }
+        return;
+    }
+    uint8_t* base = A.arena + off;
+    double* o_busy = reinterpret_cast<double*>(base);
+    double* o_mem = reinterpret_cast<double*>(base + 8ull * N + 8);
+    double* o_util = reinterpret_cast<double*>(base + 16ull * N + 8);
+    if (lane < N) o_busy[lane] = bc0, o_mem[lane] = mem0;
+    if (lane + 32 < N) o_busy[lane + 32] = bc1, o_mem[lane + 32] = mem1;
+    for (int s = 0; s < 2; ++s) {
+        const int k = lane + 32 * s;
+        if (k < K)
+            o_util[k] = (ds[s] > 0.0 && peak_rate > 0.0) ? (ls[s] / ds[s]) / peak_rate : 0.0;
+    }
+    ws_out_violation* o_v = reinterpret_cast<ws_out_violation*>(base + 16ull * N + 16 + 8ull * K);
+    for (int i = lane; i < keep; i += 32) o_v[i] = vio[i];
+    if (lane == 0) {
+        *reinterpret_cast<uint64_t*>(base + 8ull * N) = touched;
+        *reinterpret_cast<uint64_t*>(base + 16ull * N + 8 + 8ull * K) = util_mask;
+        ws_sim_result r{};
+        r.status = WS_STATUS_OK;
+        r.valid = nv == 0;
+        r.n_violations = nv;
+        r.timeline_items = timeline;
+        r.makespan = makespan;
+        r.fwd_bwd_seconds = fwd_bwd;
+        r.param_sync_seconds = param_sync;
+        r.send_recv_seconds = send_recv;
+        const double span = makespan > 1e-300 ? makespan : 1e-300;  // std::max(makespan, 1e-300)
+        r.fwd_bwd_fraction = fwd_bwd / span;
+        r.param_sync_fraction = param_sync / span;
+        r.send_recv_fraction = send_recv / span;
+        r.total_transferred_bytes = transferred;
+        r.total_inter_island_bytes = inter_bytes;
+        r.offset = off;
+        r.size = sz;
+        *res = r;
+    }
+}
+
+}  // namespace wsdev

@@ -189,6 +189,15 @@ char* wsx_result_text(const wsx_set* s, int32_t i, const ws_plan_result* results
     }
 }
 
+char* wsx_sim_text(const wsx_set* s, int32_t i, const ws_plan_result* results, const uint8_t* arena,
+                   const ws_sim_result* sims, const uint8_t* sim_arena) {
+    try {
+        return dup(sim_text(s->probs[i], results[i], arena, sims[i], sim_arena));
+    } catch (const std::exception& e) {
+        return dup(std::string("error DecodeFailure: ") + e.what() + "\n");
+    }
+}
+
 char* wsx_dump_workload(const wsx_set* s, int32_t i) { return dup(dump_workload(*s->probs[i].spec)); }
 char* wsx_dump_topology(const wsx_set* s, int32_t i) { return dup(dump_topology(*s->probs[i].topo)); }
 void wsx_free_str(char* p) { std::free(p); }

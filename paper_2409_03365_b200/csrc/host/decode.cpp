@@ -73,15 +73,16 @@ std::string module_kind(const WorkloadSpec& spec, std::int64_t index) {
     return it->first;
 }
 
+// plan.devices list of an entry: ascending device index starting at `rot`
+// with wrap-around (the sequential ablation's rolling cursor order,
+// placement.hpp:351-357; rot = 0 for the locality placer's sorted sets)
 std::vector<int> device_list(const Problem& prob, const ws_out_entry& e) {
     const auto& devs = prob.topo->devices;
     const int N = static_cast<int>(devs.size());
     std::vector<int> out;
-    if (prob.opt.placement.sequential) {  // rolling cursor order (placement.hpp:351-357)
-        for (int i = 0; i < e.n; ++i) out.push_back(devs[(e.rot + i) % N]);
-    } else {
-        for (int d = 0; d < N; ++d)
-            if (e.devmask >> d & 1ull) out.push_back(devs[d]);
+    for (int i = 0; i < N; ++i) {
+        const int d = (e.rot + i) % N;
+        if (e.devmask >> d & 1ull) out.push_back(devs[d]);
     }
     return out;
 }
@@ -219,7 +220,7 @@ PlannerResult decode_result(const Problem& prob, const ws_plan_result& r, const 
         for (int i = 0; i < s.wv[w].n_entries; ++i) {
             const ws_out_entry& e = s.en[s.wv[w].entry_begin + i];
             wave.entries.push_back({mid(e.metaop), e.n, e.layers, e.span});
-            plan.devices[{w, mid(e.metaop)}] = device_list(prob, e);
+            if (e.devmask) plan.devices[{w, mid(e.metaop)}] = device_list(prob, e);  // 0: not placed
         }
         res.schedule.waves.push_back(std::move(wave));
     }

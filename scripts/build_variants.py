@@ -1,7 +1,8 @@
 """Build libwsgpu.so plus tuning variants: python scripts/build_variants.py name.so:DEF1,DEF2 ..."""
 import os, sys; sys.path.insert(0, os.getcwd())
 import sys
-from paper_2409_03365_b200 import build
+sys.path.insert(0, os.path.join(os.getcwd(), "paper_2409_03365_b200"))
+import build  # noqa: E402  (not the package: its import loads the library)
 build.build(force=True)
 for spec in sys.argv[1:]:
     name, _, defs = spec.partition(':')

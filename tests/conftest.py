@@ -44,3 +44,23 @@ def build_set(cases):
         except ws.ParseError as e:
             failed.append((c, str(e)))
     return ps, kept, failed
+
+
+@pytest.fixture(scope="session")
+def sim_cases():
+    with gzip.open(GOLDEN / "sim_cases.json.gz", "rt") as f:
+        return json.load(f)
+
+
+@pytest.fixture(scope="session")
+def sim_sweep_hashes():
+    with gzip.open(GOLDEN / "sim_sweep_hashes.txt.gz", "rt") as f:
+        return f.read().split()
+
+
+def sim_groups(cases):
+    """Cases grouped by SimulatorOptions (one evaluation call per group)."""
+    groups = {}
+    for c in cases:
+        groups.setdefault(tuple(sorted(c["sim"].items())), []).append(c)
+    return [(dict(k), v) for k, v in groups.items()]
