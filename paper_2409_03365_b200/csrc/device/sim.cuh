@@ -109,6 +109,7 @@ struct SimRec {
     const ws_out_entry* en;
     const ws_out_flow* fl;
     uint64_t en_off;  // entries section offset inside the record
+    uint64_t fl_off;  // flows section offset
 };
 
 __device__ __forceinline__ SimRec sim_rec(const ws_plan_result& r, const uint8_t* base) {
@@ -127,6 +128,7 @@ __device__ __forceinline__ SimRec sim_rec(const ws_plan_result& r, const uint8_t
     v.en_off = o;
     o += al8(sizeof(ws_out_entry) * r.n_entries);
     v.fl = reinterpret_cast<const ws_out_flow*>(base + o);
+    v.fl_off = o;
     return v;
 }
 
@@ -192,8 +194,15 @@ __global__ void __launch_bounds__(32 * kSimWarps) k_sim(SimArgs A) {
     const int N = P.n_dev, K = R.n_metaops, nW = R.n_waves, nE = R.n_entries, nF = R.n_flows;
     const int G = P.n_groups + K, mbase = P.mod_begin;
     const uint64_t all = N == 64 ? ~0ull : ((1ull << N) - 1ull);
-    // per-entry scratch (one 32-byte slot per entry): [0] interval end, [1] start
-    double* s_iv = reinterpret_cast<double*>(A.scratch + R.offset + V.en_off);
+    // per-entry / per-flow scratch mirroring the record (one 32-byte slot each):
+    // entry: [0] interval end (f64), [1] start (f64), [2] check flags (i32),
+    //        [3] plan.devices placement of its (wave, MetaOp) key (u64)
+    // flow:  [0] source placement, [1] destination placement
+    uint8_t* const s_rec = A.scratch + R.offset;
+    auto en_iv = [&](int e) { return reinterpret_cast<double*>(s_rec + V.en_off + 32ull * e); };
+    auto en_pl = [&](int e) { return reinterpret_cast<uint64_t*>(s_rec + V.en_off + 32ull * e + 24); };
+    auto en_flags = [&](int e) { return reinterpret_cast<int*>(s_rec + V.en_off + 32ull * e + 16); };
+    auto fl_masks = [&](int f) { return reinterpret_cast<uint64_t*>(s_rec + V.fl_off + 32ull * f); };
     if (G > A.caps.G || G > 128 || nW > A.caps.W || P.n_islands > A.caps.IS || K > A.caps.K || nE > A.caps.E) {
         if (lane == 0) {
             ws_sim_result r{};
@@ -252,6 +261,45 @@ __global__ void __launch_bounds__(32 * kSimWarps) k_sim(SimArgs A) {
         }
         ord[pos] = w;
     }
+    // plan.devices lookups, resolved once: per entry the placement of its
+    // (wave, MetaOp) key (the last placed entry with that key), per flow both
+    // endpoints; duplicate keys inside a wave flagged for the validator
+    for (int w = 0; w < nW; ++w) {
+        const int eb = V.wv[w].entry_begin, ne = V.wv[w].n_entries;
+        for (int i = lane; i < ne; i += 32) {
+            const int k = V.en[eb + i].metaop;
+            uint64_t m = 0;
+            int flags = 0;
+            for (int j = 0; j < ne; ++j) {
+                const ws_out_entry& x = V.en[eb + j];
+                if (x.metaop != k) continue;
+                if (x.devmask) m = x.devmask;
+                if (j < i) flags |= 1;  // an earlier entry has this MetaOp
+            }
+            *en_pl(eb + i) = m;
+            *en_flags(eb + i) = flags;
+        }
+    }
+    __syncwarp();
+    for (int f = lane; f < nF; f += 32) {
+        const ws_out_flow& x = V.fl[f];
+        uint64_t ma = 0, mb = 0;
+        if (x.from_wave >= 0 && x.from_wave < nW)
+            for (int j = 0; j < V.wv[x.from_wave].n_entries; ++j) {
+                const int e = V.wv[x.from_wave].entry_begin + j;
+                if (V.en[e].metaop == x.from_metaop && V.en[e].devmask) ma = V.en[e].devmask;
+            }
+        if (x.to_wave >= 0 && x.to_wave < nW)
+            for (int j = 0; j < V.wv[x.to_wave].n_entries; ++j) {
+                const int e = V.wv[x.to_wave].entry_begin + j;
+                if (V.en[e].metaop == x.to_metaop && V.en[e].devmask) mb = V.en[e].devmask;
+            }
+        fl_masks(f)[0] = ma;
+        fl_masks(f)[1] = mb;
+    }
+    // the first 64 flows' waves stay in registers for the per-wave flow scans
+    const int ft0 = lane < nF ? V.fl[lane].to_wave : -1, ff0 = lane < nF ? V.fl[lane].from_wave : -1;
+    const int ft1 = lane + 32 < nF ? V.fl[lane + 32].to_wave : -1, ff1 = lane + 32 < nF ? V.fl[lane + 32].from_wave : -1;
     __syncwarp();
 
     // ---- simulate (simulate.hpp:171-280) ---------------------------------
@@ -278,13 +326,13 @@ __global__ void __launch_bounds__(32 * kSimWarps) k_sim(SimArgs A) {
         bucket += f - frontier;
         frontier = f;
     };
-    auto run_flow = [&](const ws_out_flow& f) {
+    auto run_flow = [&](int fi) {
+        const ws_out_flow& f = V.fl[fi];
+        const uint64_t ma = fl_masks(fi)[0], mb = fl_masks(fi)[1];
+        if (!ma || !mb) return;
         double dur = 0.0;  // flow_duration (simulate.hpp:96-100)
         if (!opt.zero_volumes && f.volume != 0 && f.mode != WS_FLOW_COPY)
             dur = static_cast<double>(f.volume) / (f.mode == WS_FLOW_INTER ? P.inter_bw : P.intra_bw);
-        const uint64_t ma = sim_find(V, nW, lane, f.from_wave, f.from_metaop);
-        const uint64_t mb = sim_find(V, nW, lane, f.to_wave, f.to_metaop);
-        if (!ma || !mb) return;
         const uint64_t parties = ma | mb;
         const double t0 = lane_max2(parties, lane, av0, av1);
         busy_mask(parties, t0, dur);
@@ -297,13 +345,14 @@ __global__ void __launch_bounds__(32 * kSimWarps) k_sim(SimArgs A) {
         const double scale = backward ? opt.backward_ratio : 1.0;
         const ws_out_wave& wv = V.wv[w];
         uint64_t parts = 0;
-        for (int i = 0; i < wv.n_entries; ++i) parts |= sim_find(V, nW, lane, w, V.en[wv.entry_begin + i].metaop);
+        for (int i = lane; i < wv.n_entries; i += 32) parts |= *en_pl(wv.entry_begin + i);
+        parts = (static_cast<uint64_t>(__reduce_or_sync(kFull, static_cast<unsigned>(parts >> 32))) << 32) |
+                __reduce_or_sync(kFull, static_cast<unsigned>(parts));
         const double t0 = lane_max2(parts, lane, av0, av1);
         for (int i = 0; i < wv.n_entries; ++i) {
-            const ws_out_entry& e = V.en[wv.entry_begin + i];
-            const uint64_t m = sim_find(V, nW, lane, w, e.metaop);
+            const uint64_t m = *en_pl(wv.entry_begin + i);
             if (!m) continue;
-            const double dur = e.span * scale;
+            const double dur = V.en[wv.entry_begin + i].span * scale;
             busy_mask(m, t0, dur);
             if (m >> lane & 1ull) bc0 += dur;
             if (m >> (lane + 32) & 1ull) bc1 += dur;
@@ -314,10 +363,12 @@ __global__ void __launch_bounds__(32 * kSimWarps) k_sim(SimArgs A) {
         if (parts >> (lane + 32) & 1ull) av1 = (av1 < rel) ? rel : av1;
     };
     auto flows_where = [&](bool into, int w) {  // flows_into / flows_out_of, in flow order
-        for (int base = 0; base < nF; base += 32) {
+        for (unsigned b = __ballot_sync(kFull, (into ? ft0 : ff0) == w); b; b &= b - 1) run_flow(__ffs(b) - 1);
+        for (unsigned b = __ballot_sync(kFull, (into ? ft1 : ff1) == w); b; b &= b - 1) run_flow(32 + __ffs(b) - 1);
+        for (int base = 64; base < nF; base += 32) {
             const int f = base + lane;
             const bool hit = f < nF && (into ? V.fl[f].to_wave : V.fl[f].from_wave) == w;
-            for (unsigned b = __ballot_sync(kFull, hit); b; b &= b - 1) run_flow(V.fl[base + __ffs(b) - 1]);
+            for (unsigned b = __ballot_sync(kFull, hit); b; b &= b - 1) run_flow(base + __ffs(b) - 1);
         }
     };
     for (int j = 0; j < nW; ++j) {  // forward: transmissions arrive before their consumer wave
@@ -335,19 +386,25 @@ __global__ void __launch_bounds__(32 * kSimWarps) k_sim(SimArgs A) {
         attribute(send_recv);
     }
     if (!opt.skip_sync) {  // build_param_groups (simulate.hpp:127-165), group-wise sync (:268-276)
-        if (lane == 0) {
-            for (int w = 0; w < nW; ++w)
-                for (int i = 0; i < V.wv[w].n_entries; ++i) {
-                    const int k = V.en[V.wv[w].entry_begin + i].metaop;
-                    const uint64_t m = sim_find1(V, nW, w, k);
-                    if (!m || k < 0 || k >= K) continue;
+        for (int base = 0; base < nE; base += 32) {  // groups: device union and max gradient bytes
+            const int e = base + lane;
+            int g = -1;
+            uint64_t m = 0, gb = 0;
+            if (e < nE) {
+                const int k = V.en[e].metaop;
+                m = *en_pl(e);
+                if (m && k >= 0 && k < K) {
                     const int gm = mbase + V.mo[k].module;
                     const uint64_t pb = static_cast<uint64_t>(static_cast<double>(B.mod_param[gm]) *
                                                               V.mo[k].length / B.mod_layers[gm]);
-                    const uint64_t gb = 2ull * pb / static_cast<uint64_t>(B.mod_tp[gm]);
-                    gmask[gk[k]] |= m;
-                    gbytes[gk[k]] = gbytes[gk[k]] < gb ? gb : gbytes[gk[k]];
+                    gb = 2ull * pb / static_cast<uint64_t>(B.mod_tp[gm]);
+                    g = gk[k];
                 }
+            }
+            if (g >= 0) {
+                atomicOr(reinterpret_cast<unsigned long long*>(gmask + g), m);
+                atomicMax(reinterpret_cast<unsigned long long*>(gbytes + g), gb);
+            }
         }
         __syncwarp();
         // pool entries: one per distinct device set (first group holding it), bytes summed
@@ -385,9 +442,8 @@ __global__ void __launch_bounds__(32 * kSimWarps) k_sim(SimArgs A) {
         for (int r = 0; r < npool; ++r) {
             const int g = pord[r];
             const uint64_t m = gmask[g];
-            const int size = popc64(m);
             double dur = 0.0;
-            if (size >= 2) {
+            if (popc64(m) >= 2) {
                 int widest = 0, islands = 0;
                 for (int base = 0; base < P.n_islands; base += 32) {
                     const int i = base + lane;
@@ -415,16 +471,16 @@ __global__ void __launch_bounds__(32 * kSimWarps) k_sim(SimArgs A) {
     for (int w = 0; w < nW; ++w) {
         const ws_out_wave& wv = V.wv[w];
         for (int i = 0; i < wv.n_entries; ++i) {
-            const ws_out_entry& e = V.en[wv.entry_begin + i];
-            const int k = e.metaop;
-            const uint64_t m = sim_find(V, nW, lane, w, k);
+            const int e = wv.entry_begin + i;
+            const int k = V.en[e].metaop;
+            const uint64_t m = *en_pl(e);
             if (!m || k < 0 || k >= K) continue;
             const int gm = mbase + V.mo[k].module;
             const uint64_t pb = static_cast<uint64_t>(static_cast<double>(B.mod_param[gm]) * V.mo[k].length /
                                                       B.mod_layers[gm]);
             const uint64_t charged = chg[gk[k]];
             const double pstate = (1.0 + P.grad_mult) * static_cast<double>(pb) / B.mod_tp[gm];
-            const double act = e.layers * (static_cast<double>(B.mod_act[gm]) * 1.0 / e.n);
+            const double act = V.en[e].layers * (static_cast<double>(B.mod_act[gm]) * 1.0 / V.en[e].n);
             if (m >> lane & 1ull) {
                 if (!(charged >> lane & 1ull)) mem0 += pstate;
                 mem0 += act;
@@ -466,6 +522,8 @@ __global__ void __launch_bounds__(32 * kSimWarps) k_sim(SimArgs A) {
                                __ballot_sync(kFull, seen_k[0]);
 
     // ---- validate_plan (validate.hpp:58-188) ------------------------------
+    // Checks run lane-parallel; violations are appended by lane 0 in the
+    // reference's order, so only broken plans pay for the serial emission.
     int nv = 0;  // lane 0 holds the count
     auto fail = [&](int code, int wave, int a, int b, double x, double y) {
         if (nv < WS_SIM_MAX_VIOLATIONS) vio[nv] = ws_out_violation{code, wave, a, b, x, y};
@@ -473,46 +531,73 @@ __global__ void __launch_bounds__(32 * kSimWarps) k_sim(SimArgs A) {
     };
     const double horizon = R.end_time > 1.0 ? R.end_time : 1.0;  // std::max(1.0, end_time)
     const double tol = 1e-6 * horizon;
-    if (lane == 0) {  // per-wave entry checks, recomputed spans, executed layers
-        for (int w = 0; w < nW; ++w) {
-            const ws_out_wave& wv = V.wv[w];
-            uint64_t seen = 0;
-            int used = 0;
-            for (int i = 0; i < wv.n_entries; ++i) {
-                const int ei = wv.entry_begin + i;
-                const ws_out_entry& e = V.en[ei];
-                const int k = e.metaop;
-                if (k < 0 || k >= K) {
-                    fail(WS_V_UNKNOWN_ENTITY, w, k, 0, 0, 0);
-                    continue;
-                }
-                if (seen >> k & 1ull) fail(WS_V_DUPLICATE, w, k, 0, 0, 0);
-                seen |= 1ull << k;
+    enum { F_DUP = 1, F_UNKNOWN = 2, F_SPAN = 4, F_SPAN_DUR = 8 };
+    for (int w = 0; w < nW; ++w) {  // per-wave entry checks with recomputed spans
+        const ws_out_wave& wv = V.wv[w];
+        int used = 0;
+        bool any = false;
+        for (int i = lane; i < wv.n_entries; i += 32) {
+            const int e = wv.entry_begin + i;
+            const int k = V.en[e].metaop;
+            int flags = *en_flags(e) & F_DUP;
+            if (k < 0 || k >= K) {
+                flags = F_UNKNOWN;
+            } else {
                 const int gm = mbase + V.mo[k].module;
                 const double per_layer = eval_bf(V.pc + V.mo[k].piece_begin, V.mo[k].piece_count, B.mod_c[gm],
-                                                 B.mod_w[gm], static_cast<double>(e.n), 1.0);
-                const double span = e.layers * per_layer;
-                if (fabs(span - e.span) > tol + 1e-9 * fabs(span)) fail(WS_V_SPAN, w, k, 0, e.span, span);
-                if (e.span > wv.duration + tol) fail(WS_V_SPAN_DURATION, w, 0, 0, 0, 0);
-                s_iv[4 * ei] = wv.start + span;
-                s_iv[4 * ei + 1] = wv.start;
-                exec[k] += e.layers;
-                used += e.n;
+                                                 B.mod_w[gm], static_cast<double>(V.en[e].n), 1.0);
+                const double span = V.en[e].layers * per_layer;
+                const double rec = V.en[e].span;
+                if (fabs(span - rec) > tol + 1e-9 * fabs(span)) flags |= F_SPAN;
+                if (rec > wv.duration + tol) flags |= F_SPAN_DUR;
+                en_iv(e)[0] = wv.start + span;
+                en_iv(e)[1] = wv.start;
+                atomicAdd(exec + k, V.en[e].layers);
+                used += V.en[e].n;
             }
-            if (used > N) fail(WS_V_WAVE_DEVICES, w, 0, 0, 0, 0);
+            *en_flags(e) = flags;
+            any |= flags != 0;
         }
-        for (int r = 0; r < K; ++r) {  // work completion, entities in id order
-            const int k = by_rank[r];
-            if (exec[k] != V.mo[k].length) fail(WS_V_WORK, -1, k, exec[k], V.mo[k].length, 0);
+        used = static_cast<int>(__reduce_add_sync(kFull, static_cast<unsigned>(used)));
+        if (__any_sync(kFull, any)) {
+            __syncwarp();
+            if (lane == 0)
+                for (int i = 0; i < wv.n_entries; ++i) {
+                    const int e = wv.entry_begin + i;
+                    const int flags = *en_flags(e), k = V.en[e].metaop;
+                    if (flags & F_UNKNOWN) {
+                        fail(WS_V_UNKNOWN_ENTITY, w, k, 0, 0, 0);
+                        continue;
+                    }
+                    if (flags & F_DUP) fail(WS_V_DUPLICATE, w, k, 0, 0, 0);
+                    if (flags & F_SPAN) {
+                        const int gm = mbase + V.mo[k].module;
+                        const double span = V.en[e].layers * eval_bf(V.pc + V.mo[k].piece_begin, V.mo[k].piece_count,
+                                                                      B.mod_c[gm], B.mod_w[gm],
+                                                                      static_cast<double>(V.en[e].n), 1.0);
+                        fail(WS_V_SPAN, w, k, 0, V.en[e].span, span);
+                    }
+                    if (flags & F_SPAN_DUR) fail(WS_V_SPAN_DURATION, w, 0, 0, 0, 0);
+                }
         }
+        if (lane == 0 && used > N) fail(WS_V_WAVE_DEVICES, w, 0, 0, 0, 0);
     }
     __syncwarp();
+    {  // work completion, entities in id order
+        bool bad = false;
+        for (int k = lane; k < K; k += 32) bad |= exec[k] != V.mo[k].length;
+        if (__any_sync(kFull, bad) && lane == 0)
+            for (int r = 0; r < K; ++r) {
+                const int k = by_rank[r];
+                if (exec[k] != V.mo[k].length) fail(WS_V_WORK, -1, k, exec[k], V.mo[k].length, 0);
+            }
+    }
     // entry -> (start, end, n) of its interval; known MetaOps only
-    auto iv_of = [&](int ei, double& s, double& e, int& n) {
-        if (V.en[ei].metaop < 0 || V.en[ei].metaop >= K) return false;
-        e = s_iv[4 * ei];
-        s = s_iv[4 * ei + 1];
-        n = V.en[ei].n;
+    auto iv_of = [&](int e, double& s, double& en, int& n) {
+        if (V.en[e].metaop < 0 || V.en[e].metaop >= K) return false;
+        en = en_iv(e)[0];
+        s = en_iv(e)[1];
+        n = V.en[e].n;
         return true;
     };
     {  // instantaneous capacity: the first addition event after which active > N
@@ -542,26 +627,58 @@ __global__ void __launch_bounds__(32 * kSimWarps) k_sim(SimArgs A) {
         }
         if (lane == 0 && bi != 0x7fffffff) fail(WS_V_CAPACITY, -1, bact, 0, bt, 0);
     }
-    if (lane == 0) {  // same-entity intervals pairwise disjoint, entities in id order
-        for (int r = 0; r < K; ++r) {
-            const int k = by_rank[r];
-            int cnt = 0;
-            for (int w = 0; w < nW; ++w)  // by_entity lists keep wave / entry order
-                for (int i = 0; i < V.wv[w].n_entries; ++i)
-                    if (V.en[V.wv[w].entry_begin + i].metaop == k) lst[cnt++] = V.wv[w].entry_begin + i;
-            struct ByStart {  // std::sort by interval start (exact libstdc++ emulation)
-                const double* iv;
-                __device__ bool operator()(int a, int b) const { return iv[4 * a + 1] < iv[4 * b + 1]; }
-            } cmp{s_iv};
-            ls_sort(lst, cnt, cmp);
-            for (int i = 0; i + 1 < cnt; ++i)
-                if (s_iv[4 * lst[i]] > s_iv[4 * lst[i + 1] + 1] + tol) {
-                    fail(WS_V_OVERLAP, -1, k, 0, 0, 0);
-                    break;
+    {  // same-entity intervals pairwise disjoint, entities in id order; lane per
+       // entity walks its intervals in wave order (strictly increasing starts =
+       // the sorted order), ties or inversions take the exact std::sort path
+        unsigned flag_lo = 0, flag_hi = 0;  // bit per entity: 1 overlap, 2 needs sort
+        for (int s = 0; s < 2; ++s) {
+            const int k = lane + 32 * s;
+            if (k >= K) continue;
+            int fl = 0;
+            double pe = 0.0, ps = 0.0;
+            bool first = true;
+            for (int w = 0; w < nW && !(fl & 2); ++w)
+                for (int i = 0; i < V.wv[w].n_entries; ++i) {
+                    const int e = V.wv[w].entry_begin + i;
+                    if (V.en[e].metaop != k) continue;
+                    const double st = en_iv(e)[1], en = en_iv(e)[0];
+                    if (!first) {
+                        if (!(ps < st)) {
+                            fl |= 2;
+                            break;
+                        }
+                        if (pe > st + tol) fl |= 1;
+                    }
+                    first = false;
+                    ps = st;
+                    pe = en;
                 }
+            (s ? flag_hi : flag_lo) = static_cast<unsigned>(fl);
+        }
+        const bool any = __any_sync(kFull, (flag_lo | flag_hi) != 0);
+        if (any) {
+            if (lane == 0) {
+                for (int r = 0; r < K; ++r) {
+                    const int k = by_rank[r];
+                    int cnt = 0;
+                    for (int w = 0; w < nW; ++w)  // by_entity lists keep wave / entry order
+                        for (int i = 0; i < V.wv[w].n_entries; ++i)
+                            if (V.en[V.wv[w].entry_begin + i].metaop == k) lst[cnt++] = V.wv[w].entry_begin + i;
+                    struct ByStart {  // std::sort by interval start (exact libstdc++ emulation)
+                        const double* iv;
+                        __device__ bool operator()(int a, int b) const { return iv[4 * a + 1] < iv[4 * b + 1]; }
+                    } cmp{en_iv(0)};
+                    ls_sort(lst, cnt, cmp);
+                    for (int i = 0; i + 1 < cnt; ++i)
+                        if (en_iv(lst[i])[0] > en_iv(lst[i + 1])[1] + tol) {
+                            fail(WS_V_OVERLAP, -1, k, 0, 0, 0);
+                            break;
+                        }
+                }
+            }
+            __syncwarp();
         }
     }
-    __syncwarp();
     for (int q = 0; q < R.n_edges; ++q) {  // dependencies, in MetaGraph edge order
         const int from = V.ed[q].from, to = V.ed[q].to;
         double fe = 0.0, ts = horizon * 2;
@@ -582,25 +699,39 @@ __global__ void __launch_bounds__(32 * kSimWarps) k_sim(SimArgs A) {
     bool any_placed = false;
     for (int i = lane; i < nE; i += 32) any_placed |= V.en[i].devmask != 0;
     if (__any_sync(kFull, any_placed)) {
-        if (lane == 0) {  // per wave: placed, sized, disjoint (device-list order)
-            for (int w = 0; w < nW; ++w) {
+        for (int w = 0; w < nW; ++w) {  // per wave: placed, sized, disjoint (device-list order)
+            const ws_out_wave& wv = V.wv[w];
+            bool bad = false;
+            uint64_t uni = 0;
+            int sum = 0;
+            for (int i = lane; i < wv.n_entries; i += 32) {
+                const int e = wv.entry_begin + i;
+                const uint64_t m = *en_pl(e);
+                bad |= !m || popc64(m) != V.en[e].n || (m & ~all) != 0;
+                uni |= m;
+                sum += popc64(m);
+            }
+            uni = (static_cast<uint64_t>(__reduce_or_sync(kFull, static_cast<unsigned>(uni >> 32))) << 32) |
+                  __reduce_or_sync(kFull, static_cast<unsigned>(uni));
+            sum = static_cast<int>(__reduce_add_sync(kFull, static_cast<unsigned>(sum)));
+            if (!__any_sync(kFull, bad) && sum == popc64(uni)) continue;
+            if (lane == 0) {
                 uint64_t taken = 0;
-                for (int i = 0; i < V.wv[w].n_entries; ++i) {
-                    const ws_out_entry& e = V.en[V.wv[w].entry_begin + i];
-                    const uint64_t m = sim_find1(V, nW, w, e.metaop);
+                for (int i = 0; i < wv.n_entries; ++i) {
+                    const int e = wv.entry_begin + i;
+                    const uint64_t m = *en_pl(e);
                     if (!m) {
-                        fail(WS_V_UNPLACED, w, e.metaop, 0, 0, 0);
+                        fail(WS_V_UNPLACED, w, V.en[e].metaop, 0, 0, 0);
                         continue;
                     }
-                    // the placed entry's rot orders its device list
-                    int rot = 0;
-                    for (int j = 0; j < V.wv[w].n_entries; ++j) {
-                        const ws_out_entry& x = V.en[V.wv[w].entry_begin + j];
-                        if (x.metaop == e.metaop && x.devmask) rot = x.rot;
+                    int rot = 0;  // the placed entry's rot orders its device list
+                    for (int j = 0; j < wv.n_entries; ++j) {
+                        const ws_out_entry& x = V.en[wv.entry_begin + j];
+                        if (x.metaop == V.en[e].metaop && x.devmask) rot = x.rot;
                     }
-                    if (popc64(m) != e.n) fail(WS_V_DEVICE_COUNT, w, e.metaop, popc64(m), e.n, 0);
-                    const uint64_t order[2] = {m & ~((rot >= 64 ? ~0ull : (1ull << rot)) - 1ull),
-                                               m & ((rot >= 64 ? ~0ull : (1ull << rot)) - 1ull)};
+                    if (popc64(m) != V.en[e].n) fail(WS_V_DEVICE_COUNT, w, V.en[e].metaop, popc64(m), V.en[e].n, 0);
+                    const uint64_t below = rot >= 64 ? ~0ull : ((1ull << rot) - 1ull);
+                    const uint64_t order[2] = {m & ~below, m & below};
                     for (int h = 0; h < 2; ++h)
                         for (uint64_t b = order[h]; b; b &= b - 1) {
                             const int d = low_bit(b);
@@ -613,6 +744,7 @@ __global__ void __launch_bounds__(32 * kSimWarps) k_sim(SimArgs A) {
                         }
                 }
             }
+            __syncwarp();
         }
         const double cap = static_cast<double>(P.mem_capacity) * (1.0 + 1e-9);
         for (int h = 0; h < 2; ++h) {  // memory capacity, devices in id order
@@ -622,7 +754,8 @@ __global__ void __launch_bounds__(32 * kSimWarps) k_sim(SimArgs A) {
             for (unsigned q = b; q; q &= q - 1) {
                 const int src = __ffs(q) - 1;
                 const double x = __shfl_sync(kFull, mv, src);
-                if (lane == 0) fail(WS_V_MEMORY, -1, 32 * h + src, 0, x, __longlong_as_double(static_cast<long long>(P.mem_capacity)));
+                if (lane == 0)
+                    fail(WS_V_MEMORY, -1, 32 * h + src, 0, x, __longlong_as_double(static_cast<long long>(P.mem_capacity)));
             }
         }
     }
