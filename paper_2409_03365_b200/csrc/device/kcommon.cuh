@@ -292,6 +292,24 @@ __device__ __forceinline__ double warp_max_d(double v) {  // std::max fold, NaN-
     return v;
 }
 
+// warp max of doubles >= +0.0 (clocks, durations): their IEEE bit patterns
+// order like the values, so two redux.sync steps (high word, then low word
+// among the lanes holding the maximum high word) give the exact maximum
+__device__ __forceinline__ double warp_max_nonneg(double v) {
+    const unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(v));
+    const unsigned hi = __reduce_max_sync(kFull, static_cast<unsigned>(b >> 32));
+    const unsigned lo = __reduce_max_sync(kFull, static_cast<unsigned>(b >> 32) == hi ? static_cast<unsigned>(b) : 0u);
+    return __longlong_as_double(static_cast<long long>((static_cast<unsigned long long>(hi) << 32) | lo));
+}
+
+__device__ __forceinline__ double warp_min_nonneg(double v) {  // same, minimum (+inf allowed)
+    const unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(v));
+    const unsigned hi = __reduce_min_sync(kFull, static_cast<unsigned>(b >> 32));
+    const unsigned lo =
+        __reduce_min_sync(kFull, static_cast<unsigned>(b >> 32) == hi ? static_cast<unsigned>(b) : 0xffffffffu);
+    return __longlong_as_double(static_cast<long long>((static_cast<unsigned long long>(hi) << 32) | lo));
+}
+
 __device__ __forceinline__ double warp_min_d(double v) {
     for (int off = 16; off; off >>= 1) {
         const double o = __shfl_xor_sync(kFull, v, off);

@@ -631,7 +631,7 @@ __device__ bool s_level_alloc(SCtx& C, int lvl, double& c_star_out) {
         lo0 = (lo0 < v) ? v : lo0;
         hi0[s] = t_at(F, q.gm, 1) * q.L;
     }
-    double c_lo = warp_max_d(lo0);
+    double c_lo = warp_max_nonneg(lo0);
     double c_hi = ordered_sum(hi0[0], hi0[1], w);
     auto probe_term = [&](const Mem& q, double cc) {
         const double v = q.inv(cc / q.L);
@@ -1096,7 +1096,7 @@ __device__ int fast_wave(SCtx& C, SchedView& S) {
     // align_time_span: t_wave = min span over the chosen set
     const double per = in ? t_at(F, gm, n) : 0.0;
     const double span = in ? sl * per : 0.0;
-    const double t_wave = warp_min_d(in ? span : __longlong_as_double(0x7ff0000000000000ll));
+    const double t_wave = warp_min_nonneg(in ? span : __longlong_as_double(0x7ff0000000000000ll));
     if (in) {
         int kk;
         if (sl * per <= t_wave * (1.0 + 1e-12)) {
@@ -1210,7 +1210,7 @@ __device__ bool s_schedule_level(SCtx& C, char* rec, const RecLayout& RL, int lv
             S.tl[t] -= kk - ab;
             absorb[k] = ab;
         }
-        const double dur = warp_max_d(span);
+        const double dur = warp_max_nonneg(span);
         if (lane == 0) {
             w_level[nW] = lvl;
             w_eb[nW] = nE;
@@ -1255,7 +1255,7 @@ __device__ bool s_schedule_level(SCtx& C, char* rec, const RecLayout& RL, int lv
             const double e = w_start[i] + w_dur[i];
             le = (le < e) ? e : le;
         }
-    level_end = warp_max_d(le);
+    level_end = warp_max_nonneg(le);
     return true;
 }
 

@@ -169,10 +169,13 @@ __device__ __forceinline__ double lane_max2(uint64_t mask, int lane, double a0, 
     double t = 0.0;
     if (mask >> lane & 1ull) t = a0;
     if (mask >> (lane + 32) & 1ull) t = (t < a1) ? a1 : t;
-    return warp_max_d(t);
+    return warp_max_nonneg(t);
 }
 
-__global__ void __launch_bounds__(32 * kSimWarps) k_sim(SimArgs A) {
+#ifndef WS_SIM_MINB
+#define WS_SIM_MINB 1
+#endif
+__global__ void __launch_bounds__(32 * kSimWarps, WS_SIM_MINB) k_sim(SimArgs A) {
     extern __shared__ __align__(16) char sim_smem[];
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int p = blockIdx.x * kSimWarps + wid;
@@ -197,7 +200,7 @@ __global__ void __launch_bounds__(32 * kSimWarps) k_sim(SimArgs A) {
     // per-entry / per-flow scratch mirroring the record (one 32-byte slot each):
     // entry: [0] interval end (f64), [1] start (f64), [2] check flags (i32),
     //        [3] plan.devices placement of its (wave, MetaOp) key (u64)
-    // flow:  [0] source placement, [1] destination placement
+    // flow:  [0] source placement, [1] destination placement, [2] flow_duration
     uint8_t* const s_rec = A.scratch + R.offset;
     auto en_iv = [&](int e) { return reinterpret_cast<double*>(s_rec + V.en_off + 32ull * e); };
     auto en_pl = [&](int e) { return reinterpret_cast<uint64_t*>(s_rec + V.en_off + 32ull * e + 24); };
@@ -296,6 +299,10 @@ __global__ void __launch_bounds__(32 * kSimWarps) k_sim(SimArgs A) {
             }
         fl_masks(f)[0] = ma;
         fl_masks(f)[1] = mb;
+        double dur = 0.0;  // flow_duration (simulate.hpp:96-100)
+        if (!A.opt.zero_volumes && x.volume != 0 && x.mode != WS_FLOW_COPY)
+            dur = static_cast<double>(x.volume) / (x.mode == WS_FLOW_INTER ? P.inter_bw : P.intra_bw);
+        reinterpret_cast<double*>(fl_masks(f))[2] = dur;
     }
     // the first 64 flows' waves stay in registers for the per-wave flow scans
     const int ft0 = lane < nF ? V.fl[lane].to_wave : -1, ff0 = lane < nF ? V.fl[lane].from_wave : -1;
@@ -330,9 +337,7 @@ __global__ void __launch_bounds__(32 * kSimWarps) k_sim(SimArgs A) {
         const ws_out_flow& f = V.fl[fi];
         const uint64_t ma = fl_masks(fi)[0], mb = fl_masks(fi)[1];
         if (!ma || !mb) return;
-        double dur = 0.0;  // flow_duration (simulate.hpp:96-100)
-        if (!opt.zero_volumes && f.volume != 0 && f.mode != WS_FLOW_COPY)
-            dur = static_cast<double>(f.volume) / (f.mode == WS_FLOW_INTER ? P.inter_bw : P.intra_bw);
+        const double dur = reinterpret_cast<const double*>(fl_masks(fi))[2];
         const uint64_t parties = ma | mb;
         const double t0 = lane_max2(parties, lane, av0, av1);
         busy_mask(parties, t0, dur);
