@@ -243,6 +243,34 @@ def main() -> None:
     alg_in, alg_out = ps.algorithmic_bytes(res)
     d2h_bytes = len(ps) * ctypes_sizeof_result() + int(res.arena_used.value)
 
+    # ---- plan evaluation: simulate_plan + validate_plan
+    # of every planned mixture on the device (k_sim), records already resident ----
+    for _ in range(2):
+        planner.simulate_staged(sptr)
+    barrier()
+    sim_ms = []
+    for _ in range(args.steps):
+        flush.zero_()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        planner.simulate_staged(sptr)
+        e1.record(stream)
+        e1.synchronize()
+        sim_ms.append(e0.elapsed_time(e1))
+    barrier()
+    sims = planner.fetch_sim(ps, sptr)
+    n_invalid = sum(1 for i in range(len(ps)) if sims.results[i].status == 0 and not sims.results[i].valid)
+    skey, sli = planner.best(2, sptr)
+    sgi = parallel.local_to_global(sli, rank, world) if sli >= 0 else -1
+    best_sim, best_sim_idx = parallel.global_best(skey if sli >= 0 else float("inf"), sgi, dev)
+    ts = torch.tensor([sum(sim_ms) / 1000.0, float(n_invalid)], dtype=torch.float64, device=dev)
+    if world > 1:
+        torch.distributed.all_reduce(ts[:1], op=torch.distributed.ReduceOp.MAX)
+        torch.distributed.all_reduce(ts[1:], op=torch.distributed.ReduceOp.SUM)
+    sim_value = args.mixtures * args.steps / float(ts[0].item())
+    n_invalid = int(ts[1].item())
+
     # ---- end to end through the C-ABI host call (page-locked host buffers) ----
     r2 = None
     for _ in range(2):
@@ -314,8 +342,22 @@ def main() -> None:
         latency[name] = {"gpu_e2e_ms_median": statistics.median(samples)}
 
     cpu = None
+    evaluation = {"what": "simulate_plan + validate_plan of every planned mixture (k_sim, device-resident records)",
+                  "value": sim_value, "unit": "evaluations/s", "ms_per_step": 1000.0 * float(ts[0].item()) / args.steps,
+                  "plan_and_evaluate_per_s": args.mixtures / (t_max / args.steps + float(ts[0].item()) / args.steps),
+                  "invalid_plans": n_invalid, "best_simulated_makespan": best_sim, "best_index": best_sim_idx}
     if not args.no_cpu_baseline:
         cpu = cpu_baseline(args.cpu_sample, os.cpu_count() or 1)
+        try:
+            import pyoracle as po
+            if po.ref_available():
+                n_ev = max(args.cpu_sample // 2, 500)
+                evaluation["cpu_reference_plan_and_evaluate_per_s"] = po.ref_sweep_sim_bench(
+                    0, n_ev, os.cpu_count() or 1)
+                evaluation["cpu_reference_sample"] = (f"sweep mixtures 0..{n_ev - 1}, reference plan_workload + "
+                                                      f"simulate_plan + validate_plan, {os.cpu_count()} threads")
+        except Exception:
+            pass
         try:
             import pyoracle as po
             if po.ref_available():
@@ -352,6 +394,7 @@ def main() -> None:
         "gpu_launches": launches_per_step * args.steps,
         "clocks": clk,
         "latency_ms": latency,
+        "evaluation": evaluation,
         "parity": {"infeasible_plans": int(infeasible.item()), "best_gap": best_key, "best_index": best_idx},
     }
     print(json.dumps(line), flush=True)

@@ -20,6 +20,9 @@ if timeout 600 $NCU_CMD > $OUT/ncu_plain_$TAG.log 2>&1; then
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_sched -s 4 -c 1 \
       -o $OUT/ksched_$TAG $NCU_CMD > $OUT/ncu_fullfit_$TAG.log 2>&1
   echo "ncu fit rc=$?" | tee -a $OUT/summary_$TAG.txt
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_sim -s 2 -c 1 \
+      -o $OUT/ksim_$TAG $NCU_CMD > $OUT/ncu_fullsim_$TAG.log 2>&1
+  echo "ncu sim rc=$?" | tee -a $OUT/summary_$TAG.txt
 fi
 tail -5 $OUT/pytest_gpu_$TAG.log
 cat $OUT/smoke_$TAG.log | tail -2
