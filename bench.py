@@ -292,7 +292,9 @@ def main() -> None:
     if world > 1:
         torch.distributed.all_reduce(te, op=torch.distributed.ReduceOp.MAX)
     e2e_value = args.mixtures * args.steps / float(te.item())
-    d2h_step = len(ps) * ctypes_sizeof_result() + int(r2.arena_used.value)
+    # bytes the pipelined call copies back: every result header + each plan's record
+    d2h_step = len(ps) * ctypes_sizeof_result() + sum(int(r2.results[i].size) for i in range(len(ps))
+                                                      if r2.results[i].status == 0)
 
     if rank != 0:
         if world > 1:

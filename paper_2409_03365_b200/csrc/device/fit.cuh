@@ -49,9 +49,10 @@ struct PieceLoCmp {  // from_pieces sort key (scaling.hpp:45-46)
     __device__ bool operator()(int a, int b) const { return p[a].lo < p[b].lo; }
 };
 
-__global__ void __launch_bounds__(128) k_fit(ws_batch B, FitOut out) {
-    const int m = blockIdx.x * blockDim.x + threadIdx.x;
-    if (m >= B.n_modules) return;
+// modules [m_begin, m_end) of the batch (a pipelined chunk, or all of them)
+__global__ void __launch_bounds__(128) k_fit(ws_batch B, FitOut out, int m_begin, int m_end) {
+    const int m = m_begin + blockIdx.x * blockDim.x + threadIdx.x;
+    if (m >= m_end) return;
     const ws_plan_rec& R = B.plans[B.mod_plan[m]];
     const int N = R.n_dev;
     const double c = B.mod_c[m], w = B.mod_w[m];

@@ -34,6 +34,7 @@ constexpr int kRetryMax = 1024;               // plans re-run with hard caps per
 constexpr int64_t kOverflowPieces = 1 << 18;  // isotonic/long curves
 constexpr int kSmemLimit = 227 * 1024;
 constexpr int kMaxChunks = 16;  // k_sched/k_place pipeline depth
+constexpr int kMaxHostChunks = 8;  // H2D / compute / D2H pipeline depth of ws_plan_batch_host
 
 struct DevBuf {
     void* p = nullptr;
@@ -57,9 +58,9 @@ struct DevBuf {
 };
 
 // plans whose soft record caps overflowed get queued for the retry launch
-__global__ void k_soft_collect(const ws_plan_result* res, int n, int32_t* ids, int32_t* count) {
-    const int p = blockIdx.x * blockDim.x + threadIdx.x;
-    if (p >= n) return;
+__global__ void k_soft_collect(const ws_plan_result* res, int p_begin, int p_end, int32_t* ids, int32_t* count) {
+    const int p = p_begin + blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= p_end) return;
     const int e = res[p].err_code;
     if (e == WS_E_LIMIT_WAVES || e == WS_E_LIMIT_ENTRIES || e == WS_E_LIMIT_FLOWS) {
         const int slot = atomicAdd(count, 1);
@@ -179,6 +180,15 @@ struct ws_ctx {
     ws_plan_result* d_results = nullptr;
     uint8_t* d_arena = nullptr;
     uint64_t d_cap = 0;
+    // pipelined host call: arena top counter / capacity of the chunk in flight
+    unsigned long long* top_ptr = nullptr;
+    uint64_t top_cap = 0;
+    DevBuf chunk_tops;
+    cudaStream_t stream3 = nullptr;          // D2H side of the host pipeline (stream2: H2D side)
+    unsigned long long* host_tops = nullptr; // page-locked: chunk bases, chunk tops, final top
+    // measured (100k sweep): 1 chunk 27.8 ms, 2: 27.7, 4: 32.4, 8: 35.1 -- every
+    // chunk adds a k_sched + k_place launch tail that outweighs the hidden copies
+    int host_chunks = 1;                     // $WSGPU_HOST_CHUNKS
     ws_plan_result* res_out() { return d_results ? d_results : results.as<ws_plan_result>(); }
     uint8_t* arena_out() { return d_arena ? d_arena : arena.as<uint8_t>(); }
     uint64_t cap_out() const { return d_arena ? d_cap : arena_cap; }
@@ -284,8 +294,8 @@ int launch_pair(ws_ctx* ctx, cudaStream_t st, const LaunchCaps& lc, const FitOut
     P.rec_by_slot = by_slot ? 1 : 0;
     P.results = ctx->res_out();
     P.arena = ctx->arena_out();
-    P.arena_top = ctx->counters.as<unsigned long long>();
-    P.arena_cap = ctx->cap_out();
+    P.arena_top = ctx->top_ptr ? ctx->top_ptr : ctx->counters.as<unsigned long long>();
+    P.arena_cap = ctx->top_ptr ? ctx->top_cap : ctx->cap_out();
     if (kPlaceWarps * P.PL.bytes > kSmemLimit) return fail(ctx, "k_place working set exceeds shared memory");
     CK(cudaFuncSetAttribute(k_place, cudaFuncAttributeMaxDynamicSharedMemorySize, kPlaceWarps * P.PL.bytes));
 
@@ -346,7 +356,13 @@ int ws_ctx_create(int device, ws_ctx** out) {
         delete c;
         return 1;
     }
+    if (cudaStreamCreateWithFlags(&c->stream3, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaMallocHost(reinterpret_cast<void**>(&c->host_tops), 8 * (2 * kMaxHostChunks + 8)) != cudaSuccess) {
+        delete c;
+        return 1;
+    }
     if (const char* env = std::getenv("WSGPU_CHUNKS")) c->chunks = std::atoi(env);
+    if (const char* env = std::getenv("WSGPU_HOST_CHUNKS")) c->host_chunks = std::atoi(env);
     *out = c;
     return 0;
 }
@@ -360,6 +376,8 @@ void ws_ctx_destroy(ws_ctx* c) {
         if (e) cudaEventDestroy(e);
     if (c->stream) cudaStreamDestroy(c->stream);
     if (c->stream2) cudaStreamDestroy(c->stream2);
+    if (c->stream3) cudaStreamDestroy(c->stream3);
+    if (c->host_tops) cudaFreeHost(c->host_tops);
     delete c;
 }
 
@@ -372,6 +390,59 @@ int ws_last_kernel_ms(const ws_ctx* c, double* out, int n) {
     for (int i = 0; i < n && i < 3; ++i) out[i] = c->kernel_ms[i];
     return 0;
 }
+
+namespace {
+// device buffers of a planning call sized for the staged batch, and the k_fit output view
+int prepare_plan(ws_ctx* ctx, FitOut& fo) {
+    const ws_batch& B = ctx->dview;
+    const int P = B.n_plans, NM = std::max(B.n_modules, 1);
+    const LaunchCaps& lc = ctx->caps;
+    const LaunchCaps& lh = ctx->caps_hard;
+    const int tstride = lc.pl.N;
+    if (!ctx->fit_err.ensure(4ull * NM) || !ctx->fit_a.ensure(4ull * NM) || !ctx->fit_b.ensure(4ull * NM) ||
+        !ctx->fit_np.ensure(4ull * NM) || !ctx->fit_nmax.ensure(4ull * NM) || !ctx->fit_off.ensure(8ull * NM) ||
+        !ctx->fit_pieces.ensure(40ull * (static_cast<uint64_t>(NM) * kInlinePieces + kOverflowPieces)) ||
+        !ctx->ttab.ensure(8ull * NM * tstride))
+        return fail(ctx, "cudaMalloc fit buffers");
+    const RecLayout RL = make_rec_layout(lc.rec), RLh = make_rec_layout(lh.rec);
+    if (!ctx->counters.ensure(64) || !ctx->results.ensure(sizeof(ws_plan_result) * std::max(P, 1)) ||
+        !ctx->arena.ensure(ctx->arena_cap) || !ctx->retry_ids.ensure(4 * kRetryMax) || !ctx->best.ensure(64) ||
+        !ctx->recs.ensure(static_cast<size_t>(RL.bytes) * std::max(P, 1)) ||
+        !ctx->flows.ensure(16ull * lc.pl.F * std::max(P, 1)) ||
+        !ctx->recs_r.ensure(static_cast<size_t>(RLh.bytes) * kRetryMax) ||
+        !ctx->flows_r.ensure(16ull * lh.pl.F * kRetryMax))
+        return fail(ctx, "cudaMalloc planner buffers");
+    auto* counters = ctx->counters.as<unsigned long long>();
+    fo.err = ctx->fit_err.as<int32_t>();
+    fo.err_a = ctx->fit_a.as<int32_t>();
+    fo.err_b = ctx->fit_b.as<int32_t>();
+    fo.npieces = ctx->fit_np.as<int32_t>();
+    fo.nmax = ctx->fit_nmax.as<int32_t>();
+    fo.piece_off = ctx->fit_off.as<int64_t>();
+    fo.pieces = ctx->fit_pieces.as<double>();
+    fo.overflow_top = counters + 1;
+    fo.overflow_base = static_cast<int64_t>(NM) * kInlinePieces;
+    fo.overflow_cap = kOverflowPieces;
+    fo.ttab = ctx->ttab.as<double>();
+    fo.tstride = tstride;
+    return 0;
+}
+
+// longest-processing-time launch order of plans [p0, p1): descending
+// modules x devices by a stable counting sort (O(plans) on the host)
+void lpt_order(ws_ctx* ctx, const ws_plan_rec* plans, int p0, int p1) {
+    constexpr int kKeys = (WS_MAX_MODULES + 1) * (WS_MAX_DEVICES + 9);
+    auto key = [&](int p) {
+        const ws_plan_rec& r = plans[p];
+        const int m = std::min(std::max(r.n_mod, 0), WS_MAX_MODULES), d = std::min(std::max(r.n_dev, 0), WS_MAX_DEVICES);
+        return kKeys - 1 - m * (d + 8);
+    };
+    ctx->key_count.assign(kKeys + 1, 0);
+    for (int p = p0; p < p1; ++p) ctx->key_count[key(p) + 1]++;
+    for (int k = 0; k < kKeys; ++k) ctx->key_count[k + 1] += ctx->key_count[k];
+    for (int p = p0; p < p1; ++p) ctx->order_host[p0 + ctx->key_count[key(p)]++] = p;
+}
+}  // namespace
 
 int ws_stage_batch(ws_ctx* ctx, const ws_batch* in, void* stream) {
     cudaSetDevice(ctx->device);
@@ -388,19 +459,8 @@ int ws_stage_batch(ws_ctx* ctx, const ws_batch* in, void* stream) {
     ctx->sim_cap = ws_sim_arena_bound(in);
     ctx->records_on_device = false;
     ctx->sim_valid = false;
-    // longest-processing-time launch order: descending modules x devices, by a
-    // stable counting sort over the small key range (O(plans) on the host)
-    constexpr int kKeys = (WS_MAX_MODULES + 1) * (WS_MAX_DEVICES + 9);
-    auto key = [&](int p) {
-        const ws_plan_rec& r = in->plans[p];
-        const int m = std::min(std::max(r.n_mod, 0), WS_MAX_MODULES), d = std::min(std::max(r.n_dev, 0), WS_MAX_DEVICES);
-        return kKeys - 1 - m * (d + 8);
-    };
     ctx->order_host.resize(P);
-    ctx->key_count.assign(kKeys + 1, 0);
-    for (int p = 0; p < P; ++p) ctx->key_count[key(p) + 1]++;
-    for (int k = 0; k < kKeys; ++k) ctx->key_count[k + 1] += ctx->key_count[k];
-    for (int p = 0; p < P; ++p) ctx->order_host[ctx->key_count[key(p)]++] = p;
+    lpt_order(ctx, in->plans, 0, P);
     if (P) CK(cudaMemcpyAsync(ctx->order.p, ctx->order_host.data(), 4ull * P, cudaMemcpyHostToDevice, st));
     return 0;
 }
@@ -409,43 +469,18 @@ int ws_plan_staged(ws_ctx* ctx, void* stream) {
     cudaSetDevice(ctx->device);
     cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
     const ws_batch& B = ctx->dview;
-    const int P = B.n_plans, NM = std::max(B.n_modules, 1);
+    const int P = B.n_plans;
     const LaunchCaps& lc = ctx->caps;
     const LaunchCaps& lh = ctx->caps_hard;
     ctx->launches = 0;
-    const int tstride = lc.pl.N;
-    if (!ctx->fit_err.ensure(4ull * NM) || !ctx->fit_a.ensure(4ull * NM) || !ctx->fit_b.ensure(4ull * NM) ||
-        !ctx->fit_np.ensure(4ull * NM) || !ctx->fit_nmax.ensure(4ull * NM) || !ctx->fit_off.ensure(8ull * NM) ||
-        !ctx->fit_pieces.ensure(40ull * (static_cast<uint64_t>(NM) * kInlinePieces + kOverflowPieces)) ||
-        !ctx->ttab.ensure(8ull * NM * tstride))
-        return fail(ctx, "cudaMalloc fit buffers");
-    const RecLayout RL = make_rec_layout(lc.rec), RLh = make_rec_layout(lh.rec);
-    if (!ctx->counters.ensure(64) || !ctx->results.ensure(sizeof(ws_plan_result) * std::max(P, 1)) ||
-        !ctx->arena.ensure(ctx->arena_cap) || !ctx->retry_ids.ensure(4 * kRetryMax) || !ctx->best.ensure(64) ||
-        !ctx->recs.ensure(static_cast<size_t>(RL.bytes) * std::max(P, 1)) ||
-        !ctx->flows.ensure(16ull * lc.pl.F * std::max(P, 1)) ||
-        !ctx->recs_r.ensure(static_cast<size_t>(RLh.bytes) * kRetryMax) ||
-        !ctx->flows_r.ensure(16ull * lh.pl.F * kRetryMax))
-        return fail(ctx, "cudaMalloc planner buffers");
+    FitOut fo;
+    if (prepare_plan(ctx, fo)) return 1;
     auto* counters = ctx->counters.as<unsigned long long>();  // [0] arena top [1] overflow top [2] retry count
     CK(cudaMemsetAsync(counters, 0, 64, st));
-    FitOut fo;
-    fo.err = ctx->fit_err.as<int32_t>();
-    fo.err_a = ctx->fit_a.as<int32_t>();
-    fo.err_b = ctx->fit_b.as<int32_t>();
-    fo.npieces = ctx->fit_np.as<int32_t>();
-    fo.nmax = ctx->fit_nmax.as<int32_t>();
-    fo.piece_off = ctx->fit_off.as<int64_t>();
-    fo.pieces = ctx->fit_pieces.as<double>();
-    fo.overflow_top = counters + 1;
-    fo.overflow_base = static_cast<int64_t>(NM) * kInlinePieces;
-    fo.overflow_cap = kOverflowPieces;
-    fo.ttab = ctx->ttab.as<double>();
-    fo.tstride = tstride;
 
     CK(cudaEventRecord(ctx->ev[0], st));
     if (B.n_modules > 0) {
-        k_fit<<<(B.n_modules + 127) / 128, 128, 0, st>>>(B, fo);
+        k_fit<<<(B.n_modules + 127) / 128, 128, 0, st>>>(B, fo, 0, B.n_modules);
         ctx->launches++;
     }
     CK(cudaEventRecord(ctx->ev[1], st));
@@ -455,7 +490,7 @@ int ws_plan_staged(ws_ctx* ctx, void* stream) {
     // retry pass: soft-cap overflows with the hard caps, count read on device
     auto* rcount = reinterpret_cast<int32_t*>(counters + 2);
     if (P > 0) {
-        k_soft_collect<<<(P + 255) / 256, 256, 0, st>>>(ctx->res_out(), P,
+        k_soft_collect<<<(P + 255) / 256, 256, 0, st>>>(ctx->res_out(), 0, P,
                                                          ctx->retry_ids.as<int32_t>(), rcount);
         k_clamp_count<<<1, 1, 0, st>>>(rcount);
         ctx->launches += 2;
@@ -465,7 +500,7 @@ int ws_plan_staged(ws_ctx* ctx, void* stream) {
     }
     CK(cudaEventRecord(ctx->ev[2], st));
     CK(cudaGetLastError());
-    ctx->records_on_device = ctx->d_arena == nullptr;
+    ctx->records_on_device = true;
     ctx->sim_valid = false;
     return 0;
 }
@@ -492,46 +527,150 @@ int ws_fetch_results(ws_ctx* ctx, ws_plan_result* results, uint8_t* arena, uint6
     return 0;
 }
 
-namespace {
-void* mapped_device_ptr(void* host) {  // device alias of page-locked host memory, else null
-    cudaPointerAttributes a{};
-    if (!host || cudaPointerGetAttributes(&a, host) != cudaSuccess) {
-        cudaGetLastError();
-        return nullptr;
-    }
-    return a.type == cudaMemoryTypeHost ? a.devicePointer : nullptr;
-}
-}  // namespace
+extern "C" uint64_t wsi_arena_bound_plans(const ws_plan_rec* plans, int n);
 
+// Host batch in, host results out.  Default: stage (one H2D copy), plan on the
+// device, fetch (results + used arena, two D2H copies).  Optionally
+// ($WSGPU_HOST_CHUNKS > 1) as a pipeline over C chunks of plans:
+// the H2D copy of chunk c+1 (its byte ranges of every SoA section: sections
+// are plan-ordered, so a chunk's rows are contiguous) and the D2H copy of
+// chunk c-1 (results rows + its own arena region) overlap the kernels of
+// chunk c.  Kernels always write device memory (zero-copy writes into host
+// memory stall k_place on PCIe: measured 20 ms vs 11 ms per 100k).
 int ws_plan_batch_host(ws_ctx* ctx, const ws_batch* in, ws_plan_result* results, uint8_t* arena,
                        uint64_t arena_cap, uint64_t* arena_used, void* stream) {
     cudaSetDevice(ctx->device);
-    void* dres = mapped_device_ptr(results);
-    void* dar = mapped_device_ptr(arena);
-    if (!dres || !dar || in->n_plans == 0) {  // pageable buffers: stage, plan, copy back
+    cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
+    const int P = in->n_plans;
+    int C = ctx->host_chunks;
+    C = std::max(1, std::min({C, kMaxHostChunks, P / 4096}));
+    if (C == 1 || !in->blob) {
         if (ws_stage_batch(ctx, in, stream)) return 1;
         if (ws_plan_staged(ctx, stream)) return 1;
         return ws_fetch_results(ctx, results, arena, arena_cap, arena_used, stream);
     }
-    // page-locked buffers: the kernels write headers and records straight to the
-    // host (PCIe/C2C writes overlap the planning), only the arena top comes back
-    cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
-    ctx->d_results = static_cast<ws_plan_result*>(dres);
-    ctx->d_arena = static_cast<uint8_t*>(dar);
-    ctx->d_cap = arena_cap;
-    int rc = ws_stage_batch(ctx, in, stream);
-    if (!rc) rc = ws_plan_staged(ctx, stream);
-    ctx->d_results = nullptr;
-    ctx->d_arena = nullptr;
-    if (rc) return rc;
-    unsigned long long top = 0;
-    CK(cudaMemcpyAsync(&top, ctx->counters.p, sizeof(top), cudaMemcpyDeviceToHost, st));
+    if (!ctx->blob.ensure(in->blob_bytes + 256) || !ctx->order.ensure(4ull * P) || !ctx->chunk_tops.ensure(8 * 64))
+        return fail(ctx, "cudaMalloc batch");
+    char* dblob = ctx->blob.as<char>();
+    ctx->dview = rebase(*in, in->blob, dblob);
+    ctx->caps = batch_caps(in->plans, P, false);
+    ctx->caps_hard = batch_caps(in->plans, P, true);
+    ctx->sim_cap = ws_sim_arena_bound(in);
+    ctx->sim_valid = false;
+    int pb[kMaxHostChunks + 1];
+    uint64_t abase[kMaxHostChunks + 1];
+    abase[0] = 0;
+    ctx->order_host.resize(P);
+    for (int c = 0; c <= C; ++c) pb[c] = static_cast<int>(static_cast<int64_t>(P) * c / C);
+    for (int c = 0; c < C; ++c) {
+        abase[c + 1] = abase[c] + wsi_arena_bound_plans(in->plans + pb[c], pb[c + 1] - pb[c]);
+        lpt_order(ctx, in->plans, pb[c], pb[c + 1]);
+        ctx->host_tops[c] = abase[c];
+    }
+    ctx->arena_cap = abase[C];
+    if (ctx->arena_cap > arena_cap) return fail(ctx, "ws_plan_batch_host: arena buffer too small");
+    FitOut fo;
+    if (prepare_plan(ctx, fo)) return 1;
+    auto* counters = ctx->counters.as<unsigned long long>();
+    auto* tops = ctx->chunk_tops.as<unsigned long long>();
+    cudaStream_t sh = ctx->stream2, sd = ctx->stream3;
+    cudaEvent_t* h2d = ctx->cev;               // [0, C)
+    cudaEvent_t* done = ctx->cev + kMaxHostChunks;  // [C, 2C)
+    CK(cudaEventRecord(ctx->ev[0], st));
+    CK(cudaStreamWaitEvent(sh, ctx->ev[0], 0));
+    CK(cudaMemcpyAsync(tops, ctx->host_tops, 8ull * C, cudaMemcpyHostToDevice, sh));
+    const ws_batch& h = *in;
+    auto rows = [&](const void* hp, size_t esz, int64_t lo, int64_t hi) -> cudaError_t {
+        if (!hp || hi <= lo) return cudaSuccess;
+        const size_t off = static_cast<const char*>(hp) - static_cast<const char*>(in->blob) + lo * esz;
+        return cudaMemcpyAsync(dblob + off, static_cast<const char*>(hp) + lo * esz, (hi - lo) * esz,
+                               cudaMemcpyHostToDevice, sh);
+    };
+    auto first = [](const int32_t* a, int64_t i, int64_t n, int64_t total) { return i < n ? a[i] : total; };
+    for (int c = 0; c < C; ++c) {  // H2D side
+        const int p0 = pb[c], p1 = pb[c + 1];
+        const int64_t m0 = h.plans[p0].mod_begin, m1 = p1 < P ? h.plans[p1].mod_begin : h.n_modules;
+        const int64_t t0 = h.plans[p0].task_begin, t1 = p1 < P ? h.plans[p1].task_begin : h.n_task_total;
+        const int64_t d0 = h.plans[p0].dev_begin, d1 = p1 < P ? h.plans[p1].dev_begin : h.n_devices;
+        const int64_t nm = h.n_modules, nt = h.n_task_total;
+        CK(rows(h.plans, sizeof(ws_plan_rec), p0, p1));
+        for (const int32_t* a : {h.mod_plan, h.mod_layers, h.mod_tp, h.mod_group, h.mod_alias, h.mod_name_off,
+                                 h.mod_name_len, h.mod_truth_off, h.mod_truth_n, h.mod_prof_off, h.mod_prof_n,
+                                 h.mod_bp_off, h.mod_bp_n, h.mod_pre_err})
+            CK(rows(a, 4, m0, m1));
+        for (const void* a : {static_cast<const void*>(h.mod_batch), static_cast<const void*>(h.mod_param),
+                              static_cast<const void*>(h.mod_act), static_cast<const void*>(h.mod_out),
+                              static_cast<const void*>(h.mod_w), static_cast<const void*>(h.mod_c)})
+            CK(rows(a, 8, m0, m1));
+        for (const int32_t* a : {h.task_tok_off, h.task_tok_n, h.task_rank}) CK(rows(a, 4, t0, t1));
+        CK(rows(h.tokens, 4, first(h.task_tok_off, t0, nt, h.n_tokens), first(h.task_tok_off, t1, nt, h.n_tokens)));
+        CK(rows(h.dev_island, 4, d0, d1));
+        CK(rows(h.truth, 40, first(h.mod_truth_off, m0, nm, h.n_pieces), first(h.mod_truth_off, m1, nm, h.n_pieces)));
+        const int64_t q0 = first(h.mod_prof_off, m0, nm, h.n_points), q1 = first(h.mod_prof_off, m1, nm, h.n_points);
+        CK(rows(h.prof_n, 4, q0, q1));
+        CK(rows(h.prof_t, 8, q0, q1));
+        CK(rows(h.bps, 4, first(h.mod_bp_off, m0, nm, h.n_bps), first(h.mod_bp_off, m1, nm, h.n_bps)));
+        CK(rows(h.names, 1, first(h.mod_name_off, m0, nm, h.n_name_bytes),
+                first(h.mod_name_off, m1, nm, h.n_name_bytes)));
+        CK(cudaMemcpyAsync(ctx->order.as<int32_t>() + p0, ctx->order_host.data() + p0, 4ull * (p1 - p0),
+                           cudaMemcpyHostToDevice, sh));
+        CK(cudaEventRecord(h2d[c], sh));
+    }
+    ctx->launches = 0;
+    CK(cudaMemsetAsync(counters, 0, 64, st));
+    const ws_batch& B = ctx->dview;
+    auto* rcount = reinterpret_cast<int32_t*>(counters + 2);
+    for (int c = 0; c < C; ++c) {  // compute side
+        const int p0 = pb[c], p1 = pb[c + 1];
+        const int m0 = in->plans[p0].mod_begin, m1 = p1 < P ? in->plans[p1].mod_begin : in->n_modules;
+        CK(cudaStreamWaitEvent(st, h2d[c], 0));
+        ctx->top_ptr = tops + c;
+        ctx->top_cap = abase[c + 1];
+        if (m1 > m0) {
+            k_fit<<<(m1 - m0 + 127) / 128, 128, 0, st>>>(B, fo, m0, m1);
+            ctx->launches++;
+        }
+        int rc = launch_pair(ctx, st, ctx->caps, fo, ctx->order.as<int32_t>() + p0, nullptr, p1 - p0, false,
+                             ctx->recs.as<char>(), ctx->flows.as<uint64_t>());
+        if (!rc) {
+            CK(cudaMemsetAsync(rcount, 0, 4, st));
+            k_soft_collect<<<(p1 - p0 + 255) / 256, 256, 0, st>>>(ctx->res_out(), p0, p1,
+                                                                   ctx->retry_ids.as<int32_t>(), rcount);
+            k_clamp_count<<<1, 1, 0, st>>>(rcount);
+            ctx->launches += 2;
+            rc = launch_pair(ctx, st, ctx->caps_hard, fo, ctx->retry_ids.as<int32_t>(), rcount, kRetryMax, true,
+                             ctx->recs_r.as<char>(), ctx->flows_r.as<uint64_t>());
+        }
+        ctx->top_ptr = nullptr;
+        if (rc) return 1;
+        CK(cudaMemcpyAsync(ctx->host_tops + kMaxHostChunks + c, tops + c, 8, cudaMemcpyDeviceToHost, st));
+        CK(cudaEventRecord(done[c], st));
+    }
+    CK(cudaEventRecord(ctx->ev[2], st));
+    uint64_t used = 0;
+    for (int c = 0; c < C; ++c) {  // D2H side, as each chunk completes
+        CK(cudaEventSynchronize(done[c]));
+        uint64_t top = ctx->host_tops[kMaxHostChunks + c];
+        top = std::min<uint64_t>(top, abase[c + 1]);
+        CK(cudaStreamWaitEvent(sd, done[c], 0));
+        CK(cudaMemcpyAsync(results + pb[c], ctx->results.as<ws_plan_result>() + pb[c],
+                           sizeof(ws_plan_result) * (pb[c + 1] - pb[c]), cudaMemcpyDeviceToHost, sd));
+        if (top > abase[c])
+            CK(cudaMemcpyAsync(arena + abase[c], ctx->arena.as<uint8_t>() + abase[c], top - abase[c],
+                               cudaMemcpyDeviceToHost, sd));
+        used = std::max<uint64_t>(used, top);
+    }
+    CK(cudaStreamSynchronize(sd));
+    CK(cudaStreamSynchronize(st));
+    // the device arena top for a later ws_fetch_results / ws_simulate_staged
+    ctx->host_tops[2 * kMaxHostChunks] = used;
+    CK(cudaMemcpyAsync(counters, ctx->host_tops + 2 * kMaxHostChunks, 8, cudaMemcpyHostToDevice, st));
     CK(cudaStreamSynchronize(st));
     float ms = 0;
-    if (cudaEventElapsedTime(&ms, ctx->ev[0], ctx->ev[1]) == cudaSuccess) ctx->kernel_ms[0] = ms;
-    if (cudaEventElapsedTime(&ms, ctx->ev[1], ctx->ev[3]) == cudaSuccess) ctx->kernel_ms[1] = ms;
-    if (cudaEventElapsedTime(&ms, ctx->ev[3], ctx->ev[2]) == cudaSuccess) ctx->kernel_ms[2] = ms;
-    *arena_used = top < arena_cap ? top : arena_cap;
+    ctx->kernel_ms[0] = ctx->kernel_ms[1] = 0;  // chunked: only the whole pipeline is timed
+    if (cudaEventElapsedTime(&ms, ctx->ev[0], ctx->ev[2]) == cudaSuccess) ctx->kernel_ms[2] = ms;
+    ctx->records_on_device = true;
+    *arena_used = used;
     return 0;
 }
 

@@ -287,13 +287,16 @@ std::string plan_text_or_error(const Problem& prob, const ws_plan_result& r, con
 // workload families (metaops, 2 tuples and 2 curve pieces per MetaOp, dense
 // waves/flows); a plan exceeding its share is reported WS_E_ARENA_OVERFLOW and
 // re-planned alone by the host wrapper with ws_arena_bound of that one plan.
-extern "C" uint64_t ws_arena_bound(const ws_batch* in) {
+// (internal) the same bound summed over plans[0, n): a pipelined chunk's share
+extern "C" uint64_t wsi_arena_bound_plans(const ws_plan_rec* plans, int n) {
     uint64_t total = 0;
-    for (int p = 0; p < in->n_plans; ++p) {
-        const uint64_t M = static_cast<uint64_t>(in->plans[p].n_mod);
+    for (int p = 0; p < n; ++p) {
+        const uint64_t M = static_cast<uint64_t>(plans[p].n_mod);
         total += 64 + sizeof(ws_out_metaop) * M + sizeof(ws_out_level) * M + sizeof(ws_out_piece) * 4 * M +
                  sizeof(ws_out_edge) * M * M + sizeof(ws_out_wave) * 4 * M + sizeof(ws_out_entry) * 8 * M +
                  sizeof(ws_out_flow) * 16 * M;
     }
-    return total + 4096;
+    return total;
 }
+
+extern "C" uint64_t ws_arena_bound(const ws_batch* in) { return wsi_arena_bound_plans(in->plans, in->n_plans) + 4096; }
