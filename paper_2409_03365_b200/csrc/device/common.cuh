@@ -8,7 +8,13 @@ namespace wsdev {
 
 constexpr unsigned kFull = 0xffffffffu;
 
-__device__ __forceinline__ int popc64(uint64_t m) { return __popcll(m); }
+__host__ __device__ __forceinline__ int popc64(uint64_t m) {
+#ifdef __CUDA_ARCH__
+    return __popcll(m);
+#else
+    return __builtin_popcountll(m);
+#endif
+}
 // index of the lowest set bit; m != 0 (one BREV+FLO on the nonzero half: cheaper than __ffsll)
 __device__ __forceinline__ int low_bit(uint64_t m) {
     const unsigned lo = static_cast<unsigned>(m);
@@ -67,6 +73,30 @@ __host__ __device__ __forceinline__ bool dec_less(int a, int b) {
     int p = 1;
     for (int i = da < db ? db - da : da - db; i; --i) p *= 10;
     return da < db ? a <= b / p : a / p < b;
+}
+
+// shard_moves' island-match count (placement.hpp:88-97) in closed form for
+// islands that are contiguous device ranges.  Unit i (< M) pairs A[i] with
+// B[i mod P], A and B the sorted device lists as masks, |A| = M >= |B| = P
+// (exactly one of the reference's two lists cycles).  In sorted order the
+// members of island a occupy positions [sa, sa+ca) of A and, in every block q
+// of B's cycle, [qP+sb, qP+sb+cb): the matches are the overlaps of those runs.
+// lowm[a]: devices below island a's first device.
+__host__ __device__ __forceinline__ int island_matches(uint64_t A, uint64_t B, int M, int P, const uint64_t* islm,
+                                                       const uint64_t* lowm, int n_isl) {
+    int same = 0;
+    for (int a = 0; a < n_isl; ++a) {
+        const int ca = popc64(A & islm[a]), cb = popc64(B & islm[a]);
+        if (!ca || !cb) continue;
+        const int sa = popc64(A & lowm[a]), sb = popc64(B & lowm[a]);
+        int q = sa > sb + cb ? (sa - sb - cb) / P : 0;
+        for (int off = q * P + sb; off < sa + ca && off < M; off += P) {
+            const int lo = sa > off ? sa : off;
+            const int hi = (sa + ca) < (off + cb) ? (sa + ca) : (off + cb);
+            if (hi > lo) same += hi - lo;
+        }
+    }
+    return same;
 }
 
 // ---------------------------------------------------------------------------

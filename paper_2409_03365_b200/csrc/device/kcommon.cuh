@@ -161,7 +161,10 @@ struct InvPre {
 
 // shard_moves (placement.hpp:74-103) on device-index bitmasks; isl = island id per device.
 // Unit i pairs sources[i % S] with targets[i % T] (both sorted by device id).
+// With contiguous islands (islm/lowm given) the island matches are counted in
+// closed form (island_matches), otherwise unit by unit.
 __device__ __forceinline__ void shard_moves(uint64_t from, uint64_t to, uint64_t full, const int* isl,
+                                            const uint64_t* islm, const uint64_t* lowm, int n_isl,
                                             uint64_t& intra, uint64_t& inter) {
     intra = inter = 0;
     if (!from || !to) return;
@@ -176,15 +179,21 @@ __device__ __forceinline__ void shard_moves(uint64_t from, uint64_t to, uint64_t
     const double unit_bytes = static_cast<double>(full) / static_cast<double>(units);
     const uint64_t bytes = static_cast<uint64_t>(llround(unit_bytes));
     int same = 0;
-    uint64_t rs = src, rt = dst;
-    for (int i = 0; i < moving; ++i) {
-        const int s = low_bit(rs);
-        rs &= rs - 1;
-        if (!rs) rs = src;
-        const int t = low_bit(rt);
-        rt &= rt - 1;
-        if (!rt) rt = dst;
-        same += isl[s] == isl[t];
+    if (islm) {
+        const int S = popc64(src);  // one of S, T equals moving; the other list cycles
+        same = S == moving ? island_matches(src, dst, moving, popc64(dst), islm, lowm, n_isl)
+                           : island_matches(dst, src, moving, S, islm, lowm, n_isl);
+    } else {
+        uint64_t rs = src, rt = dst;
+        for (int i = 0; i < moving; ++i) {
+            const int s = low_bit(rs);
+            rs &= rs - 1;
+            if (!rs) rs = src;
+            const int t = low_bit(rt);
+            rt &= rt - 1;
+            if (!rt) rt = dst;
+            same += isl[s] == isl[t];
+        }
     }
     intra = static_cast<uint64_t>(same) * bytes;
     inter = static_cast<uint64_t>(moving - same) * bytes;

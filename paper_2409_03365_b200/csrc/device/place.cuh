@@ -24,6 +24,7 @@ struct PlSmLayout {
     int mem;                                                      // [N] f64
     int isl;                                                      // [N] i32
     int islmask;                                                  // [IS] u64
+    int isllow;                                                   // [IS] u64 devices below island i
     int nwin;                                                     // [IS] i32
     int chg;                                                      // [G] u64
     int fin_src, fin_bytes;                                       // [M+1]
@@ -69,6 +70,7 @@ __host__ __device__ inline PlSmLayout make_pl_layout(const PlaceCaps& c) {
     L.mem = take(8 * N);
     L.isl = take(4 * N);
     L.islmask = take(8 * c.IS);
+    L.isllow = take(8 * c.IS);
     L.nwin = take(4 * (c.IS + W + 1));  // island window counts, then flows-per-wave marks
     L.chg = take(8 * c.G);
     L.fin_src = take(4 * (M + 1));
@@ -155,6 +157,8 @@ __device__ int p_wave(PCtx& C, int w, int variant) {
     uint64_t* chg = C.at<uint64_t>(L.chg);
     const int* isl = C.at<int>(L.isl);
     const uint64_t* islmask = C.at<uint64_t>(L.islmask);
+    const uint64_t* cislm = C.contig ? islmask : nullptr;  // closed-form shard_moves
+    const uint64_t* isllow = C.at<uint64_t>(L.isllow);
     int* nwin = C.at<int>(L.nwin);
     int* fin_src = C.at<int>(L.fin_src);
     uint64_t* fin_bytes = C.at<uint64_t>(L.fin_bytes);
@@ -276,7 +280,7 @@ __device__ int p_wave(PCtx& C, int w, int variant) {
             s.intra = 0.0;
             for (int f = 0; f < nfin; ++f) {
                 uint64_t a, b;
-                shard_moves(e_mask[fin_src[f]], devs, fin_bytes[f], isl, a, b);
+                shard_moves(e_mask[fin_src[f]], devs, fin_bytes[f], isl, cislm, isllow, C.n_isl, a, b);
                 s.inter += static_cast<double>(b);
                 s.intra += static_cast<double>(a);
             }
@@ -384,7 +388,7 @@ __device__ int p_wave(PCtx& C, int w, int variant) {
         for (int f = 0; f < nfin; ++f) {
             uint64_t a, b;
             const int src = fin_src[f];
-            shard_moves(e_mask[src], chosen.devs, fin_bytes[f], isl, a, b);
+            shard_moves(e_mask[src], chosen.devs, fin_bytes[f], isl, cislm, isllow, C.n_isl, a, b);
             const int need = (a + b == 0) ? 1 : (a > 0) + (b > 0);
             if (C.nF + need > C.Fcap) {
                 if (lane == 0) set_err(C.ctl, WS_E_LIMIT_FLOWS);
@@ -733,6 +737,7 @@ __global__ void __launch_bounds__(32 * kPlaceWarps, WS_PLACE_MINB) k_place(Place
             const uint64_t m = islmask[i];
             const uint64_t run = m ? m >> low_bit(m) : 0;
             if (!m || (run & (run + 1))) contig = 0;
+            C.at<uint64_t>(L.isllow)[i] = m ? (1ull << low_bit(m)) - 1ull : 0;
         }
         ctl->i0 = contig;
     }

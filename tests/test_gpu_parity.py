@@ -136,3 +136,22 @@ def test_gpu_kernel_timing_reported(planner):
     planner.plan(ps)
     fit_ms, sched_ms, place_ms = planner.kernel_ms()
     assert fit_ms > 0 and sched_ms > 0 and place_ms > 0
+
+
+def test_gpu_pipelined_host_call_matches(sweep_hashes, monkeypatch):
+    """ws_plan_batch_host as a chunked H2D / compute / D2H pipeline
+    ($WSGPU_HOST_CHUNKS) gives the same plans as the one-shot call."""
+    import paper_2409_03365_b200 as ws
+    monkeypatch.setenv("WSGPU_HOST_CHUNKS", "3")
+    pl = ws.Planner(0)
+    n = 30000
+    ps = ws.ProblemSet()
+    ps.add_sweep(0, n)
+    ps.encode(pinned=True)
+    res = pl.plan(ps)
+    got = [hashlib.sha1(ps.text(i, res.results, res.arena).encode()).hexdigest()[:16] for i in range(n)]
+    assert got == sweep_hashes[:n]
+    # records stay on the device: evaluation right after the host call
+    pl.simulate_staged()
+    sims = pl.fetch_sim(ps)
+    assert all(sims.results[i].valid for i in range(n) if res.results[i].status == 0)
