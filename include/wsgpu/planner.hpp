@@ -318,6 +318,9 @@ struct PlannerOptions {
     double grad_opt_multiplier = 3.0;
     double synth_noise = 0.0;
     std::uint64_t synth_seed = 0;
+    // Not a reference PlannerOptions field: the plan_for_strategy selector
+    // (cli.hpp:163-171) -- ws_strategy, 0 = wavefront (plan_workload).
+    int strategy = 0;
 };
 
 struct PlannerResult {

@@ -101,7 +101,16 @@ typedef struct ws_plan_rec {
     double drop_floor;           /* AllocatorOptions::drop_floor                        */
     double grad_mult;            /* PlannerOptions::grad_opt_multiplier                 */
     double intra_bw, inter_bw;   /* ClusterTopology bandwidths (simulator, flow_duration) */
+    int32_t strategy;            /* ws_strategy: plan_for_strategy selector (cli.hpp:163-171) */
+    int32_t pad_s;
 } ws_plan_rec;
+
+/* Planning strategies (cli.hpp:238-241): the wavefront planner (plan_workload)
+ * and the baseline planners of baselines.hpp. */
+enum ws_strategy {
+    WS_STRATEGY_WAVEFRONT = 0,            /* planner.hpp:156-212                  */
+    WS_STRATEGY_DECOUPLED_SEQUENTIAL = 1  /* plan_decoupled_sequential, baselines.hpp:104-131 */
+};
 
 /* Structure-of-arrays batch.  All pointers address the same memory space
  * (host for the oracle and the *_host entry points, device inside the ctx). */

@@ -28,6 +28,8 @@ typedef struct ws_options {
     double grad_mult;   /* grad_opt_multiplier = 3             */
     double synth_noise; /* = 0                                 */
     uint64_t synth_seed;/* = 0                                 */
+    int32_t strategy;   /* ws_strategy (plan_for_strategy selector) = 0 wavefront */
+    int32_t pad;
 } ws_options;
 
 void wsx_default_options(ws_options* o);

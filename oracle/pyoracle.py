@@ -55,7 +55,8 @@ def simulate_batch(pset, res, **sim_opts):
 class RefOpts(C.Structure):
     _fields_ = [("eps", C.c_double), ("max_iters", C.c_int), ("drop_floor", C.c_double),
                 ("sequential", C.c_int), ("bt_depth", C.c_int), ("bt_branching", C.c_int),
-                ("grad_mult", C.c_double), ("synth_noise", C.c_double), ("synth_seed", C.c_ulonglong)]
+                ("grad_mult", C.c_double), ("synth_noise", C.c_double), ("synth_seed", C.c_ulonglong),
+                ("strategy", C.c_int)]
 
 
 class RefSimOpts(C.Structure):
@@ -129,8 +130,10 @@ def _s(ptr) -> str:
 
 
 def ref_options(**kw) -> RefOpts:
-    o = RefOpts(1e-7, 200, 0.0, 0, 2, 3, 3.0, 0.0, 0)
+    o = RefOpts(1e-7, 200, 0.0, 0, 2, 3, 3.0, 0.0, 0, 0)
     for k, v in kw.items():
+        if k == "strategy" and isinstance(v, str):
+            v = {"wavefront": 0, "decoupled-sequential": 1}[v]
         setattr(o, k, v)
     return o
 

@@ -11,6 +11,7 @@
 #include <thread>
 #include <vector>
 
+#include "wavesched/baselines.hpp"
 #include "wavesched/planner.hpp"
 #include "wavesched/scenarios.hpp"
 #include "wavesched/simulate.hpp"
@@ -35,6 +36,7 @@ typedef struct wsref_opts {
     double grad_mult;
     double synth_noise;
     unsigned long long synth_seed;
+    int strategy;  // 0 wavefront, 1 decoupled-sequential (plan_for_strategy, cli.hpp:163-171)
 } wsref_opts;
 typedef struct wsref_sim_opts {
     double backward_ratio;
@@ -66,10 +68,18 @@ PlannerOptions to_opts(const wsref_opts* o) {
     return opt;
 }
 
+// plan_for_strategy (cli.hpp:163-171) for the strategies built on the device
+ExecutionPlan plan_strategy(const WorkloadSpec& spec, const ClusterTopology& topo, const PlannerOptions& opt,
+                            int strategy) {
+    if (strategy == 1) return plan_decoupled_sequential(prepare_planning_base(spec, topo, opt), topo, opt);
+    return plan_workload(spec, topo, opt).plan;
+}
+
 // Reference outcome as text: the plan file, or "error <Class>: <what>".
-std::string outcome(const WorkloadSpec& spec, const ClusterTopology& topo, const PlannerOptions& opt) {
+std::string outcome(const WorkloadSpec& spec, const ClusterTopology& topo, const PlannerOptions& opt,
+                    int strategy = 0) {
     try {
-        return write_plan(plan_workload(spec, topo, opt).plan);
+        return write_plan(plan_strategy(spec, topo, opt, strategy));
     } catch (const CyclicWorkload& e) {
         return std::string("error CyclicWorkload: ") + e.what() + "\n";
     } catch (const UnknownModule& e) {
@@ -146,7 +156,7 @@ char* wsref_plan_text(const char* workload, const char* topology, const wsref_op
     try {
         WorkloadSpec spec = parse_workload(workload);
         ClusterTopology topo = parse_topology(topology);
-        return dup(outcome(spec, topo, to_opts(o)));
+        return dup(outcome(spec, topo, to_opts(o), o ? o->strategy : 0));
     } catch (const Error& e) {
         return dup(std::string("error Parse: ") + e.what() + "\n");
     }
@@ -237,10 +247,11 @@ char* wsref_sim_text(const char* workload, const char* topology, const wsref_opt
     try {
         WorkloadSpec spec = parse_workload(workload);
         ClusterTopology topo = parse_topology(topology);
+        const int strategy = o ? o->strategy : 0;
         try {
-            return dup(sim_text(plan_workload(spec, topo, to_opts(o)).plan, so));
+            return dup(sim_text(plan_strategy(spec, topo, to_opts(o), strategy), so));
         } catch (const Error&) {
-            return dup(outcome(spec, topo, to_opts(o)));
+            return dup(outcome(spec, topo, to_opts(o), strategy));
         }
     } catch (const Error& e) {
         return dup(std::string("error Parse: ") + e.what() + "\n");

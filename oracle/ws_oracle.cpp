@@ -249,7 +249,10 @@ public:
         if (M > WS_MAX_MODULES) throw Fail{WS_E_LIMIT_MODULES};
         build_graph();          // graph.hpp:97-147 + topo order/contract/levels :66-226
         fit_modules();          // planner.hpp:66-94
-        allocate_and_schedule(out);
+        if (R.strategy == WS_STRATEGY_DECOUPLED_SEQUENTIAL)
+            decoupled();        // baselines.hpp:104-131
+        else
+            allocate_and_schedule(out);
         place(out);
         fill(out);
     }
@@ -467,6 +470,57 @@ private:
             level_nwaves.push_back(static_cast<int>(waves.size() - w0));
         }
         end_time = offset;
+    }
+
+    // plan_decoupled_sequential (baselines.hpp:104-131): MetaOps in
+    // detail::topo_order (ready set ordered by id string, graph.hpp:67-90),
+    // each alone on valid_allocations(m).back() for m.length * eval(n).
+    void decoupled() {
+        std::vector<int> indeg(K, 0);
+        std::vector<std::vector<int>> succ(K);
+        for (const auto& [a, b] : edges) {
+            succ[a].push_back(b);
+            ++indeg[b];
+        }
+        std::set<std::string> ready;
+        for (int k = 0; k < K; ++k)
+            if (!indeg[k]) ready.insert("m" + std::to_string(k));
+        upper_n.assign(K, 0);
+        upper_l.assign(K, 0);
+        lower_n.assign(K, 0);
+        lower_l.assign(K, 0);
+        valid.assign(K, 0);
+        double now = 0.0;
+        while (!ready.empty()) {
+            const int k = std::stoi(ready.begin()->substr(1));
+            ready.erase(ready.begin());
+            const int g = mg(mod_of[k]);
+            const int tp = B.mod_tp[g];
+            if (tp > N) throw Fail{WS_E_TP_EXCEEDS, k, tp};
+            int n = 0;
+            for (int x = 1; x <= N; ++x)
+                if (x % tp == 0 && B.mod_batch[g] % (x / tp) == 0) n = x;
+            const int L = layers(mod_of[k]);
+            const double span = L * curve(k).eval(n);
+            WaveRec wv;
+            wv.level = level[k];
+            wv.start = now;
+            wv.dur = span;
+            wv.entries.push_back(static_cast<int>(entries.size()));
+            EntryRec e;
+            e.k = k;
+            e.n = n;
+            e.layers = L;
+            e.span = span;
+            entries.push_back(e);
+            waves.push_back(wv);
+            upper_n[k] = n;
+            upper_l[k] = L;
+            now += span;
+            for (int q : succ[k])
+                if (--indeg[q] == 0) ready.insert("m" + std::to_string(q));
+        }
+        end_time = now;
     }
 
     std::vector<int> valid_list(int k) const {

@@ -102,7 +102,8 @@ class Options(C.Structure):
     """PlannerOptions (planner.hpp:21-27) as ws_options (wsx.h)."""
     _fields_ = [("eps", C.c_double), ("max_iters", C.c_int32), ("sequential", C.c_int32),
                 ("drop_floor", C.c_double), ("bt_depth", C.c_int32), ("bt_branching", C.c_int32),
-                ("grad_mult", C.c_double), ("synth_noise", C.c_double), ("synth_seed", C.c_uint64)]
+                ("grad_mult", C.c_double), ("synth_noise", C.c_double), ("synth_seed", C.c_uint64),
+                ("strategy", C.c_int32), ("pad", C.c_int32)]
 
 
 class PlanResult(C.Structure):
@@ -201,8 +202,16 @@ def make_options(**kw) -> Options:
     for k, v in kw.items():
         if not hasattr(o, k):
             raise TypeError(f"unknown planner option {k!r}")
+        if k == "strategy" and isinstance(v, str):
+            if v not in STRATEGIES:
+                raise ParseError(f"unknown strategy '{v}'")
+            v = STRATEGIES[v]
         setattr(o, k, v)
     return o
+
+
+# plan_for_strategy selectors (cli.hpp:163-171) built on the device
+STRATEGIES = {"wavefront": 0, "decoupled-sequential": 1}
 
 
 class ProblemSet:

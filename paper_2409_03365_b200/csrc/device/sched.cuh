@@ -407,13 +407,15 @@ __device__ bool s_fit_status(SCtx& C) {
 }
 
 // (3a) valid allocation sets n = tp*r with r | B (allocation.hpp:51-63)
-__device__ bool s_valid(SCtx& C) {
+// check_tp: the planner's NoValidAllocation in id order; the baselines check
+// each MetaOp when they reach it (an over-wide tp leaves an empty set).
+__device__ bool s_valid(SCtx& C, bool check_tp) {
     const ws_batch& B = *C.B;
     const int K = C.K, N = C.N, lane = C.lane;
     const int* gm_of = C.at<int>(C.L->gm_of);
     const int* by_rank = C.at<int>(C.L->by_rank);
     uint64_t* valid = C.at<uint64_t>(C.L->valid);
-    for (int base = 0; base < K; base += 32) {  // tp > N in id order (planner.hpp:168-171)
+    for (int base = 0; base < K && check_tp; base += 32) {  // tp > N in id order (planner.hpp:168-171)
         const int r = base + lane;
         const bool bad = r < K && B.mod_tp[gm_of[by_rank[r]]] > N;
         const unsigned b = __ballot_sync(kFull, bad);
@@ -1118,6 +1120,95 @@ __device__ int fast_wave(SCtx& C, SchedView& S) {
     return best_cnt;
 }
 
+// plan_decoupled_sequential (baselines.hpp:104-131): every MetaOp alone on
+// its largest valid allocation, one wave each, in lexicographic topological
+// order (detail::topo_order, graph.hpp:67-90); lane 0, K <= 64 steps.
+__device__ bool s_decoupled(SCtx& C, char* rec, const RecLayout& RL, int& nW, int& nE, double& end_time, int W_CAP,
+                            int E_CAP) {
+    const int K = C.K, lane = C.lane;
+    const int* by_rank = C.at<int>(C.L->by_rank);
+    const int* idrank = C.at<int>(C.L->idrank);
+    const int* gm_of = C.at<int>(C.L->gm_of);
+    const int* nmax_of = C.at<int>(C.L->nmax_of);
+    const int* Lk = C.at<int>(C.L->Lk);
+    const int* level = C.at<int>(C.L->level);
+    const uint64_t* pred_r = C.at<uint64_t>(C.L->pred_r);
+    const uint64_t* succ_r = C.at<uint64_t>(C.L->succ_r);
+    const uint64_t* valid = C.at<uint64_t>(C.L->valid);
+    int* indeg = C.at<int>(C.L->absorb);
+    int* up_n = C.at<int>(C.L->up_n);
+    int* up_l = C.at<int>(C.L->up_l);
+    int* lo_n = C.at<int>(C.L->lo_n);
+    int* lo_l = C.at<int>(C.L->lo_l);
+    if (lane == 0) {
+        int* w_level = reinterpret_cast<int*>(rec + RL.w_level);
+        int* w_eb = reinterpret_cast<int*>(rec + RL.w_eb);
+        int* w_ec = reinterpret_cast<int*>(rec + RL.w_ec);
+        double* w_start = reinterpret_cast<double*>(rec + RL.w_start);
+        double* w_dur = reinterpret_cast<double*>(rec + RL.w_dur);
+        int* e_k = reinterpret_cast<int*>(rec + RL.e_k);
+        int* e_n = reinterpret_cast<int*>(rec + RL.e_n);
+        int* e_l = reinterpret_cast<int*>(rec + RL.e_l);
+        double* e_span = reinterpret_cast<double*>(rec + RL.e_span);
+        uint64_t ready = 0;
+        for (int k = 0; k < K; ++k) {
+            indeg[k] = popc64(pred_r[k]);
+            if (!indeg[k]) ready |= 1ull << idrank[k];
+            up_n[k] = up_l[k] = lo_n[k] = lo_l[k] = 0;
+        }
+        double now = 0.0;
+        while (ready) {
+            const int r = low_bit(ready);
+            ready &= ready - 1;
+            const int k = by_rank[r];
+            const int gm = gm_of[k];
+            const int tp = C.B->mod_tp[gm];
+            if (tp > C.N) {  // valid_allocations (allocation.hpp:51-54)
+                set_err(C.ctl, WS_E_TP_EXCEEDS, k, tp);
+                break;
+            }
+            const int n = 64 - __clzll(static_cast<long long>(valid[k]));  // valid.back()
+            if (n > nmax_of[k]) {  // ScalingCurve::eval OutOfRange (scaling.hpp:66-68)
+                C.ctl->err = WS_E_EVAL_RANGE;
+                C.ctl->x = n;
+                C.ctl->y = nmax_of[k];
+                break;
+            }
+            if (nW + 1 > W_CAP || nE + 1 > E_CAP) {
+                set_err(C.ctl, nW + 1 > W_CAP ? WS_E_LIMIT_WAVES : WS_E_LIMIT_ENTRIES);
+                break;
+            }
+            const double span = Lk[k] * t_at(*C.F, gm, n);
+            w_level[nW] = level[k];
+            w_eb[nW] = nE;
+            w_ec[nW] = 1;
+            w_start[nW] = now;
+            w_dur[nW] = span;
+            e_k[nE] = k;
+            e_n[nE] = n;
+            e_l[nE] = Lk[k];
+            e_span[nE] = span;
+            up_n[k] = n;
+            up_l[k] = Lk[k];
+            ++nW;
+            ++nE;
+            now += span;
+            for (uint64_t sr = succ_r[k]; sr; sr &= sr - 1) {
+                const int q = by_rank[low_bit(sr)];
+                if (--indeg[q] == 0) ready |= 1ull << idrank[q];
+            }
+        }
+        end_time = now;
+        C.ctl->i2 = nW;
+        C.ctl->i3 = nE;
+    }
+    __syncwarp();
+    nW = C.ctl->i2;
+    nE = C.ctl->i3;
+    end_time = __shfl_sync(kFull, end_time, 0);
+    return C.ctl->err == 0;
+}
+
 // (4a) schedule_level + merge_levels offsets; appends waves/entries to the record
 __device__ bool s_schedule_level(SCtx& C, char* rec, const RecLayout& RL, int lvl, int& nW, int& nE,
                                  double offset, double& level_end, int W_CAP, int E_CAP) {
@@ -1306,11 +1397,14 @@ __global__ void __launch_bounds__(32 * kSchedWarps) k_sched(SchedArgs A) {
     if (ok) ok = s_graph(C);
     WS_PH_STOP(tg, 10);
     if (ok) ok = s_fit_status(C);
-    if (ok) ok = s_valid(C);
+    const bool decoupled = R.strategy == WS_STRATEGY_DECOUPLED_SEQUENTIAL;
+    if (ok) ok = s_valid(C, !decoupled);
     WS_PH_STOP(tg, 11);
     int n_levels = 0, nW = 0, nE = 0;
     double lower_bound = 0.0, offset = 0.0;
-    if (ok) {
+    if (ok && decoupled) {
+        ok = s_decoupled(C, rec, A.RL, nW, nE, offset, A.caps.W, A.caps.E);
+    } else if (ok) {
         n_levels = ctl->i1;
         double* cstar = reinterpret_cast<double*>(rec + A.RL.cstar);
         int* lfw = reinterpret_cast<int*>(rec + A.RL.lvl_fw);

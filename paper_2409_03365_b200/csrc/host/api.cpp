@@ -25,6 +25,7 @@ PlannerOptions from_c(const ws_options* o) {
     p.grad_opt_multiplier = o->grad_mult;
     p.synth_noise = o->synth_noise;
     p.synth_seed = o->synth_seed;
+    p.strategy = o->strategy;
     return p;
 }
 
@@ -128,6 +129,8 @@ void wsx_default_options(ws_options* o) {
     o->grad_mult = p.grad_opt_multiplier;
     o->synth_noise = p.synth_noise;
     o->synth_seed = p.synth_seed;
+    o->strategy = p.strategy;
+    o->pad = 0;
 }
 
 wsx_set* wsx_set_new(void) { return new wsx_set(); }

@@ -174,7 +174,9 @@ PlannerResult decode_result(const Problem& prob, const ws_plan_result& r, const 
         res.meta.metaops.emplace(m.id, std::move(m));
     }
     for (int e = 0; e < r.n_edges; ++e) res.meta.edges.insert({mid(s.ed[e].from), mid(s.ed[e].to)});
-    res.meta.levels.assign(r.n_levels, {});
+    int n_meta_levels = r.n_levels;  // the baselines carry MetaOp levels but no level plans
+    for (const auto& [id, m] : res.meta.metaops) n_meta_levels = std::max(n_meta_levels, m.level + 1);
+    res.meta.levels.assign(n_meta_levels, {});
     for (const auto& [id, m] : res.meta.metaops) res.meta.levels[m.level].push_back(id);
 
     if (build_graph) {
@@ -228,7 +230,7 @@ PlannerResult decode_result(const Problem& prob, const ws_plan_result& r, const 
     res.lower_bound = r.lower_bound;
     res.predicted_makespan = r.end_time;
 
-    plan.strategy = "wavefront";
+    plan.strategy = prob.opt.strategy == WS_STRATEGY_DECOUPLED_SEQUENTIAL ? "decoupled-sequential" : "wavefront";
     plan.topo = *prob.topo;
     for (const auto& [id, m] : res.meta.metaops) {  // build_entities (planner.hpp:99-122)
         const ModuleDecl& md = spec.module(m.kind);

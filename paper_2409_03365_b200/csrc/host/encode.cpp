@@ -360,6 +360,7 @@ EncodedBatch encode_batch(const std::vector<Problem>& problems, bool pinned) {
         r.grad_mult = pr.opt.grad_opt_multiplier;
         r.intra_bw = pr.topo ? pr.topo->intra_bw : 1.0;
         r.inter_bw = pr.topo ? pr.topo->inter_bw : 1.0;
+        r.strategy = pr.opt.strategy;
         if (!s.ok) continue;
         for (std::size_t m = 0; m < s.mods.size(); ++m, ++im) {
             const ModuleDecl& md = *s.mods[m];

@@ -64,3 +64,20 @@ def sim_groups(cases):
     for c in cases:
         groups.setdefault(tuple(sorted(c["sim"].items())), []).append(c)
     return [(dict(k), v) for k, v in groups.items()]
+
+
+@pytest.fixture(scope="session")
+def baseline_cases():
+    with gzip.open(GOLDEN / "baseline_cases.json.gz", "rt") as f:
+        return json.load(f)
+
+
+@pytest.fixture(scope="session")
+def baseline_sweep_hashes():
+    """{strategy: [sha1[:16] of the reference plan text of sweep mixture i]}"""
+    out = {}
+    with gzip.open(GOLDEN / "baseline_sweep_hashes.txt.gz", "rt") as f:
+        for line in f:
+            name, *hashes = line.split()
+            out[name] = hashes
+    return out

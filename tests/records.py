@@ -11,6 +11,7 @@ WAVE = np.dtype([("start", "<f8"), ("duration", "<f8"), ("level", "<i4"), ("entr
                  ("n_entries", "<i4"), ("pad", "<i4")])
 FLOW = np.dtype([("volume", "<u8"), ("from_wave", "<i4"), ("from_metaop", "<i4"), ("to_wave", "<i4"),
                  ("to_metaop", "<i4"), ("mode", "<i4"), ("pad", "<i4")])
+PLAN_REC_BYTES = 104  # sizeof(ws_plan_rec); mem_capacity at byte 48
 SIZES = {"metaop": 40, "level": 16, "piece": 40, "edge": 8, "wave": 32, "entry": 32, "flow": 32}
 
 
@@ -105,7 +106,7 @@ def set_mem_capacity(pset, i: int, cap: int) -> None:
     import ctypes as C
     batch = pset.batch
     plans = C.c_void_p.from_address(batch + 56).value  # ws_batch.plans
-    C.c_uint64.from_address(plans + 96 * i + 48).value = cap  # sizeof(ws_plan_rec) = 96
+    C.c_uint64.from_address(plans + PLAN_REC_BYTES * i + 48).value = cap
 
 
 def build_sim_set(cases):
