@@ -310,6 +310,8 @@ struct ExecutionPlan {
 };
 
 std::string write_plan(const ExecutionPlan& plan);
+// parse_plan (plan_io.hpp:112-255): a plan file of any strategy
+ExecutionPlan parse_plan(const std::string& text);
 
 // ---- planner API (planner.hpp:21-38,156) ------------------------------------------------------
 struct PlannerOptions {
@@ -373,6 +375,9 @@ std::string plan_text_or_error(const Problem& prob, const ws_plan_result& res, c
 // evaluated plan, or the plan's error text; see csrc/host/sim_text.cpp.
 std::string sim_text(const Problem& prob, const ws_plan_result& res, const std::uint8_t* plan_arena,
                      const ws_sim_result& sim, const std::uint8_t* sim_arena);
+// The same for a record with explicit entity names (index -> id), e.g. a parsed plan file.
+std::string sim_text_named(const ClusterTopology& topo, const ws_plan_result& res, const ws_sim_result& sim,
+                           const std::uint8_t* sim_arena, const std::vector<std::string>& names);
 [[noreturn]] void throw_result_error(const Problem& prob, const ws_plan_result& res);
 
 // Deterministic scenario generator (scenarios.hpp restated): the measurement

@@ -162,6 +162,9 @@ typedef struct ws_batch {
     const double* prof_t;         /* [n_points]                                    */
     const int32_t* bps;           /* [n_bps]                                       */
     const uint8_t* names;         /* [n_name_bytes]                                */
+    /* Optional (plan evaluation of parsed plan files, NULL = 1.0 everywhere):
+     * PlanEntity::batch_fraction per module row (plan_io.hpp:36). */
+    const double* mod_frac;       /* [n_modules]                                   */
 } ws_batch;
 
 /* ---- per-plan result header ------------------------------------------------ */

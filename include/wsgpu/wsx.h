@@ -62,6 +62,24 @@ void wsx_free_str(char* p);
 void wsx_algorithmic_bytes(const wsx_set* s, const ws_plan_result* results, const uint8_t* arena,
                            uint64_t* in_bytes, uint64_t* out_bytes);
 
+/* Plan files of any strategy (parse_plan, plan_io.hpp:112-255) as evaluator
+ * input: each plan becomes a batch row + a planned record (ws_abi.h layout)
+ * that ws_simulate_batch_host evaluates on the device. */
+typedef struct wsx_plans wsx_plans;
+wsx_plans* wsx_plans_new(void);
+void wsx_plans_free(wsx_plans* p);
+int32_t wsx_plans_size(const wsx_plans* p);
+/* Returns the plan index, or -1 with the ParseError text in wsx_plans_error. */
+int32_t wsx_plans_add_text(wsx_plans* p, const char* plan_text);
+const char* wsx_plans_error(const wsx_plans* p);
+/* Encodes every plan; returns the batch (NULL on an unsupported plan, see
+ * wsx_plans_error) and the host records to pass to ws_simulate_batch_host. */
+const ws_batch* wsx_plans_encode(wsx_plans* p, int32_t pinned, const ws_plan_result** results,
+                                 const uint8_t** arena, uint64_t* arena_bytes);
+/* write_plan text of parsed plan i (round trip); canonical evaluation text. */
+char* wsx_plans_write(const wsx_plans* p, int32_t i);
+char* wsx_plans_sim_text(const wsx_plans* p, int32_t i, const ws_sim_result* sims, const uint8_t* sim_arena);
+
 /* Page-locked host buffers for results/arena (cudaMallocHost; plain malloc
  * when no CUDA device is present).  Not zero-initialized. */
 void* wsx_host_alloc(uint64_t bytes);

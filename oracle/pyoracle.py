@@ -52,6 +52,17 @@ def simulate_batch(pset, res, **sim_opts):
     return out
 
 
+def simulate_planset(plans, **sim_opts):
+    """Oracle evaluation of a PlanSet (parsed plan files); returns SimResults."""
+    from paper_2409_03365_b200 import SimResults, make_sim_options
+    b, res, arena, _ = plans.encoded
+    cap = plans.sim_arena_bound()
+    out = SimResults(len(plans), cap)
+    oracle().wso_simulate_batch(b, res, arena, C.byref(make_sim_options(**sim_opts)), out.results, out.arena, cap,
+                                C.byref(out.arena_used))
+    return out
+
+
 class RefOpts(C.Structure):
     _fields_ = [("eps", C.c_double), ("max_iters", C.c_int), ("drop_floor", C.c_double),
                 ("sequential", C.c_int), ("bt_depth", C.c_int), ("bt_branching", C.c_int),
@@ -116,6 +127,8 @@ def ref():
         lib.wsref_sweep_sim.argtypes = [C.c_long, C.POINTER(RefSimOpts)]
         lib.wsref_sweep_sim_bench.restype = C.c_double
         lib.wsref_sweep_sim_bench.argtypes = [C.c_long, C.c_long, C.c_int]
+        lib.wsref_strategy_plan_text.restype = vp
+        lib.wsref_strategy_plan_text.argtypes = [C.c_char_p, C.c_char_p, C.c_char_p, C.POINTER(RefOpts)]
         lib.wsref_latency_ms.restype = C.c_double
         lib.wsref_latency_ms.argtypes = [C.c_char_p, C.c_int, C.c_int, C.c_int]
         _ref = lib
@@ -157,6 +170,12 @@ def ref_fuzz(count: int) -> list[tuple[str, str]]:
     ref().wsref_free_list(ws, count)
     ref().wsref_free_list(ts, count)
     return out
+
+
+def ref_strategy_plan_text(workload: str, topology: str, strategy: str, **opts) -> str:
+    """Reference plan_for_strategy (cli.hpp:163-171) plan text, any of the four strategies."""
+    return _s(ref().wsref_strategy_plan_text(workload.encode(), topology.encode(), strategy.encode(),
+                                             C.byref(ref_options(**opts))))
 
 
 def ref_sweep_plan(i: int) -> str:

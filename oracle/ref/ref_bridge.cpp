@@ -258,6 +258,29 @@ char* wsref_sim_text(const char* workload, const char* topology, const wsref_opt
     }
 }
 
+// plan_for_strategy (cli.hpp:163-171) for any of the four strategies: plan text or error.
+char* wsref_strategy_plan_text(const char* workload, const char* topology, const char* strategy,
+                               const wsref_opts* o) {
+    try {
+        const WorkloadSpec spec = parse_workload(workload);
+        const ClusterTopology topo = parse_topology(topology);
+        const PlannerOptions opt = to_opts(o);
+        const std::string s = strategy;
+        try {
+            if (s == "wavefront") return dup(write_plan(plan_workload(spec, topo, opt).plan));
+            const PlanningBase base = prepare_planning_base(spec, topo, opt);
+            if (s == "decoupled-sequential") return dup(write_plan(plan_decoupled_sequential(base, topo, opt)));
+            if (s == "task-level-optimus") return dup(write_plan(plan_task_level_optimus(base, topo, opt)));
+            if (s == "distmm-mt") return dup(write_plan(plan_distmm_mt(base, topo, opt)));
+            return dup("error ParseError: unknown strategy '" + s + "'\n");
+        } catch (const Error& e) {
+            return dup(std::string("error Error: ") + e.what() + "\n");
+        }
+    } catch (const Error& e) {
+        return dup(std::string("error Parse: ") + e.what() + "\n");
+    }
+}
+
 // simulate_plan + validate_plan of a plan file (parse_plan, plan_io.hpp:112-255).
 char* wsref_sim_plan_text(const char* plan_text, const wsref_sim_opts* so) {
     try {

@@ -59,7 +59,7 @@ bool id_less(int a, int b) { return "m" + std::to_string(a) < "m" + std::to_stri
 struct Entity {  // PlanEntity fields used by the evaluator (planner.hpp:99-122)
     int length = 0, tp = 1;
     std::uint64_t param_bytes = 0, act_bytes = 0;
-    double w = 1.0, c = 0.0;
+    double w = 1.0, c = 0.0, frac = 1.0;  // frac: batch_fraction
     std::string group;  // param_group, or the entity id when empty
     std::vector<ws_out_piece> pieces;
     // ScalingCurve::eval_batch_fraction (scaling.hpp:83-86)
@@ -119,6 +119,7 @@ struct Eval {
             e.act_bytes = B.mod_act[gm];
             e.w = B.mod_w[gm];
             e.c = B.mod_c[gm];
+            e.frac = B.mod_frac ? B.mod_frac[gm] : 1.0;
             const int grp = m.length == B.mod_layers[gm] ? B.mod_group[gm] : -1;
             if (grp < 0)
                 e.group = "m" + std::to_string(k);
@@ -156,7 +157,7 @@ struct Eval {
                         mem[d] += (1.0 + P.grad_mult) * static_cast<double>(x.param_bytes) / x.tp;
                         charged[d].insert(x.group);
                     }
-                    mem[d] += e.layers * (static_cast<double>(x.act_bytes) * 1.0 / e.n);
+                    mem[d] += e.layers * (static_cast<double>(x.act_bytes) * x.frac / e.n);
                 }
             }
         return mem;
@@ -312,12 +313,12 @@ struct Eval {
                 const ws_out_entry& e = V.en[V.wv[w].entry_begin + i];
                 if (e.metaop < 0 || e.metaop >= K) continue;
                 const Entity& x = ent[e.metaop];
-                layer_s[e.metaop] += x.w * 1.0 * e.layers;
+                layer_s[e.metaop] += x.w * x.frac * e.layers;
                 device_s[e.metaop] += e.span * e.n;
             }
         for (int k = 0; k < K; ++k) {
-            const double t1 = ent[k].eval_bf(1.0, 1.0);
-            if (t1 > 0.0) peak_rate = std::max(peak_rate, ent[k].w * 1.0 / t1);
+            const double t1 = ent[k].eval_bf(1.0, ent[k].frac);
+            if (t1 > 0.0) peak_rate = std::max(peak_rate, ent[k].w * ent[k].frac / t1);
         }
         util.assign(K, 0.0);
         util_mask = 0;
@@ -352,7 +353,7 @@ struct Eval {
                     continue;
                 }
                 if (!seen.insert(e.metaop).second) fail(WS_V_DUPLICATE, w, e.metaop, 0, 0, 0);
-                const double per_layer = ent[e.metaop].eval_bf(e.n, 1.0);
+                const double per_layer = ent[e.metaop].eval_bf(e.n, ent[e.metaop].frac);
                 const double span = e.layers * per_layer;
                 if (std::abs(span - e.span) > tol + 1e-9 * std::abs(span))
                     fail(WS_V_SPAN, w, e.metaop, 0, e.span, span);

@@ -19,7 +19,7 @@ __all__ = [
     "ParseError", "InfeasibleError", "InvariantError", "CyclicWorkload", "UnknownModule", "EmptyWorkload",
     "InsufficientProfile", "DegenerateFit", "OutOfRange", "NoValidAllocation", "EmptyLevel",
     "PlacementInfeasible", "LimitExceeded", "WS_STATUS", "raise_for_text", "SimOptions", "SimResult",
-    "SimResults", "make_sim_options",
+    "SimResults", "make_sim_options", "PlanSet", "STRATEGIES",
 ]
 
 
@@ -169,6 +169,14 @@ def _load() -> C.CDLL:
         "wsx_algorithmic_bytes": (None, [vp, vp, vp, C.POINTER(u64), C.POINTER(u64)]),
         "wsx_host_alloc": (vp, [u64]),
         "wsx_sim_text": (vp, [vp, i32, vp, vp, vp, vp]),
+        "wsx_plans_new": (vp, []),
+        "wsx_plans_free": (None, [vp]),
+        "wsx_plans_size": (i32, [vp]),
+        "wsx_plans_add_text": (i32, [vp, C.c_char_p]),
+        "wsx_plans_error": (C.c_char_p, [vp]),
+        "wsx_plans_encode": (vp, [vp, i32, C.POINTER(vp), C.POINTER(vp), C.POINTER(u64)]),
+        "wsx_plans_write": (vp, [vp, i32]),
+        "wsx_plans_sim_text": (vp, [vp, i32, vp, vp]),
         "ws_simulate_staged": (C.c_int, [vp, C.POINTER(SimOptions), vp]),
         "ws_fetch_sim": (C.c_int, [vp, vp, vp, u64, C.POINTER(u64), vp]),
         "ws_simulate_batch_host": (C.c_int, [vp, vp, vp, vp, u64, C.POINTER(SimOptions), vp, vp, u64,
@@ -288,6 +296,55 @@ class ProblemSet:
 
     def dump_topology(self, i: int) -> str:
         return _take_str(lib.wsx_dump_topology(self._h, i))
+
+
+class PlanSet:
+    """Plan files of any strategy (parse_plan, plan_io.hpp:112-255) for the
+    device evaluator: Planner.simulate_plans(PlanSet) replaces
+    simulate_plan(parse_plan(text)) + validate_plan for every plan."""
+
+    def __init__(self):
+        self._h = lib.wsx_plans_new()
+        self._enc = None
+
+    def __del__(self):
+        h, self._h = getattr(self, "_h", None), None
+        if h and lib is not None:
+            lib.wsx_plans_free(h)
+
+    def __len__(self) -> int:
+        return lib.wsx_plans_size(self._h)
+
+    def add_text(self, plan_text: str) -> int:
+        i = lib.wsx_plans_add_text(self._h, plan_text.encode())
+        if i < 0:
+            raise ParseError(lib.wsx_plans_error(self._h).decode())
+        self._enc = None
+        return i
+
+    def encode(self, pinned: bool = False):
+        """(ws_batch*, ws_plan_result*, arena*, arena bytes) of the encoded plans."""
+        res, arena, nbytes = C.c_void_p(), C.c_void_p(), C.c_uint64()
+        b = lib.wsx_plans_encode(self._h, 1 if pinned else 0, C.byref(res), C.byref(arena), C.byref(nbytes))
+        if not b:
+            raise ParseError(lib.wsx_plans_error(self._h).decode())
+        self._enc = (b, res.value, arena.value, nbytes.value)
+        return self._enc
+
+    @property
+    def encoded(self):
+        return self._enc if self._enc is not None else self.encode()
+
+    def sim_arena_bound(self) -> int:
+        return int(lib.ws_sim_arena_bound(self.encoded[0]))
+
+    def write(self, i: int) -> str:
+        """write_plan text of parsed plan i (round trip)."""
+        return _take_str(lib.wsx_plans_write(self._h, i))
+
+    def sim_text(self, i: int, sims: "SimResults") -> str:
+        return _take_str(lib.wsx_plans_sim_text(self._h, i, C.cast(sims.results, C.c_void_p),
+                                                C.cast(sims.arena, C.c_void_p)))
 
 
 class Results:
@@ -417,6 +474,19 @@ class Planner:
         self._ok(lib.ws_simulate_batch_host(self._h, pset.batch, res.results, res.arena, res.arena_used.value,
                                             C.byref(make_sim_options(**sim_opts)), out.results, out.arena, cap,
                                             C.byref(out.arena_used), stream))
+        return out
+
+    def simulate_plans(self, plans: PlanSet, stream: int | None = None, out: SimResults | None = None,
+                       **sim_opts) -> SimResults:
+        """simulate_plan + validate_plan of parsed plan files on the device."""
+        b, res, arena, nbytes = plans.encoded
+        cap = plans.sim_arena_bound()
+        n = len(plans)
+        if out is None or not out.fits(n, cap):
+            out = SimResults(n, cap)
+        out.n = n
+        self._ok(lib.ws_simulate_batch_host(self._h, b, res, arena, nbytes, C.byref(make_sim_options(**sim_opts)),
+                                            out.results, out.arena, cap, C.byref(out.arena_used), stream))
         return out
 
     def sim_ms(self) -> float:

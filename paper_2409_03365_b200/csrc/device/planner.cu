@@ -247,6 +247,7 @@ ws_batch rebase(const ws_batch& h, const void* hbase, char* dbase) {
     d.prof_t = mv(h.prof_t);
     d.bps = mv(h.bps);
     d.names = mv(h.names);
+    d.mod_frac = mv(h.mod_frac);
     d.blob = dbase;
     return d;
 }

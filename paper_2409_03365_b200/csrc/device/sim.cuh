@@ -485,7 +485,8 @@ __global__ void __launch_bounds__(32 * kSimWarps, WS_SIM_MINB) k_sim(SimArgs A) 
                                                       B.mod_layers[gm]);
             const uint64_t charged = chg[gk[k]];
             const double pstate = (1.0 + P.grad_mult) * static_cast<double>(pb) / B.mod_tp[gm];
-            const double act = V.en[e].layers * (static_cast<double>(B.mod_act[gm]) * 1.0 / V.en[e].n);
+            const double frac = B.mod_frac ? B.mod_frac[gm] : 1.0;  // PlanEntity::batch_fraction
+            const double act = V.en[e].layers * (static_cast<double>(B.mod_act[gm]) * frac / V.en[e].n);
             if (m >> lane & 1ull) {
                 if (!(charged >> lane & 1ull)) mem0 += pstate;
                 mem0 += act;
@@ -508,17 +509,18 @@ __global__ void __launch_bounds__(32 * kSimWarps, WS_SIM_MINB) k_sim(SimArgs A) 
         if (k >= K) continue;
         const int gm = mbase + V.mo[k].module;
         const double wk = B.mod_w[gm];
+        const double frac = B.mod_frac ? B.mod_frac[gm] : 1.0;
         for (int w = 0; w < nW; ++w)
             for (int i = 0; i < V.wv[w].n_entries; ++i) {
                 const ws_out_entry& e = V.en[V.wv[w].entry_begin + i];
                 if (e.metaop != k) continue;
-                ls[s] += wk * 1.0 * e.layers;
+                ls[s] += wk * frac * e.layers;
                 ds[s] += e.span * e.n;
                 seen_k[s] = true;
             }
-        const double t1 = eval_bf(V.pc + V.mo[k].piece_begin, V.mo[k].piece_count, B.mod_c[gm], wk, 1.0, 1.0);
+        const double t1 = eval_bf(V.pc + V.mo[k].piece_begin, V.mo[k].piece_count, B.mod_c[gm], wk, 1.0, frac);
         if (t1 > 0.0) {
-            const double r = wk * 1.0 / t1;
+            const double r = wk * frac / t1;
             rate = (rate < r) ? r : rate;
         }
     }
@@ -549,8 +551,9 @@ __global__ void __launch_bounds__(32 * kSimWarps, WS_SIM_MINB) k_sim(SimArgs A) 
                 flags = F_UNKNOWN;
             } else {
                 const int gm = mbase + V.mo[k].module;
-                const double per_layer = eval_bf(V.pc + V.mo[k].piece_begin, V.mo[k].piece_count, B.mod_c[gm],
-                                                 B.mod_w[gm], static_cast<double>(V.en[e].n), 1.0);
+                const double per_layer =
+                    eval_bf(V.pc + V.mo[k].piece_begin, V.mo[k].piece_count, B.mod_c[gm], B.mod_w[gm],
+                            static_cast<double>(V.en[e].n), B.mod_frac ? B.mod_frac[gm] : 1.0);
                 const double span = V.en[e].layers * per_layer;
                 const double rec = V.en[e].span;
                 if (fabs(span - rec) > tol + 1e-9 * fabs(span)) flags |= F_SPAN;
@@ -577,9 +580,10 @@ __global__ void __launch_bounds__(32 * kSimWarps, WS_SIM_MINB) k_sim(SimArgs A) 
                     if (flags & F_DUP) fail(WS_V_DUPLICATE, w, k, 0, 0, 0);
                     if (flags & F_SPAN) {
                         const int gm = mbase + V.mo[k].module;
-                        const double span = V.en[e].layers * eval_bf(V.pc + V.mo[k].piece_begin, V.mo[k].piece_count,
-                                                                      B.mod_c[gm], B.mod_w[gm],
-                                                                      static_cast<double>(V.en[e].n), 1.0);
+                        const double span =
+                            V.en[e].layers * eval_bf(V.pc + V.mo[k].piece_begin, V.mo[k].piece_count, B.mod_c[gm],
+                                                     B.mod_w[gm], static_cast<double>(V.en[e].n),
+                                                     B.mod_frac ? B.mod_frac[gm] : 1.0);
                         fail(WS_V_SPAN, w, k, 0, V.en[e].span, span);
                     }
                     if (flags & F_SPAN_DUR) fail(WS_V_SPAN_DURATION, w, 0, 0, 0, 0);

@@ -496,4 +496,150 @@ std::string write_plan(const ExecutionPlan& plan) {
     return out;
 }
 
+// ---- plan parser (plan_io.hpp:112-255): any strategy's plan file back into an ExecutionPlan ----
+ExecutionPlan parse_plan(const std::string& text) {
+    ExecutionPlan plan;
+    plan.strategy.clear();
+    std::istringstream is(text);
+    std::string line;
+    int lineno = 0;
+    std::map<std::string, std::vector<CurvePiece>> curve_pieces;
+    std::map<std::string, std::pair<double, double>> curve_cw;
+    ClusterTopology topo;
+    bool saw_bw = false, saw_mem = false, saw_end = false;
+    int last_level = -1;
+    while (std::getline(is, line)) {
+        ++lineno;
+        if (blank_or_comment(line)) continue;
+        const auto toks = tokens_of(line);
+        const std::string ctx = "plan line " + std::to_string(lineno);
+        const std::string& head = toks[0];
+        try {
+            if (head == "strategy") {
+                if (toks.size() != 2) throw ParseError(ctx + ": expected 'strategy <name>'");
+                plan.strategy = toks[1];
+            } else if (head == "island") {
+                std::vector<int> members;
+                for (std::size_t i = 2; i < toks.size(); ++i) members.push_back(std::stoi(toks[i]));
+                topo.islands.push_back(members);
+            } else if (head == "bw") {
+                Fields kv(toks, 1, ctx);
+                topo.intra_bw = kv.real("intra");
+                topo.inter_bw = kv.real("inter");
+                saw_bw = true;
+            } else if (head == "mem") {
+                topo.mem_capacity = std::stoull(toks.at(1));
+                saw_mem = true;
+            } else if (head == "entity") {
+                if (toks.size() < 2) throw ParseError(ctx + ": entity needs an id");
+                Fields kv(toks, 2, ctx);
+                PlanEntity e;
+                e.id = toks[1];
+                e.kind = kv.str("kind");
+                e.length = static_cast<int>(kv.num("L"));
+                e.level = static_cast<int>(kv.num_or("level", 0));
+                e.tp_degree = static_cast<int>(kv.num_or("tp", 1));
+                e.global_batch = kv.num_or("B", 1);
+                e.batch_fraction = kv.real_or("frac", 1.0);
+                e.param_group = kv.str_or("param_group", "");
+                e.param_bytes = static_cast<std::uint64_t>(kv.num_or("param_bytes", 0));
+                e.act_bytes = static_cast<std::uint64_t>(kv.num_or("act_bytes", 0));
+                e.out_bytes = static_cast<std::uint64_t>(kv.num_or("out_bytes", 0));
+                e.w = kv.real_or("w", 1.0);
+                e.c = kv.real_or("c", 0.0);
+                if (kv.has("tasks"))
+                    for (const std::string& t : split_char(kv.str("tasks"), ';')) e.task_ids.insert(t);
+                plan.entities[e.id] = e;
+            } else if (head == "curve") {
+                if (toks.size() < 3) throw ParseError(ctx + ": malformed curve line");
+                if (toks[2] == "piece") {
+                    if (toks.size() != 8) throw ParseError(ctx + ": curve piece needs 5 numbers");
+                    CurvePiece p;
+                    p.n_lo = std::stod(toks[3]);
+                    p.n_hi = std::stod(toks[4]);
+                    p.alpha = std::stod(toks[5]);
+                    p.beta_c = std::stod(toks[6]);
+                    p.beta_w = std::stod(toks[7]);
+                    curve_pieces[toks[1]].push_back(p);
+                } else if (toks[2] == "workload") {
+                    Fields kv(toks, 3, ctx);
+                    curve_cw[toks[1]] = {kv.real("c"), kv.real("w")};
+                } else {
+                    throw ParseError(ctx + ": unknown curve directive '" + toks[2] + "'");
+                }
+            } else if (head == "dep") {
+                if (toks.size() != 3) throw ParseError(ctx + ": expected 'dep <from> <to>'");
+                plan.deps.insert({toks[1], toks[2]});
+            } else if (head == "lower_bound") {
+                plan.lower_bound = std::stod(toks.at(1));
+            } else if (head == "mem_multiplier") {
+                plan.grad_opt_multiplier = std::stod(toks.at(1));
+            } else if (head == "wave") {
+                Fields kv(toks, 2, ctx);
+                Wave w;
+                w.index = std::stoi(toks.at(1));
+                w.level = static_cast<int>(kv.num_or("level", 0));
+                w.start = kv.real("start");
+                w.duration = kv.real("dur");
+                if (w.level != last_level) {
+                    plan.schedule.level_boundaries.push_back(w.index);
+                    last_level = w.level;
+                }
+                plan.schedule.waves.push_back(w);
+            } else if (head == "entry") {
+                if (plan.schedule.waves.empty()) throw ParseError(ctx + ": entry before any wave");
+                Fields kv(toks, 1, ctx);
+                WaveEntry e;
+                e.metaop_id = kv.str("metaop");
+                e.n = static_cast<int>(kv.num("n"));
+                e.layers = static_cast<int>(kv.num("l"));
+                e.span = kv.real("dur");
+                Wave& w = plan.schedule.waves.back();
+                w.entries.push_back(e);
+                if (kv.has("devices")) {
+                    std::vector<int> devs;
+                    for (const std::string& d : split_char(kv.str("devices"), ','))
+                        if (!d.empty()) devs.push_back(std::stoi(d));
+                    plan.devices[{w.index, e.metaop_id}] = devs;
+                }
+            } else if (head == "flow") {
+                Fields kv(toks, 1, ctx);
+                Flow f;
+                const auto from = split_char(kv.str("from"), ':');
+                const auto to = split_char(kv.str("to"), ':');
+                if (from.size() != 2 || to.size() != 2) throw ParseError(ctx + ": flow endpoints are <wave>:<id>");
+                f.from_wave = std::stoi(from[0]);
+                f.from_id = from[1];
+                f.to_wave = std::stoi(to[0]);
+                f.to_id = to[1];
+                f.volume = static_cast<std::uint64_t>(kv.num("volume"));
+                f.mode = kv.str("mode");
+                plan.flows.push_back(f);
+            } else if (head == "end_time") {
+                plan.schedule.end_time = std::stod(toks.at(1));
+                saw_end = true;
+            } else {
+                throw ParseError(ctx + ": unknown directive '" + head + "'");
+            }
+        } catch (const ParseError&) {
+            throw;
+        } catch (const std::logic_error& e) {
+            throw ParseError(ctx + ": " + e.what());
+        }
+    }
+    if (plan.strategy.empty()) throw ParseError("plan: missing strategy line");
+    if (!saw_bw || !saw_mem) throw ParseError("plan: incomplete topology");
+    if (!saw_end) throw ParseError("plan: missing end_time");
+    topo.finalize();
+    plan.topo = topo;
+    for (auto& [id, pieces] : curve_pieces) {
+        auto cw = curve_cw.find(id);
+        if (cw == curve_cw.end()) throw ParseError("plan: curve '" + id + "' missing workload line");
+        plan.curves[id] = ScalingCurve::from_pieces(pieces, cw->second.first, cw->second.second);
+    }
+    for (const auto& [id, e] : plan.entities)
+        if (!plan.curves.count(id)) throw ParseError("plan: entity '" + id + "' has no curve");
+    return plan;
+}
+
 }  // namespace wsgpu

@@ -23,7 +23,11 @@ namespace {
 
 std::string mid(int k) { return "m" + std::to_string(k); }
 
-std::string violation_text(const ws_out_violation& v, const ClusterTopology& topo) {
+std::string violation_text(const ws_out_violation& v, const ClusterTopology& topo,
+                           const std::vector<std::string>& names) {
+    auto mid = [&](int k) {
+        return k >= 0 && k < static_cast<int>(names.size()) ? names[k] : "m" + std::to_string(k);
+    };
     const std::string wave = "wave " + std::to_string(v.wave) + ": ";
     auto dev = [&](int d) {
         return d >= 0 && d < static_cast<int>(topo.devices.size()) ? std::to_string(topo.devices[d])
@@ -65,8 +69,15 @@ std::string violation_text(const ws_out_violation& v, const ClusterTopology& top
 std::string sim_text(const Problem& prob, const ws_plan_result& r, const std::uint8_t* plan_arena,
                      const ws_sim_result& s, const std::uint8_t* sim_arena) {
     if (r.status != WS_STATUS_OK) return plan_text_or_error(prob, r, plan_arena);
+    std::vector<std::string> names;
+    for (int k = 0; k < r.n_metaops; ++k) names.push_back(mid(k));
+    return sim_text_named(*prob.topo, r, s, sim_arena, names);
+}
+
+std::string sim_text_named(const ClusterTopology& topo, const ws_plan_result& r, const ws_sim_result& s,
+                           const std::uint8_t* sim_arena, const std::vector<std::string>& names) {
     if (s.status != WS_STATUS_OK) return "error Internal: simulation arena overflow\n";
-    const ClusterTopology& topo = *prob.topo;
+    auto name = [&](int k) { return k < static_cast<int>(names.size()) ? names[k] : mid(k); };
     const int N = static_cast<int>(topo.devices.size()), K = r.n_metaops;
     const std::uint8_t* b = sim_arena + s.offset;
     auto f64 = [&](std::size_t off) {
@@ -98,14 +109,14 @@ std::string sim_text(const Problem& prob, const ws_plan_result& r, const std::ui
     std::vector<int> ids;
     for (int k = 0; k < K; ++k)
         if (umask >> k & 1ull) ids.push_back(k);
-    std::sort(ids.begin(), ids.end(), [](int a, int c) { return mid(a) < mid(c); });
-    for (int k : ids) out += " " + mid(k) + "=" + fmt_exact(f64(o_util + 8ull * k));
+    std::sort(ids.begin(), ids.end(), [&](int a, int c) { return name(a) < name(c); });
+    for (int k : ids) out += " " + name(k) + "=" + fmt_exact(f64(o_util + 8ull * k));
     out += "\nvalid " + std::to_string(s.valid) + " " + std::to_string(s.n_violations) + "\n";
     const int nv = std::min(s.n_violations, WS_SIM_MAX_VIOLATIONS);
     for (int i = 0; i < nv; ++i) {
         ws_out_violation v;
         std::memcpy(&v, b + o_viol + sizeof(ws_out_violation) * i, sizeof(v));
-        out += "v " + violation_text(v, topo) + "\n";
+        out += "v " + violation_text(v, topo, names) + "\n";
     }
     return out;
 }

@@ -81,3 +81,9 @@ def baseline_sweep_hashes():
             name, *hashes = line.split()
             out[name] = hashes
     return out
+
+
+@pytest.fixture(scope="session")
+def plan_files():
+    with gzip.open(GOLDEN / "plan_files.json.gz", "rt") as f:
+        return json.load(f)
