@@ -312,6 +312,9 @@ struct ExecutionPlan {
 std::string write_plan(const ExecutionPlan& plan);
 // parse_plan (plan_io.hpp:112-255): a plan file of any strategy
 ExecutionPlan parse_plan(const std::string& text);
+// Structured ingestion (cli.hpp:46-110): the JSON forms of workload and topology
+WorkloadSpec workload_from_json(const std::string& text);
+ClusterTopology topology_from_json(const std::string& text);
 
 // ---- planner API (planner.hpp:21-38,156) ------------------------------------------------------
 struct PlannerOptions {

@@ -40,6 +40,9 @@ void wsx_set_free(wsx_set* s);
 int32_t wsx_set_size(const wsx_set* s);
 /* Each add returns the problem index, or -1 (see wsx_set_error). */
 int32_t wsx_add_text(wsx_set* s, const char* workload, const char* topology, const ws_options* o);
+/* JSON workload / topology (cli.hpp:46-110 workload_from_json, topology_from_json);
+ * an argument not starting with '{' is read with the text grammar instead. */
+int32_t wsx_add_json(wsx_set* s, const char* workload, const char* topology, const ws_options* o);
 int32_t wsx_add_scenario(wsx_set* s, const char* name, int32_t tasks, int32_t devices, uint64_t seed,
                          const ws_options* o);
 int32_t wsx_add_sweep(wsx_set* s, int64_t start, int64_t count, const ws_options* o);

@@ -127,6 +127,8 @@ def ref():
         lib.wsref_sweep_sim.argtypes = [C.c_long, C.POINTER(RefSimOpts)]
         lib.wsref_sweep_sim_bench.restype = C.c_double
         lib.wsref_sweep_sim_bench.argtypes = [C.c_long, C.c_long, C.c_int]
+        lib.wsref_json_plan_text.restype = vp
+        lib.wsref_json_plan_text.argtypes = [C.c_char_p, C.c_char_p, C.POINTER(RefOpts)]
         lib.wsref_strategy_plan_text.restype = vp
         lib.wsref_strategy_plan_text.argtypes = [C.c_char_p, C.c_char_p, C.c_char_p, C.POINTER(RefOpts)]
         lib.wsref_latency_ms.restype = C.c_double
@@ -176,6 +178,11 @@ def ref_strategy_plan_text(workload: str, topology: str, strategy: str, **opts) 
     """Reference plan_for_strategy (cli.hpp:163-171) plan text, any of the four strategies."""
     return _s(ref().wsref_strategy_plan_text(workload.encode(), topology.encode(), strategy.encode(),
                                              C.byref(ref_options(**opts))))
+
+
+def ref_json_plan_text(workload_json: str, topology_json: str, **opts) -> str:
+    """Reference workload_from_json + topology_from_json + planning (cli.hpp:46-110)."""
+    return _s(ref().wsref_json_plan_text(workload_json.encode(), topology_json.encode(), C.byref(ref_options(**opts))))
 
 
 def ref_sweep_plan(i: int) -> str:

@@ -12,6 +12,7 @@
 #include <vector>
 
 #include "wavesched/baselines.hpp"
+#include "wavesched/cli.hpp"
 #include "wavesched/planner.hpp"
 #include "wavesched/scenarios.hpp"
 #include "wavesched/simulate.hpp"
@@ -276,6 +277,17 @@ char* wsref_strategy_plan_text(const char* workload, const char* topology, const
         } catch (const Error& e) {
             return dup(std::string("error Error: ") + e.what() + "\n");
         }
+    } catch (const Error& e) {
+        return dup(std::string("error Parse: ") + e.what() + "\n");
+    }
+}
+
+// Reference plan text for JSON workload/topology (cli.hpp:46-110 ingestion).
+char* wsref_json_plan_text(const char* workload, const char* topology, const wsref_opts* o) {
+    try {
+        WorkloadSpec spec = workload_from_json(workload);
+        ClusterTopology topo = topology_from_json(topology);
+        return dup(outcome(spec, topo, to_opts(o), o ? o->strategy : 0));
     } catch (const Error& e) {
         return dup(std::string("error Parse: ") + e.what() + "\n");
     }

@@ -156,6 +156,7 @@ def _load() -> C.CDLL:
         "wsx_set_free": (None, [vp]),
         "wsx_set_size": (i32, [vp]),
         "wsx_add_text": (i32, [vp, C.c_char_p, C.c_char_p, C.POINTER(Options)]),
+        "wsx_add_json": (i32, [vp, C.c_char_p, C.c_char_p, C.POINTER(Options)]),
         "wsx_add_scenario": (i32, [vp, C.c_char_p, i32, i32, u64, C.POINTER(Options)]),
         "wsx_add_sweep": (i32, [vp, i64, i64, C.POINTER(Options)]),
         "wsx_set_error": (C.c_char_p, [vp]),
@@ -245,6 +246,11 @@ class ProblemSet:
 
     def add_text(self, workload: str, topology: str, **opts) -> int:
         return self._check(lib.wsx_add_text(self._h, workload.encode(), topology.encode(),
+                                            C.byref(make_options(**opts))))
+
+    def add_json(self, workload: str, topology: str, **opts) -> int:
+        """JSON workload / topology (cli.hpp:46-110); text grammar if not starting with '{'."""
+        return self._check(lib.wsx_add_json(self._h, workload.encode(), topology.encode(),
                                             C.byref(make_options(**opts))))
 
     def add_scenario(self, name: str, tasks: int, devices: int, seed: int = 0, **opts) -> int:

@@ -23,8 +23,11 @@ NVCC = str(CUDA / "bin" / "nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-fmad=false", "--expt-relaxed-constexpr",
               "-Xcompiler", "-fPIC", "-Xcompiler", "-ffp-contract=off", "-I", str(ROOT / "include")] + ARCH
+# nlohmann/json (header-only; the same library the reference's workload_from_json uses)
+JSON_DIR = Path(os.environ.get("WSGPU_JSON_DIR", "/opt/prime-rl/.venv/lib/python3.12/site-packages/include/"
+                                                 "cudnn_frontend/thirdparty/nlohmann"))
 CXX_FLAGS = ["-O2", "-std=c++17", "-fPIC", "-ffp-contract=off", "-Wall", "-Wno-sign-compare",
-             "-I", str(ROOT / "include"), "-I", str(CUDA / "include")]
+             "-I", str(ROOT / "include"), "-I", str(CUDA / "include"), "-I", str(JSON_DIR)]
 
 LIBNAME = LIB / "libwsgpu.so"
 

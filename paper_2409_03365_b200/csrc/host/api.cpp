@@ -138,6 +138,26 @@ void wsx_set_free(wsx_set* s) { delete s; }
 int32_t wsx_set_size(const wsx_set* s) { return static_cast<int32_t>(s->probs.size()); }
 const char* wsx_set_error(const wsx_set* s) { return s->error.c_str(); }
 
+// JSON workload/topology (cli.hpp:46-110); either may also be the text grammar
+// when it does not start with '{'.
+int32_t wsx_add_json(wsx_set* s, const char* workload, const char* topology, const ws_options* o) {
+    auto is_json = [](const char* t) {
+        while (*t == ' ' || *t == '\n' || *t == '\t' || *t == '\r') ++t;
+        return *t == '{';
+    };
+    try {
+        WorkloadSpec spec = is_json(workload) ? workload_from_json(workload) : parse_workload(workload);
+        ClusterTopology topo = is_json(topology) ? topology_from_json(topology) : parse_topology(topology);
+        s->specs.push_back(std::move(spec));
+        s->topos.push_back(std::move(topo));
+    } catch (const std::exception& e) {
+        s->error = e.what();
+        return -1;
+    }
+    s->probs.push_back({&s->specs.back(), &s->topos.back(), from_c(o)});
+    return static_cast<int32_t>(s->probs.size() - 1);
+}
+
 int32_t wsx_add_text(wsx_set* s, const char* workload, const char* topology, const ws_options* o) {
     try {
         WorkloadSpec spec = parse_workload(workload);

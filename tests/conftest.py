@@ -87,3 +87,9 @@ def baseline_sweep_hashes():
 def plan_files():
     with gzip.open(GOLDEN / "plan_files.json.gz", "rt") as f:
         return json.load(f)
+
+
+@pytest.fixture(scope="session")
+def json_cases_fixture():
+    with gzip.open(GOLDEN / "json_cases.json.gz", "rt") as f:
+        return json.load(f)
