@@ -109,7 +109,8 @@ typedef struct ws_plan_rec {
  * and the baseline planners of baselines.hpp. */
 enum ws_strategy {
     WS_STRATEGY_WAVEFRONT = 0,            /* planner.hpp:156-212                  */
-    WS_STRATEGY_DECOUPLED_SEQUENTIAL = 1  /* plan_decoupled_sequential, baselines.hpp:104-131 */
+    WS_STRATEGY_DECOUPLED_SEQUENTIAL = 1, /* plan_decoupled_sequential, baselines.hpp:104-131 */
+    WS_STRATEGY_DISTMM_MT = 2             /* plan_distmm_mt, baselines.hpp:323-413          */
 };
 
 /* Structure-of-arrays batch.  All pointers address the same memory space
@@ -174,7 +175,8 @@ typedef struct ws_plan_result {
     int64_t err_a, err_b;
     double err_x, err_y;
     int32_t n_metaops, n_edges, n_levels, n_waves;
-    int32_t n_entries, n_flows, n_pieces, pad;
+    int32_t n_entries, n_flows, n_pieces;
+    int32_t n_scopes;   /* task-scoped strategies: entities are (MetaOp, task) pairs */
     double lower_bound; /* PlannerResult::lower_bound (planner.hpp:189)          */
     double end_time;    /* predicted_makespan = schedule.end_time (:193-194)      */
     uint64_t offset;    /* byte offset of this plan's record in the arena        */
@@ -227,6 +229,13 @@ typedef struct ws_out_flow {
     int32_t from_wave, from_metaop, to_wave, to_metaop;
     int32_t mode, pad;
 } ws_out_flow;
+
+/* Last section, only for task-scoped strategies (n_scopes > 0): entity k of
+ * the record is PlanEntity "m<metaop>@<task id>" (baselines.hpp:49-55); its
+ * ws_out_metaop row carries the MetaOp's module, level, length and base curve. */
+typedef struct ws_out_scope {
+    int32_t metaop, task; /* task = declaration index within the plan */
+} ws_out_scope;
 
 /* ---- plan evaluation: simulate_plan + validate_plan (simulate.hpp, validate.hpp)
  * Evaluates planned records (ws_plan_result + arena, from the planner or any

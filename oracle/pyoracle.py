@@ -148,7 +148,7 @@ def ref_options(**kw) -> RefOpts:
     o = RefOpts(1e-7, 200, 0.0, 0, 2, 3, 3.0, 0.0, 0, 0)
     for k, v in kw.items():
         if k == "strategy" and isinstance(v, str):
-            v = {"wavefront": 0, "decoupled-sequential": 1}[v]
+            v = {"wavefront": 0, "decoupled-sequential": 1, "distmm-mt": 2}[v]
         setattr(o, k, v)
     return o
 

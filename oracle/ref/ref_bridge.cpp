@@ -73,6 +73,7 @@ PlannerOptions to_opts(const wsref_opts* o) {
 ExecutionPlan plan_strategy(const WorkloadSpec& spec, const ClusterTopology& topo, const PlannerOptions& opt,
                             int strategy) {
     if (strategy == 1) return plan_decoupled_sequential(prepare_planning_base(spec, topo, opt), topo, opt);
+    if (strategy == 2) return plan_distmm_mt(prepare_planning_base(spec, topo, opt), topo, opt);
     return plan_workload(spec, topo, opt).plan;
 }
 

@@ -18,6 +18,7 @@
 #include <cmath>
 #include <cstdint>
 #include <cstring>
+#include <map>
 #include <set>
 #include <string>
 #include <vector>
@@ -235,6 +236,7 @@ struct PlanOut {
     std::vector<WaveRec> waves;
     std::vector<EntryRec> entries;
     std::vector<FlowRec> flows;
+    std::vector<std::pair<int, int>> scope;  // per entity (metaop, task) for task-scoped strategies
     double lower_bound = 0, end_time = 0;
 };
 
@@ -251,8 +253,20 @@ public:
         fit_modules();          // planner.hpp:66-94
         if (R.strategy == WS_STRATEGY_DECOUPLED_SEQUENTIAL)
             decoupled();        // baselines.hpp:104-131
+        else if (R.strategy == WS_STRATEGY_DISTMM_MT)
+            distmm();           // baselines.hpp:323-413
         else
             allocate_and_schedule(out);
+        if (!scoped) {          // entities are the MetaOps (planner.hpp:99-122)
+            KE = K;
+            e_mod.resize(K);
+            for (int k = 0; k < K; ++k) e_mod[k] = k;
+            e_task.assign(K, -1);
+            e_frac.assign(K, 1.0);
+            e_by_rank = by_rank;
+            e_idrank = idrank;
+            e_edges = edges;
+        }
         place(out);
         fill(out);
     }
@@ -276,6 +290,13 @@ private:
     // schedule
     std::vector<int> upper_n, upper_l, lower_n, lower_l;
     std::vector<double> cstar;
+    // placement entities: the MetaOps, or (MetaOp, task) pairs for the task-scoped baselines
+    bool scoped = false;
+    int KE = 0;
+    std::vector<int> e_mod, e_task, e_by_rank, e_idrank;
+    std::vector<double> e_frac;
+    std::vector<std::pair<int, int>> e_edges;  // deps between entities, std::set<pair<string,string>> order
+    const std::vector<Curve>* curve_override = nullptr;  // per MetaOp, while a scaled level runs
     std::vector<WaveRec> waves;
     std::vector<EntryRec> entries;
     std::vector<FlowRec> flows;
@@ -430,7 +451,7 @@ private:
         }
     }
 
-    const Curve& curve(int k) const { return mcurve[mod_of[k]]; }
+    const Curve& curve(int k) const { return curve_override ? (*curve_override)[k] : mcurve[mod_of[k]]; }
     double T(int k, int n) const { return curve(k).eval(n); }
 
     // ---- subsystem (3)+(4a): allocation and wave scheduling per level ----
@@ -523,6 +544,143 @@ private:
         end_time = now;
     }
 
+    // "m<a>@<task a>" < "m<b>@<task b>" as std::string; tasks by id rank
+    static bool scoped_less(int a, int ta, int b, int tb) {
+        if (a == b) return ta < tb;
+        const std::string sa = std::to_string(a), sb = std::to_string(b);
+        if (sb.size() > sa.size() && sb.compare(0, sa.size(), sa) == 0) return false;  // '@' > digit
+        if (sa.size() > sb.size() && sa.compare(0, sb.size(), sb) == 0) return true;
+        return sa < sb;
+    }
+
+    // plan_distmm_mt (baselines.hpp:323-413): tasks in declaration order; in a
+    // task, same-level MetaOps (task_view levels) split the cluster through
+    // solve_continuous/discretize/schedule_level on curves whose per-device
+    // term is scaled by the share fraction, dependent stages run alone on
+    // their largest valid allocation.  Entities are (MetaOp, task) pairs.
+    void distmm() {
+        scoped = true;
+        valid.assign(K, 0);
+        for (int k = 0; k < K; ++k) {
+            const int g = mg(mod_of[k]);
+            const int tp = B.mod_tp[g];
+            for (int n = 1; n <= N; ++n)
+                if (n % tp == 0 && B.mod_batch[g] % (n / tp) == 0) valid[k] |= 1ull << (n - 1);
+        }
+        upper_n.assign(K, 0);
+        upper_l.assign(K, 0);
+        lower_n.assign(K, 0);
+        lower_l.assign(K, 0);
+        std::map<std::pair<int, int>, int> ent_of;
+        std::vector<int> task_rank_of;
+        auto entity = [&](int k, int t) {
+            auto it = ent_of.find({k, t});
+            if (it != ent_of.end()) return it->second;
+            const int e = KE++;
+            e_mod.push_back(k);
+            e_task.push_back(t);
+            e_frac.push_back(1.0 / static_cast<double>(popc(taskmask[mod_of[k]])));  // share_fraction
+            ent_of[{k, t}] = e;
+            return e;
+        };
+        std::vector<std::pair<int, int>> sdeps;  // (entity, entity)
+        double now = 0.0;
+        for (int t = 0; t < R.n_tasks; ++t) {
+            const int tr = B.task_rank[R.task_begin + t];
+            task_rank_of.push_back(tr);
+            std::vector<char> mem(K, 0);
+            for (int k = 0; k < K; ++k) mem[k] = (taskmask[mod_of[k]] >> tr & 1ull) ? 1 : 0;
+            std::vector<std::pair<int, int>> tedges;  // task_view edges, set order
+            for (const auto& e : edges)
+                if (mem[e.first] && mem[e.second]) tedges.push_back(e);
+            // detail::topo_order over the members (ready set by id string)
+            std::vector<int> indeg(K, 0), order;
+            for (const auto& e : tedges) ++indeg[e.second];
+            std::set<int> ready;
+            for (int k = 0; k < K; ++k)
+                if (mem[k] && !indeg[k]) ready.insert(idrank[k]);
+            while (!ready.empty()) {
+                const int k = by_rank[*ready.begin()];
+                ready.erase(ready.begin());
+                order.push_back(k);
+                for (const auto& e : tedges)
+                    if (e.first == k && --indeg[e.second] == 0) ready.insert(idrank[e.second]);
+            }
+            std::vector<int> lvl(K, 0);
+            int max_level = 0;
+            for (int k : order) {
+                int lv = 0;
+                for (const auto& e : tedges)
+                    if (e.second == k) lv = std::max(lv, lvl[e.first] + 1);
+                lvl[k] = lv;
+                max_level = std::max(max_level, lv);
+            }
+            for (int l = 0; l <= max_level; ++l) {
+                std::vector<int> ids;
+                for (int k : order)
+                    if (lvl[k] == l) ids.push_back(k);
+                if (ids.empty()) continue;
+                std::vector<Curve> scaled(K);
+                for (int k : ids) {
+                    const int e = entity(k, t);
+                    std::vector<Piece> pcs = mcurve[mod_of[k]].p;  // detail::scale_curve
+                    for (Piece& q : pcs) q.bw *= e_frac[e];
+                    scaled[k] = make_curve(pcs, mcurve[mod_of[k]].c, mcurve[mod_of[k]].w);
+                    const int tp = B.mod_tp[mg(mod_of[k])];
+                    if (tp > N) throw Fail{WS_E_TP_EXCEEDS, k, tp};  // valid_allocations
+                }
+                if (ids.size() == 1) {
+                    const int k = ids[0];
+                    const int n = 64 - __builtin_clzll(valid[k]);  // valid.back()
+                    const int L = layers(mod_of[k]);
+                    const double span = L * scaled[k].eval(n);
+                    WaveRec wv;
+                    wv.level = l;
+                    wv.start = now;
+                    wv.dur = span;
+                    wv.entries.push_back(static_cast<int>(entries.size()));
+                    EntryRec en;
+                    en.k = entity(k, t);
+                    en.n = n;
+                    en.layers = L;
+                    en.span = span;
+                    entries.push_back(en);
+                    waves.push_back(wv);
+                    now += span;
+                } else {
+                    curve_override = &scaled;
+                    solve_and_discretize(ids);  // sums in task order
+                    std::vector<int> ids_id(ids);
+                    std::sort(ids_id.begin(), ids_id.end(), [&](int a, int b) { return idrank[a] < idrank[b]; });
+                    const std::size_t w0 = waves.size(), e0 = entries.size();
+                    schedule_level(ids_id, l);
+                    curve_override = nullptr;
+                    double t_end = 0.0;
+                    for (std::size_t w = w0; w < waves.size(); ++w) t_end += waves[w].dur;
+                    for (std::size_t w = w0; w < waves.size(); ++w) waves[w].start += now;
+                    now += t_end;
+                    for (std::size_t x = e0; x < entries.size(); ++x) entries[x].k = entity(entries[x].k, t);
+                }
+            }
+            for (const auto& e : tedges) sdeps.push_back({entity(e.first, t), entity(e.second, t)});
+        }
+        auto eless = [&](int a, int b) {
+            return scoped_less(e_mod[a], task_rank_of[e_task[a]], e_mod[b], task_rank_of[e_task[b]]);
+        };
+        e_by_rank.resize(KE);
+        for (int e = 0; e < KE; ++e) e_by_rank[e] = e;
+        std::sort(e_by_rank.begin(), e_by_rank.end(), eless);
+        e_idrank.assign(KE, 0);
+        for (int r = 0; r < KE; ++r) e_idrank[e_by_rank[r]] = r;
+        std::sort(sdeps.begin(), sdeps.end(), [&](const auto& x, const auto& y) {
+            if (x.first != y.first) return e_idrank[x.first] < e_idrank[y.first];
+            return e_idrank[x.second] < e_idrank[y.second];
+        });
+        sdeps.erase(std::unique(sdeps.begin(), sdeps.end()), sdeps.end());
+        e_edges = sdeps;
+        end_time = now;
+    }
+
     std::vector<int> valid_list(int k) const {
         std::vector<int> v;
         for (int n = 1; n <= N; ++n)
@@ -554,8 +712,11 @@ private:
                 c_lo = mid;
         }
         const double cs = 0.5 * (c_lo + c_hi);
-        // discretize (allocation.hpp:149-214), MetaOps in id order
-        for (int k : lv) {
+        // discretize (allocation.hpp:149-214), MetaOps in id order (the sums above
+        // run in LevelInput order, which the distmm baseline sets to task order)
+        std::vector<int> lv_id(lv);
+        std::sort(lv_id.begin(), lv_id.end(), [&](int a, int b) { return idrank[a] < idrank[b]; });
+        for (int k : lv_id) {
             const double nstar = std::min(curve(k).inverse_exact(cs / layers(mod_of[k])), nd);
             const std::vector<int> v = valid_list(k);
             const int L = layers(mod_of[k]);
@@ -618,11 +779,11 @@ private:
         // repair_capacity (allocation.hpp:107-139)
         while (true) {
             int widest = 0;
-            for (int k : lv) widest += std::max(upper_n[k], lower_l[k] ? lower_n[k] : 0);
+            for (int k : lv_id) widest += std::max(upper_n[k], lower_l[k] ? lower_n[k] : 0);
             if (widest <= N) break;
             int best = -1, best_target = 0;
             double best_pen = 0.0;
-            for (int k : lv) {
+            for (int k : lv_id) {
                 const std::vector<int> v = valid_list(k);
                 auto it = std::lower_bound(v.begin(), v.end(), upper_n[k]);
                 if (it == v.begin()) continue;
@@ -848,7 +1009,7 @@ private:
             in.push_back({cont, cont_bytes[k]});
             return in;
         }
-        for (const auto& e : edges) {  // preds in dep-set order
+        for (const auto& e : e_edges) {  // preds in dep-set order
             if (e.second != k) continue;
             const int pe = latest_entry_before(e.first, wave);
             if (pe < 0) continue;
@@ -909,7 +1070,7 @@ private:
     double delta(const State& st, int k, int d, int lay, int n) const {  // memory_delta :132-140
         double dl = lay * (static_cast<double>(mem_act[k]) / n);
         if (!(st.charged[gkey[k]] >> d & 1ull)) {
-            const int tp = B.mod_tp[mg(mod_of[k])];
+            const int tp = B.mod_tp[mg(mod_of[e_mod[k]])];
             dl += (1.0 + R.grad_mult) * static_cast<double>(ent_param[k]) / tp;
         }
         return dl;
@@ -922,30 +1083,31 @@ private:
             isl[d] = B.dev_island[R.dev_begin + d];
             island_mask[isl[d]] |= 1ull << d;
         }
-        cont_bytes.assign(K, 0);
-        edge_bytes.assign(K, 0);
-        mem_act.assign(K, 0);
-        ent_param.assign(K, 0);
-        gkey.assign(K, 0);
-        for (int k = 0; k < K; ++k) {
-            const int g = mg(mod_of[k]);
-            const int L = layers(mod_of[k]);  // one MetaOp per module: length == layers
+        cont_bytes.assign(KE, 0);
+        edge_bytes.assign(KE, 0);
+        mem_act.assign(KE, 0);
+        ent_param.assign(KE, 0);
+        gkey.assign(KE, 0);
+        for (int k = 0; k < KE; ++k) {  // build_memory_model / build_flow_inputs (planner.hpp:124-151)
+            const int g = mg(mod_of[e_mod[k]]);
+            const int L = layers(mod_of[e_mod[k]]);  // one MetaOp per module: length == layers
+            const double frac = e_frac[k];            // batch_fraction
             ent_param[k] = static_cast<uint64_t>(static_cast<double>(B.mod_param[g]) * L / B.mod_layers[g]);
             const uint64_t act = B.mod_act[g];
-            mem_act[k] = static_cast<uint64_t>(static_cast<double>(act) * 1.0);
-            cont_bytes[k] = static_cast<uint64_t>(static_cast<double>(act) * 1.0);
+            mem_act[k] = static_cast<uint64_t>(static_cast<double>(act) * frac);
+            cont_bytes[k] = static_cast<uint64_t>(static_cast<double>(act) * frac);
             const uint64_t edge = B.mod_out[g] == 0 ? act : B.mod_out[g];
-            edge_bytes[k] = static_cast<uint64_t>(static_cast<double>(edge) * 1.0);
+            edge_bytes[k] = static_cast<uint64_t>(static_cast<double>(edge) * frac);
             const bool whole = L == B.mod_layers[g];
             const int grp = whole ? B.mod_group[g] : -1;
             if (grp < 0)
                 gkey[k] = R.n_groups + k;
-            else if (B.mod_alias[g] >= 0 && B.mod_alias[g] < K)
-                gkey[k] = R.n_groups + B.mod_alias[g];
+            else if (!scoped && B.mod_alias[g] >= 0 && B.mod_alias[g] < K)
+                gkey[k] = R.n_groups + B.mod_alias[g];  // param_group spelled like an entity id "m<j>"
             else
                 gkey[k] = grp;
         }
-        std::vector<int> last_wave(K, -1);
+        std::vector<int> last_wave(KE, -1);
         for (std::size_t w = 0; w < waves.size(); ++w)
             for (int e : waves[w].entries) last_wave[entries[e].k] = static_cast<int>(w);
         const int nW = static_cast<int>(waves.size());
@@ -959,7 +1121,7 @@ private:
         }
         State st;
         std::fill(st.mem, st.mem + WS_MAX_DEVICES, 0.0);
-        st.charged.assign(R.n_groups + K, 0);
+        st.charged.assign(R.n_groups + KE, 0);
         const uint64_t all = N == 64 ? ~0ull : ((1ull << N) - 1);
 
         auto place_wave = [&](int w, int variant) -> bool {  // :340-406
@@ -975,10 +1137,10 @@ private:
                     for (const Incoming& f : fin[a]) va += f.bytes;
                     for (const Incoming& f : fin[b]) vb += f.bytes;
                     if (va != vb) return va > vb;
-                    return idrank[entries[order[a]].k] < idrank[entries[order[b]].k];
+                    return e_idrank[entries[order[a]].k] < e_idrank[entries[order[b]].k];
                 });
             bool first = true;
-            std::vector<char> placed_now(K, 0);
+            std::vector<char> placed_now(KE, 0);
             int cursor = R.sequential ? seq_cursor[w] : 0;
             for (std::size_t oi : idx) {
                 EntryRec& e = entries[order[oi]];
@@ -1024,8 +1186,8 @@ private:
                     s.devs = devs;
                     for (int i = 0; i < R.n_islands; ++i)
                         if (devs & island_mask[i]) s.islands++;
-                    for (int r = 0; r < K; ++r) {
-                        const int e2 = by_rank[r];
+                    for (int r = 0; r < KE; ++r) {
+                        const int e2 = e_by_rank[r];
                         if (e2 == e.k || last_wave[e2] < w || placed_now[e2]) continue;
                         const int home = latest_entry_before(e2, w);
                         if (home < 0) continue;
@@ -1121,6 +1283,26 @@ private:
     }
 
     void fill(PlanOut& out) {
+        if (scoped) {  // one record per (MetaOp, task) entity; curves are the unscaled base curves
+            for (int e = 0; e < KE; ++e) {
+                const int k = e_mod[e];
+                out.mod_of.push_back(mod_of[k]);
+                out.level.push_back(level[k]);
+                out.upper_n.push_back(0);
+                out.upper_l.push_back(0);
+                out.lower_n.push_back(0);
+                out.lower_l.push_back(0);
+                out.curve_of.push_back(mcurve[mod_of[k]].p);
+                out.scope.push_back({k, e_task[e]});
+            }
+            out.edges = e_edges;
+            out.waves = waves;
+            out.entries = entries;
+            out.flows = flows;
+            out.lower_bound = 0.0;
+            out.end_time = end_time;
+            return;
+        }
         out.mod_of = mod_of;
         out.level = level;
         out.upper_n = upper_n;
@@ -1210,10 +1392,11 @@ int wso_plan_batch(const ws_batch* in, ws_plan_result* results, uint8_t* arena, 
         r.n_pieces = npieces;
         r.lower_bound = out.lower_bound;
         r.end_time = out.end_time;
+        r.n_scopes = static_cast<int>(out.scope.size());
         std::size_t sz = al8(sizeof(ws_out_metaop) * K) + al8(sizeof(ws_out_level) * r.n_levels) +
                          al8(sizeof(ws_out_piece) * npieces) + al8(sizeof(ws_out_edge) * r.n_edges) +
                          al8(sizeof(ws_out_wave) * r.n_waves) + al8(sizeof(ws_out_entry) * r.n_entries) +
-                         al8(sizeof(ws_out_flow) * r.n_flows);
+                         al8(sizeof(ws_out_flow) * r.n_flows) + al8(sizeof(ws_out_scope) * r.n_scopes);
         if (top + sz > arena_cap) {
             r.status = WS_STATUS_INTERNAL;
             r.err_code = WS_E_ARENA_OVERFLOW;
@@ -1287,6 +1470,8 @@ int wso_plan_batch(const ws_batch* in, ws_plan_result* results, uint8_t* arena, 
             fl[f].to_metaop = out.flows[f].to_k;
             fl[f].mode = out.flows[f].mode;
         }
+        auto* sc = reinterpret_cast<ws_out_scope*>(base + off + al8(sizeof(ws_out_flow) * r.n_flows));
+        for (int e = 0; e < r.n_scopes; ++e) sc[e] = {out.scope[e].first, out.scope[e].second};
     }
     *arena_used = top;
     return rc;

@@ -111,7 +111,7 @@ class PlanResult(C.Structure):
     _fields_ = [("status", C.c_int32), ("err_code", C.c_int32), ("err_a", C.c_int64), ("err_b", C.c_int64),
                 ("err_x", C.c_double), ("err_y", C.c_double), ("n_metaops", C.c_int32), ("n_edges", C.c_int32),
                 ("n_levels", C.c_int32), ("n_waves", C.c_int32), ("n_entries", C.c_int32), ("n_flows", C.c_int32),
-                ("n_pieces", C.c_int32), ("pad", C.c_int32), ("lower_bound", C.c_double), ("end_time", C.c_double),
+                ("n_pieces", C.c_int32), ("n_scopes", C.c_int32), ("lower_bound", C.c_double), ("end_time", C.c_double),
                 ("offset", C.c_uint64), ("size", C.c_uint64)]
 
 
@@ -220,7 +220,7 @@ def make_options(**kw) -> Options:
 
 
 # plan_for_strategy selectors (cli.hpp:163-171) built on the device
-STRATEGIES = {"wavefront": 0, "decoupled-sequential": 1}
+STRATEGIES = {"wavefront": 0, "decoupled-sequential": 1, "distmm-mt": 2}
 
 
 class ProblemSet:

@@ -21,6 +21,7 @@ struct Sections {
     const ws_out_wave* wv;
     const ws_out_entry* en;
     const ws_out_flow* fl;
+    const ws_out_scope* sc;
 };
 
 Sections sections_of(const ws_plan_result& r, const std::uint8_t* arena) {
@@ -40,6 +41,8 @@ Sections sections_of(const ws_plan_result& r, const std::uint8_t* arena) {
     s.en = reinterpret_cast<const ws_out_entry*>(base + off);
     off += al8(sizeof(ws_out_entry) * r.n_entries);
     s.fl = reinterpret_cast<const ws_out_flow*>(base + off);
+    off += al8(sizeof(ws_out_flow) * r.n_flows);
+    s.sc = reinterpret_cast<const ws_out_scope*>(base + off);
     return s;
 }
 
@@ -133,11 +136,86 @@ std::vector<int> device_list(const Problem& prob, const ws_out_entry& e) {
     }
 }
 
+namespace {
+// Plan of a task-scoped baseline (distmm-mt): entities "m<k>@<task>" built
+// like detail::scoped_entity (baselines.hpp:49-55) from the MetaOp's entity.
+PlannerResult decode_scoped(const Problem& prob, const ws_plan_result& r, const Sections& s) {
+    const WorkloadSpec& spec = *prob.spec;
+    std::vector<const ModuleDecl*> mods;
+    for (const auto& kv : spec.modules) mods.push_back(&kv.second);
+    std::map<std::string, std::set<std::string>> tasks_of;  // graph.hpp:101-121
+    for (const TaskDecl& t : spec.tasks)
+        for (const FlowStep& st : t.flow)
+            for (const FlowBranch& br : st)
+                for (const std::string& m : br) tasks_of[m].insert(t.id);
+    std::vector<std::string> ids(r.n_metaops);
+    PlannerResult res;
+    ExecutionPlan& plan = res.plan;
+    plan.strategy = "distmm-mt";
+    plan.topo = *prob.topo;
+    for (int e = 0; e < r.n_metaops; ++e) {
+        const ws_out_metaop& o = s.mo[e];
+        const ModuleDecl& md = *mods[o.module];
+        const std::string& task = spec.tasks[s.sc[e].task].id;
+        ids[e] = "m" + std::to_string(s.sc[e].metaop) + "@" + task;
+        PlanEntity x;
+        x.id = ids[e];
+        x.kind = md.kind;
+        x.length = o.length;
+        x.level = o.level;
+        x.tp_degree = md.tp_degree;
+        x.global_batch = md.input.batch;
+        const std::set<std::string>& tk = tasks_of[md.kind];
+        x.batch_fraction = tk.empty() ? 1.0 : 1.0 / static_cast<double>(tk.size());  // share_fraction
+        x.param_group = o.length == md.layers ? md.param_group : "";
+        x.param_bytes = static_cast<std::uint64_t>(static_cast<double>(md.param_bytes) * o.length / md.layers);
+        x.act_bytes = md.act_bytes;
+        x.out_bytes = md.out_bytes;
+        x.w = md.flops_proxy;
+        x.c = md.comm_proxy;
+        x.task_ids = {task};
+        std::vector<CurvePiece> pieces;
+        for (int i = 0; i < o.piece_count; ++i) {
+            const ws_out_piece& p = s.pc[o.piece_begin + i];
+            pieces.push_back({p.n_lo, p.n_hi, p.alpha, p.beta_c, p.beta_w});
+        }
+        plan.curves[x.id] = ScalingCurve::from_pieces(pieces, md.comm_proxy, md.flops_proxy);
+        plan.entities[x.id] = std::move(x);
+    }
+    for (int e = 0; e < r.n_edges; ++e) plan.deps.insert({ids[s.ed[e].from], ids[s.ed[e].to]});
+    plan.lower_bound = 0.0;
+    plan.grad_opt_multiplier = prob.opt.grad_opt_multiplier;
+    for (int w = 0; w < r.n_waves; ++w) {
+        Wave wave;
+        wave.index = w;
+        wave.level = s.wv[w].level;
+        wave.start = s.wv[w].start;
+        wave.duration = s.wv[w].duration;
+        for (int i = 0; i < s.wv[w].n_entries; ++i) {
+            const ws_out_entry& e = s.en[s.wv[w].entry_begin + i];
+            wave.entries.push_back({ids[e.metaop], e.n, e.layers, e.span});
+            if (e.devmask) plan.devices[{w, ids[e.metaop]}] = device_list(prob, e);
+        }
+        plan.schedule.waves.push_back(std::move(wave));
+    }
+    plan.schedule.end_time = r.end_time;
+    static const char* kModes[3] = {"copy", "intra-island", "inter-island"};
+    for (int f = 0; f < r.n_flows; ++f) {
+        const ws_out_flow& x = s.fl[f];
+        plan.flows.push_back({x.from_wave, ids[x.from_metaop], x.to_wave, ids[x.to_metaop], x.volume, kModes[x.mode]});
+    }
+    res.schedule = plan.schedule;
+    res.predicted_makespan = r.end_time;
+    return res;
+}
+}  // namespace
+
 PlannerResult decode_result(const Problem& prob, const ws_plan_result& r, const std::uint8_t* arena,
                             bool build_graph) {
     if (r.status != WS_STATUS_OK) throw_result_error(prob, r);
     const WorkloadSpec& spec = *prob.spec;
     const Sections s = sections_of(r, arena);
+    if (r.n_scopes > 0) return decode_scoped(prob, r, s);
     std::vector<const ModuleDecl*> mods;
     for (const auto& kv : spec.modules) mods.push_back(&kv.second);
     const int K = r.n_metaops;
