@@ -32,6 +32,7 @@ struct Rec {  // sections of one plan record (ws_abi.h arena layout)
     const ws_out_wave* wv;
     const ws_out_entry* en;
     const ws_out_flow* fl;
+    const ws_out_scope* sc;  // task-scoped entities (n_scopes > 0)
 };
 
 Rec view(const ws_plan_result& r, const uint8_t* arena) {
@@ -51,10 +52,21 @@ Rec view(const ws_plan_result& r, const uint8_t* arena) {
     v.en = reinterpret_cast<const ws_out_entry*>(b + o);
     o += al8(sizeof(ws_out_entry) * r.n_entries);
     v.fl = reinterpret_cast<const ws_out_flow*>(b + o);
+    o += al8(sizeof(ws_out_flow) * r.n_flows);
+    v.sc = reinterpret_cast<const ws_out_scope*>(b + o);
     return v;
 }
 
 bool id_less(int a, int b) { return "m" + std::to_string(a) < "m" + std::to_string(b); }
+
+// "m<a>@<task a>" < "m<b>@<task b>" (task-scoped entity ids), tasks by id rank
+bool wsdev_scoped_less(int a, int ta, int b, int tb) {
+    if (a == b) return ta < tb;
+    const std::string sa = std::to_string(a), sb = std::to_string(b);
+    if (sb.size() > sa.size() && sb.compare(0, sa.size(), sa) == 0) return false;
+    if (sa.size() > sb.size() && sa.compare(0, sb.size(), sb) == 0) return true;
+    return sa < sb;
+}
 
 struct Entity {  // PlanEntity fields used by the evaluator (planner.hpp:99-122)
     int length = 0, tp = 1;
@@ -121,9 +133,19 @@ struct Eval {
             e.c = B.mod_c[gm];
             e.frac = B.mod_frac ? B.mod_frac[gm] : 1.0;
             const int grp = m.length == B.mod_layers[gm] ? B.mod_group[gm] : -1;
+            if (R.n_scopes > 0) {  // entities "m<metaop>@<task>" (baselines.hpp:49-55)
+                int users = 0;     // share_fraction: tasks routing through the module
+                for (int t = 0; t < P.n_tasks; ++t) {
+                    const int tg = P.task_begin + t;
+                    bool in = false;
+                    for (int i = 0; i < B.task_tok_n[tg]; ++i) in |= B.tokens[B.task_tok_off[tg] + i] == m.module;
+                    users += in;
+                }
+                e.frac = users ? 1.0 / users : 1.0;
+            }
             if (grp < 0)
                 e.group = "m" + std::to_string(k);
-            else if (B.mod_alias[gm] >= 0)
+            else if (B.mod_alias[gm] >= 0 && R.n_scopes == 0)
                 e.group = "m" + std::to_string(B.mod_alias[gm]);  // param_group spelled "m<j>"
             else
                 e.group = "g" + std::to_string(grp);  // no entity id starts with "g"
@@ -366,7 +388,14 @@ struct Eval {
         }
         std::vector<int> ids(K);
         for (int k = 0; k < K; ++k) ids[k] = k;
-        std::sort(ids.begin(), ids.end(), id_less);
+        if (R.n_scopes > 0) {
+            auto tr = [&](int k) { return B.task_rank[P.task_begin + V.sc[k].task]; };
+            std::sort(ids.begin(), ids.end(), [&](int a, int b) {
+                return wsdev_scoped_less(V.sc[a].metaop, tr(a), V.sc[b].metaop, tr(b));
+            });
+        } else {
+            std::sort(ids.begin(), ids.end(), id_less);
+        }
         for (int k : ids) {
             auto it = executed.find(k);
             const int done = it == executed.end() ? 0 : it->second;

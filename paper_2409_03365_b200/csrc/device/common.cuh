@@ -75,6 +75,24 @@ __host__ __device__ __forceinline__ bool dec_less(int a, int b) {
     return da < db ? a <= b / p : a / p < b;
 }
 
+// "m<a>@<task a>" < "m<b>@<task b>" as std::string (ids of the task-scoped
+// entities, baselines.hpp:49-55): the decimal spellings compare digit by
+// digit, a spelling that is a prefix of the other meets '@' > digit; equal
+// MetaOps order by task id (ta, tb: id ranks).
+__host__ __device__ __forceinline__ bool scoped_less(int a, int ta, int b, int tb) {
+    if (a == b) return ta < tb;
+    const int da = dec_digits(a), db = dec_digits(b);
+    if (da == db) return a < b;
+    int p = 1;
+    for (int i = da < db ? db - da : da - db; i; --i) p *= 10;
+    if (da < db) {
+        const int pre = b / p;
+        return pre == a ? false : a < pre;
+    }
+    const int pre = a / p;
+    return pre == b ? true : pre < b;
+}
+
 // shard_moves' island-match count (placement.hpp:88-97) in closed form for
 // islands that are contiguous device ranges.  Unit i (< M) pairs A[i] with
 // B[i mod P], A and B the sorted device lists as masks, |A| = M >= |B| = P

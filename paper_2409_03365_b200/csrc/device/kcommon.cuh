@@ -61,11 +61,24 @@ __device__ __forceinline__ double t_at(const FitOut& F, int gm, int n) {
     return __ldg(F.ttab + static_cast<int64_t>(gm) * F.tstride + (n - 1));
 }
 
+// T(n) of module gm's fitted curve with the per-device term scaled by `scale`
+// (detail::scale_curve, baselines.hpp:40-44: beta_w *= frac, then eval).
+__device__ __forceinline__ double t_scaled(const FitOut& F, const ws_batch& B, int gm, int n, double scale) {
+    const double* pc = F.pieces + 5 * F.piece_off[gm];
+    const int np = F.npieces[gm];
+    int i = 0;
+    while (i < np - 1 && !(n <= __ldg(pc + 5 * i + 1) + 1e-9)) ++i;  // locate (scaling.hpp:149-154)
+    const double bw = __ldg(pc + 5 * i + 4) * scale;
+    return __ldg(pc + 5 * i + 2) + __ldg(pc + 5 * i + 3) * B.mod_c[gm] + bw * B.mod_w[gm] / n;
+}
+
 struct TErr {  // error-capturing lookup (first error wins)
     const FitOut* F;
     const int* gm_of;    // metaop -> global module (shared)
     const int* nmax_of;  // metaop -> curve n_max (shared)
     Ctl* ctl;
+    const double* scale = nullptr;  // per MetaOp beta_w scale (task-scoped baselines), null: none
+    const ws_batch* B = nullptr;
     __device__ double operator()(int k, int n) const {
         if (n > nmax_of[k]) {
             if (!ctl->err) {
@@ -75,22 +88,22 @@ struct TErr {  // error-capturing lookup (first error wins)
             }
             return 1.0;
         }
-        return t_at(*F, gm_of[k], n);
+        return scale ? t_scaled(*F, *B, gm_of[k], n, scale[k]) : t_at(*F, gm_of[k], n);
     }
 };
 
 // ScalingCurve::inverse_exact (scaling.hpp:118-137) over fitted pieces
 __device__ __forceinline__ double inverse_exact(const double* __restrict__ pc, int np, double c, double w,
-                                                double nmax, double target) {
+                                                double nmax, double target, double scale = 1.0) {
     auto val = [&](int i, double n) {
-        return __ldg(pc + 5 * i + 2) + __ldg(pc + 5 * i + 3) * c + __ldg(pc + 5 * i + 4) * w / n;
+        return __ldg(pc + 5 * i + 2) + __ldg(pc + 5 * i + 3) * c + __ldg(pc + 5 * i + 4) * scale * w / n;
     };
     if (target <= val(np - 1, nmax)) return nmax;
     for (int i = 0; i < np; ++i) {
         const double lo = __ldg(pc + 5 * i + 0), hi = __ldg(pc + 5 * i + 1);
         const double hi_val = val(i, lo);
         const double lo_val = val(i, hi);
-        const double b = __ldg(pc + 5 * i + 4) * w;
+        const double b = __ldg(pc + 5 * i + 4) * scale * w;
         const double base = __ldg(pc + 5 * i + 2) + __ldg(pc + 5 * i + 3) * c;
         if (target > hi_val + 1e-15 * fabs(hi_val)) {
             if (b <= 0.0) return 0.0;
@@ -112,20 +125,23 @@ __device__ __forceinline__ double inverse_exact(const double* __restrict__ pc, i
 struct InvPre {
     int np;  // <= 0: generic path
     const double* pc;
-    double c, w, nmax, last;
+    double c, w, nmax, last, scale;
     double lo[2], hi[2], lov[2], thr[2], b[2], base[2];
-    __device__ __forceinline__ void init(const double* pc_, int np_, double c_, double w_, double nmax_) {
+    // scale: beta_w factor of a scaled curve (detail::scale_curve), 1.0 otherwise
+    __device__ __forceinline__ void init(const double* pc_, int np_, double c_, double w_, double nmax_,
+                                         double scale_ = 1.0) {
         pc = pc_;
         c = c_;
         w = w_;
         nmax = nmax_;
+        scale = scale_;
         if (np_ > 2) {
             np = -np_;
             return;
         }
         np = np_;
         auto val = [&](int i, double n) {
-            return __ldg(pc + 5 * i + 2) + __ldg(pc + 5 * i + 3) * c + __ldg(pc + 5 * i + 4) * w / n;
+            return __ldg(pc + 5 * i + 2) + __ldg(pc + 5 * i + 3) * c + __ldg(pc + 5 * i + 4) * scale * w / n;
         };
         last = val(np - 1, nmax);
         for (int i = 0; i < np; ++i) {
@@ -134,12 +150,12 @@ struct InvPre {
             const double hv = val(i, lo[i]);
             thr[i] = hv + 1e-15 * fabs(hv);
             lov[i] = val(i, hi[i]);
-            b[i] = __ldg(pc + 5 * i + 4) * w;
+            b[i] = __ldg(pc + 5 * i + 4) * scale * w;
             base[i] = __ldg(pc + 5 * i + 2) + __ldg(pc + 5 * i + 3) * c;
         }
     }
     __device__ __forceinline__ double operator()(double target) const {
-        if (np <= 0) return inverse_exact(pc, -np, c, w, nmax, target);
+        if (np <= 0) return inverse_exact(pc, -np, c, w, nmax, target, scale);
         if (target <= last) return nmax;
 #pragma unroll
         for (int i = 0; i < 2; ++i) {

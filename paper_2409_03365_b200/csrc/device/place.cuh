@@ -435,9 +435,11 @@ __device__ void p_emit(PCtx& C, int p, const char* rec, const RecLayout& RL, con
     npieces = warp_sum(npieces);
     nedges = warp_sum(nedges);
     const int nL = h.n_levels, nW = h.nW, nE = h.nE, nF = C.nF;
+    const int nS = h.scoped ? K : 0;  // (MetaOp, task) of each entity
     const uint64_t sz = al8(sizeof(ws_out_metaop) * K) + al8(sizeof(ws_out_level) * nL) +
                         al8(sizeof(ws_out_piece) * npieces) + al8(sizeof(ws_out_edge) * nedges) +
-                        al8(sizeof(ws_out_wave) * nW) + al8(sizeof(ws_out_entry) * nE) + al8(sizeof(ws_out_flow) * nF);
+                        al8(sizeof(ws_out_wave) * nW) + al8(sizeof(ws_out_entry) * nE) + al8(sizeof(ws_out_flow) * nF) +
+                        al8(sizeof(ws_out_scope) * nS);
     unsigned long long off = 0;
     if (lane == 0) off = atomicAdd(A.arena_top, static_cast<unsigned long long>(sz));
     off = __shfl_sync(kFull, off, 0);
@@ -558,6 +560,12 @@ __device__ void p_emit(PCtx& C, int p, const char* rec, const RecLayout& RL, con
         x.pad = 0;
         fl[f] = x;
     }
+    if (nS) {
+        auto* sc = reinterpret_cast<ws_out_scope*>(base + o + al8(sizeof(ws_out_flow) * nF));
+        const int* r_met = reinterpret_cast<const int*>(rec + RL.e_met);
+        const int* r_task = reinterpret_cast<const int*>(rec + RL.e_task);
+        for (int k = lane; k < nS; k += 32) sc[k] = ws_out_scope{r_met[k], r_task[k]};
+    }
     if (lane == 0) {
         ws_plan_result r{};
         r.status = WS_STATUS_OK;
@@ -568,6 +576,7 @@ __device__ void p_emit(PCtx& C, int p, const char* rec, const RecLayout& RL, con
         r.n_entries = nE;
         r.n_flows = nF;
         r.n_pieces = npieces;
+        r.n_scopes = nS;
         r.lower_bound = h.lower_bound;
         r.end_time = h.end_time;
         r.offset = off;
@@ -628,6 +637,7 @@ __global__ void __launch_bounds__(32 * kPlaceWarps, WS_PLACE_MINB) k_place(Place
     const int* r_by_rank = reinterpret_cast<const int*>(rec + A.RL.by_rank);
     const int* r_idrank = reinterpret_cast<const int*>(rec + A.RL.idrank);
     const uint64_t* r_pred = reinterpret_cast<const uint64_t*>(rec + A.RL.pred_r);
+    const double* r_frac = reinterpret_cast<const double*>(rec + A.RL.e_frac);
     int* by_rank = C.at<int>(L.by_rank);
     int* idrank = C.at<int>(L.idrank);
     int* lastw = C.at<int>(L.lastw);
@@ -648,12 +658,13 @@ __global__ void __launch_bounds__(32 * kPlaceWarps, WS_PLACE_MINB) k_place(Place
         const int Lk = B.mod_layers[gm];  // one MetaOp per module: length == layers
         parb[k] = static_cast<uint64_t>(static_cast<double>(B.mod_param[gm]) * Lk / B.mod_layers[gm]);
         const uint64_t act = B.mod_act[gm];
-        memact[k] = static_cast<uint64_t>(static_cast<double>(act) * 1.0);
-        contb[k] = static_cast<uint64_t>(static_cast<double>(act) * 1.0);
+        const double frac = r_frac[k];  // batch_fraction (build_memory_model / build_flow_inputs)
+        memact[k] = static_cast<uint64_t>(static_cast<double>(act) * frac);
+        contb[k] = static_cast<uint64_t>(static_cast<double>(act) * frac);
         const uint64_t edge = B.mod_out[gm] == 0 ? act : B.mod_out[gm];
-        edgeb[k] = static_cast<uint64_t>(static_cast<double>(edge) * 1.0);
+        edgeb[k] = static_cast<uint64_t>(static_cast<double>(edge) * frac);
         const int grp = (Lk == B.mod_layers[gm]) ? B.mod_group[gm] : -1;
-        const int al = B.mod_alias[gm];
+        const int al = h.scoped ? -1 : B.mod_alias[gm];  // scoped ids "m<k>@<task>" match no param_group
         gkey[k] = grp < 0 ? R.n_groups + k : ((al >= 0 && al < K) ? R.n_groups + al : grp);
         tpk[k] = B.mod_tp[gm];
         home[k] = -1;

@@ -109,34 +109,40 @@ __global__ void k_best(const ws_plan_result* res, const ws_sim_result* sim, int 
 struct LaunchCaps {
     RecCaps rec;
     PlaceCaps pl;
-    int M;
+    int M;        // modules (MetaOps) per plan
+    bool scoped;  // the batch has task-scoped baseline plans
 };
 
 LaunchCaps batch_caps(const ws_plan_rec* plans, int P, bool hard) {
     int M = 1, N = 1, IS = 1, gmax = 0;
+    bool scoped = false;
     for (int p = 0; p < P; ++p) {
         const ws_plan_rec& r = plans[p];
         M = std::max(M, r.n_mod);
         N = std::max(N, r.n_dev);
         IS = std::max(IS, r.n_islands);
         gmax = std::max(gmax, r.n_groups);
+        scoped |= r.strategy == WS_STRATEGY_DISTMM_MT;
     }
     M = std::min(M, WS_MAX_MODULES);
     N = std::min(N, WS_MAX_DEVICES);
     IS = std::min(IS, N);
-    const int W = std::min(WS_MAX_WAVES, 2 * M + 1);  // each wave drains a tuple
+    // placement entities: the MetaOps, or up to 64 (MetaOp, task) pairs
+    const int ME = scoped ? WS_MAX_MODULES : M;
+    const int W = std::min(WS_MAX_WAVES, 2 * ME + 1);  // each wave drains a tuple
     int E, F;
     if (hard) {
-        E = std::min(WS_MAX_ENTRIES, std::max(64, 2 * M * M));
+        E = std::min(WS_MAX_ENTRIES, std::max(64, 2 * ME * ME));
         F = WS_MAX_FLOWS;
     } else {
-        E = std::max(32, 4 * M);
-        F = std::max(64, 8 * M);
+        E = std::max(32, 4 * ME);
+        F = std::max(64, 8 * ME);
     }
     LaunchCaps c;
     c.M = M;
-    c.rec = RecCaps{M, W, E};
-    c.pl = PlaceCaps{M, N, W, E, F, gmax + M, IS};
+    c.scoped = scoped;
+    c.rec = RecCaps{ME, W, E};
+    c.pl = PlaceCaps{ME, N, W, E, F, gmax + ME, IS};
     return c;
 }
 
@@ -274,7 +280,8 @@ int launch_pair(ws_ctx* ctx, cudaStream_t st, const LaunchCaps& lc, const FitOut
     S.fit = fo;
     S.caps = lc.rec;
     S.RL = make_rec_layout(lc.rec);
-    S.SL = make_sm_layout(lc.M);
+    S.SL = make_sm_layout(lc.M, lc.scoped);
+    S.scoped_ok = lc.scoped ? 1 : 0;
     S.recs = recs;
     S.n_ids = n_ids;
     S.rec_by_slot = by_slot ? 1 : 0;
@@ -723,7 +730,7 @@ int ws_simulate_staged(ws_ctx* ctx, const ws_sim_opts* opts, void* stream) {
     A.plans = ctx->results.as<ws_plan_result>();
     A.parena = ctx->arena.as<uint8_t>();
     A.opt = opts ? *opts : ws_sim_opts{2.0, 0, 0};
-    A.caps = SimCaps{lh.pl.G, lh.rec.W, lh.pl.IS, lh.M, lh.rec.E};
+    A.caps = SimCaps{lh.pl.G, lh.rec.W, lh.pl.IS, lh.rec.M, lh.rec.E};
     A.SL = make_sim_layout(A.caps);
     A.n_plans = P;
     if (!ctx->sim_res.ensure(sizeof(ws_sim_result) * std::max(P, 1)) || !ctx->sim_arena.ensure(ctx->sim_cap) ||

@@ -12,7 +12,7 @@ constexpr int kSchedWarps = 4;
 // ---- per-plan schedule record (global), written by k_sched, read by k_place
 struct SchedHdr {
     int ok, K, n_levels, nW;
-    int nE, pad0, pad1, pad2;
+    int nE, scoped, pad1, pad2;  // scoped: entities are (MetaOp, task) pairs (e_met/e_task)
     double lower_bound, end_time;
 };
 
@@ -22,6 +22,7 @@ struct RecCaps {
 
 struct RecLayout {
     int hdr, mod_of, level, up_n, up_l, lo_n, lo_l, by_rank, idrank, pred_r, succ_r, cstar, lvl_fw, lvl_nw;
+    int e_frac, e_met, e_task;  // per entity: batch_fraction, MetaOp, task (-1: the MetaOp itself)
     int w_level, w_eb, w_ec, w_start, w_dur, e_k, e_n, e_l, e_span;
     int bytes;
 };
@@ -50,6 +51,9 @@ __host__ __device__ inline RecLayout make_rec_layout(const RecCaps& c) {
     L.cstar = take(8 * c.M);
     L.lvl_fw = take(4 * c.M);
     L.lvl_nw = take(4 * c.M);
+    L.e_frac = take(8 * c.M);
+    L.e_met = take(4 * c.M);
+    L.e_task = take(4 * c.M);
     L.w_level = take(4 * c.W);
     L.w_eb = take(4 * c.W);
     L.w_ec = take(4 * c.W);
@@ -72,10 +76,13 @@ struct SmLayout {
     int cstar_sm, aerr_x, aerr_y, aerr;                                      // [M] per level
     int tk, tn, tl, tn2, sel, best, pool, klay;                              // [2M]
     int ord;                                                                 // [3*2M]
+    // task-scoped baselines only (sizes 0 otherwise)
+    int ent_met, ent_task, ent_frac, epred;                                  // [64] entities
+    int ent_of, kscale, tlvl, vord;                                          // [M] per task
     int bytes;
 };
 
-__host__ __device__ inline SmLayout make_sm_layout(int M) {
+__host__ __device__ inline SmLayout make_sm_layout(int M, bool scoped = false) {
     SmLayout L{};
     int o = 0;
     auto take = [&](int b) {
@@ -123,6 +130,15 @@ __host__ __device__ inline SmLayout make_sm_layout(int M) {
     L.pool = take(4 * T);
     L.klay = take(4 * T);
     L.ord = take(4 * 3 * T);
+    const int EM = scoped ? WS_MAX_MODULES : 0, MS = scoped ? M : 0;
+    L.ent_met = take(4 * EM);
+    L.ent_task = take(4 * EM);
+    L.ent_frac = take(8 * EM);
+    L.epred = take(8 * EM);
+    L.ent_of = take(4 * MS);
+    L.kscale = take(8 * MS);
+    L.tlvl = take(4 * MS);
+    L.vord = take(4 * MS);
     L.bytes = (o + 15) & ~15;
     return L;
 }
@@ -139,6 +155,7 @@ struct SchedArgs {
     int n_launch;
     int rec_by_slot;         // retry pass: records indexed by launch slot
     int M_cap;               // modules per plan this launch supports
+    int scoped_ok;           // SL carries the task-scoped working set (distmm-mt plans)
     ws_plan_result* results;
 };
 
@@ -150,11 +167,18 @@ struct SCtx {
     char* sm;
     Ctl* ctl;
     int lane, N, M, K, mbase;
+    const double* kscale = nullptr;  // per-MetaOp beta_w scale while a scaled level runs (distmm-mt)
     template <typename T>
     __device__ __forceinline__ T* at(int off) const {
         return reinterpret_cast<T*>(sm + off);
     }
 };
+
+// T_k(n): the T-table, or the scaled curve of a task-scoped baseline level
+__device__ __forceinline__ double T_of(const SCtx& C, int k, int n) {
+    const int gm = C.at<int>(C.L->gm_of)[k];
+    return C.kscale ? t_scaled(*C.F, *C.B, gm, n, C.kscale[k]) : t_at(*C.F, gm, n);
+}
 
 // ---------------------------------------------------------------------------
 // (1) module DAG from the flows (graph.hpp:97-147), lexicographic Kahn and
@@ -454,9 +478,11 @@ __device__ __forceinline__ double ordered_sum(double v0, double v1, int w) {
     return total;
 }
 
-// repair_capacity (allocation.hpp:107-139) for one level; lane i holds members i, i+32
+// repair_capacity (allocation.hpp:107-139) for one level; lane i holds members
+// i, i+32.  Ties and the first error go by MetaOp id (plan.tuples is an id map).
 __device__ bool s_level_repair(SCtx& C, int lvl) {
     const int N = C.N, lane = C.lane;
+    const int* idrank = C.at<int>(C.L->idrank);
     const int* lb = C.at<int>(C.L->lvl_begin);
     const int* lm = C.at<int>(C.L->lvl_mem) + lb[lvl];
     const int w = lb[lvl + 1] - lb[lvl];
@@ -477,10 +503,11 @@ __device__ bool s_level_repair(SCtx& C, int lvl) {
         }
         if (warp_sum(wid) <= N) break;
         double best_pen = 0.0;
-        int best_i = 0x7fffffff, best_t = 0, eidx = 0x7fffffff;
+        int best_i = 0x7fffffff, best_key = 0x7fffffff, best_t = 0, eidx = 0x7fffffff;
         double ex = 0, ey = 0;
         for (int i = lane; i < w; i += 32) {
             const int k = lm[i];
+            const int key = idrank[k];
             const int un = up_n[k];
             const uint64_t below = valid[k] & ((1ull << (un - 1)) - 1ull);  // valid values < un
             if (!below) continue;
@@ -488,15 +515,16 @@ __device__ bool s_level_repair(SCtx& C, int lvl) {
             if (lo_l[k] && target <= lo_n[k]) continue;
             const int nmax = nmax_of[k];
             if (target > nmax || un > nmax) {  // eval(target) first, then eval(t.n)
-                if (i < eidx) eidx = i, ex = target > nmax ? target : un, ey = nmax;
+                if (key < eidx) eidx = key, ex = target > nmax ? target : un, ey = nmax;
                 continue;
             }
-            const double pen = up_l[k] * (t_at(F, gm_of[k], target) - t_at(F, gm_of[k], un));
-            if (best_i == 0x7fffffff || pen < best_pen) best_pen = pen, best_i = i, best_t = target;
+            const double pen = up_l[k] * (T_of(C, k, target) - T_of(C, k, un));
+            if (best_i == 0x7fffffff || pen < best_pen || (pen == best_pen && key < best_key))
+                best_pen = pen, best_i = i, best_key = key, best_t = target;
         }
         const int emin = warp_min_i(eidx);
         if (emin != 0x7fffffff) {
-            const int src = emin & 31;
+            const int src = __ffs(__ballot_sync(kFull, eidx == emin)) - 1;
             const double xx = shfl_d(ex, src), yy = shfl_d(ey, src);
             if (lane == 0) {
                 C.ctl->err = WS_E_EVAL_RANGE;
@@ -506,12 +534,13 @@ __device__ bool s_level_repair(SCtx& C, int lvl) {
             __syncwarp();
             return false;
         }
-        for (int off = 16; off; off >>= 1) {  // argmin over (penalty, member index)
+        for (int off = 16; off; off >>= 1) {  // argmin over (penalty, MetaOp id)
             const double op = __shfl_xor_sync(kFull, best_pen, off);
             const int oi = __shfl_xor_sync(kFull, best_i, off);
+            const int okey = __shfl_xor_sync(kFull, best_key, off);
             const int ot = __shfl_xor_sync(kFull, best_t, off);
-            if (oi != 0x7fffffff && (best_i == 0x7fffffff || op < best_pen || (op == best_pen && oi < best_i)))
-                best_pen = op, best_i = oi, best_t = ot;
+            if (oi != 0x7fffffff && (best_i == 0x7fffffff || op < best_pen || (op == best_pen && okey < best_key)))
+                best_pen = op, best_i = oi, best_key = okey, best_t = ot;
         }
         if (best_i == 0x7fffffff) break;
         if (lane == 0) up_n[lm[best_i]] = best_t;
@@ -522,9 +551,11 @@ __device__ bool s_level_repair(SCtx& C, int lvl) {
 
 // bi-point discretization of one MetaOp (allocation.hpp:149-214).  Returns
 // false on OutOfRange (x = n, y = n_max; eval(n_over) is evaluated first).
+// scale: non-null for a scaled curve (T evaluated from the pieces, not the T-table)
 __device__ __forceinline__ bool discretize_one(const FitOut& F, const ws_plan_rec& R, int gm, int L, double nmax,
                                                uint64_t v, double nstar, double cs, int& un, int& ul, int& ln,
-                                               int& ll, double& ex) {
+                                               int& ll, double& ex, const ws_batch* B = nullptr,
+                                               double scale = 1.0) {
     int exact = -1, n_over = -1, n_under = -1;
     for (uint64_t b = v; b; b &= b - 1) {
         const int x = low_bit(b) + 1;
@@ -554,8 +585,8 @@ __device__ __forceinline__ bool discretize_one(const FitOut& F, const ws_plan_re
             ex = n_over > nmax ? n_over : n_under;
             return false;
         }
-        const double t_over = t_at(F, gm, n_over);
-        const double t_under = t_at(F, gm, n_under);
+        const double t_over = B ? t_scaled(F, *B, gm, n_over, scale) : t_at(F, gm, n_over);
+        const double t_under = B ? t_scaled(F, *B, gm, n_under, scale) : t_at(F, gm, n_under);
         if (t_under - t_over <= 0.0) {
             un = n_under;
         } else {
@@ -620,7 +651,8 @@ __device__ bool s_level_alloc(SCtx& C, int lvl, double& c_star_out) {
             q.gm = gm_of[q.k];
             q.L = Lk[q.k];
             q.nmax = nmax_of[q.k];
-            q.inv.init(F.pieces + 5 * F.piece_off[q.gm], F.npieces[q.gm], B.mod_c[q.gm], B.mod_w[q.gm], q.nmax);
+            q.inv.init(F.pieces + 5 * F.piece_off[q.gm], F.npieces[q.gm], B.mod_c[q.gm], B.mod_w[q.gm], q.nmax,
+                       C.kscale ? C.kscale[q.k] : 1.0);
         }
     }
     // bracket [max T(min(N,nmax))*L, sum T(1)*L] (allocation.hpp:75-80)
@@ -629,9 +661,9 @@ __device__ bool s_level_alloc(SCtx& C, int lvl, double& c_star_out) {
         const Mem& q = mem[s];
         if (q.k < 0) continue;
         const double ncap = (q.nmax < nd) ? q.nmax : nd;
-        const double v = t_at(F, q.gm, static_cast<int>(ncap)) * q.L;
+        const double v = T_of(C, q.k, static_cast<int>(ncap)) * q.L;
         lo0 = (lo0 < v) ? v : lo0;
-        hi0[s] = t_at(F, q.gm, 1) * q.L;
+        hi0[s] = T_of(C, q.k, 1) * q.L;
     }
     double c_lo = warp_max_nonneg(lo0);
     double c_hi = ordered_sum(hi0[0], hi0[1], w);
@@ -658,8 +690,9 @@ __device__ bool s_level_alloc(SCtx& C, int lvl, double& c_star_out) {
         if (q.k < 0) continue;
         int un, ul, ln, ll;
         double ex;
-        if (!discretize_one(F, R, q.gm, q.L, q.nmax, valid[q.k], probe_term(q, cs), cs, un, ul, ln, ll, ex)) {
-            const int idx = lane + 32 * s;
+        if (!discretize_one(F, R, q.gm, q.L, q.nmax, valid[q.k], probe_term(q, cs), cs, un, ul, ln, ll, ex,
+                            C.kscale ? &B : nullptr, C.kscale ? C.kscale[q.k] : 1.0)) {
+            const int idx = C.at<int>(C.L->idrank)[q.k];  // first failure in MetaOp id order
             if (idx < eidx0) eidx0 = idx, ex0 = ex, ey0 = q.nmax;
             continue;
         }
@@ -671,7 +704,7 @@ __device__ bool s_level_alloc(SCtx& C, int lvl, double& c_star_out) {
     {
         const int emin = warp_min_i(eidx0);
         if (emin != 0x7fffffff) {
-            const int src = emin & 31;
+            const int src = __ffs(__ballot_sync(kFull, eidx0 == emin)) - 1;
             const double xx = shfl_d(ex0, src), yy = shfl_d(ey0, src);
             if (lane == 0) {
                 C.ctl->err = WS_E_EVAL_RANGE;
@@ -976,8 +1009,8 @@ __device__ __forceinline__ int warp_argmax_rem(bool cand, double rem, int idr) {
 // extend_resources_if_needed (schedule.hpp:144-173), lanes = selected tuples:
 // grow the tuple whose MetaOp has the most remaining time to its next valid
 // allocation while idle devices remain.
-__device__ __forceinline__ int ext_lanes(bool in, int n, int N, uint64_t vmask, int sl, int idr, const FitOut& F,
-                                         int gm) {
+__device__ __forceinline__ int ext_lanes(bool in, int n, int N, uint64_t vmask, int sl, int idr, const SCtx& C,
+                                         int k) {
     const int lane = threadIdx.x & 31;
     while (true) {
         const int idle = N - static_cast<int>(__reduce_add_sync(kFull, in ? static_cast<unsigned>(n) : 0u));
@@ -991,7 +1024,7 @@ __device__ __forceinline__ int ext_lanes(bool in, int n, int N, uint64_t vmask, 
                 nx = low_bit(above) + 1;
                 if (nx - n <= idle) {
                     cand = true;
-                    rem = sl * t_at(F, gm, n);
+                    rem = sl * T_of(C, k, n);
                 }
             }
         }
@@ -1022,7 +1055,7 @@ __device__ int fast_wave(SCtx& C, SchedView& S) {
     const int idr = mine ? S.idrank[k] : 0;
     const uint64_t vmask = mine ? S.valid[k] : 0;
     const int gm = mine ? gm_of[k] : 0;
-    const double T0 = mine ? t_at(F, gm, n0) : 0.0;
+    const double T0 = mine ? T_of(C, k, n0) : 0.0;
     const double tt = tl * T0;  // tuple_time
     const double rt = sl * T0;  // metaop_remaining_time at own n
     // stable ranks under the three comparators
@@ -1076,7 +1109,7 @@ __device__ int fast_wave(SCtx& C, SchedView& S) {
         }
         // scratch extension (schedule.hpp:126-131)
         const bool in = (sel >> lane) & 1u;
-        const int n = ext_lanes(in, n0, N, vmask, sl, idr, F, gm);
+        const int n = ext_lanes(in, n0, N, vmask, sl, idr, C, k);
         const int usedn = static_cast<int>(__reduce_add_sync(kFull, in ? static_cast<unsigned>(n) : 0u));
         const long long key = static_cast<long long>(usedn) * 1000 + ns;
         if (key > best_key) {
@@ -1093,10 +1126,10 @@ __device__ int fast_wave(SCtx& C, SchedView& S) {
     }
     // real extension on the chosen set
     const bool in = (best_sel >> lane) & 1u;
-    const int n = ext_lanes(in, n0, N, vmask, sl, idr, F, gm);
+    const int n = ext_lanes(in, n0, N, vmask, sl, idr, C, k);
     if (mine) S.tn[lane] = n;
     // align_time_span: t_wave = min span over the chosen set
-    const double per = in ? t_at(F, gm, n) : 0.0;
+    const double per = in ? T_of(C, k, n) : 0.0;
     const double span = in ? sl * per : 0.0;
     const double t_wave = warp_min_nonneg(in ? span : __longlong_as_double(0x7ff0000000000000ll));
     if (in) {
@@ -1234,7 +1267,7 @@ __device__ bool s_schedule_level(SCtx& C, char* rec, const RecLayout& RL, int lv
     S.idrank = C.at<int>(C.L->idrank);
     S.valid = C.at<uint64_t>(C.L->valid);
     S.N = C.N;
-    S.T = TErr{C.F, C.at<int>(C.L->gm_of), nmax_of, C.ctl};
+    S.T = TErr{C.F, C.at<int>(C.L->gm_of), nmax_of, C.ctl, C.kscale, C.B};
     int* w_level = reinterpret_cast<int*>(rec + RL.w_level);
     int* w_eb = reinterpret_cast<int*>(rec + RL.w_eb);
     int* w_ec = reinterpret_cast<int*>(rec + RL.w_ec);
@@ -1290,7 +1323,7 @@ __device__ bool s_schedule_level(SCtx& C, char* rec, const RecLayout& RL, int lv
             const int t = best[lane];
             const int k = S.tk[t];
             const int kk = klay[lane];
-            span = kk * t_at(*C.F, S.T.gm_of[k], S.tn[t]);
+            span = kk * T_of(C, k, S.tn[t]);
             e_k[nE + lane] = k;
             e_n[nE + lane] = S.tn[t];
             e_l[nE + lane] = kk;
@@ -1351,6 +1384,194 @@ __device__ bool s_schedule_level(SCtx& C, char* rec, const RecLayout& RL, int lv
 }
 
 // WS_SCHED_MINB: optional resident-blocks target for register tuning builds
+// plan_distmm_mt (baselines.hpp:323-413): tasks in declaration order; inside
+// a task (task_view: members, in-task edges, lexicographic topological order,
+// longest-path task levels), a level of one MetaOp runs alone on its largest
+// valid allocation, a wider level splits the cluster through the level
+// machinery (s_level_alloc + s_schedule_level) on curves whose per-device term
+// is scaled by the share fraction 1/|tasks|; entities are (MetaOp, task) pairs.
+__device__ bool s_distmm(SCtx& C, char* rec, const RecLayout& RL, int& nW, int& nE, double& end_time, int W_CAP,
+                         int E_CAP, int& KE_out) {
+    const ws_batch& B = *C.B;
+    const ws_plan_rec& R = *C.R;
+    const int K = C.K, N = C.N, lane = C.lane;
+    const int* by_rank = C.at<int>(C.L->by_rank);
+    const int* idrank = C.at<int>(C.L->idrank);
+    const int* gm_of = C.at<int>(C.L->gm_of);
+    const int* nmax_of = C.at<int>(C.L->nmax_of);
+    const int* Lk = C.at<int>(C.L->Lk);
+    const int* mod_of = C.at<int>(C.L->mod_of);
+    const uint64_t* pred_r = C.at<uint64_t>(C.L->pred_r);
+    const uint64_t* valid = C.at<uint64_t>(C.L->valid);
+    const uint64_t* tmask = C.at<uint64_t>(C.L->tmask);
+    int* ent_met = C.at<int>(C.L->ent_met);
+    int* ent_task = C.at<int>(C.L->ent_task);
+    double* ent_frac = C.at<double>(C.L->ent_frac);
+    uint64_t* epred = C.at<uint64_t>(C.L->epred);
+    int* ent_of = C.at<int>(C.L->ent_of);
+    double* kscale = C.at<double>(C.L->kscale);
+    int* tlvl = C.at<int>(C.L->tlvl);
+    int* vord = C.at<int>(C.L->vord);
+    int* lb = C.at<int>(C.L->lvl_begin);
+    int* lm = C.at<int>(C.L->lvl_mem);
+    int* w_level = reinterpret_cast<int*>(rec + RL.w_level);
+    int* w_eb = reinterpret_cast<int*>(rec + RL.w_eb);
+    int* w_ec = reinterpret_cast<int*>(rec + RL.w_ec);
+    double* w_start = reinterpret_cast<double*>(rec + RL.w_start);
+    double* w_dur = reinterpret_cast<double*>(rec + RL.w_dur);
+    int* e_k = reinterpret_cast<int*>(rec + RL.e_k);
+    int* e_n = reinterpret_cast<int*>(rec + RL.e_n);
+    int* e_l = reinterpret_cast<int*>(rec + RL.e_l);
+    double* e_span = reinterpret_cast<double*>(rec + RL.e_span);
+    int KE = 0;
+    double now = 0.0;
+    for (int e = lane; e < WS_MAX_MODULES; e += 32) epred[e] = 0;
+    for (int t = 0; t < R.n_tasks; ++t) {
+        const int tr = B.task_rank[R.task_begin + t];
+        int nm = 0, maxl = 0;
+        if (lane == 0) {  // task_view (baselines.hpp:62-73): members in topological order, task levels
+            uint64_t memr = 0;  // members as id-rank bits
+            for (int k = 0; k < K; ++k) {
+                ent_of[k] = -1;
+                if (tmask[mod_of[k]] >> tr & 1ull) memr |= 1ull << idrank[k];
+            }
+            int* indeg = C.at<int>(C.L->absorb);
+            uint64_t ready = 0;
+            for (uint64_t b = memr; b; b &= b - 1) {
+                const int k = by_rank[low_bit(b)];
+                indeg[k] = popc64(pred_r[k] & memr);
+                if (!indeg[k]) ready |= 1ull << idrank[k];
+            }
+            const uint64_t* succ_r = C.at<uint64_t>(C.L->succ_r);
+            while (ready) {
+                const int r = low_bit(ready);
+                ready &= ready - 1;
+                const int k = by_rank[r];
+                vord[nm++] = k;
+                int lv = 0;
+                for (uint64_t p = pred_r[k] & memr; p; p &= p - 1) {
+                    const int q = tlvl[by_rank[low_bit(p)]] + 1;
+                    lv = q > lv ? q : lv;
+                }
+                tlvl[k] = lv;
+                maxl = lv > maxl ? lv : maxl;
+                for (uint64_t sr = succ_r[k] & memr; sr; sr &= sr - 1) {
+                    const int q = by_rank[low_bit(sr)];
+                    if (--indeg[q] == 0) ready |= 1ull << idrank[q];
+                }
+            }
+        }
+        nm = __shfl_sync(kFull, nm, 0);
+        maxl = __shfl_sync(kFull, maxl, 0);
+        __syncwarp();
+        for (int l = 0; l <= maxl; ++l) {
+            int w = 0;
+            if (lane == 0) {  // the level's MetaOps in task order; their entities and scaled curves
+                for (int i = 0; i < nm; ++i) {
+                    const int k = vord[i];
+                    if (tlvl[k] != l) continue;
+                    lm[w++] = k;
+                    if (ent_of[k] < 0) {
+                        if (KE >= WS_MAX_MODULES) {
+                            set_err(C.ctl, WS_E_LIMIT_MODULES);
+                            break;
+                        }
+                        ent_met[KE] = k;
+                        ent_task[KE] = t;
+                        ent_frac[KE] = 1.0 / static_cast<double>(popc64(tmask[mod_of[k]]));  // share_fraction
+                        ent_of[k] = KE++;
+                    }
+                    kscale[k] = ent_frac[ent_of[k]];
+                    const int tp = B.mod_tp[gm_of[k]];
+                    if (tp > N) {  // valid_allocations (allocation.hpp:51-54)
+                        set_err(C.ctl, WS_E_TP_EXCEEDS, k, tp);
+                        break;
+                    }
+                }
+                lb[0] = 0;
+                lb[1] = w;
+            }
+            w = __shfl_sync(kFull, w, 0);
+            KE = __shfl_sync(kFull, KE, 0);
+            __syncwarp();
+            if (C.ctl->err) return false;
+            if (w == 0) continue;
+            if (w == 1) {
+                if (lane == 0) {
+                    const int k = lm[0];
+                    const int n = 64 - __clzll(static_cast<long long>(valid[k]));  // valid.back()
+                    if (n > nmax_of[k]) {  // scaled.eval(n) OutOfRange (scaling.hpp:66-68)
+                        C.ctl->err = WS_E_EVAL_RANGE;
+                        C.ctl->x = n;
+                        C.ctl->y = nmax_of[k];
+                    } else if (nW + 1 > W_CAP || nE + 1 > E_CAP) {
+                        set_err(C.ctl, nW + 1 > W_CAP ? WS_E_LIMIT_WAVES : WS_E_LIMIT_ENTRIES);
+                    } else {
+                        const double span = Lk[k] * t_scaled(*C.F, B, gm_of[k], n, kscale[k]);
+                        w_level[nW] = l;
+                        w_eb[nW] = nE;
+                        w_ec[nW] = 1;
+                        w_start[nW] = now;
+                        w_dur[nW] = span;
+                        e_k[nE] = ent_of[k];
+                        e_n[nE] = n;
+                        e_l[nE] = Lk[k];
+                        e_span[nE] = span;
+                        now += span;
+                    }
+                }
+                __syncwarp();
+                if (C.ctl->err) return false;
+                ++nW;
+                ++nE;
+                continue;
+            }
+            C.kscale = kscale;
+            double cs = 0.0;
+            bool ok = s_level_alloc(C, 0, cs);  // sums in task order (LevelInput order)
+            if (ok) {
+                if (lane == 0)  // discretized tuples / schedule_level go by MetaOp id
+                    for (int i = 1; i < w; ++i) {
+                        const int v = lm[i];
+                        int j = i;
+                        while (j > 0 && idrank[lm[j - 1]] > idrank[v]) lm[j] = lm[j - 1], --j;
+                        lm[j] = v;
+                    }
+                __syncwarp();
+                const int w0 = nW, e0 = nE;
+                double level_end = now;
+                ok = s_schedule_level(C, rec, RL, 0, nW, nE, now, level_end, W_CAP, E_CAP);
+                if (ok && lane == 0) {
+                    double t_end = 0.0;  // schedule_level's own clock, from 0
+                    for (int x = w0; x < nW; ++x) {
+                        w_level[x] = l;
+                        t_end += w_dur[x];
+                    }
+                    for (int x = e0; x < nE; ++x) e_k[x] = ent_of[e_k[x]];
+                    now += t_end;
+                }
+            }
+            C.kscale = nullptr;
+            now = __shfl_sync(kFull, now, 0);
+            __syncwarp();
+            if (!ok) return false;
+        }
+        if (lane == 0)  // the task's edges between its entities (deps, scoped)
+            for (int i = 0; i < nm; ++i) {
+                const int k = vord[i];
+                const uint64_t* succ_r = C.at<uint64_t>(C.L->succ_r);
+                for (uint64_t sr = succ_r[k]; sr; sr &= sr - 1) {
+                    const int q = by_rank[low_bit(sr)];
+                    if (ent_of[q] >= 0) epred[ent_of[q]] |= 1ull << ent_of[k];
+                }
+            }
+        __syncwarp();
+    }
+    end_time = now;
+    KE_out = KE;
+    return true;
+}
+
 #ifdef WS_SCHED_MINB
 __global__ void __launch_bounds__(32 * kSchedWarps, WS_SCHED_MINB) k_sched(SchedArgs A) {
 #else
@@ -1398,12 +1619,20 @@ __global__ void __launch_bounds__(32 * kSchedWarps) k_sched(SchedArgs A) {
     WS_PH_STOP(tg, 10);
     if (ok) ok = s_fit_status(C);
     const bool decoupled = R.strategy == WS_STRATEGY_DECOUPLED_SEQUENTIAL;
-    if (ok) ok = s_valid(C, !decoupled);
+    const bool scoped = R.strategy == WS_STRATEGY_DISTMM_MT;
+    if (ok && scoped && !A.scoped_ok) {  // launch built without the task-scoped working set
+        ok = false;
+        if (lane == 0) ctl->err = WS_E_LIMIT_MODULES;
+        __syncwarp();
+    }
+    if (ok) ok = s_valid(C, !decoupled && !scoped);
     WS_PH_STOP(tg, 11);
-    int n_levels = 0, nW = 0, nE = 0;
+    int n_levels = 0, nW = 0, nE = 0, KE = 0;
     double lower_bound = 0.0, offset = 0.0;
     if (ok && decoupled) {
         ok = s_decoupled(C, rec, A.RL, nW, nE, offset, A.caps.W, A.caps.E);
+    } else if (ok && scoped) {
+        ok = s_distmm(C, rec, A.RL, nW, nE, offset, A.caps.W, A.caps.E, KE);
     } else if (ok) {
         n_levels = ctl->i1;
         double* cstar = reinterpret_cast<double*>(rec + A.RL.cstar);
@@ -1454,8 +1683,8 @@ __global__ void __launch_bounds__(32 * kSchedWarps) k_sched(SchedArgs A) {
         return;
     }
     WS_PH_START(tw);
-    // hand the MetaOp tables to k_place / emit
-    const int K = C.K;
+    // hand the MetaOp (or scoped entity) tables to k_place / emit
+    const int K = scoped ? KE : C.K;
     int* r_mod_of = reinterpret_cast<int*>(rec + A.RL.mod_of);
     int* r_level = reinterpret_cast<int*>(rec + A.RL.level);
     int* r_up_n = reinterpret_cast<int*>(rec + A.RL.up_n);
@@ -1466,22 +1695,58 @@ __global__ void __launch_bounds__(32 * kSchedWarps) k_sched(SchedArgs A) {
     int* r_idrank = reinterpret_cast<int*>(rec + A.RL.idrank);
     uint64_t* r_pred = reinterpret_cast<uint64_t*>(rec + A.RL.pred_r);
     uint64_t* r_succ = reinterpret_cast<uint64_t*>(rec + A.RL.succ_r);
-    for (int k = lane; k < K; k += 32) {
-        r_mod_of[k] = C.at<int>(A.SL.mod_of)[k];
-        r_level[k] = C.at<int>(A.SL.level)[k];
-        r_up_n[k] = C.at<int>(A.SL.up_n)[k];
-        r_up_l[k] = C.at<int>(A.SL.up_l)[k];
-        r_lo_n[k] = C.at<int>(A.SL.lo_n)[k];
-        r_lo_l[k] = C.at<int>(A.SL.lo_l)[k];
-        r_by_rank[k] = C.at<int>(A.SL.by_rank)[k];
-        r_idrank[k] = C.at<int>(A.SL.idrank)[k];
-        r_pred[k] = C.at<uint64_t>(A.SL.pred_r)[k];
-        r_succ[k] = C.at<uint64_t>(A.SL.succ_r)[k];
+    double* r_frac = reinterpret_cast<double*>(rec + A.RL.e_frac);
+    int* r_met = reinterpret_cast<int*>(rec + A.RL.e_met);
+    int* r_task = reinterpret_cast<int*>(rec + A.RL.e_task);
+    if (scoped) {
+        const int* ent_met = C.at<int>(A.SL.ent_met);
+        const int* ent_task = C.at<int>(A.SL.ent_task);
+        const uint64_t* epred = C.at<uint64_t>(A.SL.epred);
+        auto trank = [&](int e) { return A.B.task_rank[R.task_begin + ent_task[e]]; };
+        for (int e = lane; e < K; e += 32) {
+            const int k = ent_met[e];
+            r_mod_of[e] = C.at<int>(A.SL.mod_of)[k];
+            r_level[e] = C.at<int>(A.SL.level)[k];
+            r_up_n[e] = r_up_l[e] = r_lo_n[e] = r_lo_l[e] = 0;
+            r_frac[e] = C.at<double>(A.SL.ent_frac)[e];
+            r_met[e] = k;
+            r_task[e] = ent_task[e];
+            int r = 0;  // entity ids "m<k>@<task>" in std::map order
+            for (int e2 = 0; e2 < K; ++e2) r += scoped_less(ent_met[e2], trank(e2), k, trank(e));
+            r_idrank[e] = r;
+            r_by_rank[r] = e;
+        }
+        __syncwarp();
+        for (int e = lane; e < K; e += 32) {
+            uint64_t pr = 0, sr = 0;
+            for (uint64_t b = epred[e]; b; b &= b - 1) pr |= 1ull << r_idrank[low_bit(b)];
+            for (int e2 = 0; e2 < K; ++e2)
+                if (epred[e2] >> e & 1ull) sr |= 1ull << r_idrank[e2];
+            r_pred[e] = pr;
+            r_succ[e] = sr;
+        }
+    } else {
+        for (int k = lane; k < K; k += 32) {
+            r_mod_of[k] = C.at<int>(A.SL.mod_of)[k];
+            r_level[k] = C.at<int>(A.SL.level)[k];
+            r_up_n[k] = C.at<int>(A.SL.up_n)[k];
+            r_up_l[k] = C.at<int>(A.SL.up_l)[k];
+            r_lo_n[k] = C.at<int>(A.SL.lo_n)[k];
+            r_lo_l[k] = C.at<int>(A.SL.lo_l)[k];
+            r_by_rank[k] = C.at<int>(A.SL.by_rank)[k];
+            r_idrank[k] = C.at<int>(A.SL.idrank)[k];
+            r_pred[k] = C.at<uint64_t>(A.SL.pred_r)[k];
+            r_succ[k] = C.at<uint64_t>(A.SL.succ_r)[k];
+            r_frac[k] = 1.0;
+            r_met[k] = k;
+            r_task[k] = -1;
+        }
     }
     if (lane == 0) {
         SchedHdr h{};
         h.ok = 1;
         h.K = K;
+        h.scoped = scoped ? 1 : 0;
         h.n_levels = n_levels;
         h.nW = nW;
         h.nE = nE;

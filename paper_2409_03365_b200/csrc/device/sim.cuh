@@ -29,6 +29,7 @@ struct SimSmLayout {
     int exec;    // [K]  i32 executed layers per MetaOp
     int by_rank; // [K]  i32 MetaOps in id-string order
     int gk;      // [K]  i32 group key per MetaOp
+    int efrac;   // [K]  f64 batch_fraction per entity
     int lst;     // [E]  i32 one entity's intervals (validate)
     int vio;     // [WS_SIM_MAX_VIOLATIONS] ws_out_violation
     int bytes;
@@ -52,6 +53,7 @@ __host__ __device__ inline SimSmLayout make_sim_layout(const SimCaps& c) {
     L.exec = take(4 * c.K);
     L.by_rank = take(4 * c.K);
     L.gk = take(4 * c.K);
+    L.efrac = take(8 * c.K);
     L.lst = take(4 * c.E);
     L.vio = take(static_cast<int>(sizeof(ws_out_violation)) * WS_SIM_MAX_VIOLATIONS);
     L.bytes = o;
@@ -108,6 +110,7 @@ struct SimRec {
     const ws_out_wave* wv;
     const ws_out_entry* en;
     const ws_out_flow* fl;
+    const ws_out_scope* sc;  // task-scoped entities (n_scopes > 0)
     uint64_t en_off;  // entries section offset inside the record
     uint64_t fl_off;  // flows section offset
 };
@@ -129,6 +132,8 @@ __device__ __forceinline__ SimRec sim_rec(const ws_plan_result& r, const uint8_t
     o += al8(sizeof(ws_out_entry) * r.n_entries);
     v.fl = reinterpret_cast<const ws_out_flow*>(base + o);
     v.fl_off = o;
+    o += al8(sizeof(ws_out_flow) * r.n_flows);
+    v.sc = reinterpret_cast<const ws_out_scope*>(base + o);
     return v;
 }
 
@@ -224,6 +229,8 @@ __global__ void __launch_bounds__(32 * kSimWarps, WS_SIM_MINB) k_sim(SimArgs A) 
     int* exec = reinterpret_cast<int*>(sm + A.SL.exec);
     int* by_rank = reinterpret_cast<int*>(sm + A.SL.by_rank);
     int* gk = reinterpret_cast<int*>(sm + A.SL.gk);
+    double* efrac = reinterpret_cast<double*>(sm + A.SL.efrac);
+    const bool scoped = R.n_scopes > 0;
     int* lst = reinterpret_cast<int*>(sm + A.SL.lst);
     ws_out_violation* vio = reinterpret_cast<ws_out_violation*>(sm + A.SL.vio);
 
@@ -244,11 +251,26 @@ __global__ void __launch_bounds__(32 * kSimWarps, WS_SIM_MINB) k_sim(SimArgs A) 
     for (int k = lane; k < K; k += 32) {
         const int gm = mbase + V.mo[k].module;
         const int grp = V.mo[k].length == B.mod_layers[gm] ? B.mod_group[gm] : -1;
-        const int al = B.mod_alias[gm];
+        const int al = scoped ? -1 : B.mod_alias[gm];
         gk[k] = grp < 0 ? P.n_groups + k : ((al >= 0 && al < K) ? P.n_groups + al : grp);
         exec[k] = 0;
         int r = 0;
-        for (int j = 0; j < K; ++j) r += dec_less(j, k);
+        if (scoped) {  // ids "m<metaop>@<task>" (baselines.hpp:49-55)
+            const int tk = B.task_rank[P.task_begin + V.sc[k].task];
+            for (int j = 0; j < K; ++j)
+                r += scoped_less(V.sc[j].metaop, B.task_rank[P.task_begin + V.sc[j].task], V.sc[k].metaop, tk);
+            int users = 0;  // share_fraction: tasks whose flow routes through the module
+            for (int t = 0; t < P.n_tasks; ++t) {
+                const int tg = P.task_begin + t;
+                bool in = false;
+                for (int i = 0; i < B.task_tok_n[tg] && !in; ++i) in = B.tokens[B.task_tok_off[tg] + i] == V.mo[k].module;
+                users += in;
+            }
+            efrac[k] = users ? 1.0 / static_cast<double>(users) : 1.0;
+        } else {
+            for (int j = 0; j < K; ++j) r += dec_less(j, k);
+            efrac[k] = B.mod_frac ? B.mod_frac[gm] : 1.0;
+        }
         by_rank[r] = k;
     }
     // replay order: waves by (start, index) (simulate.hpp:208-212)
@@ -485,7 +507,7 @@ __global__ void __launch_bounds__(32 * kSimWarps, WS_SIM_MINB) k_sim(SimArgs A) 
                                                       B.mod_layers[gm]);
             const uint64_t charged = chg[gk[k]];
             const double pstate = (1.0 + P.grad_mult) * static_cast<double>(pb) / B.mod_tp[gm];
-            const double frac = B.mod_frac ? B.mod_frac[gm] : 1.0;  // PlanEntity::batch_fraction
+            const double frac = efrac[k];  // PlanEntity::batch_fraction
             const double act = V.en[e].layers * (static_cast<double>(B.mod_act[gm]) * frac / V.en[e].n);
             if (m >> lane & 1ull) {
                 if (!(charged >> lane & 1ull)) mem0 += pstate;
@@ -509,7 +531,7 @@ __global__ void __launch_bounds__(32 * kSimWarps, WS_SIM_MINB) k_sim(SimArgs A) 
         if (k >= K) continue;
         const int gm = mbase + V.mo[k].module;
         const double wk = B.mod_w[gm];
-        const double frac = B.mod_frac ? B.mod_frac[gm] : 1.0;
+        const double frac = efrac[k];
         for (int w = 0; w < nW; ++w)
             for (int i = 0; i < V.wv[w].n_entries; ++i) {
                 const ws_out_entry& e = V.en[V.wv[w].entry_begin + i];
@@ -553,7 +575,7 @@ __global__ void __launch_bounds__(32 * kSimWarps, WS_SIM_MINB) k_sim(SimArgs A) 
                 const int gm = mbase + V.mo[k].module;
                 const double per_layer =
                     eval_bf(V.pc + V.mo[k].piece_begin, V.mo[k].piece_count, B.mod_c[gm], B.mod_w[gm],
-                            static_cast<double>(V.en[e].n), B.mod_frac ? B.mod_frac[gm] : 1.0);
+                            static_cast<double>(V.en[e].n), efrac[k]);
                 const double span = V.en[e].layers * per_layer;
                 const double rec = V.en[e].span;
                 if (fabs(span - rec) > tol + 1e-9 * fabs(span)) flags |= F_SPAN;
@@ -583,7 +605,7 @@ __global__ void __launch_bounds__(32 * kSimWarps, WS_SIM_MINB) k_sim(SimArgs A) 
                         const double span =
                             V.en[e].layers * eval_bf(V.pc + V.mo[k].piece_begin, V.mo[k].piece_count, B.mod_c[gm],
                                                      B.mod_w[gm], static_cast<double>(V.en[e].n),
-                                                     B.mod_frac ? B.mod_frac[gm] : 1.0);
+                                                     efrac[k]);
                         fail(WS_V_SPAN, w, k, 0, V.en[e].span, span);
                     }
                     if (flags & F_SPAN_DUR) fail(WS_V_SPAN_DURATION, w, 0, 0, 0, 0);

@@ -70,7 +70,20 @@ std::string sim_text(const Problem& prob, const ws_plan_result& r, const std::ui
                      const ws_sim_result& s, const std::uint8_t* sim_arena) {
     if (r.status != WS_STATUS_OK) return plan_text_or_error(prob, r, plan_arena);
     std::vector<std::string> names;
-    for (int k = 0; k < r.n_metaops; ++k) names.push_back(mid(k));
+    if (r.n_scopes > 0) {  // task-scoped entities "m<metaop>@<task id>": the record's last section
+        auto a8 = [](std::size_t v) { return (v + 7) & ~std::size_t(7); };
+        const std::size_t off = r.offset + a8(sizeof(ws_out_metaop) * r.n_metaops) +
+                                a8(sizeof(ws_out_level) * r.n_levels) + a8(sizeof(ws_out_piece) * r.n_pieces) +
+                                a8(sizeof(ws_out_edge) * r.n_edges) + a8(sizeof(ws_out_wave) * r.n_waves) +
+                                a8(sizeof(ws_out_entry) * r.n_entries) + a8(sizeof(ws_out_flow) * r.n_flows);
+        for (int k = 0; k < r.n_scopes; ++k) {
+            ws_out_scope sc;
+            std::memcpy(&sc, plan_arena + off + sizeof(ws_out_scope) * k, sizeof(sc));
+            names.push_back(mid(sc.metaop) + "@" + prob.spec->tasks[sc.task].id);
+        }
+    } else {
+        for (int k = 0; k < r.n_metaops; ++k) names.push_back(mid(k));
+    }
     return sim_text_named(*prob.topo, r, s, sim_arena, names);
 }
 
