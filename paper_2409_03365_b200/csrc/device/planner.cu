@@ -289,6 +289,9 @@ int launch_pair(ws_ctx* ctx, cudaStream_t st, const LaunchCaps& lc, const FitOut
     S.results = ctx->res_out();
     if (kSchedWarps * S.SL.bytes > kSmemLimit) return fail(ctx, "k_sched working set exceeds shared memory");
     CK(cudaFuncSetAttribute(k_sched, cudaFuncAttributeMaxDynamicSharedMemorySize, kSchedWarps * S.SL.bytes));
+    if (lc.scoped)
+        CK(cudaFuncSetAttribute(k_sched_scoped, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                kSchedWarps * S.SL.bytes));
 
     PlaceArgs P{};
     P.B = B;
@@ -323,6 +326,11 @@ int launch_pair(ws_ctx* ctx, cudaStream_t st, const LaunchCaps& lc, const FitOut
         S.n_launch = cnt;
         k_sched<<<(cnt + kSchedWarps - 1) / kSchedWarps, 32 * kSchedWarps, kSchedWarps * S.SL.bytes, st>>>(S);
         ctx->launches++;
+        if (lc.scoped) {  // the batch's distmm-mt plans (each instance skips the other's plans)
+            k_sched_scoped<<<(cnt + kSchedWarps - 1) / kSchedWarps, 32 * kSchedWarps, kSchedWarps * S.SL.bytes,
+                             st>>>(S);
+            ctx->launches++;
+        }
         if (chunks > 1) {
             CK(cudaEventRecord(ctx->cev[c], st));
             CK(cudaStreamWaitEvent(sb, ctx->cev[c], 0));

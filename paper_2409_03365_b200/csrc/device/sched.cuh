@@ -177,7 +177,11 @@ struct SCtx {
 // T_k(n): the T-table, or the scaled curve of a task-scoped baseline level
 __device__ __forceinline__ double T_of(const SCtx& C, int k, int n) {
     const int gm = C.at<int>(C.L->gm_of)[k];
+#ifdef WS_NO_SCALE
+    return t_at(*C.F, gm, n);
+#else
     return C.kscale ? t_scaled(*C.F, *C.B, gm, n, C.kscale[k]) : t_at(*C.F, gm, n);
+#endif
 }
 
 // ---------------------------------------------------------------------------
@@ -1572,18 +1576,17 @@ __device__ bool s_distmm(SCtx& C, char* rec, const RecLayout& RL, int& nW, int& 
     return true;
 }
 
-#ifdef WS_SCHED_MINB
-__global__ void __launch_bounds__(32 * kSchedWarps, WS_SCHED_MINB) k_sched(SchedArgs A) {
-#else
-__global__ void __launch_bounds__(32 * kSchedWarps) k_sched(SchedArgs A) {
-#endif
-    extern __shared__ __align__(16) char smem_dyn[];
-    __shared__ Ctl ctl_s[kSchedWarps];
+// One warp per plan.  SCOPED: the kernel instance for the task-scoped
+// baselines (distmm-mt); the planner's instance carries none of that code, so
+// its register allocation and instruction stream stay those of the planner.
+template <bool SCOPED>
+__device__ __forceinline__ void sched_body(const SchedArgs& A, char* smem_dyn, Ctl* ctl_s) {
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int slot = blockIdx.x * kSchedWarps + wid;
     if (slot >= A.n_launch) return;
     if (A.n_ids && slot >= *A.n_ids) return;
     const int p = A.plan_ids[slot];
+    if ((A.B.plans[p].strategy == WS_STRATEGY_DISTMM_MT) != SCOPED) return;  // the other instance's plan
     Ctl* ctl = &ctl_s[wid];
     if (lane == 0) *ctl = Ctl{};
     __syncwarp();
@@ -1619,7 +1622,7 @@ __global__ void __launch_bounds__(32 * kSchedWarps) k_sched(SchedArgs A) {
     WS_PH_STOP(tg, 10);
     if (ok) ok = s_fit_status(C);
     const bool decoupled = R.strategy == WS_STRATEGY_DECOUPLED_SEQUENTIAL;
-    const bool scoped = R.strategy == WS_STRATEGY_DISTMM_MT;
+    constexpr bool scoped = SCOPED;
     if (ok && scoped && !A.scoped_ok) {  // launch built without the task-scoped working set
         ok = false;
         if (lane == 0) ctl->err = WS_E_LIMIT_MODULES;
@@ -1632,7 +1635,7 @@ __global__ void __launch_bounds__(32 * kSchedWarps) k_sched(SchedArgs A) {
     if (ok && decoupled) {
         ok = s_decoupled(C, rec, A.RL, nW, nE, offset, A.caps.W, A.caps.E);
     } else if (ok && scoped) {
-        ok = s_distmm(C, rec, A.RL, nW, nE, offset, A.caps.W, A.caps.E, KE);
+        if constexpr (SCOPED) ok = s_distmm(C, rec, A.RL, nW, nE, offset, A.caps.W, A.caps.E, KE);
     } else if (ok) {
         n_levels = ctl->i1;
         double* cstar = reinterpret_cast<double*>(rec + A.RL.cstar);
@@ -1698,7 +1701,7 @@ __global__ void __launch_bounds__(32 * kSchedWarps) k_sched(SchedArgs A) {
     double* r_frac = reinterpret_cast<double*>(rec + A.RL.e_frac);
     int* r_met = reinterpret_cast<int*>(rec + A.RL.e_met);
     int* r_task = reinterpret_cast<int*>(rec + A.RL.e_task);
-    if (scoped) {
+    if constexpr (SCOPED) {
         const int* ent_met = C.at<int>(A.SL.ent_met);
         const int* ent_task = C.at<int>(A.SL.ent_task);
         const uint64_t* epred = C.at<uint64_t>(A.SL.epred);
@@ -1755,6 +1758,24 @@ __global__ void __launch_bounds__(32 * kSchedWarps) k_sched(SchedArgs A) {
         *hdr = h;
     }
     WS_PH_STOP(tw, 14);
+}
+
+
+#ifdef WS_SCHED_MINB
+__global__ void __launch_bounds__(32 * kSchedWarps, WS_SCHED_MINB) k_sched(SchedArgs A) {
+#else
+__global__ void __launch_bounds__(32 * kSchedWarps) k_sched(SchedArgs A) {
+#endif
+    extern __shared__ __align__(16) char smem_dyn[];
+    __shared__ Ctl ctl_s[kSchedWarps];
+    sched_body<false>(A, smem_dyn, ctl_s);
+}
+
+// plan_distmm_mt plans of the batch (the planner instance skips them)
+__global__ void __launch_bounds__(32 * kSchedWarps) k_sched_scoped(SchedArgs A) {
+    extern __shared__ __align__(16) char smem_dyn[];
+    __shared__ Ctl ctl_s[kSchedWarps];
+    sched_body<true>(A, smem_dyn, ctl_s);
 }
 
 }  // namespace wsdev
