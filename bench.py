@@ -296,6 +296,40 @@ def main() -> None:
     d2h_step = len(ps) * ctypes_sizeof_result() + sum(int(r2.results[i].size) for i in range(len(ps))
                                                       if r2.results[i].status == 0)
 
+    # ---- baseline planners on the device, same shard ----
+    baselines = {}
+    for strategy in ("decoupled-sequential", "distmm-mt"):
+        pb = ws.ProblemSet()
+        for i in idx:
+            pb.add_sweep(i, 1, strategy=strategy)
+        pb.encode(pinned=True)
+        planner.stage(pb, sptr)
+        for _ in range(2):
+            planner.plan_staged(sptr)
+        barrier()
+        bms = []
+        for _ in range(args.steps):
+            flush.zero_()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            planner.plan_staged(sptr)
+            e1.record(stream)
+            e1.synchronize()
+            bms.append(e0.elapsed_time(e1))
+        barrier()
+        tb = torch.tensor([sum(bms) / 1000.0], dtype=torch.float64, device=dev)
+        if world > 1:
+            torch.distributed.all_reduce(tb, op=torch.distributed.ReduceOp.MAX)
+        rb = planner.fetch(pb, sptr)
+        bad = torch.tensor([sum(1 for i in range(len(pb)) if rb.results[i].status != 0)], dtype=torch.int64,
+                           device=dev)
+        if world > 1:
+            torch.distributed.all_reduce(bad)
+        baselines[strategy] = {"value": args.mixtures * args.steps / float(tb.item()), "unit": "plans/s",
+                               "ms_per_step": 1000.0 * float(tb.item()) / args.steps,
+                               "failed_plans": int(bad.item())}
+
     if rank != 0:
         if world > 1:
             torch.distributed.destroy_process_group()
@@ -367,6 +401,17 @@ def main() -> None:
                     latency[name]["cpu_reference_ms_median"] = po.ref_latency_ms(fam, tasks, devices, 100)
         except Exception:
             pass
+        try:
+            import pyoracle as po
+            if po.ref_available():
+                n_b = max(args.cpu_sample // 2, 500)
+                for strategy in baselines:
+                    baselines[strategy]["cpu_reference_per_s"] = po.ref_sweep_bench_strategy(
+                        0, n_b, os.cpu_count() or 1, strategy)
+                    baselines[strategy]["cpu_reference_sample"] = (
+                        f"sweep mixtures 0..{n_b - 1}, reference plan_for_strategy, {os.cpu_count()} threads")
+        except Exception:
+            pass
 
     line = {
         "metric": METRIC,
@@ -397,6 +442,7 @@ def main() -> None:
         "clocks": clk,
         "latency_ms": latency,
         "evaluation": evaluation,
+        "baselines": baselines,
         "parity": {"infeasible_plans": int(infeasible.item()), "best_gap": best_key, "best_index": best_idx},
     }
     print(json.dumps(line), flush=True)

@@ -131,6 +131,8 @@ def ref():
         lib.wsref_json_plan_text.argtypes = [C.c_char_p, C.c_char_p, C.POINTER(RefOpts)]
         lib.wsref_strategy_plan_text.restype = vp
         lib.wsref_strategy_plan_text.argtypes = [C.c_char_p, C.c_char_p, C.c_char_p, C.POINTER(RefOpts)]
+        lib.wsref_sweep_bench_strategy.restype = C.c_double
+        lib.wsref_sweep_bench_strategy.argtypes = [C.c_long, C.c_long, C.c_int, C.c_int]
         lib.wsref_latency_ms.restype = C.c_double
         lib.wsref_latency_ms.argtypes = [C.c_char_p, C.c_int, C.c_int, C.c_int]
         _ref = lib
@@ -193,6 +195,11 @@ def ref_sweep_bench(start: int, count: int, threads: int) -> tuple[float, int]:
     bad = C.c_long(0)
     rate = ref().wsref_sweep_bench(start, count, threads, C.byref(bad))
     return rate, bad.value
+
+
+def ref_sweep_bench_strategy(start: int, count: int, threads: int, strategy: str) -> float:
+    sid = {"wavefront": 0, "decoupled-sequential": 1, "distmm-mt": 2}[strategy]
+    return ref().wsref_sweep_bench_strategy(start, count, threads, sid)
 
 
 def ref_latency_ms(name: str, tasks: int, devices: int, reps: int) -> float:

@@ -346,6 +346,34 @@ double wsref_sweep_sim_bench(long start, long count, int threads) {
            std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
 }
 
+// CPU baseline of a baseline planner (plan_for_strategy): strategy 1 decoupled-sequential,
+// 2 distmm-mt, over sweep mixtures [start, start+count) on `threads` threads.
+double wsref_sweep_bench_strategy(long start, long count, int threads, int strategy) {
+    std::vector<WorkloadSpec> specs(count);
+    std::vector<ClusterTopology> topos(count);
+    for (long i = 0; i < count; ++i) {
+        Scenario sc = sweep(start + i);
+        specs[i] = parse_workload(sc.workload_text);
+        topos[i] = parse_topology(sc.topology_text);
+    }
+    std::atomic<long> next{0};
+    auto worker = [&] {
+        for (long i; (i = next.fetch_add(1)) < count;) {
+            try {
+                ExecutionPlan p = plan_strategy(specs[i], topos[i], PlannerOptions{}, strategy);
+                (void)p;
+            } catch (const Error&) {
+            }
+        }
+    };
+    const auto t0 = std::chrono::steady_clock::now();
+    std::vector<std::thread> pool;
+    for (int t = 0; t < threads; ++t) pool.emplace_back(worker);
+    for (auto& th : pool) th.join();
+    return static_cast<double>(count) /
+           std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
+
 // Single-plan latency of the reference planner (median of `reps`, ms).
 double wsref_latency_ms(const char* name, int tasks, int devices, int reps) {
     Scenario sc = generate_scenario(name, tasks, devices, 0);
