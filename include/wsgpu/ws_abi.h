@@ -67,6 +67,7 @@ enum ws_err {
     WS_E_BT_BUDGET = 17,        /* PlacementInfeasible "placement backtrack budget exhausted at wave <a>" */
     WS_E_NO_PLACEMENT_W0 = 18,  /* PlacementInfeasible "no feasible placement for wave 0"                */
     WS_E_HOST_PRESET = 19,      /* error detected by the host encoder; message kept host-side           */
+    WS_E_TASK_NO_VALID = 20,    /* NoValidAllocation "task '<task a>' has no allocation valid for all its metaops" */
     WS_E_LIMIT_DEVICES = 40,
     WS_E_LIMIT_MODULES = 41,
     WS_E_LIMIT_TASKS = 42,
@@ -110,7 +111,8 @@ typedef struct ws_plan_rec {
 enum ws_strategy {
     WS_STRATEGY_WAVEFRONT = 0,            /* planner.hpp:156-212                  */
     WS_STRATEGY_DECOUPLED_SEQUENTIAL = 1, /* plan_decoupled_sequential, baselines.hpp:104-131 */
-    WS_STRATEGY_DISTMM_MT = 2             /* plan_distmm_mt, baselines.hpp:323-413          */
+    WS_STRATEGY_DISTMM_MT = 2,            /* plan_distmm_mt, baselines.hpp:323-413          */
+    WS_STRATEGY_TASK_OPTIMUS = 3          /* plan_task_level_optimus, baselines.hpp:133-321 */
 };
 
 /* Structure-of-arrays batch.  All pointers address the same memory space

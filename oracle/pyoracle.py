@@ -150,7 +150,7 @@ def ref_options(**kw) -> RefOpts:
     o = RefOpts(1e-7, 200, 0.0, 0, 2, 3, 3.0, 0.0, 0, 0)
     for k, v in kw.items():
         if k == "strategy" and isinstance(v, str):
-            v = {"wavefront": 0, "decoupled-sequential": 1, "distmm-mt": 2}[v]
+            v = {"wavefront": 0, "decoupled-sequential": 1, "distmm-mt": 2, "task-level-optimus": 3}[v]
         setattr(o, k, v)
     return o
 
@@ -198,7 +198,7 @@ def ref_sweep_bench(start: int, count: int, threads: int) -> tuple[float, int]:
 
 
 def ref_sweep_bench_strategy(start: int, count: int, threads: int, strategy: str) -> float:
-    sid = {"wavefront": 0, "decoupled-sequential": 1, "distmm-mt": 2}[strategy]
+    sid = {"wavefront": 0, "decoupled-sequential": 1, "distmm-mt": 2, "task-level-optimus": 3}[strategy]
     return ref().wsref_sweep_bench_strategy(start, count, threads, sid)
 
 

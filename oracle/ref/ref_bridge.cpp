@@ -74,6 +74,7 @@ ExecutionPlan plan_strategy(const WorkloadSpec& spec, const ClusterTopology& top
                             int strategy) {
     if (strategy == 1) return plan_decoupled_sequential(prepare_planning_base(spec, topo, opt), topo, opt);
     if (strategy == 2) return plan_distmm_mt(prepare_planning_base(spec, topo, opt), topo, opt);
+    if (strategy == 3) return plan_task_level_optimus(prepare_planning_base(spec, topo, opt), topo, opt);
     return plan_workload(spec, topo, opt).plan;
 }
 

@@ -255,6 +255,8 @@ public:
             decoupled();        // baselines.hpp:104-131
         else if (R.strategy == WS_STRATEGY_DISTMM_MT)
             distmm();           // baselines.hpp:323-413
+        else if (R.strategy == WS_STRATEGY_TASK_OPTIMUS)
+            optimus();          // baselines.hpp:133-321
         else
             allocate_and_schedule(out);
         if (!scoped) {          // entities are the MetaOps (planner.hpp:99-122)
@@ -292,6 +294,11 @@ private:
     std::vector<double> cstar;
     // placement entities: the MetaOps, or (MetaOp, task) pairs for the task-scoped baselines
     bool scoped = false;
+    struct PGroup {  // one place() call: waves (record order) on devices [off, off+cnt)
+        std::vector<int> waves;
+        int off = 0, cnt = 0;
+    };
+    std::vector<PGroup> pgroups;  // empty: a single call over everything
     int KE = 0;
     std::vector<int> e_mod, e_task, e_by_rank, e_idrank;
     std::vector<double> e_frac;
@@ -679,6 +686,230 @@ private:
         sdeps.erase(std::unique(sdeps.begin(), sdeps.end()), sdeps.end());
         e_edges = sdeps;
         end_time = now;
+    }
+
+    // ScalingCurve::eval_batch_fraction (scaling.hpp:83-86)
+    double eval_bf(const Curve& cv, double n, double frac) const {
+        const Piece& q = n < 1.0 ? cv.p.front() : cv.locate(std::min(n, cv.nmax));
+        return q.alpha + q.bc * cv.c + q.bw * cv.w * frac / n;
+    }
+
+    // plan_task_level_optimus (baselines.hpp:133-321): every task gets a
+    // device block sized by marginal gain of its critical-path time, runs its
+    // MetaOps one after another on the whole block, and is placed on its own
+    // sub-topology; waves take global indices by (start, id).
+    void optimus() {
+        scoped = true;
+        valid.assign(K, 0);
+        for (int k = 0; k < K; ++k) {
+            const int g = mg(mod_of[k]);
+            const int tp = B.mod_tp[g];
+            for (int n = 1; n <= N; ++n)
+                if (n % tp == 0 && B.mod_batch[g] % (n / tp) == 0) valid[k] |= 1ull << (n - 1);
+        }
+        upper_n.assign(K, 0);
+        upper_l.assign(K, 0);
+        lower_n.assign(K, 0);
+        lower_l.assign(K, 0);
+        struct Task {
+            int t = 0;
+            std::vector<int> order;
+            std::vector<std::pair<int, int>> tedges;
+            uint64_t valid = 0;
+            int alloc = 0;
+        };
+        std::vector<Task> tasks;
+        std::vector<int> task_rank_of;
+        for (int t = 0; t < R.n_tasks; ++t) {
+            Task task;
+            task.t = t;
+            const int tr = B.task_rank[R.task_begin + t];
+            task_rank_of.push_back(tr);
+            std::vector<char> mem(K, 0);
+            for (int k = 0; k < K; ++k) mem[k] = (taskmask[mod_of[k]] >> tr & 1ull) ? 1 : 0;
+            for (const auto& e : edges)
+                if (mem[e.first] && mem[e.second]) task.tedges.push_back(e);
+            std::vector<int> indeg(K, 0);
+            for (const auto& e : task.tedges) ++indeg[e.second];
+            std::set<int> ready;
+            for (int k = 0; k < K; ++k)
+                if (mem[k] && !indeg[k]) ready.insert(idrank[k]);
+            while (!ready.empty()) {
+                const int k = by_rank[*ready.begin()];
+                ready.erase(ready.begin());
+                task.order.push_back(k);
+                for (const auto& e : task.tedges)
+                    if (e.first == k && --indeg[e.second] == 0) ready.insert(idrank[e.second]);
+            }
+            for (int n = 1; n <= N; ++n) {  // valid for every member (valid_allocations per n, in order)
+                bool ok = true;
+                for (int k : task.order) {
+                    const int tp = B.mod_tp[mg(mod_of[k])];
+                    if (tp > N) throw Fail{WS_E_TP_EXCEEDS, k, tp};
+                    if (!(valid[k] >> (n - 1) & 1ull)) {
+                        ok = false;
+                        break;
+                    }
+                }
+                if (ok) task.valid |= 1ull << (n - 1);
+            }
+            if (!task.valid) throw Fail{WS_E_TASK_NO_VALID, t};
+            tasks.push_back(task);
+        }
+        auto frac_of = [&](int k) { return 1.0 / static_cast<double>(popc(taskmask[mod_of[k]])); };
+        auto task_time = [&](const Task& task, int n) {  // critical path at allocation n
+            std::vector<double> finish(K, 0.0);
+            double total = 0.0;
+            for (int k : task.order) {
+                const double weight = layers(mod_of[k]) * eval_bf(mcurve[mod_of[k]], n, frac_of(k));
+                double start = 0.0;
+                for (const auto& e : task.tedges)
+                    if (e.second == k) start = std::max(start, finish[e.first]);
+                finish[k] = start + weight;
+                total = std::max(total, finish[k]);
+            }
+            return total;
+        };
+        auto lowest = [](uint64_t v) { return __builtin_ctzll(v) + 1; };
+        std::vector<std::vector<std::size_t>> batches;
+        {
+            std::vector<std::size_t> current;
+            int used = 0;
+            for (std::size_t i = 0; i < tasks.size(); ++i) {
+                const int need = lowest(tasks[i].valid);
+                if (used + need > N && !current.empty()) {
+                    batches.push_back(current);
+                    current.clear();
+                    used = 0;
+                }
+                current.push_back(i);
+                used += need;
+            }
+            if (!current.empty()) batches.push_back(current);
+        }
+        std::map<std::pair<int, int>, int> ent_of;
+        auto entity = [&](int k, int t) {
+            auto it = ent_of.find({k, t});
+            if (it != ent_of.end()) return it->second;
+            const int e = KE++;
+            e_mod.push_back(k);
+            e_task.push_back(t);
+            e_frac.push_back(frac_of(k));
+            ent_of[{k, t}] = e;
+            return e;
+        };
+        struct Placement {
+            std::vector<int> wave_ids;  // creation order
+            int off = 0, cnt = 0;
+        };
+        std::vector<Placement> placements;
+        std::vector<WaveRec> ws;
+        std::vector<EntryRec> es;
+        std::vector<std::pair<int, int>> sdeps;
+        double batch_offset = 0.0;
+        for (const auto& batch : batches) {
+            for (std::size_t ti : batch) tasks[ti].alloc = lowest(tasks[ti].valid);
+            while (true) {
+                int usedn = 0;
+                for (std::size_t ti : batch) usedn += tasks[ti].alloc;
+                const int free = N - usedn;
+                if (free <= 0) break;
+                std::size_t best = tasks.size();
+                double best_gain = -1.0;
+                int best_next = 0;
+                for (std::size_t ti : batch) {
+                    const Task& task = tasks[ti];
+                    const uint64_t above = task.valid & ~((task.alloc >= 64) ? ~0ull : ((1ull << task.alloc) - 1));
+                    if (!above) continue;  // std::upper_bound at the end
+                    const int nx = lowest(above);
+                    if (nx - task.alloc > free) continue;
+                    const double gain = (task_time(task, task.alloc) - task_time(task, nx)) / (nx - task.alloc);
+                    if (gain > best_gain) {
+                        best_gain = gain;
+                        best = ti;
+                        best_next = nx;
+                    }
+                }
+                if (best == tasks.size()) break;
+                tasks[best].alloc = best_next;
+            }
+            double batch_end = batch_offset;
+            int cursor = 0;
+            for (std::size_t ti : batch) {
+                Task& task = tasks[ti];
+                Placement pl;
+                pl.off = cursor;
+                pl.cnt = task.alloc;
+                cursor += task.alloc;
+                double now = batch_offset;
+                for (int k : task.order) {
+                    const int e = entity(k, task.t);
+                    const int L = layers(mod_of[k]);
+                    const double span = L * eval_bf(mcurve[mod_of[k]], task.alloc, e_frac[e]);
+                    WaveRec wv;
+                    wv.level = level[k];
+                    wv.start = now;
+                    wv.dur = span;
+                    wv.entries.push_back(static_cast<int>(es.size()));
+                    EntryRec en;
+                    en.k = e;
+                    en.n = task.alloc;
+                    en.layers = L;
+                    en.span = span;
+                    es.push_back(en);
+                    pl.wave_ids.push_back(static_cast<int>(ws.size()));
+                    ws.push_back(wv);
+                    now += span;
+                }
+                for (const auto& ed : task.tedges) sdeps.push_back({entity(ed.first, task.t), entity(ed.second, task.t)});
+                batch_end = std::max(batch_end, now);
+                placements.push_back(pl);
+            }
+            batch_offset = batch_end;
+        }
+        // global indices by (start, id of the first entry)
+        std::vector<int> order(ws.size());
+        for (std::size_t i = 0; i < order.size(); ++i) order[i] = static_cast<int>(i);
+        auto eless = [&](int a, int b) {
+            return scoped_less(e_mod[a], task_rank_of[e_task[a]], e_mod[b], task_rank_of[e_task[b]]);
+        };
+        std::sort(order.begin(), order.end(), [&](int a, int b) {
+            if (ws[a].start != ws[b].start) return ws[a].start < ws[b].start;
+            return eless(es[ws[a].entries.front()].k, es[ws[b].entries.front()].k);
+        });
+        std::vector<int> gidx(ws.size());
+        for (std::size_t i = 0; i < order.size(); ++i) gidx[order[i]] = static_cast<int>(i);
+        waves.clear();
+        entries.clear();
+        for (int wi : order) {
+            WaveRec wv = ws[wi];
+            wv.entries.clear();
+            for (int x : ws[wi].entries) {
+                wv.entries.push_back(static_cast<int>(entries.size()));
+                entries.push_back(es[x]);
+            }
+            waves.push_back(wv);
+            end_time = std::max(end_time, wv.start + wv.dur);
+        }
+        if (static_cast<int>(waves.size()) > WS_MAX_WAVES) throw Fail{WS_E_LIMIT_WAVES};
+        for (const Placement& pl : placements) {
+            PGroup g;
+            for (int wi : pl.wave_ids) g.waves.push_back(gidx[wi]);
+            g.off = pl.off;
+            g.cnt = pl.cnt;
+            pgroups.push_back(g);
+        }
+        e_by_rank.resize(KE);
+        for (int e = 0; e < KE; ++e) e_by_rank[e] = e;
+        std::sort(e_by_rank.begin(), e_by_rank.end(), eless);
+        e_idrank.assign(KE, 0);
+        for (int r = 0; r < KE; ++r) e_idrank[e_by_rank[r]] = r;
+        std::sort(sdeps.begin(), sdeps.end(), [&](const auto& x, const auto& y) {
+            if (x.first != y.first) return e_idrank[x.first] < e_idrank[y.first];
+            return e_idrank[x.second] < e_idrank[y.second];
+        });
+        sdeps.erase(std::unique(sdeps.begin(), sdeps.end()), sdeps.end());
+        e_edges = sdeps;
     }
 
     std::vector<int> valid_list(int k) const {
@@ -1110,21 +1341,44 @@ private:
         std::vector<int> last_wave(KE, -1);
         for (std::size_t w = 0; w < waves.size(); ++w)
             for (int e : waves[w].entries) last_wave[entries[e].k] = static_cast<int>(w);
-        const int nW = static_cast<int>(waves.size());
+        if (pgroups.empty()) {  // one place() call over every wave and device
+            PGroup g;
+            for (std::size_t w = 0; w < waves.size(); ++w) g.waves.push_back(static_cast<int>(w));
+            g.off = 0;
+            g.cnt = N;
+            pgroups.push_back(g);
+        }
+        const std::vector<uint64_t> full_islands = island_mask;
+        for (const PGroup& pg : pgroups) place_group(pg, last_wave, full_islands);
+    }
+
+    // one place() call (placement.hpp:168-447) over the waves of `pg` on the
+    // device block [off, off+cnt) (detail::sub_topology: islands cut to the block)
+    void place_group(const PGroup& pg, const std::vector<int>& last_wave, const std::vector<uint64_t>& full_islands) {
+        const int gN = pg.cnt;
+        const uint64_t all = (gN == 64 ? ~0ull : ((1ull << gN) - 1)) << pg.off;
+        island_mask.clear();
+        for (uint64_t m : full_islands)
+            if (m & all) island_mask.push_back(m & all);
+        const int n_isl = static_cast<int>(island_mask.size());
+        const int nW = static_cast<int>(pg.waves.size());
         std::vector<int> seq_cursor(nW, 0);
         {
             int cur = 0;
-            for (int w = 0; w < nW; ++w) {
-                seq_cursor[w] = cur;
-                for (int e : waves[w].entries) cur = (cur + entries[e].n) % N;
+            for (int j = 0; j < nW; ++j) {
+                seq_cursor[j] = cur;
+                for (int e : waves[pg.waves[j]].entries) cur = (cur + entries[e].n) % gN;
             }
         }
+        std::vector<char> in_group(KE, 0);  // entities this place() call knows
+        for (int w : pg.waves)
+            for (int e : waves[w].entries) in_group[entries[e].k] = 1;
         State st;
         std::fill(st.mem, st.mem + WS_MAX_DEVICES, 0.0);
         st.charged.assign(R.n_groups + KE, 0);
-        const uint64_t all = N == 64 ? ~0ull : ((1ull << N) - 1);
 
-        auto place_wave = [&](int w, int variant) -> bool {  // :340-406
+        auto place_wave = [&](int j, int variant) -> bool {  // :340-406
+            const int w = pg.waves[j];
             uint64_t free = all;
             std::vector<int> order(waves[w].entries);
             std::vector<std::vector<Incoming>> fin(order.size());
@@ -1141,7 +1395,7 @@ private:
                 });
             bool first = true;
             std::vector<char> placed_now(KE, 0);
-            int cursor = R.sequential ? seq_cursor[w] : 0;
+            int cursor = R.sequential ? seq_cursor[j] : 0;
             for (std::size_t oi : idx) {
                 EntryRec& e = entries[order[oi]];
                 const std::vector<Incoming>& flows_in = fin[oi];
@@ -1150,10 +1404,10 @@ private:
                 if (R.sequential) {
                     if (popc(free) >= e.n) {
                         uint64_t m = 0;
-                        for (int i = 0; i < e.n; ++i) m |= 1ull << ((cursor + i) % N);
+                        for (int i = 0; i < e.n; ++i) m |= 1ull << (pg.off + (cursor + i) % gN);
                         cands.push_back(m);
-                        rots.push_back(cursor);
-                        cursor = (cursor + e.n) % N;
+                        rots.push_back(pg.off + cursor);
+                        cursor = (cursor + e.n) % gN;
                     }
                 } else {  // candidate_sets :223-263
                     std::set<uint64_t> seen;
@@ -1176,7 +1430,7 @@ private:
                             push(m);
                         }
                     };
-                    for (int i = 0; i < R.n_islands; ++i) windows(free & island_mask[i]);
+                    for (int i = 0; i < n_isl; ++i) windows(free & island_mask[i]);
                     windows(free);
                 }
                 if (cands.empty()) return false;
@@ -1184,11 +1438,11 @@ private:
                 for (uint64_t devs : cands) {  // score_candidate :285-325
                     Score s{};
                     s.devs = devs;
-                    for (int i = 0; i < R.n_islands; ++i)
+                    for (int i = 0; i < n_isl; ++i)
                         if (devs & island_mask[i]) s.islands++;
                     for (int r = 0; r < KE; ++r) {
                         const int e2 = e_by_rank[r];
-                        if (e2 == e.k || last_wave[e2] < w || placed_now[e2]) continue;
+                        if (e2 == e.k || !in_group[e2] || last_wave[e2] < w || placed_now[e2]) continue;
                         const int home = latest_entry_before(e2, w);
                         if (home < 0) continue;
                         const uint64_t hm = entries[home].mask;
@@ -1259,8 +1513,8 @@ private:
             if (++attempts > budget) throw Fail{WS_E_BT_BUDGET, k};
             st = saved.back();
             flows.resize(saved_flows.back());
-            for (int w = k; w < nW; ++w)
-                for (int e : waves[w].entries) entries[e].mask = 0, entries[e].rot = 0;
+            for (int j = k; j < nW; ++j)
+                for (int e : waves[pg.waves[j]].entries) entries[e].mask = 0, entries[e].rot = 0;
             const int branching = R.sequential ? 1 : R.bt_branching;
             if (variant[k] >= branching) {
                 variant[k] = 0;
@@ -1336,6 +1590,7 @@ int status_of(int code) {
             return WS_STATUS_PARSE;
         case WS_E_FIT_NONPOSITIVE:
         case WS_E_TP_EXCEEDS:
+        case WS_E_TASK_NO_VALID:
         case WS_E_BT_BUDGET:
         case WS_E_NO_PLACEMENT_W0:
             return WS_STATUS_INFEASIBLE;

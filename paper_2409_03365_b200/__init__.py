@@ -220,7 +220,7 @@ def make_options(**kw) -> Options:
 
 
 # plan_for_strategy selectors (cli.hpp:163-171) built on the device
-STRATEGIES = {"wavefront": 0, "decoupled-sequential": 1, "distmm-mt": 2}
+STRATEGIES = {"wavefront": 0, "decoupled-sequential": 1, "distmm-mt": 2, "task-level-optimus": 3}
 
 
 class ProblemSet:

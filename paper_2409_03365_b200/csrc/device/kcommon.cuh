@@ -30,6 +30,7 @@ __device__ __forceinline__ int status_of(int code) {
     switch (code) {
         case WS_E_FIT_NONPOSITIVE:
         case WS_E_TP_EXCEEDS:
+        case WS_E_TASK_NO_VALID:
         case WS_E_BT_BUDGET:
         case WS_E_NO_PLACEMENT_W0: return WS_STATUS_INFEASIBLE;
         case WS_E_CURVE_START:

@@ -62,7 +62,8 @@ const char* class_of(int code) {
         case WS_E_FIT_PIECE_POINTS:
         case WS_E_FIT_DEGENERATE_X: return "InsufficientProfile";
         case WS_E_FIT_NONPOSITIVE: return "DegenerateFit";
-        case WS_E_TP_EXCEEDS: return "NoValidAllocation";
+        case WS_E_TP_EXCEEDS:
+        case WS_E_TASK_NO_VALID: return "NoValidAllocation";
         case WS_E_EVAL_RANGE: return "OutOfRange";
         case WS_E_BT_BUDGET:
         case WS_E_NO_PLACEMENT_W0: return "PlacementInfeasible";
@@ -112,6 +113,9 @@ std::vector<int> device_list(const Problem& prob, const ws_out_entry& e) {
                                       "] needs points at >= 2 distinct n");
         case WS_E_FIT_DEGENERATE_X: throw InsufficientProfile("fit: points do not span distinct n");
         case WS_E_FIT_NONPOSITIVE: throw DegenerateFit("fit: non-positive T(" + std::to_string(r.err_a) + ")");
+        case WS_E_TASK_NO_VALID:
+            throw NoValidAllocation("task '" + prob.spec->tasks[r.err_a].id +
+                                    "' has no allocation valid for all its metaops");
         case WS_E_TP_EXCEEDS:
             throw NoValidAllocation("metaop 'm" + std::to_string(r.err_a) + "': tp degree " +
                                     std::to_string(r.err_b) + " exceeds device count " + std::to_string(N));
@@ -151,7 +155,7 @@ PlannerResult decode_scoped(const Problem& prob, const ws_plan_result& r, const 
     std::vector<std::string> ids(r.n_metaops);
     PlannerResult res;
     ExecutionPlan& plan = res.plan;
-    plan.strategy = "distmm-mt";
+    plan.strategy = prob.opt.strategy == WS_STRATEGY_TASK_OPTIMUS ? "task-level-optimus" : "distmm-mt";
     plan.topo = *prob.topo;
     for (int e = 0; e < r.n_metaops; ++e) {
         const ws_out_metaop& o = s.mo[e];
