@@ -25,6 +25,8 @@ struct PlSmLayout {
     int isl;                                                      // [N] i32
     int islmask;                                                  // [IS] u64
     int isllow;                                                   // [IS] u64 devices below island i
+    int islfull;                                                  // [IS] u64 islands of the whole plan
+    int glist;                                                    // [W] i32 waves of the current place() call
     int nwin;                                                     // [IS] i32
     int chg;                                                      // [G] u64
     int fin_src, fin_bytes;                                       // [M+1]
@@ -71,6 +73,8 @@ __host__ __device__ inline PlSmLayout make_pl_layout(const PlaceCaps& c) {
     L.isl = take(4 * N);
     L.islmask = take(8 * c.IS);
     L.isllow = take(8 * c.IS);
+    L.islfull = take(8 * c.IS);
+    L.glist = take(4 * W);
     L.nwin = take(4 * (c.IS + W + 1));  // island window counts, then flows-per-wave marks
     L.chg = take(8 * c.G);
     L.fin_src = take(4 * (M + 1));
@@ -113,6 +117,7 @@ struct PCtx {
     Ctl* ctl;
     int lane, N, K, mbase, nW, nE, nF, Fcap, G, n_isl;
     int contig;  // every island is one contiguous run of device indices
+    int dev_off, dev_cnt;  // device block of the current place() call ([0, N) unless grouped)
     uint64_t all;
     uint64_t* flows;  // this plan's flow list (2 words per flow)
     template <typename T>
@@ -290,11 +295,11 @@ __device__ int p_wave(PCtx& C, int w, int variant) {
         Score chosen;
         chosen.valid = 0;
         if (R.sequential) {
-            if (popc64(free) >= n) {  // rolling cursor block (:350-358)
+            if (popc64(free) >= n) {  // rolling cursor block (:350-358), within the device block
                 uint64_t m = 0;
-                for (int i = 0; i < n; ++i) m |= 1ull << ((cursor + i) % N);
-                chosen = score_of(m, cursor);
-                cursor = (cursor + n) % N;
+                for (int i = 0; i < n; ++i) m |= 1ull << (C.dev_off + (cursor + i) % C.dev_cnt);
+                chosen = score_of(m, C.dev_off + cursor);
+                cursor = (cursor + n) % C.dev_cnt;
             }
         } else {
             // candidate_sets (:223-263): predecessor reuse, island windows, global windows
@@ -332,7 +337,7 @@ __device__ int p_wave(PCtx& C, int w, int variant) {
                             // with contiguous islands a global window inside one island is
                             // that island's window at the same offset: a duplicate (:232)
 #ifndef WS_NO_DEDUP
-                            keep = !(C.contig && !(m & ~islmask[isl[low_bit(m)]]));
+                            keep = !(C.contig && !(m & ~C.at<uint64_t>(L.islfull)[isl[low_bit(m)]]));
 #endif
                         }
                     }
@@ -709,22 +714,19 @@ __global__ void __launch_bounds__(32 * kPlaceWarps, WS_PLACE_MINB) k_place(Place
     }
     for (int g = lane; g < G; g += 32) chg[g] = 0;
     __syncwarp();
-    for (int i = 0; i < C.n_isl; ++i) {  // island masks, one ballot per 32 devices
+    uint64_t* islfull = C.at<uint64_t>(L.islfull);
+    for (int i = 0; i < R.n_islands; ++i) {  // island masks, one ballot per 32 devices
         uint64_t m = 0;
         for (int base = 0; base < N; base += 32) {
             const int d = base + lane;
             m |= static_cast<uint64_t>(__ballot_sync(kFull, d < N && isl[d] == i)) << base;
         }
-        if (lane == 0) islmask[i] = m;
+        if (lane == 0) islfull[i] = m;
     }
-    for (int w = lane; w < nW; w += 32) {
-        int cur = 0;  // sequential-ablation cursor (:331-338): sum of earlier n, mod N
-        for (int e = 0; e < w_eb[w]; ++e) cur += e_n[e];
-        w_cursor[w] = cur % N;
+    for (int w = lane; w < nW; w += 32)
         for (int i = 0; i < w_ec[w]; ++i) e_wave[w_eb[w] + i] = w;
-    }
     __syncwarp();
-    for (int e = lane; e < nE; e += 32) {  // previous entry of the same MetaOp
+    for (int e = lane; e < nE; e += 32) {  // previous entry of the same entity
         int pv = -1;
         for (int j = e - 1; j >= 0; --j)
             if (e_k[j] == e_k[e]) {
@@ -733,7 +735,7 @@ __global__ void __launch_bounds__(32 * kPlaceWarps, WS_PLACE_MINB) k_place(Place
             }
         e_prev[e] = pv;
     }
-    for (int k = lane; k < K; k += 32) {  // last entry / wave of each MetaOp
+    for (int k = lane; k < K; k += 32) {  // last entry / wave of each entity
         for (int j = nE - 1; j >= 0; --j)
             if (e_k[j] == k) {
                 lastent[k] = j;
@@ -742,19 +744,53 @@ __global__ void __launch_bounds__(32 * kPlaceWarps, WS_PLACE_MINB) k_place(Place
             }
     }
     __syncwarp();
-    if (lane == 0) {
-        int contig = 1;
-        for (int i = 0; i < C.n_isl; ++i) {
-            const uint64_t m = islmask[i];
-            const uint64_t run = m ? m >> low_bit(m) : 0;
-            if (!m || (run & (run + 1))) contig = 0;
-            C.at<uint64_t>(L.isllow)[i] = m ? (1ull << low_bit(m)) - 1ull : 0;
-        }
-        ctl->i0 = contig;
-    }
-    __syncwarp();
-    C.contig = ctl->i0;
     WS_PH_STOP(tk, 0);
+    // One place() call per placement group: task-level-optimus places every
+    // task on its own device block (detail::sub_topology: islands cut to the
+    // block) with fresh state; everything else is one group over all waves.
+    const int n_pg = h.n_pg;
+    const int* r_pg_off = reinterpret_cast<const int*>(rec + A.RL.pg_off);
+    const int* r_pg_cnt = reinterpret_cast<const int*>(rec + A.RL.pg_cnt);
+    const int* r_pg_wbeg = reinterpret_cast<const int*>(rec + A.RL.pg_wbeg);
+    const int* r_pg_wn = reinterpret_cast<const int*>(rec + A.RL.pg_wn);
+    const int* r_pg_list = reinterpret_cast<const int*>(rec + A.RL.pg_list);
+    int* glist = C.at<int>(L.glist);
+    for (int grp = 0; grp < (n_pg ? n_pg : 1); ++grp) {
+        const int goff = n_pg ? r_pg_off[grp] : 0, gcnt = n_pg ? r_pg_cnt[grp] : N;
+        const int gn = n_pg ? r_pg_wn[grp] : nW;
+        for (int i = lane; i < gn; i += 32) glist[i] = n_pg ? r_pg_list[r_pg_wbeg[grp] + i] : i;
+        C.dev_off = goff;
+        C.dev_cnt = gcnt;
+        C.all = (gcnt == 64 ? ~0ull : ((1ull << gcnt) - 1ull)) << goff;
+        __syncwarp();
+        if (lane == 0) {
+            int ni = 0, contig = 1;
+            for (int i = 0; i < R.n_islands; ++i) {  // sub_topology (baselines.hpp:81-93)
+                const uint64_t m = islfull[i] & C.all;
+                if (!m) continue;
+                const uint64_t run = m >> low_bit(m);
+                if (run & (run + 1)) contig = 0;
+                islmask[ni] = m;
+                C.at<uint64_t>(L.isllow)[ni] = (1ull << low_bit(m)) - 1ull;
+                ++ni;
+            }
+            int cur = 0;  // sequential-ablation cursor (:331-338) over this call's waves
+            for (int j = 0; j < gn; ++j) {
+                const int w = glist[j];
+                w_cursor[w] = cur;
+                for (int i = 0; i < w_ec[w]; ++i) cur = (cur + e_n[w_eb[w] + i]) % gcnt;
+                variant[j] = 0;
+            }
+            ctl->i0 = contig;
+            ctl->i1 = ni;
+        }
+        __syncwarp();
+        C.contig = ctl->i0;
+        C.n_isl = ctl->i1;
+        for (int d = lane; d < N; d += 32) mem[d] = 0.0;
+        for (int g = lane; g < G; g += 32) chg[g] = 0;
+        for (int k = lane; k < K; k += 32) home[k] = -1;
+        __syncwarp();
     // depth-first search over per-wave variants with a bounded attempt budget (:409-441).
     // The reference copies the whole state per placed wave; here the state
     // before wave k is rebuilt on demand by replaying the committed entries of
@@ -762,13 +798,13 @@ __global__ void __launch_bounds__(32 * kPlaceWarps, WS_PLACE_MINB) k_place(Place
     // use disjoint devices, so per device the additions happen in the same order
     // and the doubles are identical.  Only the flow count is recorded per wave.
     int* wave_nf = C.at<int>(L.nwin) + C.n_isl;  // [W+1] after the window counts
-    long long attempts = 0, budget = nW;
+    long long attempts = 0, budget = gn;
     for (int d = 0; d < R.bt_depth; ++d) budget *= (R.bt_branching > 1 ? R.bt_branching : 1);
     const int branching = R.sequential ? 1 : R.bt_branching;
     int k = 0;
     bool dirty = false;
-    if (lane == 0) wave_nf[0] = 0;
-    while (k < nW) {
+    if (lane == 0) wave_nf[0] = C.nF;
+    while (k < gn) {
         if (++attempts > budget) {
             if (lane == 0) {
                 set_err(ctl, WS_E_BT_BUDGET, k);
@@ -781,7 +817,8 @@ __global__ void __launch_bounds__(32 * kPlaceWarps, WS_PLACE_MINB) k_place(Place
             for (int d = lane; d < N; d += 32) mem[d] = 0.0;
             for (int g = lane; g < G; g += 32) chg[g] = 0;
             __syncwarp();
-            for (int w = 0; w < k; ++w) {
+            for (int j = 0; j < k; ++j) {
+                const int w = glist[j];
                 for (int i = 0; i < w_ec[w]; ++i) {
                     const int e = w_eb[w] + i;
                     const int ke = e_k[e];
@@ -815,8 +852,9 @@ __global__ void __launch_bounds__(32 * kPlaceWarps, WS_PLACE_MINB) k_place(Place
                 return;
             }
             --k;
-            for (int i = lane; i < w_ec[k]; i += 32) {  // home[] back to "before wave k"
-                const int e = w_eb[k] + i;
+            const int wk = glist[k];
+            for (int i = lane; i < w_ec[wk]; i += 32) {  // home[] back to "before wave k"
+                const int e = w_eb[wk] + i;
                 home[e_k[e]] = e_prev[e];
             }
             if (lane == 0) variant[k]++;
@@ -824,7 +862,8 @@ __global__ void __launch_bounds__(32 * kPlaceWarps, WS_PLACE_MINB) k_place(Place
             __syncwarp();
             continue;
         }
-        const int r = p_wave(C, k, variant[k]);
+        const int wk = glist[k];
+        const int r = p_wave(C, wk, variant[k]);
         __syncwarp();
         if (r < 0) {
             if (lane == 0) write_error(A.results + p, ctl);
@@ -832,8 +871,8 @@ __global__ void __launch_bounds__(32 * kPlaceWarps, WS_PLACE_MINB) k_place(Place
         }
         if (r > 0) {
             if (lane == 0) wave_nf[k + 1] = C.nF;  // flows recorded before wave k+1
-            for (int i = lane; i < w_ec[k]; i += 32) {
-                const int e = w_eb[k] + i;
+            for (int i = lane; i < w_ec[wk]; i += 32) {
+                const int e = w_eb[wk] + i;
                 home[e_k[e]] = e;
             }
             ++k;
@@ -842,6 +881,7 @@ __global__ void __launch_bounds__(32 * kPlaceWarps, WS_PLACE_MINB) k_place(Place
             dirty = true;
         }
         __syncwarp();
+    }
     }
     WS_PH_START(te);
     p_emit(C, p, rec, A.RL, h, A);

@@ -122,7 +122,7 @@ LaunchCaps batch_caps(const ws_plan_rec* plans, int P, bool hard) {
         N = std::max(N, r.n_dev);
         IS = std::max(IS, r.n_islands);
         gmax = std::max(gmax, r.n_groups);
-        scoped |= r.strategy == WS_STRATEGY_DISTMM_MT;
+        scoped |= r.strategy == WS_STRATEGY_DISTMM_MT || r.strategy == WS_STRATEGY_TASK_OPTIMUS;
     }
     M = std::min(M, WS_MAX_MODULES);
     N = std::min(N, WS_MAX_DEVICES);

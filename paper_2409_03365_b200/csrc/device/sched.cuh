@@ -12,7 +12,8 @@ constexpr int kSchedWarps = 4;
 // ---- per-plan schedule record (global), written by k_sched, read by k_place
 struct SchedHdr {
     int ok, K, n_levels, nW;
-    int nE, scoped, pad1, pad2;  // scoped: entities are (MetaOp, task) pairs (e_met/e_task)
+    int nE, scoped, n_pg, pad2;  // scoped: entities are (MetaOp, task) pairs (e_met/e_task);
+                                 // n_pg > 0: placement groups (one place() call each, pg_*)
     double lower_bound, end_time;
 };
 
@@ -23,6 +24,7 @@ struct RecCaps {
 struct RecLayout {
     int hdr, mod_of, level, up_n, up_l, lo_n, lo_l, by_rank, idrank, pred_r, succ_r, cstar, lvl_fw, lvl_nw;
     int e_frac, e_met, e_task;  // per entity: batch_fraction, MetaOp, task (-1: the MetaOp itself)
+    int pg_off, pg_cnt, pg_wbeg, pg_wn, pg_list;  // placement groups: device block, waves (task-level-optimus)
     int w_level, w_eb, w_ec, w_start, w_dur, e_k, e_n, e_l, e_span;
     int bytes;
 };
@@ -54,6 +56,11 @@ __host__ __device__ inline RecLayout make_rec_layout(const RecCaps& c) {
     L.e_frac = take(8 * c.M);
     L.e_met = take(4 * c.M);
     L.e_task = take(4 * c.M);
+    L.pg_off = take(4 * c.M);
+    L.pg_cnt = take(4 * c.M);
+    L.pg_wbeg = take(4 * c.M);
+    L.pg_wn = take(4 * c.M);
+    L.pg_list = take(4 * c.W);
     L.w_level = take(4 * c.W);
     L.w_eb = take(4 * c.W);
     L.w_ec = take(4 * c.W);
@@ -79,6 +86,8 @@ struct SmLayout {
     // task-scoped baselines only (sizes 0 otherwise)
     int ent_met, ent_task, ent_frac, epred;                                  // [64] entities
     int ent_of, kscale, tlvl, vord;                                          // [M] per task
+    int tvalid, talloc, cw_start, cw_dur, cw_level, cw_ent, cw_n, cw_L;     // [64] optimus tasks / waves
+    int pl_off, pl_cnt, pl_wbeg, pl_wn, perm, tfin;                         // [64] placements, [M] finish
     int bytes;
 };
 
@@ -139,6 +148,20 @@ __host__ __device__ inline SmLayout make_sm_layout(int M, bool scoped = false) {
     L.kscale = take(8 * MS);
     L.tlvl = take(4 * MS);
     L.vord = take(4 * MS);
+    L.tvalid = take(8 * EM);
+    L.talloc = take(4 * EM);
+    L.cw_start = take(8 * EM);
+    L.cw_dur = take(8 * EM);
+    L.cw_level = take(4 * EM);
+    L.cw_ent = take(4 * EM);
+    L.cw_n = take(4 * EM);
+    L.cw_L = take(4 * EM);
+    L.pl_off = take(4 * EM);
+    L.pl_cnt = take(4 * EM);
+    L.pl_wbeg = take(4 * EM);
+    L.pl_wn = take(4 * EM);
+    L.perm = take(4 * EM);
+    L.tfin = take(8 * MS);
     L.bytes = (o + 15) & ~15;
     return L;
 }
@@ -1388,6 +1411,271 @@ __device__ bool s_schedule_level(SCtx& C, char* rec, const RecLayout& RL, int lv
 }
 
 // WS_SCHED_MINB: optional resident-blocks target for register tuning builds
+// ScalingCurve::eval_batch_fraction (scaling.hpp:83-86) of a fitted module curve
+__device__ __forceinline__ double eval_bf_fit(const FitOut& F, const ws_batch& B, int gm, double n, double frac) {
+    const double* pc = F.pieces + 5 * F.piece_off[gm];
+    const int np = F.npieces[gm];
+    int i = 0;
+    if (!(n < 1.0)) {
+        const double nmax = __ldg(pc + 5 * (np - 1) + 1);
+        const double x = n < nmax ? n : nmax;  // locate(std::min(n, n_max_))
+        while (i < np - 1 && !(x <= __ldg(pc + 5 * i + 1) + 1e-9)) ++i;
+    }
+    return __ldg(pc + 5 * i + 2) + __ldg(pc + 5 * i + 3) * B.mod_c[gm] + __ldg(pc + 5 * i + 4) * B.mod_w[gm] * frac / n;
+}
+
+// plan_task_level_optimus (baselines.hpp:133-321), on lane 0: per task the
+// valid allocations common to its MetaOps, tasks packed into batches by their
+// smallest allocation, marginal-gain growth of each task's block (critical
+// path of the task's sub-DAG at eval_batch_fraction), every MetaOp one wave on
+// the whole block, waves indexed by (start, entity id), one placement group
+// (device block + waves) per task.
+__device__ bool s_optimus(SCtx& C, char* rec, const RecLayout& RL, int& nW, int& nE, double& end_time, int W_CAP,
+                          int E_CAP, int& KE_out, int& npg_out) {
+    const ws_batch& B = *C.B;
+    const ws_plan_rec& R = *C.R;
+    const FitOut& F = *C.F;
+    const int K = C.K, N = C.N, lane = C.lane, T = R.n_tasks;
+    const int* by_rank = C.at<int>(C.L->by_rank);
+    const int* idrank = C.at<int>(C.L->idrank);
+    const int* gm_of = C.at<int>(C.L->gm_of);
+    const int* Lk = C.at<int>(C.L->Lk);
+    const int* level = C.at<int>(C.L->level);
+    const int* mod_of = C.at<int>(C.L->mod_of);
+    const uint64_t* pred_r = C.at<uint64_t>(C.L->pred_r);
+    const uint64_t* succ_r = C.at<uint64_t>(C.L->succ_r);
+    const uint64_t* valid = C.at<uint64_t>(C.L->valid);
+    const uint64_t* tmask = C.at<uint64_t>(C.L->tmask);
+    int* ent_met = C.at<int>(C.L->ent_met);
+    int* ent_task = C.at<int>(C.L->ent_task);
+    double* ent_frac = C.at<double>(C.L->ent_frac);
+    uint64_t* epred = C.at<uint64_t>(C.L->epred);
+    int* ent_of = C.at<int>(C.L->ent_of);
+    int* vord = C.at<int>(C.L->vord);
+    int* indeg = C.at<int>(C.L->absorb);
+    uint64_t* tvalid = C.at<uint64_t>(C.L->tvalid);
+    int* talloc = C.at<int>(C.L->talloc);
+    double* cw_start = C.at<double>(C.L->cw_start);
+    double* cw_dur = C.at<double>(C.L->cw_dur);
+    int* cw_level = C.at<int>(C.L->cw_level);
+    int* cw_ent = C.at<int>(C.L->cw_ent);
+    int* cw_n = C.at<int>(C.L->cw_n);
+    int* cw_L = C.at<int>(C.L->cw_L);
+    int* pl_off = C.at<int>(C.L->pl_off);
+    int* pl_cnt = C.at<int>(C.L->pl_cnt);
+    int* pl_wbeg = C.at<int>(C.L->pl_wbeg);
+    int* pl_wn = C.at<int>(C.L->pl_wn);
+    int* perm = C.at<int>(C.L->perm);
+    double* tfin = C.at<double>(C.L->tfin);
+    int KE = 0, ncw = 0, npl = 0;
+    for (int e = lane; e < WS_MAX_MODULES; e += 32) epred[e] = 0;
+    __syncwarp();
+    if (lane == 0) {
+        auto members = [&](int t) {  // id-rank mask of the task's MetaOps
+            const int tr = B.task_rank[R.task_begin + t];
+            uint64_t m = 0;
+            for (int k = 0; k < K; ++k)
+                if (tmask[mod_of[k]] >> tr & 1ull) m |= 1ull << idrank[k];
+            return m;
+        };
+        auto task_order = [&](uint64_t memr) {  // detail::topo_order over the task view -> vord
+            int n = 0;
+            uint64_t ready = 0;
+            for (uint64_t b = memr; b; b &= b - 1) {
+                const int k = by_rank[low_bit(b)];
+                indeg[k] = popc64(pred_r[k] & memr);
+                if (!indeg[k]) ready |= 1ull << idrank[k];
+            }
+            while (ready) {
+                const int r = low_bit(ready);
+                ready &= ready - 1;
+                const int k = by_rank[r];
+                vord[n++] = k;
+                for (uint64_t sr = succ_r[k] & memr; sr; sr &= sr - 1) {
+                    const int q = by_rank[low_bit(sr)];
+                    if (--indeg[q] == 0) ready |= 1ull << idrank[q];
+                }
+            }
+            return n;
+        };
+        auto frac_of = [&](int k) { return 1.0 / static_cast<double>(popc64(tmask[mod_of[k]])); };
+        auto task_time = [&](int t, int n) {  // critical path of the task at allocation n
+            const uint64_t memr = members(t);
+            const int nm = task_order(memr);
+            double total = 0.0;
+            for (int i = 0; i < nm; ++i) {
+                const int k = vord[i];
+                const double weight = Lk[k] * eval_bf_fit(F, B, gm_of[k], static_cast<double>(n), frac_of(k));
+                double start = 0.0;
+                for (uint64_t p = pred_r[k] & memr; p; p &= p - 1) {
+                    const double f = tfin[by_rank[low_bit(p)]];
+                    start = start < f ? f : start;
+                }
+                tfin[k] = start + weight;
+                total = total < tfin[k] ? tfin[k] : total;
+            }
+            return total;
+        };
+        for (int t = 0; t < T && !C.ctl->err; ++t) {  // common valid allocations (valid_allocations per n)
+            const int nm = task_order(members(t));
+            uint64_t tv = 0;
+            for (int n = 1; n <= N && !C.ctl->err; ++n) {
+                bool ok = true;
+                for (int i = 0; i < nm; ++i) {
+                    const int k = vord[i];
+                    const int tp = B.mod_tp[gm_of[k]];
+                    if (tp > N) {
+                        set_err(C.ctl, WS_E_TP_EXCEEDS, k, tp);
+                        break;
+                    }
+                    if (!(valid[k] >> (n - 1) & 1ull)) {
+                        ok = false;
+                        break;
+                    }
+                }
+                if (ok && !C.ctl->err) tv |= 1ull << (n - 1);
+            }
+            if (!C.ctl->err && !tv) set_err(C.ctl, WS_E_TASK_NO_VALID, t);
+            tvalid[t] = tv;
+        }
+        double batch_offset = 0.0;
+        for (int b0 = 0; b0 < T && !C.ctl->err;) {  // batches whose minimum allocations fit
+            int b1 = b0, used = 0;
+            while (b1 < T) {
+                const int need = low_bit(tvalid[b1]) + 1;
+                if (used + need > N && b1 > b0) break;
+                used += need;
+                ++b1;
+            }
+            for (int t = b0; t < b1; ++t) talloc[t] = low_bit(tvalid[t]) + 1;
+            while (true) {  // marginal gain per added device
+                int usedn = 0;
+                for (int t = b0; t < b1; ++t) usedn += talloc[t];
+                const int free = N - usedn;
+                if (free <= 0) break;
+                int best = -1, best_next = 0;
+                double best_gain = -1.0;
+                for (int t = b0; t < b1; ++t) {
+                    const uint64_t above = tvalid[t] & ~bits_upto(talloc[t] - 1);  // std::upper_bound
+                    if (!above) continue;
+                    const int nx = low_bit(above) + 1;
+                    if (nx - talloc[t] > free) continue;
+                    const double gain = (task_time(t, talloc[t]) - task_time(t, nx)) / (nx - talloc[t]);
+                    if (gain > best_gain) {
+                        best_gain = gain;
+                        best = t;
+                        best_next = nx;
+                    }
+                }
+                if (best < 0) break;
+                talloc[best] = best_next;
+            }
+            double batch_end = batch_offset;
+            int cursor = 0;
+            for (int t = b0; t < b1 && !C.ctl->err; ++t) {
+                const uint64_t memr = members(t);
+                const int nm = task_order(memr);
+                pl_off[npl] = cursor;
+                pl_cnt[npl] = talloc[t];
+                pl_wbeg[npl] = ncw;
+                cursor += talloc[t];
+                double now = batch_offset;
+                for (int i = 0; i < nm; ++i) {
+                    const int k = vord[i];
+                    if (KE >= WS_MAX_MODULES || ncw >= WS_MAX_MODULES) {
+                        set_err(C.ctl, WS_E_LIMIT_MODULES);
+                        break;
+                    }
+                    ent_met[KE] = k;
+                    ent_task[KE] = t;
+                    ent_frac[KE] = frac_of(k);  // share_fraction
+                    ent_of[k] = KE;
+                    const double span = Lk[k] * eval_bf_fit(F, B, gm_of[k], talloc[t], ent_frac[KE]);
+                    cw_start[ncw] = now;
+                    cw_dur[ncw] = span;
+                    cw_level[ncw] = level[k];
+                    cw_ent[ncw] = KE;
+                    cw_n[ncw] = talloc[t];
+                    cw_L[ncw] = Lk[k];
+                    ++ncw;
+                    ++KE;
+                    now += span;
+                }
+                pl_wn[npl] = ncw - pl_wbeg[npl];
+                ++npl;
+                for (int i = 0; i < nm; ++i) {  // the task's edges between its entities (deps, scoped)
+                    const int k = vord[i];
+                    for (uint64_t pr = pred_r[k] & memr; pr; pr &= pr - 1)
+                        epred[ent_of[k]] |= 1ull << ent_of[by_rank[low_bit(pr)]];
+                }
+                batch_end = batch_end < now ? now : batch_end;
+            }
+            batch_offset = batch_end;
+            b0 = b1;
+        }
+        if (!C.ctl->err && (ncw > W_CAP || ncw > E_CAP))
+            set_err(C.ctl, ncw > W_CAP ? WS_E_LIMIT_WAVES : WS_E_LIMIT_ENTRIES);
+        if (!C.ctl->err) {
+            auto wless = [&](int a, int b) {  // (start, id of the wave's entry)
+                if (cw_start[a] != cw_start[b]) return cw_start[a] < cw_start[b];
+                const int ea = cw_ent[a], eb = cw_ent[b];
+                return scoped_less(ent_met[ea], B.task_rank[R.task_begin + ent_task[ea]], ent_met[eb],
+                                   B.task_rank[R.task_begin + ent_task[eb]]);
+            };
+            for (int i = 0; i < ncw; ++i) {  // insertion sort (a strict total order: stable or not alike)
+                const int v = i;
+                int j = i;
+                while (j > 0 && wless(v, perm[j - 1])) perm[j] = perm[j - 1], --j;
+                perm[j] = v;
+            }
+            int* w_level = reinterpret_cast<int*>(rec + RL.w_level);
+            int* w_eb = reinterpret_cast<int*>(rec + RL.w_eb);
+            int* w_ec = reinterpret_cast<int*>(rec + RL.w_ec);
+            double* w_start = reinterpret_cast<double*>(rec + RL.w_start);
+            double* w_dur = reinterpret_cast<double*>(rec + RL.w_dur);
+            int* e_k = reinterpret_cast<int*>(rec + RL.e_k);
+            int* e_n = reinterpret_cast<int*>(rec + RL.e_n);
+            int* e_l = reinterpret_cast<int*>(rec + RL.e_l);
+            double* e_span = reinterpret_cast<double*>(rec + RL.e_span);
+            double end = 0.0;
+            for (int i = 0; i < ncw; ++i) {
+                const int c = perm[i];
+                w_level[i] = cw_level[c];
+                w_eb[i] = i;
+                w_ec[i] = 1;
+                w_start[i] = cw_start[c];
+                w_dur[i] = cw_dur[c];
+                e_k[i] = cw_ent[c];
+                e_n[i] = cw_n[c];
+                e_l[i] = cw_L[c];
+                e_span[i] = cw_dur[c];
+                const double fin = cw_start[c] + cw_dur[c];
+                end = end < fin ? fin : end;
+            }
+            end_time = end;
+            int* pg_off = reinterpret_cast<int*>(rec + RL.pg_off);
+            int* pg_cnt = reinterpret_cast<int*>(rec + RL.pg_cnt);
+            int* pg_wbeg = reinterpret_cast<int*>(rec + RL.pg_wbeg);
+            int* pg_wn = reinterpret_cast<int*>(rec + RL.pg_wn);
+            int* pg_list = reinterpret_cast<int*>(rec + RL.pg_list);
+            for (int i = 0; i < ncw; ++i) pg_list[perm[i]] = i;  // created wave -> global index
+            for (int q = 0; q < npl; ++q) {  // pg_list[created wave] = its global index
+                pg_off[q] = pl_off[q];
+                pg_cnt[q] = pl_cnt[q];
+                pg_wbeg[q] = pl_wbeg[q];
+                pg_wn[q] = pl_wn[q];
+            }
+        }
+    }
+    __syncwarp();
+    if (C.ctl->err) return false;
+    nW = nE = __shfl_sync(kFull, ncw, 0);
+    KE_out = __shfl_sync(kFull, KE, 0);
+    npg_out = __shfl_sync(kFull, npl, 0);
+    end_time = __shfl_sync(kFull, end_time, 0);
+    return true;
+}
+
 // plan_distmm_mt (baselines.hpp:323-413): tasks in declaration order; inside
 // a task (task_view: members, in-task edges, lexicographic topological order,
 // longest-path task levels), a level of one MetaOp runs alone on its largest
@@ -1586,7 +1874,8 @@ __device__ __forceinline__ void sched_body(const SchedArgs& A, char* smem_dyn, C
     if (slot >= A.n_launch) return;
     if (A.n_ids && slot >= *A.n_ids) return;
     const int p = A.plan_ids[slot];
-    if ((A.B.plans[p].strategy == WS_STRATEGY_DISTMM_MT) != SCOPED) return;  // the other instance's plan
+    const int strat = A.B.plans[p].strategy;
+    if ((strat == WS_STRATEGY_DISTMM_MT || strat == WS_STRATEGY_TASK_OPTIMUS) != SCOPED) return;  // the other instance's
     Ctl* ctl = &ctl_s[wid];
     if (lane == 0) *ctl = Ctl{};
     __syncwarp();
@@ -1622,7 +1911,7 @@ __device__ __forceinline__ void sched_body(const SchedArgs& A, char* smem_dyn, C
     WS_PH_STOP(tg, 10);
     if (ok) ok = s_fit_status(C);
     const bool decoupled = R.strategy == WS_STRATEGY_DECOUPLED_SEQUENTIAL;
-    constexpr bool scoped = SCOPED;
+    constexpr bool scoped = SCOPED;  // task-scoped baselines: distmm-mt, task-level-optimus
     if (ok && scoped && !A.scoped_ok) {  // launch built without the task-scoped working set
         ok = false;
         if (lane == 0) ctl->err = WS_E_LIMIT_MODULES;
@@ -1630,12 +1919,17 @@ __device__ __forceinline__ void sched_body(const SchedArgs& A, char* smem_dyn, C
     }
     if (ok) ok = s_valid(C, !decoupled && !scoped);
     WS_PH_STOP(tg, 11);
-    int n_levels = 0, nW = 0, nE = 0, KE = 0;
+    int n_levels = 0, nW = 0, nE = 0, KE = 0, n_pg = 0;
     double lower_bound = 0.0, offset = 0.0;
     if (ok && decoupled) {
         ok = s_decoupled(C, rec, A.RL, nW, nE, offset, A.caps.W, A.caps.E);
     } else if (ok && scoped) {
-        if constexpr (SCOPED) ok = s_distmm(C, rec, A.RL, nW, nE, offset, A.caps.W, A.caps.E, KE);
+        if constexpr (SCOPED) {
+            if (R.strategy == WS_STRATEGY_TASK_OPTIMUS)
+                ok = s_optimus(C, rec, A.RL, nW, nE, offset, A.caps.W, A.caps.E, KE, n_pg);
+            else
+                ok = s_distmm(C, rec, A.RL, nW, nE, offset, A.caps.W, A.caps.E, KE);
+        }
     } else if (ok) {
         n_levels = ctl->i1;
         double* cstar = reinterpret_cast<double*>(rec + A.RL.cstar);
@@ -1750,6 +2044,7 @@ __device__ __forceinline__ void sched_body(const SchedArgs& A, char* smem_dyn, C
         h.ok = 1;
         h.K = K;
         h.scoped = scoped ? 1 : 0;
+        h.n_pg = n_pg;
         h.n_levels = n_levels;
         h.nW = nW;
         h.nE = nE;

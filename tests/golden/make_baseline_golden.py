@@ -28,7 +28,7 @@ import pyoracle as po  # noqa: E402
 from edge_cases import cases as edge_cases  # noqa: E402
 from make_golden import CONFIGS, SUITE, VARIANTS  # noqa: E402
 
-STRATEGIES = ["decoupled-sequential", "distmm-mt"]
+STRATEGIES = ["decoupled-sequential", "distmm-mt", "task-level-optimus"]
 
 
 def main() -> None:
