@@ -17,6 +17,7 @@
 #pragma once
 
 #include <cstdint>
+#include <exception>
 #include <map>
 #include <memory>
 #include <optional>
@@ -382,6 +383,72 @@ std::string sim_text(const Problem& prob, const ws_plan_result& res, const std::
 std::string sim_text_named(const ClusterTopology& topo, const ws_plan_result& res, const ws_sim_result& sim,
                            const std::uint8_t* sim_arena, const std::vector<std::string>& names);
 [[noreturn]] void throw_result_error(const Problem& prob, const ws_plan_result& res);
+
+// Entity ids of a planned record ("m<k>", or "m<k>@<task>" for task-scoped strategies)
+// and validate_plan's messages for its evaluation (the first WS_SIM_MAX_VIOLATIONS).
+std::vector<std::string> record_entity_names(const Problem& prob, const ws_plan_result& res,
+                                             const std::uint8_t* plan_arena);
+std::vector<std::string> violation_messages(const ClusterTopology& topo, const ws_plan_result& res,
+                                            const ws_sim_result& sim, const std::uint8_t* sim_arena,
+                                            const std::vector<std::string>& names);
+
+// ---- strategies, comparison and dynamic re-planning (cli.hpp:163-327) ---------------------
+// The strategies in the reference's order (all_strategies, cli.hpp:237-241).
+const std::vector<std::string>& all_strategies();
+// ws_strategy id of a strategy name; ParseError("unknown strategy '<s>'") otherwise.
+int strategy_id(const std::string& strategy);
+// Drop-in for plan_for_strategy (cli.hpp:163-171): the plan of one strategy,
+// planned on the device through the default context.
+ExecutionPlan plan_for_strategy(const std::string& strategy, const WorkloadSpec& spec, const ClusterTopology& topo,
+                                const PlannerOptions& opt);
+
+// One strategy's plan and its simulated iteration time (simulate_plan(plan).makespan).
+struct StrategyRun {
+    std::string strategy;
+    ExecutionPlan plan;
+    double makespan = 0.0;
+};
+
+// cmd_compare (cli.hpp:243-264) without the file I/O: every strategy planned,
+// validated and simulated on the device in one batch.  Throws what the
+// reference throws, in its order (the first strategy's planning error, or
+// InvariantError "strategy <s> produced an invalid plan: <first violation>").
+// `table` is compare.csv.
+struct CompareReport {
+    std::vector<StrategyRun> runs;
+    std::string table;
+};
+CompareReport compare_strategies(const WorkloadSpec& spec, const ClusterTopology& topo, const PlannerOptions& opt);
+
+// Dynamic re-planning (cmd_dynamic, cli.hpp:269-327): a sequence file of
+// `phase workload=<path> iters=<k>` lines.
+struct SequencePhase {
+    std::string workload;
+    int iters = 1;
+};
+std::vector<SequencePhase> parse_sequence(const std::string& text);
+
+// Every (phase, strategy) pair planned in ONE device batch and simulated in one
+// k_sim launch.  `table` is dynamic.csv, `summary` cumulative.csv.  A phase
+// whose workload failed to load is passed as a null spec with its exception in
+// `load_errors[p]`; errors surface in the reference's (phase, strategy) order.
+struct DynamicReport {
+    std::vector<std::vector<StrategyRun>> phases;
+    std::string table;
+    std::string summary;
+};
+DynamicReport dynamic_replan(const std::vector<const WorkloadSpec*>& phases, const std::vector<int>& iters,
+                             const ClusterTopology& topo, const PlannerOptions& opt,
+                             const std::vector<std::exception_ptr>& load_errors = {});
+
+// The CLI commands themselves (cli.hpp:243-327), with the reference's file
+// outputs under `out_dir` (compare.csv; phase<p>.<strategy>.plan.txt, dynamic.csv,
+// cumulative.csv).  Paths ending in ".json" load through workload_from_json /
+// topology_from_json (cli.hpp:117-130).  Return the text the command prints.
+std::string cmd_compare(const std::string& workload_path, const std::string& topology_path,
+                        const std::string& out_dir, const PlannerOptions& opt);
+std::string cmd_dynamic(const std::string& sequence_path, const std::string& topology_path,
+                        const std::string& out_dir, const PlannerOptions& opt);
 
 // Deterministic scenario generator (scenarios.hpp restated): the measurement
 // input source.  Returns workload + topology built directly (no text pass).

@@ -92,6 +92,21 @@ void wsx_host_free(void* p);
  * plan text, or "error <Class>: <what>\n". */
 char* wsx_plan_workload_text(const char* workload, const char* topology, const ws_options* o);
 
+/* plan_for_strategy (cli.hpp:163-171) on reference text inputs: plan text, or
+ * "error <Class>: <what>\n". */
+char* wsx_plan_strategy_text(const char* workload, const char* topology, const char* strategy,
+                             const ws_options* o);
+
+/* The reference's compare / dynamic commands (cli.hpp:243-327) over the device
+ * planner + evaluator: all (phase, strategy) pairs in one planning batch and one
+ * evaluation launch.  Writes the reference's files under out_dir and returns the
+ * text the command prints, or "error <Class>: <what>\n" (exit codes 2/3/4 by
+ * class, cli.hpp:330-344). */
+char* wsx_cmd_compare(const char* workload_path, const char* topology_path, const char* out_dir,
+                      const ws_options* o);
+char* wsx_cmd_dynamic(const char* sequence_path, const char* topology_path, const char* out_dir,
+                      const ws_options* o);
+
 #ifdef __cplusplus
 }
 #endif

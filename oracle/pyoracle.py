@@ -133,6 +133,10 @@ def ref():
         lib.wsref_strategy_plan_text.argtypes = [C.c_char_p, C.c_char_p, C.c_char_p, C.POINTER(RefOpts)]
         lib.wsref_sweep_bench_strategy.restype = C.c_double
         lib.wsref_sweep_bench_strategy.argtypes = [C.c_long, C.c_long, C.c_int, C.c_int]
+        lib.wsref_cmd.restype = vp
+        lib.wsref_cmd.argtypes = [C.c_int, C.c_char_p, C.c_char_p, C.c_char_p, C.c_double, C.c_int, C.c_ulonglong]
+        lib.wsref_sweep_workload.restype = vp
+        lib.wsref_sweep_workload.argtypes = [C.c_long, C.POINTER(vp)]
         lib.wsref_latency_ms.restype = C.c_double
         lib.wsref_latency_ms.argtypes = [C.c_char_p, C.c_int, C.c_int, C.c_int]
         _ref = lib
@@ -204,3 +208,19 @@ def ref_sweep_bench_strategy(start: int, count: int, threads: int, strategy: str
 
 def ref_latency_ms(name: str, tasks: int, devices: int, reps: int) -> float:
     return ref().wsref_latency_ms(name.encode(), tasks, devices, reps)
+
+
+def ref_cmd(command: str, input_path: str, topology_path: str, out_dir: str, eps: float = 1e-7,
+            bt_depth: int = 2, seed: int = 0) -> str:
+    """The reference's own cmd_compare / cmd_dynamic (cli.hpp:243-327): what it
+    prints, or "error <Class>: <what>"; files land under out_dir."""
+    which = {"compare": 0, "dynamic": 1}[command]
+    return _s(ref().wsref_cmd(which, input_path.encode(), topology_path.encode(), out_dir.encode(), eps, bt_depth,
+                              seed))
+
+
+def ref_sweep_workload(i: int) -> tuple[str, str]:
+    """Workload + topology text of sweep mixture i."""
+    t = C.c_void_p()
+    w = ref().wsref_sweep_workload(i, C.byref(t))
+    return _s(w), _s(t)

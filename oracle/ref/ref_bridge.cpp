@@ -7,6 +7,8 @@
 #include <chrono>
 #include <cstdlib>
 #include <cstring>
+#include <iostream>
+#include <sstream>
 #include <string>
 #include <thread>
 #include <vector>
@@ -373,6 +375,47 @@ double wsref_sweep_bench_strategy(long start, long count, int threads, int strat
     for (auto& th : pool) th.join();
     return static_cast<double>(count) /
            std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
+
+// The reference's own compare / dynamic commands (cli.hpp:243-327), run as
+// the CLI runs them (files under out_dir); returns what they print, or
+// "error <Class>: <what>" for the exception run_command would map to an exit code.
+char* wsref_cmd(int which, const char* input, const char* topology, const char* out_dir, double eps,
+                int backtrack_depth, unsigned long long seed) {
+    CliOptions cli;
+    (which == 0 ? cli.workload : cli.sequence) = input;
+    cli.topology = topology;
+    cli.out = out_dir;
+    cli.eps = eps;
+    cli.backtrack_depth = backtrack_depth;
+    cli.seed = seed;
+    std::ostringstream captured;
+    std::streambuf* old = std::cout.rdbuf(captured.rdbuf());
+    std::string result;
+    try {
+        if (which == 0)
+            cmd_compare(cli);
+        else
+            cmd_dynamic(cli);
+        result = captured.str();
+    } catch (const std::exception& e) {
+        const char* cls = "Error";
+        if (dynamic_cast<const CyclicWorkload*>(&e)) cls = "CyclicWorkload";
+        else if (dynamic_cast<const UnknownModule*>(&e)) cls = "UnknownModule";
+        else if (dynamic_cast<const EmptyWorkload*>(&e)) cls = "EmptyWorkload";
+        else if (dynamic_cast<const InsufficientProfile*>(&e)) cls = "InsufficientProfile";
+        else if (dynamic_cast<const ParseError*>(&e)) cls = "ParseError";
+        else if (dynamic_cast<const DegenerateFit*>(&e)) cls = "DegenerateFit";
+        else if (dynamic_cast<const NoValidAllocation*>(&e)) cls = "NoValidAllocation";
+        else if (dynamic_cast<const PlacementInfeasible*>(&e)) cls = "PlacementInfeasible";
+        else if (dynamic_cast<const OutOfRange*>(&e)) cls = "OutOfRange";
+        else if (dynamic_cast<const EmptyLevel*>(&e)) cls = "EmptyLevel";
+        else if (dynamic_cast<const InvariantError*>(&e)) cls = "InvariantError";
+        else if (dynamic_cast<const InfeasibleError*>(&e)) cls = "InfeasibleError";
+        result = std::string("error ") + cls + ": " + e.what() + "\n";
+    }
+    std::cout.rdbuf(old);
+    return dup(result);
 }
 
 // Single-plan latency of the reference planner (median of `reps`, ms).

@@ -185,6 +185,9 @@ def _load() -> C.CDLL:
         "ws_sim_arena_bound": (u64, [vp]),
         "ws_last_sim_ms": (C.c_double, [vp]),
         "wsx_host_free": (None, [vp]),
+        "wsx_plan_strategy_text": (vp, [C.c_char_p, C.c_char_p, C.c_char_p, C.POINTER(Options)]),
+        "wsx_cmd_compare": (vp, [C.c_char_p, C.c_char_p, C.c_char_p, C.POINTER(Options)]),
+        "wsx_cmd_dynamic": (vp, [C.c_char_p, C.c_char_p, C.c_char_p, C.POINTER(Options)]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -515,3 +518,30 @@ def plan_workload(workload: str, topology: str, **opts) -> str:
     write_plan() text of the plan, or raises the reference's exception class."""
     return raise_for_text(_take_str(lib.wsx_plan_workload_text(workload.encode(), topology.encode(),
                                                                C.byref(make_options(**opts)))))
+
+
+def plan_for_strategy(strategy: str, workload: str, topology: str, **opts) -> str:
+    """Drop-in for wavesched::plan_for_strategy (cli.hpp:163-171) on reference
+    text inputs: the write_plan() text of the strategy's plan, or the reference's
+    exception (ParseError "unknown strategy '<s>'" for an unknown name)."""
+    return raise_for_text(_take_str(lib.wsx_plan_strategy_text(workload.encode(), topology.encode(),
+                                                               strategy.encode(), C.byref(make_options(**opts)))))
+
+
+def compare(workload_path: str, topology_path: str, out_dir: str = "out", **opts) -> str:
+    """The reference's `compare` command (cmd_compare, cli.hpp:243-264): every
+    strategy planned, validated and simulated -- all four in one device batch
+    and one evaluation launch.  Writes out_dir/compare.csv and returns the table
+    it prints; raises the reference's exception otherwise."""
+    return raise_for_text(_take_str(lib.wsx_cmd_compare(str(workload_path).encode(), str(topology_path).encode(),
+                                                        str(out_dir).encode(), C.byref(make_options(**opts)))))
+
+
+def dynamic(sequence_path: str, topology_path: str, out_dir: str = "out", **opts) -> str:
+    """The reference's dynamic re-planning command (cmd_dynamic, cli.hpp:269-327):
+    a sequence file of `phase workload=<path> iters=<k>` lines, every (phase,
+    strategy) pair planned in one device batch and simulated in one launch.
+    Writes phase<p>.<strategy>.plan.txt, dynamic.csv and cumulative.csv under
+    out_dir and returns the cumulative table it prints."""
+    return raise_for_text(_take_str(lib.wsx_cmd_dynamic(str(sequence_path).encode(), str(topology_path).encode(),
+                                                        str(out_dir).encode(), C.byref(make_options(**opts)))))

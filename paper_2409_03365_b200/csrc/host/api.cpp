@@ -7,6 +7,7 @@
 #include <deque>
 #include <mutex>
 
+#include "internal.hpp"
 #include "wsgpu/planner.hpp"
 #include "wsgpu/wsx.h"
 
@@ -59,13 +60,10 @@ DefaultCtx& default_ctx() {
     return d;
 }
 
-struct Planned {
-    std::vector<ws_plan_result> res;
-    std::vector<std::uint8_t> arena;
-};
+}  // namespace
 
-// Plans a problem list on `ctx`; plans whose record overflowed the arena are
-// re-planned alone with a large arena.
+namespace detail {
+
 Planned plan_on(ws_ctx* ctx, const std::vector<Problem>& probs) {
     Planned out;
     EncodedBatch eb = encode_batch(probs, true);
@@ -91,7 +89,37 @@ Planned plan_on(ws_ctx* ctx, const std::vector<Problem>& probs) {
     return out;
 }
 
-}  // namespace
+ws_ctx* default_ctx_locked(std::unique_lock<std::mutex>& lock) {
+    DefaultCtx& d = default_ctx();
+    lock = std::unique_lock<std::mutex>(d.mu);
+    ws_ctx* ctx = d.get();
+    if (!ctx) throw Error(d.error);
+    return ctx;
+}
+
+const char* error_class(const std::exception& e) {
+    if (dynamic_cast<const CyclicWorkload*>(&e)) return "CyclicWorkload";
+    if (dynamic_cast<const UnknownModule*>(&e)) return "UnknownModule";
+    if (dynamic_cast<const EmptyWorkload*>(&e)) return "EmptyWorkload";
+    if (dynamic_cast<const InsufficientProfile*>(&e)) return "InsufficientProfile";
+    if (dynamic_cast<const ParseError*>(&e)) return "ParseError";
+    if (dynamic_cast<const DegenerateFit*>(&e)) return "DegenerateFit";
+    if (dynamic_cast<const NoValidAllocation*>(&e)) return "NoValidAllocation";
+    if (dynamic_cast<const PlacementInfeasible*>(&e)) return "PlacementInfeasible";
+    if (dynamic_cast<const OutOfRange*>(&e)) return "OutOfRange";
+    if (dynamic_cast<const EmptyLevel*>(&e)) return "EmptyLevel";
+    if (dynamic_cast<const InvariantError*>(&e)) return "InvariantError";
+    if (dynamic_cast<const InfeasibleError*>(&e)) return "InfeasibleError";
+    if (dynamic_cast<const LimitExceeded*>(&e)) return "LimitExceeded";
+    return "Error";
+}
+
+char* dup_c(const std::string& s) { return dup(s); }
+
+}  // namespace detail
+
+using detail::Planned;
+using detail::plan_on;
 
 PlannerResult plan_workload(const WorkloadSpec& spec, const ClusterTopology& topo, const PlannerOptions& opt) {
     validate_workload(spec);  // host-side checks first, as build_graph does (graph.hpp:98)

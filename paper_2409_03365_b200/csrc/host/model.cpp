@@ -394,6 +394,25 @@ ClusterTopology parse_topology(const std::string& text) {
     return t;
 }
 
+// Dynamic re-planning sequence (cmd_dynamic, cli.hpp:283-297).
+std::vector<SequencePhase> parse_sequence(const std::string& text) {
+    std::vector<SequencePhase> phases;
+    std::istringstream is(text);
+    std::string line;
+    int lineno = 0;
+    while (std::getline(is, line)) {
+        ++lineno;
+        if (blank_or_comment(line)) continue;
+        const std::vector<std::string> toks = tokens_of(line);
+        const std::string where = "sequence line " + std::to_string(lineno);
+        if (toks[0] != "phase") throw ParseError(where + ": expected 'phase ...'");
+        Fields f(toks, 1, where);
+        phases.push_back({f.str("workload"), static_cast<int>(f.num_or("iters", 1))});
+    }
+    if (phases.empty()) throw ParseError("dynamic sequence declares no phases");
+    return phases;
+}
+
 std::string dump_topology(const ClusterTopology& topo) {
     std::string out;
     for (std::size_t i = 0; i < topo.islands.size(); ++i) {

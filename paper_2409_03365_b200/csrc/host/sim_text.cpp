@@ -66,9 +66,8 @@ std::string violation_text(const ws_out_violation& v, const ClusterTopology& top
 
 }  // namespace
 
-std::string sim_text(const Problem& prob, const ws_plan_result& r, const std::uint8_t* plan_arena,
-                     const ws_sim_result& s, const std::uint8_t* sim_arena) {
-    if (r.status != WS_STATUS_OK) return plan_text_or_error(prob, r, plan_arena);
+std::vector<std::string> record_entity_names(const Problem& prob, const ws_plan_result& r,
+                                             const std::uint8_t* plan_arena) {
     std::vector<std::string> names;
     if (r.n_scopes > 0) {  // task-scoped entities "m<metaop>@<task id>": the record's last section
         auto a8 = [](std::size_t v) { return (v + 7) & ~std::size_t(7); };
@@ -84,7 +83,28 @@ std::string sim_text(const Problem& prob, const ws_plan_result& r, const std::ui
     } else {
         for (int k = 0; k < r.n_metaops; ++k) names.push_back(mid(k));
     }
-    return sim_text_named(*prob.topo, r, s, sim_arena, names);
+    return names;
+}
+
+std::vector<std::string> violation_messages(const ClusterTopology& topo, const ws_plan_result& r,
+                                            const ws_sim_result& s, const std::uint8_t* sim_arena,
+                                            const std::vector<std::string>& names) {
+    std::vector<std::string> out;
+    if (s.status != WS_STATUS_OK) return out;
+    const std::size_t o_viol = 16ull * topo.devices.size() + 16 + 8ull * r.n_metaops;
+    const int nv = std::min(s.n_violations, WS_SIM_MAX_VIOLATIONS);
+    for (int i = 0; i < nv; ++i) {
+        ws_out_violation v;
+        std::memcpy(&v, sim_arena + s.offset + o_viol + sizeof(ws_out_violation) * i, sizeof(v));
+        out.push_back(violation_text(v, topo, names));
+    }
+    return out;
+}
+
+std::string sim_text(const Problem& prob, const ws_plan_result& r, const std::uint8_t* plan_arena,
+                     const ws_sim_result& s, const std::uint8_t* sim_arena) {
+    if (r.status != WS_STATUS_OK) return plan_text_or_error(prob, r, plan_arena);
+    return sim_text_named(*prob.topo, r, s, sim_arena, record_entity_names(prob, r, plan_arena));
 }
 
 std::string sim_text_named(const ClusterTopology& topo, const ws_plan_result& r, const ws_sim_result& s,
@@ -111,7 +131,7 @@ std::string sim_text_named(const ClusterTopology& topo, const ws_plan_result& r,
                       " inter=" + fmt_exact(s.total_inter_island_bytes) +
                       " timeline=" + std::to_string(s.timeline_items) + "\n";
     const std::size_t o_busy = 0, o_bmask = 8ull * N, o_mem = 8ull * N + 8, o_util = 16ull * N + 8,
-                      o_umask = 16ull * N + 8 + 8ull * K, o_viol = 16ull * N + 16 + 8ull * K;
+                      o_umask = 16ull * N + 8 + 8ull * K;
     const std::uint64_t bmask = u64(o_bmask), umask = u64(o_umask);
     out += "busy";
     for (int d = 0; d < N; ++d)
@@ -125,12 +145,7 @@ std::string sim_text_named(const ClusterTopology& topo, const ws_plan_result& r,
     std::sort(ids.begin(), ids.end(), [&](int a, int c) { return name(a) < name(c); });
     for (int k : ids) out += " " + name(k) + "=" + fmt_exact(f64(o_util + 8ull * k));
     out += "\nvalid " + std::to_string(s.valid) + " " + std::to_string(s.n_violations) + "\n";
-    const int nv = std::min(s.n_violations, WS_SIM_MAX_VIOLATIONS);
-    for (int i = 0; i < nv; ++i) {
-        ws_out_violation v;
-        std::memcpy(&v, b + o_viol + sizeof(ws_out_violation) * i, sizeof(v));
-        out += "v " + violation_text(v, topo, names) + "\n";
-    }
+    for (const std::string& m : violation_messages(topo, r, s, sim_arena, names)) out += "v " + m + "\n";
     return out;
 }
 
