@@ -298,7 +298,7 @@ def main() -> None:
 
     # ---- baseline planners on the device, same shard ----
     baselines = {}
-    for strategy in ("decoupled-sequential", "distmm-mt"):
+    for strategy in ("decoupled-sequential", "task-level-optimus", "distmm-mt"):
         pb = ws.ProblemSet()
         for i in idx:
             pb.add_sweep(i, 1, strategy=strategy)
