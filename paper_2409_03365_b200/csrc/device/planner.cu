@@ -191,10 +191,16 @@ struct ws_ctx {
     uint64_t top_cap = 0;
     DevBuf chunk_tops;
     cudaStream_t stream3 = nullptr;          // D2H side of the host pipeline (stream2: H2D side)
+    cudaStream_t stream4 = nullptr;          // second compute stream of the host pipeline
+    DevBuf recs_r2, flows_r2, retry_ids2;    // its retry-pass buffers
     unsigned long long* host_tops = nullptr; // page-locked: chunk bases, chunk tops, final top
-    // measured (100k sweep): 1 chunk 27.8 ms, 2: 27.7, 4: 32.4, 8: 35.1 -- every
-    // chunk adds a k_sched + k_place launch tail that outweighs the hidden copies
-    int host_chunks = 1;                     // $WSGPU_HOST_CHUNKS
+    // measured (100k sweep, ms): one compute stream: 1 chunk 27.8, 2: 27.4, 4: 32.0 (each
+    // chunk's k_sched + k_place launch tail outweighs the hidden copies); two compute
+    // streams (consecutive chunks fill each other's tails): 3 uniform 25.5, weights
+    // 1,3,1 23.5, 1,3,3,1 23.9, 1,6,1 25.5, 1,2,2,2,1 25.0 -> default 1,3,1 x 2 streams
+    int host_chunks = 3;                     // $WSGPU_HOST_CHUNKS
+    int host_streams = 2;                    // $WSGPU_HOST_STREAMS (1 or 2)
+    std::vector<double> host_weights{1, 3, 1};  // $WSGPU_HOST_WEIGHTS: relative chunk sizes (sets the chunk count)
     ws_plan_result* res_out() { return d_results ? d_results : results.as<ws_plan_result>(); }
     uint8_t* arena_out() { return d_arena ? d_arena : arena.as<uint8_t>(); }
     uint64_t cap_out() const { return d_arena ? d_cap : arena_cap; }
@@ -373,12 +379,28 @@ int ws_ctx_create(int device, ws_ctx** out) {
         return 1;
     }
     if (cudaStreamCreateWithFlags(&c->stream3, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&c->stream4, cudaStreamNonBlocking) != cudaSuccess ||
         cudaMallocHost(reinterpret_cast<void**>(&c->host_tops), 8 * (2 * kMaxHostChunks + 8)) != cudaSuccess) {
         delete c;
         return 1;
     }
     if (const char* env = std::getenv("WSGPU_CHUNKS")) c->chunks = std::atoi(env);
-    if (const char* env = std::getenv("WSGPU_HOST_CHUNKS")) c->host_chunks = std::atoi(env);
+    if (const char* env = std::getenv("WSGPU_HOST_CHUNKS")) {
+        c->host_chunks = std::atoi(env);
+        c->host_weights.clear();  // uniform chunks
+    }
+    if (const char* env = std::getenv("WSGPU_HOST_WEIGHTS")) {
+        c->host_weights.clear();
+        for (const char* q = env; *q;) {
+            char* end = nullptr;
+            const double w = std::strtod(q, &end);
+            if (end == q) break;
+            if (w > 0) c->host_weights.push_back(w);
+            q = *end == ',' ? end + 1 : end;
+        }
+        if (!c->host_weights.empty()) c->host_chunks = static_cast<int>(c->host_weights.size());
+    }
+    if (const char* env = std::getenv("WSGPU_HOST_STREAMS")) c->host_streams = std::max(1, std::min(2, std::atoi(env)));
     *out = c;
     return 0;
 }
@@ -393,6 +415,7 @@ void ws_ctx_destroy(ws_ctx* c) {
     if (c->stream) cudaStreamDestroy(c->stream);
     if (c->stream2) cudaStreamDestroy(c->stream2);
     if (c->stream3) cudaStreamDestroy(c->stream3);
+    if (c->stream4) cudaStreamDestroy(c->stream4);
     if (c->host_tops) cudaFreeHost(c->host_tops);
     delete c;
 }
@@ -545,14 +568,16 @@ int ws_fetch_results(ws_ctx* ctx, ws_plan_result* results, uint8_t* arena, uint6
 
 extern "C" uint64_t wsi_arena_bound_plans(const ws_plan_rec* plans, int n);
 
-// Host batch in, host results out.  Default: stage (one H2D copy), plan on the
-// device, fetch (results + used arena, two D2H copies).  Optionally
-// ($WSGPU_HOST_CHUNKS > 1) as a pipeline over C chunks of plans:
-// the H2D copy of chunk c+1 (its byte ranges of every SoA section: sections
-// are plan-ordered, so a chunk's rows are contiguous) and the D2H copy of
-// chunk c-1 (results rows + its own arena region) overlap the kernels of
-// chunk c.  Kernels always write device memory (zero-copy writes into host
-// memory stall k_place on PCIe: measured 20 ms vs 11 ms per 100k).
+// Host batch in, host results out.  Batches of >= 3 x 4096 plans run as a
+// pipeline over chunks of plans (default sizes 1:3:1, $WSGPU_HOST_WEIGHTS /
+// $WSGPU_HOST_CHUNKS): the H2D copy of chunk c+1 (its byte ranges of every SoA
+// section: sections are plan-ordered, so a chunk's rows are contiguous) and the
+// D2H copy of chunk c-1 (results rows + its own arena region) overlap the
+// kernels of chunk c, and consecutive chunks alternate between two compute
+// streams so each fills the other's launch tail.  Smaller batches: stage (one
+// H2D copy), plan, fetch (two D2H copies).  Kernels always write device memory
+// (zero-copy writes into host memory stall k_place on PCIe: measured 20 ms vs
+// 11 ms per 100k).
 int ws_plan_batch_host(ws_ctx* ctx, const ws_batch* in, ws_plan_result* results, uint8_t* arena,
                        uint64_t arena_cap, uint64_t* arena_used, void* stream) {
     cudaSetDevice(ctx->device);
@@ -577,7 +602,15 @@ int ws_plan_batch_host(ws_ctx* ctx, const ws_batch* in, ws_plan_result* results,
     uint64_t abase[kMaxHostChunks + 1];
     abase[0] = 0;
     ctx->order_host.resize(P);
-    for (int c = 0; c <= C; ++c) pb[c] = static_cast<int>(static_cast<int64_t>(P) * c / C);
+    // chunk boundaries: uniform, or proportional to $WSGPU_HOST_WEIGHTS ("1,3,3,1": small
+    // first/last chunks shorten the exposed first H2D and last D2H copies)
+    double wsum = 0, wacc = 0;
+    for (int c = 0; c < C; ++c) wsum += c < static_cast<int>(ctx->host_weights.size()) ? ctx->host_weights[c] : 1.0;
+    pb[0] = 0;
+    for (int c = 0; c < C; ++c) {
+        wacc += c < static_cast<int>(ctx->host_weights.size()) ? ctx->host_weights[c] : 1.0;
+        pb[c + 1] = c + 1 == C ? P : std::max(pb[c] + 1, std::min(P - (C - 1 - c), static_cast<int>(P * (wacc / wsum))));
+    }
     for (int c = 0; c < C; ++c) {
         abase[c + 1] = abase[c] + wsi_arena_bound_plans(in->plans + pb[c], pb[c + 1] - pb[c]);
         lpt_order(ctx, in->plans, pb[c], pb[c + 1]);
@@ -635,32 +668,54 @@ int ws_plan_batch_host(ws_ctx* ctx, const ws_batch* in, ws_plan_result* results,
     ctx->launches = 0;
     CK(cudaMemsetAsync(counters, 0, 64, st));
     const ws_batch& B = ctx->dview;
-    auto* rcount = reinterpret_cast<int32_t*>(counters + 2);
+    // compute streams: chunk c runs on cs[c % S]; chunk c+1's kernels fill chunk c's launch tail
+    const int S = ctx->host_streams;
+    cudaStream_t cs[2] = {st, ctx->stream4};
+    if (S > 1) {
+        if (!ctx->recs_r2.ensure(ctx->recs_r.n) || !ctx->flows_r2.ensure(ctx->flows_r.n) ||
+            !ctx->retry_ids2.ensure(4 * kRetryMax))
+            return fail(ctx, "cudaMalloc retry buffers");
+        CK(cudaEventRecord(ctx->ev[1], st));
+        CK(cudaStreamWaitEvent(cs[1], ctx->ev[1], 0));
+    }
     for (int c = 0; c < C; ++c) {  // compute side
         const int p0 = pb[c], p1 = pb[c + 1];
         const int m0 = in->plans[p0].mod_begin, m1 = p1 < P ? in->plans[p1].mod_begin : in->n_modules;
-        CK(cudaStreamWaitEvent(st, h2d[c], 0));
+        const int k = c % S;
+        cudaStream_t s = cs[k];
+        auto* rcount = reinterpret_cast<int32_t*>(counters + 2 + k);
+        DevBuf& rids = k ? ctx->retry_ids2 : ctx->retry_ids;
+        DevBuf& rrecs = k ? ctx->recs_r2 : ctx->recs_r;
+        DevBuf& rflows = k ? ctx->flows_r2 : ctx->flows_r;
+        CK(cudaStreamWaitEvent(s, h2d[c], 0));
         ctx->top_ptr = tops + c;
         ctx->top_cap = abase[c + 1];
         if (m1 > m0) {
-            k_fit<<<(m1 - m0 + 127) / 128, 128, 0, st>>>(B, fo, m0, m1);
+            k_fit<<<(m1 - m0 + 127) / 128, 128, 0, s>>>(B, fo, m0, m1);
             ctx->launches++;
         }
-        int rc = launch_pair(ctx, st, ctx->caps, fo, ctx->order.as<int32_t>() + p0, nullptr, p1 - p0, false,
-                             ctx->recs.as<char>(), ctx->flows.as<uint64_t>());
+        // k_place's flow scratch is indexed by launch slot: each chunk gets its own
+        // region (slots of concurrent chunks would otherwise collide)
+        int rc = launch_pair(ctx, s, ctx->caps, fo, ctx->order.as<int32_t>() + p0, nullptr, p1 - p0, false,
+                             ctx->recs.as<char>(),
+                             ctx->flows.as<uint64_t>() + static_cast<int64_t>(p0) * ctx->caps.pl.F * 2);
         if (!rc) {
-            CK(cudaMemsetAsync(rcount, 0, 4, st));
-            k_soft_collect<<<(p1 - p0 + 255) / 256, 256, 0, st>>>(ctx->res_out(), p0, p1,
-                                                                   ctx->retry_ids.as<int32_t>(), rcount);
-            k_clamp_count<<<1, 1, 0, st>>>(rcount);
+            CK(cudaMemsetAsync(rcount, 0, 4, s));
+            k_soft_collect<<<(p1 - p0 + 255) / 256, 256, 0, s>>>(ctx->res_out(), p0, p1, rids.as<int32_t>(),
+                                                                  rcount);
+            k_clamp_count<<<1, 1, 0, s>>>(rcount);
             ctx->launches += 2;
-            rc = launch_pair(ctx, st, ctx->caps_hard, fo, ctx->retry_ids.as<int32_t>(), rcount, kRetryMax, true,
-                             ctx->recs_r.as<char>(), ctx->flows_r.as<uint64_t>());
+            rc = launch_pair(ctx, s, ctx->caps_hard, fo, rids.as<int32_t>(), rcount, kRetryMax, true,
+                             rrecs.as<char>(), rflows.as<uint64_t>());
         }
         ctx->top_ptr = nullptr;
         if (rc) return 1;
-        CK(cudaMemcpyAsync(ctx->host_tops + kMaxHostChunks + c, tops + c, 8, cudaMemcpyDeviceToHost, st));
-        CK(cudaEventRecord(done[c], st));
+        CK(cudaMemcpyAsync(ctx->host_tops + kMaxHostChunks + c, tops + c, 8, cudaMemcpyDeviceToHost, s));
+        CK(cudaEventRecord(done[c], s));
+    }
+    if (S > 1) {  // join the second compute stream
+        CK(cudaEventRecord(ctx->ev[3], cs[1]));
+        CK(cudaStreamWaitEvent(st, ctx->ev[3], 0));
     }
     CK(cudaEventRecord(ctx->ev[2], st));
     uint64_t used = 0;
