@@ -165,6 +165,8 @@ def main() -> None:
     ap.add_argument("--cpu-sample", type=int, default=6000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--latency-reps", type=int, default=50)
+    ap.add_argument("--compare-mixtures", type=int, default=25000,
+                    help="sweep mixtures of the strategy-comparison block (each planned by all 4 strategies)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
@@ -227,6 +229,14 @@ def main() -> None:
     if world > 1:
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
     t_max = float(t.item())
+    # per-rank device time per step (load balance of the strided shards)
+    rank_t = torch.tensor([t_local], dtype=torch.float64, device=dev)
+    if world > 1:
+        gathered = [torch.zeros_like(rank_t) for _ in range(world)]
+        torch.distributed.all_gather(gathered, rank_t)
+        rank_step_ms = [1000.0 * float(g.item()) / args.steps for g in gathered]
+    else:
+        rank_step_ms = [1000.0 * t_local / args.steps]
     value = args.mixtures * args.steps / t_max
 
     # ---- correctness + global best (min-loc over ranks) ----
@@ -330,6 +340,44 @@ def main() -> None:
                                "ms_per_step": 1000.0 * float(tb.item()) / args.steps,
                                "failed_plans": int(bad.item())}
 
+    # ---- strategy comparison (cmd_compare's loop, cli.hpp:243-255):
+    # every mixture planned by all four strategies and each plan simulated +
+    # validated, as ONE staged batch + one k_sim launch per step ----
+    compare = None
+    if args.compare_mixtures > 0:
+        cidx = idx[: max(1, len(idx) * args.compare_mixtures // max(args.mixtures, 1))]
+        pc = ws.ProblemSet()
+        for i in cidx:
+            for strategy in ws.STRATEGIES:
+                pc.add_sweep(i, 1, strategy=strategy)
+        pc.encode(pinned=True)
+        planner.stage(pc, sptr)
+        for _ in range(2):
+            planner.plan_staged(sptr)
+            planner.simulate_staged(sptr)
+        barrier()
+        cms = []
+        for _ in range(args.steps):
+            flush.zero_()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            planner.plan_staged(sptr)
+            planner.simulate_staged(sptr)
+            e1.record(stream)
+            e1.synchronize()
+            cms.append(e0.elapsed_time(e1))
+        barrier()
+        tc = torch.tensor([sum(cms) / 1000.0, float(len(cidx))], dtype=torch.float64, device=dev)
+        if world > 1:
+            torch.distributed.all_reduce(tc[:1], op=torch.distributed.ReduceOp.MAX)
+            torch.distributed.all_reduce(tc[1:], op=torch.distributed.ReduceOp.SUM)
+        n_cmp = int(tc[1].item())
+        compare = {"what": "all 4 strategies planned + simulate_plan + validate_plan per mixture "
+                           "(one staged batch + one k_sim launch per step)",
+                   "mixtures": n_cmp, "value": n_cmp * args.steps / float(tc[0].item()), "unit": "workloads/s",
+                   "ms_per_step": 1000.0 * float(tc[0].item()) / args.steps}
+
     if rank != 0:
         if world > 1:
             torch.distributed.destroy_process_group()
@@ -413,6 +461,16 @@ def main() -> None:
         except Exception:
             pass
 
+        try:
+            import pyoracle as po
+            if po.ref_available() and compare is not None:
+                n_c = max(args.cpu_sample // 8, 200)
+                compare["cpu_reference_per_s"] = po.ref_sweep_compare_bench(0, n_c, os.cpu_count() or 1)
+                compare["cpu_reference_sample"] = (f"sweep mixtures 0..{n_c - 1}, reference plan_for_strategy x4 + "
+                                                   f"validate_plan + simulate_plan, {os.cpu_count()} threads")
+        except Exception:
+            pass
+
     line = {
         "metric": METRIC,
         "value": value,
@@ -440,9 +498,11 @@ def main() -> None:
         "cpu_baseline": cpu,
         "gpu_launches": launches_per_step * args.steps,
         "clocks": clk,
+        "rank_step_ms": rank_step_ms,
         "latency_ms": latency,
         "evaluation": evaluation,
         "baselines": baselines,
+        "compare": compare,
         "parity": {"infeasible_plans": int(infeasible.item()), "best_gap": best_key, "best_index": best_idx},
     }
     print(json.dumps(line), flush=True)

@@ -137,6 +137,8 @@ def ref():
         lib.wsref_cmd.argtypes = [C.c_int, C.c_char_p, C.c_char_p, C.c_char_p, C.c_double, C.c_int, C.c_ulonglong]
         lib.wsref_sweep_workload.restype = vp
         lib.wsref_sweep_workload.argtypes = [C.c_long, C.POINTER(vp)]
+        lib.wsref_sweep_compare_bench.restype = C.c_double
+        lib.wsref_sweep_compare_bench.argtypes = [C.c_long, C.c_long, C.c_int]
         lib.wsref_latency_ms.restype = C.c_double
         lib.wsref_latency_ms.argtypes = [C.c_char_p, C.c_int, C.c_int, C.c_int]
         _ref = lib
@@ -224,3 +226,9 @@ def ref_sweep_workload(i: int) -> tuple[str, str]:
     t = C.c_void_p()
     w = ref().wsref_sweep_workload(i, C.byref(t))
     return _s(w), _s(t)
+
+
+def ref_sweep_compare_bench(start: int, count: int, threads: int) -> float:
+    """Reference compare loop (all strategies planned + validated + simulated) over
+    sweep mixtures; workloads/s on `threads` threads."""
+    return ref().wsref_sweep_compare_bench(start, count, threads)

@@ -418,6 +418,40 @@ char* wsref_cmd(int which, const char* input, const char* topology, const char* 
     return dup(result);
 }
 
+// CPU baseline of strategy comparison (cmd_compare's loop, cli.hpp:243-255):
+// per sweep mixture, every strategy planned, validated and simulated; over
+// mixtures [start, start+count) on `threads` threads.  Returns workloads/s.
+double wsref_sweep_compare_bench(long start, long count, int threads) {
+    std::vector<WorkloadSpec> specs(count);
+    std::vector<ClusterTopology> topos(count);
+    for (long i = 0; i < count; ++i) {
+        Scenario sc = sweep(start + i);
+        specs[i] = parse_workload(sc.workload_text);
+        topos[i] = parse_topology(sc.topology_text);
+    }
+    std::atomic<long> next{0};
+    auto worker = [&] {
+        for (long i; (i = next.fetch_add(1)) < count;) {
+            for (const std::string& s : all_strategies()) {
+                try {
+                    const ExecutionPlan plan = plan_for_strategy(s, specs[i], topos[i], PlannerOptions{});
+                    const ValidationReport v = validate_plan(plan);
+                    const SimulationReport r = simulate_plan(plan);
+                    (void)v;
+                    (void)r;
+                } catch (const Error&) {
+                }
+            }
+        }
+    };
+    const auto t0 = std::chrono::steady_clock::now();
+    std::vector<std::thread> pool;
+    for (int t = 0; t < threads; ++t) pool.emplace_back(worker);
+    for (auto& th : pool) th.join();
+    return static_cast<double>(count) /
+           std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
+
 // Single-plan latency of the reference planner (median of `reps`, ms).
 double wsref_latency_ms(const char* name, int tasks, int devices, int reps) {
     Scenario sc = generate_scenario(name, tasks, devices, 0);

@@ -106,6 +106,12 @@ struct PlaceArgs {
     uint8_t* arena;
     unsigned long long* arena_top;
     unsigned long long arena_cap;
+    // backtracking snapshots: a pool of per-warp slots, each (W+1) states of
+    // mem[N] f64 + chg[G] u64, claimed on a plan's first failed wave
+    double* snap;             // [snap_slots][snap_stride]
+    unsigned* snap_bits;      // claim bitmap, one bit per slot
+    int snap_slots;           // 0: no pool (replay only)
+    long long snap_stride;    // 8-byte words per slot
 };
 
 struct PCtx {
@@ -593,6 +599,28 @@ __device__ void p_emit(PCtx& C, int p, const char* rec, const RecLayout& RL, con
 #ifndef WS_PLACE_MINB
 #define WS_PLACE_MINB 3  // measured sweep 1/2/3/4: 3 blocks (<=170 regs) is fastest
 #endif
+// Snapshot slot claim / release (lane 0): a free bit of the pool bitmap, or -1
+// when every slot is taken (the warp then restores by replay).
+__device__ int snap_claim(unsigned* bits, int slots, int start) {
+    const int words = (slots + 31) >> 5;
+    for (int t = 0; t < words; ++t) {
+        const int w = (start + t) % words;
+        const unsigned valid = (w + 1) * 32 <= slots ? ~0u : ((1u << (slots - w * 32)) - 1u);
+        unsigned cur = *reinterpret_cast<volatile unsigned*>(bits + w);
+        while ((cur & valid) != valid) {
+            const int b = __ffs(~cur & valid) - 1;
+            const unsigned old = atomicOr(bits + w, 1u << b);
+            if (!(old >> b & 1u)) return w * 32 + b;
+            cur = old | (1u << b);
+        }
+    }
+    return -1;
+}
+
+__device__ __forceinline__ void snap_release(unsigned* bits, int slot) {
+    if (slot >= 0) atomicAnd(bits + (slot >> 5), ~(1u << (slot & 31)));
+}
+
 __global__ void __launch_bounds__(32 * kPlaceWarps, WS_PLACE_MINB) k_place(PlaceArgs A) {
     extern __shared__ __align__(16) char smem_dyn[];
     __shared__ Ctl ctl_s[kPlaceWarps];
@@ -755,7 +783,21 @@ __global__ void __launch_bounds__(32 * kPlaceWarps, WS_PLACE_MINB) k_place(Place
     const int* r_pg_wn = reinterpret_cast<const int*>(rec + A.RL.pg_wn);
     const int* r_pg_list = reinterpret_cast<const int*>(rec + A.RL.pg_list);
     int* glist = C.at<int>(L.glist);
+    // backtracking state restore: replay (below) until the plan's first failed
+    // wave, then per-wave snapshots in a claimed pool slot (identical doubles:
+    // a snapshot holds exactly the state the replay rebuilds)
+    int snap_slot = -1;       // claimed pool slot (uniform across the warp)
+    int snap_hi = -1;         // snapshots 0..snap_hi of this group are valid
+    const int snapN = N, snapW = N + G;  // words per wave state: mem[N], chg[G]
+    auto snap_at = [&](int j) { return A.snap + static_cast<long long>(snap_slot) * A.snap_stride +
+                                       static_cast<long long>(j) * snapW; };
+    auto snap_save = [&](int j) {  // state before wave j
+        double* dst = snap_at(j);
+        for (int d = lane; d < snapN; d += 32) dst[d] = mem[d];
+        for (int g = lane; g < G; g += 32) reinterpret_cast<uint64_t*>(dst + snapN)[g] = chg[g];
+    };
     for (int grp = 0; grp < (n_pg ? n_pg : 1); ++grp) {
+        snap_hi = -1;
         const int goff = n_pg ? r_pg_off[grp] : 0, gcnt = n_pg ? r_pg_cnt[grp] : N;
         const int gn = n_pg ? r_pg_wn[grp] : nW;
         for (int i = lane; i < gn; i += 32) glist[i] = n_pg ? r_pg_list[r_pg_wbeg[grp] + i] : i;
@@ -809,15 +851,34 @@ __global__ void __launch_bounds__(32 * kPlaceWarps, WS_PLACE_MINB) k_place(Place
             if (lane == 0) {
                 set_err(ctl, WS_E_BT_BUDGET, k);
                 write_error(A.results + p, ctl);
+                snap_release(A.snap_bits, snap_slot);
             }
             return;
         }
         WS_PH_START(tr);
-        if (dirty) {  // rebuild the state before wave k
+        if (dirty && snap_hi >= k) {  // restore the state before wave k from its snapshot
+            const double* src = snap_at(k);
+            for (int d = lane; d < N; d += 32) mem[d] = src[d];
+            for (int g = lane; g < G; g += 32) chg[g] = reinterpret_cast<const uint64_t*>(src + snapN)[g];
+            snap_hi = k;
+            C.nF = wave_nf[k];
+            WS_PH_STOP(tr, 6);
+            dirty = false;
+            __syncwarp();
+        } else if (dirty) {  // rebuild the state before wave k by replay
+            if (snap_slot < 0 && A.snap_slots > 0) {
+                int sl = 0;
+                if (lane == 0) sl = snap_claim(A.snap_bits, A.snap_slots, (blockIdx.x * kPlaceWarps + wid) >> 5);
+                snap_slot = __shfl_sync(kFull, sl, 0);
+            }
             for (int d = lane; d < N; d += 32) mem[d] = 0.0;
             for (int g = lane; g < G; g += 32) chg[g] = 0;
             __syncwarp();
             for (int j = 0; j < k; ++j) {
+                if (snap_slot >= 0) {
+                    __syncwarp();
+                    snap_save(j);
+                }
                 const int w = glist[j];
                 for (int i = 0; i < w_ec[w]; ++i) {
                     const int e = w_eb[w] + i;
@@ -836,6 +897,11 @@ __global__ void __launch_bounds__(32 * kPlaceWarps, WS_PLACE_MINB) k_place(Place
                     __syncwarp();
                 }
             }
+            if (snap_slot >= 0) {
+                __syncwarp();
+                snap_save(k);
+                snap_hi = k;
+            }
             C.nF = wave_nf[k];
             WS_PH_STOP(tr, 6);
             dirty = false;
@@ -848,6 +914,7 @@ __global__ void __launch_bounds__(32 * kPlaceWarps, WS_PLACE_MINB) k_place(Place
                 if (lane == 0) {
                     set_err(ctl, WS_E_NO_PLACEMENT_W0);
                     write_error(A.results + p, ctl);
+                    snap_release(A.snap_bits, snap_slot);
                 }
                 return;
             }
@@ -866,7 +933,10 @@ __global__ void __launch_bounds__(32 * kPlaceWarps, WS_PLACE_MINB) k_place(Place
         const int r = p_wave(C, wk, variant[k]);
         __syncwarp();
         if (r < 0) {
-            if (lane == 0) write_error(A.results + p, ctl);
+            if (lane == 0) {
+                write_error(A.results + p, ctl);
+                snap_release(A.snap_bits, snap_slot);
+            }
             return;
         }
         if (r > 0) {
@@ -876,6 +946,10 @@ __global__ void __launch_bounds__(32 * kPlaceWarps, WS_PLACE_MINB) k_place(Place
                 home[e_k[e]] = e;
             }
             ++k;
+            if (snap_slot >= 0 && k < gn) {  // snapshot mode: state before the next wave
+                snap_save(k);
+                snap_hi = k;
+            }
         } else {
             if (lane == 0) variant[k]++;
             dirty = true;
@@ -883,6 +957,7 @@ __global__ void __launch_bounds__(32 * kPlaceWarps, WS_PLACE_MINB) k_place(Place
         __syncwarp();
     }
     }
+    if (lane == 0) snap_release(A.snap_bits, snap_slot);
     WS_PH_START(te);
     p_emit(C, p, rec, A.RL, h, A);
     WS_PH_STOP(te, 7);

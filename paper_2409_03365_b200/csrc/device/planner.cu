@@ -34,7 +34,11 @@ constexpr int kRetryMax = 1024;               // plans re-run with hard caps per
 constexpr int64_t kOverflowPieces = 1 << 18;  // isotonic/long curves
 constexpr int kSmemLimit = 227 * 1024;
 constexpr int kMaxChunks = 16;  // k_sched/k_place pipeline depth
-constexpr int kMaxHostChunks = 8;  // H2D / compute / D2H pipeline depth of ws_plan_batch_host
+constexpr int kMaxHostChunks = 8;
+// k_place snapshot slots: only warps of plans that fail a wave claim one (a few
+// hundred per 100k sweep), so a small pool serves every resident warp; a warp
+// that finds none falls back to replaying the committed waves
+constexpr int kSnapSlots = 512;  // H2D / compute / D2H pipeline depth of ws_plan_batch_host
 
 struct DevBuf {
     void* p = nullptr;
@@ -167,6 +171,8 @@ struct ws_ctx {
     DevBuf fit_err, fit_a, fit_b, fit_np, fit_nmax, fit_off, fit_pieces, ttab;
     // records, flows, results
     DevBuf recs, flows, recs_r, flows_r, results, arena, counters, retry_ids, best;
+    DevBuf snap, snap_bits;    // k_place backtracking snapshot pool (kSnapSlots slots)
+    long long snap_stride = 0; // 8-byte words per slot
     uint64_t arena_cap = 0;
     int launches = 0;
     cudaEvent_t ev[4] = {};
@@ -313,6 +319,11 @@ int launch_pair(ws_ctx* ctx, cudaStream_t st, const LaunchCaps& lc, const FitOut
     P.arena = ctx->arena_out();
     P.arena_top = ctx->top_ptr ? ctx->top_ptr : ctx->counters.as<unsigned long long>();
     P.arena_cap = ctx->top_ptr ? ctx->top_cap : ctx->cap_out();
+    const bool snap_ok = ctx->snap_stride >= static_cast<long long>(lc.pl.W) * (lc.pl.N + lc.pl.G);
+    P.snap = ctx->snap.as<double>();
+    P.snap_bits = ctx->snap_bits.as<unsigned>();
+    P.snap_slots = snap_ok ? kSnapSlots : 0;
+    P.snap_stride = ctx->snap_stride;
     if (kPlaceWarps * P.PL.bytes > kSmemLimit) return fail(ctx, "k_place working set exceeds shared memory");
     CK(cudaFuncSetAttribute(k_place, cudaFuncAttributeMaxDynamicSharedMemorySize, kPlaceWarps * P.PL.bytes));
 
@@ -451,6 +462,18 @@ int prepare_plan(ws_ctx* ctx, FitOut& fo) {
         !ctx->recs_r.ensure(static_cast<size_t>(RLh.bytes) * kRetryMax) ||
         !ctx->flows_r.ensure(16ull * lh.pl.F * kRetryMax))
         return fail(ctx, "cudaMalloc planner buffers");
+    // backtracking snapshot pool sized for the larger (retry) caps; the claim
+    // bitmap is zeroed only when the pool is (re)allocated -- warps always release
+    const long long stride = std::max(static_cast<long long>(lc.pl.W) * (lc.pl.N + lc.pl.G),
+                                      static_cast<long long>(lh.pl.W) * (lh.pl.N + lh.pl.G));
+    if (stride > ctx->snap_stride) {
+        cudaDeviceSynchronize();  // no k_place of this ctx may hold a slot
+        if (!ctx->snap.ensure(8ull * stride * kSnapSlots) || !ctx->snap_bits.ensure(4 * ((kSnapSlots + 31) / 32)))
+            return fail(ctx, "cudaMalloc snapshot pool");
+        if (cudaMemset(ctx->snap_bits.p, 0, 4 * ((kSnapSlots + 31) / 32)) != cudaSuccess)
+            return fail(ctx, "cudaMemset snapshot bits");
+        ctx->snap_stride = stride;
+    }
     auto* counters = ctx->counters.as<unsigned long long>();
     fo.err = ctx->fit_err.as<int32_t>();
     fo.err_a = ctx->fit_a.as<int32_t>();

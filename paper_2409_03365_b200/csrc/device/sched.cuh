@@ -88,6 +88,7 @@ struct SmLayout {
     int ent_of, kscale, tlvl, vord;                                          // [M] per task
     int tvalid, talloc, cw_start, cw_dur, cw_level, cw_ent, cw_n, cw_L;     // [64] optimus tasks / waves
     int pl_off, pl_cnt, pl_wbeg, pl_wn, perm, tfin;                         // [64] placements, [M] finish
+    int tcur, tnext, tnxn;                                                  // [64] optimus task-time cache
     int bytes;
 };
 
@@ -162,6 +163,9 @@ __host__ __device__ inline SmLayout make_sm_layout(int M, bool scoped = false) {
     L.pl_wn = take(4 * EM);
     L.perm = take(4 * EM);
     L.tfin = take(8 * MS);
+    L.tcur = take(8 * EM);
+    L.tnext = take(8 * EM);
+    L.tnxn = take(4 * EM);
     L.bytes = (o + 15) & ~15;
     return L;
 }
@@ -1467,6 +1471,9 @@ __device__ bool s_optimus(SCtx& C, char* rec, const RecLayout& RL, int& nW, int&
     int* pl_wn = C.at<int>(C.L->pl_wn);
     int* perm = C.at<int>(C.L->perm);
     double* tfin = C.at<double>(C.L->tfin);
+    double* tcur = C.at<double>(C.L->tcur);
+    double* tnext = C.at<double>(C.L->tnext);
+    int* tnxn = C.at<int>(C.L->tnxn);
     int KE = 0, ncw = 0, npl = 0;
     for (int e = lane; e < WS_MAX_MODULES; e += 32) epred[e] = 0;
     __syncwarp();
@@ -1547,7 +1554,15 @@ __device__ bool s_optimus(SCtx& C, char* rec, const RecLayout& RL, int& nW, int&
                 used += need;
                 ++b1;
             }
-            for (int t = b0; t < b1; ++t) talloc[t] = low_bit(tvalid[t]) + 1;
+            // task_time(t, n) is a pure function of (t, n): each task's time at its
+            // current and at its next allocation is cached and only the grown
+            // task's entries are recomputed (the reference re-evaluates both for
+            // every task at every step; the values, hence the gains, are identical)
+            for (int t = b0; t < b1; ++t) {
+                talloc[t] = low_bit(tvalid[t]) + 1;
+                tcur[t] = -1.0;
+                tnxn[t] = -1;
+            }
             while (true) {  // marginal gain per added device
                 int usedn = 0;
                 for (int t = b0; t < b1; ++t) usedn += talloc[t];
@@ -1560,7 +1575,12 @@ __device__ bool s_optimus(SCtx& C, char* rec, const RecLayout& RL, int& nW, int&
                     if (!above) continue;
                     const int nx = low_bit(above) + 1;
                     if (nx - talloc[t] > free) continue;
-                    const double gain = (task_time(t, talloc[t]) - task_time(t, nx)) / (nx - talloc[t]);
+                    if (tcur[t] < 0.0) tcur[t] = task_time(t, talloc[t]);
+                    if (tnxn[t] != nx) {
+                        tnext[t] = task_time(t, nx);
+                        tnxn[t] = nx;
+                    }
+                    const double gain = (tcur[t] - tnext[t]) / (nx - talloc[t]);
                     if (gain > best_gain) {
                         best_gain = gain;
                         best = t;
@@ -1569,6 +1589,8 @@ __device__ bool s_optimus(SCtx& C, char* rec, const RecLayout& RL, int& nW, int&
                 }
                 if (best < 0) break;
                 talloc[best] = best_next;
+                tcur[best] = tnext[best];  // == task_time(best, best_next)
+                tnxn[best] = -1;
             }
             double batch_end = batch_offset;
             int cursor = 0;
