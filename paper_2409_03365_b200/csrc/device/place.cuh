@@ -621,6 +621,10 @@ __device__ __forceinline__ void snap_release(unsigned* bits, int slot) {
     if (slot >= 0) atomicAnd(bits + (slot >> 5), ~(1u << (slot & 31)));
 }
 
+// kSnap: backtracking restores from per-wave snapshots (instantiated for
+// batches with baseline-strategy plans, whose placements backtrack deep);
+// pure wavefront batches backtrack rarely and keep the replay-only kernel.
+template <bool kSnap>
 __global__ void __launch_bounds__(32 * kPlaceWarps, WS_PLACE_MINB) k_place(PlaceArgs A) {
     extern __shared__ __align__(16) char smem_dyn[];
     __shared__ Ctl ctl_s[kPlaceWarps];
@@ -851,12 +855,12 @@ __global__ void __launch_bounds__(32 * kPlaceWarps, WS_PLACE_MINB) k_place(Place
             if (lane == 0) {
                 set_err(ctl, WS_E_BT_BUDGET, k);
                 write_error(A.results + p, ctl);
-                snap_release(A.snap_bits, snap_slot);
+                if (kSnap) snap_release(A.snap_bits, snap_slot);
             }
             return;
         }
         WS_PH_START(tr);
-        if (dirty && snap_hi >= k) {  // restore the state before wave k from its snapshot
+        if (kSnap && dirty && snap_hi >= k) {  // restore the state before wave k from its snapshot
             const double* src = snap_at(k);
             for (int d = lane; d < N; d += 32) mem[d] = src[d];
             for (int g = lane; g < G; g += 32) chg[g] = reinterpret_cast<const uint64_t*>(src + snapN)[g];
@@ -866,7 +870,7 @@ __global__ void __launch_bounds__(32 * kPlaceWarps, WS_PLACE_MINB) k_place(Place
             dirty = false;
             __syncwarp();
         } else if (dirty) {  // rebuild the state before wave k by replay
-            if (snap_slot < 0 && A.snap_slots > 0) {
+            if (kSnap && snap_slot < 0 && A.snap_slots > 0) {
                 int sl = 0;
                 if (lane == 0) sl = snap_claim(A.snap_bits, A.snap_slots, (blockIdx.x * kPlaceWarps + wid) >> 5);
                 snap_slot = __shfl_sync(kFull, sl, 0);
@@ -875,7 +879,7 @@ __global__ void __launch_bounds__(32 * kPlaceWarps, WS_PLACE_MINB) k_place(Place
             for (int g = lane; g < G; g += 32) chg[g] = 0;
             __syncwarp();
             for (int j = 0; j < k; ++j) {
-                if (snap_slot >= 0) {
+                if (kSnap && snap_slot >= 0) {
                     __syncwarp();
                     snap_save(j);
                 }
@@ -897,7 +901,7 @@ __global__ void __launch_bounds__(32 * kPlaceWarps, WS_PLACE_MINB) k_place(Place
                     __syncwarp();
                 }
             }
-            if (snap_slot >= 0) {
+            if (kSnap && snap_slot >= 0) {
                 __syncwarp();
                 snap_save(k);
                 snap_hi = k;
@@ -914,7 +918,7 @@ __global__ void __launch_bounds__(32 * kPlaceWarps, WS_PLACE_MINB) k_place(Place
                 if (lane == 0) {
                     set_err(ctl, WS_E_NO_PLACEMENT_W0);
                     write_error(A.results + p, ctl);
-                    snap_release(A.snap_bits, snap_slot);
+                    if (kSnap) snap_release(A.snap_bits, snap_slot);
                 }
                 return;
             }
@@ -935,7 +939,7 @@ __global__ void __launch_bounds__(32 * kPlaceWarps, WS_PLACE_MINB) k_place(Place
         if (r < 0) {
             if (lane == 0) {
                 write_error(A.results + p, ctl);
-                snap_release(A.snap_bits, snap_slot);
+                if (kSnap) snap_release(A.snap_bits, snap_slot);
             }
             return;
         }
@@ -946,7 +950,7 @@ __global__ void __launch_bounds__(32 * kPlaceWarps, WS_PLACE_MINB) k_place(Place
                 home[e_k[e]] = e;
             }
             ++k;
-            if (snap_slot >= 0 && k < gn) {  // snapshot mode: state before the next wave
+            if (kSnap && snap_slot >= 0 && k < gn) {  // snapshot mode: state before the next wave
                 snap_save(k);
                 snap_hi = k;
             }
@@ -957,7 +961,7 @@ __global__ void __launch_bounds__(32 * kPlaceWarps, WS_PLACE_MINB) k_place(Place
         __syncwarp();
     }
     }
-    if (lane == 0) snap_release(A.snap_bits, snap_slot);
+    if (lane == 0) if (kSnap) snap_release(A.snap_bits, snap_slot);
     WS_PH_START(te);
     p_emit(C, p, rec, A.RL, h, A);
     WS_PH_STOP(te, 7);

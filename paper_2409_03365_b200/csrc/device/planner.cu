@@ -114,19 +114,23 @@ struct LaunchCaps {
     RecCaps rec;
     PlaceCaps pl;
     int M;        // modules (MetaOps) per plan
+    int T;        // tasks per plan
     bool scoped;  // the batch has task-scoped baseline plans
+    bool baseline;  // the batch has baseline-strategy plans (k_place<true>)
 };
 
 LaunchCaps batch_caps(const ws_plan_rec* plans, int P, bool hard) {
-    int M = 1, N = 1, IS = 1, gmax = 0;
-    bool scoped = false;
+    int M = 1, N = 1, IS = 1, gmax = 0, T = 1;
+    bool scoped = false, baseline = false;
     for (int p = 0; p < P; ++p) {
         const ws_plan_rec& r = plans[p];
         M = std::max(M, r.n_mod);
         N = std::max(N, r.n_dev);
         IS = std::max(IS, r.n_islands);
         gmax = std::max(gmax, r.n_groups);
+        T = std::max(T, r.n_tasks);
         scoped |= r.strategy == WS_STRATEGY_DISTMM_MT || r.strategy == WS_STRATEGY_TASK_OPTIMUS;
+        baseline |= r.strategy != WS_STRATEGY_WAVEFRONT;
     }
     M = std::min(M, WS_MAX_MODULES);
     N = std::min(N, WS_MAX_DEVICES);
@@ -144,7 +148,9 @@ LaunchCaps batch_caps(const ws_plan_rec* plans, int P, bool hard) {
     }
     LaunchCaps c;
     c.M = M;
+    c.T = std::min(T, WS_MAX_TASKS);
     c.scoped = scoped;
+    c.baseline = baseline;
     c.rec = RecCaps{ME, W, E};
     c.pl = PlaceCaps{ME, N, W, E, F, gmax + ME, IS};
     return c;
@@ -292,7 +298,7 @@ int launch_pair(ws_ctx* ctx, cudaStream_t st, const LaunchCaps& lc, const FitOut
     S.fit = fo;
     S.caps = lc.rec;
     S.RL = make_rec_layout(lc.rec);
-    S.SL = make_sm_layout(lc.M, lc.scoped);
+    S.SL = make_sm_layout(lc.M, lc.scoped, lc.T);
     S.scoped_ok = lc.scoped ? 1 : 0;
     S.recs = recs;
     S.n_ids = n_ids;
@@ -325,7 +331,10 @@ int launch_pair(ws_ctx* ctx, cudaStream_t st, const LaunchCaps& lc, const FitOut
     P.snap_slots = snap_ok ? kSnapSlots : 0;
     P.snap_stride = ctx->snap_stride;
     if (kPlaceWarps * P.PL.bytes > kSmemLimit) return fail(ctx, "k_place working set exceeds shared memory");
-    CK(cudaFuncSetAttribute(k_place, cudaFuncAttributeMaxDynamicSharedMemorySize, kPlaceWarps * P.PL.bytes));
+    // measured (100k sweep, ms): snapshots cut decoupled-sequential 9.8 -> 7.9 and
+    // distmm-mt 81 -> 47, while the extra code costs wavefront 10.6 -> 11.0
+    auto* kplace = lc.baseline ? k_place<true> : k_place<false>;
+    CK(cudaFuncSetAttribute(kplace, cudaFuncAttributeMaxDynamicSharedMemorySize, kPlaceWarps * P.PL.bytes));
 
     chunks = std::max(1, std::min(chunks, kMaxChunks));
     if (n_ids || n < 4096) chunks = 1;  // retry pass / small batches: no pipelining
@@ -356,7 +365,7 @@ int launch_pair(ws_ctx* ctx, cudaStream_t st, const LaunchCaps& lc, const FitOut
         }
         P.plan_ids = ids + base;
         P.n_launch = cnt;
-        k_place<<<(cnt + kPlaceWarps - 1) / kPlaceWarps, 32 * kPlaceWarps, kPlaceWarps * P.PL.bytes, sb>>>(P);
+        kplace<<<(cnt + kPlaceWarps - 1) / kPlaceWarps, 32 * kPlaceWarps, kPlaceWarps * P.PL.bytes, sb>>>(P);
         ctx->launches++;
     }
     if (chunks > 1) {

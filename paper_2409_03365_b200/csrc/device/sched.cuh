@@ -92,7 +92,9 @@ struct SmLayout {
     int bytes;
 };
 
-__host__ __device__ inline SmLayout make_sm_layout(int M, bool scoped = false) {
+// M: MetaOps per plan; scoped: the batch has task-scoped baseline plans;
+// tasks: the batch's largest task count (task-indexed optimus arrays)
+__host__ __device__ inline SmLayout make_sm_layout(int M, bool scoped = false, int tasks = WS_MAX_TASKS) {
     SmLayout L{};
     int o = 0;
     auto take = [&](int b) {
@@ -140,7 +142,7 @@ __host__ __device__ inline SmLayout make_sm_layout(int M, bool scoped = false) {
     L.pool = take(4 * T);
     L.klay = take(4 * T);
     L.ord = take(4 * 3 * T);
-    const int EM = scoped ? WS_MAX_MODULES : 0, MS = scoped ? M : 0;
+    const int EM = scoped ? WS_MAX_MODULES : 0, MS = scoped ? M : 0, TT = scoped ? tasks : 0;
     L.ent_met = take(4 * EM);
     L.ent_task = take(4 * EM);
     L.ent_frac = take(8 * EM);
@@ -149,23 +151,23 @@ __host__ __device__ inline SmLayout make_sm_layout(int M, bool scoped = false) {
     L.kscale = take(8 * MS);
     L.tlvl = take(4 * MS);
     L.vord = take(4 * MS);
-    L.tvalid = take(8 * EM);
-    L.talloc = take(4 * EM);
+    L.tvalid = take(8 * TT);
+    L.talloc = take(4 * TT);
     L.cw_start = take(8 * EM);
     L.cw_dur = take(8 * EM);
     L.cw_level = take(4 * EM);
     L.cw_ent = take(4 * EM);
     L.cw_n = take(4 * EM);
     L.cw_L = take(4 * EM);
-    L.pl_off = take(4 * EM);
-    L.pl_cnt = take(4 * EM);
-    L.pl_wbeg = take(4 * EM);
-    L.pl_wn = take(4 * EM);
+    L.pl_off = take(4 * TT);
+    L.pl_cnt = take(4 * TT);
+    L.pl_wbeg = take(4 * TT);
+    L.pl_wn = take(4 * TT);
     L.perm = take(4 * EM);
     L.tfin = take(8 * MS);
-    L.tcur = take(8 * EM);
-    L.tnext = take(8 * EM);
-    L.tnxn = take(4 * EM);
+    L.tcur = take(8 * TT);
+    L.tnext = take(8 * TT);
+    L.tnxn = take(4 * TT);
     L.bytes = (o + 15) & ~15;
     return L;
 }
