@@ -212,6 +212,7 @@ struct ws_ctx {
     // 1,3,1 23.5, 1,3,3,1 23.9, 1,6,1 25.5, 1,2,2,2,1 25.0 -> default 1,3,1 x 2 streams
     int host_chunks = 3;                     // $WSGPU_HOST_CHUNKS
     int host_streams = 2;                    // $WSGPU_HOST_STREAMS (1 or 2)
+    bool force_snap = false;                 // $WSGPU_FORCE_SNAP: k_place<true> for every batch (tuning)
     std::vector<double> host_weights{1, 3, 1};  // $WSGPU_HOST_WEIGHTS: relative chunk sizes (sets the chunk count)
     ws_plan_result* res_out() { return d_results ? d_results : results.as<ws_plan_result>(); }
     uint8_t* arena_out() { return d_arena ? d_arena : arena.as<uint8_t>(); }
@@ -333,7 +334,7 @@ int launch_pair(ws_ctx* ctx, cudaStream_t st, const LaunchCaps& lc, const FitOut
     if (kPlaceWarps * P.PL.bytes > kSmemLimit) return fail(ctx, "k_place working set exceeds shared memory");
     // measured (100k sweep, ms): snapshots cut decoupled-sequential 9.8 -> 7.9 and
     // distmm-mt 81 -> 47, while the extra code costs wavefront 10.6 -> 11.0
-    auto* kplace = lc.baseline ? k_place<true> : k_place<false>;
+    auto* kplace = (lc.baseline || ctx->force_snap) ? k_place<true> : k_place<false>;
     CK(cudaFuncSetAttribute(kplace, cudaFuncAttributeMaxDynamicSharedMemorySize, kPlaceWarps * P.PL.bytes));
 
     chunks = std::max(1, std::min(chunks, kMaxChunks));
@@ -420,6 +421,7 @@ int ws_ctx_create(int device, ws_ctx** out) {
         }
         if (!c->host_weights.empty()) c->host_chunks = static_cast<int>(c->host_weights.size());
     }
+    if (const char* env = std::getenv("WSGPU_FORCE_SNAP")) c->force_snap = std::atoi(env) != 0;
     if (const char* env = std::getenv("WSGPU_HOST_STREAMS")) c->host_streams = std::max(1, std::min(2, std::atoi(env)));
     *out = c;
     return 0;
