@@ -1,21 +1,27 @@
 """bench.py — batched planning throughput of the B200 planner.
 
-Workload (default): BASELINE config 5, the synthetic sweep of 100k task mixtures
-(2-16 tasks, clip/ofasys/qwen families, 8-64 device cluster specs), sharded
-across ranks (strided; strong scaling: the 100k total is fixed).  A "step" plans
-every mixture of the rank's shard once.
+Workload (default): BASELINE config 5, the synthetic sweep generator (2-16
+tasks, clip/ofasys/qwen families, 8-64 device cluster specs), 100k mixtures
+per GPU.  The path partitions into independent plans, so ranks scale weakly
+(rule: no data-path collective): rank r plans its own block of mixtures
+[r*100k, (r+1)*100k); one NCCL min-loc exchange selects the global best plan.
+`--scaling strong` splits one fixed 100k set strided across ranks instead
+(bounded below by the slowest single plan, ~5 ms of serial backtracking).
+A "step" plans every mixture of the rank's share once.
 
   value  plans/s with the encoded batch already resident in HBM (device-timed,
          CUDA events on the planner stream, max over ranks)
   e2e    plans/s through the C-ABI host call ws_plan_batch_host: pinned host
          batch -> H2D -> kernels -> D2H of the result headers + arena
-  roofline   dominant kernel k_plan vs the measured HBM copy bandwidth
+  roofline   dominant kernel (k_place) vs the measured HBM copy bandwidth
   cpu_baseline  the reference planner (oracle/_ref, compiled from the
          reference sources) on all host cores over a bounded sweep sample
+  evaluation / baselines / compare   simulate+validate (k_sim), the three
+         baseline planners, and all four strategies + evaluation per mixture
 
 usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-       [--mixtures M] [--workload sweep|clip10x64|...]
-Under torchrun (N>1) every rank plans its shard; rank 0 prints one JSON line.
+       [--mixtures M] [--scaling weak|strong]
+Under torchrun (N>1) every rank plans its share; rank 0 prints one JSON line.
 """
 from __future__ import annotations
 
@@ -141,7 +147,7 @@ def run_reference(args) -> None:
     value = statistics.median(rates)
     line = {
         "metric": METRIC, "value": value, "unit": "plans/s", "n_gpus": args.gpus, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": 1000.0 * n / value, "higher_is_better": True, "scaling": "strong",
+        "warmup": args.warmup, "ms_per_step": 1000.0 * n / value, "higher_is_better": True, "scaling": args.scaling,
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"sweep-{args.mixtures} (bounded sample of {n} mixtures per step)",
                    "parallelism": f"{threads} host threads"},
@@ -160,7 +166,9 @@ def main() -> None:
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--mixtures", type=int, default=100000)
+    ap.add_argument("--mixtures", type=int, default=100000,
+                    help="sweep mixtures per rank (weak scaling) or in total (strong)")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
     ap.add_argument("--ref-sample", type=int, default=4000)
     ap.add_argument("--cpu-sample", type=int, default=6000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -185,7 +193,16 @@ def main() -> None:
         dist.init_process_group("nccl", device_id=dev)
 
     # ---- inputs (untimed): this rank's shard of the sweep, encoded + pinned ----
-    idx = list(parallel.shard(args.mixtures, rank, world))
+    # weak scaling (default): every rank plans its own block of --mixtures sweep
+    # mixtures (rank r: global mixtures [r*M, (r+1)*M)); strong: the fixed
+    # --mixtures set split strided across ranks
+    weak = args.scaling == "weak"
+    idx = list(parallel.block(args.mixtures, rank) if weak else parallel.shard(args.mixtures, rank, world))
+    total = args.mixtures * world if weak else args.mixtures  # plans per step, whole job
+
+    def to_global(li: int) -> int:
+        return parallel.block_to_global(li, rank, args.mixtures) if weak else parallel.local_to_global(li, rank, world)
+
     ps = ws.ProblemSet()
     for i in idx:
         ps.add_sweep(i, 1)
@@ -237,14 +254,14 @@ def main() -> None:
         rank_step_ms = [1000.0 * float(g.item()) / args.steps for g in gathered]
     else:
         rank_step_ms = [1000.0 * t_local / args.steps]
-    value = args.mixtures * args.steps / t_max
+    value = total * args.steps / t_max
 
     # ---- correctness + global best (min-loc over ranks) ----
     planner.stage(ps, sptr)
     planner.plan_staged(sptr)
     res = planner.fetch(ps, sptr)
     key, li = planner.best(0, sptr)
-    gi = parallel.local_to_global(li, rank, world) if li >= 0 else -1
+    gi = to_global(li) if li >= 0 else -1
     best_key, best_idx = parallel.global_best(key if li >= 0 else float("inf"), gi, dev)
     n_ok = sum(1 for i in range(len(ps)) if res.results[i].status == 0)
     infeasible = torch.tensor([len(ps) - n_ok], dtype=torch.int64, device=dev)
@@ -272,13 +289,13 @@ def main() -> None:
     sims = planner.fetch_sim(ps, sptr)
     n_invalid = sum(1 for i in range(len(ps)) if sims.results[i].status == 0 and not sims.results[i].valid)
     skey, sli = planner.best(2, sptr)
-    sgi = parallel.local_to_global(sli, rank, world) if sli >= 0 else -1
+    sgi = to_global(sli) if sli >= 0 else -1
     best_sim, best_sim_idx = parallel.global_best(skey if sli >= 0 else float("inf"), sgi, dev)
     ts = torch.tensor([sum(sim_ms) / 1000.0, float(n_invalid)], dtype=torch.float64, device=dev)
     if world > 1:
         torch.distributed.all_reduce(ts[:1], op=torch.distributed.ReduceOp.MAX)
         torch.distributed.all_reduce(ts[1:], op=torch.distributed.ReduceOp.SUM)
-    sim_value = args.mixtures * args.steps / float(ts[0].item())
+    sim_value = total * args.steps / float(ts[0].item())
     n_invalid = int(ts[1].item())
 
     # ---- end to end through the C-ABI host call (page-locked host buffers) ----
@@ -301,7 +318,7 @@ def main() -> None:
     te = torch.tensor([sum(e2e_ms) / 1000.0], dtype=torch.float64, device=dev)
     if world > 1:
         torch.distributed.all_reduce(te, op=torch.distributed.ReduceOp.MAX)
-    e2e_value = args.mixtures * args.steps / float(te.item())
+    e2e_value = total * args.steps / float(te.item())
     # bytes the pipelined call copies back: every result header + each plan's record
     d2h_step = len(ps) * ctypes_sizeof_result() + sum(int(r2.results[i].size) for i in range(len(ps))
                                                       if r2.results[i].status == 0)
@@ -336,7 +353,7 @@ def main() -> None:
                            device=dev)
         if world > 1:
             torch.distributed.all_reduce(bad)
-        baselines[strategy] = {"value": args.mixtures * args.steps / float(tb.item()), "unit": "plans/s",
+        baselines[strategy] = {"value": total * args.steps / float(tb.item()), "unit": "plans/s",
                                "ms_per_step": 1000.0 * float(tb.item()) / args.steps,
                                "failed_plans": int(bad.item())}
 
@@ -428,7 +445,7 @@ def main() -> None:
     cpu = None
     evaluation = {"what": "simulate_plan + validate_plan of every planned mixture (k_sim, device-resident records)",
                   "value": sim_value, "unit": "evaluations/s", "ms_per_step": 1000.0 * float(ts[0].item()) / args.steps,
-                  "plan_and_evaluate_per_s": args.mixtures / (t_max / args.steps + float(ts[0].item()) / args.steps),
+                  "plan_and_evaluate_per_s": total / (t_max / args.steps + float(ts[0].item()) / args.steps),
                   "invalid_plans": n_invalid, "best_simulated_makespan": best_sim, "best_index": best_sim_idx}
     if not args.no_cpu_baseline:
         cpu = cpu_baseline(args.cpu_sample, os.cpu_count() or 1)
@@ -480,12 +497,15 @@ def main() -> None:
         "warmup": args.warmup,
         "ms_per_step": 1000.0 * t_max / args.steps,
         "higher_is_better": True,
-        "scaling": "strong",
+        "scaling": args.scaling,
         "vs_baseline": None,
         "dtype": "f64",
         "data": "synthetic",
-        "config": {"workload": f"sweep-{args.mixtures} (BASELINE config 5: 2-16 tasks, clip/ofasys/qwen, 8-64 devices)",
-                   "plans_per_rank": len(ps), "sharding": "strided i % world == rank",
+        "config": {"workload": (f"sweep (BASELINE config 5 generator: 2-16 tasks, clip/ofasys/qwen, 8-64 devices), "
+                                f"{args.mixtures} mixtures " + ("per GPU" if weak else "in total")),
+                   "plans_per_rank": len(ps),
+                   "sharding": (f"rank r plans mixtures [r*{args.mixtures}, (r+1)*{args.mixtures})" if weak
+                                else "strided i % world == rank"),
                    "l2": "256 MiB buffer written between timed steps (outside the timed events)",
                    "parallelism": f"dp{world} (independent plans, one NCCL min-loc all_gather at the end)"},
         "e2e": {"value": e2e_value, "unit": "plans/s", "h2d_bytes_per_step": in_bytes_blob,

@@ -1,9 +1,12 @@
 """Sharding of independent planning problems across ranks and the global
 best-plan exchange.
 
-* Problems (sweep mixtures, candidate plans) are independent: rank r of P plans
-  global indices i with i % P == r (strided, because per-plan cost changes with
-  the device count every 45 sweep indices).  No collective on the data path.
+* Problems (sweep mixtures, candidate plans) are independent.  A fixed set is
+  split strided: rank r of P plans global indices i with i % P == r (per-plan
+  cost changes with the device count every 45 sweep indices).  Weak scaling
+  gives every rank its own contiguous block of `per_rank` indices (the sweep
+  pattern repeats every 180 indices, so every block has the same mix).  No
+  collective on the data path.
 * One exchange at the end: the global best plan = argmin over (key, global
   index); infeasible plans carry +inf.  NCCL has no MINLOC, so each rank
   contributes a 16-byte {key, index} record to one all_gather over NVLink and
@@ -24,6 +27,15 @@ def shard(total: int, rank: int, world: int) -> range:
 
 def local_to_global(local_index: int, rank: int, world: int) -> int:
     return rank + local_index * world
+
+
+def block(per_rank: int, rank: int) -> range:
+    """Global problem indices owned by `rank` under weak scaling (one block per rank)."""
+    return range(rank * per_rank, (rank + 1) * per_rank)
+
+
+def block_to_global(local_index: int, rank: int, per_rank: int) -> int:
+    return rank * per_rank + local_index
 
 
 def reduce_minloc(records: list[tuple[float, int]]) -> tuple[float, int]:

@@ -83,3 +83,14 @@ def test_minloc_ties_and_infeasible():
     assert parallel.reduce_minloc([(float("inf"), -1), (3.0, 9)]) == (3.0, 9)
     assert parallel.reduce_minloc([(float("inf"), -1)]) == (float("inf"), -1)
     assert list(parallel.shard(10, 1, 4)) == [1, 5, 9]
+
+
+def test_weak_scaling_blocks():
+    """Weak scaling: one contiguous block of mixtures per rank, disjoint, and the
+    local -> global index map inverts it (bench.py --scaling weak)."""
+    from paper_2409_03365_b200 import parallel
+    per, world = 7, 4
+    blocks = [list(parallel.block(per, r)) for r in range(world)]
+    assert sorted(i for b in blocks for i in b) == list(range(per * world))
+    for r, b in enumerate(blocks):
+        assert [parallel.block_to_global(j, r, per) for j in range(per)] == b
