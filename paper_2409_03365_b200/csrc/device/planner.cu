@@ -186,6 +186,7 @@ struct ws_ctx {
     cudaEvent_t cev[kMaxChunks + 2] = {};       // chunk hand-offs + fork/join
     int chunks = 1;  // measured: concurrent k_sched/k_place chunks share the I-cache and lose ($WSGPU_CHUNKS)
     double kernel_ms[3] = {0, 0, 0};  // k_fit, k_sched, k_place (+ retry pass)
+    bool staged_events = false;       // ev[0..3] bracket the kernels of the last ws_plan_staged
     // plan evaluation (k_sim)
     DevBuf sim_res, sim_arena, sim_scratch, sim_top;
     uint64_t sim_cap = 0;           // ws_sim_arena_bound of the staged batch
@@ -448,7 +449,15 @@ int ws_last_launch_count(const ws_ctx* c) { return c ? c->launches : 0; }
 
 int ws_last_kernel_ms(const ws_ctx* c, double* out, int n) {
     if (!c) return 1;
-    for (int i = 0; i < n && i < 3; ++i) out[i] = c->kernel_ms[i];
+    double ms3[3] = {c->kernel_ms[0], c->kernel_ms[1], c->kernel_ms[2]};
+    if (c->staged_events && cudaEventSynchronize(c->ev[2]) == cudaSuccess) {
+        // read the events of the last ws_plan_staged directly (no fetch needed)
+        float ms = 0;
+        if (cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]) == cudaSuccess) ms3[0] = ms;
+        if (cudaEventElapsedTime(&ms, c->ev[1], c->ev[3]) == cudaSuccess) ms3[1] = ms;
+        if (cudaEventElapsedTime(&ms, c->ev[3], c->ev[2]) == cudaSuccess) ms3[2] = ms;
+    }
+    for (int i = 0; i < n && i < 3; ++i) out[i] = ms3[i];
     return 0;
 }
 
@@ -573,6 +582,7 @@ int ws_plan_staged(ws_ctx* ctx, void* stream) {
     }
     CK(cudaEventRecord(ctx->ev[2], st));
     CK(cudaGetLastError());
+    ctx->staged_events = P > 0;
     ctx->records_on_device = true;
     ctx->sim_valid = false;
     return 0;
@@ -772,6 +782,7 @@ int ws_plan_batch_host(ws_ctx* ctx, const ws_batch* in, ws_plan_result* results,
     CK(cudaMemcpyAsync(counters, ctx->host_tops + 2 * kMaxHostChunks, 8, cudaMemcpyHostToDevice, st));
     CK(cudaStreamSynchronize(st));
     float ms = 0;
+    ctx->staged_events = false;
     ctx->kernel_ms[0] = ctx->kernel_ms[1] = 0;  // chunked: only the whole pipeline is timed
     if (cudaEventElapsedTime(&ms, ctx->ev[0], ctx->ev[2]) == cudaSuccess) ctx->kernel_ms[2] = ms;
     ctx->records_on_device = true;
