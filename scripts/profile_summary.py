@@ -69,7 +69,8 @@ for rep in sorted(g.glob(f"*_{tag}.ncu-rep")):
         v = float(data[i].replace(",", ""))
         u = units[i].lower()
         return v * {"byte": 1, "kbyte": 1e3, "mbyte": 1e6, "gbyte": 1e9}.get(u, 1)
-    kname = data[hdr.index("Kernel Name")].split("(")[0].split("::")[-1]
+    kname = data[hdr.index("Kernel Name")].split("(")[0].split("::")[-1].split("<")[0]
+    kname = kname[len("void "):] if kname.startswith("void ") else kname
     traffic[kname] = val("dram__bytes_read.sum") + val("dram__bytes_write.sum")
 (out_dir / "traffic.json").write_text(json.dumps(traffic, indent=1) + "\n")
 print(traffic)
