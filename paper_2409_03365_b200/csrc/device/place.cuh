@@ -126,6 +126,10 @@ struct PCtx {
     int dev_off, dev_cnt;  // device block of the current place() call ([0, N) unless grouped)
     uint64_t all;
     uint64_t* flows;  // this plan's flow list (2 words per flow)
+    // plan options hoisted out of the per-attempt loops (registers, not global loads)
+    double gmul1;     // 1 + grad_opt_multiplier
+    double cap;       // mem_capacity
+    int sequential;
     template <typename T>
     __device__ __forceinline__ T* at(int off) const {
         return reinterpret_cast<T*>(sm + off);
@@ -199,7 +203,7 @@ __device__ int p_wave(PCtx& C, int w, int variant) {
     __syncwarp();
     for (int i = lane; i < ec; i += 32) {
         int pos = i;
-        if (!R.sequential) {
+        if (!C.sequential) {
             pos = 0;
             const int ki = e_k[eb + i];
             for (int j = 0; j < ec; ++j) {
@@ -214,7 +218,7 @@ __device__ int p_wave(PCtx& C, int w, int variant) {
     WS_PH_STOP(tw, 1);
     uint64_t free = C.all;
     uint64_t placed_now = 0;
-    int cursor = R.sequential ? w_cursor[w] : 0;
+    int cursor = C.sequential ? w_cursor[w] : 0;
     for (int oi = 0; oi < ec; ++oi) {
         const int e = eb + eorder[oi];
         const int k = e_k[e], n = e_n[e], lay = e_l[e];
@@ -254,9 +258,9 @@ __device__ int p_wave(PCtx& C, int w, int variant) {
         WS_PH_STOP(tw, 2);
         // memory_delta constants (:132-140)
         const double A = lay * (static_cast<double>(memact[k]) / n);
-        const double Pm = (1.0 + R.grad_mult) * static_cast<double>(parb[k]) / tpk[k];
+        const double Pm = C.gmul1 * static_cast<double>(parb[k]) / tpk[k];
         const uint64_t charged = chg[gkey[k]];
-        const double cap = static_cast<double>(R.mem_capacity);
+        const double cap = C.cap;
         // device memory if this entry lands there (memory_delta), once per entry
         double* used_if = C.at<double>(L.used_if);
         for (int dv = lane; dv < N; dv += 32) {
@@ -300,7 +304,7 @@ __device__ int p_wave(PCtx& C, int w, int variant) {
 
         Score chosen;
         chosen.valid = 0;
-        if (R.sequential) {
+        if (C.sequential) {
             if (popc64(free) >= n) {  // rolling cursor block (:350-358), within the device block
                 uint64_t m = 0;
                 for (int i = 0; i < n; ++i) m |= 1ull << (C.dev_off + (cursor + i) % C.dev_cnt);
@@ -648,6 +652,9 @@ __global__ void __launch_bounds__(32 * kPlaceWarps, WS_PLACE_MINB) k_place(Place
     C.ctl = ctl;
     C.lane = lane;
     C.N = R.n_dev;
+    C.gmul1 = 1.0 + R.grad_mult;
+    C.cap = static_cast<double>(R.mem_capacity);
+    C.sequential = R.sequential;
     C.K = h.K;
     C.mbase = R.mod_begin;
     C.nW = h.nW;
@@ -888,7 +895,7 @@ __global__ void __launch_bounds__(32 * kPlaceWarps, WS_PLACE_MINB) k_place(Place
                     const int e = w_eb[w] + i;
                     const int ke = e_k[e];
                     const double Ae = e_l[e] * (static_cast<double>(memact[ke]) / e_n[e]);
-                    const double Pe = (1.0 + R.grad_mult) * static_cast<double>(parb[ke]) / tpk[ke];
+                    const double Pe = C.gmul1 * static_cast<double>(parb[ke]) / tpk[ke];
                     const uint64_t charged = chg[gkey[ke]];
                     for (int dv = lane; dv < N; dv += 32) {
                         if (!(e_mask[e] >> dv & 1ull)) continue;
