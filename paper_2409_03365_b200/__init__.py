@@ -235,7 +235,7 @@ class ProblemSet:
 
     def __del__(self):
         h, self._h = getattr(self, "_h", None), None
-        if h:
+        if h and lib is not None:  # module globals are gone at interpreter shutdown
             lib.wsx_set_free(h)
 
     def __len__(self) -> int:
@@ -377,7 +377,7 @@ class Results:
     def __del__(self):
         for name in ("_res_ptr", "_arena_ptr"):
             ptr = getattr(self, name, None)
-            if ptr:
+            if ptr and lib is not None:
                 lib.wsx_host_free(ptr)
                 setattr(self, name, None)
 
@@ -418,7 +418,7 @@ class Planner:
         self._h = h
 
     def close(self):
-        if getattr(self, "_h", None):
+        if getattr(self, "_h", None) and lib is not None:
             lib.ws_ctx_destroy(self._h)
             self._h = None
 

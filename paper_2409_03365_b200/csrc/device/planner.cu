@@ -21,6 +21,7 @@
 #include <string>
 #include <vector>
 
+#include "../host/bounds.h"
 #include "fit.cuh"
 #include "place.cuh"
 #include "sched.cuh"
@@ -119,11 +120,11 @@ struct LaunchCaps {
     bool baseline;  // the batch has baseline-strategy plans (k_place<true>)
 };
 
-LaunchCaps batch_caps(const ws_plan_rec* plans, int P, bool hard) {
+// Batch maxima that size a launch (one pass over the plan records).
+struct BatchMax {
     int M = 1, N = 1, IS = 1, gmax = 0, T = 1;
     bool scoped = false, baseline = false;
-    for (int p = 0; p < P; ++p) {
-        const ws_plan_rec& r = plans[p];
+    void add(const ws_plan_rec& r) {
         M = std::max(M, r.n_mod);
         N = std::max(N, r.n_dev);
         IS = std::max(IS, r.n_islands);
@@ -132,11 +133,14 @@ LaunchCaps batch_caps(const ws_plan_rec* plans, int P, bool hard) {
         scoped |= r.strategy == WS_STRATEGY_DISTMM_MT || r.strategy == WS_STRATEGY_TASK_OPTIMUS;
         baseline |= r.strategy != WS_STRATEGY_WAVEFRONT;
     }
-    M = std::min(M, WS_MAX_MODULES);
-    N = std::min(N, WS_MAX_DEVICES);
-    IS = std::min(IS, N);
+};
+
+LaunchCaps caps_from(const BatchMax& b, bool hard) {
+    const int M = std::min(b.M, WS_MAX_MODULES);
+    const int N = std::min(b.N, WS_MAX_DEVICES);
+    const int IS = std::min(b.IS, N);
     // placement entities: the MetaOps, or up to 64 (MetaOp, task) pairs
-    const int ME = scoped ? WS_MAX_MODULES : M;
+    const int ME = b.scoped ? WS_MAX_MODULES : M;
     const int W = std::min(WS_MAX_WAVES, 2 * ME + 1);  // each wave drains a tuple
     int E, F;
     if (hard) {
@@ -148,12 +152,18 @@ LaunchCaps batch_caps(const ws_plan_rec* plans, int P, bool hard) {
     }
     LaunchCaps c;
     c.M = M;
-    c.T = std::min(T, WS_MAX_TASKS);
-    c.scoped = scoped;
-    c.baseline = baseline;
+    c.T = std::min(b.T, WS_MAX_TASKS);
+    c.scoped = b.scoped;
+    c.baseline = b.baseline;
     c.rec = RecCaps{ME, W, E};
-    c.pl = PlaceCaps{ME, N, W, E, F, gmax + ME, IS};
+    c.pl = PlaceCaps{ME, N, W, E, F, b.gmax + ME, IS};
     return c;
+}
+
+LaunchCaps batch_caps(const ws_plan_rec* plans, int P, bool hard) {
+    BatchMax b;
+    for (int p = 0; p < P; ++p) b.add(plans[p]);
+    return caps_from(b, hard);
 }
 
 int warps_for(int bytes_per_warp, int want) {
@@ -172,6 +182,7 @@ struct ws_ctx {
     DevBuf blob, order;
     ws_batch dview{};
     std::vector<int32_t> order_host, key_count;  // launch order (pageable: copied before the call returns)
+    std::vector<uint16_t> lpt_keys;              // per-plan LPT key of the pipelined host call
     LaunchCaps caps{}, caps_hard{};
     // K2 outputs
     DevBuf fit_err, fit_a, fit_b, fit_np, fit_nmax, fit_off, fit_pieces, ttab;
@@ -510,19 +521,19 @@ int prepare_plan(ws_ctx* ctx, FitOut& fo) {
     return 0;
 }
 
-// longest-processing-time launch order of plans [p0, p1): descending
-// modules x devices by a stable counting sort (O(plans) on the host)
+// longest-processing-time launch order: descending modules x devices, stable
+constexpr int kLptKeys = (WS_MAX_MODULES + 1) * (WS_MAX_DEVICES + 9);
+inline int lpt_key(const ws_plan_rec& r) {
+    const int m = std::min(std::max(r.n_mod, 0), WS_MAX_MODULES), d = std::min(std::max(r.n_dev, 0), WS_MAX_DEVICES);
+    return kLptKeys - 1 - m * (d + 8);
+}
+
+// LPT order of plans [p0, p1) by a stable counting sort (O(plans) on the host)
 void lpt_order(ws_ctx* ctx, const ws_plan_rec* plans, int p0, int p1) {
-    constexpr int kKeys = (WS_MAX_MODULES + 1) * (WS_MAX_DEVICES + 9);
-    auto key = [&](int p) {
-        const ws_plan_rec& r = plans[p];
-        const int m = std::min(std::max(r.n_mod, 0), WS_MAX_MODULES), d = std::min(std::max(r.n_dev, 0), WS_MAX_DEVICES);
-        return kKeys - 1 - m * (d + 8);
-    };
-    ctx->key_count.assign(kKeys + 1, 0);
-    for (int p = p0; p < p1; ++p) ctx->key_count[key(p) + 1]++;
-    for (int k = 0; k < kKeys; ++k) ctx->key_count[k + 1] += ctx->key_count[k];
-    for (int p = p0; p < p1; ++p) ctx->order_host[p0 + ctx->key_count[key(p)]++] = p;
+    ctx->key_count.assign(kLptKeys + 1, 0);
+    for (int p = p0; p < p1; ++p) ctx->key_count[lpt_key(plans[p]) + 1]++;
+    for (int k = 0; k < kLptKeys; ++k) ctx->key_count[k + 1] += ctx->key_count[k];
+    for (int p = p0; p < p1; ++p) ctx->order_host[p0 + ctx->key_count[lpt_key(plans[p])]++] = p;
 }
 }  // namespace
 
@@ -638,9 +649,6 @@ int ws_plan_batch_host(ws_ctx* ctx, const ws_batch* in, ws_plan_result* results,
         return fail(ctx, "cudaMalloc batch");
     char* dblob = ctx->blob.as<char>();
     ctx->dview = rebase(*in, in->blob, dblob);
-    ctx->caps = batch_caps(in->plans, P, false);
-    ctx->caps_hard = batch_caps(in->plans, P, true);
-    ctx->sim_cap = ws_sim_arena_bound(in);
     ctx->sim_valid = false;
     int pb[kMaxHostChunks + 1];
     uint64_t abase[kMaxHostChunks + 1];
@@ -655,11 +663,36 @@ int ws_plan_batch_host(ws_ctx* ctx, const ws_batch* in, ws_plan_result* results,
         wacc += c < static_cast<int>(ctx->host_weights.size()) ? ctx->host_weights[c] : 1.0;
         pb[c + 1] = c + 1 == C ? P : std::max(pb[c] + 1, std::min(P - (C - 1 - c), static_cast<int>(P * (wacc / wsum))));
     }
+    // ONE pass over the plan records: launch maxima, per-chunk arena bounds, the
+    // evaluation bound and per-chunk LPT key histograms; then one scatter pass
+    // (the host work before the first copy is exposed in the end-to-end time)
+    BatchMax bm;
+    uint64_t sim_total = 0;
+    ctx->lpt_keys.resize(P);
+    ctx->key_count.assign(static_cast<size_t>(C) * (kLptKeys + 1), 0);
     for (int c = 0; c < C; ++c) {
-        abase[c + 1] = abase[c] + wsi_arena_bound_plans(in->plans + pb[c], pb[c + 1] - pb[c]);
-        lpt_order(ctx, in->plans, pb[c], pb[c + 1]);
+        uint64_t ab = 0;
+        int* hist = ctx->key_count.data() + static_cast<size_t>(c) * (kLptKeys + 1);
+        for (int p = pb[c]; p < pb[c + 1]; ++p) {
+            const ws_plan_rec& r = in->plans[p];
+            bm.add(r);
+            ab += wsi_plan_arena_bound(&r);
+            sim_total += wsi_plan_sim_bound(&r);
+            const int key = lpt_key(r);
+            ctx->lpt_keys[p] = static_cast<uint16_t>(key);
+            hist[key + 1]++;
+        }
+        abase[c + 1] = abase[c] + ab;
         ctx->host_tops[c] = abase[c];
     }
+    for (int c = 0; c < C; ++c) {
+        int* hist = ctx->key_count.data() + static_cast<size_t>(c) * (kLptKeys + 1);
+        for (int k = 0; k < kLptKeys; ++k) hist[k + 1] += hist[k];
+        for (int p = pb[c]; p < pb[c + 1]; ++p) ctx->order_host[pb[c] + hist[ctx->lpt_keys[p]]++] = p;
+    }
+    ctx->caps = caps_from(bm, false);
+    ctx->caps_hard = caps_from(bm, true);
+    ctx->sim_cap = sim_total + 4096;  // == ws_sim_arena_bound(in)
     ctx->arena_cap = abase[C];
     if (ctx->arena_cap > arena_cap) return fail(ctx, "ws_plan_batch_host: arena buffer too small");
     FitOut fo;

@@ -6,6 +6,7 @@
 #include <algorithm>
 #include <cstring>
 
+#include "bounds.h"
 #include "wsgpu/planner.hpp"
 
 namespace wsgpu {
@@ -374,12 +375,7 @@ std::string plan_text_or_error(const Problem& prob, const ws_plan_result& r, con
 // (internal) the same bound summed over plans[0, n): a pipelined chunk's share
 extern "C" uint64_t wsi_arena_bound_plans(const ws_plan_rec* plans, int n) {
     uint64_t total = 0;
-    for (int p = 0; p < n; ++p) {
-        const uint64_t M = static_cast<uint64_t>(plans[p].n_mod);
-        total += 64 + sizeof(ws_out_metaop) * M + sizeof(ws_out_level) * M + sizeof(ws_out_piece) * 4 * M +
-                 sizeof(ws_out_edge) * M * M + sizeof(ws_out_wave) * 4 * M + sizeof(ws_out_entry) * 8 * M +
-                 sizeof(ws_out_flow) * 16 * M;
-    }
+    for (int p = 0; p < n; ++p) total += wsi_plan_arena_bound(plans + p);
     return total;
 }
 

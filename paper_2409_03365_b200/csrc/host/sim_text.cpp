@@ -15,6 +15,7 @@
 #include <string>
 #include <vector>
 
+#include "bounds.h"
 #include "wsgpu/planner.hpp"
 
 namespace wsgpu {
@@ -153,8 +154,6 @@ std::string sim_text_named(const ClusterTopology& topo, const ws_plan_result& r,
 
 extern "C" uint64_t ws_sim_arena_bound(const ws_batch* in) {
     uint64_t total = 0;
-    for (int p = 0; p < in->n_plans; ++p)
-        total += 16ull * in->plans[p].n_dev + 8ull * in->plans[p].n_mod + 16 +
-                 sizeof(ws_out_violation) * WS_SIM_MAX_VIOLATIONS;
+    for (int p = 0; p < in->n_plans; ++p) total += wsi_plan_sim_bound(in->plans + p);
     return total + 4096;
 }
