@@ -19,6 +19,7 @@
 #include <cstring>
 #include <numeric>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../host/bounds.h"
@@ -183,6 +184,8 @@ struct ws_ctx {
     ws_batch dview{};
     std::vector<int32_t> order_host, key_count;  // launch order (pageable: copied before the call returns)
     std::vector<uint16_t> lpt_keys;              // per-plan LPT key of the pipelined host call
+    int32_t* order_pinned = nullptr;             // its launch order, page-locked so the chunk
+    size_t order_pinned_n = 0;                   //   copies stay asynchronous
     LaunchCaps caps{}, caps_hard{};
     // K2 outputs
     DevBuf fit_err, fit_a, fit_b, fit_np, fit_nmax, fit_off, fit_pieces, ttab;
@@ -220,12 +223,12 @@ struct ws_ctx {
     unsigned long long* host_tops = nullptr; // page-locked: chunk bases, chunk tops, final top
     // measured (100k sweep, ms): one compute stream: 1 chunk 27.8, 2: 27.4, 4: 32.0 (each
     // chunk's k_sched + k_place launch tail outweighs the hidden copies); two compute
-    // streams (consecutive chunks fill each other's tails): 3 uniform 25.5, weights
-    // 1,3,1 23.5, 1,3,3,1 23.9, 1,6,1 25.5, 1,2,2,2,1 25.0 -> default 1,3,1 x 2 streams
-    int host_chunks = 3;                     // $WSGPU_HOST_CHUNKS
+    // streams (consecutive chunks fill each other's tails) with completion-order D2H:
+    // weights 1,3,1 24.9, 1,3,3,1 22.8, 1,4,4,1 22.8, 1,3,3,3,1 22.8, 1,5,5,1 23.8
+    int host_chunks = 4;                     // $WSGPU_HOST_CHUNKS
     int host_streams = 2;                    // $WSGPU_HOST_STREAMS (1 or 2)
     bool force_snap = false;                 // $WSGPU_FORCE_SNAP: k_place<true> for every batch (tuning)
-    std::vector<double> host_weights{1, 3, 1};  // $WSGPU_HOST_WEIGHTS: relative chunk sizes (sets the chunk count)
+    std::vector<double> host_weights{1, 3, 3, 1};  // $WSGPU_HOST_WEIGHTS: relative chunk sizes (sets the chunk count)
     ws_plan_result* res_out() { return d_results ? d_results : results.as<ws_plan_result>(); }
     uint8_t* arena_out() { return d_arena ? d_arena : arena.as<uint8_t>(); }
     uint64_t cap_out() const { return d_arena ? d_cap : arena_cap; }
@@ -451,6 +454,7 @@ void ws_ctx_destroy(ws_ctx* c) {
     if (c->stream3) cudaStreamDestroy(c->stream3);
     if (c->stream4) cudaStreamDestroy(c->stream4);
     if (c->host_tops) cudaFreeHost(c->host_tops);
+    if (c->order_pinned) cudaFreeHost(c->order_pinned);
     delete c;
 }
 
@@ -623,8 +627,8 @@ int ws_fetch_results(ws_ctx* ctx, ws_plan_result* results, uint8_t* arena, uint6
 
 extern "C" uint64_t wsi_arena_bound_plans(const ws_plan_rec* plans, int n);
 
-// Host batch in, host results out.  Batches of >= 3 x 4096 plans run as a
-// pipeline over chunks of plans (default sizes 1:3:1, $WSGPU_HOST_WEIGHTS /
+// Host batch in, host results out.  Batches of >= 2 x 4096 plans run as a
+// pipeline over chunks of plans (default sizes 1:3:3:1, $WSGPU_HOST_WEIGHTS /
 // $WSGPU_HOST_CHUNKS): the H2D copy of chunk c+1 (its byte ranges of every SoA
 // section: sections are plan-ordered, so a chunk's rows are contiguous) and the
 // D2H copy of chunk c-1 (results rows + its own arena region) overlap the
@@ -653,7 +657,14 @@ int ws_plan_batch_host(ws_ctx* ctx, const ws_batch* in, ws_plan_result* results,
     int pb[kMaxHostChunks + 1];
     uint64_t abase[kMaxHostChunks + 1];
     abase[0] = 0;
-    ctx->order_host.resize(P);
+    if (ctx->order_pinned_n < static_cast<size_t>(P)) {
+        if (ctx->order_pinned) cudaFreeHost(ctx->order_pinned);
+        ctx->order_pinned = nullptr;
+        ctx->order_pinned_n = 0;
+        if (cudaMallocHost(reinterpret_cast<void**>(&ctx->order_pinned), 4ull * P) != cudaSuccess)
+            return fail(ctx, "cudaMallocHost launch order");
+        ctx->order_pinned_n = P;
+    }
     // chunk boundaries: uniform, or proportional to $WSGPU_HOST_WEIGHTS ("1,3,3,1": small
     // first/last chunks shorten the exposed first H2D and last D2H copies)
     double wsum = 0, wacc = 0;
@@ -688,7 +699,7 @@ int ws_plan_batch_host(ws_ctx* ctx, const ws_batch* in, ws_plan_result* results,
     for (int c = 0; c < C; ++c) {
         int* hist = ctx->key_count.data() + static_cast<size_t>(c) * (kLptKeys + 1);
         for (int k = 0; k < kLptKeys; ++k) hist[k + 1] += hist[k];
-        for (int p = pb[c]; p < pb[c + 1]; ++p) ctx->order_host[pb[c] + hist[ctx->lpt_keys[p]]++] = p;
+        for (int p = pb[c]; p < pb[c + 1]; ++p) ctx->order_pinned[pb[c] + hist[ctx->lpt_keys[p]]++] = p;
     }
     ctx->caps = caps_from(bm, false);
     ctx->caps_hard = caps_from(bm, true);
@@ -738,7 +749,7 @@ int ws_plan_batch_host(ws_ctx* ctx, const ws_batch* in, ws_plan_result* results,
         CK(rows(h.bps, 4, first(h.mod_bp_off, m0, nm, h.n_bps), first(h.mod_bp_off, m1, nm, h.n_bps)));
         CK(rows(h.names, 1, first(h.mod_name_off, m0, nm, h.n_name_bytes),
                 first(h.mod_name_off, m1, nm, h.n_name_bytes)));
-        CK(cudaMemcpyAsync(ctx->order.as<int32_t>() + p0, ctx->order_host.data() + p0, 4ull * (p1 - p0),
+        CK(cudaMemcpyAsync(ctx->order.as<int32_t>() + p0, ctx->order_pinned + p0, 4ull * (p1 - p0),
                            cudaMemcpyHostToDevice, sh));
         CK(cudaEventRecord(h2d[c], sh));
     }
@@ -796,17 +807,29 @@ int ws_plan_batch_host(ws_ctx* ctx, const ws_batch* in, ws_plan_result* results,
     }
     CK(cudaEventRecord(ctx->ev[2], st));
     uint64_t used = 0;
-    for (int c = 0; c < C; ++c) {  // D2H side, as each chunk completes
-        CK(cudaEventSynchronize(done[c]));
-        uint64_t top = ctx->host_tops[kMaxHostChunks + c];
-        top = std::min<uint64_t>(top, abase[c + 1]);
-        CK(cudaStreamWaitEvent(sd, done[c], 0));
-        CK(cudaMemcpyAsync(results + pb[c], ctx->results.as<ws_plan_result>() + pb[c],
-                           sizeof(ws_plan_result) * (pb[c + 1] - pb[c]), cudaMemcpyDeviceToHost, sd));
-        if (top > abase[c])
-            CK(cudaMemcpyAsync(arena + abase[c], ctx->arena.as<uint8_t>() + abase[c], top - abase[c],
-                               cudaMemcpyDeviceToHost, sd));
-        used = std::max<uint64_t>(used, top);
+    // D2H side, in completion order (chunks on two compute streams finish out of
+    // order): poll the chunk events and copy each finished chunk back at once
+    bool copied[kMaxHostChunks] = {};
+    for (int left = C; left > 0;) {
+        bool progressed = false;
+        for (int c = 0; c < C; ++c) {
+            if (copied[c]) continue;
+            const cudaError_t q = cudaEventQuery(done[c]);
+            if (q == cudaErrorNotReady) continue;
+            CK(q);
+            uint64_t top = ctx->host_tops[kMaxHostChunks + c];
+            top = std::min<uint64_t>(top, abase[c + 1]);
+            CK(cudaMemcpyAsync(results + pb[c], ctx->results.as<ws_plan_result>() + pb[c],
+                               sizeof(ws_plan_result) * (pb[c + 1] - pb[c]), cudaMemcpyDeviceToHost, sd));
+            if (top > abase[c])
+                CK(cudaMemcpyAsync(arena + abase[c], ctx->arena.as<uint8_t>() + abase[c], top - abase[c],
+                                   cudaMemcpyDeviceToHost, sd));
+            used = std::max<uint64_t>(used, top);
+            copied[c] = true;
+            --left;
+            progressed = true;
+        }
+        if (!progressed) std::this_thread::yield();
     }
     CK(cudaStreamSynchronize(sd));
     CK(cudaStreamSynchronize(st));

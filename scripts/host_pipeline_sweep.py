@@ -44,15 +44,16 @@ for chunks, streams in configs:
     res = pl.plan(ps)
     res = pl.plan(ps, out=res)
     times = []
-    for _ in range(8):
+    for _ in range(20):
         t0 = time.perf_counter()
         res = pl.plan(ps, out=res)
         times.append(time.perf_counter() - t0)
     d = digest(res)
     ref = ref or d
-    ms = sorted(times)[len(times) // 2] * 1e3
+    ts = sorted(times)
+    ms = ts[len(ts) // 2] * 1e3
     bad = [i for i in range(n) if d[i] != ref[i]]
-    print(f"chunks={chunks} streams={streams}: median {ms:7.2f} ms  min {min(times) * 1e3:7.2f} ms  "
+    print(f"chunks={chunks} streams={streams}: median {ms:7.2f} ms  min {ts[0] * 1e3:7.2f}  p90 {ts[int(0.9 * len(ts))] * 1e3:7.2f} ms  "
           f"{n / ms * 1e3 / 1e6:5.2f} M plans/s  records "
           f"{'identical' if not bad else f'DIFFER on {len(bad)} plans, first {bad[:5]}'}", flush=True)
     pl.close()
