@@ -426,6 +426,36 @@ def main() -> None:
         except Exception:
             traffic = None
 
+    # ---- candidate-plan search of one workload: the 96 planner
+    # variants of each BASELINE config planned in one batch, best selected on the
+    # device (k_best); latency = host batch in -> best index out ----
+    from paper_2409_03365_b200 import candidates as cd
+    variants = cd.candidate_variants()
+    cand = {"variants": len(variants), "key": "makespan (predicted, planner.hpp:193-194)",
+            "what": "stage (H2D) + plan all variants + on-device min-loc + D2H of {key, index}", "configs": {}}
+    for name, (fam, tasks, devices) in CONFIGS.items():
+        pcs = cd.candidate_set_for_scenario(fam, tasks, devices, 0, variants)
+        for _ in range(3):
+            cd.best_candidate(planner, pcs, "makespan", sptr)
+        samples = []
+        for _ in range(max(args.latency_reps // 2, 5)):
+            t0 = time.perf_counter()
+            bk, bi = cd.best_candidate(planner, pcs, "makespan", sptr)
+            samples.append((time.perf_counter() - t0) * 1000.0)
+        ms = statistics.median(samples)
+        cand["configs"][name] = {"gpu_ms": ms, "candidate_plans_per_s": len(variants) / ms * 1000.0,
+                                 "best_index": bi, "best_makespan": bk}
+        if not args.no_cpu_baseline:
+            try:
+                import pyoracle as po
+                if po.ref_available():
+                    rms, rbi = po.ref_candidates_ms(pcs.dump_workload(0), pcs.dump_topology(0), variants,
+                                                    os.cpu_count() or 1)
+                    cand["configs"][name].update({"cpu_reference_ms": rms, "cpu_threads": os.cpu_count(),
+                                                  "reference_best_index": rbi})
+            except Exception:
+                pass
+
     # ---- single-plan latency of the BASELINE configs ----
     latency = {}
     for name, (fam, tasks, devices) in CONFIGS.items():
@@ -523,6 +553,7 @@ def main() -> None:
         "evaluation": evaluation,
         "baselines": baselines,
         "compare": compare,
+        "candidates": cand,
         "parity": {"infeasible_plans": int(infeasible.item()), "best_gap": best_key, "best_index": best_idx},
     }
     print(json.dumps(line), flush=True)

@@ -139,6 +139,9 @@ def ref():
         lib.wsref_sweep_workload.argtypes = [C.c_long, C.POINTER(vp)]
         lib.wsref_sweep_compare_bench.restype = C.c_double
         lib.wsref_sweep_compare_bench.argtypes = [C.c_long, C.c_long, C.c_int]
+        lib.wsref_candidates_ms.restype = C.c_double
+        lib.wsref_candidates_ms.argtypes = [C.c_char_p, C.c_char_p, C.POINTER(RefOpts), C.c_int, C.c_int,
+                                            C.POINTER(C.c_long)]
         lib.wsref_latency_ms.restype = C.c_double
         lib.wsref_latency_ms.argtypes = [C.c_char_p, C.c_int, C.c_int, C.c_int]
         _ref = lib
@@ -232,3 +235,38 @@ def ref_sweep_compare_bench(start: int, count: int, threads: int) -> float:
     """Reference compare loop (all strategies planned + validated + simulated) over
     sweep mixtures; workloads/s on `threads` threads."""
     return ref().wsref_sweep_compare_bench(start, count, threads)
+
+
+def best_candidate(pset, key: str = "makespan") -> tuple[float, int]:
+    """Oracle side of the candidate search (paper_2409_03365_b200.candidates):
+    every candidate planned (and, for "simulated", evaluated) on the CPU oracle,
+    then the same selection rule -- key = end_time / lower_bound ("gap"),
+    end_time ("makespan") or the simulated makespan; failed plans are +inf;
+    ties go to the smaller index.  Returns (key, index), (+inf, -1) if none."""
+    res = plan_batch(pset)
+    sims = simulate_batch(pset, res) if key == "simulated" else None
+    best_k, best_i = float("inf"), -1
+    for i in range(len(pset)):
+        r = res.results[i]
+        if r.status != 0:
+            continue
+        if key == "gap":
+            k = r.end_time / r.lower_bound
+        elif key == "makespan":
+            k = r.end_time
+        else:
+            if sims.results[i].status != 0:
+                continue
+            k = sims.results[i].makespan
+        if best_i < 0 or k < best_k:
+            best_k, best_i = k, i
+    return best_k, best_i
+
+
+def ref_candidates_ms(workload: str, topology: str, variants: list[dict], threads: int) -> tuple[float, int]:
+    """Reference planner over every candidate variant of one workload on `threads`
+    threads: (wall ms, best candidate index by predicted makespan)."""
+    arr = (RefOpts * len(variants))(*[ref_options(**v) for v in variants])
+    best = C.c_long(-1)
+    ms = ref().wsref_candidates_ms(workload.encode(), topology.encode(), arr, len(variants), threads, C.byref(best))
+    return ms, best.value

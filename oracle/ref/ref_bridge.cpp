@@ -452,6 +452,36 @@ double wsref_sweep_compare_bench(long start, long count, int threads) {
            std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
 }
 
+// CPU baseline of the candidate search: the reference plan_workload under each
+// of n option variants of one workload, on `threads` threads; writes the best
+// candidate by predicted makespan (ties -> smaller index, failures skipped).
+// Returns the wall time in ms (inputs parsed outside the timed region).
+double wsref_candidates_ms(const char* workload, const char* topology, const wsref_opts* opts, int n, int threads,
+                           long* best_index) {
+    const WorkloadSpec spec = parse_workload(workload);
+    const ClusterTopology topo = parse_topology(topology);
+    std::vector<double> key(n, -1.0);
+    std::atomic<int> next{0};
+    auto worker = [&] {
+        for (int i; (i = next.fetch_add(1)) < n;) {
+            try {
+                key[i] = plan_workload(spec, topo, to_opts(opts + i)).predicted_makespan;
+            } catch (const Error&) {
+            }
+        }
+    };
+    const auto t0 = std::chrono::steady_clock::now();
+    std::vector<std::thread> pool;
+    for (int t = 0; t < threads; ++t) pool.emplace_back(worker);
+    for (auto& th : pool) th.join();
+    const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    long best = -1;
+    for (int i = 0; i < n; ++i)
+        if (key[i] >= 0.0 && (best < 0 || key[i] < key[best])) best = i;
+    *best_index = best;
+    return ms;
+}
+
 // Single-plan latency of the reference planner (median of `reps`, ms).
 double wsref_latency_ms(const char* name, int tasks, int devices, int reps) {
     Scenario sc = generate_scenario(name, tasks, devices, 0);
