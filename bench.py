@@ -172,7 +172,7 @@ def main() -> None:
     ap.add_argument("--ref-sample", type=int, default=4000)
     ap.add_argument("--cpu-sample", type=int, default=6000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--latency-reps", type=int, default=50)
+    ap.add_argument("--latency-reps", type=int, default=300, help="single-plan latency samples (SURVEY 8(d): >= 300)")
     ap.add_argument("--compare-mixtures", type=int, default=25000,
                     help="sweep mixtures of the strategy-comparison block (each planned by all 4 strategies)")
     args = ap.parse_args()
@@ -438,7 +438,7 @@ def main() -> None:
         for _ in range(3):
             cd.best_candidate(planner, pcs, "makespan", sptr)
         samples = []
-        for _ in range(max(args.latency_reps // 2, 5)):
+        for _ in range(max(args.latency_reps // 6, 5)):
             t0 = time.perf_counter()
             bk, bi = cd.best_candidate(planner, pcs, "makespan", sptr)
             samples.append((time.perf_counter() - t0) * 1000.0)
@@ -470,7 +470,10 @@ def main() -> None:
             t0 = time.perf_counter()
             ro = planner.plan(one, sptr, out=ro)
             samples.append((time.perf_counter() - t0) * 1000.0)
-        latency[name] = {"gpu_e2e_ms_median": statistics.median(samples)}
+        ss = sorted(samples)
+        latency[name] = {"gpu_e2e_ms_median": statistics.median(samples), "gpu_e2e_ms_p10": ss[len(ss) // 10],
+                         "gpu_e2e_ms_p90": ss[(9 * len(ss)) // 10], "samples": len(ss),
+                         "path": "ws_plan_batch_host, one plan, pinned host in/out"}
 
     cpu = None
     evaluation = {"what": "simulate_plan + validate_plan of every planned mixture (k_sim, device-resident records)",
@@ -493,7 +496,7 @@ def main() -> None:
             import pyoracle as po
             if po.ref_available():
                 for name, (fam, tasks, devices) in CONFIGS.items():
-                    latency[name]["cpu_reference_ms_median"] = po.ref_latency_ms(fam, tasks, devices, 100)
+                    latency[name]["cpu_reference_ms_median"] = po.ref_latency_ms(fam, tasks, devices, max(args.latency_reps, 1))
         except Exception:
             pass
         try:
