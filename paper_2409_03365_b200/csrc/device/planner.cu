@@ -40,7 +40,9 @@ constexpr int kMaxHostChunks = 8;
 // k_place snapshot slots: only warps of plans that fail a wave claim one (a few
 // hundred per 100k sweep), so a small pool serves every resident warp; a warp
 // that finds none falls back to replaying the committed waves
-constexpr int kSnapSlots = 512;  // H2D / compute / D2H pipeline depth of ws_plan_batch_host
+constexpr int kSnapSlots = 512;
+// arena bound up to which ws_fetch_results copies the whole bound in one go
+constexpr uint64_t kOneSyncArena = 256u << 10;  // H2D / compute / D2H pipeline depth of ws_plan_batch_host
 
 struct DevBuf {
     void* p = nullptr;
@@ -182,10 +184,12 @@ struct ws_ctx {
     // staged batch
     DevBuf blob, order;
     ws_batch dview{};
-    std::vector<int32_t> order_host, key_count;  // launch order (pageable: copied before the call returns)
+    std::vector<int32_t> key_count;              // LPT counting-sort histograms
     std::vector<uint16_t> lpt_keys;              // per-plan LPT key of the pipelined host call
-    int32_t* order_pinned = nullptr;             // its launch order, page-locked so the chunk
-    size_t order_pinned_n = 0;                   //   copies stay asynchronous
+    int32_t* order_pinned = nullptr;             // launch order, page-locked so its H2D
+    size_t order_pinned_n = 0;                   //   copies stay asynchronous;
+    cudaEvent_t order_ev = nullptr;              //   recorded after the last one (the host
+    bool order_ev_pending = false;               //   waits on it before rewriting the buffer)
     LaunchCaps caps{}, caps_hard{};
     // K2 outputs
     DevBuf fit_err, fit_a, fit_b, fit_np, fit_nmax, fit_off, fit_pieces, ttab;
@@ -409,6 +413,7 @@ int ws_ctx_create(int device, ws_ctx** out) {
         if (e) cudaEventDestroy(e);
     for (auto& e : c->ev) cudaEventCreate(&e);
     for (auto& e : c->cev) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&c->order_ev, cudaEventDisableTiming);
     for (auto& e : c->sev) cudaEventCreate(&e);
     if (cudaStreamCreateWithFlags(&c->stream2, cudaStreamNonBlocking) != cudaSuccess) {
         delete c;
@@ -455,6 +460,7 @@ void ws_ctx_destroy(ws_ctx* c) {
     if (c->stream4) cudaStreamDestroy(c->stream4);
     if (c->host_tops) cudaFreeHost(c->host_tops);
     if (c->order_pinned) cudaFreeHost(c->order_pinned);
+    if (c->order_ev) cudaEventDestroy(c->order_ev);
     delete c;
 }
 
@@ -533,11 +539,28 @@ inline int lpt_key(const ws_plan_rec& r) {
 }
 
 // LPT order of plans [p0, p1) by a stable counting sort (O(plans) on the host)
-void lpt_order(ws_ctx* ctx, const ws_plan_rec* plans, int p0, int p1) {
+void lpt_order(ws_ctx* ctx, const ws_plan_rec* plans, int p0, int p1, int32_t* out) {
     ctx->key_count.assign(kLptKeys + 1, 0);
     for (int p = p0; p < p1; ++p) ctx->key_count[lpt_key(plans[p]) + 1]++;
     for (int k = 0; k < kLptKeys; ++k) ctx->key_count[k + 1] += ctx->key_count[k];
-    for (int p = p0; p < p1; ++p) ctx->order_host[p0 + ctx->key_count[lpt_key(plans[p])]++] = p;
+    for (int p = p0; p < p1; ++p) out[p0 + ctx->key_count[lpt_key(plans[p])]++] = p;
+}
+
+// page-locked launch-order buffer of at least P entries (asynchronous H2D
+// copies), safe to rewrite: the previous call's copies have completed
+int ensure_order_pinned(ws_ctx* ctx, int P) {
+    if (ctx->order_ev_pending) {
+        cudaEventSynchronize(ctx->order_ev);
+        ctx->order_ev_pending = false;
+    }
+    if (ctx->order_pinned_n >= static_cast<size_t>(P)) return 0;
+    if (ctx->order_pinned) cudaFreeHost(ctx->order_pinned);
+    ctx->order_pinned = nullptr;
+    ctx->order_pinned_n = 0;
+    if (cudaMallocHost(reinterpret_cast<void**>(&ctx->order_pinned), 4ull * std::max(P, 1)) != cudaSuccess)
+        return fail(ctx, "cudaMallocHost launch order");
+    ctx->order_pinned_n = std::max(P, 1);
+    return 0;
 }
 }  // namespace
 
@@ -556,9 +579,13 @@ int ws_stage_batch(ws_ctx* ctx, const ws_batch* in, void* stream) {
     ctx->sim_cap = ws_sim_arena_bound(in);
     ctx->records_on_device = false;
     ctx->sim_valid = false;
-    ctx->order_host.resize(P);
-    lpt_order(ctx, in->plans, 0, P);
-    if (P) CK(cudaMemcpyAsync(ctx->order.p, ctx->order_host.data(), 4ull * P, cudaMemcpyHostToDevice, st));
+    if (ensure_order_pinned(ctx, P)) return 1;
+    lpt_order(ctx, in->plans, 0, P, ctx->order_pinned);
+    if (P) {
+        CK(cudaMemcpyAsync(ctx->order.p, ctx->order_pinned, 4ull * P, cudaMemcpyHostToDevice, st));
+        CK(cudaEventRecord(ctx->order_ev, st));
+        ctx->order_ev_pending = true;
+    }
     return 0;
 }
 
@@ -609,9 +636,15 @@ int ws_fetch_results(ws_ctx* ctx, ws_plan_result* results, uint8_t* arena, uint6
     cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
     const int P = ctx->dview.n_plans;
     unsigned long long top = 0;
+    // small batches (single-plan latency): copy the whole arena bound with the
+    // headers and the top counter, one synchronization instead of two
+    const bool one_sync = ctx->arena_cap <= kOneSyncArena && ctx->arena_cap <= arena_cap;
     if (P) CK(cudaMemcpyAsync(results, ctx->results.p, sizeof(ws_plan_result) * P, cudaMemcpyDeviceToHost, st));
-    CK(cudaMemcpyAsync(&top, ctx->counters.p, sizeof(top), cudaMemcpyDeviceToHost, st));
+    unsigned long long* htop = ctx->host_tops + 2 * kMaxHostChunks + 1;  // page-locked
+    CK(cudaMemcpyAsync(htop, ctx->counters.p, sizeof(top), cudaMemcpyDeviceToHost, st));
+    if (one_sync && ctx->arena_cap) CK(cudaMemcpyAsync(arena, ctx->arena.p, ctx->arena_cap, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
+    top = *htop;
     float ms = 0;
     ctx->kernel_ms[1] = ctx->kernel_ms[2] = 0;
     if (cudaEventElapsedTime(&ms, ctx->ev[0], ctx->ev[1]) == cudaSuccess) ctx->kernel_ms[0] = ms;
@@ -619,8 +652,10 @@ int ws_fetch_results(ws_ctx* ctx, ws_plan_result* results, uint8_t* arena, uint6
     if (P && cudaEventElapsedTime(&ms, ctx->ev[3], ctx->ev[2]) == cudaSuccess) ctx->kernel_ms[2] = ms;
     if (top > ctx->arena_cap) top = ctx->arena_cap;
     if (top > arena_cap) return fail(ctx, "ws_fetch_results: arena buffer too small");
-    if (top) CK(cudaMemcpyAsync(arena, ctx->arena.p, top, cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
+    if (!one_sync && top) {
+        CK(cudaMemcpyAsync(arena, ctx->arena.p, top, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+    }
     *arena_used = top;
     return 0;
 }
@@ -657,14 +692,7 @@ int ws_plan_batch_host(ws_ctx* ctx, const ws_batch* in, ws_plan_result* results,
     int pb[kMaxHostChunks + 1];
     uint64_t abase[kMaxHostChunks + 1];
     abase[0] = 0;
-    if (ctx->order_pinned_n < static_cast<size_t>(P)) {
-        if (ctx->order_pinned) cudaFreeHost(ctx->order_pinned);
-        ctx->order_pinned = nullptr;
-        ctx->order_pinned_n = 0;
-        if (cudaMallocHost(reinterpret_cast<void**>(&ctx->order_pinned), 4ull * P) != cudaSuccess)
-            return fail(ctx, "cudaMallocHost launch order");
-        ctx->order_pinned_n = P;
-    }
+    if (ensure_order_pinned(ctx, P)) return 1;
     // chunk boundaries: uniform, or proportional to $WSGPU_HOST_WEIGHTS ("1,3,3,1": small
     // first/last chunks shorten the exposed first H2D and last D2H copies)
     double wsum = 0, wacc = 0;
@@ -753,6 +781,8 @@ int ws_plan_batch_host(ws_ctx* ctx, const ws_batch* in, ws_plan_result* results,
                            cudaMemcpyHostToDevice, sh));
         CK(cudaEventRecord(h2d[c], sh));
     }
+    CK(cudaEventRecord(ctx->order_ev, sh));
+    ctx->order_ev_pending = true;
     ctx->launches = 0;
     CK(cudaMemsetAsync(counters, 0, 64, st));
     const ws_batch& B = ctx->dview;
