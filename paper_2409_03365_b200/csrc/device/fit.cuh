@@ -59,6 +59,8 @@ __global__ void __launch_bounds__(128) k_fit(ws_batch B, FitOut out, int m_begin
     int err = 0, ea = 0, eb = 0;
     int np = 0, nmax = 1;
     DPiece fp[WS_MAX_PIECES];
+    double fv[128];         // T(k) of the fitted curve at k = 1..nmax (when cache_fv)
+    bool cache_fv = false;
 
     do {
         if (B.mod_pre_err[m]) {
@@ -115,16 +117,21 @@ __global__ void __launch_bounds__(128) k_fit(ws_batch B, FitOut out, int m_begin
             ea = m - R.mod_begin;
             break;
         }
-        // point source: profile points, or truth.eval(n) for n = 1..N
+        // point source: profile points, or truth.eval(n) for n = 1..N, each
+        // truth value evaluated once (a pure function of n) and reused
         const int npts = has_prof ? B.mod_prof_n[m] : N;
         const int poff = has_prof ? B.mod_prof_off[m] : 0;
+        double tv[WS_MAX_DEVICES];
+        if (!has_prof)
+            for (int i = 0; i < N && i < WS_MAX_DEVICES; ++i)
+                tv[i] = piece_value(tp[locate_piece(tp, ntp, i + 1)], c, w, static_cast<double>(i + 1));
         auto point = [&](int i, int& n, double& t) {
             if (has_prof) {
                 n = B.prof_n[poff + i];
                 t = B.prof_t[poff + i];
             } else {
                 n = i + 1;
-                t = piece_value(tp[locate_piece(tp, ntp, n)], c, w, static_cast<double>(n));
+                t = tv[i];
             }
         };
         // fit_curve argument checks (scaling.hpp:231-238)
@@ -180,7 +187,10 @@ __global__ void __launch_bounds__(128) k_fit(ws_batch B, FitOut out, int m_begin
             const int lo = bounds[i], hi = bounds[i + 1];
             double sx = 0, sy = 0, sxy = 0, sxx = 0;
             int cnt = 0, nlo = 0x7fffffff, nhi = -1;
-            for (int j = 0; j < npts; ++j) {
+            // truth points are n = j + 1 in order: only the piece's own range
+            // contributes, visited in the same (ascending) order
+            const int j0 = has_prof ? 0 : (i == 0 ? lo - 1 : lo), j1 = has_prof ? npts : (hi < npts ? hi : npts);
+            for (int j = j0 < 0 ? 0 : j0; j < j1; ++j) {
                 int n;
                 double t;
                 point(j, n, t);
@@ -220,10 +230,19 @@ __global__ void __launch_bounds__(128) k_fit(ws_batch B, FitOut out, int m_begin
         }
         // isotonic check: PAV changes the anchors iff some adjacent pair violates
         // v[k-1] >= v[k] - 1e-15 (scaling.hpp:193-220, first merge is adjacent)
+        // T(k) at the integer anchors k = 1..nmax, evaluated once and reused by the
+        // isotonic check, the positivity check and the T-table
+        cache_fv = nmax <= 128;
+        auto fval = [&](int k) {
+            return cache_fv ? fv[k - 1] : piece_value(fp[locate_piece(fp, np, k)], c, w, static_cast<double>(k));
+        };
+        if (cache_fv)
+            for (int k = 1; k <= nmax; ++k)
+                fv[k - 1] = piece_value(fp[locate_piece(fp, np, k)], c, w, static_cast<double>(k));
         bool changed = false;
         double prev = 0.0;
         for (int k = 1; k <= nmax; ++k) {
-            const double v = piece_value(fp[locate_piece(fp, np, k)], c, w, static_cast<double>(k));
+            const double v = fval(k);
             if (k > 1 && prev < v - 1e-15) {
                 changed = true;
                 break;
@@ -239,7 +258,7 @@ __global__ void __launch_bounds__(128) k_fit(ws_batch B, FitOut out, int m_begin
             double bsum[128];
             int bcnt[128];
             int nbk = 0;
-            for (int k = 1; k <= nmax; ++k) vals[k - 1] = piece_value(fp[locate_piece(fp, np, k)], c, w, k);
+            for (int k = 1; k <= nmax; ++k) vals[k - 1] = fval(k);
             for (int k = 0; k < nmax; ++k) {
                 bsum[nbk] = vals[k];
                 bcnt[nbk] = 1;
@@ -268,9 +287,12 @@ __global__ void __launch_bounds__(128) k_fit(ws_batch B, FitOut out, int m_begin
                 q.bc = 0.0;
                 fp[k - 1] = q;
             }
+            if (cache_fv)  // the rebuilt curve's anchor values
+                for (int k = 1; k <= nmax; ++k)
+                    fv[k - 1] = piece_value(fp[locate_piece(fp, np, k)], c, w, static_cast<double>(k));
         }
         for (int k = 1; k <= nmax; ++k) {  // positivity (scaling.hpp:317-320)
-            if (piece_value(fp[locate_piece(fp, np, k)], c, w, static_cast<double>(k)) <= 0.0) {
+            if (fval(k) <= 0.0) {
                 err = WS_E_FIT_NONPOSITIVE;
                 ea = k;
                 break;
@@ -308,7 +330,8 @@ __global__ void __launch_bounds__(128) k_fit(ws_batch B, FitOut out, int m_begin
     }
     const int lim = N < nmax ? N : nmax;
     double* tt = out.ttab + static_cast<int64_t>(m) * out.tstride;
-    for (int n = 1; n <= lim; ++n) tt[n - 1] = piece_value(fp[locate_piece(fp, np, n)], c, w, static_cast<double>(n));
+    for (int n = 1; n <= lim; ++n)
+        tt[n - 1] = cache_fv ? fv[n - 1] : piece_value(fp[locate_piece(fp, np, n)], c, w, static_cast<double>(n));
 }
 
 }  // namespace wsdev
