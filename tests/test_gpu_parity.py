@@ -155,3 +155,23 @@ def test_gpu_pipelined_host_call_matches(sweep_hashes, monkeypatch):
     pl.simulate_staged()
     sims = pl.fetch_sim(ps)
     assert all(sims.results[i].valid for i in range(n) if res.results[i].status == 0)
+
+
+def test_gpu_weak_scaling_mixtures_match_oracle(planner):
+    """bench.py's weak scaling plans sweep mixtures beyond the 100k reference
+    hashes (rank r: [r*100k, (r+1)*100k)); a sample of each 100k block up to 8
+    GPUs equals the oracle record for record."""
+    import random
+
+    import paper_2409_03365_b200 as ws
+    import pyoracle as po
+    rng = random.Random(8)
+    idx = sorted(rng.sample(range(100000, 800000), 2100))
+    ps = ws.ProblemSet()
+    for i in idx:
+        ps.add_sweep(i, 1)
+    ps.encode(pinned=True)
+    res = planner.plan(ps)
+    ores = po.plan_batch(ps)
+    bad = [idx[i] for i in range(len(idx)) if records(res, i) != records(ores, i)]
+    assert not bad, bad[:10]
