@@ -618,7 +618,8 @@ int ws_plan_staged(ws_ctx* ctx, void* stream) {
                                                          ctx->retry_ids.as<int32_t>(), rcount);
         k_clamp_count<<<1, 1, 0, st>>>(rcount);
         ctx->launches += 2;
-        if (launch_pair(ctx, st, lh, fo, ctx->retry_ids.as<int32_t>(), rcount, kRetryMax, true,
+        // retry grid sized for at most min(P, kRetryMax) plans (small batches: one block)
+        if (launch_pair(ctx, st, lh, fo, ctx->retry_ids.as<int32_t>(), rcount, std::min(P, kRetryMax), true,
                         ctx->recs_r.as<char>(), ctx->flows_r.as<uint64_t>()))
             return 1;
     }
@@ -823,7 +824,7 @@ int ws_plan_batch_host(ws_ctx* ctx, const ws_batch* in, ws_plan_result* results,
                                                                   rcount);
             k_clamp_count<<<1, 1, 0, s>>>(rcount);
             ctx->launches += 2;
-            rc = launch_pair(ctx, s, ctx->caps_hard, fo, rids.as<int32_t>(), rcount, kRetryMax, true,
+            rc = launch_pair(ctx, s, ctx->caps_hard, fo, rids.as<int32_t>(), rcount, std::min(p1 - p0, kRetryMax), true,
                              rrecs.as<char>(), rflows.as<uint64_t>());
         }
         ctx->top_ptr = nullptr;
