@@ -106,12 +106,22 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def cpu_baseline(n_sample: int, threads: int) -> dict:
     """Reference planner (compiled from the reference sources) on host cores."""
     import pyoracle as po
     if po.ref_available():
         rate, bad = po.ref_sweep_bench(0, n_sample, threads)
-        return {"value": rate, "unit": "plans/s", "cores": threads, "kind": "reference",
+        return {"value": rate, "unit": "plans/s", "cores": threads, "kind": "reference", "cpu_model": cpu_model(),
                 "sample": f"sweep mixtures 0..{n_sample - 1}, reference plan_workload, inputs pre-parsed, "
                           f"{threads} std::threads ({bad} infeasible)"}
     import paper_2409_03365_b200 as ws
@@ -121,7 +131,7 @@ def cpu_baseline(n_sample: int, threads: int) -> dict:
     t0 = time.perf_counter()
     po.plan_batch(ps)
     dt = time.perf_counter() - t0
-    return {"value": n_sample / dt, "unit": "plans/s", "cores": 1, "kind": "port",
+    return {"value": n_sample / dt, "unit": "plans/s", "cores": 1, "kind": "port", "cpu_model": cpu_model(),
             "sample": f"sweep mixtures 0..{n_sample - 1}, oracle restatement, 1 thread"}
 
 
@@ -152,7 +162,7 @@ def run_reference(args) -> None:
         "config": {"workload": f"sweep-{args.mixtures} (bounded sample of {n} mixtures per step)",
                    "parallelism": f"{threads} host threads"},
         "impl": "reference",
-        "cpu_baseline": {"value": value, "unit": "plans/s", "cores": threads, "kind": "reference",
+        "cpu_baseline": {"value": value, "unit": "plans/s", "cores": threads, "kind": "reference", "cpu_model": cpu_model(),
                          "sample": f"{n} sweep mixtures per step, reference plan_workload compiled from the "
                                    f"reference headers (-O2 -ffp-contract=off)"},
         "e2e": {"value": value, "unit": "plans/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
