@@ -557,6 +557,9 @@ def main() -> None:
                      "frac": achieved / peak, "traffic": traffic, "kernel": dom,
                      "algorithmic_bytes_per_launch": dom_bytes, "kernel_ms": dom_ms, "peak_source": peak_src,
                      "kernels_ms": {"k_fit": kfit_ms, "k_sched": ksched_ms, "k_place": kplace_ms},
+                     "kernels_note": ("k_sched is launched programmatic-dependent on k_fit (its graph stage "
+                                      "overlaps the fit), so the k_sched time includes k_fit's"
+                                      if kfit_ms < 0.01 else "kernels timed separately"),
                      "planner_alg_bytes": {"in": alg_in, "out": alg_out, "schedule": sched_bytes}},
         "cpu_baseline": cpu,
         "gpu_launches": launches_per_step * args.steps,

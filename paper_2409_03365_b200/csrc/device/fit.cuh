@@ -51,6 +51,9 @@ struct PieceLoCmp {  // from_pieces sort key (scaling.hpp:45-46)
 
 // modules [m_begin, m_end) of the batch (a pipelined chunk, or all of them)
 __global__ void __launch_bounds__(128) k_fit(ws_batch B, FitOut out, int m_begin, int m_end) {
+    // let a k_sched launched with programmatic stream serialization start its
+    // graph stage now; it waits (griddepcontrol.wait) before reading our output
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     const int m = m_begin + blockIdx.x * blockDim.x + threadIdx.x;
     if (m >= m_end) return;
     const ws_plan_rec& R = B.plans[B.mod_plan[m]];

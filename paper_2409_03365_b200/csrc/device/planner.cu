@@ -232,6 +232,10 @@ struct ws_ctx {
     int host_chunks = 4;                     // $WSGPU_HOST_CHUNKS
     int host_streams = 2;                    // $WSGPU_HOST_STREAMS (1 or 2)
     bool force_snap = false;                 // $WSGPU_FORCE_SNAP: k_place<true> for every batch (tuning)
+    // k_sched launched programmatic-dependent on k_fit: its graph stage overlaps
+    // k_fit (measured: single-plan latency -7..-10%, 100k throughput unchanged);
+    // k_fit's time is then reported inside k_sched's.  $WSGPU_PDL=0 disables.
+    bool pdl = true;
     std::vector<double> host_weights{1, 3, 3, 1};  // $WSGPU_HOST_WEIGHTS: relative chunk sizes (sets the chunk count)
     ws_plan_result* res_out() { return d_results ? d_results : results.as<ws_plan_result>(); }
     uint8_t* arena_out() { return d_arena ? d_arena : arena.as<uint8_t>(); }
@@ -302,7 +306,7 @@ ws_batch rebase(const ws_batch& h, const void* hbase, char* dbase) {
 // kernels share the SMs, so each SM has more resident warps to hide latency.
 int launch_pair(ws_ctx* ctx, cudaStream_t st, const LaunchCaps& lc, const FitOut& fo, const int32_t* ids,
                 const int32_t* n_ids, int n, bool by_slot, char* recs, uint64_t* flows,
-                cudaEvent_t mid = nullptr, int chunks = 1);
+                cudaEvent_t mid = nullptr, int chunks = 1, bool pdl = false);
 
 }  // namespace
 
@@ -310,7 +314,7 @@ namespace {
 
 int launch_pair(ws_ctx* ctx, cudaStream_t st, const LaunchCaps& lc, const FitOut& fo, const int32_t* ids,
                 const int32_t* n_ids, int n, bool by_slot, char* recs, uint64_t* flows, cudaEvent_t mid,
-                int chunks) {
+                int chunks, bool pdl) {
     if (n <= 0) return 0;
     const ws_batch& B = ctx->dview;
     SchedArgs S{};
@@ -370,7 +374,21 @@ int launch_pair(ws_ctx* ctx, cudaStream_t st, const LaunchCaps& lc, const FitOut
         if (cnt <= 0) break;
         S.plan_ids = ids + base;
         S.n_launch = cnt;
-        k_sched<<<(cnt + kSchedWarps - 1) / kSchedWarps, 32 * kSchedWarps, kSchedWarps * S.SL.bytes, st>>>(S);
+        if (pdl && c == 0) {  // right behind k_fit: programmatic dependent launch
+            cudaLaunchConfig_t cfg{};
+            cfg.gridDim = dim3((cnt + kSchedWarps - 1) / kSchedWarps);
+            cfg.blockDim = dim3(32 * kSchedWarps);
+            cfg.dynamicSmemBytes = kSchedWarps * S.SL.bytes;
+            cfg.stream = st;
+            cudaLaunchAttribute attr[1];
+            attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+            attr[0].val.programmaticStreamSerializationAllowed = 1;
+            cfg.attrs = attr;
+            cfg.numAttrs = 1;
+            CK(cudaLaunchKernelEx(&cfg, k_sched, S));
+        } else {
+            k_sched<<<(cnt + kSchedWarps - 1) / kSchedWarps, 32 * kSchedWarps, kSchedWarps * S.SL.bytes, st>>>(S);
+        }
         ctx->launches++;
         if (lc.scoped) {  // the batch's distmm-mt plans (each instance skips the other's plans)
             k_sched_scoped<<<(cnt + kSchedWarps - 1) / kSchedWarps, 32 * kSchedWarps, kSchedWarps * S.SL.bytes,
@@ -442,6 +460,7 @@ int ws_ctx_create(int device, ws_ctx** out) {
         if (!c->host_weights.empty()) c->host_chunks = static_cast<int>(c->host_weights.size());
     }
     if (const char* env = std::getenv("WSGPU_FORCE_SNAP")) c->force_snap = std::atoi(env) != 0;
+    if (const char* env = std::getenv("WSGPU_PDL")) c->pdl = std::atoi(env) != 0;
     if (const char* env = std::getenv("WSGPU_HOST_STREAMS")) c->host_streams = std::max(1, std::min(2, std::atoi(env)));
     *out = c;
     return 0;
@@ -603,13 +622,16 @@ int ws_plan_staged(ws_ctx* ctx, void* stream) {
     CK(cudaMemsetAsync(counters, 0, 64, st));
 
     CK(cudaEventRecord(ctx->ev[0], st));
+    // with programmatic dependent launch k_sched directly follows k_fit (no
+    // event in between), so k_fit's time is reported inside k_sched's
+    if (ctx->pdl) CK(cudaEventRecord(ctx->ev[1], st));
     if (B.n_modules > 0) {
         k_fit<<<(B.n_modules + 127) / 128, 128, 0, st>>>(B, fo, 0, B.n_modules);
         ctx->launches++;
     }
-    CK(cudaEventRecord(ctx->ev[1], st));
+    if (!ctx->pdl) CK(cudaEventRecord(ctx->ev[1], st));
     if (launch_pair(ctx, st, lc, fo, ctx->order.as<int32_t>(), nullptr, P, false, ctx->recs.as<char>(),
-                    ctx->flows.as<uint64_t>(), ctx->ev[3], ctx->chunks))
+                    ctx->flows.as<uint64_t>(), ctx->ev[3], ctx->chunks, ctx->pdl && B.n_modules > 0))
         return 1;
     // retry pass: soft-cap overflows with the hard caps, count read on device
     auto* rcount = reinterpret_cast<int32_t*>(counters + 2);
@@ -817,7 +839,8 @@ int ws_plan_batch_host(ws_ctx* ctx, const ws_batch* in, ws_plan_result* results,
         // region (slots of concurrent chunks would otherwise collide)
         int rc = launch_pair(ctx, s, ctx->caps, fo, ctx->order.as<int32_t>() + p0, nullptr, p1 - p0, false,
                              ctx->recs.as<char>(),
-                             ctx->flows.as<uint64_t>() + static_cast<int64_t>(p0) * ctx->caps.pl.F * 2);
+                             ctx->flows.as<uint64_t>() + static_cast<int64_t>(p0) * ctx->caps.pl.F * 2, nullptr, 1,
+                             ctx->pdl && m1 > m0);
         if (!rc) {
             CK(cudaMemsetAsync(rcount, 0, 4, s));
             k_soft_collect<<<(p1 - p0 + 255) / 256, 256, 0, s>>>(ctx->res_out(), p0, p1, rids.as<int32_t>(),

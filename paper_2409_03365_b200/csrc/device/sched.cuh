@@ -383,7 +383,6 @@ __device__ bool s_graph(SCtx& C) {
     int* idrank = C.at<int>(C.L->idrank);
     int* by_rank = C.at<int>(C.L->by_rank);
     int* gm_of = C.at<int>(C.L->gm_of);
-    int* nmax_of = C.at<int>(C.L->nmax_of);
     int* Lk = C.at<int>(C.L->Lk);
     for (int k = lane; k < K; k += 32) {  // MetaOp ids "m<k>" in std::map order
         int r = 0;
@@ -392,8 +391,7 @@ __device__ bool s_graph(SCtx& C) {
         by_rank[r] = k;
         const int gm = C.mbase + mod_of[k];
         gm_of[k] = gm;
-        nmax_of[k] = C.F->nmax[gm];
-        Lk[k] = B.mod_layers[gm];
+        Lk[k] = B.mod_layers[gm];  // nmax_of (a k_fit output) is read after griddepcontrol.wait
     }
     __syncwarp();
     uint64_t* predk = C.at<uint64_t>(C.L->predk);
@@ -1933,6 +1931,16 @@ __device__ __forceinline__ void sched_body(const SchedArgs& A, char* smem_dyn, C
     WS_PH_START(tg);
     if (ok) ok = s_graph(C);
     WS_PH_STOP(tg, 10);
+    // programmatic dependent launch: the graph stage above reads only the batch,
+    // so it overlaps k_fit; wait for k_fit's grid (and its memory) before the
+    // first fit output is read.  A no-op when launched without the attribute.
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (ok) {  // the first k_fit outputs read by k_sched
+        int* nmax_of = C.at<int>(C.L->nmax_of);
+        const int* gm_of = C.at<int>(C.L->gm_of);
+        for (int k = lane; k < C.K; k += 32) nmax_of[k] = C.F->nmax[gm_of[k]];
+        __syncwarp();
+    }
     if (ok) ok = s_fit_status(C);
     const bool decoupled = R.strategy == WS_STRATEGY_DECOUPLED_SEQUENTIAL;
     constexpr bool scoped = SCOPED;  // task-scoped baselines: distmm-mt, task-level-optimus
