@@ -49,20 +49,36 @@ struct PieceLoCmp {  // from_pieces sort key (scaling.hpp:45-46)
     __device__ bool operator()(int a, int b) const { return p[a].lo < p[b].lo; }
 };
 
+// Lanes per module: 1 for large batches (one thread per module), kFitWarp for
+// small ones (single-plan latency), where the 32 lanes of a warp run the
+// serial fit redundantly (identical values, uniform branches) and split the
+// per-n evaluations (truth points, integer anchors, T-table) between them
+// through shared memory.  Every value is computed by the same expression in
+// both modes, so the results are bit-identical.
+constexpr int kFitWarp = 32;
+constexpr int kFitWarpMaxModules = 4096;  // batches up to this use kFitWarp
+
 // modules [m_begin, m_end) of the batch (a pipelined chunk, or all of them)
+template <int kLanes>
 __global__ void __launch_bounds__(128) k_fit(ws_batch B, FitOut out, int m_begin, int m_end) {
     // let a k_sched launched with programmatic stream serialization start its
     // graph stage now; it waits (griddepcontrol.wait) before reading our output
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-    const int m = m_begin + blockIdx.x * blockDim.x + threadIdx.x;
-    if (m >= m_end) return;
+    constexpr int kWarps = kLanes > 1 ? 128 / kLanes : 1;
+    __shared__ double s_tv[kWarps][kLanes > 1 ? WS_MAX_DEVICES : 1];
+    __shared__ double s_fv[kWarps][kLanes > 1 ? 128 : 1];
+    const int gt = blockIdx.x * blockDim.x + threadIdx.x;
+    const int m = m_begin + gt / kLanes;
+    const int lane = kLanes > 1 ? gt % kLanes : 0;
+    if (m >= m_end) return;  // uniform over a module's lanes
     const ws_plan_rec& R = B.plans[B.mod_plan[m]];
     const int N = R.n_dev;
     const double c = B.mod_c[m], w = B.mod_w[m];
     int err = 0, ea = 0, eb = 0;
     int np = 0, nmax = 1;
     DPiece fp[WS_MAX_PIECES];
-    double fv[128];         // T(k) of the fitted curve at k = 1..nmax (when cache_fv)
+    double fv_local[kLanes > 1 ? 1 : 128];  // T(k) of the fitted curve at k = 1..nmax (when cache_fv)
+    double* fv = kLanes > 1 ? s_fv[threadIdx.x / kLanes] : fv_local;
     bool cache_fv = false;
 
     do {
@@ -124,10 +140,12 @@ __global__ void __launch_bounds__(128) k_fit(ws_batch B, FitOut out, int m_begin
         // truth value evaluated once (a pure function of n) and reused
         const int npts = has_prof ? B.mod_prof_n[m] : N;
         const int poff = has_prof ? B.mod_prof_off[m] : 0;
-        double tv[WS_MAX_DEVICES];
+        double tv_local[kLanes > 1 ? 1 : WS_MAX_DEVICES];
+        double* tv = kLanes > 1 ? s_tv[threadIdx.x / kLanes] : tv_local;
         if (!has_prof)
-            for (int i = 0; i < N && i < WS_MAX_DEVICES; ++i)
+            for (int i = lane; i < N && i < WS_MAX_DEVICES; i += kLanes)
                 tv[i] = piece_value(tp[locate_piece(tp, ntp, i + 1)], c, w, static_cast<double>(i + 1));
+        if (kLanes > 1) __syncwarp();
         auto point = [&](int i, int& n, double& t) {
             if (has_prof) {
                 n = B.prof_n[poff + i];
@@ -240,8 +258,9 @@ __global__ void __launch_bounds__(128) k_fit(ws_batch B, FitOut out, int m_begin
             return cache_fv ? fv[k - 1] : piece_value(fp[locate_piece(fp, np, k)], c, w, static_cast<double>(k));
         };
         if (cache_fv)
-            for (int k = 1; k <= nmax; ++k)
+            for (int k = 1 + lane; k <= nmax; k += kLanes)
                 fv[k - 1] = piece_value(fp[locate_piece(fp, np, k)], c, w, static_cast<double>(k));
+        if (kLanes > 1) __syncwarp();
         bool changed = false;
         double prev = 0.0;
         for (int k = 1; k <= nmax; ++k) {
@@ -290,9 +309,11 @@ __global__ void __launch_bounds__(128) k_fit(ws_batch B, FitOut out, int m_begin
                 q.bc = 0.0;
                 fp[k - 1] = q;
             }
+            if (kLanes > 1) __syncwarp();  // every lane has read the old anchors
             if (cache_fv)  // the rebuilt curve's anchor values
-                for (int k = 1; k <= nmax; ++k)
+                for (int k = 1 + lane; k <= nmax; k += kLanes)
                     fv[k - 1] = piece_value(fp[locate_piece(fp, np, k)], c, w, static_cast<double>(k));
+            if (kLanes > 1) __syncwarp();
         }
         for (int k = 1; k <= nmax; ++k) {  // positivity (scaling.hpp:317-320)
             if (fval(k) <= 0.0) {
@@ -303,28 +324,36 @@ __global__ void __launch_bounds__(128) k_fit(ws_batch B, FitOut out, int m_begin
         }
     } while (false);
 
-    out.err[m] = err;
-    out.err_a[m] = ea;
-    out.err_b[m] = eb;
+    if (lane == 0) {
+        out.err[m] = err;
+        out.err_a[m] = ea;
+        out.err_b[m] = eb;
+    }
     if (err) {
-        out.npieces[m] = 0;
-        out.nmax[m] = 0;
+        if (lane == 0) {
+            out.npieces[m] = 0;
+            out.nmax[m] = 0;
+        }
         return;
     }
     int64_t off = static_cast<int64_t>(m) * kInlinePieces;
     if (np > kInlinePieces) {
-        const unsigned long long o = atomicAdd(out.overflow_top, static_cast<unsigned long long>(np));
+        unsigned long long o = 0;
+        if (lane == 0) o = atomicAdd(out.overflow_top, static_cast<unsigned long long>(np));
+        if (kLanes > 1) o = __shfl_sync(0xffffffffu, o, 0);
         if (static_cast<int64_t>(o) + np > out.overflow_cap) {
-            out.err[m] = WS_E_LIMIT_PIECES;
+            if (lane == 0) out.err[m] = WS_E_LIMIT_PIECES;
             return;
         }
         off = out.overflow_base + static_cast<int64_t>(o);
     }
-    out.piece_off[m] = off;
-    out.npieces[m] = np;
-    out.nmax[m] = nmax;
+    if (lane == 0) {
+        out.piece_off[m] = off;
+        out.npieces[m] = np;
+        out.nmax[m] = nmax;
+    }
     double* dst = out.pieces + 5 * off;
-    for (int i = 0; i < np; ++i) {
+    for (int i = lane; i < np; i += kLanes) {
         dst[5 * i + 0] = fp[i].lo;
         dst[5 * i + 1] = fp[i].hi;
         dst[5 * i + 2] = fp[i].alpha;
@@ -333,7 +362,7 @@ __global__ void __launch_bounds__(128) k_fit(ws_batch B, FitOut out, int m_begin
     }
     const int lim = N < nmax ? N : nmax;
     double* tt = out.ttab + static_cast<int64_t>(m) * out.tstride;
-    for (int n = 1; n <= lim; ++n)
+    for (int n = 1 + lane; n <= lim; n += kLanes)
         tt[n - 1] = cache_fv ? fv[n - 1] : piece_value(fp[locate_piece(fp, np, n)], c, w, static_cast<double>(n));
 }
 

@@ -1,7 +1,7 @@
 // planner.cu — C-ABI implementation: planning context, device buffers and the
 // launch sequence of the sm_100a planner kernels.
 //
-//   k_fit    (subsystem 2)        one thread per declared module
+//   k_fit    (subsystem 2)        one thread (large batches) or warp (small) per declared module
 //   k_sched  (subsystems 1, 3, 4a) one warp per plan, working set in shared memory
 //   k_place  (subsystem 4b + out)  one warp per plan, working set in shared memory
 //   retry    plans that overflow the soft record caps re-run with the hard
@@ -608,6 +608,21 @@ int ws_stage_batch(ws_ctx* ctx, const ws_batch* in, void* stream) {
     return 0;
 }
 
+// k_fit over modules [m0, m1): a warp per module for small batches (latency),
+// a thread per module for large ones (throughput); identical results
+// ($WSGPU_FIT_WARP_MAX overrides the 4096-module threshold; 0 = always a thread)
+static void launch_fit(const ws_batch& B, const FitOut& fo, int m0, int m1, cudaStream_t s) {
+    static const int64_t warp_max = [] {
+        const char* env = std::getenv("WSGPU_FIT_WARP_MAX");
+        return env ? static_cast<int64_t>(std::atoll(env)) : static_cast<int64_t>(kFitWarpMaxModules);
+    }();
+    const int64_t nm = m1 - m0;
+    if (nm <= warp_max)
+        k_fit<kFitWarp><<<static_cast<int>((nm * kFitWarp + 127) / 128), 128, 0, s>>>(B, fo, m0, m1);
+    else
+        k_fit<1><<<static_cast<int>((nm + 127) / 128), 128, 0, s>>>(B, fo, m0, m1);
+}
+
 int ws_plan_staged(ws_ctx* ctx, void* stream) {
     cudaSetDevice(ctx->device);
     cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
@@ -626,7 +641,7 @@ int ws_plan_staged(ws_ctx* ctx, void* stream) {
     // event in between), so k_fit's time is reported inside k_sched's
     if (ctx->pdl) CK(cudaEventRecord(ctx->ev[1], st));
     if (B.n_modules > 0) {
-        k_fit<<<(B.n_modules + 127) / 128, 128, 0, st>>>(B, fo, 0, B.n_modules);
+        launch_fit(B, fo, 0, B.n_modules, st);
         ctx->launches++;
     }
     if (!ctx->pdl) CK(cudaEventRecord(ctx->ev[1], st));
@@ -832,7 +847,7 @@ int ws_plan_batch_host(ws_ctx* ctx, const ws_batch* in, ws_plan_result* results,
         ctx->top_ptr = tops + c;
         ctx->top_cap = abase[c + 1];
         if (m1 > m0) {
-            k_fit<<<(m1 - m0 + 127) / 128, 128, 0, s>>>(B, fo, m0, m1);
+            launch_fit(B, fo, m0, m1, s);
             ctx->launches++;
         }
         // k_place's flow scratch is indexed by launch slot: each chunk gets its own

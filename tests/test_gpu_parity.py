@@ -175,3 +175,26 @@ def test_gpu_weak_scaling_mixtures_match_oracle(planner):
     ores = po.plan_batch(ps)
     bad = [idx[i] for i in range(len(idx)) if records(res, i) != records(ores, i)]
     assert not bad, bad[:10]
+
+
+def test_gpu_small_batches_warp_fit_match_oracle(planner, golden_cases):
+    """Batches of at most kFitWarpMaxModules (4096) modules fit each curve with
+    a warp per module, larger ones with a thread per module: small batches
+    (golden cases one at a time, sweep mixtures in groups of 50) give records
+    bit-identical to the oracle's."""
+    import paper_2409_03365_b200 as ws
+    import pyoracle
+    bad = []
+    for c in golden_cases[:40]:
+        ps, kept, _ = build_set([c])
+        ps.encode(pinned=True)
+        g, o = planner.plan(ps), pyoracle.plan_batch(ps)
+        if any(records(g, i) != records(o, i) for i in range(len(ps))):
+            bad.append(c["name"])
+    for start in range(0, 2000, 50):
+        ps = ws.ProblemSet()
+        ps.add_sweep(start, 50)
+        ps.encode(pinned=True)
+        g, o = planner.plan(ps), pyoracle.plan_batch(ps)
+        bad += [start + i for i in range(len(ps)) if records(g, i) != records(o, i)]
+    assert not bad, bad[:10]
