@@ -10,9 +10,17 @@ import paper_2409_03365_b200 as ws
 NAMES = {0: "place:prologue", 1: "place:wave order", 2: "place:flows_in+disp", 3: "place:candidates",
          4: "place:score", 8: "place:minloc", 5: "place:commit+flows", 6: "place:restore", 7: "place:emit",
          10: "sched:graph", 11: "sched:fit+valid", 12: "sched:alloc", 13: "sched:schedule", 14: "sched:writeback"}
-n = int(sys.argv[1]) if len(sys.argv) > 1 else 100000
+# argument: a mixture count (sweep prefix), or family:tasks:devices for one
+# BASELINE scenario plan (single-plan latency)
+arg = sys.argv[1] if len(sys.argv) > 1 else "100000"
 ps = ws.ProblemSet()
-ps.add_sweep(0, n)
+if ":" in arg:
+    fam, t, d = arg.split(":")
+    ps.add_scenario(fam, int(t), int(d), 0)
+    n = 1
+else:
+    n = int(arg)
+    ps.add_sweep(0, n)
 ps.encode(pinned=True)
 pl = ws.Planner(0)
 f = ws.lib.ws_debug_phase_cycles
