@@ -66,44 +66,68 @@ def measured_peak():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons during the timed region."""
+    """SM clocks + throttle reasons sampled DURING the timed regions: an NVML
+    thread polls every 5 ms while a `with sampler.sampling():` block is open
+    (the timed regions are a few hundred ms, so nvidia-smi's 100 ms loop would
+    see only 1-3 samples); nvidia-smi is the fallback when NVML is missing."""
+
+    REASONS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20, "sw_power_cap": 0x4}
 
     def __init__(self, index: int):
-        self.proc = None
-        self.path = ROOT / "gpurun_out" / f"clocks_rank{index}.csv"
+        import threading
+        self.sm, self.mx, self.reasons = [], [], set()
+        self.active = threading.Event()
+        self.stop_ev = threading.Event()
+        self.thread = None
         try:
-            self.path.parent.mkdir(exist_ok=True)
-            self.f = open(self.path, "w")
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", f"--id={index}", "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
-                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
-                 "--format=csv,noheader,nounits", "-lms", "100"], stdout=self.f, stderr=subprocess.DEVNULL)
+            import pynvml
+            pynvml.nvmlInit()
+            self.nvml = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = float(pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM))
+            self.thread = threading.Thread(target=self._loop, daemon=True)
+            self.thread.start()
         except Exception:
-            self.proc = None
+            self.nvml = None
 
-    def stop(self) -> dict:
-        if not self.proc:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        self.proc.terminate()
-        self.proc.wait()
-        self.f.close()
-        sm, mx, reasons = [], [], set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for line in self.path.read_text().splitlines():
-            parts = [x.strip() for x in line.split(",")]
-            if len(parts) < 7:
+    def _loop(self):
+        nv = self.nvml
+        while not self.stop_ev.is_set():
+            if not self.active.wait(0.05):
                 continue
             try:
-                sm.append(float(parts[0]))
-                mx.append(float(parts[1]))
-            except ValueError:
-                continue
-            for n, v in zip(names, parts[3:7]):
-                if v.lower().startswith("active"):
-                    reasons.add(n)
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                self.sm.append(float(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)))
+                self.mx.append(self.max_mhz)
+                bits = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for name, b in self.REASONS.items():
+                    if bits & b:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.005)
+
+    def sampling(self):
+        sampler = self
+
+        class _Scope:
+            def __enter__(self):
+                sampler.active.set()
+
+            def __exit__(self, *exc):
+                sampler.active.clear()
+
+        return _Scope()
+
+    def stop(self) -> dict:
+        if self.thread is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml unavailable"], "samples": 0}
+        self.stop_ev.set()
+        self.active.set()
+        self.thread.join()
+        return {"sm_mhz": statistics.median(self.sm) if self.sm else None,
+                "sm_max_mhz": max(self.mx) if self.mx else None,
+                "reasons": sorted(self.reasons), "samples": len(self.sm),
+                "how": "NVML every 5 ms inside the timed loops (device-resident, evaluation, e2e, baselines, compare)"}
 
 
 def cpu_model() -> str:
@@ -135,36 +159,59 @@ def cpu_baseline(n_sample: int, threads: int) -> dict:
             "sample": f"sweep mixtures 0..{n_sample - 1}, oracle restatement, 1 thread"}
 
 
+def workload_config(args, world: int) -> dict:
+    """`config` of both arms (identical dicts: the reference arm plans the same
+    workload; its threads and sample are described in its cpu_baseline)."""
+    weak = args.scaling == "weak"
+    return {"workload": (f"sweep (BASELINE config 5 generator: 2-16 tasks, clip/ofasys/qwen, 8-64 devices), "
+                         f"{args.mixtures} mixtures " + ("per GPU" if weak else "in total")),
+            "plans_per_rank": args.mixtures if weak else (args.mixtures + world - 1) // world,
+            "sharding": (f"rank r plans mixtures [r*{args.mixtures}, (r+1)*{args.mixtures})" if weak
+                         else "strided i % world == rank"),
+            "l2": "256 MiB buffer written between timed steps (outside the timed events)",
+            "parallelism": f"dp{world} (independent plans, one NCCL min-loc all_gather at the end)"}
+
+
 def run_reference(args) -> None:
+    """The reference planner (plan_workload compiled from the reference headers,
+    -O3 -ffp-contract=off) on all host cores.  At N=1 every timed step plans
+    exactly the mixtures our arm plans (sweep [0, --mixtures)); at N>1 the whole
+    job (N x --mixtures per step) does not fit a few minutes of CPU, so each
+    step plans rank 0's block (the N=1 set) and the rate is per plan."""
     rank, world, _ = dist_env()
     if rank != 0:
         return
     import pyoracle as po
     threads = os.cpu_count() or 1
-    n = args.ref_sample
     if not po.ref_available():
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libwsref.so not built (needs /root/reference)"}))
         return
-    for _ in range(args.warmup):
-        po.ref_sweep_bench(0, min(n, 200), threads)
-    rates = []
-    t_total = 0.0
-    for s in range(args.steps):
-        t0 = time.perf_counter()
-        rate, _ = po.ref_sweep_bench(s * n, n, threads)
-        t_total += time.perf_counter() - t0
+    n = args.ref_sample or args.mixtures
+    job = args.mixtures * world if args.scaling == "weak" else args.mixtures
+    n = min(n, job)
+    sweep = po.RefSweepSet(0, n, threads)  # generation + parse, untimed
+    for _ in range(args.warmup):  # warm-up steps: a bounded 2000-plan prefix
+        sweep.run(threads, 0, min(n, 2000))
+    rates, bad = [], 0
+    for _ in range(args.steps):
+        rate, bad = sweep.run(threads)
         rates.append(rate)
-    value = statistics.median(rates)
+    t_total = sum(n / r for r in rates)
+    value = args.steps * n / t_total
+    same = n == job
+    scope = "the whole job" if same else f"{n} of the job's {job} plans per step"
     line = {
         "metric": METRIC, "value": value, "unit": "plans/s", "n_gpus": args.gpus, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": 1000.0 * n / value, "higher_is_better": True, "scaling": args.scaling,
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"sweep-{args.mixtures} (bounded sample of {n} mixtures per step)",
-                   "parallelism": f"{threads} host threads"},
+        "warmup": args.warmup, "ms_per_step": 1000.0 * t_total / args.steps * (job / n), "higher_is_better": True,
+        "scaling": args.scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": workload_config(args, world),
         "impl": "reference",
         "cpu_baseline": {"value": value, "unit": "plans/s", "cores": threads, "kind": "reference", "cpu_model": cpu_model(),
-                         "sample": f"{n} sweep mixtures per step, reference plan_workload compiled from the "
-                                   f"reference headers (-O2 -ffp-contract=off)"},
+                         "sample": (f"sweep mixtures 0..{n - 1} every step ({scope}), "
+                                    f"reference plan_workload compiled from the reference headers "
+                                    f"(-O3 -ffp-contract=off), inputs pre-parsed, {threads} std::threads, "
+                                    f"{bad} PlacementInfeasible/other errors per step"),
+                         "same_plans_as_ours": same},
         "e2e": {"value": value, "unit": "plans/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -179,7 +226,8 @@ def main() -> None:
     ap.add_argument("--mixtures", type=int, default=100000,
                     help="sweep mixtures per rank (weak scaling) or in total (strong)")
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
-    ap.add_argument("--ref-sample", type=int, default=4000)
+    ap.add_argument("--ref-sample", type=int, default=0,
+                    help="reference-arm mixtures per step (default: --mixtures, i.e. our arm's set at N=1)")
     ap.add_argument("--cpu-sample", type=int, default=6000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--latency-reps", type=int, default=300, help="single-plan latency samples (SURVEY 8(d): >= 300)")
@@ -239,18 +287,18 @@ def main() -> None:
     clocks = ClockSampler(local)
     barrier()
     step_ms, plan_kernel_ms = [], []
-    for _ in range(args.steps):
-        flush.zero_()  # L2 flush between timed steps (outside the events)
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        planner.plan_staged(sptr)
-        e1.record(stream)
-        e1.synchronize()
-        step_ms.append(e0.elapsed_time(e1))
-        plan_kernel_ms.append(planner.kernel_ms())
+    with clocks.sampling():
+        for _ in range(args.steps):
+            flush.zero_()  # L2 flush between timed steps (outside the events)
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            planner.plan_staged(sptr)
+            e1.record(stream)
+            e1.synchronize()
+            step_ms.append(e0.elapsed_time(e1))
+            plan_kernel_ms.append(planner.kernel_ms())
     barrier()
-    clk = clocks.stop()
     t_local = sum(step_ms) / 1000.0
     t = torch.tensor([t_local], dtype=torch.float64, device=dev)
     if world > 1:
@@ -286,15 +334,16 @@ def main() -> None:
         planner.simulate_staged(sptr)
     barrier()
     sim_ms = []
-    for _ in range(args.steps):
-        flush.zero_()
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        planner.simulate_staged(sptr)
-        e1.record(stream)
-        e1.synchronize()
-        sim_ms.append(e0.elapsed_time(e1))
+    with clocks.sampling():
+        for _ in range(args.steps):
+            flush.zero_()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            planner.simulate_staged(sptr)
+            e1.record(stream)
+            e1.synchronize()
+            sim_ms.append(e0.elapsed_time(e1))
     barrier()
     sims = planner.fetch_sim(ps, sptr)
     n_invalid = sum(1 for i in range(len(ps)) if sims.results[i].status == 0 and not sims.results[i].valid)
@@ -314,16 +363,17 @@ def main() -> None:
         r2 = planner.plan(ps, sptr, out=r2)
     barrier()
     e2e_ms = []
-    for _ in range(args.steps):
-        flush.zero_()
-        torch.cuda.synchronize(dev)
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        r2 = planner.plan(ps, sptr, out=r2)
-        e1.record(stream)
-        e1.synchronize()
-        e2e_ms.append(e0.elapsed_time(e1))
+    with clocks.sampling():
+        for _ in range(args.steps):
+            flush.zero_()
+            torch.cuda.synchronize(dev)
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            r2 = planner.plan(ps, sptr, out=r2)
+            e1.record(stream)
+            e1.synchronize()
+            e2e_ms.append(e0.elapsed_time(e1))
     barrier()
     te = torch.tensor([sum(e2e_ms) / 1000.0], dtype=torch.float64, device=dev)
     if world > 1:
@@ -345,15 +395,16 @@ def main() -> None:
             planner.plan_staged(sptr)
         barrier()
         bms = []
-        for _ in range(args.steps):
-            flush.zero_()
-            e0 = torch.cuda.Event(enable_timing=True)
-            e1 = torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-            planner.plan_staged(sptr)
-            e1.record(stream)
-            e1.synchronize()
-            bms.append(e0.elapsed_time(e1))
+        with clocks.sampling():
+            for _ in range(args.steps):
+                flush.zero_()
+                e0 = torch.cuda.Event(enable_timing=True)
+                e1 = torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                planner.plan_staged(sptr)
+                e1.record(stream)
+                e1.synchronize()
+                bms.append(e0.elapsed_time(e1))
         barrier()
         tb = torch.tensor([sum(bms) / 1000.0], dtype=torch.float64, device=dev)
         if world > 1:
@@ -384,16 +435,17 @@ def main() -> None:
             planner.simulate_staged(sptr)
         barrier()
         cms = []
-        for _ in range(args.steps):
-            flush.zero_()
-            e0 = torch.cuda.Event(enable_timing=True)
-            e1 = torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-            planner.plan_staged(sptr)
-            planner.simulate_staged(sptr)
-            e1.record(stream)
-            e1.synchronize()
-            cms.append(e0.elapsed_time(e1))
+        with clocks.sampling():
+            for _ in range(args.steps):
+                flush.zero_()
+                e0 = torch.cuda.Event(enable_timing=True)
+                e1 = torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                planner.plan_staged(sptr)
+                planner.simulate_staged(sptr)
+                e1.record(stream)
+                e1.synchronize()
+                cms.append(e0.elapsed_time(e1))
         barrier()
         tc = torch.tensor([sum(cms) / 1000.0, float(len(cidx))], dtype=torch.float64, device=dev)
         if world > 1:
@@ -405,6 +457,7 @@ def main() -> None:
                    "mixtures": n_cmp, "value": n_cmp * args.steps / float(tc[0].item()), "unit": "workloads/s",
                    "ms_per_step": 1000.0 * float(tc[0].item()) / args.steps}
 
+    clk = clocks.stop()
     if rank != 0:
         if world > 1:
             torch.distributed.destroy_process_group()
@@ -544,13 +597,7 @@ def main() -> None:
         "vs_baseline": None,
         "dtype": "f64",
         "data": "synthetic",
-        "config": {"workload": (f"sweep (BASELINE config 5 generator: 2-16 tasks, clip/ofasys/qwen, 8-64 devices), "
-                                f"{args.mixtures} mixtures " + ("per GPU" if weak else "in total")),
-                   "plans_per_rank": len(ps),
-                   "sharding": (f"rank r plans mixtures [r*{args.mixtures}, (r+1)*{args.mixtures})" if weak
-                                else "strided i % world == rank"),
-                   "l2": "256 MiB buffer written between timed steps (outside the timed events)",
-                   "parallelism": f"dp{world} (independent plans, one NCCL min-loc all_gather at the end)"},
+        "config": workload_config(args, world),
         "e2e": {"value": e2e_value, "unit": "plans/s", "h2d_bytes_per_step": in_bytes_blob,
                 "d2h_bytes_per_step": d2h_step, "path": "ws_plan_batch_host (pinned host in/out)"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",

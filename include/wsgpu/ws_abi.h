@@ -314,6 +314,10 @@ int ws_fetch_results(ws_ctx* ctx, ws_plan_result* results, uint8_t* arena, uint6
                      uint64_t* arena_used, void* stream);
 /* Number of kernel launches issued by the last ws_plan_staged / ws_plan_batch_host. */
 int ws_last_launch_count(const ws_ctx* ctx);
+/* Plans of the last planning call that overflowed the launch's soft record caps
+ * and were re-planned with the hard caps (all of them, any number; valid once
+ * the results were fetched).  Diagnostic only: results never depend on it. */
+long long ws_last_retry_count(const ws_ctx* ctx);
 /* Device time (ms) of each planner kernel in the last planning call, measured
  * with CUDA events on the launching stream: out[0]=k_fit, out[1]=k_sched,
  * out[2]=k_place (including the soft-cap retry pass). */

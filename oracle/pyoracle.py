@@ -117,6 +117,11 @@ def ref():
         lib.wsref_free_list.argtypes = [C.POINTER(vp), C.c_int]
         lib.wsref_sweep_plan.restype = vp
         lib.wsref_sweep_plan.argtypes = [C.c_long]
+        lib.wsref_sweep_prepare.restype = vp
+        lib.wsref_sweep_prepare.argtypes = [C.c_long, C.c_long, C.c_int]
+        lib.wsref_sweep_free.argtypes = [vp]
+        lib.wsref_sweep_run.restype = C.c_double
+        lib.wsref_sweep_run.argtypes = [vp, C.c_long, C.c_long, C.c_int, C.POINTER(C.c_long)]
         lib.wsref_sweep_bench.restype = C.c_double
         lib.wsref_sweep_bench.argtypes = [C.c_long, C.c_long, C.c_int, C.POINTER(C.c_long)]
         lib.wsref_sim_text.restype = vp
@@ -204,6 +209,27 @@ def ref_sweep_bench(start: int, count: int, threads: int) -> tuple[float, int]:
     bad = C.c_long(0)
     rate = ref().wsref_sweep_bench(start, count, threads, C.byref(bad))
     return rate, bad.value
+
+
+class RefSweepSet:
+    """Sweep mixtures [start, start+count) generated and parsed once by the
+    reference (outside any timed region); run() plans them with the reference
+    plan_workload on `threads` std::threads and returns (plans/s, infeasible)."""
+
+    def __init__(self, start: int, count: int, threads: int):
+        self.count = count
+        self._h = ref().wsref_sweep_prepare(start, count, threads)
+
+    def run(self, threads: int, first: int = 0, count: int | None = None) -> tuple[float, int]:
+        bad = C.c_long(0)
+        n = self.count if count is None else count
+        rate = ref().wsref_sweep_run(self._h, first, n, threads, C.byref(bad))
+        return rate, int(bad.value)
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            ref().wsref_sweep_free(self._h)
+            self._h = None
 
 
 def ref_sweep_bench_strategy(start: int, count: int, threads: int, strategy: str) -> float:

@@ -246,6 +246,58 @@ double wsref_sweep_bench(long start, long count, int threads, long* infeasible) 
     return static_cast<double>(count) / sec;
 }
 
+// Pre-parsed sweep mixtures [start, start + count) (generation + parse spread
+// over `threads`), so the reference arm can plan the identical 100k set every
+// step with only plan_workload inside the timed region.
+struct wsref_sweep_set {
+    std::vector<WorkloadSpec> specs;
+    std::vector<ClusterTopology> topos;
+};
+
+wsref_sweep_set* wsref_sweep_prepare(long start, long count, int threads) {
+    auto* s = new wsref_sweep_set();
+    s->specs.resize(count);
+    s->topos.resize(count);
+    std::atomic<long> next{0};
+    auto worker = [&] {
+        for (long i; (i = next.fetch_add(1)) < count;) {
+            Scenario sc = sweep(start + i);
+            s->specs[i] = parse_workload(sc.workload_text);
+            s->topos[i] = parse_topology(sc.topology_text);
+        }
+    };
+    std::vector<std::thread> pool;
+    for (int t = 0; t < std::max(threads, 1); ++t) pool.emplace_back(worker);
+    for (auto& th : pool) th.join();
+    return s;
+}
+
+void wsref_sweep_free(wsref_sweep_set* s) { delete s; }
+
+// plan_workload over plans [first, first + count) of a prepared set on
+// `threads` std::threads; returns plans/s, infeasible count in *bad
+double wsref_sweep_run(const wsref_sweep_set* s, long first, long count, int threads, long* infeasible) {
+    count = std::max(0L, std::min<long>(count, static_cast<long>(s->specs.size()) - first));
+    std::atomic<long> next{0}, bad{0};
+    auto worker = [&] {
+        for (long i; (i = next.fetch_add(1)) < count;) {
+            try {
+                PlannerResult r = plan_workload(s->specs[first + i], s->topos[first + i]);
+                (void)r;
+            } catch (const Error&) {
+                bad.fetch_add(1);
+            }
+        }
+    };
+    const auto t0 = std::chrono::steady_clock::now();
+    std::vector<std::thread> pool;
+    for (int t = 0; t < threads; ++t) pool.emplace_back(worker);
+    for (auto& th : pool) th.join();
+    const double sec = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    if (infeasible) *infeasible = bad.load();
+    return static_cast<double>(count) / sec;
+}
+
 // Reference plan_workload + simulate_plan + validate_plan: the canonical
 // evaluation text (or the planner's "error ..." outcome).
 char* wsref_sim_text(const char* workload, const char* topology, const wsref_opts* o, const wsref_sim_opts* so) {

@@ -10,7 +10,8 @@
 // compared byte-for-byte with the reference planner compiled from the
 // reference headers (oracle/_ref, see oracle/Makefile) over the bundled
 // suite, the acceptance fuzz workloads and thousands of sweep mixtures
-// (tests/test_oracle_pin.py, tests/golden/).
+// (tests/test_oracle.py against the fixtures tests/golden/make_golden.py
+// generates from the reference; oracle/ref/pin.cpp for direct runs against it).
 //
 // Sorting uses std::sort with the reference comparators, i.e. the same
 // libstdc++ algorithm the reference runs.

@@ -148,6 +148,7 @@ def _load() -> C.CDLL:
         "ws_plan_staged": (C.c_int, [vp, vp]),
         "ws_fetch_results": (C.c_int, [vp, vp, vp, u64, C.POINTER(u64), vp]),
         "ws_last_launch_count": (C.c_int, [vp]),
+        "ws_last_retry_count": (C.c_longlong, [vp]),
         "ws_last_kernel_ms": (C.c_int, [vp, C.POINTER(C.c_double), C.c_int]),
         "ws_best_staged": (C.c_int, [vp, C.c_int, C.POINTER(C.c_double), C.POINTER(i64), vp]),
         "ws_arena_bound": (u64, [vp]),
@@ -505,6 +506,11 @@ class Planner:
     @property
     def launch_count(self) -> int:
         return lib.ws_last_launch_count(self._h)
+
+    @property
+    def retry_count(self) -> int:
+        """Soft-cap overflows of the last planning call, all re-planned with the hard caps."""
+        return int(lib.ws_last_retry_count(self._h))
 
     def kernel_ms(self) -> tuple[float, float, float]:
         """Device ms of (k_fit, k_sched, k_place incl. retry) in the last call."""

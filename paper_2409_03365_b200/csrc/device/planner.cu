@@ -32,7 +32,7 @@ using namespace wsdev;
 
 namespace {
 
-constexpr int kRetryMax = 1024;               // plans re-run with hard caps per call
+constexpr int kRetryMax = 1024;               // plans re-run with hard caps per retry launch
 constexpr int64_t kOverflowPieces = 1 << 18;  // isotonic/long curves
 constexpr int kSmemLimit = 227 * 1024;
 constexpr int kMaxChunks = 16;  // k_sched/k_place pipeline depth
@@ -43,6 +43,31 @@ constexpr int kMaxHostChunks = 8;
 constexpr int kSnapSlots = 512;
 // arena bound up to which ws_fetch_results copies the whole bound in one go
 constexpr uint64_t kOneSyncArena = 256u << 10;  // H2D / compute / D2H pipeline depth of ws_plan_batch_host
+
+// host_tops (page-locked u64 words): [0, 8) chunk arena bases, [8, 16) chunk
+// arena tops, [16] final top, [17] fetched top, [18] retry count of a staged
+// call, [24, 32) retry counts of the pipelined chunks
+constexpr int kHostTopsWords = 4 * kMaxHostChunks + 8;
+constexpr int kHtFinal = 2 * kMaxHostChunks, kHtFetch = kHtFinal + 1, kHtRetry = kHtFinal + 2;
+constexpr int kHtChunkRetry = 3 * kMaxHostChunks;
+
+// Makes `device` current for the scope of an entry point and restores the
+// caller's device on every exit path (the caller's torch/CUDA state stays put).
+struct DevGuard {
+    int prev = -1;
+    bool ok = true;
+    explicit DevGuard(int device) {
+        if (cudaGetDevice(&prev) != cudaSuccess) {
+            cudaGetLastError();
+            prev = -1;
+        }
+        if (prev != device) ok = cudaSetDevice(device) == cudaSuccess;
+    }
+    ~DevGuard() {
+        int cur = -1;
+        if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+    }
+};
 
 struct DevBuf {
     void* p = nullptr;
@@ -65,19 +90,14 @@ struct DevBuf {
     }
 };
 
-// plans whose soft record caps overflowed get queued for the retry launch
+// plans whose soft record caps overflowed get queued for the retry pass: ALL
+// of them (ids has room for every plan of the range); the first retry launch
+// covers the first kRetryMax without a host round trip, drain_overflow() the rest
 __global__ void k_soft_collect(const ws_plan_result* res, int p_begin, int p_end, int32_t* ids, int32_t* count) {
     const int p = p_begin + blockIdx.x * blockDim.x + threadIdx.x;
     if (p >= p_end) return;
     const int e = res[p].err_code;
-    if (e == WS_E_LIMIT_WAVES || e == WS_E_LIMIT_ENTRIES || e == WS_E_LIMIT_FLOWS) {
-        const int slot = atomicAdd(count, 1);
-        if (slot < kRetryMax) ids[slot] = p;
-    }
-}
-
-__global__ void k_clamp_count(int32_t* count) {
-    if (*count > kRetryMax) *count = kRetryMax;
+    if (e == WS_E_LIMIT_WAVES || e == WS_E_LIMIT_ENTRIES || e == WS_E_LIMIT_FLOWS) ids[atomicAdd(count, 1)] = p;
 }
 
 // Global min-loc over plan keys; ties -> smaller index.
@@ -138,7 +158,7 @@ struct BatchMax {
     }
 };
 
-LaunchCaps caps_from(const BatchMax& b, bool hard) {
+LaunchCaps caps_from(const BatchMax& b, bool hard, bool tiny = false) {
     const int M = std::min(b.M, WS_MAX_MODULES);
     const int N = std::min(b.N, WS_MAX_DEVICES);
     const int IS = std::min(b.IS, N);
@@ -149,6 +169,9 @@ LaunchCaps caps_from(const BatchMax& b, bool hard) {
     if (hard) {
         E = std::min(WS_MAX_ENTRIES, std::max(64, 2 * ME * ME));
         F = WS_MAX_FLOWS;
+    } else if (tiny) {  // $WSGPU_TINY_SOFT_CAPS (tests): nearly every plan overflows
+        E = 4;
+        F = 2;
     } else {
         E = std::max(32, 4 * ME);
         F = std::max(64, 8 * ME);
@@ -163,10 +186,10 @@ LaunchCaps caps_from(const BatchMax& b, bool hard) {
     return c;
 }
 
-LaunchCaps batch_caps(const ws_plan_rec* plans, int P, bool hard) {
+LaunchCaps batch_caps(const ws_plan_rec* plans, int P, bool hard, bool tiny = false) {
     BatchMax b;
     for (int p = 0; p < P; ++p) b.add(plans[p]);
-    return caps_from(b, hard);
+    return caps_from(b, hard, tiny);
 }
 
 int warps_for(int bytes_per_warp, int want) {
@@ -223,8 +246,16 @@ struct ws_ctx {
     DevBuf chunk_tops;
     cudaStream_t stream3 = nullptr;          // D2H side of the host pipeline (stream2: H2D side)
     cudaStream_t stream4 = nullptr;          // second compute stream of the host pipeline
-    DevBuf recs_r2, flows_r2, retry_ids2;    // its retry-pass buffers
-    unsigned long long* host_tops = nullptr; // page-locked: chunk bases, chunk tops, final top
+    DevBuf recs_r2, flows_r2;                // its retry-pass buffers
+    unsigned long long* host_tops = nullptr; // page-locked: chunk bases, chunk tops, final top, retry counts
+    // soft-cap overflows beyond the first retry launch (kRetryMax plans): the
+    // overflow count is copied back asynchronously and the remaining plans are
+    // re-planned at the next call that consumes the staged results
+    cudaEvent_t drain_ev = nullptr;
+    bool drain_pending = false;
+    cudaStream_t drain_stream = nullptr;
+    long long last_retry = 0;   // soft-cap overflows of the last planning call (all re-planned)
+    bool tiny_soft = false;     // $WSGPU_TINY_SOFT_CAPS: soft caps below every plan (tests of the retry pass)
     // measured (100k sweep, ms): one compute stream: 1 chunk 27.8, 2: 27.4, 4: 32.0 (each
     // chunk's k_sched + k_place launch tail outweighs the hidden copies); two compute
     // streams (consecutive chunks fill each other's tails) with completion-order D2H:
@@ -243,6 +274,16 @@ struct ws_ctx {
 };
 
 namespace {
+
+// arena top counter / capacity of a pipelined chunk for the launches in scope
+struct TopScope {
+    ws_ctx* c;
+    TopScope(ws_ctx* ctx, unsigned long long* top, uint64_t cap) : c(ctx) {
+        c->top_ptr = top;
+        c->top_cap = cap;
+    }
+    ~TopScope() { c->top_ptr = nullptr; }
+};
 
 int fail(ws_ctx* c, const std::string& what, cudaError_t e = cudaSuccess) {
     c->err = what;
@@ -420,29 +461,26 @@ extern "C" {
 
 int ws_ctx_create(int device, ws_ctx** out) {
     *out = nullptr;
-    if (cudaSetDevice(device) != cudaSuccess) return 1;
+    DevGuard g(device);
+    if (!g.ok) return 1;
     auto* c = new ws_ctx();
     c->device = device;
-    if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) {
-        delete c;
+    bool ok = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) == cudaSuccess &&
+              cudaStreamCreateWithFlags(&c->stream2, cudaStreamNonBlocking) == cudaSuccess &&
+              cudaStreamCreateWithFlags(&c->stream3, cudaStreamNonBlocking) == cudaSuccess &&
+              cudaStreamCreateWithFlags(&c->stream4, cudaStreamNonBlocking) == cudaSuccess &&
+              cudaMallocHost(reinterpret_cast<void**>(&c->host_tops), 8 * kHostTopsWords) == cudaSuccess;
+    for (auto& e : c->ev) ok = ok && cudaEventCreate(&e) == cudaSuccess;
+    for (auto& e : c->sev) ok = ok && cudaEventCreate(&e) == cudaSuccess;
+    for (auto& e : c->cev) ok = ok && cudaEventCreateWithFlags(&e, cudaEventDisableTiming) == cudaSuccess;
+    ok = ok && cudaEventCreateWithFlags(&c->order_ev, cudaEventDisableTiming) == cudaSuccess;
+    ok = ok && cudaEventCreateWithFlags(&c->drain_ev, cudaEventDisableTiming) == cudaSuccess;
+    if (!ok) {
+        cudaGetLastError();
+        ws_ctx_destroy(c);
         return 1;
     }
-    for (auto& e : c->sev)
-        if (e) cudaEventDestroy(e);
-    for (auto& e : c->ev) cudaEventCreate(&e);
-    for (auto& e : c->cev) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
-    cudaEventCreateWithFlags(&c->order_ev, cudaEventDisableTiming);
-    for (auto& e : c->sev) cudaEventCreate(&e);
-    if (cudaStreamCreateWithFlags(&c->stream2, cudaStreamNonBlocking) != cudaSuccess) {
-        delete c;
-        return 1;
-    }
-    if (cudaStreamCreateWithFlags(&c->stream3, cudaStreamNonBlocking) != cudaSuccess ||
-        cudaStreamCreateWithFlags(&c->stream4, cudaStreamNonBlocking) != cudaSuccess ||
-        cudaMallocHost(reinterpret_cast<void**>(&c->host_tops), 8 * (2 * kMaxHostChunks + 8)) != cudaSuccess) {
-        delete c;
-        return 1;
-    }
+    std::memset(c->host_tops, 0, 8 * kHostTopsWords);
     if (const char* env = std::getenv("WSGPU_CHUNKS")) c->chunks = std::atoi(env);
     if (const char* env = std::getenv("WSGPU_HOST_CHUNKS")) {
         c->host_chunks = std::atoi(env);
@@ -462,30 +500,31 @@ int ws_ctx_create(int device, ws_ctx** out) {
     if (const char* env = std::getenv("WSGPU_FORCE_SNAP")) c->force_snap = std::atoi(env) != 0;
     if (const char* env = std::getenv("WSGPU_PDL")) c->pdl = std::atoi(env) != 0;
     if (const char* env = std::getenv("WSGPU_HOST_STREAMS")) c->host_streams = std::max(1, std::min(2, std::atoi(env)));
+    if (const char* env = std::getenv("WSGPU_TINY_SOFT_CAPS")) c->tiny_soft = std::atoi(env) != 0;
     *out = c;
     return 0;
 }
 
 void ws_ctx_destroy(ws_ctx* c) {
     if (!c) return;
-    cudaSetDevice(c->device);
-    for (auto& e : c->ev)
-        if (e) cudaEventDestroy(e);
+    DevGuard g(c->device);
+    if (c->stream) cudaStreamSynchronize(c->stream);
+    for (cudaEvent_t* e : {c->ev, c->ev + 1, c->ev + 2, c->ev + 3, c->sev, c->sev + 1, &c->order_ev, &c->drain_ev})
+        if (*e) cudaEventDestroy(*e);
     for (auto& e : c->cev)
         if (e) cudaEventDestroy(e);
-    if (c->stream) cudaStreamDestroy(c->stream);
-    if (c->stream2) cudaStreamDestroy(c->stream2);
-    if (c->stream3) cudaStreamDestroy(c->stream3);
-    if (c->stream4) cudaStreamDestroy(c->stream4);
+    for (cudaStream_t s : {c->stream, c->stream2, c->stream3, c->stream4})
+        if (s) cudaStreamDestroy(s);
     if (c->host_tops) cudaFreeHost(c->host_tops);
     if (c->order_pinned) cudaFreeHost(c->order_pinned);
-    if (c->order_ev) cudaEventDestroy(c->order_ev);
-    delete c;
+    delete c;  // DevBuf destructors free device memory on c->device (guarded)
 }
 
 const char* ws_ctx_last_error(const ws_ctx* c) { return c ? c->err.c_str() : "null ctx"; }
 
 int ws_last_launch_count(const ws_ctx* c) { return c ? c->launches : 0; }
+
+long long ws_last_retry_count(const ws_ctx* c) { return c ? c->last_retry : 0; }
 
 int ws_last_kernel_ms(const ws_ctx* c, double* out, int n) {
     if (!c) return 1;
@@ -516,7 +555,7 @@ int prepare_plan(ws_ctx* ctx, FitOut& fo) {
         return fail(ctx, "cudaMalloc fit buffers");
     const RecLayout RL = make_rec_layout(lc.rec), RLh = make_rec_layout(lh.rec);
     if (!ctx->counters.ensure(64) || !ctx->results.ensure(sizeof(ws_plan_result) * std::max(P, 1)) ||
-        !ctx->arena.ensure(ctx->arena_cap) || !ctx->retry_ids.ensure(4 * kRetryMax) || !ctx->best.ensure(64) ||
+        !ctx->arena.ensure(ctx->arena_cap) || !ctx->retry_ids.ensure(4ull * std::max(P, 1)) || !ctx->best.ensure(64) ||
         !ctx->recs.ensure(static_cast<size_t>(RL.bytes) * std::max(P, 1)) ||
         !ctx->flows.ensure(16ull * lc.pl.F * std::max(P, 1)) ||
         !ctx->recs_r.ensure(static_cast<size_t>(RLh.bytes) * kRetryMax) ||
@@ -547,6 +586,29 @@ int prepare_plan(ws_ctx* ctx, FitOut& fo) {
     fo.overflow_cap = kOverflowPieces;
     fo.ttab = ctx->ttab.as<double>();
     fo.tstride = tstride;
+    return 0;
+}
+
+// Re-plans the soft-cap overflows the first retry launch of the last
+// ws_plan_staged did not cover (more than kRetryMax in one batch), in further
+// kRetryMax-plan launches on `st`.  Called by every entry point that consumes
+// the staged results; waits for the overflow count of that call.
+int drain_overflow(ws_ctx* ctx, cudaStream_t st) {
+    if (!ctx->drain_pending) return 0;
+    ctx->drain_pending = false;
+    CK(cudaEventSynchronize(ctx->drain_ev));
+    const long long total = static_cast<int32_t>(ctx->host_tops[kHtRetry] & 0xffffffffull);
+    ctx->last_retry = total;
+    if (total <= kRetryMax) return 0;
+    FitOut fo;
+    if (prepare_plan(ctx, fo)) return 1;
+    for (long long b = kRetryMax; b < total; b += kRetryMax) {
+        const int n = static_cast<int>(std::min<long long>(kRetryMax, total - b));
+        if (launch_pair(ctx, st, ctx->caps_hard, fo, ctx->retry_ids.as<int32_t>() + b, nullptr, n, true,
+                        ctx->recs_r.as<char>(), ctx->flows_r.as<uint64_t>()))
+            return 1;
+    }
+    CK(cudaGetLastError());
     return 0;
 }
 
@@ -584,7 +646,7 @@ int ensure_order_pinned(ws_ctx* ctx, int P) {
 }  // namespace
 
 int ws_stage_batch(ws_ctx* ctx, const ws_batch* in, void* stream) {
-    cudaSetDevice(ctx->device);
+    DevGuard dg_(ctx->device);
     cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
     if (!in->blob) return fail(ctx, "ws_stage_batch: batch must be contiguous (ws_batch.blob)");
     const int P = in->n_plans;
@@ -592,7 +654,8 @@ int ws_stage_batch(ws_ctx* ctx, const ws_batch* in, void* stream) {
         return fail(ctx, "cudaMalloc batch");
     CK(cudaMemcpyAsync(ctx->blob.p, in->blob, in->blob_bytes, cudaMemcpyHostToDevice, st));
     ctx->dview = rebase(*in, in->blob, ctx->blob.as<char>());
-    ctx->caps = batch_caps(in->plans, P, false);
+    ctx->drain_pending = false;  // results of an earlier staged batch are superseded
+    ctx->caps = batch_caps(in->plans, P, false, ctx->tiny_soft);
     ctx->caps_hard = batch_caps(in->plans, P, true);
     ctx->arena_cap = ws_arena_bound(in);
     ctx->sim_cap = ws_sim_arena_bound(in);
@@ -624,13 +687,15 @@ static void launch_fit(const ws_batch& B, const FitOut& fo, int m0, int m1, cuda
 }
 
 int ws_plan_staged(ws_ctx* ctx, void* stream) {
-    cudaSetDevice(ctx->device);
+    DevGuard dg_(ctx->device);
     cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
     const ws_batch& B = ctx->dview;
     const int P = B.n_plans;
     const LaunchCaps& lc = ctx->caps;
     const LaunchCaps& lh = ctx->caps_hard;
     ctx->launches = 0;
+    ctx->drain_pending = false;  // this call re-plans every plan of the staged batch
+    ctx->last_retry = 0;
     FitOut fo;
     if (prepare_plan(ctx, fo)) return 1;
     auto* counters = ctx->counters.as<unsigned long long>();  // [0] arena top [1] overflow top [2] retry count
@@ -648,19 +713,26 @@ int ws_plan_staged(ws_ctx* ctx, void* stream) {
     if (launch_pair(ctx, st, lc, fo, ctx->order.as<int32_t>(), nullptr, P, false, ctx->recs.as<char>(),
                     ctx->flows.as<uint64_t>(), ctx->ev[3], ctx->chunks, ctx->pdl && B.n_modules > 0))
         return 1;
-    // retry pass: soft-cap overflows with the hard caps, count read on device
+    // retry pass: soft-cap overflows with the hard caps, count read on device;
+    // the first kRetryMax run here, any beyond in drain_overflow()
     auto* rcount = reinterpret_cast<int32_t*>(counters + 2);
     if (P > 0) {
         k_soft_collect<<<(P + 255) / 256, 256, 0, st>>>(ctx->res_out(), 0, P,
                                                          ctx->retry_ids.as<int32_t>(), rcount);
-        k_clamp_count<<<1, 1, 0, st>>>(rcount);
-        ctx->launches += 2;
+        ctx->launches++;
         // retry grid sized for at most min(P, kRetryMax) plans (small batches: one block)
         if (launch_pair(ctx, st, lh, fo, ctx->retry_ids.as<int32_t>(), rcount, std::min(P, kRetryMax), true,
                         ctx->recs_r.as<char>(), ctx->flows_r.as<uint64_t>()))
             return 1;
     }
     CK(cudaEventRecord(ctx->ev[2], st));
+    if (P > 0) {
+        ctx->host_tops[kHtRetry] = 0;
+        CK(cudaMemcpyAsync(ctx->host_tops + kHtRetry, rcount, 4, cudaMemcpyDeviceToHost, st));
+        CK(cudaEventRecord(ctx->drain_ev, st));
+        ctx->drain_pending = true;
+        ctx->drain_stream = st;
+    }
     CK(cudaGetLastError());
     ctx->staged_events = P > 0;
     ctx->records_on_device = true;
@@ -670,15 +742,16 @@ int ws_plan_staged(ws_ctx* ctx, void* stream) {
 
 int ws_fetch_results(ws_ctx* ctx, ws_plan_result* results, uint8_t* arena, uint64_t arena_cap,
                      uint64_t* arena_used, void* stream) {
-    cudaSetDevice(ctx->device);
+    DevGuard dg_(ctx->device);
     cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
+    if (drain_overflow(ctx, st)) return 1;
     const int P = ctx->dview.n_plans;
     unsigned long long top = 0;
     // small batches (single-plan latency): copy the whole arena bound with the
     // headers and the top counter, one synchronization instead of two
     const bool one_sync = ctx->arena_cap <= kOneSyncArena && ctx->arena_cap <= arena_cap;
     if (P) CK(cudaMemcpyAsync(results, ctx->results.p, sizeof(ws_plan_result) * P, cudaMemcpyDeviceToHost, st));
-    unsigned long long* htop = ctx->host_tops + 2 * kMaxHostChunks + 1;  // page-locked
+    unsigned long long* htop = ctx->host_tops + kHtFetch;  // page-locked
     CK(cudaMemcpyAsync(htop, ctx->counters.p, sizeof(top), cudaMemcpyDeviceToHost, st));
     if (one_sync && ctx->arena_cap) CK(cudaMemcpyAsync(arena, ctx->arena.p, ctx->arena_cap, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
@@ -712,7 +785,7 @@ extern "C" uint64_t wsi_arena_bound_plans(const ws_plan_rec* plans, int n);
 // 11 ms per 100k).
 int ws_plan_batch_host(ws_ctx* ctx, const ws_batch* in, ws_plan_result* results, uint8_t* arena,
                        uint64_t arena_cap, uint64_t* arena_used, void* stream) {
-    cudaSetDevice(ctx->device);
+    DevGuard dg_(ctx->device);
     cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
     const int P = in->n_plans;
     int C = ctx->host_chunks;
@@ -727,6 +800,7 @@ int ws_plan_batch_host(ws_ctx* ctx, const ws_batch* in, ws_plan_result* results,
     char* dblob = ctx->blob.as<char>();
     ctx->dview = rebase(*in, in->blob, dblob);
     ctx->sim_valid = false;
+    ctx->drain_pending = false;
     int pb[kMaxHostChunks + 1];
     uint64_t abase[kMaxHostChunks + 1];
     abase[0] = 0;
@@ -767,7 +841,7 @@ int ws_plan_batch_host(ws_ctx* ctx, const ws_batch* in, ws_plan_result* results,
         for (int k = 0; k < kLptKeys; ++k) hist[k + 1] += hist[k];
         for (int p = pb[c]; p < pb[c + 1]; ++p) ctx->order_pinned[pb[c] + hist[ctx->lpt_keys[p]]++] = p;
     }
-    ctx->caps = caps_from(bm, false);
+    ctx->caps = caps_from(bm, false, ctx->tiny_soft);
     ctx->caps_hard = caps_from(bm, true);
     ctx->sim_cap = sim_total + 4096;  // == ws_sim_arena_bound(in)
     ctx->arena_cap = abase[C];
@@ -828,8 +902,7 @@ int ws_plan_batch_host(ws_ctx* ctx, const ws_batch* in, ws_plan_result* results,
     const int S = ctx->host_streams;
     cudaStream_t cs[2] = {st, ctx->stream4};
     if (S > 1) {
-        if (!ctx->recs_r2.ensure(ctx->recs_r.n) || !ctx->flows_r2.ensure(ctx->flows_r.n) ||
-            !ctx->retry_ids2.ensure(4 * kRetryMax))
+        if (!ctx->recs_r2.ensure(ctx->recs_r.n) || !ctx->flows_r2.ensure(ctx->flows_r.n))
             return fail(ctx, "cudaMalloc retry buffers");
         CK(cudaEventRecord(ctx->ev[1], st));
         CK(cudaStreamWaitEvent(cs[1], ctx->ev[1], 0));
@@ -840,12 +913,11 @@ int ws_plan_batch_host(ws_ctx* ctx, const ws_batch* in, ws_plan_result* results,
         const int k = c % S;
         cudaStream_t s = cs[k];
         auto* rcount = reinterpret_cast<int32_t*>(counters + 2 + k);
-        DevBuf& rids = k ? ctx->retry_ids2 : ctx->retry_ids;
+        int32_t* rids = ctx->retry_ids.as<int32_t>() + p0;  // chunks own disjoint plan ranges
         DevBuf& rrecs = k ? ctx->recs_r2 : ctx->recs_r;
         DevBuf& rflows = k ? ctx->flows_r2 : ctx->flows_r;
         CK(cudaStreamWaitEvent(s, h2d[c], 0));
-        ctx->top_ptr = tops + c;
-        ctx->top_cap = abase[c + 1];
+        TopScope ts(ctx, tops + c, abase[c + 1]);
         if (m1 > m0) {
             launch_fit(B, fo, m0, m1, s);
             ctx->launches++;
@@ -858,15 +930,14 @@ int ws_plan_batch_host(ws_ctx* ctx, const ws_batch* in, ws_plan_result* results,
                              ctx->pdl && m1 > m0);
         if (!rc) {
             CK(cudaMemsetAsync(rcount, 0, 4, s));
-            k_soft_collect<<<(p1 - p0 + 255) / 256, 256, 0, s>>>(ctx->res_out(), p0, p1, rids.as<int32_t>(),
-                                                                  rcount);
-            k_clamp_count<<<1, 1, 0, s>>>(rcount);
-            ctx->launches += 2;
-            rc = launch_pair(ctx, s, ctx->caps_hard, fo, rids.as<int32_t>(), rcount, std::min(p1 - p0, kRetryMax), true,
+            k_soft_collect<<<(p1 - p0 + 255) / 256, 256, 0, s>>>(ctx->res_out(), p0, p1, rids, rcount);
+            ctx->launches++;
+            rc = launch_pair(ctx, s, ctx->caps_hard, fo, rids, rcount, std::min(p1 - p0, kRetryMax), true,
                              rrecs.as<char>(), rflows.as<uint64_t>());
         }
-        ctx->top_ptr = nullptr;
         if (rc) return 1;
+        ctx->host_tops[kHtChunkRetry + c] = 0;
+        CK(cudaMemcpyAsync(ctx->host_tops + kHtChunkRetry + c, rcount, 4, cudaMemcpyDeviceToHost, s));
         CK(cudaMemcpyAsync(ctx->host_tops + kMaxHostChunks + c, tops + c, 8, cudaMemcpyDeviceToHost, s));
         CK(cudaEventRecord(done[c], s));
     }
@@ -902,9 +973,37 @@ int ws_plan_batch_host(ws_ctx* ctx, const ws_batch* in, ws_plan_result* results,
     }
     CK(cudaStreamSynchronize(sd));
     CK(cudaStreamSynchronize(st));
+    // soft-cap overflows beyond a chunk's first retry launch (more than kRetryMax
+    // in one chunk): re-plan the rest now, then copy that chunk back again
+    ctx->last_retry = 0;
+    for (int c = 0; c < C; ++c) {
+        const long long total = static_cast<int32_t>(ctx->host_tops[kHtChunkRetry + c] & 0xffffffffull);
+        ctx->last_retry += total;
+        if (total <= kRetryMax) continue;
+        {
+            TopScope ts(ctx, tops + c, abase[c + 1]);
+            const int32_t* rids = ctx->retry_ids.as<int32_t>() + pb[c];
+            for (long long b = kRetryMax; b < total; b += kRetryMax) {
+                const int n = static_cast<int>(std::min<long long>(kRetryMax, total - b));
+                if (launch_pair(ctx, st, ctx->caps_hard, fo, rids + b, nullptr, n, true, ctx->recs_r.as<char>(),
+                                ctx->flows_r.as<uint64_t>()))
+                    return 1;
+            }
+        }
+        CK(cudaMemcpyAsync(ctx->host_tops + kMaxHostChunks + c, tops + c, 8, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        const uint64_t top = std::min<uint64_t>(ctx->host_tops[kMaxHostChunks + c], abase[c + 1]);
+        CK(cudaMemcpyAsync(results + pb[c], ctx->results.as<ws_plan_result>() + pb[c],
+                           sizeof(ws_plan_result) * (pb[c + 1] - pb[c]), cudaMemcpyDeviceToHost, st));
+        if (top > abase[c])
+            CK(cudaMemcpyAsync(arena + abase[c], ctx->arena.as<uint8_t>() + abase[c], top - abase[c],
+                               cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        used = std::max<uint64_t>(used, top);
+    }
     // the device arena top for a later ws_fetch_results / ws_simulate_staged
-    ctx->host_tops[2 * kMaxHostChunks] = used;
-    CK(cudaMemcpyAsync(counters, ctx->host_tops + 2 * kMaxHostChunks, 8, cudaMemcpyHostToDevice, st));
+    ctx->host_tops[kHtFinal] = used;
+    CK(cudaMemcpyAsync(counters, ctx->host_tops + kHtFinal, 8, cudaMemcpyHostToDevice, st));
     CK(cudaStreamSynchronize(st));
     float ms = 0;
     ctx->staged_events = false;
@@ -930,8 +1029,9 @@ int ws_debug_phase_cycles(unsigned long long* out, int n) {
 }
 
 int ws_best_staged(ws_ctx* ctx, int mode, double* key, int64_t* index, void* stream) {
-    cudaSetDevice(ctx->device);
+    DevGuard dg_(ctx->device);
     cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
+    if (drain_overflow(ctx, st)) return 1;
     auto* kb = ctx->best.as<double>();
     auto* ib = reinterpret_cast<long long*>(kb + 1);
     if (mode == 2 && !ctx->sim_valid) return fail(ctx, "ws_best_staged: mode 2 needs ws_simulate_staged first");
@@ -951,11 +1051,12 @@ int ws_best_staged(ws_ctx* ctx, int mode, double* key, int64_t* index, void* str
 
 // ---- plan evaluation (simulate_plan + validate_plan) -------------------------
 int ws_simulate_staged(ws_ctx* ctx, const ws_sim_opts* opts, void* stream) {
-    cudaSetDevice(ctx->device);
+    DevGuard dg_(ctx->device);
     cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
     if (!ctx->records_on_device)
         return fail(ctx, "ws_simulate_staged: no device-resident plan records (plan with ws_plan_staged, "
                          "or evaluate host records with ws_simulate_batch_host)");
+    if (drain_overflow(ctx, st)) return 1;
     const int P = ctx->dview.n_plans;
     const LaunchCaps& lh = ctx->caps_hard;
     SimArgs A{};
@@ -988,7 +1089,7 @@ int ws_simulate_staged(ws_ctx* ctx, const ws_sim_opts* opts, void* stream) {
 
 int ws_fetch_sim(ws_ctx* ctx, ws_sim_result* out, uint8_t* arena, uint64_t arena_cap, uint64_t* arena_used,
                  void* stream) {
-    cudaSetDevice(ctx->device);
+    DevGuard dg_(ctx->device);
     cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
     if (!ctx->sim_valid) return fail(ctx, "ws_fetch_sim: nothing simulated");
     const int P = ctx->dview.n_plans;
@@ -1009,7 +1110,7 @@ int ws_fetch_sim(ws_ctx* ctx, ws_sim_result* out, uint8_t* arena, uint64_t arena
 int ws_simulate_batch_host(ws_ctx* ctx, const ws_batch* in, const ws_plan_result* plans, const uint8_t* plan_arena,
                            uint64_t plan_arena_bytes, const ws_sim_opts* opts, ws_sim_result* out, uint8_t* arena,
                            uint64_t arena_cap, uint64_t* arena_used, void* stream) {
-    cudaSetDevice(ctx->device);
+    DevGuard dg_(ctx->device);
     cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
     if (ws_stage_batch(ctx, in, stream)) return 1;
     const int P = in->n_plans;

@@ -128,14 +128,81 @@ def test_gpu_dropin_plan_workload(golden_cases):
         ws.plan_workload(c["workload"], c["topology"])
 
 
-def test_gpu_kernel_timing_reported(planner):
+def test_gpu_kernel_timing_reported(planner, monkeypatch):
+    """With programmatic dependent launch (default) k_sched starts behind k_fit
+    and the fit is reported inside k_sched's time; with WSGPU_PDL=0 each kernel
+    has its own events."""
     import paper_2409_03365_b200 as ws
     ps = ws.ProblemSet()
     ps.add_sweep(0, 2000)
     ps.encode(pinned=True)
     planner.plan(ps)
     fit_ms, sched_ms, place_ms = planner.kernel_ms()
+    assert fit_ms >= 0 and sched_ms > 0 and place_ms > 0
+    monkeypatch.setenv("WSGPU_PDL", "0")
+    pl = ws.Planner(0)
+    pl.plan(ps)
+    fit_ms, sched_ms, place_ms = pl.kernel_ms()
     assert fit_ms > 0 and sched_ms > 0 and place_ms > 0
+
+
+def _tiny_soft_caps_planner(monkeypatch, **env):
+    import paper_2409_03365_b200 as ws
+    monkeypatch.setenv("WSGPU_TINY_SOFT_CAPS", "1")
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    return ws.Planner(0)
+
+
+def test_gpu_retry_pass_drains_every_overflow(monkeypatch, golden_cases):
+    """Soft-cap overflows are all re-planned with the hard caps, however many
+    a batch holds (no per-call cap): with soft caps below every plan
+    ($WSGPU_TINY_SOFT_CAPS) a 2600-plan batch overflows > 2048 plans and still
+    equals the oracle record for record -- staged path (fetch, best, simulate
+    drain the rest) and the one-shot host call."""
+    import paper_2409_03365_b200 as ws
+    import pyoracle
+    pl = _tiny_soft_caps_planner(monkeypatch)
+    ps, kept, _ = build_set(golden_cases[:100])
+    ps.add_sweep(0, 2500)
+    ps.encode(pinned=True)
+    o = pyoracle.plan_batch(ps)
+    g = pl.plan(ps)
+    assert pl.retry_count >= 2048
+    bad = [i for i in range(len(ps)) if records(g, i) != records(o, i)]
+    assert not bad, bad[:10]
+    # staged: best() and simulate_staged() consume the results before any fetch
+    pl.stage(ps)
+    pl.plan_staged()
+    key, idx = pl.best(1)
+    okeys = [(o.results[i].end_time, i) for i in range(len(ps)) if o.results[i].status == 0]
+    assert (key, idx) == min(okeys)
+    pl.plan_staged()
+    pl.simulate_staged()
+    sims = pl.fetch_sim(ps)
+    g2 = pl.fetch(ps)
+    assert pl.retry_count >= 2048
+    bad = [i for i in range(len(ps)) if records(g2, i) != records(o, i)]
+    assert not bad, bad[:10]
+    osims = pyoracle.simulate_batch(ps, o)
+    bad = [i for i in range(len(ps)) if ps.sim_text(i, g2, sims) != ps.sim_text(i, o, osims)]
+    assert not bad, bad[:10]
+
+
+def test_gpu_retry_pass_drains_pipelined_chunks(monkeypatch):
+    """The same for the chunked H2D / compute / D2H pipeline of
+    ws_plan_batch_host: every chunk overflows more than one retry launch."""
+    import paper_2409_03365_b200 as ws
+    import pyoracle
+    pl = _tiny_soft_caps_planner(monkeypatch, WSGPU_HOST_CHUNKS="2")
+    ps = ws.ProblemSet()
+    ps.add_sweep(0, 9000)
+    ps.encode(pinned=True)
+    g = pl.plan(ps)
+    assert pl.retry_count >= 4096
+    o = pyoracle.plan_batch(ps)
+    bad = [i for i in range(len(ps)) if records(g, i) != records(o, i)]
+    assert not bad, bad[:10]
 
 
 def test_gpu_pipelined_host_call_matches(sweep_hashes, monkeypatch):
