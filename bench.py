@@ -231,6 +231,8 @@ def main() -> None:
     ap.add_argument("--cpu-sample", type=int, default=6000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--latency-reps", type=int, default=300, help="single-plan latency samples (SURVEY 8(d): >= 300)")
+    ap.add_argument("--dropin-plans", type=int, default=20000, help="sweep plans of the drop-in throughput block")
+    ap.add_argument("--no-dropin", action="store_true")
     ap.add_argument("--compare-mixtures", type=int, default=25000,
                     help="sweep mixtures of the strategy-comparison block (each planned by all 4 strategies)")
     args = ap.parse_args()
@@ -536,7 +538,9 @@ def main() -> None:
         ss = sorted(samples)
         latency[name] = {"gpu_e2e_ms_median": statistics.median(samples), "gpu_e2e_ms_p10": ss[len(ss) // 10],
                          "gpu_e2e_ms_p90": ss[(9 * len(ss)) // 10], "samples": len(ss),
-                         "path": "ws_plan_batch_host, one plan, pinned host in/out"}
+                         "path": ("C-ABI only: ws_plan_batch_host on a pre-encoded plan, pinned host in, "
+                                  "binary records out, warm context (no encode/decode; the reference-typed "
+                                  "drop-in with both is dropin.latency_ms)")}
 
     cpu = None
     evaluation = {"what": "simulate_plan + validate_plan of every planned mixture (k_sim, device-resident records)",
@@ -584,6 +588,26 @@ def main() -> None:
         except Exception:
             pass
 
+    # ---- the drop-in through the reference's own types (wavesched_gpu::plan_workload:
+    # reference WorkloadSpec in, reference PlannerResult out, every host step
+    # inside the timer) next to the reference planner, same process and host ----
+    dropin = None
+    exe = ROOT / "oracle" / "_ref" / "dropin_bench"
+    if exe.exists() and not args.no_dropin:
+        try:
+            r = subprocess.run([str(exe), str(args.latency_reps), str(args.dropin_plans), str(os.cpu_count() or 1)],
+                               capture_output=True, text=True, timeout=900,
+                               env={**os.environ, "CUDA_VISIBLE_DEVICES": str(local)} if world > 1 else None)
+            dropin = json.loads(r.stdout.strip().splitlines()[-1]) if r.returncode == 0 else {"error": r.stderr[-500:]}
+            dropin["what"] = ("oracle/ref/dropin_bench.cpp: wavesched_gpu::plan_workload (reference types in, "
+                              "PlannerResult out: conversion, encode, H2D, kernels, D2H, decode all timed) vs the "
+                              "reference plan_workload in the same process; cold_start_ms = first call of the "
+                              "process (CUDA context + module load); throughput = host threads each calling "
+                              "the drop-in (one pooled context per thread) vs the reference on the same threads; "
+                              "batched = plan_workloads(_each): one device batch, decode on all threads")
+        except Exception as e:  # noqa: BLE001
+            dropin = {"error": str(e)}
+
     line = {
         "metric": METRIC,
         "value": value,
@@ -599,7 +623,10 @@ def main() -> None:
         "data": "synthetic",
         "config": workload_config(args, world),
         "e2e": {"value": e2e_value, "unit": "plans/s", "h2d_bytes_per_step": in_bytes_blob,
-                "d2h_bytes_per_step": d2h_step, "path": "ws_plan_batch_host (pinned host in/out)"},
+                "d2h_bytes_per_step": d2h_step,
+                "path": ("ws_plan_batch_host, the C-ABI (pinned host batch in, result headers + plan records "
+                         "out); a caller of the reference-typed API also pays encode + decode per plan on "
+                         "host threads: see dropin")},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "kernel": dom,
                      "algorithmic_bytes_per_launch": dom_bytes, "kernel_ms": dom_ms, "peak_source": peak_src,
@@ -613,6 +640,7 @@ def main() -> None:
         "clocks": clk,
         "rank_step_ms": rank_step_ms,
         "latency_ms": latency,
+        "dropin": dropin,
         "evaluation": evaluation,
         "baselines": baselines,
         "compare": compare,

@@ -18,6 +18,7 @@
 
 #include <cstdint>
 #include <exception>
+#include <functional>
 #include <map>
 #include <memory>
 #include <optional>
@@ -341,8 +342,11 @@ struct PlannerResult {
 };
 
 // Drop-in for wavesched::plan_workload: same arguments, same result, same
-// exceptions.  Runs on the process-wide default context (CUDA device 0, or
-// $WSGPU_DEVICE).  Throws if the CUDA planner cannot run (no fallback).
+// exceptions.  Reentrant like the reference: each call checks a
+// planning context with its own streams and page-locked staging buffers out of
+// a pool for the calling thread's current CUDA device ($WSGPU_DEVICE
+// overrides), so concurrent callers plan in parallel.  Throws if the CUDA
+// planner cannot run (no fallback).
 PlannerResult plan_workload(const WorkloadSpec& spec, const ClusterTopology& topo,
                             const PlannerOptions& opt = {});
 
@@ -353,6 +357,25 @@ struct Problem {
     const ClusterTopology* topo = nullptr;
     PlannerOptions opt;
 };
+
+// plan_workload over many problems in ONE device batch: the per-problem host
+// preparation and the decode into PlannerResult run on `threads` host threads
+// (0 = all cores).  Each outcome holds the result or the exception
+// plan_workload would have thrown for that problem.
+struct PlanOutcome {
+    PlannerResult result;
+    std::exception_ptr error;
+};
+std::vector<PlanOutcome> plan_workloads(const std::vector<Problem>& problems, int threads = 0);
+
+// The raw device output of plan_workload / plan_workloads, for callers that
+// decode into their own types (wavesched_compat.hpp decodes straight into the
+// reference's types with detail::decode_into): `consume` sees the result
+// header(s) and record arena, valid only during the call.
+void plan_workload_raw(const WorkloadSpec& spec, const ClusterTopology& topo, const PlannerOptions& opt,
+                       const std::function<void(const ws_plan_result& res, const std::uint8_t* arena)>& consume);
+void plan_workloads_raw(const std::vector<Problem>& problems, int threads,
+                        const std::function<void(const ws_plan_result* res, const std::uint8_t* arena)>& consume);
 
 // Owns the memory behind a ws_batch (one contiguous, optionally pinned,
 // block = ws_batch.blob).  Host-side validation (validate_workload) runs while

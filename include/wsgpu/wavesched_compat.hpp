@@ -5,12 +5,20 @@
 //                                const wavesched::ClusterTopology&,
 //                                const wavesched::PlannerOptions& = {})
 //       -> wavesched::PlannerResult
-// with the reference signature (planner.hpp:156-157), running the B200
-// planner through wsgpu::plan_workload and rethrowing the reference's own
-// exception classes (common.hpp:20-60) with the same what() text.
+// with the reference signature (planner.hpp:156-157): reentrant (concurrent
+// callers plan in parallel on pooled contexts), the device record decoded
+// straight into the reference's types (decode_impl.hpp), and the reference's
+// own exception classes (common.hpp:20-60) rethrown with the same what() text.
+// plan_workloads / plan_workloads_each plan many problems in one device batch
+// with the decode spread over host threads.
 // Link with paper_2409_03365_b200/lib/libwsgpu.so.
 #pragma once
 
+#include <algorithm>
+#include <atomic>
+#include <thread>
+
+#include "wsgpu/decode_impl.hpp"
 #include "wsgpu/planner.hpp"
 
 namespace wavesched_gpu {
@@ -192,11 +200,88 @@ inline wavesched::PlannerResult plan_workload(const wavesched::WorkloadSpec& spe
                                               const wavesched::PlannerOptions& opt = {}) {
     const wsgpu::WorkloadSpec s = detail::to_mirror(spec);
     const wsgpu::ClusterTopology t = detail::to_mirror(topo);
+    const wsgpu::PlannerOptions o = detail::to_mirror(opt);
+    wavesched::PlannerResult out;
     try {
-        return detail::to_ref(wsgpu::plan_workload(s, t, detail::to_mirror(opt)), topo);
+        wsgpu::plan_workload_raw(s, t, o, [&](const ws_plan_result& r, const std::uint8_t* arena) {
+            if (r.status != WS_STATUS_OK) wsgpu::throw_result_error(wsgpu::Problem{&s, &t, o}, r);
+            wsgpu::detail::decode_into(spec, topo, WS_STRATEGY_WAVEFRONT, opt.grad_opt_multiplier, r, arena, true, out);
+        });
     } catch (const wsgpu::Error& e) {
         detail::rethrow_as_reference(e);
     }
+    return out;
+}
+
+// plan_workload over many (spec, topology) pairs in ONE device batch, with the
+// conversion and the decode into the reference's types spread over `threads`
+// host threads (0 = all cores).  Streaming form: `each(i, result, error)` is
+// called on a worker thread for every problem as soon as its result is
+// decoded (error: the reference exception plan_workload would have thrown),
+// so a consumer that keeps only what it needs never holds every PlannerResult.
+template <typename Each>
+void plan_workloads_each(
+    const std::vector<std::pair<const wavesched::WorkloadSpec*, const wavesched::ClusterTopology*>>& problems,
+    const wavesched::PlannerOptions& opt, int threads, Each&& each) {
+    const std::size_t P = problems.size();
+    if (threads <= 0) threads = std::max(1u, std::thread::hardware_concurrency());
+    auto par = [&](auto&& fn) {
+        std::atomic<std::size_t> next{0};
+        auto work = [&] {
+            for (std::size_t i; (i = next.fetch_add(16)) < P;)
+                for (std::size_t j = i; j < std::min(P, i + 16); ++j) fn(j);
+        };
+        std::vector<std::thread> pool;
+        for (int t = 1; t < threads && static_cast<std::size_t>(t) * 16 < P; ++t) pool.emplace_back(work);
+        work();
+        for (auto& th : pool) th.join();
+    };
+    std::vector<wsgpu::WorkloadSpec> specs(P);
+    std::vector<wsgpu::ClusterTopology> topos(P);
+    par([&](std::size_t i) {
+        specs[i] = detail::to_mirror(*problems[i].first);
+        topos[i] = detail::to_mirror(*problems[i].second);
+    });
+    const wsgpu::PlannerOptions o = detail::to_mirror(opt);
+    std::vector<wsgpu::Problem> probs(P);
+    for (std::size_t i = 0; i < P; ++i) probs[i] = wsgpu::Problem{&specs[i], &topos[i], o};
+    wsgpu::plan_workloads_raw(probs, threads, [&](const ws_plan_result* res, const std::uint8_t* arena) {
+        par([&](std::size_t i) {
+            wavesched::PlannerResult r;
+            std::exception_ptr err;
+            try {
+                try {
+                    if (res[i].status != WS_STATUS_OK) wsgpu::throw_result_error(probs[i], res[i]);
+                    wsgpu::detail::decode_into(*problems[i].first, *problems[i].second, WS_STRATEGY_WAVEFRONT,
+                                               opt.grad_opt_multiplier, res[i], arena, true, r);
+                } catch (const wsgpu::Error& e) {
+                    detail::rethrow_as_reference(e);
+                }
+            } catch (...) {
+                err = std::current_exception();
+            }
+            each(i, std::move(r), err);
+            specs[i] = {};  // release the converted inputs on the worker threads too
+            topos[i] = {};
+        });
+    });
+}
+
+// The same, collecting every outcome.
+struct Outcome {
+    wavesched::PlannerResult result;
+    std::exception_ptr error;
+};
+
+inline std::vector<Outcome> plan_workloads(
+    const std::vector<std::pair<const wavesched::WorkloadSpec*, const wavesched::ClusterTopology*>>& problems,
+    const wavesched::PlannerOptions& opt = {}, int threads = 0) {
+    std::vector<Outcome> out(problems.size());
+    plan_workloads_each(problems, opt, threads, [&](std::size_t i, wavesched::PlannerResult&& r, std::exception_ptr e) {
+        out[i].result = std::move(r);
+        out[i].error = e;
+    });
+    return out;
 }
 
 }  // namespace wavesched_gpu

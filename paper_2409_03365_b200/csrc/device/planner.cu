@@ -17,6 +17,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <numeric>
 #include <string>
 #include <thread>
@@ -256,6 +257,7 @@ struct ws_ctx {
     cudaStream_t drain_stream = nullptr;
     long long last_retry = 0;   // soft-cap overflows of the last planning call (all re-planned)
     bool tiny_soft = false;     // $WSGPU_TINY_SOFT_CAPS: soft caps below every plan (tests of the retry pass)
+    bool small_path = true;     // $WSGPU_SMALL_PATH=0: small host batches take the staged path
     // measured (100k sweep, ms): one compute stream: 1 chunk 27.8, 2: 27.4, 4: 32.0 (each
     // chunk's k_sched + k_place launch tail outweighs the hidden copies); two compute
     // streams (consecutive chunks fill each other's tails) with completion-order D2H:
@@ -269,6 +271,11 @@ struct ws_ctx {
     bool pdl = true;
     std::vector<double> host_weights{1, 3, 3, 1};  // $WSGPU_HOST_WEIGHTS: relative chunk sizes (sets the chunk count)
     ws_plan_result* res_out() { return d_results ? d_results : results.as<ws_plan_result>(); }
+    // small host batches stage their zeroed counters with the batch (one H2D copy)
+    unsigned long long* small_counters = nullptr;
+    unsigned long long* counters_dev() { return small_counters ? small_counters : counters.as<unsigned long long>(); }
+    uint8_t* small_host = nullptr;  // page-locked staging of the small-batch path
+    size_t small_host_n = 0;
     uint8_t* arena_out() { return d_arena ? d_arena : arena.as<uint8_t>(); }
     uint64_t cap_out() const { return d_arena ? d_cap : arena_cap; }
 };
@@ -296,6 +303,34 @@ int fail(ws_ctx* c, const std::string& what, cudaError_t e = cudaSuccess) {
         cudaError_t e_ = (call);                            \
         if (e_ != cudaSuccess) return fail(ctx, #call, e_); \
     } while (0)
+
+// The dynamic shared-memory opt-in of every kernel, set ONCE per device to the
+// most a block may take.  The attribute is process-wide state of the function:
+// setting it per launch to that launch's size would let a concurrent context
+// (another host thread) lower it between another launch's set and its launch.
+template <typename K>
+cudaError_t smem_opt_in(K* fn) {
+    cudaFuncAttributes a{};
+    cudaError_t e = cudaFuncGetAttributes(&a, fn);
+    if (e != cudaSuccess) return e;
+    return cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                kSmemLimit - static_cast<int>(a.sharedSizeBytes));
+}
+
+cudaError_t smem_opt_in_all(int device) {
+    static std::once_flag once[64];
+    static cudaError_t status[64] = {};
+    if (device < 0 || device >= 64) return cudaErrorInvalidDevice;
+    std::call_once(once[device], [&] {
+        cudaError_t e = smem_opt_in(k_sched);
+        if (e == cudaSuccess) e = smem_opt_in(k_sched_scoped);
+        if (e == cudaSuccess) e = smem_opt_in(k_place<true>);
+        if (e == cudaSuccess) e = smem_opt_in(k_place<false>);
+        if (e == cudaSuccess) e = smem_opt_in(k_sim);
+        status[device] = e;
+    });
+    return status[device];
+}
 
 // rebase every section pointer of a host batch into device memory at `dbase`
 ws_batch rebase(const ws_batch& h, const void* hbase, char* dbase) {
@@ -371,10 +406,6 @@ int launch_pair(ws_ctx* ctx, cudaStream_t st, const LaunchCaps& lc, const FitOut
     S.M_cap = lc.M;
     S.results = ctx->res_out();
     if (kSchedWarps * S.SL.bytes > kSmemLimit) return fail(ctx, "k_sched working set exceeds shared memory");
-    CK(cudaFuncSetAttribute(k_sched, cudaFuncAttributeMaxDynamicSharedMemorySize, kSchedWarps * S.SL.bytes));
-    if (lc.scoped)
-        CK(cudaFuncSetAttribute(k_sched_scoped, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                kSchedWarps * S.SL.bytes));
 
     PlaceArgs P{};
     P.B = B;
@@ -388,7 +419,7 @@ int launch_pair(ws_ctx* ctx, cudaStream_t st, const LaunchCaps& lc, const FitOut
     P.rec_by_slot = by_slot ? 1 : 0;
     P.results = ctx->res_out();
     P.arena = ctx->arena_out();
-    P.arena_top = ctx->top_ptr ? ctx->top_ptr : ctx->counters.as<unsigned long long>();
+    P.arena_top = ctx->top_ptr ? ctx->top_ptr : ctx->counters_dev();
     P.arena_cap = ctx->top_ptr ? ctx->top_cap : ctx->cap_out();
     const bool snap_ok = ctx->snap_stride >= static_cast<long long>(lc.pl.W) * (lc.pl.N + lc.pl.G);
     P.snap = ctx->snap.as<double>();
@@ -399,7 +430,6 @@ int launch_pair(ws_ctx* ctx, cudaStream_t st, const LaunchCaps& lc, const FitOut
     // measured (100k sweep, ms): snapshots cut decoupled-sequential 9.8 -> 7.9 and
     // distmm-mt 81 -> 47, while the extra code costs wavefront 10.6 -> 11.0
     auto* kplace = (lc.baseline || ctx->force_snap) ? k_place<true> : k_place<false>;
-    CK(cudaFuncSetAttribute(kplace, cudaFuncAttributeMaxDynamicSharedMemorySize, kPlaceWarps * P.PL.bytes));
 
     chunks = std::max(1, std::min(chunks, kMaxChunks));
     if (n_ids || n < 4096) chunks = 1;  // retry pass / small batches: no pipelining
@@ -475,6 +505,7 @@ int ws_ctx_create(int device, ws_ctx** out) {
     for (auto& e : c->cev) ok = ok && cudaEventCreateWithFlags(&e, cudaEventDisableTiming) == cudaSuccess;
     ok = ok && cudaEventCreateWithFlags(&c->order_ev, cudaEventDisableTiming) == cudaSuccess;
     ok = ok && cudaEventCreateWithFlags(&c->drain_ev, cudaEventDisableTiming) == cudaSuccess;
+    ok = ok && smem_opt_in_all(device) == cudaSuccess;
     if (!ok) {
         cudaGetLastError();
         ws_ctx_destroy(c);
@@ -501,6 +532,7 @@ int ws_ctx_create(int device, ws_ctx** out) {
     if (const char* env = std::getenv("WSGPU_PDL")) c->pdl = std::atoi(env) != 0;
     if (const char* env = std::getenv("WSGPU_HOST_STREAMS")) c->host_streams = std::max(1, std::min(2, std::atoi(env)));
     if (const char* env = std::getenv("WSGPU_TINY_SOFT_CAPS")) c->tiny_soft = std::atoi(env) != 0;
+    if (const char* env = std::getenv("WSGPU_SMALL_PATH")) c->small_path = std::atoi(env) != 0;
     *out = c;
     return 0;
 }
@@ -517,6 +549,7 @@ void ws_ctx_destroy(ws_ctx* c) {
         if (s) cudaStreamDestroy(s);
     if (c->host_tops) cudaFreeHost(c->host_tops);
     if (c->order_pinned) cudaFreeHost(c->order_pinned);
+    if (c->small_host) cudaFreeHost(c->small_host);
     delete c;  // DevBuf destructors free device memory on c->device (guarded)
 }
 
@@ -573,7 +606,7 @@ int prepare_plan(ws_ctx* ctx, FitOut& fo) {
             return fail(ctx, "cudaMemset snapshot bits");
         ctx->snap_stride = stride;
     }
-    auto* counters = ctx->counters.as<unsigned long long>();
+    auto* counters = ctx->counters_dev();
     fo.err = ctx->fit_err.as<int32_t>();
     fo.err_a = ctx->fit_a.as<int32_t>();
     fo.err_b = ctx->fit_b.as<int32_t>();
@@ -654,6 +687,7 @@ int ws_stage_batch(ws_ctx* ctx, const ws_batch* in, void* stream) {
         return fail(ctx, "cudaMalloc batch");
     CK(cudaMemcpyAsync(ctx->blob.p, in->blob, in->blob_bytes, cudaMemcpyHostToDevice, st));
     ctx->dview = rebase(*in, in->blob, ctx->blob.as<char>());
+    ctx->small_counters = nullptr;
     ctx->drain_pending = false;  // results of an earlier staged batch are superseded
     ctx->caps = batch_caps(in->plans, P, false, ctx->tiny_soft);
     ctx->caps_hard = batch_caps(in->plans, P, true);
@@ -698,7 +732,8 @@ int ws_plan_staged(ws_ctx* ctx, void* stream) {
     ctx->last_retry = 0;
     FitOut fo;
     if (prepare_plan(ctx, fo)) return 1;
-    auto* counters = ctx->counters.as<unsigned long long>();  // [0] arena top [1] overflow top [2] retry count
+    ctx->small_counters = nullptr;
+    auto* counters = ctx->counters_dev();  // [0] arena top [1] overflow top [2] retry count
     CK(cudaMemsetAsync(counters, 0, 64, st));
 
     CK(cudaEventRecord(ctx->ev[0], st));
@@ -752,7 +787,7 @@ int ws_fetch_results(ws_ctx* ctx, ws_plan_result* results, uint8_t* arena, uint6
     const bool one_sync = ctx->arena_cap <= kOneSyncArena && ctx->arena_cap <= arena_cap;
     if (P) CK(cudaMemcpyAsync(results, ctx->results.p, sizeof(ws_plan_result) * P, cudaMemcpyDeviceToHost, st));
     unsigned long long* htop = ctx->host_tops + kHtFetch;  // page-locked
-    CK(cudaMemcpyAsync(htop, ctx->counters.p, sizeof(top), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(htop, ctx->counters_dev(), sizeof(top), cudaMemcpyDeviceToHost, st));
     if (one_sync && ctx->arena_cap) CK(cudaMemcpyAsync(arena, ctx->arena.p, ctx->arena_cap, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     top = *htop;
@@ -773,6 +808,82 @@ int ws_fetch_results(ws_ctx* ctx, ws_plan_result* results, uint8_t* arena, uint6
 
 extern "C" uint64_t wsi_arena_bound_plans(const ws_plan_rec* plans, int n);
 
+namespace {
+constexpr int kSmallBatch = 64;  // host batches planned by plan_small
+
+// Small host batches (single-plan latency, concurrent drop-in callers): the
+// batch, its launch order and zeroed counters go to the device in ONE copy,
+// the kernels run with the hard record caps (no soft-cap overflow, so no
+// retry pass and no host round trip for its count), and the results come back
+// in one or two copies: 6-7 CUDA calls per call instead of ~25 (the CUDA
+// driver serializes concurrent callers' API calls, so their count bounds the
+// multi-threaded drop-in throughput).
+int plan_small(ws_ctx* ctx, const ws_batch* in, ws_plan_result* results, uint8_t* arena, uint64_t arena_cap,
+               uint64_t* arena_used, cudaStream_t st) {
+    const int P = in->n_plans;
+    const uint64_t o_order = 256, o_blob = (o_order + 4ull * P + 255) & ~255ull;
+    const uint64_t bytes = o_blob + in->blob_bytes;
+    if (ctx->small_host_n < bytes) {
+        if (ctx->small_host) cudaFreeHost(ctx->small_host);
+        ctx->small_host = nullptr;
+        ctx->small_host_n = 0;
+        const size_t want = std::max<size_t>(bytes, 64 << 10);
+        if (cudaMallocHost(reinterpret_cast<void**>(&ctx->small_host), want) != cudaSuccess)
+            return fail(ctx, "cudaMallocHost small-batch staging");
+        ctx->small_host_n = want;
+    }
+    if (!ctx->blob.ensure(bytes + 256)) return fail(ctx, "cudaMalloc batch");
+    uint8_t* h = ctx->small_host;
+    std::memset(h, 0, 256);  // counters
+    auto* order = reinterpret_cast<int32_t*>(h + o_order);
+    for (int p = 0; p < P; ++p) order[p] = p;
+    std::sort(order, order + P, [&](int a, int b) {  // LPT, stable by index
+        const int ka = lpt_key(in->plans[a]), kb = lpt_key(in->plans[b]);
+        return ka != kb ? ka < kb : a < b;
+    });
+    std::memcpy(h + o_blob, in->blob, in->blob_bytes);
+    char* d = ctx->blob.as<char>();
+    CK(cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, st));
+    ctx->dview = rebase(*in, in->blob, d + o_blob);
+    ctx->drain_pending = false;
+    ctx->last_retry = 0;
+    ctx->caps = batch_caps(in->plans, P, true);
+    ctx->caps_hard = ctx->caps;
+    ctx->arena_cap = ws_arena_bound(in);
+    ctx->sim_cap = ws_sim_arena_bound(in);
+    ctx->sim_valid = false;
+    ctx->small_counters = reinterpret_cast<unsigned long long*>(d);
+    FitOut fo;
+    if (prepare_plan(ctx, fo)) return 1;
+    ctx->launches = 0;
+    const ws_batch& B = ctx->dview;
+    if (B.n_modules > 0) {
+        launch_fit(B, fo, 0, B.n_modules, st);
+        ctx->launches++;
+    }
+    if (launch_pair(ctx, st, ctx->caps, fo, reinterpret_cast<const int32_t*>(d + o_order), nullptr, P, false,
+                    ctx->recs.as<char>(), ctx->flows.as<uint64_t>(), nullptr, 1, ctx->pdl && B.n_modules > 0))
+        return 1;
+    ctx->staged_events = false;
+    ctx->records_on_device = true;
+    const bool one_sync = ctx->arena_cap <= kOneSyncArena && ctx->arena_cap <= arena_cap;
+    if (P) CK(cudaMemcpyAsync(results, ctx->results.p, sizeof(ws_plan_result) * P, cudaMemcpyDeviceToHost, st));
+    if (one_sync) CK(cudaMemcpyAsync(arena, ctx->arena.p, ctx->arena_cap, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    uint64_t top = 0;  // records are bump-allocated: the arena top is the furthest record end
+    for (int p = 0; p < P; ++p)
+        if (results[p].status == WS_STATUS_OK) top = std::max<uint64_t>(top, results[p].offset + results[p].size);
+    if (top > arena_cap) return fail(ctx, "ws_plan_batch_host: arena buffer too small");
+    if (!one_sync && top) {
+        CK(cudaMemcpyAsync(arena, ctx->arena.p, top, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+    }
+    ctx->kernel_ms[0] = ctx->kernel_ms[1] = ctx->kernel_ms[2] = 0;  // not timed on this path
+    *arena_used = top;
+    return 0;
+}
+}  // namespace
+
 // Host batch in, host results out.  Batches of >= 2 x 4096 plans run as a
 // pipeline over chunks of plans (default sizes 1:3:3:1, $WSGPU_HOST_WEIGHTS /
 // $WSGPU_HOST_CHUNKS): the H2D copy of chunk c+1 (its byte ranges of every SoA
@@ -788,6 +899,8 @@ int ws_plan_batch_host(ws_ctx* ctx, const ws_batch* in, ws_plan_result* results,
     DevGuard dg_(ctx->device);
     cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
     const int P = in->n_plans;
+    if (P > 0 && P <= kSmallBatch && in->blob && ctx->small_path)
+        return plan_small(ctx, in, results, arena, arena_cap, arena_used, st);
     int C = ctx->host_chunks;
     C = std::max(1, std::min({C, kMaxHostChunks, P / 4096}));
     if (C == 1 || !in->blob) {
@@ -846,9 +959,10 @@ int ws_plan_batch_host(ws_ctx* ctx, const ws_batch* in, ws_plan_result* results,
     ctx->sim_cap = sim_total + 4096;  // == ws_sim_arena_bound(in)
     ctx->arena_cap = abase[C];
     if (ctx->arena_cap > arena_cap) return fail(ctx, "ws_plan_batch_host: arena buffer too small");
+    ctx->small_counters = nullptr;
     FitOut fo;
     if (prepare_plan(ctx, fo)) return 1;
-    auto* counters = ctx->counters.as<unsigned long long>();
+    auto* counters = ctx->counters_dev();
     auto* tops = ctx->chunk_tops.as<unsigned long long>();
     cudaStream_t sh = ctx->stream2, sd = ctx->stream3;
     cudaEvent_t* h2d = ctx->cev;               // [0, C)
@@ -1077,7 +1191,6 @@ int ws_simulate_staged(ws_ctx* ctx, const ws_sim_opts* opts, void* stream) {
     A.arena_cap = ctx->sim_cap;
     const int smem = kSimWarps * A.SL.bytes;
     if (smem > kSmemLimit) return fail(ctx, "ws_simulate_staged: per-warp working set exceeds shared memory");
-    CK(cudaFuncSetAttribute(k_sim, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     CK(cudaMemsetAsync(A.arena_top, 0, 8, st));
     CK(cudaEventRecord(ctx->sev[0], st));
     if (P > 0) k_sim<<<(P + kSimWarps - 1) / kSimWarps, 32 * kSimWarps, smem, st>>>(A);

@@ -7,6 +7,7 @@
 #include <cstring>
 
 #include "bounds.h"
+#include "wsgpu/decode_impl.hpp"
 #include "wsgpu/planner.hpp"
 
 namespace wsgpu {
@@ -218,132 +219,10 @@ PlannerResult decode_scoped(const Problem& prob, const ws_plan_result& r, const 
 PlannerResult decode_result(const Problem& prob, const ws_plan_result& r, const std::uint8_t* arena,
                             bool build_graph) {
     if (r.status != WS_STATUS_OK) throw_result_error(prob, r);
-    const WorkloadSpec& spec = *prob.spec;
-    const Sections s = sections_of(r, arena);
-    if (r.n_scopes > 0) return decode_scoped(prob, r, s);
-    std::vector<const ModuleDecl*> mods;
-    for (const auto& kv : spec.modules) mods.push_back(&kv.second);
-    const int K = r.n_metaops;
-    auto mid = [](int k) { return "m" + std::to_string(k); };
-
-    // tasks routing through each module (graph.hpp:101-121)
-    std::map<std::string, std::set<std::string>> tasks_of;
-    for (const TaskDecl& t : spec.tasks)
-        for (const FlowStep& st : t.flow)
-            for (const FlowBranch& br : st)
-                for (const std::string& m : br) tasks_of[m].insert(t.id);
-
+    if (r.n_scopes > 0) return decode_scoped(prob, r, sections_of(r, arena));
     PlannerResult res;
-    for (int k = 0; k < K; ++k) {
-        const ws_out_metaop& o = s.mo[k];
-        const ModuleDecl& md = *mods[o.module];
-        MetaOp m;
-        m.id = mid(k);
-        for (int l = 0; l < o.length; ++l) m.member_ops.push_back(md.kind + "." + std::to_string(o.first_layer + l));
-        m.length = o.length;
-        m.kind = md.kind;
-        m.input = md.input;
-        m.global_batch = md.input.batch;
-        m.tp_degree = md.tp_degree;
-        m.level = o.level;
-        m.param_group = md.param_group;
-        m.task_ids = tasks_of[md.kind];
-        std::vector<CurvePiece> pieces;
-        for (int i = 0; i < o.piece_count; ++i) {
-            const ws_out_piece& p = s.pc[o.piece_begin + i];
-            pieces.push_back({p.n_lo, p.n_hi, p.alpha, p.beta_c, p.beta_w});
-        }
-        res.curves[m.id] = ScalingCurve::from_pieces(pieces, md.comm_proxy, md.flops_proxy);
-        res.meta.metaops.emplace(m.id, std::move(m));
-    }
-    for (int e = 0; e < r.n_edges; ++e) res.meta.edges.insert({mid(s.ed[e].from), mid(s.ed[e].to)});
-    int n_meta_levels = r.n_levels;  // the baselines carry MetaOp levels but no level plans
-    for (const auto& [id, m] : res.meta.metaops) n_meta_levels = std::max(n_meta_levels, m.level + 1);
-    res.meta.levels.assign(n_meta_levels, {});
-    for (const auto& [id, m] : res.meta.metaops) res.meta.levels[m.level].push_back(id);
-
-    if (build_graph) {
-        for (const auto& [id, m] : res.meta.metaops) {
-            for (const std::string& op : m.member_ops) {
-                Operator o;
-                o.id = op;
-                o.kind = m.kind;
-                o.task_ids = m.task_ids;
-                o.input = m.input;
-                o.tp_degree = m.tp_degree;
-                o.param_group = m.param_group;
-                res.graph.operators.emplace(op, std::move(o));
-            }
-            for (std::size_t i = 1; i < m.member_ops.size(); ++i)
-                res.graph.edges.insert({m.member_ops[i - 1], m.member_ops[i]});
-        }
-        for (const auto& [a, b] : res.meta.edges)
-            res.graph.edges.insert({res.meta.metaops.at(a).member_ops.back(), res.meta.metaops.at(b).member_ops.front()});
-    }
-
-    for (int l = 0; l < r.n_levels; ++l) {
-        AllocationPlan ap;
-        ap.level = l;
-        ap.c_star = s.lv[l].c_star;
-        for (const std::string& id : res.meta.levels[l]) {
-            const ws_out_metaop& o = s.mo[std::stoi(id.substr(1))];
-            TuplePair tp;
-            tp.upper = {id, o.upper_n, -1.0, o.upper_l};
-            if (o.lower_l > 0) tp.lower = AslTuple{id, o.lower_n, -1.0, o.lower_l};
-            ap.tuples.emplace(id, tp);
-        }
-        res.level_plans.push_back(std::move(ap));
-        res.schedule.level_boundaries.push_back(s.lv[l].first_wave);
-    }
-    ExecutionPlan& plan = res.plan;
-    for (int w = 0; w < r.n_waves; ++w) {
-        Wave wave;
-        wave.index = w;
-        wave.level = s.wv[w].level;
-        wave.start = s.wv[w].start;
-        wave.duration = s.wv[w].duration;
-        for (int i = 0; i < s.wv[w].n_entries; ++i) {
-            const ws_out_entry& e = s.en[s.wv[w].entry_begin + i];
-            wave.entries.push_back({mid(e.metaop), e.n, e.layers, e.span});
-            if (e.devmask) plan.devices[{w, mid(e.metaop)}] = device_list(prob, e);  // 0: not placed
-        }
-        res.schedule.waves.push_back(std::move(wave));
-    }
-    res.schedule.end_time = r.end_time;
-    res.lower_bound = r.lower_bound;
-    res.predicted_makespan = r.end_time;
-
-    plan.strategy = prob.opt.strategy == WS_STRATEGY_DECOUPLED_SEQUENTIAL ? "decoupled-sequential" : "wavefront";
-    plan.topo = *prob.topo;
-    for (const auto& [id, m] : res.meta.metaops) {  // build_entities (planner.hpp:99-122)
-        const ModuleDecl& md = spec.module(m.kind);
-        PlanEntity e;
-        e.id = id;
-        e.kind = m.kind;
-        e.length = m.length;
-        e.level = m.level;
-        e.tp_degree = m.tp_degree;
-        e.global_batch = m.global_batch;
-        e.batch_fraction = 1.0;
-        e.param_group = m.length == md.layers ? md.param_group : "";
-        e.param_bytes = static_cast<std::uint64_t>(static_cast<double>(md.param_bytes) * m.length / md.layers);
-        e.act_bytes = md.act_bytes;
-        e.out_bytes = md.out_bytes;
-        e.w = md.flops_proxy;
-        e.c = md.comm_proxy;
-        e.task_ids = m.task_ids;
-        plan.entities[id] = std::move(e);
-    }
-    plan.curves = res.curves;
-    plan.deps = res.meta.edges;
-    plan.schedule = res.schedule;
-    plan.lower_bound = res.lower_bound;
-    plan.grad_opt_multiplier = prob.opt.grad_opt_multiplier;
-    static const char* kModes[3] = {"copy", "intra-island", "inter-island"};
-    for (int f = 0; f < r.n_flows; ++f) {
-        const ws_out_flow& x = s.fl[f];
-        plan.flows.push_back({x.from_wave, mid(x.from_metaop), x.to_wave, mid(x.to_metaop), x.volume, kModes[x.mode]});
-    }
+    detail::decode_into(*prob.spec, *prob.topo, prob.opt.strategy, prob.opt.grad_opt_multiplier, r, arena,
+                        build_graph, res);
     return res;
 }
 

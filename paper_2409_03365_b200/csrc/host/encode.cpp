@@ -9,9 +9,12 @@
 #include <cuda_runtime_api.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstring>
+#include <thread>
 
+#include "internal.hpp"
 #include "wsgpu/planner.hpp"
 
 namespace wsgpu {
@@ -206,14 +209,12 @@ T* carve(std::uint8_t* base, std::size_t& off, std::size_t count) {
 
 }  // namespace
 
-EncodedBatch encode_batch(const std::vector<Problem>& problems, bool pinned) {
-    EncodedBatch eb;
+namespace {
+// per-problem host preparation (validation, name resolution, ranks); spread
+// over host threads for large batches (problems are independent)
+void prepare_all(const std::vector<Problem>& problems, std::vector<PlanScratch>& ps, EncodedBatch& eb, int threads) {
     const std::size_t P = problems.size();
-    std::vector<PlanScratch> ps(P);
-    eb.host_error_class.assign(P, "");
-    eb.host_error_msg.assign(P, "");
-    std::size_t nm = 0, nt = 0, ntok = 0, nd = 0, npc = 0, npt = 0, nbp = 0, nname = 0;
-    for (std::size_t i = 0; i < P; ++i) {
+    auto one = [&](std::size_t i) {
         try {
             prepare(problems[i], ps[i]);
         } catch (const CyclicWorkload& e) {
@@ -230,8 +231,60 @@ EncodedBatch encode_batch(const std::vector<Problem>& problems, bool pinned) {
         if (!eb.host_error_class[i].empty()) {
             ps[i] = PlanScratch{};
             ps[i].ok = false;
-            continue;
         }
+    };
+    if (threads <= 1 || P < 2048) {
+        for (std::size_t i = 0; i < P; ++i) one(i);
+        return;
+    }
+    std::atomic<std::size_t> next{0};
+    std::vector<std::thread> pool;
+    for (int t = 0; t < threads; ++t)
+        pool.emplace_back([&] {
+            for (std::size_t i; (i = next.fetch_add(256)) < P;)
+                for (std::size_t j = i; j < std::min(P, i + 256); ++j) one(j);
+        });
+    for (auto& th : pool) th.join();
+}
+}  // namespace
+
+namespace detail {
+bool HostBuffer::ensure(std::size_t bytes) {
+    if (bytes <= cap && p) return true;
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    const std::size_t want = std::max<std::size_t>({bytes, 2 * cap, std::size_t(64) << 10});
+    cap = 0;
+    if (cudaMallocHost(reinterpret_cast<void**>(&p), want) != cudaSuccess) {
+        cudaGetLastError();
+        p = nullptr;
+        return false;
+    }
+    cap = want;
+    return true;
+}
+
+HostBuffer::~HostBuffer() {
+    if (p) cudaFreeHost(p);
+}
+}  // namespace detail
+
+EncodedBatch encode_batch(const std::vector<Problem>& problems, bool pinned) {
+    return detail::encode_batch_with(problems, pinned, nullptr, 1);
+}
+
+namespace detail {
+
+EncodedBatch encode_batch_with(const std::vector<Problem>& problems, bool pinned, HostBuffer* reuse, int threads) {
+    EncodedBatch eb;
+    const std::size_t P = problems.size();
+    std::vector<PlanScratch> ps(P);
+    eb.host_error_class.assign(P, "");
+    eb.host_error_msg.assign(P, "");
+    prepare_all(problems, ps, eb, threads);
+    std::size_t nm = 0, nt = 0, ntok = 0, nd = 0, npc = 0, npt = 0, nbp = 0, nname = 0;
+    for (std::size_t i = 0; i < P; ++i) {
+        if (!ps[i].ok) continue;
         const PlanScratch& s = ps[i];
         nm += s.mods.size();
         nt += s.task_tokens.size();
@@ -251,7 +304,11 @@ EncodedBatch encode_batch(const std::vector<Problem>& problems, bool pinned) {
     total += align16(4 * npt) + align16(8 * npt) + align16(4 * nbp) + align16(nname) + 64;
 
     std::uint8_t* raw = nullptr;
-    if (pinned && cudaMallocHost(reinterpret_cast<void**>(&raw), total) == cudaSuccess) {
+    if (reuse && reuse->ensure(total)) {  // caller-owned page-locked buffer, reused across calls
+        raw = reuse->p;
+        eb.pinned = true;
+        eb.buffer = std::shared_ptr<std::uint8_t>(raw, [](std::uint8_t*) {});
+    } else if (pinned && cudaMallocHost(reinterpret_cast<void**>(&raw), total) == cudaSuccess) {
         eb.pinned = true;
         eb.buffer = std::shared_ptr<std::uint8_t>(raw, [](std::uint8_t* p) { cudaFreeHost(p); });
     } else {
@@ -412,4 +469,5 @@ EncodedBatch encode_batch(const std::vector<Problem>& problems, bool pinned) {
     return eb;
 }
 
+}  // namespace detail
 }  // namespace wsgpu

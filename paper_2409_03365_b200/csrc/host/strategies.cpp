@@ -82,9 +82,9 @@ Evaluated plan_and_simulate(const std::vector<const WorkloadSpec*>& specs, const
         }
     }
     if (ev.probs.empty()) return ev;
-    std::unique_lock<std::mutex> lock;
-    ws_ctx* ctx = detail::default_ctx_locked(lock);
-    ev.planned = detail::plan_on(ctx, ev.probs);
+    detail::CtxLease lease;
+    ws_ctx* ctx = lease.ctx();
+    ev.planned = detail::plan_on(lease, ev.probs);
     // evaluate the host records: one staging of batch + records, one k_sim launch
     EncodedBatch eb = encode_batch(ev.probs, true);
     const ws_sim_opts so{2.0, 0, 0};  // SimulatorOptions defaults (simulate.hpp:69-73)
@@ -179,9 +179,8 @@ ExecutionPlan plan_for_strategy(const std::string& strategy, const WorkloadSpec&
         known = false;
         p.opt.strategy = WS_STRATEGY_DECOUPLED_SEQUENTIAL;
     }
-    std::unique_lock<std::mutex> lock;
-    ws_ctx* ctx = detail::default_ctx_locked(lock);
-    detail::Planned r = detail::plan_on(ctx, {p});
+    detail::CtxLease lease;
+    detail::Planned r = detail::plan_on(lease, {p});
     if (!known) {
         if (r.res[0].status != WS_STATUS_OK && base_stage_error(r.res[0].err_code)) throw_result_error(p, r.res[0]);
         throw ParseError("unknown strategy '" + strategy + "'");

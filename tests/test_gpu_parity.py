@@ -128,6 +128,32 @@ def test_gpu_dropin_plan_workload(golden_cases):
         ws.plan_workload(c["workload"], c["topology"])
 
 
+def test_gpu_dropin_concurrent_callers(golden_cases):
+    """The drop-in is reentrant: 8 host threads planning at once
+    (each on its own pooled context) get the reference's plan texts."""
+    import threading
+
+    import paper_2409_03365_b200 as ws
+    cases = [c for c in golden_cases if c["name"].startswith(("config/", "sweep-bt/", "suite/", "fuzz/"))][:96]
+    got = [None] * len(cases)
+
+    def work(t):
+        for i in range(t, len(cases), 8):
+            c = cases[i]
+            try:
+                got[i] = ws.plan_workload(c["workload"], c["topology"], **c["options"])
+            except ws.PlannerError as e:
+                got[i] = f"error {type(e).__name__}: {e}\n"
+
+    th = [threading.Thread(target=work, args=(t,)) for t in range(8)]
+    for x in th:
+        x.start()
+    for x in th:
+        x.join()
+    bad = [c["name"] for c, g in zip(cases, got) if g != c["expected"]]
+    assert not bad, bad[:10]
+
+
 def test_gpu_kernel_timing_reported(planner, monkeypatch):
     """With programmatic dependent launch (default) k_sched starts behind k_fit
     and the fit is reported inside k_sched's time; with WSGPU_PDL=0 each kernel

@@ -28,3 +28,21 @@ def test_reference_acceptance_suite_passes_on_gpu_planner():
     r = _run("acceptance_gpu", 1200)
     assert r.returncode == 0, r.stdout[-3000:]
     assert r.stdout.count("[PASS] criterion") == 10
+
+
+def test_dropin_reference_types_concurrent_threads_and_batch():
+    """wavesched_gpu::plan_workload (reference types in, PlannerResult out) from
+    many host threads at once and wavesched_gpu::plan_workloads (one batch,
+    parallel decode) give the reference planner's plans (oracle/ref/dropin_bench.cpp
+    checks the 4 BASELINE configs and every 97th sweep plan)."""
+    import json
+    exe = REF / "dropin_bench"
+    if not exe.exists():
+        pytest.skip(f"{exe} not built")
+    r = subprocess.run([str(exe), "20", "3000", "8"], cwd=REF, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    d = json.loads(r.stdout.strip().splitlines()[-1])
+    assert all(v["identical_plan"] for v in d["latency_ms"].values())
+    t = d["throughput"]
+    assert t["batched_spot_mismatches"] == 0
+    assert len(set(t["errors"])) == 1  # the same infeasible plans on every path
