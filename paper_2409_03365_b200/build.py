@@ -51,7 +51,7 @@ def _stale(target: Path, deps: list[Path]) -> bool:
 
 
 def build(verbose: bool = False, force: bool = False, defines: list[str] | None = None,
-          name: str | None = None) -> Path:
+          name: str | None = None, extra_nvcc: list[str] | None = None) -> Path:
     """Compile host + device sources and link libwsgpu.so; returns its path.
     `defines`/`name` build a tuning variant (e.g. ["WS_PLACE_MINB=6"], "libwsgpu_v6.so")
     with its own object directory."""
@@ -69,7 +69,8 @@ def build(verbose: bool = False, force: bool = False, defines: list[str] | None 
     for src in sorted((CSRC / "device").glob("*.cu")):
         obj = build_dir / (src.stem + ".cu.o")
         if force or _stale(obj, [src] + headers):
-            _run([NVCC, *NVCC_FLAGS, *dflags, "-Xptxas", "-v" if verbose else "-O3", "-c", str(src), "-o", str(obj)], verbose)
+            _run([NVCC, *NVCC_FLAGS, *dflags, *(extra_nvcc or []), "-Xptxas", "-v" if verbose else "-O3", "-c", str(src),
+                  "-o", str(obj)], verbose)
         objs.append(obj)
     if force or _stale(libname, objs):
         _run([NVCC, *ARCH, "-shared", "-o", str(libname), *map(str, objs), "-cudart", "static",

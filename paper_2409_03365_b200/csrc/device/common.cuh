@@ -71,6 +71,7 @@ __host__ __device__ __forceinline__ bool dec_less(int a, int b) {
     const int da = dec_digits(a), db = dec_digits(b);
     if (da == db) return a < b;
     int p = 1;
+    #pragma unroll 1
     for (int i = da < db ? db - da : da - db; i; --i) p *= 10;
     return da < db ? a <= b / p : a / p < b;
 }
@@ -84,6 +85,7 @@ __host__ __device__ __forceinline__ bool scoped_less(int a, int ta, int b, int t
     const int da = dec_digits(a), db = dec_digits(b);
     if (da == db) return a < b;
     int p = 1;
+    #pragma unroll 1
     for (int i = da < db ? db - da : da - db; i; --i) p *= 10;
     if (da < db) {
         const int pre = b / p;
@@ -103,11 +105,13 @@ __host__ __device__ __forceinline__ bool scoped_less(int a, int ta, int b, int t
 __host__ __device__ __forceinline__ int island_matches(uint64_t A, uint64_t B, int M, int P, const uint64_t* islm,
                                                        const uint64_t* lowm, int n_isl) {
     int same = 0;
+    #pragma unroll 1
     for (int a = 0; a < n_isl; ++a) {
         const int ca = popc64(A & islm[a]), cb = popc64(B & islm[a]);
         if (!ca || !cb) continue;
         const int sa = popc64(A & lowm[a]), sb = popc64(B & lowm[a]);
         int q = sa > sb + cb ? (sa - sb - cb) / P : 0;
+        #pragma unroll 1
         for (int off = q * P + sb; off < sa + ca && off < M; off += P) {
             const int lo = sa > off ? sa : off;
             const int hi = (sa + ca) < (off + cb) ? (sa + ca) : (off + cb);
@@ -155,11 +159,13 @@ __host__ __device__ void ls_adjust_heap(int* a, int hole, int len, int value, Cm
 template <typename Cmp>
 __host__ __device__ void ls_heap_sort(int* a, int len, Cmp& comp) {  // __partial_sort(first, last, last)
     if (len >= 2) {
+        #pragma unroll 1
         for (int parent = (len - 2) / 2;; --parent) {
             ls_adjust_heap(a, parent, len, a[parent], comp);
             if (parent == 0) break;
         }
     }
+    #pragma unroll 1
     for (int last = len; last > 1;) {
         --last;
         const int v = a[last];
@@ -171,9 +177,11 @@ __host__ __device__ void ls_heap_sort(int* a, int len, Cmp& comp) {  // __partia
 template <typename Cmp>
 __host__ __device__ void ls_insertion_sort(int* a, int lo, int hi, Cmp& comp) {
     if (lo == hi) return;
+    #pragma unroll 1
     for (int i = lo + 1; i < hi; ++i) {
         const int v = a[i];
         if (comp(v, a[lo])) {
+            #pragma unroll 1
             for (int j = i; j > lo; --j) a[j] = a[j - 1];
             a[lo] = v;
         } else {
@@ -243,6 +251,7 @@ __host__ __device__ void ls_sort(int* a, int n, Cmp& comp) {
     // __final_insertion_sort
     if (n > 16) {
         ls_insertion_sort(a, 0, 16, comp);
+        #pragma unroll 1
         for (int i = 16; i < n; ++i) {
             const int v = a[i];
             int j = i;

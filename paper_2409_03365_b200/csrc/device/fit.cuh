@@ -39,6 +39,7 @@ __device__ __forceinline__ double piece_value(const DPiece& p, double c, double 
 
 // ScalingCurve::locate (scaling.hpp:149-154)
 __device__ __forceinline__ int locate_piece(const DPiece* p, int np, double n) {
+    #pragma unroll 1
     for (int i = 0; i < np; ++i)
         if (n <= p[i].hi + 1e-9) return i;
     return np - 1;
@@ -104,6 +105,7 @@ __global__ void __launch_bounds__(128) k_fit(ws_batch B, FitOut out, int m_begin
             }
             DPiece raw[kMaxDeclared];
             int order[kMaxDeclared];
+            #pragma unroll 1
             for (int i = 0; i < nd; ++i) {
                 const double* q = B.truth + 5 * (B.mod_truth_off[m] + i);
                 DPiece p{q[0], q[1], q[2], q[3], q[4]};
@@ -116,15 +118,18 @@ __global__ void __launch_bounds__(128) k_fit(ws_batch B, FitOut out, int m_begin
                 break;
             }
             raw[ntp - 1].hi = N;
+            #pragma unroll 1
             for (int i = 0; i < ntp; ++i) order[i] = i;
             PieceLoCmp cmp{raw};
             ls_sort(order, ntp, cmp);
+            #pragma unroll 1
             for (int i = 0; i < ntp; ++i) tp[i] = raw[order[i]];
             if (fabs(tp[0].lo - 1.0) > 1e-9) {
                 err = WS_E_CURVE_START;
                 break;
             }
             bool contig = true;
+            #pragma unroll 1
             for (int i = 0; i + 1 < ntp; ++i)
                 if (fabs(tp[i].hi - tp[i + 1].lo) > 1e-9) contig = false;
             if (!contig) {
@@ -143,6 +148,7 @@ __global__ void __launch_bounds__(128) k_fit(ws_batch B, FitOut out, int m_begin
         double tv_local[kLanes > 1 ? 1 : WS_MAX_DEVICES];
         double* tv = kLanes > 1 ? s_tv[threadIdx.x / kLanes] : tv_local;
         if (!has_prof)
+            #pragma unroll 1
             for (int i = lane; i < N && i < WS_MAX_DEVICES; i += kLanes)
                 tv[i] = piece_value(tp[locate_piece(tp, ntp, i + 1)], c, w, static_cast<double>(i + 1));
         if (kLanes > 1) __syncwarp();
@@ -160,6 +166,7 @@ __global__ void __launch_bounds__(128) k_fit(ws_batch B, FitOut out, int m_begin
             err = WS_E_FIT_NO_POINTS;
             break;
         }
+        #pragma unroll 1
         for (int i = 0; i < npts && !err; ++i) {
             int n;
             double t;
@@ -171,6 +178,7 @@ __global__ void __launch_bounds__(128) k_fit(ws_batch B, FitOut out, int m_begin
         if (err) break;
         // breaks: spec breakpoints, else truth piece ends (planner.hpp:72-87)
         if (B.mod_bp_n[m] >= 0) {
+            #pragma unroll 1
             for (int i = 0; i < B.mod_bp_n[m] && !err; ++i) {
                 const int b = B.bps[B.mod_bp_off[m] + i];
                 if (!(b > 1 && b < N)) continue;
@@ -187,6 +195,7 @@ __global__ void __launch_bounds__(128) k_fit(ws_batch B, FitOut out, int m_begin
             if (err) break;
         }
         if (nbreak_in == 0 && !has_prof && has_truth) {
+            #pragma unroll 1
             for (int i = 0; i + 1 < ntp && !err; ++i) {
                 const int b = static_cast<int>(llround(tp[i].hi));
                 if (!(b > 1 && b < N)) continue;
@@ -204,6 +213,7 @@ __global__ void __launch_bounds__(128) k_fit(ws_batch B, FitOut out, int m_begin
         bounds[nb++] = nmax;
         // per-piece least squares of time vs 1/n (scaling.hpp:175-190, 248-280)
         np = nb - 1;
+        #pragma unroll 1
         for (int i = 0; i < np && !err; ++i) {
             const int lo = bounds[i], hi = bounds[i + 1];
             double sx = 0, sy = 0, sxy = 0, sxx = 0;
@@ -211,6 +221,7 @@ __global__ void __launch_bounds__(128) k_fit(ws_batch B, FitOut out, int m_begin
             // truth points are n = j + 1 in order: only the piece's own range
             // contributes, visited in the same (ascending) order
             const int j0 = has_prof ? 0 : (i == 0 ? lo - 1 : lo), j1 = has_prof ? npts : (hi < npts ? hi : npts);
+            #pragma unroll 1
             for (int j = j0 < 0 ? 0 : j0; j < j1; ++j) {
                 int n;
                 double t;
@@ -243,6 +254,7 @@ __global__ void __launch_bounds__(128) k_fit(ws_batch B, FitOut out, int m_begin
             fp[i] = DPiece{static_cast<double>(lo), static_cast<double>(hi), intercept, 0.0, slope / w};
         }
         if (err) break;
+        #pragma unroll 1
         for (int i = 1; i < np; ++i) {  // continuity join (scaling.hpp:282-287)
             const double bound = fp[i].lo;
             const double left = fp[i - 1].alpha + fp[i - 1].bw * w / bound;
@@ -258,11 +270,13 @@ __global__ void __launch_bounds__(128) k_fit(ws_batch B, FitOut out, int m_begin
             return cache_fv ? fv[k - 1] : piece_value(fp[locate_piece(fp, np, k)], c, w, static_cast<double>(k));
         };
         if (cache_fv)
+            #pragma unroll 1
             for (int k = 1 + lane; k <= nmax; k += kLanes)
                 fv[k - 1] = piece_value(fp[locate_piece(fp, np, k)], c, w, static_cast<double>(k));
         if (kLanes > 1) __syncwarp();
         bool changed = false;
         double prev = 0.0;
+        #pragma unroll 1
         for (int k = 1; k <= nmax; ++k) {
             const double v = fval(k);
             if (k > 1 && prev < v - 1e-15) {
@@ -280,7 +294,9 @@ __global__ void __launch_bounds__(128) k_fit(ws_batch B, FitOut out, int m_begin
             double bsum[128];
             int bcnt[128];
             int nbk = 0;
+            #pragma unroll 1
             for (int k = 1; k <= nmax; ++k) vals[k - 1] = fval(k);
+            #pragma unroll 1
             for (int k = 0; k < nmax; ++k) {
                 bsum[nbk] = vals[k];
                 bcnt[nbk] = 1;
@@ -293,11 +309,14 @@ __global__ void __launch_bounds__(128) k_fit(ws_batch B, FitOut out, int m_begin
                 }
             }
             int idx = 0;
+            #pragma unroll 1
             for (int b = 0; b < nbk; ++b) {
                 const double mean = bsum[b] / bcnt[b];
+                #pragma unroll 1
                 for (int k = 0; k < bcnt[b]; ++k) vals[idx++] = mean;
             }
             np = nmax - 1;
+            #pragma unroll 1
             for (int k = 1; k < nmax; ++k) {
                 const double v0 = vals[k - 1], v1 = vals[k];
                 const double b = (v0 - v1) / (1.0 / k - 1.0 / (k + 1.0));
@@ -311,10 +330,12 @@ __global__ void __launch_bounds__(128) k_fit(ws_batch B, FitOut out, int m_begin
             }
             if (kLanes > 1) __syncwarp();  // every lane has read the old anchors
             if (cache_fv)  // the rebuilt curve's anchor values
+                #pragma unroll 1
                 for (int k = 1 + lane; k <= nmax; k += kLanes)
                     fv[k - 1] = piece_value(fp[locate_piece(fp, np, k)], c, w, static_cast<double>(k));
             if (kLanes > 1) __syncwarp();
         }
+        #pragma unroll 1
         for (int k = 1; k <= nmax; ++k) {  // positivity (scaling.hpp:317-320)
             if (fval(k) <= 0.0) {
                 err = WS_E_FIT_NONPOSITIVE;
@@ -353,6 +374,7 @@ __global__ void __launch_bounds__(128) k_fit(ws_batch B, FitOut out, int m_begin
         out.nmax[m] = nmax;
     }
     double* dst = out.pieces + 5 * off;
+    #pragma unroll 1
     for (int i = lane; i < np; i += kLanes) {
         dst[5 * i + 0] = fp[i].lo;
         dst[5 * i + 1] = fp[i].hi;
@@ -362,6 +384,7 @@ __global__ void __launch_bounds__(128) k_fit(ws_batch B, FitOut out, int m_begin
     }
     const int lim = N < nmax ? N : nmax;
     double* tt = out.ttab + static_cast<int64_t>(m) * out.tstride;
+    #pragma unroll 1
     for (int n = 1 + lane; n <= lim; n += kLanes)
         tt[n - 1] = cache_fv ? fv[n - 1] : piece_value(fp[locate_piece(fp, np, n)], c, w, static_cast<double>(n));
 }

@@ -100,6 +100,7 @@ __device__ __forceinline__ double inverse_exact(const double* __restrict__ pc, i
         return __ldg(pc + 5 * i + 2) + __ldg(pc + 5 * i + 3) * c + __ldg(pc + 5 * i + 4) * scale * w / n;
     };
     if (target <= val(np - 1, nmax)) return nmax;
+    #pragma unroll 1
     for (int i = 0; i < np; ++i) {
         const double lo = __ldg(pc + 5 * i + 0), hi = __ldg(pc + 5 * i + 1);
         const double hi_val = val(i, lo);
@@ -145,6 +146,7 @@ struct InvPre {
             return __ldg(pc + 5 * i + 2) + __ldg(pc + 5 * i + 3) * c + __ldg(pc + 5 * i + 4) * scale * w / n;
         };
         last = val(np - 1, nmax);
+        #pragma unroll 1
         for (int i = 0; i < np; ++i) {
             lo[i] = __ldg(pc + 5 * i + 0);
             hi[i] = __ldg(pc + 5 * i + 1);
@@ -202,6 +204,7 @@ __device__ __forceinline__ void shard_moves(uint64_t from, uint64_t to, uint64_t
                            : island_matches(dst, src, moving, S, islm, lowm, n_isl);
     } else {
         uint64_t rs = src, rt = dst;
+        #pragma unroll 1
         for (int i = 0; i < moving; ++i) {
             const int s = low_bit(rs);
             rs &= rs - 1;
@@ -254,6 +257,7 @@ __device__ __forceinline__ Score shfl_xor_score(const Score& s, int m) {
 
 #ifdef WS_MINLOC_SHFL
 __device__ __forceinline__ Score warp_min_score(Score s) {
+    #pragma unroll 1
     for (int off = 16; off; off >>= 1) {
         const Score o = shfl_xor_score(s, off);
         if (o.valid && (!s.valid || score_less(o, s))) s = o;
@@ -298,11 +302,13 @@ __device__ __forceinline__ Score warp_min_score(const Score& s) {
 #endif
 
 __device__ __forceinline__ int warp_sum(int v) {
+    #pragma unroll 1
     for (int off = 16; off; off >>= 1) v += __shfl_xor_sync(kFull, v, off);
     return v;
 }
 
 __device__ __forceinline__ int warp_min_i(int v) {
+    #pragma unroll 1
     for (int off = 16; off; off >>= 1) {
         const int o = __shfl_xor_sync(kFull, v, off);
         v = o < v ? o : v;
@@ -311,6 +317,7 @@ __device__ __forceinline__ int warp_min_i(int v) {
 }
 
 __device__ __forceinline__ double warp_max_d(double v) {  // std::max fold, NaN-free inputs
+    #pragma unroll 1
     for (int off = 16; off; off >>= 1) {
         const double o = __shfl_xor_sync(kFull, v, off);
         v = (v < o) ? o : v;
@@ -337,6 +344,7 @@ __device__ __forceinline__ double warp_min_nonneg(double v) {  // same, minimum 
 }
 
 __device__ __forceinline__ double warp_min_d(double v) {
+    #pragma unroll 1
     for (int off = 16; off; off >>= 1) {
         const double o = __shfl_xor_sync(kFull, v, off);
         v = (o < v) ? o : v;
@@ -372,6 +380,7 @@ __device__ __forceinline__ OpKey op_key(const ws_batch& B, int gm, int layer, bo
 __device__ __forceinline__ bool key_less(const OpKey& a, const OpKey& b) {  // std::string operator<
     const int la = a.size(), lb = b.size();
     const int l = la < lb ? la : lb;
+    #pragma unroll 1
     for (int i = 0; i < l; ++i) {
         const unsigned char ca = static_cast<unsigned char>(a.at(i)), cb = static_cast<unsigned char>(b.at(i));
         if (ca != cb) return ca < cb;

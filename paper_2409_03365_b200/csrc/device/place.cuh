@@ -187,12 +187,14 @@ __device__ int p_wave(PCtx& C, int w, int variant) {
 
     WS_PH_START(tw);
     // incoming volume per entry (incoming_flows :188-206), entry order (:208-221)
+    #pragma unroll 1
     for (int i = lane; i < ec; i += 32) {
         const int k = e_k[eb + i];
         uint64_t v = 0;
         if (home[k] >= 0) {
             v = contb[k];
         } else {
+            #pragma unroll 1
             for (uint64_t pr = pred_r[k]; pr; pr &= pr - 1) {
                 const int p = by_rank[low_bit(pr)];
                 if (home[p] >= 0) v += edgeb[p];
@@ -201,11 +203,13 @@ __device__ int p_wave(PCtx& C, int w, int variant) {
         va[i] = v;
     }
     __syncwarp();
+    #pragma unroll 1
     for (int i = lane; i < ec; i += 32) {
         int pos = i;
         if (!C.sequential) {
             pos = 0;
             const int ki = e_k[eb + i];
+            #pragma unroll 1
             for (int j = 0; j < ec; ++j) {
                 if (j == i) continue;
                 const int kj = e_k[eb + j];
@@ -219,6 +223,7 @@ __device__ int p_wave(PCtx& C, int w, int variant) {
     uint64_t free = C.all;
     uint64_t placed_now = 0;
     int cursor = C.sequential ? w_cursor[w] : 0;
+    #pragma unroll 1
     for (int oi = 0; oi < ec; ++oi) {
         const int e = eb + eorder[oi];
         const int k = e_k[e], n = e_n[e], lay = e_l[e];
@@ -228,6 +233,7 @@ __device__ int p_wave(PCtx& C, int w, int variant) {
             if (lane == 0) fin_src[0] = home[k], fin_bytes[0] = contb[k];
             nfin = 1;
         } else {
+            #pragma unroll 1
             for (uint64_t pr = pred_r[k]; pr; pr &= pr - 1) {
                 const int p = by_rank[low_bit(pr)];
                 if (home[p] < 0) continue;
@@ -237,6 +243,7 @@ __device__ int p_wave(PCtx& C, int w, int variant) {
         }
         // homes this entry could displace (score_candidate :293-305), in id order
         int ndisp = 0;
+        #pragma unroll 1
         for (int base = 0; base < C.K; base += 32) {
             const int r = base + lane;
             bool ok = false;
@@ -263,6 +270,7 @@ __device__ int p_wave(PCtx& C, int w, int variant) {
         const double cap = C.cap;
         // device memory if this entry lands there (memory_delta), once per entry
         double* used_if = C.at<double>(L.used_if);
+        #pragma unroll 1
         for (int dv = lane; dv < N; dv += 32) {
             double delta = A;
             if (!(charged >> dv & 1ull)) delta += Pm;
@@ -276,8 +284,10 @@ __device__ int p_wave(PCtx& C, int w, int variant) {
             s.devs = devs;
             s.rot = rot;
             s.islands = 0;
+            #pragma unroll 1
             for (int i = 0; i < C.n_isl; ++i) s.islands += (devs & islmask[i]) != 0;
             s.displaced = 0.0;
+            #pragma unroll 1
             for (int j = 0; j < ndisp; ++j) {
                 const int ov = popc64(devs & disp_mask[j]);
                 if (ov == 0) continue;
@@ -285,6 +295,7 @@ __device__ int p_wave(PCtx& C, int w, int variant) {
             }
             s.feasible = 1;
             double peak = 0.0;
+            #pragma unroll 1
             for (uint64_t d = devs; d; d &= d - 1) {
                 const double used = used_if[low_bit(d)];
                 peak = (peak < used) ? used : peak;
@@ -293,6 +304,7 @@ __device__ int p_wave(PCtx& C, int w, int variant) {
             s.peak = peak;
             s.inter = 0.0;
             s.intra = 0.0;
+            #pragma unroll 1
             for (int f = 0; f < nfin; ++f) {
                 uint64_t a, b;
                 shard_moves(e_mask[fin_src[f]], devs, fin_bytes[f], isl, cislm, isllow, C.n_isl, a, b);
@@ -307,6 +319,7 @@ __device__ int p_wave(PCtx& C, int w, int variant) {
         if (C.sequential) {
             if (popc64(free) >= n) {  // rolling cursor block (:350-358), within the device block
                 uint64_t m = 0;
+                #pragma unroll 1
                 for (int i = 0; i < n; ++i) m |= 1ull << (C.dev_off + (cursor + i) % C.dev_cnt);
                 chosen = score_of(m, C.dev_off + cursor);
                 cursor = (cursor + n) % C.dev_cnt;
@@ -316,6 +329,7 @@ __device__ int p_wave(PCtx& C, int w, int variant) {
             const int nfree = popc64(free);
             if (nfree >= n) {
                 int total = nfin;
+                #pragma unroll 1
                 for (int i = 0; i < C.n_isl; ++i) {
                     const int c = popc64(free & islmask[i]);
                     const int nw = c >= n ? c - n + 1 : 0;
@@ -328,6 +342,7 @@ __device__ int p_wave(PCtx& C, int w, int variant) {
                 // in lockstep: skipping inside the scoring loop would split the warp
                 uint64_t* cmask = C.at<uint64_t>(L.cmask);
                 int ncand = 0;
+                #pragma unroll 1
                 for (int base = 0; base < total; base += 32) {
                     const int j = base + lane;
                     uint64_t m = 0;
@@ -338,6 +353,7 @@ __device__ int p_wave(PCtx& C, int w, int variant) {
                     } else if (j < total) {
                         int r = j - nfin;
                         int i = 0;
+                        #pragma unroll 1
                         for (; i < C.n_isl && r >= nwin[i]; ++i) r -= nwin[i];
                         keep = true;
                         if (i < C.n_isl) {
@@ -368,9 +384,11 @@ __device__ int p_wave(PCtx& C, int w, int variant) {
                 const int rounds = oi == 0 ? variant + 1 : 1;  // first entry takes scores[variant]
                 Score prev;
                 prev.valid = 0;
+                #pragma unroll 1
                 for (int rd = 0; rd < rounds; ++rd) {
                     Score best;
                     best.valid = 0;
+                    #pragma unroll 1
                     for (int j = lane; j < ncand; j += 32) {
                         const Score s = score_of(cmask[j], 0);
                         if (prev.valid && !score_less(prev, s)) continue;  // next distinct rank
@@ -388,6 +406,7 @@ __device__ int p_wave(PCtx& C, int w, int variant) {
         WS_PH_STOP(tw, 4);
         if (!chosen.valid || !chosen.feasible) return 0;
         // commit_memory (:142-149), lane per device
+        #pragma unroll 1
         for (int dv = lane; dv < N; dv += 32) {
             if (!(chosen.devs >> dv & 1ull)) continue;
             double delta = A;
@@ -400,6 +419,7 @@ __device__ int p_wave(PCtx& C, int w, int variant) {
             e_rot[e] = chosen.rot;
         }
         // flow records (:376-400), lane 0 appends in order
+        #pragma unroll 1
         for (int f = 0; f < nfin; ++f) {
             uint64_t a, b;
             const int src = fin_src[f];
@@ -443,6 +463,7 @@ __device__ void p_emit(PCtx& C, int p, const char* rec, const RecLayout& RL, con
     const uint64_t* r_succ = reinterpret_cast<const uint64_t*>(rec + RL.succ_r);
     const int* by_rank = C.at<int>(C.L->by_rank);
     int npieces = 0, nedges = 0;
+    #pragma unroll 1
     for (int k = lane; k < K; k += 32) {
         npieces += C.F->npieces[C.mbase + r_mod_of[k]];
         nedges += popc64(r_succ[k]);
@@ -484,11 +505,13 @@ __device__ void p_emit(PCtx& C, int p, const char* rec, const RecLayout& RL, con
     o += al8(sizeof(ws_out_entry) * nE);
     auto* fl = reinterpret_cast<ws_out_flow*>(base + o);
     // lane per MetaOp; piece offsets by a warp prefix sum over piece counts
+    #pragma unroll 1
     for (int base = 0, pb0 = 0; base < K; base += 32) {
         const int k = base + lane;
         const int gm = k < K ? C.mbase + r_mod_of[k] : 0;
         const int np = k < K ? C.F->npieces[gm] : 0;
         int incl = np;
+        #pragma unroll 1
         for (int off = 1; off < 32; off <<= 1) {
             const int v = __shfl_up_sync(kFull, incl, off);
             if (lane >= off) incl += v;
@@ -509,6 +532,7 @@ __device__ void p_emit(PCtx& C, int p, const char* rec, const RecLayout& RL, con
             x.lower_l = r_lo_l[k];
             mo[k] = x;
             const double* src = C.F->pieces + 5 * C.F->piece_off[gm];
+            #pragma unroll 1
             for (int i = 0; i < np; ++i)
                 pc[pb + i] = ws_out_piece{src[5 * i], src[5 * i + 1], src[5 * i + 2], src[5 * i + 3], src[5 * i + 4]};
         }
@@ -516,20 +540,24 @@ __device__ void p_emit(PCtx& C, int p, const char* rec, const RecLayout& RL, con
     const double* cstar = reinterpret_cast<const double*>(rec + RL.cstar);
     const int* lfw = reinterpret_cast<const int*>(rec + RL.lvl_fw);
     const int* lnw = reinterpret_cast<const int*>(rec + RL.lvl_nw);
+    #pragma unroll 1
     for (int l = lane; l < nL; l += 32) lv[l] = ws_out_level{cstar[l], lfw[l], lnw[l]};
     // MetaGraph edges in std::set<pair<string,string>> order: lane per source rank
+    #pragma unroll 1
     for (int base = 0, ne0 = 0; base < K; base += 32) {
         const int ra = base + lane;
         const int a = ra < K ? by_rank[ra] : 0;
         const uint64_t succ = ra < K ? r_succ[a] : 0;
         const int cnt = popc64(succ);
         int incl = cnt;
+        #pragma unroll 1
         for (int off = 1; off < 32; off <<= 1) {
             const int v = __shfl_up_sync(kFull, incl, off);
             if (lane >= off) incl += v;
         }
         int ne = ne0 + incl - cnt;
         ne0 += __shfl_sync(kFull, incl, 31);
+        #pragma unroll 1
         for (uint64_t s = succ; s; s &= s - 1) ed[ne++] = ws_out_edge{a, by_rank[low_bit(s)]};
     }
     const double* w_start = reinterpret_cast<const double*>(rec + RL.w_start);
@@ -537,6 +565,7 @@ __device__ void p_emit(PCtx& C, int p, const char* rec, const RecLayout& RL, con
     const int* w_level = reinterpret_cast<const int*>(rec + RL.w_level);
     const int* w_eb = C.at<int>(C.L->w_eb);
     const int* w_ec = C.at<int>(C.L->w_ec);
+    #pragma unroll 1
     for (int w = lane; w < nW; w += 32) {
         ws_out_wave x;
         x.start = w_start[w];
@@ -553,6 +582,7 @@ __device__ void p_emit(PCtx& C, int p, const char* rec, const RecLayout& RL, con
     const double* e_span = reinterpret_cast<const double*>(rec + RL.e_span);
     const uint64_t* e_mask = C.at<uint64_t>(C.L->e_mask);
     const int* e_rot = C.at<int>(C.L->e_rot);
+    #pragma unroll 1
     for (int e = lane; e < nE; e += 32) {
         ws_out_entry x;
         x.span = e_span[e];
@@ -563,6 +593,7 @@ __device__ void p_emit(PCtx& C, int p, const char* rec, const RecLayout& RL, con
         x.rot = e_rot[e];
         en[e] = x;
     }
+    #pragma unroll 1
     for (int f = lane; f < nF; f += 32) {
         const uint64_t meta = C.flows[2 * f + 1];
         ws_out_flow x;
@@ -579,6 +610,7 @@ __device__ void p_emit(PCtx& C, int p, const char* rec, const RecLayout& RL, con
         auto* sc = reinterpret_cast<ws_out_scope*>(base + o + al8(sizeof(ws_out_flow) * nF));
         const int* r_met = reinterpret_cast<const int*>(rec + RL.e_met);
         const int* r_task = reinterpret_cast<const int*>(rec + RL.e_task);
+        #pragma unroll 1
         for (int k = lane; k < nS; k += 32) sc[k] = ws_out_scope{r_met[k], r_task[k]};
     }
     if (lane == 0) {
@@ -601,12 +633,13 @@ __device__ void p_emit(PCtx& C, int p, const char* rec, const RecLayout& RL, con
 }
 
 #ifndef WS_PLACE_MINB
-#define WS_PLACE_MINB 3  // measured sweep 1/2/3/4: 3 blocks (<=170 regs) is fastest
+#define WS_PLACE_MINB 4  // measured (no-unroll build): 4 blocks (<=128 regs) 7.29 ms vs 3 blocks 7.60 ms per 100k
 #endif
 // Snapshot slot claim / release (lane 0): a free bit of the pool bitmap, or -1
 // when every slot is taken (the warp then restores by replay).
 __device__ int snap_claim(unsigned* bits, int slots, int start) {
     const int words = (slots + 31) >> 5;
+    #pragma unroll 1
     for (int t = 0; t < words; ++t) {
         const int w = (start + t) % words;
         const unsigned valid = (w + 1) * 32 <= slots ? ~0u : ((1u << (slots - w * 32)) - 1u);
@@ -694,6 +727,7 @@ __global__ void __launch_bounds__(32 * kPlaceWarps, WS_PLACE_MINB) k_place(Place
     uint64_t* edgeb = C.at<uint64_t>(L.edgeb);
     uint64_t* memact = C.at<uint64_t>(L.memact);
     uint64_t* parb = C.at<uint64_t>(L.parb);
+    #pragma unroll 1
     for (int k = lane; k < K; k += 32) {
         by_rank[k] = r_by_rank[k];
         idrank[k] = r_idrank[k];
@@ -731,11 +765,13 @@ __global__ void __launch_bounds__(32 * kPlaceWarps, WS_PLACE_MINB) k_place(Place
     int* e_wave = C.at<int>(L.e_wave);
     uint64_t* e_mask = C.at<uint64_t>(L.e_mask);
     int* e_rot = C.at<int>(L.e_rot);
+    #pragma unroll 1
     for (int w = lane; w < nW; w += 32) {
         w_eb[w] = r_w_eb[w];
         w_ec[w] = r_w_ec[w];
         variant[w] = 0;
     }
+    #pragma unroll 1
     for (int e = lane; e < nE; e += 32) {
         e_k[e] = r_e_k[e];
         e_n[e] = r_e_n[e];
@@ -747,26 +783,34 @@ __global__ void __launch_bounds__(32 * kPlaceWarps, WS_PLACE_MINB) k_place(Place
     uint64_t* chg = C.at<uint64_t>(L.chg);
     int* isl = C.at<int>(L.isl);
     uint64_t* islmask = C.at<uint64_t>(L.islmask);
+    #pragma unroll 1
     for (int d = lane; d < N; d += 32) {
         isl[d] = B.dev_island[R.dev_begin + d];
         mem[d] = 0.0;
     }
+    #pragma unroll 1
     for (int g = lane; g < G; g += 32) chg[g] = 0;
     __syncwarp();
     uint64_t* islfull = C.at<uint64_t>(L.islfull);
+    #pragma unroll 1
     for (int i = 0; i < R.n_islands; ++i) {  // island masks, one ballot per 32 devices
         uint64_t m = 0;
+        #pragma unroll 1
         for (int base = 0; base < N; base += 32) {
             const int d = base + lane;
             m |= static_cast<uint64_t>(__ballot_sync(kFull, d < N && isl[d] == i)) << base;
         }
         if (lane == 0) islfull[i] = m;
     }
+    #pragma unroll 1
     for (int w = lane; w < nW; w += 32)
+        #pragma unroll 1
         for (int i = 0; i < w_ec[w]; ++i) e_wave[w_eb[w] + i] = w;
     __syncwarp();
+    #pragma unroll 1
     for (int e = lane; e < nE; e += 32) {  // previous entry of the same entity
         int pv = -1;
+        #pragma unroll 1
         for (int j = e - 1; j >= 0; --j)
             if (e_k[j] == e_k[e]) {
                 pv = j;
@@ -774,7 +818,9 @@ __global__ void __launch_bounds__(32 * kPlaceWarps, WS_PLACE_MINB) k_place(Place
             }
         e_prev[e] = pv;
     }
+    #pragma unroll 1
     for (int k = lane; k < K; k += 32) {  // last entry / wave of each entity
+        #pragma unroll 1
         for (int j = nE - 1; j >= 0; --j)
             if (e_k[j] == k) {
                 lastent[k] = j;
@@ -804,13 +850,17 @@ __global__ void __launch_bounds__(32 * kPlaceWarps, WS_PLACE_MINB) k_place(Place
                                        static_cast<long long>(j) * snapW; };
     auto snap_save = [&](int j) {  // state before wave j
         double* dst = snap_at(j);
+        #pragma unroll 1
         for (int d = lane; d < snapN; d += 32) dst[d] = mem[d];
+        #pragma unroll 1
         for (int g = lane; g < G; g += 32) reinterpret_cast<uint64_t*>(dst + snapN)[g] = chg[g];
     };
+    #pragma unroll 1
     for (int grp = 0; grp < (n_pg ? n_pg : 1); ++grp) {
         snap_hi = -1;
         const int goff = n_pg ? r_pg_off[grp] : 0, gcnt = n_pg ? r_pg_cnt[grp] : N;
         const int gn = n_pg ? r_pg_wn[grp] : nW;
+        #pragma unroll 1
         for (int i = lane; i < gn; i += 32) glist[i] = n_pg ? r_pg_list[r_pg_wbeg[grp] + i] : i;
         C.dev_off = goff;
         C.dev_cnt = gcnt;
@@ -818,6 +868,7 @@ __global__ void __launch_bounds__(32 * kPlaceWarps, WS_PLACE_MINB) k_place(Place
         __syncwarp();
         if (lane == 0) {
             int ni = 0, contig = 1;
+            #pragma unroll 1
             for (int i = 0; i < R.n_islands; ++i) {  // sub_topology (baselines.hpp:81-93)
                 const uint64_t m = islfull[i] & C.all;
                 if (!m) continue;
@@ -828,9 +879,11 @@ __global__ void __launch_bounds__(32 * kPlaceWarps, WS_PLACE_MINB) k_place(Place
                 ++ni;
             }
             int cur = 0;  // sequential-ablation cursor (:331-338) over this call's waves
+            #pragma unroll 1
             for (int j = 0; j < gn; ++j) {
                 const int w = glist[j];
                 w_cursor[w] = cur;
+                #pragma unroll 1
                 for (int i = 0; i < w_ec[w]; ++i) cur = (cur + e_n[w_eb[w] + i]) % gcnt;
                 variant[j] = 0;
             }
@@ -840,8 +893,11 @@ __global__ void __launch_bounds__(32 * kPlaceWarps, WS_PLACE_MINB) k_place(Place
         __syncwarp();
         C.contig = ctl->i0;
         C.n_isl = ctl->i1;
+        #pragma unroll 1
         for (int d = lane; d < N; d += 32) mem[d] = 0.0;
+        #pragma unroll 1
         for (int g = lane; g < G; g += 32) chg[g] = 0;
+        #pragma unroll 1
         for (int k = lane; k < K; k += 32) home[k] = -1;
         __syncwarp();
     // depth-first search over per-wave variants with a bounded attempt budget (:409-441).
@@ -852,6 +908,7 @@ __global__ void __launch_bounds__(32 * kPlaceWarps, WS_PLACE_MINB) k_place(Place
     // and the doubles are identical.  Only the flow count is recorded per wave.
     int* wave_nf = C.at<int>(L.nwin) + C.n_isl;  // [W+1] after the window counts
     long long attempts = 0, budget = gn;
+    #pragma unroll 1
     for (int d = 0; d < R.bt_depth; ++d) budget *= (R.bt_branching > 1 ? R.bt_branching : 1);
     const int branching = R.sequential ? 1 : R.bt_branching;
     int k = 0;
@@ -869,7 +926,9 @@ __global__ void __launch_bounds__(32 * kPlaceWarps, WS_PLACE_MINB) k_place(Place
         WS_PH_START(tr);
         if (kSnap && dirty && snap_hi >= k) {  // restore the state before wave k from its snapshot
             const double* src = snap_at(k);
+            #pragma unroll 1
             for (int d = lane; d < N; d += 32) mem[d] = src[d];
+            #pragma unroll 1
             for (int g = lane; g < G; g += 32) chg[g] = reinterpret_cast<const uint64_t*>(src + snapN)[g];
             snap_hi = k;
             C.nF = wave_nf[k];
@@ -882,21 +941,26 @@ __global__ void __launch_bounds__(32 * kPlaceWarps, WS_PLACE_MINB) k_place(Place
                 if (lane == 0) sl = snap_claim(A.snap_bits, A.snap_slots, (blockIdx.x * kPlaceWarps + wid) >> 5);
                 snap_slot = __shfl_sync(kFull, sl, 0);
             }
+            #pragma unroll 1
             for (int d = lane; d < N; d += 32) mem[d] = 0.0;
+            #pragma unroll 1
             for (int g = lane; g < G; g += 32) chg[g] = 0;
             __syncwarp();
+            #pragma unroll 1
             for (int j = 0; j < k; ++j) {
                 if (kSnap && snap_slot >= 0) {
                     __syncwarp();
                     snap_save(j);
                 }
                 const int w = glist[j];
+                #pragma unroll 1
                 for (int i = 0; i < w_ec[w]; ++i) {
                     const int e = w_eb[w] + i;
                     const int ke = e_k[e];
                     const double Ae = e_l[e] * (static_cast<double>(memact[ke]) / e_n[e]);
                     const double Pe = C.gmul1 * static_cast<double>(parb[ke]) / tpk[ke];
                     const uint64_t charged = chg[gkey[ke]];
+                    #pragma unroll 1
                     for (int dv = lane; dv < N; dv += 32) {
                         if (!(e_mask[e] >> dv & 1ull)) continue;
                         double delta = Ae;
@@ -931,6 +995,7 @@ __global__ void __launch_bounds__(32 * kPlaceWarps, WS_PLACE_MINB) k_place(Place
             }
             --k;
             const int wk = glist[k];
+            #pragma unroll 1
             for (int i = lane; i < w_ec[wk]; i += 32) {  // home[] back to "before wave k"
                 const int e = w_eb[wk] + i;
                 home[e_k[e]] = e_prev[e];
@@ -952,6 +1017,7 @@ __global__ void __launch_bounds__(32 * kPlaceWarps, WS_PLACE_MINB) k_place(Place
         }
         if (r > 0) {
             if (lane == 0) wave_nf[k + 1] = C.nF;  // flows recorded before wave k+1
+            #pragma unroll 1
             for (int i = lane; i < w_ec[wk]; i += 32) {
                 const int e = w_eb[wk] + i;
                 home[e_k[e]] = e;

@@ -228,6 +228,7 @@ __device__ bool s_graph(SCtx& C) {
     int* keyrank = C.at<int>(C.L->keyrank);
     int* modat = C.at<int>(C.L->modat);
     int* mod_of = C.at<int>(C.L->mod_of);
+    #pragma unroll 1
     for (int m = lane; m < M; m += 32) {
         adj[m] = 0;
         tmask[m] = 0;
@@ -235,6 +236,7 @@ __device__ bool s_graph(SCtx& C) {
     }
     __syncwarp();
     // tasks in parallel: lane t walks the flow of task t
+    #pragma unroll 1
     for (int t = lane; t < R.n_tasks; t += 32) {
         const int tg = R.task_begin + t;
         const int* tok = B.tokens + B.task_tok_off[tg];
@@ -243,6 +245,7 @@ __device__ bool s_graph(SCtx& C) {
         uint64_t prev_tails = 0, heads = 0, tails = 0;
         int last = -1;
         bool start = true;
+        #pragma unroll 1
         for (int i = 0; i <= ntok; ++i) {
             const int v = i < ntok ? __ldg(tok + i) : WS_TOK_STEP;
             if (v >= 0) {
@@ -258,6 +261,7 @@ __device__ bool s_graph(SCtx& C) {
                 last = -1;
                 start = true;
                 if (v == WS_TOK_STEP) {  // every tail of step k feeds every head of step k+1 (:137-139)
+                    #pragma unroll 1
                     for (uint64_t f = prev_tails; f; f &= f - 1)
                         atomicOr(reinterpret_cast<unsigned long long*>(&adj[low_bit(f)]), heads);
                     prev_tails = tails;
@@ -268,6 +272,7 @@ __device__ bool s_graph(SCtx& C) {
     }
     __syncwarp();
     uint64_t used = 0;
+    #pragma unroll 1
     for (int base = 0; base < M; base += 32) {
         const int m = base + lane;
         used |= static_cast<uint64_t>(__ballot_sync(kFull, m < M && tmask[m] != 0)) << base;
@@ -275,10 +280,12 @@ __device__ bool s_graph(SCtx& C) {
     // keys kind+"." packed big-endian into their first 8 bytes (zero padded);
     // `valid` is scratch here, s_valid fills it later
     uint64_t* key8 = C.at<uint64_t>(C.L->valid);
+    #pragma unroll 1
     for (int m = lane; m < M; m += 32) {
         const uint8_t* nm = B.names + B.mod_name_off[C.mbase + m];
         const int len = B.mod_name_len[C.mbase + m];
         uint64_t k = 0;
+        #pragma unroll 1
         for (int i = 0; i < 8 && i <= len; ++i)
             k |= static_cast<uint64_t>(i < len ? nm[i] : static_cast<uint8_t>('.')) << (56 - 8 * i);
         key8[m] = k;
@@ -286,8 +293,10 @@ __device__ bool s_graph(SCtx& C) {
     __syncwarp();
     // in-degrees, rank of the key kind+"." and kinds prefixed by another kind+"."
     int conflict = 0;
+    #pragma unroll 1
     for (int m = lane; m < M; m += 32) {
         int d = 0;
+        #pragma unroll 1
         for (int a = 0; a < M; ++a) d += (adj[a] >> m) & 1ull;
         indeg[m] = d;
         if (!(used >> m & 1ull)) {
@@ -298,6 +307,7 @@ __device__ bool s_graph(SCtx& C) {
         const int lm_ = B.mod_name_len[C.mbase + m];
         const uint64_t pmask = lm_ < 7 ? ~0ull << (56 - 8 * lm_) : ~0ull;  // bytes 0..len
         int r = 0;
+        #pragma unroll 1
         for (uint64_t o = used; o; o &= o - 1) {
             const int q = low_bit(o);
             if (q == m) continue;
@@ -315,6 +325,7 @@ __device__ bool s_graph(SCtx& C) {
                 } else {
                     const OpKey km = op_key(B, C.mbase + m, 0, false), kq = op_key(B, C.mbase + q, 0, false);
                     pre = true;
+                    #pragma unroll 1
                     for (int i = 0; i <= km.len && pre; ++i) pre = kq.at(i) == km.at(i);
                 }
                 if (pre) conflict = 1;
@@ -332,6 +343,7 @@ __device__ bool s_graph(SCtx& C) {
             // once kind.0 pops, its remaining layers pop consecutively,
             // so the operator-level lexicographic Kahn is the module Kahn by kind+"."
             uint64_t ready = 0;
+            #pragma unroll 1
             for (uint64_t u = used; u; u &= u - 1) {
                 const int m = low_bit(u);
                 if (indeg[m] == 0) ready |= 1ull << keyrank[m];
@@ -342,6 +354,7 @@ __device__ bool s_graph(SCtx& C) {
                 const int m = modat[r];
                 kofm[m] = K;
                 mod_of[K++] = m;
+                #pragma unroll 1
                 for (uint64_t s = adj[m]; s; s &= s - 1) {
                     const int q = low_bit(s);
                     if (--indeg[q] == 0) ready |= 1ull << keyrank[q];
@@ -350,10 +363,12 @@ __device__ bool s_graph(SCtx& C) {
         } else {
             // general operator-level lexicographic Kahn with per-module layer cursors
             int* cursor = C.at<int>(C.L->sumlay);
+            #pragma unroll 1
             for (int m = 0; m < M; ++m) cursor[m] = 0;
             while (true) {
                 int best = -1;
                 OpKey bk;
+                #pragma unroll 1
                 for (uint64_t u = used; u; u &= u - 1) {
                     const int m = low_bit(u);
                     const int L = B.mod_layers[C.mbase + m];
@@ -370,6 +385,7 @@ __device__ bool s_graph(SCtx& C) {
                     mod_of[K++] = best;
                 }
                 if (++cursor[best] == B.mod_layers[C.mbase + best])
+                    #pragma unroll 1
                     for (uint64_t s = adj[best]; s; s &= s - 1) --indeg[low_bit(s)];
             }
         }
@@ -384,8 +400,10 @@ __device__ bool s_graph(SCtx& C) {
     int* by_rank = C.at<int>(C.L->by_rank);
     int* gm_of = C.at<int>(C.L->gm_of);
     int* Lk = C.at<int>(C.L->Lk);
+    #pragma unroll 1
     for (int k = lane; k < K; k += 32) {  // MetaOp ids "m<k>" in std::map order
         int r = 0;
+        #pragma unroll 1
         for (int j = 0; j < K; ++j) r += dec_less(j, k);
         idrank[k] = r;
         by_rank[r] = k;
@@ -397,9 +415,11 @@ __device__ bool s_graph(SCtx& C) {
     uint64_t* predk = C.at<uint64_t>(C.L->predk);
     uint64_t* pred_r = C.at<uint64_t>(C.L->pred_r);
     uint64_t* succ_r = C.at<uint64_t>(C.L->succ_r);
+    #pragma unroll 1
     for (int k = lane; k < K; k += 32) {
         const int m = mod_of[k];
         uint64_t pk = 0, pr = 0, sr = 0;
+        #pragma unroll 1
         for (int j = 0; j < K; ++j) {
             if (j == k) continue;
             const int q = mod_of[j];
@@ -414,8 +434,10 @@ __device__ bool s_graph(SCtx& C) {
     if (lane == 0) {  // longest-path levels; numbering order is topological
         int* level = C.at<int>(C.L->level);
         int maxl = 0;
+        #pragma unroll 1
         for (int k = 0; k < K; ++k) {
             int lv = 0;
+            #pragma unroll 1
             for (uint64_t p = predk[k]; p; p &= p - 1) {
                 const int q = level[low_bit(p)] + 1;
                 lv = q > lv ? q : lv;
@@ -426,10 +448,15 @@ __device__ bool s_graph(SCtx& C) {
         int* lb = C.at<int>(C.L->lvl_begin);
         int* lm = C.at<int>(C.L->lvl_mem);
         int* fill = C.at<int>(C.L->absorb);
+        #pragma unroll 1
         for (int l = 0; l <= maxl + 1; ++l) lb[l] = 0;
+        #pragma unroll 1
         for (int k = 0; k < K; ++k) lb[level[k] + 1]++;
+        #pragma unroll 1
         for (int l = 0; l <= maxl; ++l) lb[l + 1] += lb[l];
+        #pragma unroll 1
         for (int l = 0; l <= maxl; ++l) fill[l] = lb[l];
+        #pragma unroll 1
         for (int r = 0; r < K; ++r) {
             const int k = by_rank[r];
             lm[fill[level[k]]++] = k;
@@ -443,6 +470,7 @@ __device__ bool s_graph(SCtx& C) {
 // (2) results of k_fit: the first module in kind order whose fit failed
 __device__ bool s_fit_status(SCtx& C) {
     const int M = C.M;
+    #pragma unroll 1
     for (int base = 0; base < M; base += 32) {
         const int m = base + C.lane;
         const int e = m < M ? C.F->err[C.mbase + m] : 0;
@@ -470,6 +498,7 @@ __device__ bool s_valid(SCtx& C, bool check_tp) {
     const int* gm_of = C.at<int>(C.L->gm_of);
     const int* by_rank = C.at<int>(C.L->by_rank);
     uint64_t* valid = C.at<uint64_t>(C.L->valid);
+    #pragma unroll 1
     for (int base = 0; base < K && check_tp; base += 32) {  // tp > N in id order (planner.hpp:168-171)
         const int r = base + lane;
         const bool bad = r < K && B.mod_tp[gm_of[by_rank[r]]] > N;
@@ -483,11 +512,13 @@ __device__ bool s_valid(SCtx& C, bool check_tp) {
             return false;
         }
     }
+    #pragma unroll 1
     for (int k = 0; k < K; ++k) {  // lanes = device counts n, one ballot per 32 n
         const int gm = gm_of[k];
         const int tp = B.mod_tp[gm];
         const long long batch = B.mod_batch[gm];
         uint64_t v = 0;
+        #pragma unroll 1
         for (int base = 0; base < N; base += 32) {
             const int n = base + lane + 1;
             bool ok = n <= N && n % tp == 0;
@@ -504,7 +535,9 @@ __device__ bool s_valid(SCtx& C, bool check_tp) {
 
 __device__ __forceinline__ double ordered_sum(double v0, double v1, int w) {
     double total = 0.0;  // reference order: ((0 + v_0) + v_1) + ...
+    #pragma unroll 1
     for (int j = 0; j < 32 && j < w; ++j) total += shfl_d(v0, j);
+    #pragma unroll 1
     for (int j = 0; j + 32 < w; ++j) total += shfl_d(v1, j);
     return total;
 }
@@ -527,6 +560,7 @@ __device__ bool s_level_repair(SCtx& C, int lvl) {
     const FitOut& F = *C.F;
     while (true) {
         int wid = 0;
+        #pragma unroll 1
         for (int i = lane; i < w; i += 32) {
             const int k = lm[i];
             const int a = up_n[k], b = lo_l[k] ? lo_n[k] : 0;
@@ -536,6 +570,7 @@ __device__ bool s_level_repair(SCtx& C, int lvl) {
         double best_pen = 0.0;
         int best_i = 0x7fffffff, best_key = 0x7fffffff, best_t = 0, eidx = 0x7fffffff;
         double ex = 0, ey = 0;
+        #pragma unroll 1
         for (int i = lane; i < w; i += 32) {
             const int k = lm[i];
             const int key = idrank[k];
@@ -565,6 +600,7 @@ __device__ bool s_level_repair(SCtx& C, int lvl) {
             __syncwarp();
             return false;
         }
+        #pragma unroll 1
         for (int off = 16; off; off >>= 1) {  // argmin over (penalty, MetaOp id)
             const double op = __shfl_xor_sync(kFull, best_pen, off);
             const int oi = __shfl_xor_sync(kFull, best_i, off);
@@ -588,6 +624,7 @@ __device__ __forceinline__ bool discretize_one(const FitOut& F, const ws_plan_re
                                                int& ll, double& ex, const ws_batch* B = nullptr,
                                                double scale = 1.0) {
     int exact = -1, n_over = -1, n_under = -1;
+    #pragma unroll 1
     for (uint64_t b = v; b; b &= b - 1) {
         const int x = low_bit(b) + 1;
         if (fabs(x - nstar) < 1e-9) {
@@ -596,6 +633,7 @@ __device__ __forceinline__ bool discretize_one(const FitOut& F, const ws_plan_re
         }
     }
     if (exact < 0)
+        #pragma unroll 1
         for (uint64_t b = v; b; b &= b - 1) {
             const int x = low_bit(b) + 1;
             if (x < nstar) n_under = x;
@@ -702,6 +740,7 @@ __device__ bool s_level_alloc(SCtx& C, int lvl, double& c_star_out) {
         const double v = q.inv(cc / q.L);
         return (nd < v) ? nd : v;  // std::min(v, N)
     };
+    #pragma unroll 1
     for (int it = 0; it < R.max_iters && (c_hi - c_lo) > R.eps * c_hi; ++it) {
         const double mid = 0.5 * (c_lo + c_hi);
         const double t0 = mem[0].k >= 0 ? probe_term(mem[0], mid) : 0.0;
@@ -779,6 +818,7 @@ __device__ void s_alloc_concurrent(SCtx& C, int n_levels) {
     const int s0 = has ? lb[lv] : lane;
     const int sw = has ? lb[lv + 1] - lb[lv] : 0;
     int maxw = 0;
+    #pragma unroll 1
     for (int l = 0; l < n_levels; ++l) maxw = lb[l + 1] - lb[l] > maxw ? lb[l + 1] - lb[l] : maxw;
     const int gm = has ? gm_of[k] : 0;
     const int L = has ? Lk[k] : 1;
@@ -787,6 +827,7 @@ __device__ void s_alloc_concurrent(SCtx& C, int n_levels) {
     if (has) inv.init(F.pieces + 5 * F.piece_off[gm], F.npieces[gm], B.mod_c[gm], B.mod_w[gm], nmax);
     auto seg_sum = [&](double v) {  // ((0 + v_s) + v_s+1) + ... over this lane's segment
         double total = 0.0;
+        #pragma unroll 1
         for (int j = 0; j < maxw; ++j) {
             const double x = __shfl_sync(kFull, v, s0 + (j < sw ? j : (sw ? sw - 1 : 0)));
             if (j < sw) total += x;
@@ -795,6 +836,7 @@ __device__ void s_alloc_concurrent(SCtx& C, int n_levels) {
     };
     auto seg_max = [&](double v) {
         double m = 0.0;
+        #pragma unroll 1
         for (int j = 0; j < maxw; ++j) {
             const double x = __shfl_sync(kFull, v, s0 + (j < sw ? j : (sw ? sw - 1 : 0)));
             if (j < sw) m = (m < x) ? x : m;
@@ -907,11 +949,13 @@ struct CmpByCheap {  // schedule.hpp:112-118
 __device__ void ser_extend(const SchedView& S, int* n, const int* sel, int nsel) {  // schedule.hpp:144-173
     while (true) {
         int usedn = 0;
+        #pragma unroll 1
         for (int i = 0; i < nsel; ++i) usedn += n[sel[i]];
         const int idle = S.N - usedn;
         if (idle <= 0) break;
         int best = -1, best_next = 0;
         double best_time = -1.0;
+        #pragma unroll 1
         for (int i = 0; i < nsel; ++i) {
             const int t = sel[i];
             const int k = S.tk[t];
@@ -935,6 +979,7 @@ __device__ void ser_extend(const SchedView& S, int* n, const int* sel, int nsel)
 __device__ int ser_greedy(const SchedView& S, const int* order, int* sel) {
     int ns = 0, cap = S.N;
     uint64_t taken = 0;
+    #pragma unroll 1
     for (int i = 0; i < S.R; ++i) {
         const int t = order[i];
         if (S.tn[t] > cap) continue;
@@ -960,6 +1005,7 @@ __device__ int ser_wave(SCtx& C, SchedView& S) {
     int* o1 = o0 + cap2;
     int* o2 = o0 + 2 * cap2;
     const int R = S.R;
+    #pragma unroll 1
     for (int i = 0; i < R; ++i) o0[i] = o1[i] = o2[i] = i;
     CmpByN c0{&S};
     ls_sort(o0, R, c0);
@@ -973,15 +1019,18 @@ __device__ int ser_wave(SCtx& C, SchedView& S) {
     for (int o = 0; o < 3; ++o) {
         const int* order = o == 0 ? o0 : (o == 1 ? o1 : o2);
         const int ns = ser_greedy(S, order, sel);
+        #pragma unroll 1
         for (int i = 0; i < R; ++i) n2[i] = S.tn[i];
         ser_extend(S, n2, sel, ns);
         if (C.ctl->err) return -1;
         int usedn = 0;
+        #pragma unroll 1
         for (int i = 0; i < ns; ++i) usedn += n2[sel[i]];
         const long long key = static_cast<long long>(usedn) * 1000 + ns;
         if (key > best_key) {  // strict: earlier orders win ties
             best_key = key;
             nbest = ns;
+            #pragma unroll 1
             for (int i = 0; i < ns; ++i) best[i] = sel[i];
         }
     }
@@ -993,6 +1042,7 @@ __device__ int ser_wave(SCtx& C, SchedView& S) {
     if (C.ctl->err) return -1;
     // align_time_span (schedule.hpp:190-227)
     double t_wave = 0.0;
+    #pragma unroll 1
     for (int i = 0; i < nbest; ++i) {
         const int t = best[i];
         pool[i] = S.sumlay[S.tk[t]];
@@ -1000,6 +1050,7 @@ __device__ int ser_wave(SCtx& C, SchedView& S) {
         if (i == 0 || span < t_wave) t_wave = span;
     }
     if (C.ctl->err) return -1;
+    #pragma unroll 1
     for (int i = 0; i < nbest; ++i) {
         const int t = best[i];
         const int k = S.tk[t];
@@ -1091,6 +1142,7 @@ __device__ int fast_wave(SCtx& C, SchedView& S) {
     const double rt = sl * T0;  // metaop_remaining_time at own n
     // stable ranks under the three comparators
     int p0 = 0, p1 = 0, p2 = 0;
+    #pragma unroll 1
     for (int j = 0; j < R; ++j) {
         const int nj = __shfl_sync(kFull, n0, j);
         const double ttj = __shfl_sync(kFull, tt, j);
@@ -1128,6 +1180,7 @@ __device__ int fast_wave(SCtx& C, SchedView& S) {
         unsigned sel = 0;
         int cap = N, ns = 0, mypos = -1;
         uint64_t taken = 0;
+        #pragma unroll 1
         for (int i = 0; i < R; ++i) {
             const int t = order[i];
             const int nt = S.tn[t], kt = S.tk[t];
@@ -1215,6 +1268,7 @@ __device__ bool s_decoupled(SCtx& C, char* rec, const RecLayout& RL, int& nW, in
         int* e_l = reinterpret_cast<int*>(rec + RL.e_l);
         double* e_span = reinterpret_cast<double*>(rec + RL.e_span);
         uint64_t ready = 0;
+        #pragma unroll 1
         for (int k = 0; k < K; ++k) {
             indeg[k] = popc64(pred_r[k]);
             if (!indeg[k]) ready |= 1ull << idrank[k];
@@ -1257,6 +1311,7 @@ __device__ bool s_decoupled(SCtx& C, char* rec, const RecLayout& RL, int& nW, in
             ++nW;
             ++nE;
             now += span;
+            #pragma unroll 1
             for (uint64_t sr = succ_r[k]; sr; sr &= sr - 1) {
                 const int q = by_rank[low_bit(sr)];
                 if (--indeg[q] == 0) ready |= 1ull << idrank[q];
@@ -1312,6 +1367,7 @@ __device__ bool s_schedule_level(SCtx& C, char* rec, const RecLayout& RL, int lv
     int R = 0;
     bool all_defined = true;
     if (lane == 0) {
+        #pragma unroll 1
         for (int i = 0; i < w; ++i) {
             const int k = lm[i];
             S.tk[R] = k, S.tn[R] = up_n[k], S.tl[R] = up_l[k], ++R;
@@ -1321,6 +1377,7 @@ __device__ bool s_schedule_level(SCtx& C, char* rec, const RecLayout& RL, int lv
         }
         C.ctl->i2 = R;
     }
+    #pragma unroll 1
     for (int i = lane; i < w; i += 32) all_defined &= nmax_of[lm[i]] >= C.N;
     all_defined = __all_sync(kFull, all_defined);
     __syncwarp();
@@ -1330,7 +1387,9 @@ __device__ bool s_schedule_level(SCtx& C, char* rec, const RecLayout& RL, int lv
         S.R = R;
         // layers each MetaOp still owes (schedule.hpp:49-61)
         if (lane == 0) {
+            #pragma unroll 1
             for (int i = 0; i < R; ++i) sumlay[S.tk[i]] = 0;
+            #pragma unroll 1
             for (int i = 0; i < R; ++i) sumlay[S.tk[i]] += S.tl[i];
         }
         __syncwarp();
@@ -1378,10 +1437,12 @@ __device__ bool s_schedule_level(SCtx& C, char* rec, const RecLayout& RL, int lv
         now += dur;
         __syncwarp();
         // the sibling tuple (same MetaOp, not selected) gives up the absorbed layers
+        #pragma unroll 1
         for (int j = lane; j < R; j += 32) {
             const int kj = S.tk[j];
             const int ab = absorb[kj];
             bool selected = false;
+            #pragma unroll 1
             for (int i = 0; i < nbest; ++i) selected |= best[i] == j;
             if (ab > 0 && !selected) {
                 const int take = ab < S.tl[j] ? ab : S.tl[j];
@@ -1389,11 +1450,13 @@ __device__ bool s_schedule_level(SCtx& C, char* rec, const RecLayout& RL, int lv
             }
         }
         __syncwarp();
+        #pragma unroll 1
         for (int i = lane; i < nbest; i += 32) absorb[S.tk[best[i]]] = 0;
         __syncwarp();
         // compact the remaining tuples (order kept)
         if (lane == 0) {
             int R2 = 0;
+            #pragma unroll 1
             for (int i = 0; i < R; ++i)
                 if (S.tl[i] > 0) S.tk[R2] = S.tk[i], S.tn[R2] = S.tn[i], S.tl[R2] = S.tl[i], ++R2;
             if (R2 == R) set_err(C.ctl, WS_E_NO_PROGRESS);
@@ -1405,6 +1468,7 @@ __device__ bool s_schedule_level(SCtx& C, char* rec, const RecLayout& RL, int lv
     }
     // merge_levels: level end = max over its waves of start + duration
     double le = offset;
+    #pragma unroll 1
     for (int i = lane; i < nW; i += 32)
         if (w_level[i] == lvl) {
             const double e = w_start[i] + w_dur[i];
@@ -1475,12 +1539,14 @@ __device__ bool s_optimus(SCtx& C, char* rec, const RecLayout& RL, int& nW, int&
     double* tnext = C.at<double>(C.L->tnext);
     int* tnxn = C.at<int>(C.L->tnxn);
     int KE = 0, ncw = 0, npl = 0;
+    #pragma unroll 1
     for (int e = lane; e < WS_MAX_MODULES; e += 32) epred[e] = 0;
     __syncwarp();
     if (lane == 0) {
         auto members = [&](int t) {  // id-rank mask of the task's MetaOps
             const int tr = B.task_rank[R.task_begin + t];
             uint64_t m = 0;
+            #pragma unroll 1
             for (int k = 0; k < K; ++k)
                 if (tmask[mod_of[k]] >> tr & 1ull) m |= 1ull << idrank[k];
             return m;
@@ -1488,6 +1554,7 @@ __device__ bool s_optimus(SCtx& C, char* rec, const RecLayout& RL, int& nW, int&
         auto task_order = [&](uint64_t memr) {  // detail::topo_order over the task view -> vord
             int n = 0;
             uint64_t ready = 0;
+            #pragma unroll 1
             for (uint64_t b = memr; b; b &= b - 1) {
                 const int k = by_rank[low_bit(b)];
                 indeg[k] = popc64(pred_r[k] & memr);
@@ -1498,6 +1565,7 @@ __device__ bool s_optimus(SCtx& C, char* rec, const RecLayout& RL, int& nW, int&
                 ready &= ready - 1;
                 const int k = by_rank[r];
                 vord[n++] = k;
+                #pragma unroll 1
                 for (uint64_t sr = succ_r[k] & memr; sr; sr &= sr - 1) {
                     const int q = by_rank[low_bit(sr)];
                     if (--indeg[q] == 0) ready |= 1ull << idrank[q];
@@ -1510,10 +1578,12 @@ __device__ bool s_optimus(SCtx& C, char* rec, const RecLayout& RL, int& nW, int&
             const uint64_t memr = members(t);
             const int nm = task_order(memr);
             double total = 0.0;
+            #pragma unroll 1
             for (int i = 0; i < nm; ++i) {
                 const int k = vord[i];
                 const double weight = Lk[k] * eval_bf_fit(F, B, gm_of[k], static_cast<double>(n), frac_of(k));
                 double start = 0.0;
+                #pragma unroll 1
                 for (uint64_t p = pred_r[k] & memr; p; p &= p - 1) {
                     const double f = tfin[by_rank[low_bit(p)]];
                     start = start < f ? f : start;
@@ -1523,11 +1593,14 @@ __device__ bool s_optimus(SCtx& C, char* rec, const RecLayout& RL, int& nW, int&
             }
             return total;
         };
+        #pragma unroll 1
         for (int t = 0; t < T && !C.ctl->err; ++t) {  // common valid allocations (valid_allocations per n)
             const int nm = task_order(members(t));
             uint64_t tv = 0;
+            #pragma unroll 1
             for (int n = 1; n <= N && !C.ctl->err; ++n) {
                 bool ok = true;
+                #pragma unroll 1
                 for (int i = 0; i < nm; ++i) {
                     const int k = vord[i];
                     const int tp = B.mod_tp[gm_of[k]];
@@ -1546,6 +1619,7 @@ __device__ bool s_optimus(SCtx& C, char* rec, const RecLayout& RL, int& nW, int&
             tvalid[t] = tv;
         }
         double batch_offset = 0.0;
+        #pragma unroll 1
         for (int b0 = 0; b0 < T && !C.ctl->err;) {  // batches whose minimum allocations fit
             int b1 = b0, used = 0;
             while (b1 < T) {
@@ -1558,6 +1632,7 @@ __device__ bool s_optimus(SCtx& C, char* rec, const RecLayout& RL, int& nW, int&
             // current and at its next allocation is cached and only the grown
             // task's entries are recomputed (the reference re-evaluates both for
             // every task at every step; the values, hence the gains, are identical)
+            #pragma unroll 1
             for (int t = b0; t < b1; ++t) {
                 talloc[t] = low_bit(tvalid[t]) + 1;
                 tcur[t] = -1.0;
@@ -1565,11 +1640,13 @@ __device__ bool s_optimus(SCtx& C, char* rec, const RecLayout& RL, int& nW, int&
             }
             while (true) {  // marginal gain per added device
                 int usedn = 0;
+                #pragma unroll 1
                 for (int t = b0; t < b1; ++t) usedn += talloc[t];
                 const int free = N - usedn;
                 if (free <= 0) break;
                 int best = -1, best_next = 0;
                 double best_gain = -1.0;
+                #pragma unroll 1
                 for (int t = b0; t < b1; ++t) {
                     const uint64_t above = tvalid[t] & ~bits_upto(talloc[t] - 1);  // std::upper_bound
                     if (!above) continue;
@@ -1594,6 +1671,7 @@ __device__ bool s_optimus(SCtx& C, char* rec, const RecLayout& RL, int& nW, int&
             }
             double batch_end = batch_offset;
             int cursor = 0;
+            #pragma unroll 1
             for (int t = b0; t < b1 && !C.ctl->err; ++t) {
                 const uint64_t memr = members(t);
                 const int nm = task_order(memr);
@@ -1602,6 +1680,7 @@ __device__ bool s_optimus(SCtx& C, char* rec, const RecLayout& RL, int& nW, int&
                 pl_wbeg[npl] = ncw;
                 cursor += talloc[t];
                 double now = batch_offset;
+                #pragma unroll 1
                 for (int i = 0; i < nm; ++i) {
                     const int k = vord[i];
                     if (KE >= WS_MAX_MODULES || ncw >= WS_MAX_MODULES) {
@@ -1625,8 +1704,10 @@ __device__ bool s_optimus(SCtx& C, char* rec, const RecLayout& RL, int& nW, int&
                 }
                 pl_wn[npl] = ncw - pl_wbeg[npl];
                 ++npl;
+                #pragma unroll 1
                 for (int i = 0; i < nm; ++i) {  // the task's edges between its entities (deps, scoped)
                     const int k = vord[i];
+                    #pragma unroll 1
                     for (uint64_t pr = pred_r[k] & memr; pr; pr &= pr - 1)
                         epred[ent_of[k]] |= 1ull << ent_of[by_rank[low_bit(pr)]];
                 }
@@ -1644,6 +1725,7 @@ __device__ bool s_optimus(SCtx& C, char* rec, const RecLayout& RL, int& nW, int&
                 return scoped_less(ent_met[ea], B.task_rank[R.task_begin + ent_task[ea]], ent_met[eb],
                                    B.task_rank[R.task_begin + ent_task[eb]]);
             };
+            #pragma unroll 1
             for (int i = 0; i < ncw; ++i) {  // insertion sort (a strict total order: stable or not alike)
                 const int v = i;
                 int j = i;
@@ -1660,6 +1742,7 @@ __device__ bool s_optimus(SCtx& C, char* rec, const RecLayout& RL, int& nW, int&
             int* e_l = reinterpret_cast<int*>(rec + RL.e_l);
             double* e_span = reinterpret_cast<double*>(rec + RL.e_span);
             double end = 0.0;
+            #pragma unroll 1
             for (int i = 0; i < ncw; ++i) {
                 const int c = perm[i];
                 w_level[i] = cw_level[c];
@@ -1680,7 +1763,9 @@ __device__ bool s_optimus(SCtx& C, char* rec, const RecLayout& RL, int& nW, int&
             int* pg_wbeg = reinterpret_cast<int*>(rec + RL.pg_wbeg);
             int* pg_wn = reinterpret_cast<int*>(rec + RL.pg_wn);
             int* pg_list = reinterpret_cast<int*>(rec + RL.pg_list);
+            #pragma unroll 1
             for (int i = 0; i < ncw; ++i) pg_list[perm[i]] = i;  // created wave -> global index
+            #pragma unroll 1
             for (int q = 0; q < npl; ++q) {  // pg_list[created wave] = its global index
                 pg_off[q] = pl_off[q];
                 pg_cnt[q] = pl_cnt[q];
@@ -1739,18 +1824,22 @@ __device__ bool s_distmm(SCtx& C, char* rec, const RecLayout& RL, int& nW, int& 
     double* e_span = reinterpret_cast<double*>(rec + RL.e_span);
     int KE = 0;
     double now = 0.0;
+    #pragma unroll 1
     for (int e = lane; e < WS_MAX_MODULES; e += 32) epred[e] = 0;
+    #pragma unroll 1
     for (int t = 0; t < R.n_tasks; ++t) {
         const int tr = B.task_rank[R.task_begin + t];
         int nm = 0, maxl = 0;
         if (lane == 0) {  // task_view (baselines.hpp:62-73): members in topological order, task levels
             uint64_t memr = 0;  // members as id-rank bits
+            #pragma unroll 1
             for (int k = 0; k < K; ++k) {
                 ent_of[k] = -1;
                 if (tmask[mod_of[k]] >> tr & 1ull) memr |= 1ull << idrank[k];
             }
             int* indeg = C.at<int>(C.L->absorb);
             uint64_t ready = 0;
+            #pragma unroll 1
             for (uint64_t b = memr; b; b &= b - 1) {
                 const int k = by_rank[low_bit(b)];
                 indeg[k] = popc64(pred_r[k] & memr);
@@ -1763,12 +1852,14 @@ __device__ bool s_distmm(SCtx& C, char* rec, const RecLayout& RL, int& nW, int& 
                 const int k = by_rank[r];
                 vord[nm++] = k;
                 int lv = 0;
+                #pragma unroll 1
                 for (uint64_t p = pred_r[k] & memr; p; p &= p - 1) {
                     const int q = tlvl[by_rank[low_bit(p)]] + 1;
                     lv = q > lv ? q : lv;
                 }
                 tlvl[k] = lv;
                 maxl = lv > maxl ? lv : maxl;
+                #pragma unroll 1
                 for (uint64_t sr = succ_r[k] & memr; sr; sr &= sr - 1) {
                     const int q = by_rank[low_bit(sr)];
                     if (--indeg[q] == 0) ready |= 1ull << idrank[q];
@@ -1778,9 +1869,11 @@ __device__ bool s_distmm(SCtx& C, char* rec, const RecLayout& RL, int& nW, int& 
         nm = __shfl_sync(kFull, nm, 0);
         maxl = __shfl_sync(kFull, maxl, 0);
         __syncwarp();
+        #pragma unroll 1
         for (int l = 0; l <= maxl; ++l) {
             int w = 0;
             if (lane == 0) {  // the level's MetaOps in task order; their entities and scaled curves
+                #pragma unroll 1
                 for (int i = 0; i < nm; ++i) {
                     const int k = vord[i];
                     if (tlvl[k] != l) continue;
@@ -1845,6 +1938,7 @@ __device__ bool s_distmm(SCtx& C, char* rec, const RecLayout& RL, int& nW, int& 
             bool ok = s_level_alloc(C, 0, cs);  // sums in task order (LevelInput order)
             if (ok) {
                 if (lane == 0)  // discretized tuples / schedule_level go by MetaOp id
+                    #pragma unroll 1
                     for (int i = 1; i < w; ++i) {
                         const int v = lm[i];
                         int j = i;
@@ -1857,10 +1951,12 @@ __device__ bool s_distmm(SCtx& C, char* rec, const RecLayout& RL, int& nW, int& 
                 ok = s_schedule_level(C, rec, RL, 0, nW, nE, now, level_end, W_CAP, E_CAP);
                 if (ok && lane == 0) {
                     double t_end = 0.0;  // schedule_level's own clock, from 0
+                    #pragma unroll 1
                     for (int x = w0; x < nW; ++x) {
                         w_level[x] = l;
                         t_end += w_dur[x];
                     }
+                    #pragma unroll 1
                     for (int x = e0; x < nE; ++x) e_k[x] = ent_of[e_k[x]];
                     now += t_end;
                 }
@@ -1871,9 +1967,11 @@ __device__ bool s_distmm(SCtx& C, char* rec, const RecLayout& RL, int& nW, int& 
             if (!ok) return false;
         }
         if (lane == 0)  // the task's edges between its entities (deps, scoped)
+            #pragma unroll 1
             for (int i = 0; i < nm; ++i) {
                 const int k = vord[i];
                 const uint64_t* succ_r = C.at<uint64_t>(C.L->succ_r);
+                #pragma unroll 1
                 for (uint64_t sr = succ_r[k]; sr; sr &= sr - 1) {
                     const int q = by_rank[low_bit(sr)];
                     if (ent_of[q] >= 0) epred[ent_of[q]] |= 1ull << ent_of[k];
@@ -1938,6 +2036,7 @@ __device__ __forceinline__ void sched_body(const SchedArgs& A, char* smem_dyn, C
     if (ok) {  // the first k_fit outputs read by k_sched
         int* nmax_of = C.at<int>(C.L->nmax_of);
         const int* gm_of = C.at<int>(C.L->gm_of);
+        #pragma unroll 1
         for (int k = lane; k < C.K; k += 32) nmax_of[k] = C.F->nmax[gm_of[k]];
         __syncwarp();
     }
@@ -1969,6 +2068,7 @@ __device__ __forceinline__ void sched_body(const SchedArgs& A, char* smem_dyn, C
         int* lnw = reinterpret_cast<int*>(rec + A.RL.lvl_nw);
         const bool conc = C.K <= 32;  // every level's bisection at once
         if (conc) s_alloc_concurrent(C, n_levels);
+        #pragma unroll 1
         for (int l = 0; l < n_levels && ok; ++l) {
             double cs = 0.0;
             if (conc) {
@@ -2032,6 +2132,7 @@ __device__ __forceinline__ void sched_body(const SchedArgs& A, char* smem_dyn, C
         const int* ent_task = C.at<int>(A.SL.ent_task);
         const uint64_t* epred = C.at<uint64_t>(A.SL.epred);
         auto trank = [&](int e) { return A.B.task_rank[R.task_begin + ent_task[e]]; };
+        #pragma unroll 1
         for (int e = lane; e < K; e += 32) {
             const int k = ent_met[e];
             r_mod_of[e] = C.at<int>(A.SL.mod_of)[k];
@@ -2041,20 +2142,25 @@ __device__ __forceinline__ void sched_body(const SchedArgs& A, char* smem_dyn, C
             r_met[e] = k;
             r_task[e] = ent_task[e];
             int r = 0;  // entity ids "m<k>@<task>" in std::map order
+            #pragma unroll 1
             for (int e2 = 0; e2 < K; ++e2) r += scoped_less(ent_met[e2], trank(e2), k, trank(e));
             r_idrank[e] = r;
             r_by_rank[r] = e;
         }
         __syncwarp();
+        #pragma unroll 1
         for (int e = lane; e < K; e += 32) {
             uint64_t pr = 0, sr = 0;
+            #pragma unroll 1
             for (uint64_t b = epred[e]; b; b &= b - 1) pr |= 1ull << r_idrank[low_bit(b)];
+            #pragma unroll 1
             for (int e2 = 0; e2 < K; ++e2)
                 if (epred[e2] >> e & 1ull) sr |= 1ull << r_idrank[e2];
             r_pred[e] = pr;
             r_succ[e] = sr;
         }
     } else {
+        #pragma unroll 1
         for (int k = lane; k < K; k += 32) {
             r_mod_of[k] = C.at<int>(A.SL.mod_of)[k];
             r_level[k] = C.at<int>(A.SL.level)[k];

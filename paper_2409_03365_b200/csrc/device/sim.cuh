@@ -85,6 +85,7 @@ __device__ __forceinline__ double eval_bf(const ws_out_piece* pc, int np, double
         const double nmax = pc[np - 1].n_hi;
         const double x = n < nmax ? n : nmax;  // std::min(n, n_max_)
         p = pc + np - 1;
+        #pragma unroll 1
         for (int i = 0; i < np; ++i)  // locate (scaling.hpp:149-154)
             if (x <= pc[i].n_hi + 1e-9) {
                 p = pc + i;
@@ -143,6 +144,7 @@ __device__ __forceinline__ uint64_t sim_find(const SimRec& V, int nW, int lane, 
     if (w < 0 || w >= nW) return 0;
     const ws_out_wave& wv = V.wv[w];
     uint64_t m = 0;
+    #pragma unroll 1
     for (int base = 0; base < wv.n_entries; base += 32) {
         const int i = base + lane;
         uint64_t dm = 0;
@@ -162,6 +164,7 @@ __device__ __forceinline__ uint64_t sim_find(const SimRec& V, int nW, int lane, 
 __device__ __forceinline__ uint64_t sim_find1(const SimRec& V, int nW, int w, int k) {
     if (w < 0 || w >= nW) return 0;
     uint64_t m = 0;
+    #pragma unroll 1
     for (int i = 0; i < V.wv[w].n_entries; ++i) {
         const ws_out_entry& e = V.en[V.wv[w].entry_begin + i];
         if (e.metaop == k && e.devmask) m = e.devmask;
@@ -235,19 +238,23 @@ __global__ void __launch_bounds__(32 * kSimWarps, WS_SIM_MINB) k_sim(SimArgs A) 
     ws_out_violation* vio = reinterpret_cast<ws_out_violation*>(sm + A.SL.vio);
 
     // ---- per-plan tables ------------------------------------------------
+    #pragma unroll 1
     for (int i = 0; i < P.n_islands; ++i) {
         uint64_t m = 0;
+        #pragma unroll 1
         for (int base = 0; base < N; base += 32) {
             const int d = base + lane;
             m |= static_cast<uint64_t>(__ballot_sync(kFull, d < N && B.dev_island[P.dev_begin + d] == i)) << base;
         }
         if (lane == 0) islm[i] = m;
     }
+    #pragma unroll 1
     for (int g = lane; g < G; g += 32) {
         chg[g] = 0;
         gmask[g] = 0;
         gbytes[g] = 0;
     }
+    #pragma unroll 1
     for (int k = lane; k < K; k += 32) {
         const int gm = mbase + V.mo[k].module;
         const int grp = V.mo[k].length == B.mod_layers[gm] ? B.mod_group[gm] : -1;
@@ -257,17 +264,21 @@ __global__ void __launch_bounds__(32 * kSimWarps, WS_SIM_MINB) k_sim(SimArgs A) 
         int r = 0;
         if (scoped) {  // ids "m<metaop>@<task>" (baselines.hpp:49-55)
             const int tk = B.task_rank[P.task_begin + V.sc[k].task];
+            #pragma unroll 1
             for (int j = 0; j < K; ++j)
                 r += scoped_less(V.sc[j].metaop, B.task_rank[P.task_begin + V.sc[j].task], V.sc[k].metaop, tk);
             int users = 0;  // share_fraction: tasks whose flow routes through the module
+            #pragma unroll 1
             for (int t = 0; t < P.n_tasks; ++t) {
                 const int tg = P.task_begin + t;
                 bool in = false;
+                #pragma unroll 1
                 for (int i = 0; i < B.task_tok_n[tg] && !in; ++i) in = B.tokens[B.task_tok_off[tg] + i] == V.mo[k].module;
                 users += in;
             }
             efrac[k] = users ? 1.0 / static_cast<double>(users) : 1.0;
         } else {
+            #pragma unroll 1
             for (int j = 0; j < K; ++j) r += dec_less(j, k);
             efrac[k] = B.mod_frac ? B.mod_frac[gm] : 1.0;
         }
@@ -275,13 +286,16 @@ __global__ void __launch_bounds__(32 * kSimWarps, WS_SIM_MINB) k_sim(SimArgs A) 
     }
     // replay order: waves by (start, index) (simulate.hpp:208-212)
     bool sorted = true;
+    #pragma unroll 1
     for (int w = lane + 1; w < nW; w += 32) sorted &= !(V.wv[w].start < V.wv[w - 1].start);
     sorted = __all_sync(kFull, sorted);
+    #pragma unroll 1
     for (int w = lane; w < nW; w += 32) {
         int pos = w;
         if (!sorted) {
             pos = 0;
             const double sw = V.wv[w].start;
+            #pragma unroll 1
             for (int j = 0; j < nW; ++j) pos += V.wv[j].start < sw || (V.wv[j].start == sw && j < w);
         }
         ord[pos] = w;
@@ -289,12 +303,15 @@ __global__ void __launch_bounds__(32 * kSimWarps, WS_SIM_MINB) k_sim(SimArgs A) 
     // plan.devices lookups, resolved once: per entry the placement of its
     // (wave, MetaOp) key (the last placed entry with that key), per flow both
     // endpoints; duplicate keys inside a wave flagged for the validator
+    #pragma unroll 1
     for (int w = 0; w < nW; ++w) {
         const int eb = V.wv[w].entry_begin, ne = V.wv[w].n_entries;
+        #pragma unroll 1
         for (int i = lane; i < ne; i += 32) {
             const int k = V.en[eb + i].metaop;
             uint64_t m = 0;
             int flags = 0;
+            #pragma unroll 1
             for (int j = 0; j < ne; ++j) {
                 const ws_out_entry& x = V.en[eb + j];
                 if (x.metaop != k) continue;
@@ -306,15 +323,18 @@ __global__ void __launch_bounds__(32 * kSimWarps, WS_SIM_MINB) k_sim(SimArgs A) 
         }
     }
     __syncwarp();
+    #pragma unroll 1
     for (int f = lane; f < nF; f += 32) {
         const ws_out_flow& x = V.fl[f];
         uint64_t ma = 0, mb = 0;
         if (x.from_wave >= 0 && x.from_wave < nW)
+            #pragma unroll 1
             for (int j = 0; j < V.wv[x.from_wave].n_entries; ++j) {
                 const int e = V.wv[x.from_wave].entry_begin + j;
                 if (V.en[e].metaop == x.from_metaop && V.en[e].devmask) ma = V.en[e].devmask;
             }
         if (x.to_wave >= 0 && x.to_wave < nW)
+            #pragma unroll 1
             for (int j = 0; j < V.wv[x.to_wave].n_entries; ++j) {
                 const int e = V.wv[x.to_wave].entry_begin + j;
                 if (V.en[e].metaop == x.to_metaop && V.en[e].devmask) mb = V.en[e].devmask;
@@ -372,10 +392,12 @@ __global__ void __launch_bounds__(32 * kSimWarps, WS_SIM_MINB) k_sim(SimArgs A) 
         const double scale = backward ? opt.backward_ratio : 1.0;
         const ws_out_wave& wv = V.wv[w];
         uint64_t parts = 0;
+        #pragma unroll 1
         for (int i = lane; i < wv.n_entries; i += 32) parts |= *en_pl(wv.entry_begin + i);
         parts = (static_cast<uint64_t>(__reduce_or_sync(kFull, static_cast<unsigned>(parts >> 32))) << 32) |
                 __reduce_or_sync(kFull, static_cast<unsigned>(parts));
         const double t0 = lane_max2(parts, lane, av0, av1);
+        #pragma unroll 1
         for (int i = 0; i < wv.n_entries; ++i) {
             const uint64_t m = *en_pl(wv.entry_begin + i);
             if (!m) continue;
@@ -390,14 +412,19 @@ __global__ void __launch_bounds__(32 * kSimWarps, WS_SIM_MINB) k_sim(SimArgs A) 
         if (parts >> (lane + 32) & 1ull) av1 = (av1 < rel) ? rel : av1;
     };
     auto flows_where = [&](bool into, int w) {  // flows_into / flows_out_of, in flow order
+        #pragma unroll 1
         for (unsigned b = __ballot_sync(kFull, (into ? ft0 : ff0) == w); b; b &= b - 1) run_flow(__ffs(b) - 1);
+        #pragma unroll 1
         for (unsigned b = __ballot_sync(kFull, (into ? ft1 : ff1) == w); b; b &= b - 1) run_flow(32 + __ffs(b) - 1);
+        #pragma unroll 1
         for (int base = 64; base < nF; base += 32) {
             const int f = base + lane;
             const bool hit = f < nF && (into ? V.fl[f].to_wave : V.fl[f].from_wave) == w;
+            #pragma unroll 1
             for (unsigned b = __ballot_sync(kFull, hit); b; b &= b - 1) run_flow(base + __ffs(b) - 1);
         }
     };
+    #pragma unroll 1
     for (int j = 0; j < nW; ++j) {  // forward: transmissions arrive before their consumer wave
         const int w = ord[j];
         flows_where(true, w);
@@ -405,6 +432,7 @@ __global__ void __launch_bounds__(32 * kSimWarps, WS_SIM_MINB) k_sim(SimArgs A) 
         run_wave(w, false);
         attribute(fwd_bwd);
     }
+    #pragma unroll 1
     for (int j = nW - 1; j >= 0; --j) {  // backward: reverse order, gradients mirror the flows
         const int w = ord[j];
         run_wave(w, true);
@@ -413,6 +441,7 @@ __global__ void __launch_bounds__(32 * kSimWarps, WS_SIM_MINB) k_sim(SimArgs A) 
         attribute(send_recv);
     }
     if (!opt.skip_sync) {  // build_param_groups (simulate.hpp:127-165), group-wise sync (:268-276)
+        #pragma unroll 1
         for (int base = 0; base < nE; base += 32) {  // groups: device union and max gradient bytes
             const int e = base + lane;
             int g = -1;
@@ -436,11 +465,13 @@ __global__ void __launch_bounds__(32 * kSimWarps, WS_SIM_MINB) k_sim(SimArgs A) 
         __syncwarp();
         // pool entries: one per distinct device set (first group holding it), bytes summed
         int npool = 0;
+        #pragma unroll 1
         for (int base = 0; base < G; base += 32) {
             const int g = base + lane;
             bool rep = g < G && gmask[g] != 0;
             uint64_t sum = 0;
             if (rep) {
+                #pragma unroll 1
                 for (int h = 0; h < G; ++h)
                     if (gmask[h] == gmask[g]) {
                         if (h < g) rep = false;
@@ -458,6 +489,7 @@ __global__ void __launch_bounds__(32 * kSimWarps, WS_SIM_MINB) k_sim(SimArgs A) 
             rk[s] = -1;
             if (g < G && pord[g] == 1) {
                 int r = 0;
+                #pragma unroll 1
                 for (int h = 0; h < G; ++h) r += pord[h] == 1 && devlist_less(gmask[h], gmask[g]);
                 rk[s] = r;
             }
@@ -466,12 +498,14 @@ __global__ void __launch_bounds__(32 * kSimWarps, WS_SIM_MINB) k_sim(SimArgs A) 
         for (int s = 0; s < 4; ++s)
             if (rk[s] >= 0) pord[rk[s]] = s * 32 + lane;  // pord reused: rank -> group
         __syncwarp();
+        #pragma unroll 1
         for (int r = 0; r < npool; ++r) {
             const int g = pord[r];
             const uint64_t m = gmask[g];
             double dur = 0.0;
             if (popc64(m) >= 2) {
                 int widest = 0, islands = 0;
+                #pragma unroll 1
                 for (int base = 0; base < P.n_islands; base += 32) {
                     const int i = base + lane;
                     const int c = i < P.n_islands ? popc64(m & islm[i]) : 0;
@@ -495,8 +529,10 @@ __global__ void __launch_bounds__(32 * kSimWarps, WS_SIM_MINB) k_sim(SimArgs A) 
 
     // ---- compute_device_memory (validate.hpp:27-50) -----------------------
     double mem0 = 0.0, mem1 = 0.0;
+    #pragma unroll 1
     for (int w = 0; w < nW; ++w) {
         const ws_out_wave& wv = V.wv[w];
+        #pragma unroll 1
         for (int i = 0; i < wv.n_entries; ++i) {
             const int e = wv.entry_begin + i;
             const int k = V.en[e].metaop;
@@ -532,7 +568,9 @@ __global__ void __launch_bounds__(32 * kSimWarps, WS_SIM_MINB) k_sim(SimArgs A) 
         const int gm = mbase + V.mo[k].module;
         const double wk = B.mod_w[gm];
         const double frac = efrac[k];
+        #pragma unroll 1
         for (int w = 0; w < nW; ++w)
+            #pragma unroll 1
             for (int i = 0; i < V.wv[w].n_entries; ++i) {
                 const ws_out_entry& e = V.en[V.wv[w].entry_begin + i];
                 if (e.metaop != k) continue;
@@ -561,10 +599,12 @@ __global__ void __launch_bounds__(32 * kSimWarps, WS_SIM_MINB) k_sim(SimArgs A) 
     const double horizon = R.end_time > 1.0 ? R.end_time : 1.0;  // std::max(1.0, end_time)
     const double tol = 1e-6 * horizon;
     enum { F_DUP = 1, F_UNKNOWN = 2, F_SPAN = 4, F_SPAN_DUR = 8 };
+    #pragma unroll 1
     for (int w = 0; w < nW; ++w) {  // per-wave entry checks with recomputed spans
         const ws_out_wave& wv = V.wv[w];
         int used = 0;
         bool any = false;
+        #pragma unroll 1
         for (int i = lane; i < wv.n_entries; i += 32) {
             const int e = wv.entry_begin + i;
             const int k = V.en[e].metaop;
@@ -592,6 +632,7 @@ __global__ void __launch_bounds__(32 * kSimWarps, WS_SIM_MINB) k_sim(SimArgs A) 
         if (__any_sync(kFull, any)) {
             __syncwarp();
             if (lane == 0)
+                #pragma unroll 1
                 for (int i = 0; i < wv.n_entries; ++i) {
                     const int e = wv.entry_begin + i;
                     const int flags = *en_flags(e), k = V.en[e].metaop;
@@ -616,8 +657,10 @@ __global__ void __launch_bounds__(32 * kSimWarps, WS_SIM_MINB) k_sim(SimArgs A) 
     __syncwarp();
     {  // work completion, entities in id order
         bool bad = false;
+        #pragma unroll 1
         for (int k = lane; k < K; k += 32) bad |= exec[k] != V.mo[k].length;
         if (__any_sync(kFull, bad) && lane == 0)
+            #pragma unroll 1
             for (int r = 0; r < K; ++r) {
                 const int k = by_rank[r];
                 if (exec[k] != V.mo[k].length) fail(WS_V_WORK, -1, k, exec[k], V.mo[k].length, 0);
@@ -634,11 +677,13 @@ __global__ void __launch_bounds__(32 * kSimWarps, WS_SIM_MINB) k_sim(SimArgs A) 
     {  // instantaneous capacity: the first addition event after which active > N
         double bt = 0.0;
         int bn = 0, bi = 0x7fffffff, bact = 0;
+        #pragma unroll 1
         for (int i = lane; i < nE; i += 32) {
             double si, ei_, sj, ej;
             int ni, nj;
             if (!iv_of(i, si, ei_, ni)) continue;
             int act = 0;
+            #pragma unroll 1
             for (int j = 0; j < nE; ++j) {
                 if (!iv_of(j, sj, ej, nj)) continue;
                 if (sj < si || (sj == si && (nj < ni || (nj == ni && j <= i)))) act += nj;
@@ -648,6 +693,7 @@ __global__ void __launch_bounds__(32 * kSimWarps, WS_SIM_MINB) k_sim(SimArgs A) 
             if (act > N && (bi == 0x7fffffff || si < bt || (si == bt && (ni < bn || (ni == bn && i < bi)))))
                 bt = si, bn = ni, bi = i, bact = act;
         }
+        #pragma unroll 1
         for (int off = 16; off; off >>= 1) {
             const double ot = __shfl_xor_sync(kFull, bt, off);
             const int on = __shfl_xor_sync(kFull, bn, off), oi = __shfl_xor_sync(kFull, bi, off),
@@ -668,7 +714,9 @@ __global__ void __launch_bounds__(32 * kSimWarps, WS_SIM_MINB) k_sim(SimArgs A) 
             int fl = 0;
             double pe = 0.0, ps = 0.0;
             bool first = true;
+            #pragma unroll 1
             for (int w = 0; w < nW && !(fl & 2); ++w)
+                #pragma unroll 1
                 for (int i = 0; i < V.wv[w].n_entries; ++i) {
                     const int e = V.wv[w].entry_begin + i;
                     if (V.en[e].metaop != k) continue;
@@ -689,10 +737,13 @@ __global__ void __launch_bounds__(32 * kSimWarps, WS_SIM_MINB) k_sim(SimArgs A) 
         const bool any = __any_sync(kFull, (flag_lo | flag_hi) != 0);
         if (any) {
             if (lane == 0) {
+                #pragma unroll 1
                 for (int r = 0; r < K; ++r) {
                     const int k = by_rank[r];
                     int cnt = 0;
+                    #pragma unroll 1
                     for (int w = 0; w < nW; ++w)  // by_entity lists keep wave / entry order
+                        #pragma unroll 1
                         for (int i = 0; i < V.wv[w].n_entries; ++i)
                             if (V.en[V.wv[w].entry_begin + i].metaop == k) lst[cnt++] = V.wv[w].entry_begin + i;
                     struct ByStart {  // std::sort by interval start (exact libstdc++ emulation)
@@ -700,6 +751,7 @@ __global__ void __launch_bounds__(32 * kSimWarps, WS_SIM_MINB) k_sim(SimArgs A) 
                         __device__ bool operator()(int a, int b) const { return iv[4 * a + 1] < iv[4 * b + 1]; }
                     } cmp{en_iv(0)};
                     ls_sort(lst, cnt, cmp);
+                    #pragma unroll 1
                     for (int i = 0; i + 1 < cnt; ++i)
                         if (en_iv(lst[i])[0] > en_iv(lst[i + 1])[1] + tol) {
                             fail(WS_V_OVERLAP, -1, k, 0, 0, 0);
@@ -710,10 +762,12 @@ __global__ void __launch_bounds__(32 * kSimWarps, WS_SIM_MINB) k_sim(SimArgs A) 
             __syncwarp();
         }
     }
+    #pragma unroll 1
     for (int q = 0; q < R.n_edges; ++q) {  // dependencies, in MetaGraph edge order
         const int from = V.ed[q].from, to = V.ed[q].to;
         double fe = 0.0, ts = horizon * 2;
         bool hf = false, ht = false;
+        #pragma unroll 1
         for (int i = lane; i < nE; i += 32) {
             double s, e;
             int n;
@@ -728,13 +782,16 @@ __global__ void __launch_bounds__(32 * kSimWarps, WS_SIM_MINB) k_sim(SimArgs A) 
         if (lane == 0 && hf && ht && ts + tol < fe) fail(WS_V_DEPENDENCY, -1, from, to, ts, fe);
     }
     bool any_placed = false;
+    #pragma unroll 1
     for (int i = lane; i < nE; i += 32) any_placed |= V.en[i].devmask != 0;
     if (__any_sync(kFull, any_placed)) {
+        #pragma unroll 1
         for (int w = 0; w < nW; ++w) {  // per wave: placed, sized, disjoint (device-list order)
             const ws_out_wave& wv = V.wv[w];
             bool bad = false;
             uint64_t uni = 0;
             int sum = 0;
+            #pragma unroll 1
             for (int i = lane; i < wv.n_entries; i += 32) {
                 const int e = wv.entry_begin + i;
                 const uint64_t m = *en_pl(e);
@@ -748,6 +805,7 @@ __global__ void __launch_bounds__(32 * kSimWarps, WS_SIM_MINB) k_sim(SimArgs A) 
             if (!__any_sync(kFull, bad) && sum == popc64(uni)) continue;
             if (lane == 0) {
                 uint64_t taken = 0;
+                #pragma unroll 1
                 for (int i = 0; i < wv.n_entries; ++i) {
                     const int e = wv.entry_begin + i;
                     const uint64_t m = *en_pl(e);
@@ -756,6 +814,7 @@ __global__ void __launch_bounds__(32 * kSimWarps, WS_SIM_MINB) k_sim(SimArgs A) 
                         continue;
                     }
                     int rot = 0;  // the placed entry's rot orders its device list
+                    #pragma unroll 1
                     for (int j = 0; j < wv.n_entries; ++j) {
                         const ws_out_entry& x = V.en[wv.entry_begin + j];
                         if (x.metaop == V.en[e].metaop && x.devmask) rot = x.rot;
@@ -764,6 +823,7 @@ __global__ void __launch_bounds__(32 * kSimWarps, WS_SIM_MINB) k_sim(SimArgs A) 
                     const uint64_t below = rot >= 64 ? ~0ull : ((1ull << rot) - 1ull);
                     const uint64_t order[2] = {m & ~below, m & below};
                     for (int h = 0; h < 2; ++h)
+                        #pragma unroll 1
                         for (uint64_t b = order[h]; b; b &= b - 1) {
                             const int d = low_bit(b);
                             if (d >= N)
@@ -782,6 +842,7 @@ __global__ void __launch_bounds__(32 * kSimWarps, WS_SIM_MINB) k_sim(SimArgs A) 
             const double mv = h ? mem1 : mem0;
             const int d = lane + 32 * h;
             const unsigned b = __ballot_sync(kFull, d < N && mv > cap);
+            #pragma unroll 1
             for (unsigned q = b; q; q &= q - 1) {
                 const int src = __ffs(q) - 1;
                 const double x = __shfl_sync(kFull, mv, src);
@@ -819,6 +880,7 @@ __global__ void __launch_bounds__(32 * kSimWarps, WS_SIM_MINB) k_sim(SimArgs A) 
             o_util[k] = (ds[s] > 0.0 && peak_rate > 0.0) ? (ls[s] / ds[s]) / peak_rate : 0.0;
     }
     ws_out_violation* o_v = reinterpret_cast<ws_out_violation*>(base + 16ull * N + 16 + 8ull * K);
+    #pragma unroll 1
     for (int i = lane; i < keep; i += 32) o_v[i] = vio[i];
     if (lane == 0) {
         *reinterpret_cast<uint64_t*>(base + 8ull * N) = touched;

@@ -27,3 +27,4 @@ tot = [sum(k) for k in ks]
 best = min(tot)
 print(f"{os.environ.get('WSGPU_LIB', 'default')}: {n / (best / 1000):,.0f} plans/s  "
       f"fit/sched/place ms = {min(k[0] for k in ks):.2f}/{min(k[1] for k in ks):.2f}/{min(k[2] for k in ks):.2f}")
+print(f"soft-cap overflows re-planned: {pl.retry_count}")
