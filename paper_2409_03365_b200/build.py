@@ -59,7 +59,8 @@ def build(verbose: bool = False, force: bool = False, defines: list[str] | None 
     build_dir = BUILD if not name else LIB / ("obj_" + Path(name).stem)
     dflags = [f"-D{d}" for d in (defines or [])]
     build_dir.mkdir(parents=True, exist_ok=True)
-    headers = list((ROOT / "include").rglob("*.h*")) + list((CSRC / "device").glob("*.cuh"))
+    headers = (list((ROOT / "include").rglob("*.h*")) + list((CSRC / "device").glob("*.cuh")) +
+               list((CSRC / "host").glob("*.h*")))
     objs = []
     for src in sorted((CSRC / "host").glob("*.cpp")):
         obj = build_dir / (src.stem + ".o")

@@ -70,20 +70,32 @@ struct DevGuard {
     }
 };
 
+// Device buffer that only grows.  A grown buffer's old block is retired, not
+// freed: cudaFree synchronizes the whole device (every other host thread's
+// context included), and kernels of this ctx still in flight may use it.
+// Growth is geometric (1.5x) so a ctx settles after a few calls.
 struct DevBuf {
     void* p = nullptr;
     size_t n = 0;
+    std::vector<void*> retired;
     bool ensure(size_t bytes) {
         if (bytes <= n) return true;
-        if (p) cudaFree(p);
-        p = nullptr;
-        n = 0;
-        if (cudaMalloc(&p, bytes) != cudaSuccess) return false;
-        n = bytes;
+        const size_t want = std::max(bytes, n + n / 2);
+        void* q = nullptr;
+        if (cudaMalloc(&q, want) != cudaSuccess) {
+            cudaGetLastError();
+            if (want == bytes || cudaMalloc(&q, bytes) != cudaSuccess) return false;
+            n = bytes;
+        } else {
+            n = want;
+        }
+        if (p) retired.push_back(p);
+        p = q;
         return true;
     }
     ~DevBuf() {
         if (p) cudaFree(p);
+        for (void* q : retired) cudaFree(q);
     }
     template <typename T>
     T* as() const {
@@ -276,6 +288,7 @@ struct ws_ctx {
     unsigned long long* counters_dev() { return small_counters ? small_counters : counters.as<unsigned long long>(); }
     uint8_t* small_host = nullptr;  // page-locked staging of the small-batch path
     size_t small_host_n = 0;
+    std::vector<void*> retired_host;  // grown page-locked buffers (cudaFreeHost synchronizes: freed at destroy)
     uint8_t* arena_out() { return d_arena ? d_arena : arena.as<uint8_t>(); }
     uint64_t cap_out() const { return d_arena ? d_cap : arena_cap; }
 };
@@ -550,6 +563,7 @@ void ws_ctx_destroy(ws_ctx* c) {
     if (c->host_tops) cudaFreeHost(c->host_tops);
     if (c->order_pinned) cudaFreeHost(c->order_pinned);
     if (c->small_host) cudaFreeHost(c->small_host);
+    for (void* q : c->retired_host) cudaFreeHost(q);
     delete c;  // DevBuf destructors free device memory on c->device (guarded)
 }
 
@@ -575,7 +589,7 @@ int ws_last_kernel_ms(const ws_ctx* c, double* out, int n) {
 
 namespace {
 // device buffers of a planning call sized for the staged batch, and the k_fit output view
-int prepare_plan(ws_ctx* ctx, FitOut& fo) {
+int prepare_plan(ws_ctx* ctx, FitOut& fo, cudaStream_t st) {
     const ws_batch& B = ctx->dview;
     const int P = B.n_plans, NM = std::max(B.n_modules, 1);
     const LaunchCaps& lc = ctx->caps;
@@ -598,11 +612,16 @@ int prepare_plan(ws_ctx* ctx, FitOut& fo) {
     // bitmap is zeroed only when the pool is (re)allocated -- warps always release
     const long long stride = std::max(static_cast<long long>(lc.pl.W) * (lc.pl.N + lc.pl.G),
                                       static_cast<long long>(lh.pl.W) * (lh.pl.N + lh.pl.G));
-    if (stride > ctx->snap_stride) {
-        cudaDeviceSynchronize();  // no k_place of this ctx may hold a slot
-        if (!ctx->snap.ensure(8ull * stride * kSnapSlots) || !ctx->snap_bits.ensure(4 * ((kSnapSlots + 31) / 32)))
-            return fail(ctx, "cudaMalloc snapshot pool");
-        if (cudaMemset(ctx->snap_bits.p, 0, 4 * ((kSnapSlots + 31) / 32)) != cudaSuccess)
+    // (only k_place<true>, batches with baseline strategies, uses snapshots).
+    // A grown pool is a fresh allocation (the old one stays with any k_place of
+    // this ctx still running), its bits zeroed on the launch stream.
+    if ((lc.baseline || ctx->force_snap) && stride > ctx->snap_stride) {
+        if (!ctx->snap.ensure(8ull * stride * kSnapSlots)) return fail(ctx, "cudaMalloc snapshot pool");
+        if (ctx->snap_bits.p) ctx->snap_bits.retired.push_back(ctx->snap_bits.p);
+        ctx->snap_bits.p = nullptr;
+        ctx->snap_bits.n = 0;
+        if (!ctx->snap_bits.ensure(4 * ((kSnapSlots + 31) / 32))) return fail(ctx, "cudaMalloc snapshot bits");
+        if (cudaMemsetAsync(ctx->snap_bits.p, 0, 4 * ((kSnapSlots + 31) / 32), st) != cudaSuccess)
             return fail(ctx, "cudaMemset snapshot bits");
         ctx->snap_stride = stride;
     }
@@ -634,7 +653,7 @@ int drain_overflow(ws_ctx* ctx, cudaStream_t st) {
     ctx->last_retry = total;
     if (total <= kRetryMax) return 0;
     FitOut fo;
-    if (prepare_plan(ctx, fo)) return 1;
+    if (prepare_plan(ctx, fo, st)) return 1;
     for (long long b = kRetryMax; b < total; b += kRetryMax) {
         const int n = static_cast<int>(std::min<long long>(kRetryMax, total - b));
         if (launch_pair(ctx, st, ctx->caps_hard, fo, ctx->retry_ids.as<int32_t>() + b, nullptr, n, true,
@@ -668,12 +687,13 @@ int ensure_order_pinned(ws_ctx* ctx, int P) {
         ctx->order_ev_pending = false;
     }
     if (ctx->order_pinned_n >= static_cast<size_t>(P)) return 0;
-    if (ctx->order_pinned) cudaFreeHost(ctx->order_pinned);
+    if (ctx->order_pinned) ctx->retired_host.push_back(ctx->order_pinned);
     ctx->order_pinned = nullptr;
+    const size_t want = std::max<size_t>({static_cast<size_t>(P), ctx->order_pinned_n * 3 / 2, 1024});
     ctx->order_pinned_n = 0;
-    if (cudaMallocHost(reinterpret_cast<void**>(&ctx->order_pinned), 4ull * std::max(P, 1)) != cudaSuccess)
+    if (cudaMallocHost(reinterpret_cast<void**>(&ctx->order_pinned), 4ull * want) != cudaSuccess)
         return fail(ctx, "cudaMallocHost launch order");
-    ctx->order_pinned_n = std::max(P, 1);
+    ctx->order_pinned_n = want;
     return 0;
 }
 }  // namespace
@@ -731,7 +751,7 @@ int ws_plan_staged(ws_ctx* ctx, void* stream) {
     ctx->drain_pending = false;  // this call re-plans every plan of the staged batch
     ctx->last_retry = 0;
     FitOut fo;
-    if (prepare_plan(ctx, fo)) return 1;
+    if (prepare_plan(ctx, fo, st)) return 1;
     ctx->small_counters = nullptr;
     auto* counters = ctx->counters_dev();  // [0] arena top [1] overflow top [2] retry count
     CK(cudaMemsetAsync(counters, 0, 64, st));
@@ -824,10 +844,10 @@ int plan_small(ws_ctx* ctx, const ws_batch* in, ws_plan_result* results, uint8_t
     const uint64_t o_order = 256, o_blob = (o_order + 4ull * P + 255) & ~255ull;
     const uint64_t bytes = o_blob + in->blob_bytes;
     if (ctx->small_host_n < bytes) {
-        if (ctx->small_host) cudaFreeHost(ctx->small_host);
+        if (ctx->small_host) ctx->retired_host.push_back(ctx->small_host);
         ctx->small_host = nullptr;
+        const size_t want = std::max<size_t>({bytes, ctx->small_host_n * 3 / 2, 256 << 10});
         ctx->small_host_n = 0;
-        const size_t want = std::max<size_t>(bytes, 64 << 10);
         if (cudaMallocHost(reinterpret_cast<void**>(&ctx->small_host), want) != cudaSuccess)
             return fail(ctx, "cudaMallocHost small-batch staging");
         ctx->small_host_n = want;
@@ -854,7 +874,7 @@ int plan_small(ws_ctx* ctx, const ws_batch* in, ws_plan_result* results, uint8_t
     ctx->sim_valid = false;
     ctx->small_counters = reinterpret_cast<unsigned long long*>(d);
     FitOut fo;
-    if (prepare_plan(ctx, fo)) return 1;
+    if (prepare_plan(ctx, fo, st)) return 1;
     ctx->launches = 0;
     const ws_batch& B = ctx->dview;
     if (B.n_modules > 0) {
@@ -961,7 +981,7 @@ int ws_plan_batch_host(ws_ctx* ctx, const ws_batch* in, ws_plan_result* results,
     if (ctx->arena_cap > arena_cap) return fail(ctx, "ws_plan_batch_host: arena buffer too small");
     ctx->small_counters = nullptr;
     FitOut fo;
-    if (prepare_plan(ctx, fo)) return 1;
+    if (prepare_plan(ctx, fo, st)) return 1;
     auto* counters = ctx->counters_dev();
     auto* tops = ctx->chunk_tops.as<unsigned long long>();
     cudaStream_t sh = ctx->stream2, sd = ctx->stream3;

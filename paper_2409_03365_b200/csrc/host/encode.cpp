@@ -251,7 +251,7 @@ void prepare_all(const std::vector<Problem>& problems, std::vector<PlanScratch>&
 namespace detail {
 bool HostBuffer::ensure(std::size_t bytes) {
     if (bytes <= cap && p) return true;
-    if (p) cudaFreeHost(p);
+    if (p) retired.push_back(p);  // cudaFreeHost would synchronize the device: freed with the buffer
     p = nullptr;
     const std::size_t want = std::max<std::size_t>({bytes, 2 * cap, std::size_t(64) << 10});
     cap = 0;
@@ -266,6 +266,7 @@ bool HostBuffer::ensure(std::size_t bytes) {
 
 HostBuffer::~HostBuffer() {
     if (p) cudaFreeHost(p);
+    for (std::uint8_t* q : retired) cudaFreeHost(q);
 }
 }  // namespace detail
 

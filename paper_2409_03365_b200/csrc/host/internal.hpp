@@ -13,6 +13,7 @@ namespace wsgpu::detail {
 struct HostBuffer {
     std::uint8_t* p = nullptr;
     std::size_t cap = 0;
+    std::vector<std::uint8_t*> retired;  // outgrown blocks, freed with the buffer
     bool ensure(std::size_t bytes);
     ~HostBuffer();
     HostBuffer() = default;
