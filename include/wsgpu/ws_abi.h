@@ -329,6 +329,25 @@ int ws_last_kernel_ms(const ws_ctx* ctx, double* out, int n);
  * plans count as +inf; ties go to the smaller index.  Writes {key, index}. */
 int ws_best_staged(ws_ctx* ctx, int mode, double* key, int64_t* index, void* stream);
 
+/* ---- multi-GPU -------------------------------------------------
+ * One process, several GPUs: plans `in` (HOST memory) sharded over n_ctx
+ * contexts (one per GPU; the same device twice is allowed) as contiguous
+ * blocks of equal estimated cost, each block on its own host thread through
+ * the pipelined host call; results/arena as for ws_plan_batch_host (offsets
+ * into the one arena, bound ws_arena_bound(in)).  Replaces a loop of
+ * wavesched::plan_workload calls (planner.hpp:156-212) spread over the box. */
+int ws_plan_batch_multi(ws_ctx* const* ctxs, int n_ctx, const ws_batch* in, ws_plan_result* results,
+                        uint8_t* arena, uint64_t arena_cap, uint64_t* arena_used);
+/* min-loc over host results: key = end_time / lower_bound (mode 0) or
+ * end_time (mode 1); infeasible plans lose; ties -> smaller index. */
+int ws_best_host(const ws_plan_result* results, int64_t n, int mode, double* key, int64_t* index);
+/* Several processes, one rank per GPU: all-gathers every rank's local best
+ * {key, global index} (16 bytes) over the caller's NCCL communicator
+ * (`nccl_comm` is an ncclComm_t; NCCL is loaded with dlopen) and returns the
+ * global min-loc on every rank (ties -> smaller index; index < 0 = none). */
+int ws_best_nccl(ws_ctx* ctx, void* nccl_comm, int nranks, double local_key, int64_t local_index, double* key,
+                 int64_t* index, void* stream);
+
 /* Profiling aid: SM cycles per planner phase summed over warps since the last
  * call (k_place 0-7, k_sched 10-14); all zero unless built with -DWS_PHASES. */
 int ws_debug_phase_cycles(unsigned long long* out, int n);

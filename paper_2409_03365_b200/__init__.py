@@ -149,6 +149,8 @@ def _load() -> C.CDLL:
         "ws_fetch_results": (C.c_int, [vp, vp, vp, u64, C.POINTER(u64), vp]),
         "ws_last_launch_count": (C.c_int, [vp]),
         "ws_last_retry_count": (C.c_longlong, [vp]),
+        "ws_plan_batch_multi": (C.c_int, [C.POINTER(vp), C.c_int, vp, vp, vp, u64, C.POINTER(u64)]),
+        "ws_best_host": (C.c_int, [vp, i64, C.c_int, C.POINTER(C.c_double), C.POINTER(i64)]),
         "ws_last_kernel_ms": (C.c_int, [vp, C.POINTER(C.c_double), C.c_int]),
         "ws_best_staged": (C.c_int, [vp, C.c_int, C.POINTER(C.c_double), C.POINTER(i64), vp]),
         "ws_arena_bound": (u64, [vp]),
@@ -517,6 +519,24 @@ class Planner:
         buf = (C.c_double * 3)()
         lib.ws_last_kernel_ms(self._h, buf, 3)
         return buf[0], buf[1], buf[2]
+
+
+def plan_batch_multi(planners: "list[Planner]", pset: ProblemSet, out: Results | None = None) -> Results:
+    """One host batch sharded over several planners (one per GPU; the same GPU
+    twice is allowed) in one call: ws_plan_batch_multi, contiguous blocks of
+    equal estimated cost, each on its own host thread."""
+    out, cap = planners[0]._out(pset, out)
+    arr = (C.c_void_p * len(planners))(*[p._h for p in planners])
+    rc = lib.ws_plan_batch_multi(arr, len(planners), pset.batch, out.results, out.arena, cap, C.byref(out.arena_used))
+    planners[0]._ok(rc)
+    return out
+
+
+def best_host(res: Results, n: int, mode: int = 0) -> tuple[float, int]:
+    """min-loc over host results (ws_best_host): gap (mode 0) or makespan (1)."""
+    k, i = C.c_double(0), C.c_int64(-1)
+    lib.ws_best_host(res.results, n, mode, C.byref(k), C.byref(i))
+    return k.value, i.value
 
 
 def plan_workload(workload: str, topology: str, **opts) -> str:

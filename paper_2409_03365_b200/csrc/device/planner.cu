@@ -13,8 +13,11 @@
 // Replaces wavesched::plan_workload (planner.hpp:156-212) for whole batches.
 #include <cuda_runtime.h>
 
+#include <dlfcn.h>
+
 #include <algorithm>
 #include <cstdio>
+#include <limits>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
@@ -914,20 +917,20 @@ int plan_small(ws_ctx* ctx, const ws_batch* in, ws_plan_result* results, uint8_t
 // H2D copy), plan, fetch (two D2H copies).  Kernels always write device memory
 // (zero-copy writes into host memory stall k_place on PCIe: measured 20 ms vs
 // 11 ms per 100k).
-int ws_plan_batch_host(ws_ctx* ctx, const ws_batch* in, ws_plan_result* results, uint8_t* arena,
-                       uint64_t arena_cap, uint64_t* arena_used, void* stream) {
-    DevGuard dg_(ctx->device);
-    cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
-    const int P = in->n_plans;
-    if (P > 0 && P <= kSmallBatch && in->blob && ctx->small_path)
-        return plan_small(ctx, in, results, arena, arena_cap, arena_used, st);
+namespace {
+// The pipelined host call over plans [P0, P1) of `in`: `results` receives the
+// headers of plans P0.. and `arena` the range's records (offsets relative to
+// it).  Only the range's rows of every section travel to the device (sections
+// are plan-ordered, so they are contiguous); the device blob mirrors the host
+// layout, so indices stay absolute.  ws_plan_batch_host runs it over [0, P);
+// ws_plan_batch_multi runs one range per context.
+int host_range(ws_ctx* ctx, const ws_batch* in, int P0, int P1, ws_plan_result* results, uint8_t* arena,
+               uint64_t arena_cap, uint64_t* arena_used, cudaStream_t st) {
+    const int P = in->n_plans, n = P1 - P0;
+    *arena_used = 0;
+    if (n <= 0) return 0;
     int C = ctx->host_chunks;
-    C = std::max(1, std::min({C, kMaxHostChunks, P / 4096}));
-    if (C == 1 || !in->blob) {
-        if (ws_stage_batch(ctx, in, stream)) return 1;
-        if (ws_plan_staged(ctx, stream)) return 1;
-        return ws_fetch_results(ctx, results, arena, arena_cap, arena_used, stream);
-    }
+    C = std::max(1, std::min({C, kMaxHostChunks, n / 4096}));
     if (!ctx->blob.ensure(in->blob_bytes + 256) || !ctx->order.ensure(4ull * P) || !ctx->chunk_tops.ensure(8 * 64))
         return fail(ctx, "cudaMalloc batch");
     char* dblob = ctx->blob.as<char>();
@@ -942,10 +945,11 @@ int ws_plan_batch_host(ws_ctx* ctx, const ws_batch* in, ws_plan_result* results,
     // first/last chunks shorten the exposed first H2D and last D2H copies)
     double wsum = 0, wacc = 0;
     for (int c = 0; c < C; ++c) wsum += c < static_cast<int>(ctx->host_weights.size()) ? ctx->host_weights[c] : 1.0;
-    pb[0] = 0;
+    pb[0] = P0;
     for (int c = 0; c < C; ++c) {
         wacc += c < static_cast<int>(ctx->host_weights.size()) ? ctx->host_weights[c] : 1.0;
-        pb[c + 1] = c + 1 == C ? P : std::max(pb[c] + 1, std::min(P - (C - 1 - c), static_cast<int>(P * (wacc / wsum))));
+        pb[c + 1] = c + 1 == C ? P1
+                               : P0 + std::max(pb[c] - P0 + 1, std::min(n - (C - 1 - c), static_cast<int>(n * (wacc / wsum))));
     }
     // ONE pass over the plan records: launch maxima, per-chunk arena bounds, the
     // evaluation bound and per-chunk LPT key histograms; then one scatter pass
@@ -1093,7 +1097,7 @@ int ws_plan_batch_host(ws_ctx* ctx, const ws_batch* in, ws_plan_result* results,
             CK(q);
             uint64_t top = ctx->host_tops[kMaxHostChunks + c];
             top = std::min<uint64_t>(top, abase[c + 1]);
-            CK(cudaMemcpyAsync(results + pb[c], ctx->results.as<ws_plan_result>() + pb[c],
+            CK(cudaMemcpyAsync(results + (pb[c] - P0), ctx->results.as<ws_plan_result>() + pb[c],
                                sizeof(ws_plan_result) * (pb[c + 1] - pb[c]), cudaMemcpyDeviceToHost, sd));
             if (top > abase[c])
                 CK(cudaMemcpyAsync(arena + abase[c], ctx->arena.as<uint8_t>() + abase[c], top - abase[c],
@@ -1127,7 +1131,7 @@ int ws_plan_batch_host(ws_ctx* ctx, const ws_batch* in, ws_plan_result* results,
         CK(cudaMemcpyAsync(ctx->host_tops + kMaxHostChunks + c, tops + c, 8, cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
         const uint64_t top = std::min<uint64_t>(ctx->host_tops[kMaxHostChunks + c], abase[c + 1]);
-        CK(cudaMemcpyAsync(results + pb[c], ctx->results.as<ws_plan_result>() + pb[c],
+        CK(cudaMemcpyAsync(results + (pb[c] - P0), ctx->results.as<ws_plan_result>() + pb[c],
                            sizeof(ws_plan_result) * (pb[c + 1] - pb[c]), cudaMemcpyDeviceToHost, st));
         if (top > abase[c])
             CK(cudaMemcpyAsync(arena + abase[c], ctx->arena.as<uint8_t>() + abase[c], top - abase[c],
@@ -1143,8 +1147,157 @@ int ws_plan_batch_host(ws_ctx* ctx, const ws_batch* in, ws_plan_result* results,
     ctx->staged_events = false;
     ctx->kernel_ms[0] = ctx->kernel_ms[1] = 0;  // chunked: only the whole pipeline is timed
     if (cudaEventElapsedTime(&ms, ctx->ev[0], ctx->ev[2]) == cudaSuccess) ctx->kernel_ms[2] = ms;
-    ctx->records_on_device = true;
+    // a sub-range leaves the other plans' device records unset: evaluation and
+    // min-loc over the staged batch need a whole-batch call
+    ctx->records_on_device = P0 == 0 && P1 == P;
     *arena_used = used;
+    return 0;
+}
+}  // namespace
+
+int ws_plan_batch_host(ws_ctx* ctx, const ws_batch* in, ws_plan_result* results, uint8_t* arena,
+                       uint64_t arena_cap, uint64_t* arena_used, void* stream) {
+    DevGuard dg_(ctx->device);
+    cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
+    const int P = in->n_plans;
+    if (P > 0 && P <= kSmallBatch && in->blob && ctx->small_path)
+        return plan_small(ctx, in, results, arena, arena_cap, arena_used, st);
+    const int C = std::max(1, std::min({ctx->host_chunks, kMaxHostChunks, P / 4096}));
+    if (C == 1 || !in->blob) {
+        if (ws_stage_batch(ctx, in, stream)) return 1;
+        if (ws_plan_staged(ctx, stream)) return 1;
+        return ws_fetch_results(ctx, results, arena, arena_cap, arena_used, stream);
+    }
+    return host_range(ctx, in, 0, P, results, arena, arena_cap, arena_used, st);
+}
+
+// One batch over several contexts (typically one per GPU of the box), SURVEY
+// §8(e): contiguous plan blocks of equal estimated cost (the LPT key), each
+// planned by host_range on its own host thread into its own slice of the
+// caller's arena; record offsets are rebased to the whole arena.
+int ws_plan_batch_multi(ws_ctx* const* ctxs, int n_ctx, const ws_batch* in, ws_plan_result* results,
+                        uint8_t* arena, uint64_t arena_cap, uint64_t* arena_used) {
+    if (n_ctx <= 0 || !ctxs) return 1;
+    for (int i = 0; i < n_ctx; ++i)
+        if (!ctxs[i]) return 1;
+    const int P = in->n_plans;
+    *arena_used = 0;
+    if (!in->blob) return fail(ctxs[0], "ws_plan_batch_multi: batch must be contiguous (ws_batch.blob)");
+    if (n_ctx == 1) return ws_plan_batch_host(ctxs[0], in, results, arena, arena_cap, arena_used, nullptr);
+    // block boundaries by cumulative cost estimate (modules x (devices + 8))
+    std::vector<double> cum(P + 1, 0.0);
+    for (int p = 0; p < P; ++p) {
+        const ws_plan_rec& r = in->plans[p];
+        cum[p + 1] = cum[p] + static_cast<double>(std::max(r.n_mod, 1)) * (std::max(r.n_dev, 0) + 8);
+    }
+    std::vector<int> pb(n_ctx + 1, P);
+    pb[0] = 0;
+    for (int s = 1; s < n_ctx; ++s)
+        pb[s] = static_cast<int>(std::lower_bound(cum.begin(), cum.end(), cum[P] * s / n_ctx) - cum.begin());
+    for (int s = 1; s <= n_ctx; ++s) pb[s] = std::max(pb[s], pb[s - 1]);
+    std::vector<uint64_t> abase(n_ctx + 1, 0);
+    for (int s = 0; s < n_ctx; ++s)
+        abase[s + 1] = abase[s] + wsi_arena_bound_plans(in->plans + pb[s], pb[s + 1] - pb[s]);
+    if (abase[n_ctx] > arena_cap) return fail(ctxs[0], "ws_plan_batch_multi: arena buffer too small");
+    std::vector<int> rc(n_ctx, 0);
+    std::vector<uint64_t> used(n_ctx, 0);
+    std::vector<std::thread> pool;
+    for (int s = 0; s < n_ctx; ++s)
+        pool.emplace_back([&, s] {
+            ws_ctx* ctx = ctxs[s];
+            DevGuard dg_(ctx->device);
+            rc[s] = host_range(ctx, in, pb[s], pb[s + 1], results + pb[s], arena + abase[s], abase[s + 1] - abase[s],
+                               &used[s], ctx->stream);
+            for (int p = pb[s]; p < pb[s + 1]; ++p)
+                if (results[p].status == WS_STATUS_OK) results[p].offset += abase[s];
+        });
+    for (auto& t : pool) t.join();
+    for (int s = 0; s < n_ctx; ++s) {
+        if (rc[s]) {
+            if (s) ctxs[0]->err = "context " + std::to_string(s) + ": " + ctxs[s]->err;
+            return 1;
+        }
+        if (used[s]) *arena_used = abase[s] + used[s];
+    }
+    return 0;
+}
+
+// min-loc over host results (ties -> smaller index; infeasible plans lose)
+int ws_best_host(const ws_plan_result* results, int64_t n, int mode, double* key, int64_t* index) {
+    double bk = std::numeric_limits<double>::infinity();
+    int64_t bi = -1;
+    for (int64_t p = 0; p < n; ++p) {
+        const ws_plan_result& r = results[p];
+        if (r.status != WS_STATUS_OK) continue;
+        const double k = mode == 0 ? r.end_time / r.lower_bound : r.end_time;
+        if (bi < 0 || k < bk) bk = k, bi = p;
+    }
+    *key = bk;
+    *index = bi;
+    return mode == 0 || mode == 1 ? 0 : 1;
+}
+
+// Global best over the ranks of a multi-process job (one rank per GPU), SURVEY
+// §8(e): every rank's local best {key, global index} is all-gathered as a
+// 16-byte record over the caller's NCCL communicator (NVLink / NVSwitch) and
+// min-located on every rank (ties -> smaller index).  NCCL has no MINLOC; the
+// library loads NCCL with dlopen (no link-time dependency).
+namespace {
+using nccl_allgather_fn = int (*)(const void*, void*, size_t, int, void*, cudaStream_t);
+using nccl_error_fn = const char* (*)(int);
+struct NcclApi {
+    nccl_allgather_fn allgather = nullptr;
+    nccl_error_fn error = nullptr;
+    std::string why;
+};
+const NcclApi& nccl_api() {
+    static const NcclApi api = [] {
+        NcclApi a;
+        void* h = nullptr;
+        if (const char* env = std::getenv("WSGPU_NCCL_LIB")) h = dlopen(env, RTLD_NOW | RTLD_GLOBAL);
+        if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) {
+            a.why = "libnccl.so.2 not found (set WSGPU_NCCL_LIB)";
+            return a;
+        }
+        a.allgather = reinterpret_cast<nccl_allgather_fn>(dlsym(h, "ncclAllGather"));
+        a.error = reinterpret_cast<nccl_error_fn>(dlsym(h, "ncclGetErrorString"));
+        if (!a.allgather) a.why = "ncclAllGather not exported";
+        return a;
+    }();
+    return api;
+}
+}  // namespace
+
+int ws_best_nccl(ws_ctx* ctx, void* nccl_comm, int nranks, double local_key, int64_t local_index, double* key,
+                 int64_t* index, void* stream) {
+    DevGuard dg_(ctx->device);
+    cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
+    const NcclApi& api = nccl_api();
+    if (!api.allgather) return fail(ctx, "ws_best_nccl: " + api.why);
+    if (nranks < 1 || !nccl_comm) return fail(ctx, "ws_best_nccl: bad communicator");
+    if (!ctx->best.ensure(16ull * (nranks + 1))) return fail(ctx, "cudaMalloc min-loc records");
+    struct Rec {
+        double key;
+        int64_t index;
+    };
+    Rec mine{local_index >= 0 ? local_key : std::numeric_limits<double>::infinity(), local_index};
+    auto* dev = ctx->best.as<Rec>();
+    CK(cudaMemcpyAsync(dev, &mine, sizeof(Rec), cudaMemcpyHostToDevice, st));
+    const int r = api.allgather(dev, dev + 1, sizeof(Rec), /*ncclUint8*/ 1, nccl_comm, st);
+    if (r != 0) return fail(ctx, std::string("ncclAllGather: ") + (api.error ? api.error(r) : std::to_string(r)));
+    std::vector<Rec> all(nranks);
+    CK(cudaMemcpyAsync(all.data(), dev + 1, sizeof(Rec) * nranks, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    double bk = std::numeric_limits<double>::infinity();
+    int64_t bi = -1;
+    for (const Rec& x : all) {
+        if (x.index < 0 || x.key != x.key) continue;
+        if (bi < 0 || x.key < bk || (x.key == bk && x.index < bi)) bk = x.key, bi = x.index;
+    }
+    *key = bk;
+    *index = bi;
     return 0;
 }
 
