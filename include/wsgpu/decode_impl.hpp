@@ -35,6 +35,7 @@ struct RecordView {
     const ws_out_entry* en;
     const ws_out_flow* fl;
     const ws_out_scope* sc;
+    const uint64_t* ext;  // device words 1..3 per entry (clusters of more than 64 devices)
 };
 
 inline RecordView record_view(const ws_plan_result& r, const std::uint8_t* arena) {
@@ -56,6 +57,8 @@ inline RecordView record_view(const ws_plan_result& r, const std::uint8_t* arena
     s.fl = reinterpret_cast<const ws_out_flow*>(base + off);
     off += rec_al8(sizeof(ws_out_flow) * r.n_flows);
     s.sc = reinterpret_cast<const ws_out_scope*>(base + off);
+    off += rec_al8(sizeof(ws_out_scope) * r.n_scopes);
+    s.ext = reinterpret_cast<const uint64_t*>(base + off);
     return s;
 }
 
@@ -70,13 +73,21 @@ inline std::vector<int> key_order(const std::vector<std::string>& keys) {
 // plan.devices list of an entry: ascending device index starting at `rot`
 // with wrap-around (the sequential ablation's rolling cursor order,
 // placement.hpp:351-357; rot = 0 for the locality placer's sorted sets)
-inline void entry_devices(const std::vector<int>& devs, const ws_out_entry& e, std::vector<int>& out) {
+// ext: the entry's device words 1..3 (clusters of more than 64 devices), else null
+inline void entry_devices(const std::vector<int>& devs, const ws_out_entry& e, const uint64_t* ext,
+                          std::vector<int>& out) {
     const int N = static_cast<int>(devs.size());
     out.clear();
     for (int i = 0; i < N; ++i) {
         const int d = (e.rot + i) % N;
-        if (e.devmask >> d & 1ull) out.push_back(devs[d]);
+        const uint64_t word = d < 64 ? e.devmask : ext[d / 64 - 1];
+        if (word >> (d & 63) & 1ull) out.push_back(devs[d]);
     }
+}
+
+// any device in the entry's set (0: not placed)
+inline bool entry_placed(const ws_out_entry& e, const uint64_t* ext) {
+    return e.devmask || (ext && (ext[0] | ext[1] | ext[2]));
 }
 
 // Decodes a successful (status OK, not task-scoped) record into `res`.
@@ -100,6 +111,7 @@ void decode_into(const Spec& spec, const Topo& topo, int strategy, double grad_m
 
     const RecordView s = record_view(r, arena);
     const int K = r.n_metaops;
+    const bool wide = topo.devices.size() > 64;
     std::vector<const ModuleT*> mods;
     mods.reserve(spec.modules.size());
     for (const auto& kv : spec.modules) mods.push_back(&kv.second);
@@ -236,11 +248,12 @@ void decode_into(const Spec& spec, const Topo& topo, int strategy, double grad_m
             x.n = e.n;
             x.layers = e.layers;
             x.span = e.span;
-            if (e.devmask) placed.push_back(s.wv[w].entry_begin + i);  // 0: not placed
+            if (entry_placed(e, wide ? s.ext + 3 * (s.wv[w].entry_begin + i) : nullptr))  // else: not placed
+                placed.push_back(s.wv[w].entry_begin + i);
         }
         std::sort(placed.begin(), placed.end(), [&](int a, int b) { return ids[s.en[a].metaop] < ids[s.en[b].metaop]; });
         for (int i : placed) {
-            entry_devices(topo.devices, s.en[i], devs);
+            entry_devices(topo.devices, s.en[i], wide ? s.ext + 3 * i : nullptr, devs);
             plan.devices.emplace_hint(plan.devices.end(), std::make_pair(w, ids[s.en[i].metaop]), devs);
         }
         res.schedule.waves.push_back(std::move(wave));

@@ -26,7 +26,8 @@ extern "C" {
 
 /* Device-side limits of this build (per plan).  A plan exceeding one returns
  * WS_STATUS_LIMIT with err_code naming the limit; nothing falls back to CPU. */
-#define WS_MAX_DEVICES 64   /* device sets are u64 masks                       */
+#define WS_MAX_DEVICES 256  /* device sets: one u64 mask up to 64 devices, four words up to 256 */
+#define WS_MAX_DEVICES_EVAL 64 /* plan evaluation (simulate/validate, plan files) */
 #define WS_MAX_MODULES 64   /* module DAG adjacency is u64 masks               */
 #define WS_MAX_TASKS 64     /* task sets are u64 masks                         */
 #define WS_MAX_PIECES 64    /* fitted pieces per curve (isotonic: nmax-1)      */
@@ -219,7 +220,8 @@ typedef struct ws_out_wave {
 
 typedef struct ws_out_entry {
     double span;         /* layers * T(n)                                        */
-    uint64_t devmask;    /* placement device set (bit i = i-th device id)         */
+    uint64_t devmask;    /* placement device set, devices 0..63 (bit i = i-th device id);
+                            devices 64.. of a wider cluster are in the last section */
     int32_t metaop, n, layers;
     int32_t rot;         /* device-list start index (sequential ablation order)  */
 } ws_out_entry;
@@ -232,9 +234,13 @@ typedef struct ws_out_flow {
     int32_t mode, pad;
 } ws_out_flow;
 
-/* Last section, only for task-scoped strategies (n_scopes > 0): entity k of
- * the record is PlanEntity "m<metaop>@<task id>" (baselines.hpp:49-55); its
- * ws_out_metaop row carries the MetaOp's module, level, length and base curve. */
+/* Section after the flows, only for task-scoped strategies (n_scopes > 0):
+ * entity k of the record is PlanEntity "m<metaop>@<task id>"
+ * (baselines.hpp:49-55); its ws_out_metaop row carries the MetaOp's module,
+ * level, length and base curve.
+ * Last section, only for clusters of more than 64 devices: 3 uint64_t per
+ * entry, words 1..3 of its device set (devices 64..255): entry e's word j at
+ * [3 * e + j - 1]. */
 typedef struct ws_out_scope {
     int32_t metaop, task; /* task = declaration index within the plan */
 } ws_out_scope;

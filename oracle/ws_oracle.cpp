@@ -28,6 +28,10 @@
 
 namespace {
 
+// the restatement keeps device sets in one u64: clusters of up to 64 devices
+// (wider clusters are pinned to the reference directly, tests/golden/wide_cases)
+constexpr int kOracleMaxDevices = 64;
+
 struct Fail {
     int code;
     int64_t a = 0, b = 0;
@@ -248,7 +252,7 @@ public:
     void run(PlanOut& out) {
         N = R.n_dev;
         M = R.n_mod;
-        if (N > WS_MAX_DEVICES) throw Fail{WS_E_LIMIT_DEVICES};
+        if (N > kOracleMaxDevices) throw Fail{WS_E_LIMIT_DEVICES};  // u64 device masks
         if (M > WS_MAX_MODULES) throw Fail{WS_E_LIMIT_MODULES};
         build_graph();          // graph.hpp:97-147 + topo order/contract/levels :66-226
         fit_modules();          // planner.hpp:66-94

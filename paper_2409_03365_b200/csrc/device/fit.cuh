@@ -66,7 +66,7 @@ __global__ void __launch_bounds__(128) k_fit(ws_batch B, FitOut out, int m_begin
     // graph stage now; it waits (griddepcontrol.wait) before reading our output
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     constexpr int kWarps = kLanes > 1 ? 128 / kLanes : 1;
-    __shared__ double s_tv[kWarps][kLanes > 1 ? WS_MAX_DEVICES : 1];
+    __shared__ double s_tv[kWarps][kLanes > 1 ? WS_MAX_DEVICES : 1];  // truth values n = 1..N
     __shared__ double s_fv[kWarps][kLanes > 1 ? 128 : 1];
     const int gt = blockIdx.x * blockDim.x + threadIdx.x;
     const int m = m_begin + gt / kLanes;

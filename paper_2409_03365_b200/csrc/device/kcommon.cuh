@@ -5,6 +5,7 @@
 #pragma once
 #include "common.cuh"
 #include "fit.cuh"
+#include "mask.cuh"
 
 namespace wsdev {
 
@@ -178,40 +179,62 @@ struct InvPre {
     }
 };
 
+// island_matches (common.cuh) over a device-mask type DM (uint64_t or DevMask<W>)
+template <class DM>
+__device__ __forceinline__ int island_matches_dm(const DM& A, const DM& B, int M, int P, const DM* islm,
+                                                 const DM* lowm, int n_isl) {
+    int same = 0;
+#pragma unroll 1
+    for (int a = 0; a < n_isl; ++a) {
+        const int ca = dm_popc(A & islm[a]), cb = dm_popc(B & islm[a]);
+        if (!ca || !cb) continue;
+        const int sa = dm_popc(A & lowm[a]), sb = dm_popc(B & lowm[a]);
+        int q = sa > sb + cb ? (sa - sb - cb) / P : 0;
+#pragma unroll 1
+        for (int off = q * P + sb; off < sa + ca && off < M; off += P) {
+            const int lo = sa > off ? sa : off;
+            const int hi = (sa + ca) < (off + cb) ? (sa + ca) : (off + cb);
+            if (hi > lo) same += hi - lo;
+        }
+    }
+    return same;
+}
+
 // shard_moves (placement.hpp:74-103) on device-index bitmasks; isl = island id per device.
 // Unit i pairs sources[i % S] with targets[i % T] (both sorted by device id).
 // With contiguous islands (islm/lowm given) the island matches are counted in
 // closed form (island_matches), otherwise unit by unit.
-__device__ __forceinline__ void shard_moves(uint64_t from, uint64_t to, uint64_t full, const int* isl,
-                                            const uint64_t* islm, const uint64_t* lowm, int n_isl,
-                                            uint64_t& intra, uint64_t& inter) {
+template <class DM>
+__device__ __forceinline__ void shard_moves(const DM& from, const DM& to, uint64_t full, const int* isl,
+                                            const DM* islm, const DM* lowm, int n_isl, uint64_t& intra,
+                                            uint64_t& inter) {
     intra = inter = 0;
-    if (!from || !to) return;
-    const uint64_t shared = from & to;
-    uint64_t src = from & ~shared, dst = to & ~shared;
-    const int pf = popc64(from), pt = popc64(to);
+    if (!dm_any(from) || !dm_any(to)) return;
+    const DM shared = from & to;
+    DM src = from & ~shared, dst = to & ~shared;
+    const int pf = dm_popc(from), pt = dm_popc(to);
     const int units = pf > pt ? pf : pt;
-    const int moving = units - popc64(shared);
+    const int moving = units - dm_popc(shared);
     if (moving == 0) return;
-    if (!src) src = from;
-    if (!dst) dst = to;
+    if (!dm_any(src)) src = from;
+    if (!dm_any(dst)) dst = to;
     const double unit_bytes = static_cast<double>(full) / static_cast<double>(units);
     const uint64_t bytes = static_cast<uint64_t>(llround(unit_bytes));
     int same = 0;
     if (islm) {
-        const int S = popc64(src);  // one of S, T equals moving; the other list cycles
-        same = S == moving ? island_matches(src, dst, moving, popc64(dst), islm, lowm, n_isl)
-                           : island_matches(dst, src, moving, S, islm, lowm, n_isl);
+        const int S = dm_popc(src);  // one of S, T equals moving; the other list cycles
+        same = S == moving ? island_matches_dm(src, dst, moving, dm_popc(dst), islm, lowm, n_isl)
+                           : island_matches_dm(dst, src, moving, S, islm, lowm, n_isl);
     } else {
-        uint64_t rs = src, rt = dst;
-        #pragma unroll 1
+        DM rs = src, rt = dst;
+#pragma unroll 1
         for (int i = 0; i < moving; ++i) {
-            const int s = low_bit(rs);
-            rs &= rs - 1;
-            if (!rs) rs = src;
-            const int t = low_bit(rt);
-            rt &= rt - 1;
-            if (!rt) rt = dst;
+            const int s = dm_low(rs);
+            rs = dm_drop_low(rs);
+            if (!dm_any(rs)) rs = src;
+            const int t = dm_low(rt);
+            rt = dm_drop_low(rt);
+            if (!dm_any(rt)) rt = dst;
             same += isl[s] == isl[t];
         }
     }
@@ -220,57 +243,35 @@ __device__ __forceinline__ void shard_moves(uint64_t from, uint64_t to, uint64_t
 }
 
 // Score (placement.hpp:265-283)
-struct Score {
+template <class DM>
+struct ScoreT {
     int valid;
     int feasible;
     int islands;
     int rot;
     double inter, intra, displaced, peak;
-    uint64_t devs;
+    DM devs;
 };
 
-__device__ __forceinline__ bool score_less(const Score& a, const Score& b) {
+template <class DM>
+__device__ __forceinline__ bool score_less(const ScoreT<DM>& a, const ScoreT<DM>& b) {
     if (a.feasible != b.feasible) return a.feasible;
     if (a.inter != b.inter) return a.inter < b.inter;
     if (a.intra != b.intra) return a.intra < b.intra;
     if (a.displaced != b.displaced) return a.displaced < b.displaced;
     if (a.islands != b.islands) return a.islands < b.islands;
     if (a.peak != b.peak) return a.peak < b.peak;
-    const uint64_t diff = a.devs ^ b.devs;  // sorted device-list lexicographic order
-    if (!diff) return false;
-    return (a.devs & (diff & (~diff + 1))) != 0;
+    return dm_list_less(a.devs, b.devs);  // sorted device-list lexicographic order
 }
 
-__device__ __forceinline__ Score shfl_xor_score(const Score& s, int m) {
-    Score o;
-    o.valid = __shfl_xor_sync(kFull, s.valid, m);
-    o.feasible = __shfl_xor_sync(kFull, s.feasible, m);
-    o.islands = __shfl_xor_sync(kFull, s.islands, m);
-    o.rot = __shfl_xor_sync(kFull, s.rot, m);
-    o.inter = __shfl_xor_sync(kFull, s.inter, m);
-    o.intra = __shfl_xor_sync(kFull, s.intra, m);
-    o.displaced = __shfl_xor_sync(kFull, s.displaced, m);
-    o.peak = __shfl_xor_sync(kFull, s.peak, m);
-    o.devs = __shfl_xor_sync(kFull, s.devs, m);
-    return o;
-}
-
-#ifdef WS_MINLOC_SHFL
-__device__ __forceinline__ Score warp_min_score(Score s) {
-    #pragma unroll 1
-    for (int off = 16; off; off >>= 1) {
-        const Score o = shfl_xor_score(s, off);
-        if (o.valid && (!s.valid || score_less(o, s))) s = o;
-    }
-    return s;
-}
-#else
 // Same order as score_less, as a field-by-field elimination over 32-bit words
 // with redux.sync: the doubles are all >= +0.0 (sums/maxima of non-negative
 // terms starting at 0.0), whose IEEE bit patterns order like the values; the
-// sorted device-list order is the unsigned order of ~brev(devs).  Stops as
-// soon as one lane is left; the winner's Score is then broadcast once.
-__device__ __forceinline__ Score warp_min_score(const Score& s) {
+// sorted device-list order is the unsigned order of ~brev(devs), word by
+// word.  Stops as soon as one lane is left; the winner's Score is then
+// broadcast once.
+template <class DM>
+__device__ __forceinline__ ScoreT<DM> warp_min_score(const ScoreT<DM>& s) {
     unsigned cand = __ballot_sync(kFull, s.valid);
     if (!cand) return s;  // no lane holds a candidate (s.valid == 0 everywhere)
     const int lane = threadIdx.x & 31;
@@ -281,13 +282,14 @@ __device__ __forceinline__ Score warp_min_score(const Score& s) {
     };
     auto hi = [](double d) { return static_cast<unsigned>(__double_as_longlong(d) >> 32); };
     auto lo = [](double d) { return static_cast<unsigned>(__double_as_longlong(d)); };
-    const uint64_t rd = ~__brevll(s.devs);
-    (void)(stage(s.feasible ? 0u : 1u) || stage(hi(s.inter)) || stage(lo(s.inter)) || stage(hi(s.intra)) ||
-           stage(lo(s.intra)) || stage(hi(s.displaced)) || stage(lo(s.displaced)) ||
-           stage(static_cast<unsigned>(s.islands)) || stage(hi(s.peak)) || stage(lo(s.peak)) ||
-           stage(static_cast<unsigned>(rd >> 32)) || stage(static_cast<unsigned>(rd)));
+    bool one = stage(s.feasible ? 0u : 1u) || stage(hi(s.inter)) || stage(lo(s.inter)) || stage(hi(s.intra)) ||
+               stage(lo(s.intra)) || stage(hi(s.displaced)) || stage(lo(s.displaced)) ||
+               stage(static_cast<unsigned>(s.islands)) || stage(hi(s.peak)) || stage(lo(s.peak));
+#pragma unroll
+    for (int i = 0; i < 2 * MaskTraits<DM>::kWords; ++i)
+        if (!one) one = stage(dm_key_word(s.devs, i));
     const int src = __ffs(cand) - 1;  // equal devs => equal Scores
-    Score o;
+    ScoreT<DM> o;
     o.valid = 1;
     o.feasible = __shfl_sync(kFull, s.feasible, src);
     o.islands = __shfl_sync(kFull, s.islands, src);
@@ -296,10 +298,9 @@ __device__ __forceinline__ Score warp_min_score(const Score& s) {
     o.intra = __shfl_sync(kFull, s.intra, src);
     o.displaced = __shfl_sync(kFull, s.displaced, src);
     o.peak = __shfl_sync(kFull, s.peak, src);
-    o.devs = __shfl_sync(kFull, s.devs, src);
+    o.devs = dm_shfl(s.devs, src);
     return o;
 }
-#endif
 
 __device__ __forceinline__ int warp_sum(int v) {
     #pragma unroll 1

@@ -36,7 +36,8 @@ struct PlSmLayout {
     int bytes;
 };
 
-__host__ __device__ inline PlSmLayout make_pl_layout(const PlaceCaps& c) {
+// mb: bytes of one device mask (8: uint64_t, N <= 64; 32: DevMask<4>, N <= 256)
+__host__ __device__ inline PlSmLayout make_pl_layout(const PlaceCaps& c, int mb = 8) {
     PlSmLayout L{};
     int o = 0;
     auto take = [&](int b) {
@@ -64,27 +65,27 @@ __host__ __device__ inline PlSmLayout make_pl_layout(const PlaceCaps& c) {
     L.e_rot = take(4 * E);
     L.e_prev = take(4 * E);
     L.e_wave = take(4 * E);
-    L.e_mask = take(8 * E);
+    L.e_mask = take(mb * E);
     L.w_eb = take(4 * W);
     L.w_ec = take(4 * W);
     L.w_cursor = take(4 * W);
     L.variant = take(4 * W);
     L.mem = take(8 * N);
     L.isl = take(4 * N);
-    L.islmask = take(8 * c.IS);
-    L.isllow = take(8 * c.IS);
-    L.islfull = take(8 * c.IS);
+    L.islmask = take(mb * c.IS);
+    L.isllow = take(mb * c.IS);
+    L.islfull = take(mb * c.IS);
     L.glist = take(4 * W);
     L.nwin = take(4 * (c.IS + W + 1));  // island window counts, then flows-per-wave marks
-    L.chg = take(8 * c.G);
+    L.chg = take(mb * c.G);
     L.fin_src = take(4 * (M + 1));
     L.fin_bytes = take(8 * (M + 1));
-    L.disp_mask = take(8 * M);
+    L.disp_mask = take(mb * M);
     L.disp_bytes = take(8 * M);
     L.disp_cnt = take(4 * M);
     L.eorder = take(4 * M);
     L.va = take(8 * M);
-    L.cmask = take(8 * (2 * N + M + 1));
+    L.cmask = take(mb * (2 * N + M + 1));
     L.used_if = take(8 * N);
     L.bytes = (o + 15) & ~15;
     return L;
@@ -114,6 +115,7 @@ struct PlaceArgs {
     long long snap_stride;    // 8-byte words per slot
 };
 
+template <class DM>
 struct PCtx {
     const ws_batch* B;
     const ws_plan_rec* R;
@@ -124,7 +126,7 @@ struct PCtx {
     int lane, N, K, mbase, nW, nE, nF, Fcap, G, n_isl;
     int contig;  // every island is one contiguous run of device indices
     int dev_off, dev_cnt;  // device block of the current place() call ([0, N) unless grouped)
-    uint64_t all;
+    DM all;           // devices of the current place() call
     uint64_t* flows;  // this plan's flow list (2 words per flow)
     // plan options hoisted out of the per-attempt loops (registers, not global loads)
     double gmul1;     // 1 + grad_opt_multiplier
@@ -145,44 +147,45 @@ __device__ __forceinline__ uint64_t pack_flow(int fw, int fk, int tw, int tk, in
 }
 
 // One wave: 1 placed, 0 infeasible (caller tries the next variant), -1 error.
-__device__ int p_wave(PCtx& C, int w, int variant) {
+template <class DM>
+__device__ int p_wave(PCtx<DM>& C, int w, int variant) {
     const PlSmLayout& L = *C.L;
     const ws_plan_rec& R = *C.R;
     const int lane = C.lane, N = C.N;
-    const int* w_eb = C.at<int>(L.w_eb);
-    const int* w_ec = C.at<int>(L.w_ec);
-    const int* e_k = C.at<int>(L.e_k);
-    const int* e_n = C.at<int>(L.e_n);
-    const int* e_l = C.at<int>(L.e_l);
-    uint64_t* e_mask = C.at<uint64_t>(L.e_mask);
-    int* e_rot = C.at<int>(L.e_rot);
-    const int* e_wave = C.at<int>(L.e_wave);
-    const int* home = C.at<int>(L.home);
-    const int* lastw = C.at<int>(L.lastw);
-    const int* by_rank = C.at<int>(L.by_rank);
-    const int* idrank = C.at<int>(L.idrank);
-    const uint64_t* pred_r = C.at<uint64_t>(L.pred_r);
-    const uint64_t* contb = C.at<uint64_t>(L.contb);
-    const uint64_t* edgeb = C.at<uint64_t>(L.edgeb);
-    const uint64_t* memact = C.at<uint64_t>(L.memact);
-    const uint64_t* parb = C.at<uint64_t>(L.parb);
-    const int* gkey = C.at<int>(L.gkey);
-    const int* tpk = C.at<int>(L.tp);
-    double* mem = C.at<double>(L.mem);
-    uint64_t* chg = C.at<uint64_t>(L.chg);
-    const int* isl = C.at<int>(L.isl);
-    const uint64_t* islmask = C.at<uint64_t>(L.islmask);
-    const uint64_t* cislm = C.contig ? islmask : nullptr;  // closed-form shard_moves
-    const uint64_t* isllow = C.at<uint64_t>(L.isllow);
-    int* nwin = C.at<int>(L.nwin);
-    int* fin_src = C.at<int>(L.fin_src);
-    uint64_t* fin_bytes = C.at<uint64_t>(L.fin_bytes);
-    uint64_t* disp_mask = C.at<uint64_t>(L.disp_mask);
-    double* disp_bytes = C.at<double>(L.disp_bytes);
-    int* disp_cnt = C.at<int>(L.disp_cnt);
-    int* eorder = C.at<int>(L.eorder);
-    uint64_t* va = C.at<uint64_t>(L.va);
-    const int* w_cursor = C.at<int>(L.w_cursor);
+    const int* w_eb = C.template at<int>(L.w_eb);
+    const int* w_ec = C.template at<int>(L.w_ec);
+    const int* e_k = C.template at<int>(L.e_k);
+    const int* e_n = C.template at<int>(L.e_n);
+    const int* e_l = C.template at<int>(L.e_l);
+    DM* e_mask = C.template at<DM>(L.e_mask);
+    int* e_rot = C.template at<int>(L.e_rot);
+    const int* e_wave = C.template at<int>(L.e_wave);
+    const int* home = C.template at<int>(L.home);
+    const int* lastw = C.template at<int>(L.lastw);
+    const int* by_rank = C.template at<int>(L.by_rank);
+    const int* idrank = C.template at<int>(L.idrank);
+    const uint64_t* pred_r = C.template at<uint64_t>(L.pred_r);
+    const uint64_t* contb = C.template at<uint64_t>(L.contb);
+    const uint64_t* edgeb = C.template at<uint64_t>(L.edgeb);
+    const uint64_t* memact = C.template at<uint64_t>(L.memact);
+    const uint64_t* parb = C.template at<uint64_t>(L.parb);
+    const int* gkey = C.template at<int>(L.gkey);
+    const int* tpk = C.template at<int>(L.tp);
+    double* mem = C.template at<double>(L.mem);
+    DM* chg = C.template at<DM>(L.chg);
+    const int* isl = C.template at<int>(L.isl);
+    const DM* islmask = C.template at<DM>(L.islmask);
+    const DM* cislm = C.contig ? islmask : nullptr;  // closed-form shard_moves
+    const DM* isllow = C.template at<DM>(L.isllow);
+    int* nwin = C.template at<int>(L.nwin);
+    int* fin_src = C.template at<int>(L.fin_src);
+    uint64_t* fin_bytes = C.template at<uint64_t>(L.fin_bytes);
+    DM* disp_mask = C.template at<DM>(L.disp_mask);
+    double* disp_bytes = C.template at<double>(L.disp_bytes);
+    int* disp_cnt = C.template at<int>(L.disp_cnt);
+    int* eorder = C.template at<int>(L.eorder);
+    uint64_t* va = C.template at<uint64_t>(L.va);
+    const int* w_cursor = C.template at<int>(L.w_cursor);
     const int eb = w_eb[w], ec = w_ec[w];
 
     WS_PH_START(tw);
@@ -220,8 +223,8 @@ __device__ int p_wave(PCtx& C, int w, int variant) {
     }
     __syncwarp();
     WS_PH_STOP(tw, 1);
-    uint64_t free = C.all;
-    uint64_t placed_now = 0;
+    DM free = C.all;
+    uint64_t placed_now = 0;  // entities placed in this wave (K <= 64)
     int cursor = C.sequential ? w_cursor[w] : 0;
     #pragma unroll 1
     for (int oi = 0; oi < ec; ++oi) {
@@ -255,10 +258,10 @@ __device__ int p_wave(PCtx& C, int w, int variant) {
             const unsigned b = __ballot_sync(kFull, ok);
             if (ok) {
                 const int slot = ndisp + __popc(b & ((1u << lane) - 1u));
-                const uint64_t hm = e_mask[home[e2]];
+                const DM hm = e_mask[home[e2]];
                 disp_mask[slot] = hm;
                 disp_bytes[slot] = static_cast<double>(contb[e2]);
-                disp_cnt[slot] = popc64(hm);
+                disp_cnt[slot] = dm_popc(hm);
             }
             ndisp += __popc(b);
         }
@@ -266,38 +269,38 @@ __device__ int p_wave(PCtx& C, int w, int variant) {
         // memory_delta constants (:132-140)
         const double A = lay * (static_cast<double>(memact[k]) / n);
         const double Pm = C.gmul1 * static_cast<double>(parb[k]) / tpk[k];
-        const uint64_t charged = chg[gkey[k]];
+        const DM charged = chg[gkey[k]];
         const double cap = C.cap;
         // device memory if this entry lands there (memory_delta), once per entry
-        double* used_if = C.at<double>(L.used_if);
+        double* used_if = C.template at<double>(L.used_if);
         #pragma unroll 1
         for (int dv = lane; dv < N; dv += 32) {
             double delta = A;
-            if (!(charged >> dv & 1ull)) delta += Pm;
+            if (!dm_test(charged, dv)) delta += Pm;
             used_if[dv] = mem[dv] + delta;
         }
         __syncwarp();
 
-        auto score_of = [&](uint64_t devs, int rot) {
-            Score s;
+        auto score_of = [&](DM devs, int rot) {
+            ScoreT<DM> s;
             s.valid = 1;
             s.devs = devs;
             s.rot = rot;
             s.islands = 0;
             #pragma unroll 1
-            for (int i = 0; i < C.n_isl; ++i) s.islands += (devs & islmask[i]) != 0;
+            for (int i = 0; i < C.n_isl; ++i) s.islands += dm_any(devs & islmask[i]);
             s.displaced = 0.0;
             #pragma unroll 1
             for (int j = 0; j < ndisp; ++j) {
-                const int ov = popc64(devs & disp_mask[j]);
+                const int ov = dm_popc(devs & disp_mask[j]);
                 if (ov == 0) continue;
                 s.displaced += disp_bytes[j] * static_cast<double>(ov) / static_cast<double>(disp_cnt[j]);
             }
             s.feasible = 1;
             double peak = 0.0;
             #pragma unroll 1
-            for (uint64_t d = devs; d; d &= d - 1) {
-                const double used = used_if[low_bit(d)];
+            for (DM d = devs; dm_any(d); d = dm_drop_low(d)) {
+                const double used = used_if[dm_low(d)];
                 peak = (peak < used) ? used : peak;
             }
             s.feasible = !(peak > cap);  // a device above capacity <=> the maximum is
@@ -314,24 +317,24 @@ __device__ int p_wave(PCtx& C, int w, int variant) {
             return s;
         };
 
-        Score chosen;
+        ScoreT<DM> chosen;
         chosen.valid = 0;
         if (C.sequential) {
-            if (popc64(free) >= n) {  // rolling cursor block (:350-358), within the device block
-                uint64_t m = 0;
+            if (dm_popc(free) >= n) {  // rolling cursor block (:350-358), within the device block
+                DM m = dm_zero<DM>();
                 #pragma unroll 1
-                for (int i = 0; i < n; ++i) m |= 1ull << (C.dev_off + (cursor + i) % C.dev_cnt);
+                for (int i = 0; i < n; ++i) m |= dm_bit<DM>(C.dev_off + (cursor + i) % C.dev_cnt);
                 chosen = score_of(m, C.dev_off + cursor);
                 cursor = (cursor + n) % C.dev_cnt;
             }
         } else {
             // candidate_sets (:223-263): predecessor reuse, island windows, global windows
-            const int nfree = popc64(free);
+            const int nfree = dm_popc(free);
             if (nfree >= n) {
                 int total = nfin;
                 #pragma unroll 1
                 for (int i = 0; i < C.n_isl; ++i) {
-                    const int c = popc64(free & islmask[i]);
+                    const int c = dm_popc(free & islmask[i]);
                     const int nw = c >= n ? c - n + 1 : 0;
                     if (lane == 0) nwin[i] = nw;
                     total += nw;
@@ -340,16 +343,16 @@ __device__ int p_wave(PCtx& C, int w, int variant) {
                 __syncwarp();
                 // compact the candidate list first (ballot + popc), so lanes score
                 // in lockstep: skipping inside the scoring loop would split the warp
-                uint64_t* cmask = C.at<uint64_t>(L.cmask);
+                DM* cmask = C.template at<DM>(L.cmask);
                 int ncand = 0;
                 #pragma unroll 1
                 for (int base = 0; base < total; base += 32) {
                     const int j = base + lane;
-                    uint64_t m = 0;
+                    DM m = dm_zero<DM>();
                     bool keep = false;
                     if (j < nfin) {
                         m = e_mask[fin_src[j]];
-                        keep = popc64(m) == n && !(m & ~free);
+                        keep = dm_popc(m) == n && !dm_any(m & ~free);
                     } else if (j < total) {
                         int r = j - nfin;
                         int i = 0;
@@ -357,13 +360,13 @@ __device__ int p_wave(PCtx& C, int w, int variant) {
                         for (; i < C.n_isl && r >= nwin[i]; ++i) r -= nwin[i];
                         keep = true;
                         if (i < C.n_isl) {
-                            m = window_mask(free & islmask[i], r, n);
+                            m = dm_window(free & islmask[i], r, n);
                         } else {
-                            m = window_mask(free, r, n);
+                            m = dm_window(free, r, n);
                             // with contiguous islands a global window inside one island is
                             // that island's window at the same offset: a duplicate (:232)
 #ifndef WS_NO_DEDUP
-                            keep = !(C.contig && !(m & ~C.at<uint64_t>(L.islfull)[isl[low_bit(m)]]));
+                            keep = !(C.contig && !dm_any(m & ~C.template at<DM>(L.islfull)[isl[dm_low(m)]]));
 #endif
                         }
                     }
@@ -382,15 +385,15 @@ __device__ int p_wave(PCtx& C, int w, int variant) {
                 WS_PH_COUNT(26, (ncand + 31) / 32);
                 WS_PH_COUNT(27, N);
                 const int rounds = oi == 0 ? variant + 1 : 1;  // first entry takes scores[variant]
-                Score prev;
+                ScoreT<DM> prev;
                 prev.valid = 0;
                 #pragma unroll 1
                 for (int rd = 0; rd < rounds; ++rd) {
-                    Score best;
+                    ScoreT<DM> best;
                     best.valid = 0;
                     #pragma unroll 1
                     for (int j = lane; j < ncand; j += 32) {
-                        const Score s = score_of(cmask[j], 0);
+                        const ScoreT<DM> s = score_of(cmask[j], 0);
                         if (prev.valid && !score_less(prev, s)) continue;  // next distinct rank
                         if (!best.valid || score_less(s, best)) best = s;
                     }
@@ -408,9 +411,9 @@ __device__ int p_wave(PCtx& C, int w, int variant) {
         // commit_memory (:142-149), lane per device
         #pragma unroll 1
         for (int dv = lane; dv < N; dv += 32) {
-            if (!(chosen.devs >> dv & 1ull)) continue;
+            if (!dm_test(chosen.devs, dv)) continue;
             double delta = A;
-            if (!(charged >> dv & 1ull)) delta += Pm;
+            if (!dm_test(charged, dv)) delta += Pm;
             mem[dv] += delta;
         }
         if (lane == 0) {
@@ -451,7 +454,10 @@ __device__ int p_wave(PCtx& C, int w, int variant) {
     return 1;
 }
 
-__device__ void p_emit(PCtx& C, int p, const char* rec, const RecLayout& RL, const SchedHdr& h, const PlaceArgs& A) {
+template <class DM>
+__device__ void p_emit(PCtx<DM>& C, int p, const char* rec, const RecLayout& RL, const SchedHdr& h,
+                       const PlaceArgs& A) {
+    constexpr int kExt = MaskTraits<DM>::kWords - 1;  // device words 1.. of each entry (N > 64)
     const int lane = C.lane, K = C.K;
     const ws_batch& B = *C.B;
     const int* r_mod_of = reinterpret_cast<const int*>(rec + RL.mod_of);
@@ -461,7 +467,7 @@ __device__ void p_emit(PCtx& C, int p, const char* rec, const RecLayout& RL, con
     const int* r_lo_n = reinterpret_cast<const int*>(rec + RL.lo_n);
     const int* r_lo_l = reinterpret_cast<const int*>(rec + RL.lo_l);
     const uint64_t* r_succ = reinterpret_cast<const uint64_t*>(rec + RL.succ_r);
-    const int* by_rank = C.at<int>(C.L->by_rank);
+    const int* by_rank = C.template at<int>(C.L->by_rank);
     int npieces = 0, nedges = 0;
     #pragma unroll 1
     for (int k = lane; k < K; k += 32) {
@@ -475,7 +481,7 @@ __device__ void p_emit(PCtx& C, int p, const char* rec, const RecLayout& RL, con
     const uint64_t sz = al8(sizeof(ws_out_metaop) * K) + al8(sizeof(ws_out_level) * nL) +
                         al8(sizeof(ws_out_piece) * npieces) + al8(sizeof(ws_out_edge) * nedges) +
                         al8(sizeof(ws_out_wave) * nW) + al8(sizeof(ws_out_entry) * nE) + al8(sizeof(ws_out_flow) * nF) +
-                        al8(sizeof(ws_out_scope) * nS);
+                        al8(sizeof(ws_out_scope) * nS) + 8ull * kExt * nE;
     unsigned long long off = 0;
     if (lane == 0) off = atomicAdd(A.arena_top, static_cast<unsigned long long>(sz));
     off = __shfl_sync(kFull, off, 0);
@@ -563,8 +569,8 @@ __device__ void p_emit(PCtx& C, int p, const char* rec, const RecLayout& RL, con
     const double* w_start = reinterpret_cast<const double*>(rec + RL.w_start);
     const double* w_dur = reinterpret_cast<const double*>(rec + RL.w_dur);
     const int* w_level = reinterpret_cast<const int*>(rec + RL.w_level);
-    const int* w_eb = C.at<int>(C.L->w_eb);
-    const int* w_ec = C.at<int>(C.L->w_ec);
+    const int* w_eb = C.template at<int>(C.L->w_eb);
+    const int* w_ec = C.template at<int>(C.L->w_ec);
     #pragma unroll 1
     for (int w = lane; w < nW; w += 32) {
         ws_out_wave x;
@@ -576,17 +582,17 @@ __device__ void p_emit(PCtx& C, int p, const char* rec, const RecLayout& RL, con
         x.pad = 0;
         wv[w] = x;
     }
-    const int* e_k = C.at<int>(C.L->e_k);
-    const int* e_n = C.at<int>(C.L->e_n);
-    const int* e_l = C.at<int>(C.L->e_l);
+    const int* e_k = C.template at<int>(C.L->e_k);
+    const int* e_n = C.template at<int>(C.L->e_n);
+    const int* e_l = C.template at<int>(C.L->e_l);
     const double* e_span = reinterpret_cast<const double*>(rec + RL.e_span);
-    const uint64_t* e_mask = C.at<uint64_t>(C.L->e_mask);
-    const int* e_rot = C.at<int>(C.L->e_rot);
+    const DM* e_mask = C.template at<DM>(C.L->e_mask);
+    const int* e_rot = C.template at<int>(C.L->e_rot);
     #pragma unroll 1
     for (int e = lane; e < nE; e += 32) {
         ws_out_entry x;
         x.span = e_span[e];
-        x.devmask = e_mask[e];
+        x.devmask = dm_word(e_mask[e], 0);
         x.metaop = e_k[e];
         x.n = e_n[e];
         x.layers = e_l[e];
@@ -612,6 +618,12 @@ __device__ void p_emit(PCtx& C, int p, const char* rec, const RecLayout& RL, con
         const int* r_task = reinterpret_cast<const int*>(rec + RL.e_task);
         #pragma unroll 1
         for (int k = lane; k < nS; k += 32) sc[k] = ws_out_scope{r_met[k], r_task[k]};
+    }
+    if constexpr (kExt > 0) {  // device words 1..W-1 of entry e at [e * kExt + j - 1] (ws_abi.h)
+        auto* ext = reinterpret_cast<uint64_t*>(base + o + al8(sizeof(ws_out_flow) * nF) +
+                                                al8(sizeof(ws_out_scope) * nS));
+        #pragma unroll 1
+        for (int i = lane; i < nE * kExt; i += 32) ext[i] = dm_word(e_mask[i / kExt], 1 + i % kExt);
     }
     if (lane == 0) {
         ws_plan_result r{};
@@ -661,12 +673,14 @@ __device__ __forceinline__ void snap_release(unsigned* bits, int slot) {
 // kSnap: backtracking restores from per-wave snapshots (instantiated for
 // batches with baseline-strategy plans, whose placements backtrack deep);
 // pure wavefront batches backtrack rarely and keep the replay-only kernel.
-template <bool kSnap>
-__global__ void __launch_bounds__(32 * kPlaceWarps, WS_PLACE_MINB) k_place(PlaceArgs A) {
+// DM: device-mask type (uint64_t: N <= 64, 4 warps per block; DevMask<4>: N <= 256,
+// one warp per block for the larger shared working set).
+template <bool kSnap, class DM = uint64_t, int WARPS = kPlaceWarps, int MINB = WS_PLACE_MINB>
+__global__ void __launch_bounds__(32 * WARPS, MINB) k_place(PlaceArgs A) {
     extern __shared__ __align__(16) char smem_dyn[];
-    __shared__ Ctl ctl_s[kPlaceWarps];
+    __shared__ Ctl ctl_s[WARPS];
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int slot = blockIdx.x * kPlaceWarps + wid;
+    const int slot = blockIdx.x * WARPS + wid;
     if (slot >= A.n_launch) return;
     if (A.n_ids && slot >= *A.n_ids) return;
     const int p = A.plan_ids[slot];
@@ -676,7 +690,7 @@ __global__ void __launch_bounds__(32 * kPlaceWarps, WS_PLACE_MINB) k_place(Place
     Ctl* ctl = &ctl_s[wid];
     if (lane == 0) *ctl = Ctl{};
     const ws_plan_rec& R = A.B.plans[p];
-    PCtx C;
+    PCtx<DM> C;
     C.B = &A.B;
     C.R = &R;
     C.F = &A.fit;
@@ -696,7 +710,7 @@ __global__ void __launch_bounds__(32 * kPlaceWarps, WS_PLACE_MINB) k_place(Place
     C.Fcap = A.caps.F;
     C.G = R.n_groups + h.K;
     C.n_isl = R.n_islands;
-    C.all = C.N == 64 ? ~0ull : ((1ull << C.N) - 1ull);
+    C.all = dm_first<DM>(C.N);
     C.flows = A.flows + static_cast<int64_t>(slot) * A.caps.F * 2;
     const ws_batch& B = A.B;
     const PlSmLayout& L = A.PL;
@@ -715,18 +729,18 @@ __global__ void __launch_bounds__(32 * kPlaceWarps, WS_PLACE_MINB) k_place(Place
     const int* r_idrank = reinterpret_cast<const int*>(rec + A.RL.idrank);
     const uint64_t* r_pred = reinterpret_cast<const uint64_t*>(rec + A.RL.pred_r);
     const double* r_frac = reinterpret_cast<const double*>(rec + A.RL.e_frac);
-    int* by_rank = C.at<int>(L.by_rank);
-    int* idrank = C.at<int>(L.idrank);
-    int* lastw = C.at<int>(L.lastw);
-    int* home = C.at<int>(L.home);
-    int* lastent = C.at<int>(L.lastent);
-    int* gkey = C.at<int>(L.gkey);
-    int* tpk = C.at<int>(L.tp);
-    uint64_t* pred_r = C.at<uint64_t>(L.pred_r);
-    uint64_t* contb = C.at<uint64_t>(L.contb);
-    uint64_t* edgeb = C.at<uint64_t>(L.edgeb);
-    uint64_t* memact = C.at<uint64_t>(L.memact);
-    uint64_t* parb = C.at<uint64_t>(L.parb);
+    int* by_rank = C.template at<int>(L.by_rank);
+    int* idrank = C.template at<int>(L.idrank);
+    int* lastw = C.template at<int>(L.lastw);
+    int* home = C.template at<int>(L.home);
+    int* lastent = C.template at<int>(L.lastent);
+    int* gkey = C.template at<int>(L.gkey);
+    int* tpk = C.template at<int>(L.tp);
+    uint64_t* pred_r = C.template at<uint64_t>(L.pred_r);
+    uint64_t* contb = C.template at<uint64_t>(L.contb);
+    uint64_t* edgeb = C.template at<uint64_t>(L.edgeb);
+    uint64_t* memact = C.template at<uint64_t>(L.memact);
+    uint64_t* parb = C.template at<uint64_t>(L.parb);
     #pragma unroll 1
     for (int k = lane; k < K; k += 32) {
         by_rank[k] = r_by_rank[k];
@@ -754,17 +768,17 @@ __global__ void __launch_bounds__(32 * kPlaceWarps, WS_PLACE_MINB) k_place(Place
     const int* r_e_k = reinterpret_cast<const int*>(rec + A.RL.e_k);
     const int* r_e_n = reinterpret_cast<const int*>(rec + A.RL.e_n);
     const int* r_e_l = reinterpret_cast<const int*>(rec + A.RL.e_l);
-    int* w_eb = C.at<int>(L.w_eb);
-    int* w_ec = C.at<int>(L.w_ec);
-    int* w_cursor = C.at<int>(L.w_cursor);
-    int* variant = C.at<int>(L.variant);
-    int* e_k = C.at<int>(L.e_k);
-    int* e_n = C.at<int>(L.e_n);
-    int* e_l = C.at<int>(L.e_l);
-    int* e_prev = C.at<int>(L.e_prev);
-    int* e_wave = C.at<int>(L.e_wave);
-    uint64_t* e_mask = C.at<uint64_t>(L.e_mask);
-    int* e_rot = C.at<int>(L.e_rot);
+    int* w_eb = C.template at<int>(L.w_eb);
+    int* w_ec = C.template at<int>(L.w_ec);
+    int* w_cursor = C.template at<int>(L.w_cursor);
+    int* variant = C.template at<int>(L.variant);
+    int* e_k = C.template at<int>(L.e_k);
+    int* e_n = C.template at<int>(L.e_n);
+    int* e_l = C.template at<int>(L.e_l);
+    int* e_prev = C.template at<int>(L.e_prev);
+    int* e_wave = C.template at<int>(L.e_wave);
+    DM* e_mask = C.template at<DM>(L.e_mask);
+    int* e_rot = C.template at<int>(L.e_rot);
     #pragma unroll 1
     for (int w = lane; w < nW; w += 32) {
         w_eb[w] = r_w_eb[w];
@@ -776,29 +790,29 @@ __global__ void __launch_bounds__(32 * kPlaceWarps, WS_PLACE_MINB) k_place(Place
         e_k[e] = r_e_k[e];
         e_n[e] = r_e_n[e];
         e_l[e] = r_e_l[e];
-        e_mask[e] = 0;
+        e_mask[e] = dm_zero<DM>();
         e_rot[e] = 0;
     }
-    double* mem = C.at<double>(L.mem);
-    uint64_t* chg = C.at<uint64_t>(L.chg);
-    int* isl = C.at<int>(L.isl);
-    uint64_t* islmask = C.at<uint64_t>(L.islmask);
+    double* mem = C.template at<double>(L.mem);
+    DM* chg = C.template at<DM>(L.chg);
+    int* isl = C.template at<int>(L.isl);
+    DM* islmask = C.template at<DM>(L.islmask);
     #pragma unroll 1
     for (int d = lane; d < N; d += 32) {
         isl[d] = B.dev_island[R.dev_begin + d];
         mem[d] = 0.0;
     }
     #pragma unroll 1
-    for (int g = lane; g < G; g += 32) chg[g] = 0;
+    for (int g = lane; g < G; g += 32) chg[g] = dm_zero<DM>();
     __syncwarp();
-    uint64_t* islfull = C.at<uint64_t>(L.islfull);
+    DM* islfull = C.template at<DM>(L.islfull);
     #pragma unroll 1
     for (int i = 0; i < R.n_islands; ++i) {  // island masks, one ballot per 32 devices
-        uint64_t m = 0;
+        DM m = dm_zero<DM>();
         #pragma unroll 1
         for (int base = 0; base < N; base += 32) {
             const int d = base + lane;
-            m |= static_cast<uint64_t>(__ballot_sync(kFull, d < N && isl[d] == i)) << base;
+            dm_or_bits32(m, base, __ballot_sync(kFull, d < N && isl[d] == i));
         }
         if (lane == 0) islfull[i] = m;
     }
@@ -839,13 +853,14 @@ __global__ void __launch_bounds__(32 * kPlaceWarps, WS_PLACE_MINB) k_place(Place
     const int* r_pg_wbeg = reinterpret_cast<const int*>(rec + A.RL.pg_wbeg);
     const int* r_pg_wn = reinterpret_cast<const int*>(rec + A.RL.pg_wn);
     const int* r_pg_list = reinterpret_cast<const int*>(rec + A.RL.pg_list);
-    int* glist = C.at<int>(L.glist);
+    int* glist = C.template at<int>(L.glist);
     // backtracking state restore: replay (below) until the plan's first failed
     // wave, then per-wave snapshots in a claimed pool slot (identical doubles:
     // a snapshot holds exactly the state the replay rebuilds)
     int snap_slot = -1;       // claimed pool slot (uniform across the warp)
     int snap_hi = -1;         // snapshots 0..snap_hi of this group are valid
-    const int snapN = N, snapW = N + G;  // words per wave state: mem[N], chg[G]
+    constexpr int kMW = MaskTraits<DM>::kWords;
+    const int snapN = N, snapW = N + G * kMW;  // words per wave state: mem[N], chg[G] (kMW words each)
     auto snap_at = [&](int j) { return A.snap + static_cast<long long>(snap_slot) * A.snap_stride +
                                        static_cast<long long>(j) * snapW; };
     auto snap_save = [&](int j) {  // state before wave j
@@ -853,7 +868,8 @@ __global__ void __launch_bounds__(32 * kPlaceWarps, WS_PLACE_MINB) k_place(Place
         #pragma unroll 1
         for (int d = lane; d < snapN; d += 32) dst[d] = mem[d];
         #pragma unroll 1
-        for (int g = lane; g < G; g += 32) reinterpret_cast<uint64_t*>(dst + snapN)[g] = chg[g];
+        for (int g = lane; g < G * kMW; g += 32)
+            reinterpret_cast<uint64_t*>(dst + snapN)[g] = reinterpret_cast<const uint64_t*>(chg)[g];
     };
     #pragma unroll 1
     for (int grp = 0; grp < (n_pg ? n_pg : 1); ++grp) {
@@ -864,18 +880,18 @@ __global__ void __launch_bounds__(32 * kPlaceWarps, WS_PLACE_MINB) k_place(Place
         for (int i = lane; i < gn; i += 32) glist[i] = n_pg ? r_pg_list[r_pg_wbeg[grp] + i] : i;
         C.dev_off = goff;
         C.dev_cnt = gcnt;
-        C.all = (gcnt == 64 ? ~0ull : ((1ull << gcnt) - 1ull)) << goff;
+        C.all = dm_range<DM>(goff, gcnt);
         __syncwarp();
         if (lane == 0) {
             int ni = 0, contig = 1;
             #pragma unroll 1
             for (int i = 0; i < R.n_islands; ++i) {  // sub_topology (baselines.hpp:81-93)
-                const uint64_t m = islfull[i] & C.all;
-                if (!m) continue;
-                const uint64_t run = m >> low_bit(m);
-                if (run & (run + 1)) contig = 0;
+                const DM m = islfull[i] & C.all;
+                if (!dm_any(m)) continue;
+                const int lo = dm_low(m);
+                if (m != dm_range<DM>(lo, dm_popc(m))) contig = 0;  // not one run of device indices
                 islmask[ni] = m;
-                C.at<uint64_t>(L.isllow)[ni] = (1ull << low_bit(m)) - 1ull;
+                C.template at<DM>(L.isllow)[ni] = dm_first<DM>(lo);
                 ++ni;
             }
             int cur = 0;  // sequential-ablation cursor (:331-338) over this call's waves
@@ -896,7 +912,7 @@ __global__ void __launch_bounds__(32 * kPlaceWarps, WS_PLACE_MINB) k_place(Place
         #pragma unroll 1
         for (int d = lane; d < N; d += 32) mem[d] = 0.0;
         #pragma unroll 1
-        for (int g = lane; g < G; g += 32) chg[g] = 0;
+        for (int g = lane; g < G; g += 32) chg[g] = dm_zero<DM>();
         #pragma unroll 1
         for (int k = lane; k < K; k += 32) home[k] = -1;
         __syncwarp();
@@ -906,7 +922,7 @@ __global__ void __launch_bounds__(32 * kPlaceWarps, WS_PLACE_MINB) k_place(Place
     // waves 0..k-1 (their device masks are still in e_mask): entries of one wave
     // use disjoint devices, so per device the additions happen in the same order
     // and the doubles are identical.  Only the flow count is recorded per wave.
-    int* wave_nf = C.at<int>(L.nwin) + C.n_isl;  // [W+1] after the window counts
+    int* wave_nf = C.template at<int>(L.nwin) + C.n_isl;  // [W+1] after the window counts
     long long attempts = 0, budget = gn;
     #pragma unroll 1
     for (int d = 0; d < R.bt_depth; ++d) budget *= (R.bt_branching > 1 ? R.bt_branching : 1);
@@ -929,7 +945,8 @@ __global__ void __launch_bounds__(32 * kPlaceWarps, WS_PLACE_MINB) k_place(Place
             #pragma unroll 1
             for (int d = lane; d < N; d += 32) mem[d] = src[d];
             #pragma unroll 1
-            for (int g = lane; g < G; g += 32) chg[g] = reinterpret_cast<const uint64_t*>(src + snapN)[g];
+            for (int g = lane; g < G * kMW; g += 32)
+                reinterpret_cast<uint64_t*>(chg)[g] = reinterpret_cast<const uint64_t*>(src + snapN)[g];
             snap_hi = k;
             C.nF = wave_nf[k];
             WS_PH_STOP(tr, 6);
@@ -938,13 +955,13 @@ __global__ void __launch_bounds__(32 * kPlaceWarps, WS_PLACE_MINB) k_place(Place
         } else if (dirty) {  // rebuild the state before wave k by replay
             if (kSnap && snap_slot < 0 && A.snap_slots > 0) {
                 int sl = 0;
-                if (lane == 0) sl = snap_claim(A.snap_bits, A.snap_slots, (blockIdx.x * kPlaceWarps + wid) >> 5);
+                if (lane == 0) sl = snap_claim(A.snap_bits, A.snap_slots, (blockIdx.x * WARPS + wid) >> 5);
                 snap_slot = __shfl_sync(kFull, sl, 0);
             }
             #pragma unroll 1
             for (int d = lane; d < N; d += 32) mem[d] = 0.0;
             #pragma unroll 1
-            for (int g = lane; g < G; g += 32) chg[g] = 0;
+            for (int g = lane; g < G; g += 32) chg[g] = dm_zero<DM>();
             __syncwarp();
             #pragma unroll 1
             for (int j = 0; j < k; ++j) {
@@ -959,12 +976,12 @@ __global__ void __launch_bounds__(32 * kPlaceWarps, WS_PLACE_MINB) k_place(Place
                     const int ke = e_k[e];
                     const double Ae = e_l[e] * (static_cast<double>(memact[ke]) / e_n[e]);
                     const double Pe = C.gmul1 * static_cast<double>(parb[ke]) / tpk[ke];
-                    const uint64_t charged = chg[gkey[ke]];
+                    const DM charged = chg[gkey[ke]];
                     #pragma unroll 1
                     for (int dv = lane; dv < N; dv += 32) {
-                        if (!(e_mask[e] >> dv & 1ull)) continue;
+                        if (!dm_test(e_mask[e], dv)) continue;
                         double delta = Ae;
-                        if (!(charged >> dv & 1ull)) delta += Pe;
+                        if (!dm_test(charged, dv)) delta += Pe;
                         mem[dv] += delta;
                     }
                     __syncwarp();

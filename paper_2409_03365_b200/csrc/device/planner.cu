@@ -338,10 +338,13 @@ cudaError_t smem_opt_in_all(int device) {
     static cudaError_t status[64] = {};
     if (device < 0 || device >= 64) return cudaErrorInvalidDevice;
     std::call_once(once[device], [&] {
-        cudaError_t e = smem_opt_in(k_sched);
+        cudaError_t e = smem_opt_in(k_sched<uint64_t>);
+        if (e == cudaSuccess) e = smem_opt_in(k_sched<DevMask<4>>);
         if (e == cudaSuccess) e = smem_opt_in(k_sched_scoped);
         if (e == cudaSuccess) e = smem_opt_in(k_place<true>);
         if (e == cudaSuccess) e = smem_opt_in(k_place<false>);
+        if (e == cudaSuccess) e = smem_opt_in(k_place<true, DevMask<4>, 1, 1>);
+        if (e == cudaSuccess) e = smem_opt_in(k_place<false, DevMask<4>, 1, 1>);
         if (e == cudaSuccess) e = smem_opt_in(k_sim);
         status[device] = e;
     });
@@ -400,6 +403,13 @@ int launch_pair(ws_ctx* ctx, cudaStream_t st, const LaunchCaps& lc, const FitOut
                 const int32_t* n_ids, int n, bool by_slot, char* recs, uint64_t* flows,
                 cudaEvent_t mid = nullptr, int chunks = 1, bool pdl = false);
 
+// 8-byte words of one k_place snapshot slot: W wave states of mem[N] doubles +
+// chg[G] device masks (1 word each up to 64 devices, 4 above)
+long long snap_words(const LaunchCaps& lc) {
+    const int mw = lc.pl.N > 64 ? 4 : 1;
+    return static_cast<long long>(lc.pl.W) * (lc.pl.N + static_cast<long long>(lc.pl.G) * mw);
+}
+
 }  // namespace
 
 namespace {
@@ -414,7 +424,12 @@ int launch_pair(ws_ctx* ctx, cudaStream_t st, const LaunchCaps& lc, const FitOut
     S.fit = fo;
     S.caps = lc.rec;
     S.RL = make_rec_layout(lc.rec);
-    S.SL = make_sm_layout(lc.M, lc.scoped, lc.T);
+    // clusters over 64 devices: DevMask<4> instances (valid sets and device
+    // masks of 4 words), k_place with one warp per block for the wider working set
+    const bool wide = lc.pl.N > 64;
+    const int mb = wide ? static_cast<int>(sizeof(DevMask<4>)) : 8;
+    const int pw = wide ? 1 : kPlaceWarps;
+    S.SL = make_sm_layout(lc.M, lc.scoped, lc.T, mb);
     S.scoped_ok = lc.scoped ? 1 : 0;
     S.recs = recs;
     S.n_ids = n_ids;
@@ -428,7 +443,7 @@ int launch_pair(ws_ctx* ctx, cudaStream_t st, const LaunchCaps& lc, const FitOut
     P.fit = fo;
     P.caps = lc.pl;
     P.RL = S.RL;
-    P.PL = make_pl_layout(lc.pl);
+    P.PL = make_pl_layout(lc.pl, mb);
     P.recs = recs;
     P.flows = flows;
     P.n_ids = n_ids;
@@ -437,15 +452,18 @@ int launch_pair(ws_ctx* ctx, cudaStream_t st, const LaunchCaps& lc, const FitOut
     P.arena = ctx->arena_out();
     P.arena_top = ctx->top_ptr ? ctx->top_ptr : ctx->counters_dev();
     P.arena_cap = ctx->top_ptr ? ctx->top_cap : ctx->cap_out();
-    const bool snap_ok = ctx->snap_stride >= static_cast<long long>(lc.pl.W) * (lc.pl.N + lc.pl.G);
+    const bool snap_ok = ctx->snap_stride >= snap_words(lc);
     P.snap = ctx->snap.as<double>();
     P.snap_bits = ctx->snap_bits.as<unsigned>();
     P.snap_slots = snap_ok ? kSnapSlots : 0;
     P.snap_stride = ctx->snap_stride;
-    if (kPlaceWarps * P.PL.bytes > kSmemLimit) return fail(ctx, "k_place working set exceeds shared memory");
+    if (pw * P.PL.bytes > kSmemLimit) return fail(ctx, "k_place working set exceeds shared memory");
     // measured (100k sweep, ms): snapshots cut decoupled-sequential 9.8 -> 7.9 and
     // distmm-mt 81 -> 47, while the extra code costs wavefront 10.6 -> 11.0
-    auto* kplace = (lc.baseline || ctx->force_snap) ? k_place<true> : k_place<false>;
+    const bool snap = lc.baseline || ctx->force_snap;
+    auto* kplace = wide ? (snap ? k_place<true, DevMask<4>, 1, 1> : k_place<false, DevMask<4>, 1, 1>)
+                        : (snap ? k_place<true> : k_place<false>);
+    auto* ksched = wide ? k_sched<DevMask<4>> : k_sched<uint64_t>;
 
     chunks = std::max(1, std::min(chunks, kMaxChunks));
     if (n_ids || n < 4096) chunks = 1;  // retry pass / small batches: no pipelining
@@ -472,9 +490,9 @@ int launch_pair(ws_ctx* ctx, cudaStream_t st, const LaunchCaps& lc, const FitOut
             attr[0].val.programmaticStreamSerializationAllowed = 1;
             cfg.attrs = attr;
             cfg.numAttrs = 1;
-            CK(cudaLaunchKernelEx(&cfg, k_sched, S));
+            CK(cudaLaunchKernelEx(&cfg, ksched, S));
         } else {
-            k_sched<<<(cnt + kSchedWarps - 1) / kSchedWarps, 32 * kSchedWarps, kSchedWarps * S.SL.bytes, st>>>(S);
+            ksched<<<(cnt + kSchedWarps - 1) / kSchedWarps, 32 * kSchedWarps, kSchedWarps * S.SL.bytes, st>>>(S);
         }
         ctx->launches++;
         if (lc.scoped) {  // the batch's distmm-mt plans (each instance skips the other's plans)
@@ -490,7 +508,7 @@ int launch_pair(ws_ctx* ctx, cudaStream_t st, const LaunchCaps& lc, const FitOut
         }
         P.plan_ids = ids + base;
         P.n_launch = cnt;
-        kplace<<<(cnt + kPlaceWarps - 1) / kPlaceWarps, 32 * kPlaceWarps, kPlaceWarps * P.PL.bytes, sb>>>(P);
+        kplace<<<(cnt + pw - 1) / pw, 32 * pw, pw * P.PL.bytes, sb>>>(P);
         ctx->launches++;
     }
     if (chunks > 1) {
@@ -613,8 +631,7 @@ int prepare_plan(ws_ctx* ctx, FitOut& fo, cudaStream_t st) {
         return fail(ctx, "cudaMalloc planner buffers");
     // backtracking snapshot pool sized for the larger (retry) caps; the claim
     // bitmap is zeroed only when the pool is (re)allocated -- warps always release
-    const long long stride = std::max(static_cast<long long>(lc.pl.W) * (lc.pl.N + lc.pl.G),
-                                      static_cast<long long>(lh.pl.W) * (lh.pl.N + lh.pl.G));
+    const long long stride = std::max(snap_words(lc), snap_words(lh));
     // (only k_place<true>, batches with baseline strategies, uses snapshots).
     // A grown pool is a fresh allocation (the old one stays with any k_place of
     // this ctx still running), its bits zeroed on the launch stream.

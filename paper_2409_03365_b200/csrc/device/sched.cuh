@@ -4,6 +4,7 @@
 // per-plan record in global memory.
 #pragma once
 #include "kcommon.cuh"
+#include "mask.cuh"
 
 namespace wsdev {
 
@@ -94,7 +95,8 @@ struct SmLayout {
 
 // M: MetaOps per plan; scoped: the batch has task-scoped baseline plans;
 // tasks: the batch's largest task count (task-indexed optimus arrays)
-__host__ __device__ inline SmLayout make_sm_layout(int M, bool scoped = false, int tasks = WS_MAX_TASKS) {
+// mb: bytes of one valid-allocation set (8: n <= 64; 32: DevMask<4>, n <= 256)
+__host__ __device__ inline SmLayout make_sm_layout(int M, bool scoped = false, int tasks = WS_MAX_TASKS, int mb = 8) {
     SmLayout L{};
     int o = 0;
     auto take = [&](int b) {
@@ -108,7 +110,7 @@ __host__ __device__ inline SmLayout make_sm_layout(int M, bool scoped = false, i
     L.predk = take(8 * M);
     L.pred_r = take(8 * M);
     L.succ_r = take(8 * M);
-    L.valid = take(8 * M);
+    L.valid = take(mb * M);
     L.credit = take(8 * M);
     L.indeg = take(4 * M);
     L.keyrank = take(4 * M);
@@ -492,12 +494,13 @@ __device__ bool s_fit_status(SCtx& C) {
 // (3a) valid allocation sets n = tp*r with r | B (allocation.hpp:51-63)
 // check_tp: the planner's NoValidAllocation in id order; the baselines check
 // each MetaOp when they reach it (an over-wide tp leaves an empty set).
+template <class DM>
 __device__ bool s_valid(SCtx& C, bool check_tp) {
     const ws_batch& B = *C.B;
     const int K = C.K, N = C.N, lane = C.lane;
     const int* gm_of = C.at<int>(C.L->gm_of);
     const int* by_rank = C.at<int>(C.L->by_rank);
-    uint64_t* valid = C.at<uint64_t>(C.L->valid);
+    DM* valid = C.at<DM>(C.L->valid);
     #pragma unroll 1
     for (int base = 0; base < K && check_tp; base += 32) {  // tp > N in id order (planner.hpp:168-171)
         const int r = base + lane;
@@ -517,7 +520,7 @@ __device__ bool s_valid(SCtx& C, bool check_tp) {
         const int gm = gm_of[k];
         const int tp = B.mod_tp[gm];
         const long long batch = B.mod_batch[gm];
-        uint64_t v = 0;
+        DM v = dm_zero<DM>();
         #pragma unroll 1
         for (int base = 0; base < N; base += 32) {
             const int n = base + lane + 1;
@@ -525,7 +528,7 @@ __device__ bool s_valid(SCtx& C, bool check_tp) {
             if (ok)  // 32-bit remainder when the batch fits (same result, fewer instructions)
                 ok = batch <= 0xffffffffll ? (static_cast<unsigned>(batch) % static_cast<unsigned>(n / tp)) == 0u
                                            : batch % (n / tp) == 0;
-            v |= static_cast<uint64_t>(__ballot_sync(kFull, ok)) << base;
+            dm_or_bits32(v, base, __ballot_sync(kFull, ok));
         }
         if (lane == 0) valid[k] = v;
     }
@@ -544,6 +547,7 @@ __device__ __forceinline__ double ordered_sum(double v0, double v1, int w) {
 
 // repair_capacity (allocation.hpp:107-139) for one level; lane i holds members
 // i, i+32.  Ties and the first error go by MetaOp id (plan.tuples is an id map).
+template <class DM>
 __device__ bool s_level_repair(SCtx& C, int lvl) {
     const int N = C.N, lane = C.lane;
     const int* idrank = C.at<int>(C.L->idrank);
@@ -552,7 +556,7 @@ __device__ bool s_level_repair(SCtx& C, int lvl) {
     const int w = lb[lvl + 1] - lb[lvl];
     const int* gm_of = C.at<int>(C.L->gm_of);
     const int* nmax_of = C.at<int>(C.L->nmax_of);
-    const uint64_t* valid = C.at<uint64_t>(C.L->valid);
+    const DM* valid = C.at<DM>(C.L->valid);
     int* up_n = C.at<int>(C.L->up_n);
     const int* up_l = C.at<int>(C.L->up_l);
     const int* lo_n = C.at<int>(C.L->lo_n);
@@ -575,9 +579,9 @@ __device__ bool s_level_repair(SCtx& C, int lvl) {
             const int k = lm[i];
             const int key = idrank[k];
             const int un = up_n[k];
-            const uint64_t below = valid[k] & ((1ull << (un - 1)) - 1ull);  // valid values < un
-            if (!below) continue;
-            const int target = 64 - __clzll(static_cast<long long>(below));
+            const DM below = valid[k] & dm_first<DM>(un - 1);  // valid values < un
+            if (!dm_any(below)) continue;
+            const int target = dm_high(below) + 1;
             if (lo_l[k] && target <= lo_n[k]) continue;
             const int nmax = nmax_of[k];
             if (target > nmax || un > nmax) {  // eval(target) first, then eval(t.n)
@@ -619,14 +623,15 @@ __device__ bool s_level_repair(SCtx& C, int lvl) {
 // bi-point discretization of one MetaOp (allocation.hpp:149-214).  Returns
 // false on OutOfRange (x = n, y = n_max; eval(n_over) is evaluated first).
 // scale: non-null for a scaled curve (T evaluated from the pieces, not the T-table)
+template <class DM>
 __device__ __forceinline__ bool discretize_one(const FitOut& F, const ws_plan_rec& R, int gm, int L, double nmax,
-                                               uint64_t v, double nstar, double cs, int& un, int& ul, int& ln,
+                                               const DM& v, double nstar, double cs, int& un, int& ul, int& ln,
                                                int& ll, double& ex, const ws_batch* B = nullptr,
                                                double scale = 1.0) {
     int exact = -1, n_over = -1, n_under = -1;
     #pragma unroll 1
-    for (uint64_t b = v; b; b &= b - 1) {
-        const int x = low_bit(b) + 1;
+    for (DM b = v; dm_any(b); b = dm_drop_low(b)) {
+        const int x = dm_low(b) + 1;
         if (fabs(x - nstar) < 1e-9) {
             exact = x;
             break;
@@ -634,8 +639,8 @@ __device__ __forceinline__ bool discretize_one(const FitOut& F, const ws_plan_re
     }
     if (exact < 0)
         #pragma unroll 1
-        for (uint64_t b = v; b; b &= b - 1) {
-            const int x = low_bit(b) + 1;
+        for (DM b = v; dm_any(b); b = dm_drop_low(b)) {
+            const int x = dm_low(b) + 1;
             if (x < nstar) n_under = x;
             if (x > nstar) {
                 n_over = x;
@@ -646,9 +651,9 @@ __device__ __forceinline__ bool discretize_one(const FitOut& F, const ws_plan_re
     if (exact >= 0) {
         un = exact;
     } else if (n_over == -1) {
-        un = 64 - __clzll(static_cast<long long>(v));
+        un = dm_high(v) + 1;
     } else if (n_under == -1) {
-        un = low_bit(v) + 1;
+        un = dm_low(v) + 1;
     } else {
         if (n_over > nmax || n_under > nmax) {
             ex = n_over > nmax ? n_over : n_under;
@@ -689,6 +694,7 @@ __device__ __forceinline__ bool discretize_one(const FitOut& F, const ws_plan_re
 
 // (3b) bisection on the capacity equation, bi-point discretization and
 // capacity repair for one level; lane i holds members i and i+32
+template <class DM>
 __device__ bool s_level_alloc(SCtx& C, int lvl, double& c_star_out) {
     const ws_batch& B = *C.B;
     const ws_plan_rec& R = *C.R;
@@ -699,7 +705,7 @@ __device__ bool s_level_alloc(SCtx& C, int lvl, double& c_star_out) {
     const int* gm_of = C.at<int>(C.L->gm_of);
     const int* nmax_of = C.at<int>(C.L->nmax_of);
     const int* Lk = C.at<int>(C.L->Lk);
-    const uint64_t* valid = C.at<uint64_t>(C.L->valid);
+    const DM* valid = C.at<DM>(C.L->valid);
     int* up_n = C.at<int>(C.L->up_n);
     int* up_l = C.at<int>(C.L->up_l);
     int* lo_n = C.at<int>(C.L->lo_n);
@@ -786,7 +792,7 @@ __device__ bool s_level_alloc(SCtx& C, int lvl, double& c_star_out) {
         }
     }
     __syncwarp();
-    return s_level_repair(C, lvl);
+    return s_level_repair<DM>(C, lvl);
 }
 
 
@@ -795,6 +801,7 @@ __device__ bool s_level_alloc(SCtx& C, int lvl, double& c_star_out) {
 // own lane segment; segment-local ordered sums reproduce each level's
 // reference summation order exactly.  Per level: c* (cstar_sm) and the first
 // discretization OutOfRange (aerr_*), reported in level order by the caller.
+template <class DM>
 __device__ void s_alloc_concurrent(SCtx& C, int n_levels) {
     const ws_batch& B = *C.B;
     const ws_plan_rec& R = *C.R;
@@ -805,7 +812,7 @@ __device__ void s_alloc_concurrent(SCtx& C, int n_levels) {
     const int* gm_of = C.at<int>(C.L->gm_of);
     const int* nmax_of = C.at<int>(C.L->nmax_of);
     const int* Lk = C.at<int>(C.L->Lk);
-    const uint64_t* valid = C.at<uint64_t>(C.L->valid);
+    const DM* valid = C.at<DM>(C.L->valid);
     double* cstar_sm = C.at<double>(C.L->cstar_sm);
     double* aerr_x = C.at<double>(C.L->aerr_x);
     double* aerr_y = C.at<double>(C.L->aerr_y);
@@ -902,20 +909,23 @@ __device__ void s_alloc_concurrent(SCtx& C, int n_levels) {
 // ---------------------------------------------------------------------------
 // (4a) wave scheduling of one level (schedule.hpp:49-288)
 // ---------------------------------------------------------------------------
-struct SchedView {
+template <class DM>
+struct SchedViewT {
     int* tk;
     int* tn;
     int* tl;
     int R;
     const int* sumlay;
     const int* idrank;
-    const uint64_t* valid;
+    const DM* valid;
     int N;
     TErr T;
 };
+using SchedView = SchedViewT<uint64_t>;
 
+template <class SV>
 struct CmpByN {  // schedule.hpp:98-104
-    const SchedView* s;
+    const SV* s;
     __device__ bool operator()(int a, int b) const {
         if (s->tn[a] != s->tn[b]) return s->tn[a] > s->tn[b];
         const double ra = s->tl[a] * s->T(s->tk[a], s->tn[a]);
@@ -924,8 +934,9 @@ struct CmpByN {  // schedule.hpp:98-104
         return s->idrank[s->tk[a]] < s->idrank[s->tk[b]];
     }
 };
+template <class SV>
 struct CmpByTime {  // schedule.hpp:105-111
-    const SchedView* s;
+    const SV* s;
     __device__ bool operator()(int a, int b) const {
         const double ra = s->sumlay[s->tk[a]] * s->T(s->tk[a], s->tn[a]);
         const double rb = s->sumlay[s->tk[b]] * s->T(s->tk[b], s->tn[b]);
@@ -934,8 +945,9 @@ struct CmpByTime {  // schedule.hpp:105-111
         return s->idrank[s->tk[a]] < s->idrank[s->tk[b]];
     }
 };
+template <class SV>
 struct CmpByCheap {  // schedule.hpp:112-118
-    const SchedView* s;
+    const SV* s;
     __device__ bool operator()(int a, int b) const {
         if (s->tn[a] != s->tn[b]) return s->tn[a] < s->tn[b];
         const double ra = s->sumlay[s->tk[a]] * s->T(s->tk[a], s->tn[a]);
@@ -946,7 +958,8 @@ struct CmpByCheap {  // schedule.hpp:112-118
 };
 
 // serial path (lane 0): any tuple count, out-of-range-capable curves
-__device__ void ser_extend(const SchedView& S, int* n, const int* sel, int nsel) {  // schedule.hpp:144-173
+template <class DM>
+__device__ void ser_extend(const SchedViewT<DM>& S, int* n, const int* sel, int nsel) {  // schedule.hpp:144-173
     while (true) {
         int usedn = 0;
         #pragma unroll 1
@@ -959,9 +972,9 @@ __device__ void ser_extend(const SchedView& S, int* n, const int* sel, int nsel)
         for (int i = 0; i < nsel; ++i) {
             const int t = sel[i];
             const int k = S.tk[t];
-            const uint64_t above = S.valid[k] & ~bits_upto(n[t] - 1);
-            if (!above) continue;
-            const int nx = low_bit(above) + 1;
+            const DM above = S.valid[k] & ~dm_first<DM>(n[t]);
+            if (!dm_any(above)) continue;
+            const int nx = dm_low(above) + 1;
             if (nx - n[t] > idle) continue;
             const double rem = S.sumlay[k] * S.T(k, n[t]);
             if (S.T.ctl->err) return;
@@ -976,7 +989,8 @@ __device__ void ser_extend(const SchedView& S, int* n, const int* sel, int nsel)
     }
 }
 
-__device__ int ser_greedy(const SchedView& S, const int* order, int* sel) {
+template <class DM>
+__device__ int ser_greedy(const SchedViewT<DM>& S, const int* order, int* sel) {
     int ns = 0, cap = S.N;
     uint64_t taken = 0;
     #pragma unroll 1
@@ -993,7 +1007,8 @@ __device__ int ser_greedy(const SchedView& S, const int* order, int* sel) {
 
 // One wave on lane 0: propose (3 exact std::sort emulations), extend, align.
 // Fills best[0..nbest) (selection order) and klay[]; returns nbest or -1.
-__device__ int ser_wave(SCtx& C, SchedView& S) {
+template <class DM>
+__device__ int ser_wave(SCtx& C, SchedViewT<DM>& S) {
     int* n2 = C.at<int>(C.L->tn2);
     int* sel = C.at<int>(C.L->sel);
     int* best = C.at<int>(C.L->best);
@@ -1007,11 +1022,11 @@ __device__ int ser_wave(SCtx& C, SchedView& S) {
     const int R = S.R;
     #pragma unroll 1
     for (int i = 0; i < R; ++i) o0[i] = o1[i] = o2[i] = i;
-    CmpByN c0{&S};
+    CmpByN<SchedViewT<DM>> c0{&S};
     ls_sort(o0, R, c0);
-    CmpByTime c1{&S};
+    CmpByTime<SchedViewT<DM>> c1{&S};
     ls_sort(o1, R, c1);
-    CmpByCheap c2{&S};
+    CmpByCheap<SchedViewT<DM>> c2{&S};
     ls_sort(o2, R, c2);
     if (C.ctl->err) return -1;
     int nbest = 0;
@@ -1091,7 +1106,8 @@ __device__ __forceinline__ int warp_argmax_rem(bool cand, double rem, int idr) {
 // extend_resources_if_needed (schedule.hpp:144-173), lanes = selected tuples:
 // grow the tuple whose MetaOp has the most remaining time to its next valid
 // allocation while idle devices remain.
-__device__ __forceinline__ int ext_lanes(bool in, int n, int N, uint64_t vmask, int sl, int idr, const SCtx& C,
+template <class DM>
+__device__ __forceinline__ int ext_lanes(bool in, int n, int N, const DM& vmask, int sl, int idr, const SCtx& C,
                                          int k) {
     const int lane = threadIdx.x & 31;
     while (true) {
@@ -1101,9 +1117,9 @@ __device__ __forceinline__ int ext_lanes(bool in, int n, int N, uint64_t vmask, 
         int nx = 0;
         double rem = 0.0;
         if (in) {
-            const uint64_t above = vmask & ~bits_upto(n - 1);
-            if (above) {
-                nx = low_bit(above) + 1;
+            const DM above = vmask & ~dm_first<DM>(n);
+            if (dm_any(above)) {
+                nx = dm_low(above) + 1;
                 if (nx - n <= idle) {
                     cand = true;
                     rem = sl * T_of(C, k, n);
@@ -1120,7 +1136,8 @@ __device__ __forceinline__ int ext_lanes(bool in, int n, int N, uint64_t vmask, 
 // Fast path (R <= 16 tuples, every curve defined up to N): lanes = tuples.
 // Stable ranks reproduce std::sort exactly for <= 16 elements (insertion
 // sort); greedy runs warp-uniformly; extension/alignment are lane-parallel.
-__device__ int fast_wave(SCtx& C, SchedView& S) {
+template <class DM>
+__device__ int fast_wave(SCtx& C, SchedViewT<DM>& S) {
     const int lane = C.lane, R = S.R, N = S.N;
     const FitOut& F = *C.F;
     const int* gm_of = C.at<int>(C.L->gm_of);
@@ -1135,7 +1152,7 @@ __device__ int fast_wave(SCtx& C, SchedView& S) {
     const int tl = mine ? S.tl[lane] : 0;
     const int sl = mine ? S.sumlay[k] : 0;
     const int idr = mine ? S.idrank[k] : 0;
-    const uint64_t vmask = mine ? S.valid[k] : 0;
+    const DM vmask = mine ? S.valid[k] : dm_zero<DM>();
     const int gm = mine ? gm_of[k] : 0;
     const double T0 = mine ? T_of(C, k, n0) : 0.0;
     const double tt = tl * T0;  // tuple_time
@@ -1240,6 +1257,7 @@ __device__ int fast_wave(SCtx& C, SchedView& S) {
 // plan_decoupled_sequential (baselines.hpp:104-131): every MetaOp alone on
 // its largest valid allocation, one wave each, in lexicographic topological
 // order (detail::topo_order, graph.hpp:67-90); lane 0, K <= 64 steps.
+template <class DM>
 __device__ bool s_decoupled(SCtx& C, char* rec, const RecLayout& RL, int& nW, int& nE, double& end_time, int W_CAP,
                             int E_CAP) {
     const int K = C.K, lane = C.lane;
@@ -1251,7 +1269,7 @@ __device__ bool s_decoupled(SCtx& C, char* rec, const RecLayout& RL, int& nW, in
     const int* level = C.at<int>(C.L->level);
     const uint64_t* pred_r = C.at<uint64_t>(C.L->pred_r);
     const uint64_t* succ_r = C.at<uint64_t>(C.L->succ_r);
-    const uint64_t* valid = C.at<uint64_t>(C.L->valid);
+    const DM* valid = C.at<DM>(C.L->valid);
     int* indeg = C.at<int>(C.L->absorb);
     int* up_n = C.at<int>(C.L->up_n);
     int* up_l = C.at<int>(C.L->up_l);
@@ -1285,7 +1303,7 @@ __device__ bool s_decoupled(SCtx& C, char* rec, const RecLayout& RL, int& nW, in
                 set_err(C.ctl, WS_E_TP_EXCEEDS, k, tp);
                 break;
             }
-            const int n = 64 - __clzll(static_cast<long long>(valid[k]));  // valid.back()
+            const int n = dm_high(valid[k]) + 1;  // valid.back()
             if (n > nmax_of[k]) {  // ScalingCurve::eval OutOfRange (scaling.hpp:66-68)
                 C.ctl->err = WS_E_EVAL_RANGE;
                 C.ctl->x = n;
@@ -1329,6 +1347,7 @@ __device__ bool s_decoupled(SCtx& C, char* rec, const RecLayout& RL, int& nW, in
 }
 
 // (4a) schedule_level + merge_levels offsets; appends waves/entries to the record
+template <class DM>
 __device__ bool s_schedule_level(SCtx& C, char* rec, const RecLayout& RL, int lvl, int& nW, int& nE,
                                  double offset, double& level_end, int W_CAP, int E_CAP) {
     const int lane = C.lane;
@@ -1345,13 +1364,13 @@ __device__ bool s_schedule_level(SCtx& C, char* rec, const RecLayout& RL, int lv
     int* best = C.at<int>(C.L->best);
     int* klay = C.at<int>(C.L->klay);
     int* absorb = C.at<int>(C.L->absorb);
-    SchedView S;
+    SchedViewT<DM> S;
     S.tk = C.at<int>(C.L->tk);
     S.tn = C.at<int>(C.L->tn);
     S.tl = C.at<int>(C.L->tl);
     S.sumlay = sumlay;
     S.idrank = C.at<int>(C.L->idrank);
-    S.valid = C.at<uint64_t>(C.L->valid);
+    S.valid = C.at<DM>(C.L->valid);
     S.N = C.N;
     S.T = TErr{C.F, C.at<int>(C.L->gm_of), nmax_of, C.ctl, C.kscale, C.B};
     int* w_level = reinterpret_cast<int*>(rec + RL.w_level);
@@ -1935,7 +1954,7 @@ __device__ bool s_distmm(SCtx& C, char* rec, const RecLayout& RL, int& nW, int& 
             }
             C.kscale = kscale;
             double cs = 0.0;
-            bool ok = s_level_alloc(C, 0, cs);  // sums in task order (LevelInput order)
+            bool ok = s_level_alloc<uint64_t>(C, 0, cs);  // sums in task order (LevelInput order)
             if (ok) {
                 if (lane == 0)  // discretized tuples / schedule_level go by MetaOp id
                     #pragma unroll 1
@@ -1948,7 +1967,7 @@ __device__ bool s_distmm(SCtx& C, char* rec, const RecLayout& RL, int& nW, int& 
                 __syncwarp();
                 const int w0 = nW, e0 = nE;
                 double level_end = now;
-                ok = s_schedule_level(C, rec, RL, 0, nW, nE, now, level_end, W_CAP, E_CAP);
+                ok = s_schedule_level<uint64_t>(C, rec, RL, 0, nW, nE, now, level_end, W_CAP, E_CAP);
                 if (ok && lane == 0) {
                     double t_end = 0.0;  // schedule_level's own clock, from 0
                     #pragma unroll 1
@@ -1987,7 +2006,7 @@ __device__ bool s_distmm(SCtx& C, char* rec, const RecLayout& RL, int& nW, int& 
 // One warp per plan.  SCOPED: the kernel instance for the task-scoped
 // baselines (distmm-mt); the planner's instance carries none of that code, so
 // its register allocation and instruction stream stay those of the planner.
-template <bool SCOPED>
+template <bool SCOPED, class DM = uint64_t>
 __device__ __forceinline__ void sched_body(const SchedArgs& A, char* smem_dyn, Ctl* ctl_s) {
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int slot = blockIdx.x * kSchedWarps + wid;
@@ -2018,7 +2037,7 @@ __device__ __forceinline__ void sched_body(const SchedArgs& A, char* smem_dyn, C
     if (R.n_mod == 0 && R.n_tasks == 0) {
         ok = false;
         if (lane == 0) ctl->err = WS_E_HOST_PRESET;
-    } else if (R.n_dev > WS_MAX_DEVICES) {
+    } else if (R.n_dev > MaskTraits<DM>::kBits) {  // wider clusters take the DevMask<4> instance
         ok = false;
         if (lane == 0) ctl->err = WS_E_LIMIT_DEVICES;
     } else if (R.n_mod > A.M_cap) {
@@ -2048,12 +2067,12 @@ __device__ __forceinline__ void sched_body(const SchedArgs& A, char* smem_dyn, C
         if (lane == 0) ctl->err = WS_E_LIMIT_MODULES;
         __syncwarp();
     }
-    if (ok) ok = s_valid(C, !decoupled && !scoped);
+    if (ok) ok = s_valid<DM>(C, !decoupled && !scoped);
     WS_PH_STOP(tg, 11);
     int n_levels = 0, nW = 0, nE = 0, KE = 0, n_pg = 0;
     double lower_bound = 0.0, offset = 0.0;
     if (ok && decoupled) {
-        ok = s_decoupled(C, rec, A.RL, nW, nE, offset, A.caps.W, A.caps.E);
+        ok = s_decoupled<DM>(C, rec, A.RL, nW, nE, offset, A.caps.W, A.caps.E);
     } else if (ok && scoped) {
         if constexpr (SCOPED) {
             if (R.strategy == WS_STRATEGY_TASK_OPTIMUS)
@@ -2067,7 +2086,7 @@ __device__ __forceinline__ void sched_body(const SchedArgs& A, char* smem_dyn, C
         int* lfw = reinterpret_cast<int*>(rec + A.RL.lvl_fw);
         int* lnw = reinterpret_cast<int*>(rec + A.RL.lvl_nw);
         const bool conc = C.K <= 32;  // every level's bisection at once
-        if (conc) s_alloc_concurrent(C, n_levels);
+        if (conc) s_alloc_concurrent<DM>(C, n_levels);
         #pragma unroll 1
         for (int l = 0; l < n_levels && ok; ++l) {
             double cs = 0.0;
@@ -2083,17 +2102,17 @@ __device__ __forceinline__ void sched_body(const SchedArgs& A, char* smem_dyn, C
                     __syncwarp();
                     ok = false;
                 } else {
-                    ok = s_level_repair(C, l);
+                    ok = s_level_repair<DM>(C, l);
                 }
             } else {
-                ok = s_level_alloc(C, l, cs);
+                ok = s_level_alloc<DM>(C, l, cs);
             }
             WS_PH_STOP(tg, 12);
             if (!ok) break;
             lower_bound += cs;  // planner.hpp:189
             const int w0 = nW;
             double level_end = offset;
-            ok = s_schedule_level(C, rec, A.RL, l, nW, nE, offset, level_end, A.caps.W, A.caps.E);
+            ok = s_schedule_level<DM>(C, rec, A.RL, l, nW, nE, offset, level_end, A.caps.W, A.caps.E);
             WS_PH_STOP(tg, 13);
             if (!ok) break;
             if (lane == 0) {
@@ -2194,6 +2213,8 @@ __device__ __forceinline__ void sched_body(const SchedArgs& A, char* smem_dyn, C
 }
 
 
+// DM: valid-allocation set type (uint64_t: N <= 64; DevMask<4>: N <= 256)
+template <class DM = uint64_t>
 #ifdef WS_SCHED_MINB
 __global__ void __launch_bounds__(32 * kSchedWarps, WS_SCHED_MINB) k_sched(SchedArgs A) {
 #else
@@ -2201,7 +2222,7 @@ __global__ void __launch_bounds__(32 * kSchedWarps) k_sched(SchedArgs A) {
 #endif
     extern __shared__ __align__(16) char smem_dyn[];
     __shared__ Ctl ctl_s[kSchedWarps];
-    sched_body<false>(A, smem_dyn, ctl_s);
+    sched_body<false, DM>(A, smem_dyn, ctl_s);
 }
 
 // plan_distmm_mt plans of the batch (the planner instance skips them)

@@ -190,10 +190,10 @@ __global__ void __launch_bounds__(32 * kSimWarps, WS_SIM_MINB) k_sim(SimArgs A) 
     if (p >= A.n_plans) return;
     const ws_plan_result& R = A.plans[p];
     ws_sim_result* res = A.out + p;
-    if (R.status != WS_STATUS_OK) {
-        if (lane == 0) {
+    if (R.status != WS_STATUS_OK || A.B.plans[p].n_dev > WS_MAX_DEVICES_EVAL) {
+        if (lane == 0) {  // evaluation covers clusters of up to 64 devices (u64 masks)
             ws_sim_result r{};
-            r.status = R.status;
+            r.status = R.status != WS_STATUS_OK ? R.status : WS_STATUS_LIMIT;
             *res = r;
         }
         return;

@@ -10,7 +10,7 @@ static inline uint64_t wsi_plan_arena_bound(const ws_plan_rec* r) {
     const uint64_t M = (uint64_t)r->n_mod;
     return 64 + sizeof(ws_out_metaop) * M + sizeof(ws_out_level) * M + sizeof(ws_out_piece) * 4 * M +
            sizeof(ws_out_edge) * M * M + sizeof(ws_out_wave) * 4 * M + sizeof(ws_out_entry) * 8 * M +
-           sizeof(ws_out_flow) * 16 * M;
+           sizeof(ws_out_flow) * 16 * M + (r->n_dev > 64 ? 24 * 8 * M : 0);
 }
 
 /* evaluation record: busy/mem per device, utilization per entity, violations */

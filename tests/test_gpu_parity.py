@@ -109,14 +109,17 @@ def test_gpu_ragged_batch_and_determinism(planner, golden_cases):
 
 
 def test_gpu_device_limit_is_loud(planner):
-    """More devices than the build supports is a reported LimitExceeded, not a fallback."""
+    """More devices than the build supports (WS_MAX_DEVICES = 256) is a reported
+    LimitExceeded, not a fallback; 70 devices (the wide kernels) plan."""
     import paper_2409_03365_b200 as ws
-    topo = "island 0: " + " ".join(str(i) for i in range(70)) + "\nbw intra=1e11 inter=1e10\nmem 100000000000\n"
     ps = ws.ProblemSet()
-    ps.add_text("module a layers=2 B=48\ntruth a piece 1 1024 0.1 0 1\ntask t flow=a\n", topo)
+    for n in (300, 70):
+        topo = "island 0: " + " ".join(str(i) for i in range(n)) + "\nbw intra=1e11 inter=1e10\nmem 100000000000\n"
+        ps.add_text("module a layers=2 B=48\ntruth a piece 1 1024 0.1 0 1\ntask t flow=a\n", topo)
     ps.encode(pinned=True)
-    text = planner.plan(ps).texts(ps)[0]
-    assert text.startswith("error LimitExceeded")
+    texts = planner.plan(ps).texts(ps)
+    assert texts[0].startswith("error LimitExceeded")
+    assert texts[1].startswith("# wavesched plan v1") and "devices" in texts[1]
 
 
 def test_gpu_dropin_plan_workload(golden_cases):
