@@ -41,6 +41,7 @@ constexpr int64_t kOverflowPieces = 1 << 18;  // isotonic/long curves
 constexpr int kSmemLimit = 227 * 1024;
 constexpr int kMaxChunks = 16;  // k_sched/k_place pipeline depth
 constexpr int kMaxHostChunks = 8;
+constexpr int kSplitMin = 2048;  // launches of at least this many plans run k_sched as three phase kernels
 // k_place snapshot slots: only warps of plans that fail a wave claim one (a few
 // hundred per 100k sweep), so a small pool serves every resident warp; a warp
 // that finds none falls back to replaying the committed waves
@@ -273,6 +274,10 @@ struct ws_ctx {
     long long last_retry = 0;   // soft-cap overflows of the last planning call (all re-planned)
     bool tiny_soft = false;     // $WSGPU_TINY_SOFT_CAPS: soft caps below every plan (tests of the retry pass)
     bool small_path = true;     // $WSGPU_SMALL_PATH=0: small host batches take the staged path
+    // k_sched as three phase kernels for launches of >= kSplitMin plans
+    // ($WSGPU_SCHED_SPLIT: 0 never, 1 default, 2 always); state between them
+    int sched_split = 1;
+    DevBuf sched_state;
     // measured (100k sweep, ms): one compute stream: 1 chunk 27.8, 2: 27.4, 4: 32.0 (each
     // chunk's k_sched + k_place launch tail outweighs the hidden copies); two compute
     // streams (consecutive chunks fill each other's tails) with completion-order D2H:
@@ -340,6 +345,12 @@ cudaError_t smem_opt_in_all(int device) {
     std::call_once(once[device], [&] {
         cudaError_t e = smem_opt_in(k_sched<uint64_t>);
         if (e == cudaSuccess) e = smem_opt_in(k_sched<DevMask<4>>);
+        if (e == cudaSuccess) e = smem_opt_in(k_sched<uint64_t, 1>);
+        if (e == cudaSuccess) e = smem_opt_in(k_sched<uint64_t, 2>);
+        if (e == cudaSuccess) e = smem_opt_in(k_sched<uint64_t, 3>);
+        if (e == cudaSuccess) e = smem_opt_in(k_sched<DevMask<4>, 1>);
+        if (e == cudaSuccess) e = smem_opt_in(k_sched<DevMask<4>, 2>);
+        if (e == cudaSuccess) e = smem_opt_in(k_sched<DevMask<4>, 3>);
         if (e == cudaSuccess) e = smem_opt_in(k_sched_scoped);
         if (e == cudaSuccess) e = smem_opt_in(k_place<true>);
         if (e == cudaSuccess) e = smem_opt_in(k_place<false>);
@@ -437,6 +448,16 @@ int launch_pair(ws_ctx* ctx, cudaStream_t st, const LaunchCaps& lc, const FitOut
     S.M_cap = lc.M;
     S.results = ctx->res_out();
     if (kSchedWarps * S.SL.bytes > kSmemLimit) return fail(ctx, "k_sched working set exceeds shared memory");
+    // phase-split k_sched (sched_body): smaller per-kernel instruction footprint;
+    // the warp's working set travels through global memory between the phases
+    const bool split = !n_ids && !by_slot &&
+                       (ctx->sched_split == 2 || (ctx->sched_split == 1 && n >= kSplitMin));
+    if (split) {
+        S.state_stride = S.SL.bytes + kSchedStateHdr;
+        if (!ctx->sched_state.ensure(static_cast<size_t>(S.state_stride) * std::max(B.n_plans, 1)))
+            return fail(ctx, "cudaMalloc k_sched phase state");
+        S.state = ctx->sched_state.as<char>();
+    }
 
     PlaceArgs P{};
     P.B = B;
@@ -464,6 +485,9 @@ int launch_pair(ws_ctx* ctx, cudaStream_t st, const LaunchCaps& lc, const FitOut
     auto* kplace = wide ? (snap ? k_place<true, DevMask<4>, 1, 1> : k_place<false, DevMask<4>, 1, 1>)
                         : (snap ? k_place<true> : k_place<false>);
     auto* ksched = wide ? k_sched<DevMask<4>> : k_sched<uint64_t>;
+    auto* ksched1 = wide ? k_sched<DevMask<4>, 1> : k_sched<uint64_t, 1>;
+    auto* ksched2 = wide ? k_sched<DevMask<4>, 2> : k_sched<uint64_t, 2>;
+    auto* ksched3 = wide ? k_sched<DevMask<4>, 3> : k_sched<uint64_t, 3>;
 
     chunks = std::max(1, std::min(chunks, kMaxChunks));
     if (n_ids || n < 4096) chunks = 1;  // retry pass / small batches: no pipelining
@@ -490,11 +514,17 @@ int launch_pair(ws_ctx* ctx, cudaStream_t st, const LaunchCaps& lc, const FitOut
             attr[0].val.programmaticStreamSerializationAllowed = 1;
             cfg.attrs = attr;
             cfg.numAttrs = 1;
-            CK(cudaLaunchKernelEx(&cfg, ksched, S));
+            CK(cudaLaunchKernelEx(&cfg, split ? ksched1 : ksched, S));
         } else {
-            ksched<<<(cnt + kSchedWarps - 1) / kSchedWarps, 32 * kSchedWarps, kSchedWarps * S.SL.bytes, st>>>(S);
+            (split ? ksched1 : ksched)<<<(cnt + kSchedWarps - 1) / kSchedWarps, 32 * kSchedWarps,
+                                         kSchedWarps * S.SL.bytes, st>>>(S);
         }
         ctx->launches++;
+        if (split) {
+            ksched2<<<(cnt + kSchedWarps - 1) / kSchedWarps, 32 * kSchedWarps, kSchedWarps * S.SL.bytes, st>>>(S);
+            ksched3<<<(cnt + kSchedWarps - 1) / kSchedWarps, 32 * kSchedWarps, kSchedWarps * S.SL.bytes, st>>>(S);
+            ctx->launches += 2;
+        }
         if (lc.scoped) {  // the batch's distmm-mt plans (each instance skips the other's plans)
             k_sched_scoped<<<(cnt + kSchedWarps - 1) / kSchedWarps, 32 * kSchedWarps, kSchedWarps * S.SL.bytes,
                              st>>>(S);
@@ -567,6 +597,7 @@ int ws_ctx_create(int device, ws_ctx** out) {
     if (const char* env = std::getenv("WSGPU_HOST_STREAMS")) c->host_streams = std::max(1, std::min(2, std::atoi(env)));
     if (const char* env = std::getenv("WSGPU_TINY_SOFT_CAPS")) c->tiny_soft = std::atoi(env) != 0;
     if (const char* env = std::getenv("WSGPU_SMALL_PATH")) c->small_path = std::atoi(env) != 0;
+    if (const char* env = std::getenv("WSGPU_SCHED_SPLIT")) c->sched_split = std::atoi(env);
     *out = c;
     return 0;
 }

@@ -188,7 +188,14 @@ struct SchedArgs {
     int M_cap;               // modules per plan this launch supports
     int scoped_ok;           // SL carries the task-scoped working set (distmm-mt plans)
     ws_plan_result* results;
+    // phase-split launches (k_sched<DM, 1..3>): per launch slot the warp's
+    // shared working set, control block and flags between the phases
+    char* state;
+    long long state_stride;  // bytes per slot: SL.bytes + kSchedStateHdr
 };
+
+// bytes before the saved shared working set of a phase-split slot: Ctl + flags
+constexpr int kSchedStateHdr = 128;
 
 struct SCtx {
     const ws_batch* B;
@@ -2006,7 +2013,44 @@ __device__ bool s_distmm(SCtx& C, char* rec, const RecLayout& RL, int& nW, int& 
 // One warp per plan.  SCOPED: the kernel instance for the task-scoped
 // baselines (distmm-mt); the planner's instance carries none of that code, so
 // its register allocation and instruction stream stay those of the planner.
-template <bool SCOPED, class DM = uint64_t>
+// Warp copy of a slot's shared working set to / from its global state slot
+// (16-byte words; SL.bytes is a multiple of 16) plus the control block and
+// the flags that live in registers between the phases.
+__device__ __forceinline__ void sched_state_io(bool save, char* g, char* sm, int bytes, Ctl* ctl, int& ok, int& K,
+                                               int lane) {
+    int4* gs = reinterpret_cast<int4*>(g + kSchedStateHdr);
+    int4* ss = reinterpret_cast<int4*>(sm);
+    #pragma unroll 1
+    for (int i = lane; i < bytes / 16; i += 32) {
+        if (save)
+            gs[i] = ss[i];
+        else
+            ss[i] = gs[i];
+    }
+    int* flags = reinterpret_cast<int*>(g + sizeof(Ctl));
+    if (save) {
+        if (lane == 0) {
+            *reinterpret_cast<Ctl*>(g) = *ctl;
+            flags[0] = ok;
+            flags[1] = K;
+        }
+    } else {
+        if (lane == 0) *ctl = *reinterpret_cast<const Ctl*>(g);
+        ok = flags[0];
+        K = flags[1];
+    }
+    __syncwarp();
+}
+
+// PHASE 0: the whole k_sched in one kernel.  Phase-split launches (large
+// batches): 1 = graph, contraction, levels, fit status, valid sets; 2 = the
+// concurrent bisection + discretization of every level; 3 = repair, wave
+// scheduling, the baselines and the hand-off record.  Each phase kernel
+// carries only its own code, so the warps resident on an SM share a much
+// smaller hot instruction footprint (the monolithic kernel's executed code is
+// ~70 KB against a 32 KB L1.5 instruction cache: ncu showed "no instruction"
+// as the largest stall).
+template <bool SCOPED, class DM = uint64_t, int PHASE = 0>
 __device__ __forceinline__ void sched_body(const SchedArgs& A, char* smem_dyn, Ctl* ctl_s) {
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int slot = blockIdx.x * kSchedWarps + wid;
@@ -2016,11 +2060,12 @@ __device__ __forceinline__ void sched_body(const SchedArgs& A, char* smem_dyn, C
     const int strat = A.B.plans[p].strategy;
     if ((strat == WS_STRATEGY_DISTMM_MT || strat == WS_STRATEGY_TASK_OPTIMUS) != SCOPED) return;  // the other instance's
     Ctl* ctl = &ctl_s[wid];
-    if (lane == 0) *ctl = Ctl{};
+    if (PHASE <= 1 && lane == 0) *ctl = Ctl{};
     __syncwarp();
     const ws_plan_rec& R = A.B.plans[p];
     char* rec = A.recs + static_cast<int64_t>(A.rec_by_slot ? slot : p) * A.RL.bytes;
     SchedHdr* hdr = reinterpret_cast<SchedHdr*>(rec + A.RL.hdr);
+    char* gstate = PHASE ? A.state + static_cast<int64_t>(A.rec_by_slot ? slot : p) * A.state_stride : nullptr;
     SCtx C;
     C.B = &A.B;
     C.R = &R;
@@ -2033,7 +2078,15 @@ __device__ __forceinline__ void sched_body(const SchedArgs& A, char* smem_dyn, C
     C.M = R.n_mod;
     C.K = 0;
     C.mbase = R.mod_begin;
+    const bool decoupled = R.strategy == WS_STRATEGY_DECOUPLED_SEQUENTIAL;
+    constexpr bool scoped = SCOPED;  // task-scoped baselines: distmm-mt, task-level-optimus
     bool ok = true;
+    WS_PH_START(tg);
+    if constexpr (PHASE >= 2) {  // resume the plan where the previous phase left it
+        int ok_i = 0;
+        sched_state_io(false, gstate, C.sm, A.SL.bytes, ctl, ok_i, C.K, lane);
+        ok = ok_i != 0;
+    } else {
     if (R.n_mod == 0 && R.n_tasks == 0) {
         ok = false;
         if (lane == 0) ctl->err = WS_E_HOST_PRESET;
@@ -2045,7 +2098,6 @@ __device__ __forceinline__ void sched_body(const SchedArgs& A, char* smem_dyn, C
         if (lane == 0) ctl->err = WS_E_LIMIT_MODULES;
     }
     __syncwarp();
-    WS_PH_START(tg);
     if (ok) ok = s_graph(C);
     WS_PH_STOP(tg, 10);
     // programmatic dependent launch: the graph stage above reads only the batch,
@@ -2060,8 +2112,6 @@ __device__ __forceinline__ void sched_body(const SchedArgs& A, char* smem_dyn, C
         __syncwarp();
     }
     if (ok) ok = s_fit_status(C);
-    const bool decoupled = R.strategy == WS_STRATEGY_DECOUPLED_SEQUENTIAL;
-    constexpr bool scoped = SCOPED;  // task-scoped baselines: distmm-mt, task-level-optimus
     if (ok && scoped && !A.scoped_ok) {  // launch built without the task-scoped working set
         ok = false;
         if (lane == 0) ctl->err = WS_E_LIMIT_MODULES;
@@ -2069,6 +2119,16 @@ __device__ __forceinline__ void sched_body(const SchedArgs& A, char* smem_dyn, C
     }
     if (ok) ok = s_valid<DM>(C, !decoupled && !scoped);
     WS_PH_STOP(tg, 11);
+    }
+    const bool conc = C.K <= 32;  // every level's bisection at once
+    if constexpr (PHASE == 0 || PHASE == 2) {
+        if (ok && !decoupled && !scoped && conc) s_alloc_concurrent<DM>(C, ctl->i1);
+    }
+    if constexpr (PHASE == 1 || PHASE == 2) {  // hand the plan to the next phase
+        int ok_i = ok;
+        sched_state_io(true, gstate, C.sm, A.SL.bytes, ctl, ok_i, C.K, lane);
+        return;
+    }
     int n_levels = 0, nW = 0, nE = 0, KE = 0, n_pg = 0;
     double lower_bound = 0.0, offset = 0.0;
     if (ok && decoupled) {
@@ -2085,8 +2145,6 @@ __device__ __forceinline__ void sched_body(const SchedArgs& A, char* smem_dyn, C
         double* cstar = reinterpret_cast<double*>(rec + A.RL.cstar);
         int* lfw = reinterpret_cast<int*>(rec + A.RL.lvl_fw);
         int* lnw = reinterpret_cast<int*>(rec + A.RL.lvl_nw);
-        const bool conc = C.K <= 32;  // every level's bisection at once
-        if (conc) s_alloc_concurrent<DM>(C, n_levels);
         #pragma unroll 1
         for (int l = 0; l < n_levels && ok; ++l) {
             double cs = 0.0;
@@ -2213,8 +2271,9 @@ __device__ __forceinline__ void sched_body(const SchedArgs& A, char* smem_dyn, C
 }
 
 
-// DM: valid-allocation set type (uint64_t: N <= 64; DevMask<4>: N <= 256)
-template <class DM = uint64_t>
+// DM: valid-allocation set type (uint64_t: N <= 64; DevMask<4>: N <= 256);
+// PHASE: 0 whole, 1..3 the phase-split launches (sched_body)
+template <class DM = uint64_t, int PHASE = 0>
 #ifdef WS_SCHED_MINB
 __global__ void __launch_bounds__(32 * kSchedWarps, WS_SCHED_MINB) k_sched(SchedArgs A) {
 #else
@@ -2222,7 +2281,7 @@ __global__ void __launch_bounds__(32 * kSchedWarps) k_sched(SchedArgs A) {
 #endif
     extern __shared__ __align__(16) char smem_dyn[];
     __shared__ Ctl ctl_s[kSchedWarps];
-    sched_body<false, DM>(A, smem_dyn, ctl_s);
+    sched_body<false, DM, PHASE>(A, smem_dyn, ctl_s);
 }
 
 // plan_distmm_mt plans of the batch (the planner instance skips them)
