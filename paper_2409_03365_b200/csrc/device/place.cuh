@@ -113,6 +113,12 @@ struct PlaceArgs {
     unsigned* snap_bits;      // claim bitmap, one bit per slot
     int snap_slots;           // 0: no pool (replay only)
     long long snap_stride;    // 8-byte words per slot
+    // split emission (k_emit): k_place leaves each plan's placement here
+    // (indexed like the schedule records) and k_emit writes the output record
+    char* emit_mask;          // [.][caps.E] device masks (sizeof(DM) each)
+    int32_t* emit_rot;        // [.][caps.E]
+    int32_t* emit_nf;         // [.] flow count, -1: no record (error written)
+    int split_emit;
 };
 
 template <class DM>
@@ -454,9 +460,17 @@ __device__ int p_wave(PCtx<DM>& C, int w, int variant) {
     return 1;
 }
 
+// Where p_emit reads the schedule tables and the placement: shared memory
+// inside k_place, or the schedule record + the placement scratch in k_emit.
+template <class DM>
+struct EmitSrc {
+    const int *by_rank, *w_eb, *w_ec, *e_k, *e_n, *e_l, *e_rot;
+    const DM* e_mask;
+};
+
 template <class DM>
 __device__ void p_emit(PCtx<DM>& C, int p, const char* rec, const RecLayout& RL, const SchedHdr& h,
-                       const PlaceArgs& A) {
+                       const PlaceArgs& A, const EmitSrc<DM>& S) {
     constexpr int kExt = MaskTraits<DM>::kWords - 1;  // device words 1.. of each entry (N > 64)
     const int lane = C.lane, K = C.K;
     const ws_batch& B = *C.B;
@@ -467,7 +481,7 @@ __device__ void p_emit(PCtx<DM>& C, int p, const char* rec, const RecLayout& RL,
     const int* r_lo_n = reinterpret_cast<const int*>(rec + RL.lo_n);
     const int* r_lo_l = reinterpret_cast<const int*>(rec + RL.lo_l);
     const uint64_t* r_succ = reinterpret_cast<const uint64_t*>(rec + RL.succ_r);
-    const int* by_rank = C.template at<int>(C.L->by_rank);
+    const int* by_rank = S.by_rank;
     int npieces = 0, nedges = 0;
     #pragma unroll 1
     for (int k = lane; k < K; k += 32) {
@@ -569,8 +583,8 @@ __device__ void p_emit(PCtx<DM>& C, int p, const char* rec, const RecLayout& RL,
     const double* w_start = reinterpret_cast<const double*>(rec + RL.w_start);
     const double* w_dur = reinterpret_cast<const double*>(rec + RL.w_dur);
     const int* w_level = reinterpret_cast<const int*>(rec + RL.w_level);
-    const int* w_eb = C.template at<int>(C.L->w_eb);
-    const int* w_ec = C.template at<int>(C.L->w_ec);
+    const int* w_eb = S.w_eb;
+    const int* w_ec = S.w_ec;
     #pragma unroll 1
     for (int w = lane; w < nW; w += 32) {
         ws_out_wave x;
@@ -582,12 +596,12 @@ __device__ void p_emit(PCtx<DM>& C, int p, const char* rec, const RecLayout& RL,
         x.pad = 0;
         wv[w] = x;
     }
-    const int* e_k = C.template at<int>(C.L->e_k);
-    const int* e_n = C.template at<int>(C.L->e_n);
-    const int* e_l = C.template at<int>(C.L->e_l);
+    const int* e_k = S.e_k;
+    const int* e_n = S.e_n;
+    const int* e_l = S.e_l;
     const double* e_span = reinterpret_cast<const double*>(rec + RL.e_span);
-    const DM* e_mask = C.template at<DM>(C.L->e_mask);
-    const int* e_rot = C.template at<int>(C.L->e_rot);
+    const DM* e_mask = S.e_mask;
+    const int* e_rot = S.e_rot;
     #pragma unroll 1
     for (int e = lane; e < nE; e += 32) {
         ws_out_entry x;
@@ -687,6 +701,8 @@ __global__ void __launch_bounds__(32 * WARPS, MINB) k_place(PlaceArgs A) {
     const char* rec = A.recs + static_cast<int64_t>(A.rec_by_slot ? slot : p) * A.RL.bytes;
     const SchedHdr h = *reinterpret_cast<const SchedHdr*>(rec + A.RL.hdr);
     if (!h.ok) return;  // k_sched already wrote the error result
+    const int64_t ridx = A.rec_by_slot ? slot : p;
+    if (A.split_emit && lane == 0) A.emit_nf[ridx] = -1;  // set to the flow count once placed
     Ctl* ctl = &ctl_s[wid];
     if (lane == 0) *ctl = Ctl{};
     const ws_plan_rec& R = A.B.plans[p];
@@ -1053,8 +1069,70 @@ __global__ void __launch_bounds__(32 * WARPS, MINB) k_place(PlaceArgs A) {
     }
     if (lane == 0) if (kSnap) snap_release(A.snap_bits, snap_slot);
     WS_PH_START(te);
-    p_emit(C, p, rec, A.RL, h, A);
+    if (A.split_emit) {  // k_emit writes the record: leave the placement behind
+        DM* gm = reinterpret_cast<DM*>(A.emit_mask) + ridx * A.caps.E;
+        int32_t* gr = A.emit_rot + ridx * A.caps.E;
+        const DM* sm_mask = C.template at<DM>(L.e_mask);
+        const int* sm_rot = C.template at<int>(L.e_rot);
+        #pragma unroll 1
+        for (int e = lane; e < nE; e += 32) {
+            gm[e] = sm_mask[e];
+            gr[e] = sm_rot[e];
+        }
+        if (lane == 0) A.emit_nf[ridx] = C.nF;
+    } else {
+        EmitSrc<DM> src;
+        src.by_rank = C.template at<int>(L.by_rank);
+        src.w_eb = C.template at<int>(L.w_eb);
+        src.w_ec = C.template at<int>(L.w_ec);
+        src.e_k = C.template at<int>(L.e_k);
+        src.e_n = C.template at<int>(L.e_n);
+        src.e_l = C.template at<int>(L.e_l);
+        src.e_rot = C.template at<int>(L.e_rot);
+        src.e_mask = C.template at<DM>(L.e_mask);
+        p_emit(C, p, rec, A.RL, h, A, src);
+    }
     WS_PH_STOP(te, 7);
+}
+
+// Output records of the plans k_place placed (split emission): a warp per
+// launch slot, no shared working set, so many warps keep the record reads and
+// stores in flight; the schedule tables come from the k_sched record and the
+// placement from k_place's scratch.
+template <class DM = uint64_t>
+__global__ void __launch_bounds__(32 * kPlaceWarps) k_emit(PlaceArgs A) {
+    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int slot = blockIdx.x * kPlaceWarps + wid;
+    if (slot >= A.n_launch) return;
+    if (A.n_ids && slot >= *A.n_ids) return;
+    const int p = A.plan_ids[slot];
+    const char* rec = A.recs + static_cast<int64_t>(A.rec_by_slot ? slot : p) * A.RL.bytes;
+    const SchedHdr h = *reinterpret_cast<const SchedHdr*>(rec + A.RL.hdr);
+    if (!h.ok) return;
+    const int64_t ridx = A.rec_by_slot ? slot : p;
+    const int nf = A.emit_nf[ridx];
+    if (nf < 0) return;  // k_place wrote the error result
+    const ws_plan_rec& R = A.B.plans[p];
+    PCtx<DM> C;
+    C.B = &A.B;
+    C.R = &R;
+    C.F = &A.fit;
+    C.L = &A.PL;
+    C.lane = lane;
+    C.K = h.K;
+    C.mbase = R.mod_begin;
+    C.nF = nf;
+    C.flows = A.flows + static_cast<int64_t>(slot) * A.caps.F * 2;
+    EmitSrc<DM> src;
+    src.by_rank = reinterpret_cast<const int*>(rec + A.RL.by_rank);
+    src.w_eb = reinterpret_cast<const int*>(rec + A.RL.w_eb);
+    src.w_ec = reinterpret_cast<const int*>(rec + A.RL.w_ec);
+    src.e_k = reinterpret_cast<const int*>(rec + A.RL.e_k);
+    src.e_n = reinterpret_cast<const int*>(rec + A.RL.e_n);
+    src.e_l = reinterpret_cast<const int*>(rec + A.RL.e_l);
+    src.e_rot = A.emit_rot + ridx * A.caps.E;
+    src.e_mask = reinterpret_cast<const DM*>(A.emit_mask) + ridx * A.caps.E;
+    p_emit(C, p, rec, A.RL, h, A, src);
 }
 
 }  // namespace wsdev

@@ -278,6 +278,10 @@ struct ws_ctx {
     // ($WSGPU_SCHED_SPLIT: 0 never, 1 default, 2 always); state between them
     int sched_split = 1;
     DevBuf sched_state;
+    // output records by k_emit after k_place for launches of >= kSplitMin plans
+    // ($WSGPU_EMIT_SPLIT: 0 never, 1 default, 2 always); placement scratch
+    int emit_split = 1;
+    DevBuf emit_mask, emit_rot, emit_nf;
     // measured (100k sweep, ms): one compute stream: 1 chunk 27.8, 2: 27.4, 4: 32.0 (each
     // chunk's k_sched + k_place launch tail outweighs the hidden copies); two compute
     // streams (consecutive chunks fill each other's tails) with completion-order D2H:
@@ -484,6 +488,18 @@ int launch_pair(ws_ctx* ctx, cudaStream_t st, const LaunchCaps& lc, const FitOut
     const bool snap = lc.baseline || ctx->force_snap;
     auto* kplace = wide ? (snap ? k_place<true, DevMask<4>, 1, 1> : k_place<false, DevMask<4>, 1, 1>)
                         : (snap ? k_place<true> : k_place<false>);
+    // split emission: k_place leaves the placement, k_emit writes the records
+    P.split_emit = !n_ids && !by_slot && (ctx->emit_split == 2 || (ctx->emit_split == 1 && n >= kSplitMin));
+    if (P.split_emit) {
+        const size_t rows = static_cast<size_t>(std::max(B.n_plans, 1)) * lc.pl.E;
+        if (!ctx->emit_mask.ensure(rows * mb) || !ctx->emit_rot.ensure(rows * 4) ||
+            !ctx->emit_nf.ensure(4ull * std::max(B.n_plans, 1)))
+            return fail(ctx, "cudaMalloc placement scratch");
+        P.emit_mask = ctx->emit_mask.as<char>();
+        P.emit_rot = ctx->emit_rot.as<int32_t>();
+        P.emit_nf = ctx->emit_nf.as<int32_t>();
+    }
+    auto* kemit = wide ? k_emit<DevMask<4>> : k_emit<uint64_t>;
     auto* ksched = wide ? k_sched<DevMask<4>> : k_sched<uint64_t>;
     auto* ksched1 = wide ? k_sched<DevMask<4>, 1> : k_sched<uint64_t, 1>;
     auto* ksched2 = wide ? k_sched<DevMask<4>, 2> : k_sched<uint64_t, 2>;
@@ -540,6 +556,10 @@ int launch_pair(ws_ctx* ctx, cudaStream_t st, const LaunchCaps& lc, const FitOut
         P.n_launch = cnt;
         kplace<<<(cnt + pw - 1) / pw, 32 * pw, pw * P.PL.bytes, sb>>>(P);
         ctx->launches++;
+        if (P.split_emit) {
+            kemit<<<(cnt + kPlaceWarps - 1) / kPlaceWarps, 32 * kPlaceWarps, 0, sb>>>(P);
+            ctx->launches++;
+        }
     }
     if (chunks > 1) {
         if (mid) CK(cudaEventRecord(mid, st));  // end of the last k_sched chunk
@@ -598,6 +618,7 @@ int ws_ctx_create(int device, ws_ctx** out) {
     if (const char* env = std::getenv("WSGPU_TINY_SOFT_CAPS")) c->tiny_soft = std::atoi(env) != 0;
     if (const char* env = std::getenv("WSGPU_SMALL_PATH")) c->small_path = std::atoi(env) != 0;
     if (const char* env = std::getenv("WSGPU_SCHED_SPLIT")) c->sched_split = std::atoi(env);
+    if (const char* env = std::getenv("WSGPU_EMIT_SPLIT")) c->emit_split = std::atoi(env);
     *out = c;
     return 0;
 }
