@@ -947,6 +947,7 @@ __global__ void __launch_bounds__(32 * WARPS, MINB) k_place(PlaceArgs A) {
     bool dirty = false;
     if (lane == 0) wave_nf[0] = C.nF;
     while (k < gn) {
+        WS_PH_COUNT(28, 1);
         if (++attempts > budget) {
             if (lane == 0) {
                 set_err(ctl, WS_E_BT_BUDGET, k);
@@ -979,6 +980,7 @@ __global__ void __launch_bounds__(32 * WARPS, MINB) k_place(PlaceArgs A) {
             #pragma unroll 1
             for (int g = lane; g < G; g += 32) chg[g] = dm_zero<DM>();
             __syncwarp();
+            WS_PH_COUNT(29, k);
             #pragma unroll 1
             for (int j = 0; j < k; ++j) {
                 if (kSnap && snap_slot >= 0) {
@@ -1039,6 +1041,7 @@ __global__ void __launch_bounds__(32 * WARPS, MINB) k_place(PlaceArgs A) {
             continue;
         }
         const int wk = glist[k];
+        WS_PH_COUNT(30, 1);
         const int r = p_wave(C, wk, variant[k]);
         __syncwarp();
         if (r < 0) {

@@ -18,6 +18,9 @@ if ":" in arg:
     fam, t, d = arg.split(":")
     ps.add_scenario(fam, int(t), int(d), 0)
     n = 1
+elif arg.startswith("mix"):  # one sweep mixture, e.g. mix37617
+    ps.add_sweep(int(arg[3:]), 1)
+    n = 1
 else:
     n = int(arg)
     ps.add_sweep(0, n)
@@ -42,3 +45,5 @@ ne = buf[20] or 1
 print(f"scored entries/plan {buf[20] / n:.1f}; per entry: ncand {buf[21] / ne:.1f}  n {buf[22] / ne:.1f}  "
       f"ndisp {buf[23] / ne:.1f}  nfin {buf[24] / ne:.2f}  islands {buf[25] / ne:.1f}  "
       f"lane-iters {buf[26] / ne:.2f}  N {buf[27] / ne:.1f}")
+print(f"placement attempts/plan {buf[28] / n:.1f}; replayed waves/plan {buf[29] / n:.1f}; "
+      f"wave placements/plan {buf[30] / n:.1f}")
