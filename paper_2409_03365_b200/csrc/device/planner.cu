@@ -16,6 +16,7 @@
 #include <dlfcn.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cstdio>
 #include <limits>
 #include <cstdlib>
@@ -274,6 +275,7 @@ struct ws_ctx {
     long long last_retry = 0;   // soft-cap overflows of the last planning call (all re-planned)
     bool tiny_soft = false;     // $WSGPU_TINY_SOFT_CAPS: soft caps below every plan (tests of the retry pass)
     bool small_path = true;     // $WSGPU_SMALL_PATH=0: small host batches take the staged path
+    bool trace = false;         // $WSGPU_TRACE: host-side timing of the pipelined host call on stderr
     // k_sched as three phase kernels for launches of >= kSplitMin plans
     // ($WSGPU_SCHED_SPLIT: 0 never, 1 default, 2 always); state between them
     int sched_split = 1;
@@ -617,6 +619,7 @@ int ws_ctx_create(int device, ws_ctx** out) {
     if (const char* env = std::getenv("WSGPU_HOST_STREAMS")) c->host_streams = std::max(1, std::min(2, std::atoi(env)));
     if (const char* env = std::getenv("WSGPU_TINY_SOFT_CAPS")) c->tiny_soft = std::atoi(env) != 0;
     if (const char* env = std::getenv("WSGPU_SMALL_PATH")) c->small_path = std::atoi(env) != 0;
+    if (const char* env = std::getenv("WSGPU_TRACE")) c->trace = std::atoi(env) != 0;
     if (const char* env = std::getenv("WSGPU_SCHED_SPLIT")) c->sched_split = std::atoi(env);
     if (const char* env = std::getenv("WSGPU_EMIT_SPLIT")) c->emit_split = std::atoi(env);
     *out = c;
@@ -998,6 +1001,9 @@ int host_range(ws_ctx* ctx, const ws_batch* in, int P0, int P1, ws_plan_result* 
     const int P = in->n_plans, n = P1 - P0;
     *arena_used = 0;
     if (n <= 0) return 0;
+    using hclk = std::chrono::steady_clock;
+    const auto t_enter = hclk::now();
+    hclk::time_point t_prep, t_issued;
     int C = ctx->host_chunks;
     C = std::max(1, std::min({C, kMaxHostChunks, n / 4096}));
     if (!ctx->blob.ensure(in->blob_bytes + 256) || !ctx->order.ensure(4ull * P) || !ctx->chunk_tops.ensure(8 * 64))
@@ -1060,6 +1066,7 @@ int host_range(ws_ctx* ctx, const ws_batch* in, int P0, int P1, ws_plan_result* 
     cudaStream_t sh = ctx->stream2, sd = ctx->stream3;
     cudaEvent_t* h2d = ctx->cev;               // [0, C)
     cudaEvent_t* done = ctx->cev + kMaxHostChunks;  // [C, 2C)
+    t_prep = hclk::now();
     CK(cudaEventRecord(ctx->ev[0], st));
     CK(cudaStreamWaitEvent(sh, ctx->ev[0], 0));
     CK(cudaMemcpyAsync(tops, ctx->host_tops, 8ull * C, cudaMemcpyHostToDevice, sh));
@@ -1153,6 +1160,7 @@ int host_range(ws_ctx* ctx, const ws_batch* in, int P0, int P1, ws_plan_result* 
         CK(cudaStreamWaitEvent(st, ctx->ev[3], 0));
     }
     CK(cudaEventRecord(ctx->ev[2], st));
+    t_issued = hclk::now();
     uint64_t used = 0;
     // D2H side, in completion order (chunks on two compute streams finish out of
     // order): poll the chunk events and copy each finished chunk back at once
@@ -1219,6 +1227,14 @@ int host_range(ws_ctx* ctx, const ws_batch* in, int P0, int P1, ws_plan_result* 
     // a sub-range leaves the other plans' device records unset: evaluation and
     // min-loc over the staged batch need a whole-batch call
     ctx->records_on_device = P0 == 0 && P1 == P;
+    if (ctx->trace) {
+        auto ms = [](hclk::time_point a, hclk::time_point b) {
+            return std::chrono::duration<double, std::milli>(b - a).count();
+        };
+        std::fprintf(stderr, "[wsgpu] host_range %d plans, %d chunks: host prep %.3f ms, launches issued %.3f ms, "
+                             "end %.3f ms, device pipeline %.3f ms\n", n, C, ms(t_enter, t_prep),
+                     ms(t_enter, t_issued), ms(t_enter, hclk::now()), ctx->kernel_ms[2]);
+    }
     *arena_used = used;
     return 0;
 }
