@@ -334,6 +334,13 @@ int ws_last_kernel_ms(const ws_ctx* ctx, double* out, int n);
  * simulated makespan of the last ws_simulate_staged (mode 2); infeasible
  * plans count as +inf; ties go to the smaller index.  Writes {key, index}. */
 int ws_best_staged(ws_ctx* ctx, int mode, double* key, int64_t* index, void* stream);
+/* The candidate search of one workload in one call: plans the HOST batch `in`
+ * (its candidate variants), evaluates it when mode == 2 (sim: SimulatorOptions,
+ * NULL = defaults), and returns the min-loc as ws_best_staged does.  Batches
+ * of up to 512 plans take the small-batch launch (one H2D copy, no retry pass,
+ * one 16-byte copy back); the records stay on the device (ws_fetch_results). */
+int ws_best_batch_host(ws_ctx* ctx, const ws_batch* in, int mode, const ws_sim_opts* sim, double* key,
+                       int64_t* index, void* stream);
 
 /* ---- multi-GPU -------------------------------------------------
  * One process, several GPUs: plans `in` (HOST memory) sharded over n_ctx

@@ -153,6 +153,8 @@ def _load() -> C.CDLL:
         "ws_best_host": (C.c_int, [vp, i64, C.c_int, C.POINTER(C.c_double), C.POINTER(i64)]),
         "ws_last_kernel_ms": (C.c_int, [vp, C.POINTER(C.c_double), C.c_int]),
         "ws_best_staged": (C.c_int, [vp, C.c_int, C.POINTER(C.c_double), C.POINTER(i64), vp]),
+        "ws_best_batch_host": (C.c_int, [vp, vp, C.c_int, C.POINTER(SimOptions), C.POINTER(C.c_double),
+                                         C.POINTER(i64), vp]),
         "ws_arena_bound": (u64, [vp]),
         "wsx_default_options": (None, [C.POINTER(Options)]),
         "wsx_set_new": (vp, []),
@@ -460,6 +462,14 @@ class Planner:
     def best(self, mode: int = 0, stream: int | None = None) -> tuple[float, int]:
         key, idx = C.c_double(), C.c_int64()
         self._ok(lib.ws_best_staged(self._h, mode, C.byref(key), C.byref(idx), stream))
+        return key.value, idx.value
+
+    def best_of(self, pset: ProblemSet, mode: int = 0, stream: int | None = None, **sim_opts) -> tuple[float, int]:
+        """Plan (and for mode 2 evaluate) a host batch and min-locate it in one
+        call (ws_best_batch_host: the candidate search of one workload)."""
+        key, idx = C.c_double(), C.c_int64()
+        so = make_sim_options(**sim_opts)
+        self._ok(lib.ws_best_batch_host(self._h, pset.batch, mode, C.byref(so), C.byref(key), C.byref(idx), stream))
         return key.value, idx.value
 
     def _sim_out(self, pset: ProblemSet, out: SimResults | None) -> tuple[SimResults, int]:

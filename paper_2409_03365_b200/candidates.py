@@ -67,11 +67,7 @@ def best_candidate(planner, pset, key: str = "makespan", stream=None) -> tuple[f
     (key value, candidate index); (+inf, -1) when every candidate failed."""
     if key not in KEYS:
         raise ValueError(f"unknown candidate key {key!r} (one of {sorted(KEYS)})")
-    planner.stage(pset, stream)
-    planner.plan_staged(stream)
-    if key == "simulated":
-        planner.simulate_staged(stream)
-    return planner.best(KEYS[key], stream)
+    return planner.best_of(pset, KEYS[key], stream)  # ws_best_batch_host: one call
 
 
 def best_candidate_sharded(planner, workload: str, topology: str, variants: list[dict] | None = None,

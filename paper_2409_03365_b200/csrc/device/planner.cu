@@ -42,7 +42,8 @@ constexpr int64_t kOverflowPieces = 1 << 18;  // isotonic/long curves
 constexpr int kSmemLimit = 227 * 1024;
 constexpr int kMaxChunks = 16;  // k_sched/k_place pipeline depth
 constexpr int kMaxHostChunks = 8;
-constexpr int kSplitMin = 2048;  // launches of at least this many plans run k_sched as three phase kernels
+constexpr int kSplitMin = 2048;
+constexpr int kBestBatchMax = 512;  // ws_best_batch_host: batches up to this take the small-batch launch  // launches of at least this many plans run k_sched as three phase kernels
 // k_place snapshot slots: only warps of plans that fail a wave claim one (a few
 // hundred per 100k sweep), so a small pool serves every resident warp; a warp
 // that finds none falls back to replaying the committed waves
@@ -52,9 +53,10 @@ constexpr uint64_t kOneSyncArena = 256u << 10;  // H2D / compute / D2H pipeline 
 
 // host_tops (page-locked u64 words): [0, 8) chunk arena bases, [8, 16) chunk
 // arena tops, [16] final top, [17] fetched top, [18] retry count of a staged
-// call, [24, 32) retry counts of the pipelined chunks
+// call, [20, 22) the last min-loc, [24, 32) retry counts of the pipelined chunks
 constexpr int kHostTopsWords = 4 * kMaxHostChunks + 8;
 constexpr int kHtFinal = 2 * kMaxHostChunks, kHtFetch = kHtFinal + 1, kHtRetry = kHtFinal + 2;
+constexpr int kHtBest = kHtFinal + 4;  // [20, 22): {key, index} of k_best
 constexpr int kHtChunkRetry = 3 * kMaxHostChunks;
 
 // Makes `device` current for the scope of an entry point and restores the
@@ -913,8 +915,8 @@ constexpr int kSmallBatch = 64;  // host batches planned by plan_small
 // in one or two copies: 6-7 CUDA calls per call instead of ~25 (the CUDA
 // driver serializes concurrent callers' API calls, so their count bounds the
 // multi-threaded drop-in throughput).
-int plan_small(ws_ctx* ctx, const ws_batch* in, ws_plan_result* results, uint8_t* arena, uint64_t arena_cap,
-               uint64_t* arena_used, cudaStream_t st) {
+// stage + launch of the small-batch path (results stay on the device)
+int small_launch(ws_ctx* ctx, const ws_batch* in, cudaStream_t st) {
     const int P = in->n_plans;
     const uint64_t o_order = 256, o_blob = (o_order + 4ull * P + 255) & ~255ull;
     const uint64_t bytes = o_blob + in->blob_bytes;
@@ -961,6 +963,13 @@ int plan_small(ws_ctx* ctx, const ws_batch* in, ws_plan_result* results, uint8_t
         return 1;
     ctx->staged_events = false;
     ctx->records_on_device = true;
+    return 0;
+}
+
+int plan_small(ws_ctx* ctx, const ws_batch* in, ws_plan_result* results, uint8_t* arena, uint64_t arena_cap,
+               uint64_t* arena_used, cudaStream_t st) {
+    const int P = in->n_plans;
+    if (small_launch(ctx, in, st)) return 1;
     const bool one_sync = ctx->arena_cap <= kOneSyncArena && ctx->arena_cap <= arena_cap;
     if (P) CK(cudaMemcpyAsync(results, ctx->results.p, sizeof(ws_plan_result) * P, cudaMemcpyDeviceToHost, st));
     if (one_sync) CK(cudaMemcpyAsync(arena, ctx->arena.p, ctx->arena_cap, cudaMemcpyDeviceToHost, st));
@@ -1400,6 +1409,25 @@ int ws_debug_phase_cycles(unsigned long long* out, int n) {
     return 0;
 }
 
+// Candidate search in one call: a host batch of up to
+// kBestBatchMax plans through the small-batch launch (one H2D copy, hard record
+// caps, no retry pass), optionally the device evaluation (mode 2), the on-device
+// min-loc and one 16-byte copy back.  The records stay on the device for a later
+// ws_fetch_results; larger batches go through stage + plan + best.
+int ws_best_batch_host(ws_ctx* ctx, const ws_batch* in, int mode, const ws_sim_opts* sim, double* key,
+                       int64_t* index, void* stream) {
+    DevGuard dg_(ctx->device);
+    cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
+    const int P = in->n_plans;
+    if (P > kBestBatchMax || !in->blob) {
+        if (ws_stage_batch(ctx, in, stream) || ws_plan_staged(ctx, stream)) return 1;
+    } else if (small_launch(ctx, in, st)) {
+        return 1;
+    }
+    if (mode == 2 && ws_simulate_staged(ctx, sim, stream)) return 1;
+    return ws_best_staged(ctx, mode, key, index, stream);
+}
+
 int ws_best_staged(ws_ctx* ctx, int mode, double* key, int64_t* index, void* stream) {
     DevGuard dg_(ctx->device);
     cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
@@ -1409,13 +1437,12 @@ int ws_best_staged(ws_ctx* ctx, int mode, double* key, int64_t* index, void* str
     if (mode == 2 && !ctx->sim_valid) return fail(ctx, "ws_best_staged: mode 2 needs ws_simulate_staged first");
     k_best<<<1, 1024, 0, st>>>(ctx->results.as<ws_plan_result>(), ctx->sim_res.as<ws_sim_result>(),
                                ctx->dview.n_plans, mode, kb, ib);
-    double hk = 0;
-    long long hi = -1;
-    CK(cudaMemcpyAsync(&hk, kb, sizeof(double), cudaMemcpyDeviceToHost, st));
-    CK(cudaMemcpyAsync(&hi, ib, sizeof(long long), cudaMemcpyDeviceToHost, st));
+    // {key, index} are adjacent: one copy into page-locked host memory
+    unsigned long long* hb = ctx->host_tops + kHtBest;
+    CK(cudaMemcpyAsync(hb, kb, 16, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
-    *key = hk;
-    *index = hi;
+    std::memcpy(key, hb, sizeof(double));
+    *index = static_cast<int64_t>(hb[1]);
     return 0;
 }
 
