@@ -285,6 +285,7 @@ struct ws_ctx {
     // output records by k_emit after k_place for launches of >= kSplitMin plans
     // ($WSGPU_EMIT_SPLIT: 0 never, 1 default, 2 always); placement scratch
     int emit_split = 1;
+    bool fixed_layout = true;  // $WSGPU_FIXED_LAYOUT=0: always the runtime-layout k_place
     DevBuf emit_mask, emit_rot, emit_nf;
     // measured (100k sweep, ms): one compute stream: 1 chunk 27.8, 2: 27.4, 4: 32.0 (each
     // chunk's k_sched + k_place launch tail outweighs the hidden copies); two compute
@@ -363,6 +364,8 @@ cudaError_t smem_opt_in_all(int device) {
         if (e == cudaSuccess) e = smem_opt_in(k_place<true>);
         if (e == cudaSuccess) e = smem_opt_in(k_place<false>);
         if (e == cudaSuccess) e = smem_opt_in(k_place<true, DevMask<4>, 1, 1>);
+        if (e == cudaSuccess) e = smem_opt_in(k_place<true, uint64_t, kPlaceWarps, WS_PLACE_MINB, true>);
+        if (e == cudaSuccess) e = smem_opt_in(k_place<false, uint64_t, kPlaceWarps, WS_PLACE_MINB, true>);
         if (e == cudaSuccess) e = smem_opt_in(k_place<false, DevMask<4>, 1, 1>);
         if (e == cudaSuccess) e = smem_opt_in(k_sim);
         status[device] = e;
@@ -471,8 +474,18 @@ int launch_pair(ws_ctx* ctx, cudaStream_t st, const LaunchCaps& lc, const FitOut
     P.B = B;
     P.fit = fo;
     P.caps = lc.pl;
+    // the fixed-shape k_place instance (compile-time shared layout) when the
+    // launch's caps fit kFixedPlaceCaps; the placement result does not depend
+    // on the caps, only the working-set sizes do
+    const PlaceCaps& fc = kFixedPlaceCaps;
+    const bool fixed = !wide && ctx->fixed_layout && lc.pl.M <= fc.M && lc.pl.N <= fc.N && lc.pl.W <= fc.W &&
+                       lc.pl.E <= fc.E && lc.pl.G <= fc.G && lc.pl.IS <= fc.IS;
+    if (fixed) {
+        P.caps = fc;
+        P.caps.F = lc.pl.F;
+    }
     P.RL = S.RL;
-    P.PL = make_pl_layout(lc.pl, mb);
+    P.PL = make_pl_layout(P.caps, mb);
     P.recs = recs;
     P.flows = flows;
     P.n_ids = n_ids;
@@ -490,12 +503,14 @@ int launch_pair(ws_ctx* ctx, cudaStream_t st, const LaunchCaps& lc, const FitOut
     // measured (100k sweep, ms): snapshots cut decoupled-sequential 9.8 -> 7.9 and
     // distmm-mt 81 -> 47, while the extra code costs wavefront 10.6 -> 11.0
     const bool snap = lc.baseline || ctx->force_snap;
-    auto* kplace = wide ? (snap ? k_place<true, DevMask<4>, 1, 1> : k_place<false, DevMask<4>, 1, 1>)
-                        : (snap ? k_place<true> : k_place<false>);
+    auto* kplace = wide    ? (snap ? k_place<true, DevMask<4>, 1, 1> : k_place<false, DevMask<4>, 1, 1>)
+                   : fixed ? (snap ? k_place<true, uint64_t, kPlaceWarps, WS_PLACE_MINB, true>
+                                   : k_place<false, uint64_t, kPlaceWarps, WS_PLACE_MINB, true>)
+                           : (snap ? k_place<true> : k_place<false>);
     // split emission: k_place leaves the placement, k_emit writes the records
     P.split_emit = !n_ids && !by_slot && (ctx->emit_split == 2 || (ctx->emit_split == 1 && n >= kSplitMin));
     if (P.split_emit) {
-        const size_t rows = static_cast<size_t>(std::max(B.n_plans, 1)) * lc.pl.E;
+        const size_t rows = static_cast<size_t>(std::max(B.n_plans, 1)) * P.caps.E;
         if (!ctx->emit_mask.ensure(rows * mb) || !ctx->emit_rot.ensure(rows * 4) ||
             !ctx->emit_nf.ensure(4ull * std::max(B.n_plans, 1)))
             return fail(ctx, "cudaMalloc placement scratch");
@@ -624,6 +639,7 @@ int ws_ctx_create(int device, ws_ctx** out) {
     if (const char* env = std::getenv("WSGPU_TRACE")) c->trace = std::atoi(env) != 0;
     if (const char* env = std::getenv("WSGPU_SCHED_SPLIT")) c->sched_split = std::atoi(env);
     if (const char* env = std::getenv("WSGPU_EMIT_SPLIT")) c->emit_split = std::atoi(env);
+    if (const char* env = std::getenv("WSGPU_FIXED_LAYOUT")) c->fixed_layout = std::atoi(env) != 0;
     *out = c;
     return 0;
 }
