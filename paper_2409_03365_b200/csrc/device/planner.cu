@@ -452,6 +452,8 @@ int launch_pair(ws_ctx* ctx, cudaStream_t st, const LaunchCaps& lc, const FitOut
     const int mb = wide ? static_cast<int>(sizeof(DevMask<4>)) : 8;
     const int pw = wide ? 1 : kPlaceWarps;
     S.SL = make_sm_layout(lc.M, lc.scoped, lc.T, mb);
+    // (a compile-time layout for k_sched, as k_place has, measured slower: the
+    // fixed class's larger working set costs occupancy and phase-state traffic)
     S.scoped_ok = lc.scoped ? 1 : 0;
     S.recs = recs;
     S.n_ids = n_ids;
@@ -931,8 +933,10 @@ constexpr int kSmallBatch = 64;  // host batches planned by plan_small
 // in one or two copies: 6-7 CUDA calls per call instead of ~25 (the CUDA
 // driver serializes concurrent callers' API calls, so their count bounds the
 // multi-threaded drop-in throughput).
-// stage + launch of the small-batch path (results stay on the device)
-int small_launch(ws_ctx* ctx, const ws_batch* in, cudaStream_t st) {
+// stage + launch of the small-batch path (results stay on the device).
+// soft: launch with the soft record caps (the fixed-shape k_place instance
+// applies when they fit); the caller re-plans on a soft-cap overflow.
+int small_launch(ws_ctx* ctx, const ws_batch* in, cudaStream_t st, bool soft = false) {
     const int P = in->n_plans;
     const uint64_t o_order = 256, o_blob = (o_order + 4ull * P + 255) & ~255ull;
     const uint64_t bytes = o_blob + in->blob_bytes;
@@ -960,8 +964,8 @@ int small_launch(ws_ctx* ctx, const ws_batch* in, cudaStream_t st) {
     ctx->dview = rebase(*in, in->blob, d + o_blob);
     ctx->drain_pending = false;
     ctx->last_retry = 0;
-    ctx->caps = batch_caps(in->plans, P, true);
-    ctx->caps_hard = ctx->caps;
+    ctx->caps = batch_caps(in->plans, P, !soft, ctx->tiny_soft);
+    ctx->caps_hard = soft ? batch_caps(in->plans, P, true) : ctx->caps;
     ctx->arena_cap = ws_arena_bound(in);
     ctx->sim_cap = ws_sim_arena_bound(in);
     ctx->sim_valid = false;
@@ -985,11 +989,20 @@ int small_launch(ws_ctx* ctx, const ws_batch* in, cudaStream_t st) {
 int plan_small(ws_ctx* ctx, const ws_batch* in, ws_plan_result* results, uint8_t* arena, uint64_t arena_cap,
                uint64_t* arena_used, cudaStream_t st) {
     const int P = in->n_plans;
-    if (small_launch(ctx, in, st)) return 1;
+    if (small_launch(ctx, in, st, true)) return 1;
     const bool one_sync = ctx->arena_cap <= kOneSyncArena && ctx->arena_cap <= arena_cap;
     if (P) CK(cudaMemcpyAsync(results, ctx->results.p, sizeof(ws_plan_result) * P, cudaMemcpyDeviceToHost, st));
     if (one_sync) CK(cudaMemcpyAsync(arena, ctx->arena.p, ctx->arena_cap, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
+    // a plan over the soft record caps (rare: > 4 entries per MetaOp on average):
+    // re-plan the batch on the staged path, whose retry pass uses the hard caps
+    for (int p = 0; p < P; ++p) {
+        const int e = results[p].err_code;
+        if (e == WS_E_LIMIT_WAVES || e == WS_E_LIMIT_ENTRIES || e == WS_E_LIMIT_FLOWS) {
+            if (ws_stage_batch(ctx, in, st) || ws_plan_staged(ctx, st)) return 1;
+            return ws_fetch_results(ctx, results, arena, arena_cap, arena_used, st);
+        }
+    }
     uint64_t top = 0;  // records are bump-allocated: the arena top is the furthest record end
     for (int p = 0; p < P; ++p)
         if (results[p].status == WS_STATUS_OK) top = std::max<uint64_t>(top, results[p].offset + results[p].size);

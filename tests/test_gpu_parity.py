@@ -218,6 +218,22 @@ def test_gpu_retry_pass_drains_every_overflow(monkeypatch, golden_cases):
     assert not bad, bad[:10]
 
 
+def test_gpu_small_batch_soft_cap_fallback(monkeypatch):
+    """Host batches of <= 64 plans launch with the soft record caps; a plan
+    over them sends the batch to the staged path (hard-cap retry): with soft
+    caps below every plan, small batches still equal the oracle."""
+    import paper_2409_03365_b200 as ws
+    import pyoracle
+    pl = _tiny_soft_caps_planner(monkeypatch)
+    for start in (0, 500, 1000):
+        ps = ws.ProblemSet()
+        ps.add_sweep(start, 40)
+        ps.encode(pinned=True)
+        g, o = pl.plan(ps), pyoracle.plan_batch(ps)
+        bad = [i for i in range(len(ps)) if records(g, i) != records(o, i)]
+        assert not bad, bad[:10]
+
+
 def test_gpu_retry_pass_drains_pipelined_chunks(monkeypatch):
     """The same for the chunked H2D / compute / D2H pipeline of
     ws_plan_batch_host: every chunk overflows more than one retry launch."""
