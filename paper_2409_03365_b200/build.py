@@ -61,18 +61,22 @@ def build(verbose: bool = False, force: bool = False, defines: list[str] | None 
     build_dir.mkdir(parents=True, exist_ok=True)
     headers = (list((ROOT / "include").rglob("*.h*")) + list((CSRC / "device").glob("*.cuh")) +
                list((CSRC / "host").glob("*.h*")))
-    objs = []
+    objs, jobs = [], []
+    for src in sorted((CSRC / "device").glob("*.cu")):  # the long nvcc compile first
+        obj = build_dir / (src.stem + ".cu.o")
+        if force or _stale(obj, [src] + headers):
+            jobs.append([NVCC, *NVCC_FLAGS, *dflags, *(extra_nvcc or []), "-Xptxas", "-v" if verbose else "-O3",
+                         "-c", str(src), "-o", str(obj)])
+        objs.append(obj)
     for src in sorted((CSRC / "host").glob("*.cpp")):
         obj = build_dir / (src.stem + ".o")
         if force or _stale(obj, [src] + headers):
-            _run(["g++", *CXX_FLAGS, "-c", str(src), "-o", str(obj)], verbose)
+            jobs.append(["g++", *CXX_FLAGS, "-c", str(src), "-o", str(obj)])
         objs.append(obj)
-    for src in sorted((CSRC / "device").glob("*.cu")):
-        obj = build_dir / (src.stem + ".cu.o")
-        if force or _stale(obj, [src] + headers):
-            _run([NVCC, *NVCC_FLAGS, *dflags, *(extra_nvcc or []), "-Xptxas", "-v" if verbose else "-O3", "-c", str(src),
-                  "-o", str(obj)], verbose)
-        objs.append(obj)
+    # independent translation units compile concurrently
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(max_workers=max(1, os.cpu_count() or 1)) as pool:
+        list(pool.map(lambda cmd: _run(cmd, verbose), jobs))
     if force or _stale(libname, objs):
         _run([NVCC, *ARCH, "-shared", "-o", str(libname), *map(str, objs), "-cudart", "static",
               "-Xlinker", "--no-undefined", "-lpthread", "-ldl", "-lrt"], verbose)
