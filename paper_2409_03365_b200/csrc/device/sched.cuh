@@ -2020,12 +2020,18 @@ __device__ __forceinline__ void sched_state_io(bool save, char* g, char* sm, int
                                                int lane) {
     int4* gs = reinterpret_cast<int4*>(g + kSchedStateHdr);
     int4* ss = reinterpret_cast<int4*>(sm);
-    #pragma unroll 1
-    for (int i = lane; i < bytes / 16; i += 32) {
-        if (save)
-            gs[i] = ss[i];
-        else
-            ss[i] = gs[i];
+    if (save) {
+        #pragma unroll 1
+        for (int i = lane; i < bytes / 16; i += 32) gs[i] = ss[i];
+    } else {
+        // restore with cp.async: every 16-byte chunk in flight at once instead
+        // of one global-load round trip per loop iteration
+        #pragma unroll 1
+        for (int i = lane; i < bytes / 16; i += 32) {
+            const unsigned dst = static_cast<unsigned>(__cvta_generic_to_shared(ss + i));
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(gs + i) : "memory");
+        }
+        asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
     }
     int* flags = reinterpret_cast<int*>(g + sizeof(Ctl));
     if (save) {
