@@ -766,24 +766,30 @@ __global__ void __launch_bounds__(32 * WARPS, MINB) k_place(PlaceArgs A) {
     uint64_t* edgeb = C.template at<uint64_t>(L.edgeb);
     uint64_t* memact = C.template at<uint64_t>(L.memact);
     uint64_t* parb = C.template at<uint64_t>(L.parb);
+    // every global load of an iteration first, then the shared stores: the
+    // compiler cannot move loads across the (possibly aliasing) generic stores,
+    // so interleaving them would serialize one DRAM round trip per field
     #pragma unroll 1
     for (int k = lane; k < K; k += 32) {
-        by_rank[k] = r_by_rank[k];
-        idrank[k] = r_idrank[k];
-        pred_r[k] = r_pred[k];
-        const int gm = C.mbase + r_mod_of[k];
-        const int Lk = B.mod_layers[gm];  // one MetaOp per module: length == layers
-        parb[k] = static_cast<uint64_t>(static_cast<double>(B.mod_param[gm]) * Lk / B.mod_layers[gm]);
-        const uint64_t act = B.mod_act[gm];
+        const int rb = r_by_rank[k], ir = r_idrank[k], mo = r_mod_of[k];
+        const uint64_t pr = r_pred[k];
         const double frac = r_frac[k];  // batch_fraction (build_memory_model / build_flow_inputs)
+        const int gm = C.mbase + mo;
+        const int Lk = B.mod_layers[gm];  // one MetaOp per module: length == layers
+        const uint64_t par = B.mod_param[gm], act = B.mod_act[gm], out = B.mod_out[gm];
+        const int grp0 = B.mod_group[gm], al0 = B.mod_alias[gm], tp = B.mod_tp[gm];
+        by_rank[k] = rb;
+        idrank[k] = ir;
+        pred_r[k] = pr;
+        parb[k] = static_cast<uint64_t>(static_cast<double>(par) * Lk / Lk);
         memact[k] = static_cast<uint64_t>(static_cast<double>(act) * frac);
         contb[k] = static_cast<uint64_t>(static_cast<double>(act) * frac);
-        const uint64_t edge = B.mod_out[gm] == 0 ? act : B.mod_out[gm];
+        const uint64_t edge = out == 0 ? act : out;
         edgeb[k] = static_cast<uint64_t>(static_cast<double>(edge) * frac);
-        const int grp = (Lk == B.mod_layers[gm]) ? B.mod_group[gm] : -1;
-        const int al = h.scoped ? -1 : B.mod_alias[gm];  // scoped ids "m<k>@<task>" match no param_group
+        const int grp = grp0;  // length == layers: the MetaOp covers the whole module
+        const int al = h.scoped ? -1 : al0;  // scoped ids "m<k>@<task>" match no param_group
         gkey[k] = grp < 0 ? R.n_groups + k : ((al >= 0 && al < K) ? R.n_groups + al : grp);
-        tpk[k] = B.mod_tp[gm];
+        tpk[k] = tp;
         home[k] = -1;
         lastw[k] = -1;
         lastent[k] = -1;
@@ -806,15 +812,17 @@ __global__ void __launch_bounds__(32 * WARPS, MINB) k_place(PlaceArgs A) {
     int* e_rot = C.template at<int>(L.e_rot);
     #pragma unroll 1
     for (int w = lane; w < nW; w += 32) {
-        w_eb[w] = r_w_eb[w];
-        w_ec[w] = r_w_ec[w];
+        const int eb = r_w_eb[w], ec = r_w_ec[w];
+        w_eb[w] = eb;
+        w_ec[w] = ec;
         variant[w] = 0;
     }
     #pragma unroll 1
     for (int e = lane; e < nE; e += 32) {
-        e_k[e] = r_e_k[e];
-        e_n[e] = r_e_n[e];
-        e_l[e] = r_e_l[e];
+        const int ek = r_e_k[e], en = r_e_n[e], el = r_e_l[e];
+        e_k[e] = ek;
+        e_n[e] = en;
+        e_l[e] = el;
         e_mask[e] = dm_zero<DM>();
         e_rot[e] = 0;
     }
