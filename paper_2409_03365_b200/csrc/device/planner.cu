@@ -266,7 +266,9 @@ struct ws_ctx {
     DevBuf chunk_tops;
     cudaStream_t stream3 = nullptr;          // D2H side of the host pipeline (stream2: H2D side)
     cudaStream_t stream4 = nullptr;          // second compute stream of the host pipeline
-    DevBuf recs_r2, flows_r2;                // its retry-pass buffers
+    cudaStream_t stream5 = nullptr;          // third compute stream ($WSGPU_HOST_STREAMS=3)
+    DevBuf recs_r2, flows_r2, recs_r3, flows_r3;  // their retry-pass buffers
+    cudaEvent_t join_ev = nullptr;           // joins the third compute stream
     unsigned long long* host_tops = nullptr; // page-locked: chunk bases, chunk tops, final top, retry counts
     // soft-cap overflows beyond the first retry launch (kRetryMax plans): the
     // overflow count is copied back asynchronously and the remaining plans are
@@ -292,7 +294,7 @@ struct ws_ctx {
     // streams (consecutive chunks fill each other's tails) with completion-order D2H:
     // weights 1,3,1 24.9, 1,3,3,1 22.8, 1,4,4,1 22.8, 1,3,3,3,1 22.8, 1,5,5,1 23.8
     int host_chunks = 5;                     // $WSGPU_HOST_CHUNKS
-    int host_streams = 2;                    // $WSGPU_HOST_STREAMS (1 or 2)
+    int host_streams = 2;                    // $WSGPU_HOST_STREAMS (1 to 3)
     bool force_snap = false;                 // $WSGPU_FORCE_SNAP: k_place<true> for every batch (tuning)
     // k_sched launched programmatic-dependent on k_fit: its graph stage overlaps
     // k_fit (measured: single-plan latency -7..-10%, 100k throughput unchanged);
@@ -604,12 +606,14 @@ int ws_ctx_create(int device, ws_ctx** out) {
               cudaStreamCreateWithFlags(&c->stream2, cudaStreamNonBlocking) == cudaSuccess &&
               cudaStreamCreateWithFlags(&c->stream3, cudaStreamNonBlocking) == cudaSuccess &&
               cudaStreamCreateWithFlags(&c->stream4, cudaStreamNonBlocking) == cudaSuccess &&
+              cudaStreamCreateWithFlags(&c->stream5, cudaStreamNonBlocking) == cudaSuccess &&
               cudaMallocHost(reinterpret_cast<void**>(&c->host_tops), 8 * kHostTopsWords) == cudaSuccess;
     for (auto& e : c->ev) ok = ok && cudaEventCreate(&e) == cudaSuccess;
     for (auto& e : c->sev) ok = ok && cudaEventCreate(&e) == cudaSuccess;
     for (auto& e : c->cev) ok = ok && cudaEventCreateWithFlags(&e, cudaEventDisableTiming) == cudaSuccess;
     ok = ok && cudaEventCreateWithFlags(&c->order_ev, cudaEventDisableTiming) == cudaSuccess;
     ok = ok && cudaEventCreateWithFlags(&c->drain_ev, cudaEventDisableTiming) == cudaSuccess;
+    ok = ok && cudaEventCreateWithFlags(&c->join_ev, cudaEventDisableTiming) == cudaSuccess;
     ok = ok && smem_opt_in_all(device) == cudaSuccess;
     if (!ok) {
         cudaGetLastError();
@@ -635,7 +639,7 @@ int ws_ctx_create(int device, ws_ctx** out) {
     }
     if (const char* env = std::getenv("WSGPU_FORCE_SNAP")) c->force_snap = std::atoi(env) != 0;
     if (const char* env = std::getenv("WSGPU_PDL")) c->pdl = std::atoi(env) != 0;
-    if (const char* env = std::getenv("WSGPU_HOST_STREAMS")) c->host_streams = std::max(1, std::min(2, std::atoi(env)));
+    if (const char* env = std::getenv("WSGPU_HOST_STREAMS")) c->host_streams = std::max(1, std::min(3, std::atoi(env)));
     if (const char* env = std::getenv("WSGPU_TINY_SOFT_CAPS")) c->tiny_soft = std::atoi(env) != 0;
     if (const char* env = std::getenv("WSGPU_SMALL_PATH")) c->small_path = std::atoi(env) != 0;
     if (const char* env = std::getenv("WSGPU_TRACE")) c->trace = std::atoi(env) != 0;
@@ -650,11 +654,11 @@ void ws_ctx_destroy(ws_ctx* c) {
     if (!c) return;
     DevGuard g(c->device);
     if (c->stream) cudaStreamSynchronize(c->stream);
-    for (cudaEvent_t* e : {c->ev, c->ev + 1, c->ev + 2, c->ev + 3, c->sev, c->sev + 1, &c->order_ev, &c->drain_ev})
+    for (cudaEvent_t* e : {c->ev, c->ev + 1, c->ev + 2, c->ev + 3, c->sev, c->sev + 1, &c->order_ev, &c->drain_ev, &c->join_ev})
         if (*e) cudaEventDestroy(*e);
     for (auto& e : c->cev)
         if (e) cudaEventDestroy(e);
-    for (cudaStream_t s : {c->stream, c->stream2, c->stream3, c->stream4})
+    for (cudaStream_t s : {c->stream, c->stream2, c->stream3, c->stream4, c->stream5})
         if (s) cudaStreamDestroy(s);
     if (c->host_tops) cudaFreeHost(c->host_tops);
     if (c->order_pinned) cudaFreeHost(c->order_pinned);
@@ -1152,12 +1156,13 @@ int host_range(ws_ctx* ctx, const ws_batch* in, int P0, int P1, ws_plan_result* 
     const ws_batch& B = ctx->dview;
     // compute streams: chunk c runs on cs[c % S]; chunk c+1's kernels fill chunk c's launch tail
     const int S = ctx->host_streams;
-    cudaStream_t cs[2] = {st, ctx->stream4};
+    cudaStream_t cs[3] = {st, ctx->stream4, ctx->stream5};
     if (S > 1) {
-        if (!ctx->recs_r2.ensure(ctx->recs_r.n) || !ctx->flows_r2.ensure(ctx->flows_r.n))
+        if (!ctx->recs_r2.ensure(ctx->recs_r.n) || !ctx->flows_r2.ensure(ctx->flows_r.n) ||
+            (S > 2 && (!ctx->recs_r3.ensure(ctx->recs_r.n) || !ctx->flows_r3.ensure(ctx->flows_r.n))))
             return fail(ctx, "cudaMalloc retry buffers");
         CK(cudaEventRecord(ctx->ev[1], st));
-        CK(cudaStreamWaitEvent(cs[1], ctx->ev[1], 0));
+        for (int k = 1; k < S; ++k) CK(cudaStreamWaitEvent(cs[k], ctx->ev[1], 0));
     }
     for (int c = 0; c < C; ++c) {  // compute side
         const int p0 = pb[c], p1 = pb[c + 1];
@@ -1166,8 +1171,8 @@ int host_range(ws_ctx* ctx, const ws_batch* in, int P0, int P1, ws_plan_result* 
         cudaStream_t s = cs[k];
         auto* rcount = reinterpret_cast<int32_t*>(counters + 2 + k);
         int32_t* rids = ctx->retry_ids.as<int32_t>() + p0;  // chunks own disjoint plan ranges
-        DevBuf& rrecs = k ? ctx->recs_r2 : ctx->recs_r;
-        DevBuf& rflows = k ? ctx->flows_r2 : ctx->flows_r;
+        DevBuf& rrecs = k == 2 ? ctx->recs_r3 : k ? ctx->recs_r2 : ctx->recs_r;
+        DevBuf& rflows = k == 2 ? ctx->flows_r3 : k ? ctx->flows_r2 : ctx->flows_r;
         CK(cudaStreamWaitEvent(s, h2d[c], 0));
         TopScope ts(ctx, tops + c, abase[c + 1]);
         if (m1 > m0) {
@@ -1193,9 +1198,13 @@ int host_range(ws_ctx* ctx, const ws_batch* in, int P0, int P1, ws_plan_result* 
         CK(cudaMemcpyAsync(ctx->host_tops + kMaxHostChunks + c, tops + c, 8, cudaMemcpyDeviceToHost, s));
         CK(cudaEventRecord(done[c], s));
     }
-    if (S > 1) {  // join the second compute stream
+    if (S > 1) {  // join the other compute streams
         CK(cudaEventRecord(ctx->ev[3], cs[1]));
         CK(cudaStreamWaitEvent(st, ctx->ev[3], 0));
+    }
+    if (S > 2) {
+        CK(cudaEventRecord(ctx->join_ev, cs[2]));
+        CK(cudaStreamWaitEvent(st, ctx->join_ev, 0));
     }
     CK(cudaEventRecord(ctx->ev[2], st));
     t_issued = hclk::now();

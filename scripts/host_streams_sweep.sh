@@ -1,0 +1,13 @@
+# e2e of ws_plan_batch_host (100k sweep): compute streams x chunk weights, repeated
+for rep in 1 2 3; do for cfg in 2:1,4,4,2,1 3:1,2,2,2,2,1 3:1,3,3,3,2,1 3:1,4,4,2,1; do
+s=${cfg%%:*}; w=${cfg#*:}
+WSGPU_HOST_STREAMS=$s WSGPU_HOST_WEIGHTS=$w python -c "
+import sys,time; sys.path.insert(0,'.')
+import torch, paper_2409_03365_b200 as ws
+ps=ws.ProblemSet(); ps.add_sweep(0,100000); ps.encode(pinned=True); pl=ws.Planner(0); r=pl.plan(ps); r=pl.plan(ps,out=r)
+best=1e9
+for _ in range(8):
+    torch.cuda.synchronize(); t0=time.perf_counter(); r=pl.plan(ps,out=r); best=min(best,time.perf_counter()-t0)
+print('streams $s weights $w', round(best*1e3,2), 'ms')
+"
+done; done
