@@ -34,6 +34,7 @@ struct PlSmLayout {
     int isllow;                                                   // [IS] u64 devices below island i
     int islfull;                                                  // [IS] u64 islands of the whole plan
     int glist;                                                    // [W] i32 waves of the current place() call
+    int btm;                                                      // [W] int2 backtracking memo (k_place DFS)
     int nwin;                                                     // [IS] i32
     int chg;                                                      // [G] u64
     int fin_src, fin_bytes;                                       // [M+1]
@@ -83,6 +84,7 @@ __host__ __device__ constexpr PlSmLayout make_pl_layout(const PlaceCaps& c, int 
     L.isllow = take(mb * c.IS);
     L.islfull = take(mb * c.IS);
     L.glist = take(4 * W);
+    L.btm = take(8 * W);
     L.nwin = take(4 * (c.IS + W + 1));  // island window counts, then flows-per-wave marks
     L.chg = take(mb * c.G);
     L.fin_src = take(4 * (M + 1));
@@ -139,6 +141,7 @@ struct PCtx {
     int lane, N, K, mbase, nW, nE, nF, Fcap, G, n_isl;
     int contig;  // every island is one contiguous run of device indices
     int dev_off, dev_cnt;  // device block of the current place() call ([0, N) unless grouped)
+    int first_nc;          // candidate count of the wave's first entry (p_wave; 1 << 30: unknown)
     DM all;           // devices of the current place() call
     uint64_t* flows;  // this plan's flow list (2 words per flow)
     // plan options hoisted out of the per-attempt loops (registers, not global loads)
@@ -201,6 +204,7 @@ __device__ int p_wave(PCtx<DM>& C, int w, int variant) {
     uint64_t* va = C.template at<uint64_t>(L.va);
     const int* w_cursor = C.template at<int>(L.w_cursor);
     const int eb = w_eb[w], ec = w_ec[w];
+    C.first_nc = 1 << 30;
 
     WS_PH_START(tw);
     // incoming volume per entry (incoming_flows :188-206), entry order (:208-221)
@@ -389,6 +393,7 @@ __device__ int p_wave(PCtx<DM>& C, int w, int variant) {
                     ncand += __popc(bal);
                 }
                 __syncwarp();
+                if (oi == 0) C.first_nc = ncand;
                 WS_PH_STOP(tw, 3);
                 WS_PH_COUNT(20, 1);
                 WS_PH_COUNT(21, ncand);
@@ -963,8 +968,31 @@ __global__ void __launch_bounds__(32 * WARPS, MINB) k_place(PlaceArgs A) {
     int k = 0;
     bool dirty = false;
     if (lane == 0) wave_nf[0] = C.nF;
+    // Repeated attempts are skipped, not re-run.  Variant v of wave k takes rank
+    // min(v, c - 1) of its first entry's c sorted candidates, so for v >= c it
+    // places exactly what variant v - 1 placed from the same state: a failure
+    // fails again, and a success re-runs the subtree below it attempt for
+    // attempt (deeper variants are back at 0) until it steps back into wave k.
+    // Such an attempt only advances the counter: by 1, or by 1 + the subtree's
+    // recorded attempt count.  Skips stay within the budget; an attempt that
+    // would cross it runs for real, so the exhaustion error names the same wave.
+    // btm[k] = {c of wave k's last attempt, -1 if it failed, else the attempt
+    // number it succeeded at, turned into the subtree length on the step-back}.
+    int2* btm = C.template at<int2>(L.btm);
+    const bool memo = budget < (1ll << 30);
     while (k < gn) {
         WS_PH_COUNT(28, 1);
+        if (memo && variant[k] >= 1 && variant[k] < branching) {
+            const int2 m = btm[k];
+            const long long add = m.y >= 0 ? 1ll + m.y : 1ll;
+            if (variant[k] >= m.x && attempts + add <= budget) {
+                attempts += add;
+                __syncwarp();
+                if (lane == 0) variant[k]++;
+                __syncwarp();
+                continue;
+            }
+        }
         if (++attempts > budget) {
             if (lane == 0) {
                 set_err(ctl, WS_E_BT_BUDGET, k);
@@ -1052,7 +1080,10 @@ __global__ void __launch_bounds__(32 * WARPS, MINB) k_place(PlaceArgs A) {
                 const int e = w_eb[wk] + i;
                 home[e_k[e]] = e_prev[e];
             }
-            if (lane == 0) variant[k]++;
+            if (lane == 0) {
+                btm[k].y = static_cast<int>(attempts) - btm[k].y;  // subtree attempts incl. this step-back
+                variant[k]++;
+            }
             dirty = true;
             __syncwarp();
             continue;
@@ -1061,6 +1092,7 @@ __global__ void __launch_bounds__(32 * WARPS, MINB) k_place(PlaceArgs A) {
         WS_PH_COUNT(30, 1);
         const int r = p_wave<DM, FIXED>(C, wk, variant[k]);
         __syncwarp();
+        if (lane == 0) btm[k] = make_int2(C.first_nc, r > 0 ? static_cast<int>(attempts) : -1);
         if (r < 0) {
             if (lane == 0) {
                 write_error(A.results + p, ctl);
