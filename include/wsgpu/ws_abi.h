@@ -27,7 +27,7 @@ extern "C" {
 /* Device-side limits of this build (per plan).  A plan exceeding one returns
  * WS_STATUS_LIMIT with err_code naming the limit; nothing falls back to CPU. */
 #define WS_MAX_DEVICES 256  /* device sets: one u64 mask up to 64 devices, four words up to 256 */
-#define WS_MAX_DEVICES_EVAL 64 /* plan evaluation (simulate/validate, plan files) */
+#define WS_MAX_DEVICES_EVAL 256 /* plan evaluation (simulate/validate, plan files)  */
 #define WS_MAX_MODULES 64   /* module DAG adjacency is u64 masks               */
 #define WS_MAX_TASKS 64     /* task sets are u64 masks                         */
 #define WS_MAX_PIECES 64    /* fitted pieces per curve (isotonic: nmax-1)      */
@@ -264,8 +264,9 @@ typedef struct ws_sim_result {
     double fwd_bwd_fraction, param_sync_fraction, send_recv_fraction;
     double total_transferred_bytes, total_inter_island_bytes;
     uint64_t offset;        /* this plan's record in the simulation arena:             */
-    uint64_t size;          /*   busy[N] f64, busy_mask u64, mem[N] f64, util[K] f64,   */
-                            /*   util_mask u64, ws_out_violation[min(n, MAX)]          */
+    uint64_t size;          /*   busy[N] f64, busy_mask (1 u64; 4 when N > 64),         */
+                            /*   mem[N] f64, util[K] f64, util_mask u64,               */
+                            /*   ws_out_violation[min(n, MAX)]                         */
 } ws_sim_result;
 
 #define WS_SIM_MAX_VIOLATIONS 16

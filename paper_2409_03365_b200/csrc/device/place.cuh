@@ -505,10 +505,13 @@ __device__ void p_emit(PCtx<DM>& C, int p, const char* rec, const RecLayout& RL,
     nedges = warp_sum(nedges);
     const int nL = h.n_levels, nW = h.nW, nE = h.nE, nF = C.nF;
     const int nS = h.scoped ? K : 0;  // (MetaOp, task) of each entity
+    // the ext section exists for clusters over 64 devices only (a narrow plan of
+    // a wide launch has the narrow record layout; readers go by the plan's N)
+    const bool ext_on = kExt > 0 && C.R->n_dev > 64;
     const uint64_t sz = al8(sizeof(ws_out_metaop) * K) + al8(sizeof(ws_out_level) * nL) +
                         al8(sizeof(ws_out_piece) * npieces) + al8(sizeof(ws_out_edge) * nedges) +
                         al8(sizeof(ws_out_wave) * nW) + al8(sizeof(ws_out_entry) * nE) + al8(sizeof(ws_out_flow) * nF) +
-                        al8(sizeof(ws_out_scope) * nS) + 8ull * kExt * nE;
+                        al8(sizeof(ws_out_scope) * nS) + (ext_on ? 8ull * kExt * nE : 0ull);
     unsigned long long off = 0;
     if (lane == 0) off = atomicAdd(A.arena_top, static_cast<unsigned long long>(sz));
     off = __shfl_sync(kFull, off, 0);
@@ -647,10 +650,12 @@ __device__ void p_emit(PCtx<DM>& C, int p, const char* rec, const RecLayout& RL,
         for (int k = lane; k < nS; k += 32) sc[k] = ws_out_scope{r_met[k], r_task[k]};
     }
     if constexpr (kExt > 0) {  // device words 1..W-1 of entry e at [e * kExt + j - 1] (ws_abi.h)
-        auto* ext = reinterpret_cast<uint64_t*>(base + o + al8(sizeof(ws_out_flow) * nF) +
-                                                al8(sizeof(ws_out_scope) * nS));
-        #pragma unroll 1
-        for (int i = lane; i < nE * kExt; i += 32) ext[i] = dm_word(e_mask[i / kExt], 1 + i % kExt);
+        if (ext_on) {
+            auto* ext = reinterpret_cast<uint64_t*>(base + o + al8(sizeof(ws_out_flow) * nF) +
+                                                    al8(sizeof(ws_out_scope) * nS));
+            #pragma unroll 1
+            for (int i = lane; i < nE * kExt; i += 32) ext[i] = dm_word(e_mask[i / kExt], 1 + i % kExt);
+        }
     }
     if (lane == 0) {
         ws_plan_result r{};

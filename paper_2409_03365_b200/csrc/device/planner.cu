@@ -362,14 +362,16 @@ cudaError_t smem_opt_in_all(int device) {
         if (e == cudaSuccess) e = smem_opt_in(k_sched<DevMask<4>, 1>);
         if (e == cudaSuccess) e = smem_opt_in(k_sched<DevMask<4>, 2>);
         if (e == cudaSuccess) e = smem_opt_in(k_sched<DevMask<4>, 3>);
-        if (e == cudaSuccess) e = smem_opt_in(k_sched_scoped);
+        if (e == cudaSuccess) e = smem_opt_in(k_sched_scoped<uint64_t>);
+        if (e == cudaSuccess) e = smem_opt_in(k_sched_scoped<DevMask<4>>);
         if (e == cudaSuccess) e = smem_opt_in(k_place<true>);
         if (e == cudaSuccess) e = smem_opt_in(k_place<false>);
         if (e == cudaSuccess) e = smem_opt_in(k_place<true, DevMask<4>, 1, 1>);
         if (e == cudaSuccess) e = smem_opt_in(k_place<true, uint64_t, kPlaceWarps, WS_PLACE_MINB, true>);
         if (e == cudaSuccess) e = smem_opt_in(k_place<false, uint64_t, kPlaceWarps, WS_PLACE_MINB, true>);
         if (e == cudaSuccess) e = smem_opt_in(k_place<false, DevMask<4>, 1, 1>);
-        if (e == cudaSuccess) e = smem_opt_in(k_sim);
+        if (e == cudaSuccess) e = smem_opt_in(k_sim<uint64_t>);
+        if (e == cudaSuccess) e = smem_opt_in(k_sim<DevMask<4>>);
         status[device] = e;
     });
     return status[device];
@@ -565,7 +567,7 @@ int launch_pair(ws_ctx* ctx, cudaStream_t st, const LaunchCaps& lc, const FitOut
             ctx->launches += 2;
         }
         if (lc.scoped) {  // the batch's distmm-mt plans (each instance skips the other's plans)
-            k_sched_scoped<<<(cnt + kSchedWarps - 1) / kSchedWarps, 32 * kSchedWarps, kSchedWarps * S.SL.bytes,
+            (wide ? k_sched_scoped<DevMask<4>> : k_sched_scoped<uint64_t>)<<<(cnt + kSchedWarps - 1) / kSchedWarps, 32 * kSchedWarps, kSchedWarps * S.SL.bytes,
                              st>>>(S);
             ctx->launches++;
         }
@@ -1502,7 +1504,8 @@ int ws_simulate_staged(ws_ctx* ctx, const ws_sim_opts* opts, void* stream) {
     A.parena = ctx->arena.as<uint8_t>();
     A.opt = opts ? *opts : ws_sim_opts{2.0, 0, 0};
     A.caps = SimCaps{lh.pl.G, lh.rec.W, lh.pl.IS, lh.rec.M, lh.rec.E};
-    A.SL = make_sim_layout(A.caps);
+    const bool wide = lh.pl.N > 64;  // DevMask<4> device sets, as the planning launch
+    A.SL = make_sim_layout(A.caps, wide ? static_cast<int>(sizeof(DevMask<4>)) : 8);
     A.n_plans = P;
     if (!ctx->sim_res.ensure(sizeof(ws_sim_result) * std::max(P, 1)) || !ctx->sim_arena.ensure(ctx->sim_cap) ||
         !ctx->sim_scratch.ensure(std::max<uint64_t>(ctx->arena_cap, 8)) || !ctx->sim_top.ensure(64))
@@ -1516,7 +1519,8 @@ int ws_simulate_staged(ws_ctx* ctx, const ws_sim_opts* opts, void* stream) {
     if (smem > kSmemLimit) return fail(ctx, "ws_simulate_staged: per-warp working set exceeds shared memory");
     CK(cudaMemsetAsync(A.arena_top, 0, 8, st));
     CK(cudaEventRecord(ctx->sev[0], st));
-    if (P > 0) k_sim<<<(P + kSimWarps - 1) / kSimWarps, 32 * kSimWarps, smem, st>>>(A);
+    if (P > 0)
+        (wide ? k_sim<DevMask<4>> : k_sim<uint64_t>)<<<(P + kSimWarps - 1) / kSimWarps, 32 * kSimWarps, smem, st>>>(A);
     CK(cudaEventRecord(ctx->sev[1], st));
     CK(cudaGetLastError());
     ctx->sim_valid = true;

@@ -153,7 +153,7 @@ __host__ __device__ inline SmLayout make_sm_layout(int M, bool scoped = false, i
     L.kscale = take(8 * MS);
     L.tlvl = take(4 * MS);
     L.vord = take(4 * MS);
-    L.tvalid = take(8 * TT);
+    L.tvalid = take(mb * TT);
     L.talloc = take(4 * TT);
     L.cw_start = take(8 * EM);
     L.cw_dur = take(8 * EM);
@@ -1524,6 +1524,7 @@ __device__ __forceinline__ double eval_bf_fit(const FitOut& F, const ws_batch& B
 // path of the task's sub-DAG at eval_batch_fraction), every MetaOp one wave on
 // the whole block, waves indexed by (start, entity id), one placement group
 // (device block + waves) per task.
+template <class DM>
 __device__ bool s_optimus(SCtx& C, char* rec, const RecLayout& RL, int& nW, int& nE, double& end_time, int W_CAP,
                           int E_CAP, int& KE_out, int& npg_out) {
     const ws_batch& B = *C.B;
@@ -1538,7 +1539,7 @@ __device__ bool s_optimus(SCtx& C, char* rec, const RecLayout& RL, int& nW, int&
     const int* mod_of = C.at<int>(C.L->mod_of);
     const uint64_t* pred_r = C.at<uint64_t>(C.L->pred_r);
     const uint64_t* succ_r = C.at<uint64_t>(C.L->succ_r);
-    const uint64_t* valid = C.at<uint64_t>(C.L->valid);
+    const DM* valid = C.at<DM>(C.L->valid);
     const uint64_t* tmask = C.at<uint64_t>(C.L->tmask);
     int* ent_met = C.at<int>(C.L->ent_met);
     int* ent_task = C.at<int>(C.L->ent_task);
@@ -1547,7 +1548,7 @@ __device__ bool s_optimus(SCtx& C, char* rec, const RecLayout& RL, int& nW, int&
     int* ent_of = C.at<int>(C.L->ent_of);
     int* vord = C.at<int>(C.L->vord);
     int* indeg = C.at<int>(C.L->absorb);
-    uint64_t* tvalid = C.at<uint64_t>(C.L->tvalid);
+    DM* tvalid = C.at<DM>(C.L->tvalid);
     int* talloc = C.at<int>(C.L->talloc);
     double* cw_start = C.at<double>(C.L->cw_start);
     double* cw_dur = C.at<double>(C.L->cw_dur);
@@ -1622,7 +1623,7 @@ __device__ bool s_optimus(SCtx& C, char* rec, const RecLayout& RL, int& nW, int&
         #pragma unroll 1
         for (int t = 0; t < T && !C.ctl->err; ++t) {  // common valid allocations (valid_allocations per n)
             const int nm = task_order(members(t));
-            uint64_t tv = 0;
+            DM tv = dm_zero<DM>();
             #pragma unroll 1
             for (int n = 1; n <= N && !C.ctl->err; ++n) {
                 bool ok = true;
@@ -1634,14 +1635,14 @@ __device__ bool s_optimus(SCtx& C, char* rec, const RecLayout& RL, int& nW, int&
                         set_err(C.ctl, WS_E_TP_EXCEEDS, k, tp);
                         break;
                     }
-                    if (!(valid[k] >> (n - 1) & 1ull)) {
+                    if (!dm_test(valid[k], n - 1)) {
                         ok = false;
                         break;
                     }
                 }
-                if (ok && !C.ctl->err) tv |= 1ull << (n - 1);
+                if (ok && !C.ctl->err) tv |= dm_bit<DM>(n - 1);
             }
-            if (!C.ctl->err && !tv) set_err(C.ctl, WS_E_TASK_NO_VALID, t);
+            if (!C.ctl->err && !dm_any(tv)) set_err(C.ctl, WS_E_TASK_NO_VALID, t);
             tvalid[t] = tv;
         }
         double batch_offset = 0.0;
@@ -1649,7 +1650,7 @@ __device__ bool s_optimus(SCtx& C, char* rec, const RecLayout& RL, int& nW, int&
         for (int b0 = 0; b0 < T && !C.ctl->err;) {  // batches whose minimum allocations fit
             int b1 = b0, used = 0;
             while (b1 < T) {
-                const int need = low_bit(tvalid[b1]) + 1;
+                const int need = dm_low(tvalid[b1]) + 1;
                 if (used + need > N && b1 > b0) break;
                 used += need;
                 ++b1;
@@ -1660,7 +1661,7 @@ __device__ bool s_optimus(SCtx& C, char* rec, const RecLayout& RL, int& nW, int&
             // every task at every step; the values, hence the gains, are identical)
             #pragma unroll 1
             for (int t = b0; t < b1; ++t) {
-                talloc[t] = low_bit(tvalid[t]) + 1;
+                talloc[t] = dm_low(tvalid[t]) + 1;
                 tcur[t] = -1.0;
                 tnxn[t] = -1;
             }
@@ -1674,9 +1675,9 @@ __device__ bool s_optimus(SCtx& C, char* rec, const RecLayout& RL, int& nW, int&
                 double best_gain = -1.0;
                 #pragma unroll 1
                 for (int t = b0; t < b1; ++t) {
-                    const uint64_t above = tvalid[t] & ~bits_upto(talloc[t] - 1);  // std::upper_bound
-                    if (!above) continue;
-                    const int nx = low_bit(above) + 1;
+                    const DM above = tvalid[t] & ~dm_first<DM>(talloc[t]);  // std::upper_bound
+                    if (!dm_any(above)) continue;
+                    const int nx = dm_low(above) + 1;
                     if (nx - talloc[t] > free) continue;
                     if (tcur[t] < 0.0) tcur[t] = task_time(t, talloc[t]);
                     if (tnxn[t] != nx) {
@@ -1815,6 +1816,7 @@ __device__ bool s_optimus(SCtx& C, char* rec, const RecLayout& RL, int& nW, int&
 // valid allocation, a wider level splits the cluster through the level
 // machinery (s_level_alloc + s_schedule_level) on curves whose per-device term
 // is scaled by the share fraction 1/|tasks|; entities are (MetaOp, task) pairs.
+template <class DM>
 __device__ bool s_distmm(SCtx& C, char* rec, const RecLayout& RL, int& nW, int& nE, double& end_time, int W_CAP,
                          int E_CAP, int& KE_out) {
     const ws_batch& B = *C.B;
@@ -1827,7 +1829,7 @@ __device__ bool s_distmm(SCtx& C, char* rec, const RecLayout& RL, int& nW, int& 
     const int* Lk = C.at<int>(C.L->Lk);
     const int* mod_of = C.at<int>(C.L->mod_of);
     const uint64_t* pred_r = C.at<uint64_t>(C.L->pred_r);
-    const uint64_t* valid = C.at<uint64_t>(C.L->valid);
+    const DM* valid = C.at<DM>(C.L->valid);
     const uint64_t* tmask = C.at<uint64_t>(C.L->tmask);
     int* ent_met = C.at<int>(C.L->ent_met);
     int* ent_task = C.at<int>(C.L->ent_task);
@@ -1932,7 +1934,7 @@ __device__ bool s_distmm(SCtx& C, char* rec, const RecLayout& RL, int& nW, int& 
             if (w == 1) {
                 if (lane == 0) {
                     const int k = lm[0];
-                    const int n = 64 - __clzll(static_cast<long long>(valid[k]));  // valid.back()
+                    const int n = dm_high(valid[k]) + 1;  // valid.back()
                     if (n > nmax_of[k]) {  // scaled.eval(n) OutOfRange (scaling.hpp:66-68)
                         C.ctl->err = WS_E_EVAL_RANGE;
                         C.ctl->x = n;
@@ -1961,7 +1963,7 @@ __device__ bool s_distmm(SCtx& C, char* rec, const RecLayout& RL, int& nW, int& 
             }
             C.kscale = kscale;
             double cs = 0.0;
-            bool ok = s_level_alloc<uint64_t>(C, 0, cs);  // sums in task order (LevelInput order)
+            bool ok = s_level_alloc<DM>(C, 0, cs);  // sums in task order (LevelInput order)
             if (ok) {
                 if (lane == 0)  // discretized tuples / schedule_level go by MetaOp id
                     #pragma unroll 1
@@ -1974,7 +1976,7 @@ __device__ bool s_distmm(SCtx& C, char* rec, const RecLayout& RL, int& nW, int& 
                 __syncwarp();
                 const int w0 = nW, e0 = nE;
                 double level_end = now;
-                ok = s_schedule_level<uint64_t>(C, rec, RL, 0, nW, nE, now, level_end, W_CAP, E_CAP);
+                ok = s_schedule_level<DM>(C, rec, RL, 0, nW, nE, now, level_end, W_CAP, E_CAP);
                 if (ok && lane == 0) {
                     double t_end = 0.0;  // schedule_level's own clock, from 0
                     #pragma unroll 1
@@ -2142,9 +2144,9 @@ __device__ __forceinline__ void sched_body(const SchedArgs& A, char* smem_dyn, C
     } else if (ok && scoped) {
         if constexpr (SCOPED) {
             if (R.strategy == WS_STRATEGY_TASK_OPTIMUS)
-                ok = s_optimus(C, rec, A.RL, nW, nE, offset, A.caps.W, A.caps.E, KE, n_pg);
+                ok = s_optimus<DM>(C, rec, A.RL, nW, nE, offset, A.caps.W, A.caps.E, KE, n_pg);
             else
-                ok = s_distmm(C, rec, A.RL, nW, nE, offset, A.caps.W, A.caps.E, KE);
+                ok = s_distmm<DM>(C, rec, A.RL, nW, nE, offset, A.caps.W, A.caps.E, KE);
         }
     } else if (ok) {
         n_levels = ctl->i1;
@@ -2291,10 +2293,11 @@ __global__ void __launch_bounds__(32 * kSchedWarps) k_sched(SchedArgs A) {
 }
 
 // plan_distmm_mt plans of the batch (the planner instance skips them)
+template <class DM = uint64_t>
 __global__ void __launch_bounds__(32 * kSchedWarps) k_sched_scoped(SchedArgs A) {
     extern __shared__ __align__(16) char smem_dyn[];
     __shared__ Ctl ctl_s[kSchedWarps];
-    sched_body<true>(A, smem_dyn, ctl_s);
+    sched_body<true, DM>(A, smem_dyn, ctl_s);
 }
 
 }  // namespace wsdev

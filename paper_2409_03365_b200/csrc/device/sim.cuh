@@ -9,6 +9,10 @@
 // every double is produced by the same operations in the same order.
 // Validation (a verdict plus the first WS_SIM_MAX_VIOLATIONS violation records)
 // runs on the same warp; the host rebuilds the reference messages.
+//
+// Written over the device-mask type DM (mask.cuh): uint64_t for clusters of up
+// to 64 devices, DevMask<4> up to 256; a lane then owns devices lane + 32 s,
+// s < 2 * kWords, and the record's device words 1..3 come from its ext section.
 #pragma once
 #include "kcommon.cuh"
 
@@ -19,9 +23,9 @@ struct SimCaps {
 };
 
 struct SimSmLayout {
-    int isl;     // [IS] u64 island device masks
-    int chg;     // [G]  u64 devices charged per group (compute_device_memory)
-    int gmask;   // [G]  u64 devices per group (build_param_groups)
+    int isl;     // [IS] DM  island device masks
+    int chg;     // [G]  DM  devices charged per group (compute_device_memory)
+    int gmask;   // [G]  DM  devices per group (build_param_groups)
     int gbytes;  // [G]  u64 gradient bytes per group
     int pbytes;  // [G]  u64 pooled bytes per representative group
     int pord;    // [G]  i32 pool representatives in device-list order
@@ -35,7 +39,8 @@ struct SimSmLayout {
     int bytes;
 };
 
-__host__ __device__ inline SimSmLayout make_sim_layout(const SimCaps& c) {
+// mb: bytes of one device mask (8: uint64_t, 32: DevMask<4>)
+__host__ __device__ inline SimSmLayout make_sim_layout(const SimCaps& c, int mb = 8) {
     SimSmLayout L{};
     int o = 0;
     auto take = [&](int b) {
@@ -43,9 +48,9 @@ __host__ __device__ inline SimSmLayout make_sim_layout(const SimCaps& c) {
         o = (o + b + 7) & ~7;
         return at;
     };
-    L.isl = take(8 * c.IS);
-    L.chg = take(8 * c.G);
-    L.gmask = take(8 * c.G);
+    L.isl = take(mb * c.IS);
+    L.chg = take(mb * c.G);
+    L.gmask = take(mb * c.G);
     L.gbytes = take(8 * c.G);
     L.pbytes = take(8 * c.G);
     L.pord = take(4 * c.G);
@@ -104,6 +109,26 @@ __device__ __forceinline__ bool devlist_less(uint64_t a, uint64_t b) {
     return (a & d) ? (b & above) != 0 : !(a & above);
 }
 
+template <int W>
+__device__ __forceinline__ bool devlist_less(const DevMask<W>& a, const DevMask<W>& b) {
+    const DevMask<W> diff = a ^ b;
+    if (!dm_any(diff)) return false;
+    const int d = dm_low(diff);
+    const DevMask<W> above = ~dm_first<DevMask<W>>(d + 1);  // devices strictly above d
+    return dm_test(a, d) ? dm_any(b & above) : !dm_any(a & above);
+}
+
+// m |= x on a shared-memory mask, one atomic per nonzero word
+__device__ __forceinline__ void dm_atomic_or(uint64_t* p, uint64_t x) {
+    atomicOr(reinterpret_cast<unsigned long long*>(p), x);
+}
+template <int W>
+__device__ __forceinline__ void dm_atomic_or(DevMask<W>* p, const DevMask<W>& x) {
+    #pragma unroll
+    for (int i = 0; i < W; ++i)
+        if (x.w[i]) atomicOr(reinterpret_cast<unsigned long long*>(&p->w[i]), x.w[i]);
+}
+
 struct SimRec {
     const ws_out_metaop* mo;
     const ws_out_piece* pc;
@@ -112,8 +137,10 @@ struct SimRec {
     const ws_out_entry* en;
     const ws_out_flow* fl;
     const ws_out_scope* sc;  // task-scoped entities (n_scopes > 0)
+    const uint64_t* ext;     // device words 1..3 per entry (records of clusters over 64 devices)
     uint64_t en_off;  // entries section offset inside the record
     uint64_t fl_off;  // flows section offset
+    uint64_t ext_off; // ext section offset
 };
 
 __device__ __forceinline__ SimRec sim_rec(const ws_plan_result& r, const uint8_t* base) {
@@ -135,63 +162,38 @@ __device__ __forceinline__ SimRec sim_rec(const ws_plan_result& r, const uint8_t
     v.fl_off = o;
     o += al8(sizeof(ws_out_flow) * r.n_flows);
     v.sc = reinterpret_cast<const ws_out_scope*>(base + o);
+    o += al8(sizeof(ws_out_scope) * r.n_scopes);
+    v.ext = reinterpret_cast<const uint64_t*>(base + o);
+    v.ext_off = o;
     return v;
 }
 
-// plan.devices.find({w, k}): device mask of the last entry of wave w with
-// MetaOp k and a nonzero placement, 0 when absent (warp-uniform result)
-__device__ __forceinline__ uint64_t sim_find(const SimRec& V, int nW, int lane, int w, int k) {
-    if (w < 0 || w >= nW) return 0;
-    const ws_out_wave& wv = V.wv[w];
-    uint64_t m = 0;
-    #pragma unroll 1
-    for (int base = 0; base < wv.n_entries; base += 32) {
-        const int i = base + lane;
-        uint64_t dm = 0;
-        bool hit = false;
-        if (i < wv.n_entries) {
-            const ws_out_entry& e = V.en[wv.entry_begin + i];
-            dm = e.devmask;
-            hit = e.metaop == k && dm != 0;
-        }
-        const unsigned b = __ballot_sync(kFull, hit);
-        if (b) m = __shfl_sync(kFull, dm, 31 - __clz(b));
-    }
-    return m;
-}
-
-// the same lookup on one thread
-__device__ __forceinline__ uint64_t sim_find1(const SimRec& V, int nW, int w, int k) {
-    if (w < 0 || w >= nW) return 0;
-    uint64_t m = 0;
-    #pragma unroll 1
-    for (int i = 0; i < V.wv[w].n_entries; ++i) {
-        const ws_out_entry& e = V.en[V.wv[w].entry_begin + i];
-        if (e.metaop == k && e.devmask) m = e.devmask;
-    }
-    return m;
-}
-
-// max over the devices of `mask` of a per-lane pair (d = lane, lane + 32), from 0.0
-__device__ __forceinline__ double lane_max2(uint64_t mask, int lane, double a0, double a1) {
+// max over the devices of `mask` of the lane's per-device values (devices
+// lane + 32 s), from 0.0
+template <class DM, int DPL>
+__device__ __forceinline__ double lane_max(const DM& mask, int lane, const double (&a)[DPL]) {
     double t = 0.0;
-    if (mask >> lane & 1ull) t = a0;
-    if (mask >> (lane + 32) & 1ull) t = (t < a1) ? a1 : t;
+    #pragma unroll
+    for (int s = 0; s < DPL; ++s)
+        if (dm_test(mask, lane + 32 * s)) t = s == 0 ? a[0] : ((t < a[s]) ? a[s] : t);
     return warp_max_nonneg(t);
 }
 
 #ifndef WS_SIM_MINB
 #define WS_SIM_MINB 1
 #endif
+template <class DM = uint64_t>
 __global__ void __launch_bounds__(32 * kSimWarps, WS_SIM_MINB) k_sim(SimArgs A) {
+    constexpr int kW = MaskTraits<DM>::kWords;  // 64-bit words per device mask
+    constexpr int DPL = 2 * kW;                 // devices per lane: lane + 32 s
     extern __shared__ __align__(16) char sim_smem[];
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int p = blockIdx.x * kSimWarps + wid;
     if (p >= A.n_plans) return;
     const ws_plan_result& R = A.plans[p];
     ws_sim_result* res = A.out + p;
-    if (R.status != WS_STATUS_OK || A.B.plans[p].n_dev > WS_MAX_DEVICES_EVAL) {
-        if (lane == 0) {  // evaluation covers clusters of up to 64 devices (u64 masks)
+    if (R.status != WS_STATUS_OK || A.B.plans[p].n_dev > MaskTraits<DM>::kBits) {
+        if (lane == 0) {  // (the launch picks the mask width for the batch's widest cluster)
             ws_sim_result r{};
             r.status = R.status != WS_STATUS_OK ? R.status : WS_STATUS_LIMIT;
             *res = r;
@@ -204,16 +206,53 @@ __global__ void __launch_bounds__(32 * kSimWarps, WS_SIM_MINB) k_sim(SimArgs A) 
     const SimRec V = sim_rec(R, A.parena + R.offset);
     const int N = P.n_dev, K = R.n_metaops, nW = R.n_waves, nE = R.n_entries, nF = R.n_flows;
     const int G = P.n_groups + K, mbase = P.mod_begin;
-    const uint64_t all = N == 64 ? ~0ull : ((1ull << N) - 1ull);
+    const DM all = dm_first<DM>(N);
+    const bool wide_rec = kW > 1 && N > 64;  // the record carries device words 1..3 per entry
     // per-entry / per-flow scratch mirroring the record (one 32-byte slot each):
     // entry: [0] interval end (f64), [1] start (f64), [2] check flags (i32),
     //        [3] plan.devices placement of its (wave, MetaOp) key (u64)
     // flow:  [0] source placement, [1] destination placement, [2] flow_duration
     uint8_t* const s_rec = A.scratch + R.offset;
     auto en_iv = [&](int e) { return reinterpret_cast<double*>(s_rec + V.en_off + 32ull * e); };
-    auto en_pl = [&](int e) { return reinterpret_cast<uint64_t*>(s_rec + V.en_off + 32ull * e + 24); };
     auto en_flags = [&](int e) { return reinterpret_cast<int*>(s_rec + V.en_off + 32ull * e + 16); };
     auto fl_masks = [&](int f) { return reinterpret_cast<uint64_t*>(s_rec + V.fl_off + 32ull * f); };
+    // entry e's device set as recorded (word 0 + the ext words of wide records)
+    auto raw_mask = [&](int e) {
+        DM m = dm_zero<DM>();
+        dm_set_word(m, 0, V.en[e].devmask);
+        if (wide_rec)
+            #pragma unroll
+            for (int j = 1; j < kW; ++j) dm_set_word(m, j, V.ext[(kW - 1) * e + j - 1]);
+        return m;
+    };
+    // per-entry placement of its (wave, MetaOp) key: word 0 in the entry's
+    // scratch slot, words 1..3 in the scratch mirror of the ext section
+    auto pl_set = [&](int e, const DM& m) {
+        *reinterpret_cast<uint64_t*>(s_rec + V.en_off + 32ull * e + 24) = dm_word(m, 0);
+        if (wide_rec)
+            #pragma unroll
+            for (int j = 1; j < kW; ++j)
+                reinterpret_cast<uint64_t*>(s_rec + V.ext_off)[(kW - 1) * e + j - 1] = dm_word(m, j);
+    };
+    auto en_pl = [&](int e) {
+        DM m = dm_zero<DM>();
+        dm_set_word(m, 0, *reinterpret_cast<const uint64_t*>(s_rec + V.en_off + 32ull * e + 24));
+        if (wide_rec)
+            #pragma unroll
+            for (int j = 1; j < kW; ++j)
+                dm_set_word(m, j, reinterpret_cast<const uint64_t*>(s_rec + V.ext_off)[(kW - 1) * e + j - 1]);
+        return m;
+    };
+    // a flow's endpoint placements: the masks (u64), or for DevMask the entry
+    // indices whose recorded sets they are (-1: none)
+    auto fl_end = [&](int f, int h) {
+        if constexpr (kW == 1) {
+            return fl_masks(f)[h];
+        } else {
+            const long long i = static_cast<long long>(fl_masks(f)[h]);
+            return i < 0 ? dm_zero<DM>() : raw_mask(static_cast<int>(i));
+        }
+    };
     if (G > A.caps.G || G > 128 || nW > A.caps.W || P.n_islands > A.caps.IS || K > A.caps.K || nE > A.caps.E) {
         if (lane == 0) {
             ws_sim_result r{};
@@ -222,9 +261,9 @@ __global__ void __launch_bounds__(32 * kSimWarps, WS_SIM_MINB) k_sim(SimArgs A) 
         }
         return;
     }
-    uint64_t* islm = reinterpret_cast<uint64_t*>(sm + A.SL.isl);
-    uint64_t* chg = reinterpret_cast<uint64_t*>(sm + A.SL.chg);
-    uint64_t* gmask = reinterpret_cast<uint64_t*>(sm + A.SL.gmask);
+    DM* islm = reinterpret_cast<DM*>(sm + A.SL.isl);
+    DM* chg = reinterpret_cast<DM*>(sm + A.SL.chg);
+    DM* gmask = reinterpret_cast<DM*>(sm + A.SL.gmask);
     uint64_t* gbytes = reinterpret_cast<uint64_t*>(sm + A.SL.gbytes);
     uint64_t* pbytes = reinterpret_cast<uint64_t*>(sm + A.SL.pbytes);
     int* pord = reinterpret_cast<int*>(sm + A.SL.pord);
@@ -240,18 +279,18 @@ __global__ void __launch_bounds__(32 * kSimWarps, WS_SIM_MINB) k_sim(SimArgs A) 
     // ---- per-plan tables ------------------------------------------------
     #pragma unroll 1
     for (int i = 0; i < P.n_islands; ++i) {
-        uint64_t m = 0;
+        DM m = dm_zero<DM>();
         #pragma unroll 1
         for (int base = 0; base < N; base += 32) {
             const int d = base + lane;
-            m |= static_cast<uint64_t>(__ballot_sync(kFull, d < N && B.dev_island[P.dev_begin + d] == i)) << base;
+            dm_or_bits32(m, base, __ballot_sync(kFull, d < N && B.dev_island[P.dev_begin + d] == i));
         }
         if (lane == 0) islm[i] = m;
     }
     #pragma unroll 1
     for (int g = lane; g < G; g += 32) {
-        chg[g] = 0;
-        gmask[g] = 0;
+        chg[g] = dm_zero<DM>();
+        gmask[g] = dm_zero<DM>();
         gbytes[g] = 0;
     }
     #pragma unroll 1
@@ -309,16 +348,17 @@ __global__ void __launch_bounds__(32 * kSimWarps, WS_SIM_MINB) k_sim(SimArgs A) 
         #pragma unroll 1
         for (int i = lane; i < ne; i += 32) {
             const int k = V.en[eb + i].metaop;
-            uint64_t m = 0;
+            DM m = dm_zero<DM>();
             int flags = 0;
             #pragma unroll 1
             for (int j = 0; j < ne; ++j) {
                 const ws_out_entry& x = V.en[eb + j];
                 if (x.metaop != k) continue;
-                if (x.devmask) m = x.devmask;
+                const DM xm = raw_mask(eb + j);
+                if (dm_any(xm)) m = xm;
                 if (j < i) flags |= 1;  // an earlier entry has this MetaOp
             }
-            *en_pl(eb + i) = m;
+            pl_set(eb + i, m);
             *en_flags(eb + i) = flags;
         }
     }
@@ -326,21 +366,26 @@ __global__ void __launch_bounds__(32 * kSimWarps, WS_SIM_MINB) k_sim(SimArgs A) 
     #pragma unroll 1
     for (int f = lane; f < nF; f += 32) {
         const ws_out_flow& x = V.fl[f];
-        uint64_t ma = 0, mb = 0;
+        int ia = -1, ib = -1;  // the last placed entry of each endpoint key
         if (x.from_wave >= 0 && x.from_wave < nW)
             #pragma unroll 1
             for (int j = 0; j < V.wv[x.from_wave].n_entries; ++j) {
                 const int e = V.wv[x.from_wave].entry_begin + j;
-                if (V.en[e].metaop == x.from_metaop && V.en[e].devmask) ma = V.en[e].devmask;
+                if (V.en[e].metaop == x.from_metaop && dm_any(raw_mask(e))) ia = e;
             }
         if (x.to_wave >= 0 && x.to_wave < nW)
             #pragma unroll 1
             for (int j = 0; j < V.wv[x.to_wave].n_entries; ++j) {
                 const int e = V.wv[x.to_wave].entry_begin + j;
-                if (V.en[e].metaop == x.to_metaop && V.en[e].devmask) mb = V.en[e].devmask;
+                if (V.en[e].metaop == x.to_metaop && dm_any(raw_mask(e))) ib = e;
             }
-        fl_masks(f)[0] = ma;
-        fl_masks(f)[1] = mb;
+        if constexpr (kW == 1) {
+            fl_masks(f)[0] = ia < 0 ? 0ull : V.en[ia].devmask;
+            fl_masks(f)[1] = ib < 0 ? 0ull : V.en[ib].devmask;
+        } else {
+            fl_masks(f)[0] = static_cast<uint64_t>(static_cast<long long>(ia));
+            fl_masks(f)[1] = static_cast<uint64_t>(static_cast<long long>(ib));
+        }
         double dur = 0.0;  // flow_duration (simulate.hpp:96-100)
         if (!A.opt.zero_volumes && x.volume != 0 && x.mode != WS_FLOW_COPY)
             dur = static_cast<double>(x.volume) / (x.mode == WS_FLOW_INTER ? P.inter_bw : P.intra_bw);
@@ -353,35 +398,37 @@ __global__ void __launch_bounds__(32 * kSimWarps, WS_SIM_MINB) k_sim(SimArgs A) 
 
     // ---- simulate (simulate.hpp:171-280) ---------------------------------
     const ws_sim_opts& opt = A.opt;
-    double av0 = 0.0, av1 = 0.0;  // availability clocks of devices lane, lane+32
-    double bc0 = 0.0, bc1 = 0.0;  // compute seconds (per_device_busy)
-    uint64_t touched = 0;         // devices present in per_device_busy
+    double av[DPL], bc[DPL];  // availability clocks / compute seconds (per_device_busy) of devices lane + 32 s
+    #pragma unroll
+    for (int s = 0; s < DPL; ++s) av[s] = 0.0, bc[s] = 0.0;
+    DM touched = dm_zero<DM>();  // devices present in per_device_busy
     double frontier = 0.0, fwd_bwd = 0.0, send_recv = 0.0, param_sync = 0.0;
     double transferred = 0.0, inter_bytes = 0.0;
     int timeline = 0;
-    auto busy_mask = [&](uint64_t m, double t0, double dur) {  // busy(d, t0, dur) for every d in m
-        const bool b0 = m >> lane & 1ull, b1 = m >> (lane + 32) & 1ull;
+    auto busy_mask = [&](const DM& m, double t0, double dur) {  // busy(d, t0, dur) for every d in m
         if (dur <= 0.0) {
-            if (b0) av0 = (av0 < t0) ? t0 : av0;
-            if (b1) av1 = (av1 < t0) ? t0 : av1;
+            #pragma unroll
+            for (int s = 0; s < DPL; ++s)
+                if (dm_test(m, lane + 32 * s)) av[s] = (av[s] < t0) ? t0 : av[s];
         } else {
-            if (b0) av0 = t0 + dur;
-            if (b1) av1 = t0 + dur;
-            timeline += popc64(m);
+            #pragma unroll
+            for (int s = 0; s < DPL; ++s)
+                if (dm_test(m, lane + 32 * s)) av[s] = t0 + dur;
+            timeline += dm_popc(m);
         }
     };
     auto attribute = [&](double& bucket) {
-        const double f = lane_max2(all, lane, av0, av1);
+        const double f = lane_max(all, lane, av);
         bucket += f - frontier;
         frontier = f;
     };
     auto run_flow = [&](int fi) {
         const ws_out_flow& f = V.fl[fi];
-        const uint64_t ma = fl_masks(fi)[0], mb = fl_masks(fi)[1];
-        if (!ma || !mb) return;
+        const DM ma = fl_end(fi, 0), mb = fl_end(fi, 1);
+        if (!dm_any(ma) || !dm_any(mb)) return;
         const double dur = reinterpret_cast<const double*>(fl_masks(fi))[2];
-        const uint64_t parties = ma | mb;
-        const double t0 = lane_max2(parties, lane, av0, av1);
+        const DM parties = ma | mb;
+        const double t0 = lane_max(parties, lane, av);
         busy_mask(parties, t0, dur);
         if (!opt.zero_volumes) {
             transferred += static_cast<double>(f.volume);
@@ -391,25 +438,26 @@ __global__ void __launch_bounds__(32 * kSimWarps, WS_SIM_MINB) k_sim(SimArgs A) 
     auto run_wave = [&](int w, bool backward) {
         const double scale = backward ? opt.backward_ratio : 1.0;
         const ws_out_wave& wv = V.wv[w];
-        uint64_t parts = 0;
+        DM parts = dm_zero<DM>();
         #pragma unroll 1
-        for (int i = lane; i < wv.n_entries; i += 32) parts |= *en_pl(wv.entry_begin + i);
-        parts = (static_cast<uint64_t>(__reduce_or_sync(kFull, static_cast<unsigned>(parts >> 32))) << 32) |
-                __reduce_or_sync(kFull, static_cast<unsigned>(parts));
-        const double t0 = lane_max2(parts, lane, av0, av1);
+        for (int i = lane; i < wv.n_entries; i += 32) parts |= en_pl(wv.entry_begin + i);
+        parts = dm_or_reduce(parts);
+        const double t0 = lane_max(parts, lane, av);
         #pragma unroll 1
         for (int i = 0; i < wv.n_entries; ++i) {
-            const uint64_t m = *en_pl(wv.entry_begin + i);
-            if (!m) continue;
+            const DM m = en_pl(wv.entry_begin + i);
+            if (!dm_any(m)) continue;
             const double dur = V.en[wv.entry_begin + i].span * scale;
             busy_mask(m, t0, dur);
-            if (m >> lane & 1ull) bc0 += dur;
-            if (m >> (lane + 32) & 1ull) bc1 += dur;
+            #pragma unroll
+            for (int s = 0; s < DPL; ++s)
+                if (dm_test(m, lane + 32 * s)) bc[s] += dur;
             touched |= m;
         }
         const double rel = t0 + wv.duration * scale;  // the wave releases its devices together
-        if (parts >> lane & 1ull) av0 = (av0 < rel) ? rel : av0;
-        if (parts >> (lane + 32) & 1ull) av1 = (av1 < rel) ? rel : av1;
+        #pragma unroll
+        for (int s = 0; s < DPL; ++s)
+            if (dm_test(parts, lane + 32 * s)) av[s] = (av[s] < rel) ? rel : av[s];
     };
     auto flows_where = [&](bool into, int w) {  // flows_into / flows_out_of, in flow order
         #pragma unroll 1
@@ -445,11 +493,12 @@ __global__ void __launch_bounds__(32 * kSimWarps, WS_SIM_MINB) k_sim(SimArgs A) 
         for (int base = 0; base < nE; base += 32) {  // groups: device union and max gradient bytes
             const int e = base + lane;
             int g = -1;
-            uint64_t m = 0, gb = 0;
+            DM m = dm_zero<DM>();
+            uint64_t gb = 0;
             if (e < nE) {
                 const int k = V.en[e].metaop;
-                m = *en_pl(e);
-                if (m && k >= 0 && k < K) {
+                m = en_pl(e);
+                if (dm_any(m) && k >= 0 && k < K) {
                     const int gm = mbase + V.mo[k].module;
                     const uint64_t pb = static_cast<uint64_t>(static_cast<double>(B.mod_param[gm]) *
                                                               V.mo[k].length / B.mod_layers[gm]);
@@ -458,7 +507,7 @@ __global__ void __launch_bounds__(32 * kSimWarps, WS_SIM_MINB) k_sim(SimArgs A) 
                 }
             }
             if (g >= 0) {
-                atomicOr(reinterpret_cast<unsigned long long*>(gmask + g), m);
+                dm_atomic_or(gmask + g, m);
                 atomicMax(reinterpret_cast<unsigned long long*>(gbytes + g), gb);
             }
         }
@@ -468,7 +517,7 @@ __global__ void __launch_bounds__(32 * kSimWarps, WS_SIM_MINB) k_sim(SimArgs A) 
         #pragma unroll 1
         for (int base = 0; base < G; base += 32) {
             const int g = base + lane;
-            bool rep = g < G && gmask[g] != 0;
+            bool rep = g < G && dm_any(gmask[g]);
             uint64_t sum = 0;
             if (rep) {
                 #pragma unroll 1
@@ -501,14 +550,14 @@ __global__ void __launch_bounds__(32 * kSimWarps, WS_SIM_MINB) k_sim(SimArgs A) 
         #pragma unroll 1
         for (int r = 0; r < npool; ++r) {
             const int g = pord[r];
-            const uint64_t m = gmask[g];
+            const DM m = gmask[g];
             double dur = 0.0;
-            if (popc64(m) >= 2) {
+            if (dm_popc(m) >= 2) {
                 int widest = 0, islands = 0;
                 #pragma unroll 1
                 for (int base = 0; base < P.n_islands; base += 32) {
                     const int i = base + lane;
-                    const int c = i < P.n_islands ? popc64(m & islm[i]) : 0;
+                    const int c = i < P.n_islands ? dm_popc(m & islm[i]) : 0;
                     widest = max(widest, static_cast<int>(__reduce_max_sync(kFull, static_cast<unsigned>(c))));
                     islands += __popc(__ballot_sync(kFull, c > 0));
                 }
@@ -520,15 +569,17 @@ __global__ void __launch_bounds__(32 * kSimWarps, WS_SIM_MINB) k_sim(SimArgs A) 
                            P.inter_bw;
             }
             if (dur <= 0.0) continue;
-            const double t0 = lane_max2(m, lane, av0, av1);
+            const double t0 = lane_max(m, lane, av);
             busy_mask(m, t0, dur);
         }
         attribute(param_sync);
     }
-    const double makespan = lane_max2(all, lane, av0, av1);
+    const double makespan = lane_max(all, lane, av);
 
     // ---- compute_device_memory (validate.hpp:27-50) -----------------------
-    double mem0 = 0.0, mem1 = 0.0;
+    double mem[DPL];
+    #pragma unroll
+    for (int s = 0; s < DPL; ++s) mem[s] = 0.0;
     #pragma unroll 1
     for (int w = 0; w < nW; ++w) {
         const ws_out_wave& wv = V.wv[w];
@@ -536,23 +587,21 @@ __global__ void __launch_bounds__(32 * kSimWarps, WS_SIM_MINB) k_sim(SimArgs A) 
         for (int i = 0; i < wv.n_entries; ++i) {
             const int e = wv.entry_begin + i;
             const int k = V.en[e].metaop;
-            const uint64_t m = *en_pl(e);
-            if (!m || k < 0 || k >= K) continue;
+            const DM m = en_pl(e);
+            if (!dm_any(m) || k < 0 || k >= K) continue;
             const int gm = mbase + V.mo[k].module;
             const uint64_t pb = static_cast<uint64_t>(static_cast<double>(B.mod_param[gm]) * V.mo[k].length /
                                                       B.mod_layers[gm]);
-            const uint64_t charged = chg[gk[k]];
+            const DM charged = chg[gk[k]];
             const double pstate = (1.0 + P.grad_mult) * static_cast<double>(pb) / B.mod_tp[gm];
             const double frac = efrac[k];  // PlanEntity::batch_fraction
             const double act = V.en[e].layers * (static_cast<double>(B.mod_act[gm]) * frac / V.en[e].n);
-            if (m >> lane & 1ull) {
-                if (!(charged >> lane & 1ull)) mem0 += pstate;
-                mem0 += act;
-            }
-            if (m >> (lane + 32) & 1ull) {
-                if (!(charged >> (lane + 32) & 1ull)) mem1 += pstate;
-                mem1 += act;
-            }
+            #pragma unroll
+            for (int s = 0; s < DPL; ++s)
+                if (dm_test(m, lane + 32 * s)) {
+                    if (!dm_test(charged, lane + 32 * s)) mem[s] += pstate;
+                    mem[s] += act;
+                }
             __syncwarp();
             if (lane == 0) chg[gk[k]] = charged | m;
             __syncwarp();
@@ -783,33 +832,32 @@ __global__ void __launch_bounds__(32 * kSimWarps, WS_SIM_MINB) k_sim(SimArgs A) 
     }
     bool any_placed = false;
     #pragma unroll 1
-    for (int i = lane; i < nE; i += 32) any_placed |= V.en[i].devmask != 0;
+    for (int i = lane; i < nE; i += 32) any_placed |= dm_any(raw_mask(i));
     if (__any_sync(kFull, any_placed)) {
         #pragma unroll 1
         for (int w = 0; w < nW; ++w) {  // per wave: placed, sized, disjoint (device-list order)
             const ws_out_wave& wv = V.wv[w];
             bool bad = false;
-            uint64_t uni = 0;
+            DM uni = dm_zero<DM>();
             int sum = 0;
             #pragma unroll 1
             for (int i = lane; i < wv.n_entries; i += 32) {
                 const int e = wv.entry_begin + i;
-                const uint64_t m = *en_pl(e);
-                bad |= !m || popc64(m) != V.en[e].n || (m & ~all) != 0;
+                const DM m = en_pl(e);
+                bad |= !dm_any(m) || dm_popc(m) != V.en[e].n || dm_any(m & ~all);
                 uni |= m;
-                sum += popc64(m);
+                sum += dm_popc(m);
             }
-            uni = (static_cast<uint64_t>(__reduce_or_sync(kFull, static_cast<unsigned>(uni >> 32))) << 32) |
-                  __reduce_or_sync(kFull, static_cast<unsigned>(uni));
+            uni = dm_or_reduce(uni);
             sum = static_cast<int>(__reduce_add_sync(kFull, static_cast<unsigned>(sum)));
-            if (!__any_sync(kFull, bad) && sum == popc64(uni)) continue;
+            if (!__any_sync(kFull, bad) && sum == dm_popc(uni)) continue;
             if (lane == 0) {
-                uint64_t taken = 0;
+                DM taken = dm_zero<DM>();
                 #pragma unroll 1
                 for (int i = 0; i < wv.n_entries; ++i) {
                     const int e = wv.entry_begin + i;
-                    const uint64_t m = *en_pl(e);
-                    if (!m) {
+                    const DM m = en_pl(e);
+                    if (!dm_any(m)) {
                         fail(WS_V_UNPLACED, w, V.en[e].metaop, 0, 0, 0);
                         continue;
                     }
@@ -817,29 +865,30 @@ __global__ void __launch_bounds__(32 * kSimWarps, WS_SIM_MINB) k_sim(SimArgs A) 
                     #pragma unroll 1
                     for (int j = 0; j < wv.n_entries; ++j) {
                         const ws_out_entry& x = V.en[wv.entry_begin + j];
-                        if (x.metaop == V.en[e].metaop && x.devmask) rot = x.rot;
+                        if (x.metaop == V.en[e].metaop && dm_any(raw_mask(wv.entry_begin + j))) rot = x.rot;
                     }
-                    if (popc64(m) != V.en[e].n) fail(WS_V_DEVICE_COUNT, w, V.en[e].metaop, popc64(m), V.en[e].n, 0);
-                    const uint64_t below = rot >= 64 ? ~0ull : ((1ull << rot) - 1ull);
-                    const uint64_t order[2] = {m & ~below, m & below};
+                    if (dm_popc(m) != V.en[e].n) fail(WS_V_DEVICE_COUNT, w, V.en[e].metaop, dm_popc(m), V.en[e].n, 0);
+                    const DM below = dm_first<DM>(rot);
+                    const DM order[2] = {m & ~below, m & below};
                     for (int h = 0; h < 2; ++h)
                         #pragma unroll 1
-                        for (uint64_t b = order[h]; b; b &= b - 1) {
-                            const int d = low_bit(b);
+                        for (DM b = order[h]; dm_any(b); b = dm_drop_low(b)) {
+                            const int d = dm_low(b);
                             if (d >= N)
                                 fail(WS_V_UNKNOWN_DEVICE, -1, d, 0, 0, 0);
-                            else if (taken >> d & 1ull)
+                            else if (dm_test(taken, d))
                                 fail(WS_V_DEVICE_TWICE, w, d, 0, 0, 0);
                             else
-                                taken |= 1ull << d;
+                                taken |= dm_bit<DM>(d);
                         }
                 }
             }
             __syncwarp();
         }
         const double cap = static_cast<double>(P.mem_capacity) * (1.0 + 1e-9);
-        for (int h = 0; h < 2; ++h) {  // memory capacity, devices in id order
-            const double mv = h ? mem1 : mem0;
+        #pragma unroll
+        for (int h = 0; h < DPL; ++h) {  // memory capacity, devices in id order
+            const double mv = mem[h];
             const int d = lane + 32 * h;
             const unsigned b = __ballot_sync(kFull, d < N && mv > cap);
             #pragma unroll 1
@@ -856,7 +905,10 @@ __global__ void __launch_bounds__(32 * kSimWarps, WS_SIM_MINB) k_sim(SimArgs A) 
     // ---- write the record ---------------------------------------------------
     nv = __shfl_sync(kFull, nv, 0);
     const int keep = nv < WS_SIM_MAX_VIOLATIONS ? nv : WS_SIM_MAX_VIOLATIONS;
-    const uint64_t sz = 16ull * N + 16 + 8ull * K + sizeof(ws_out_violation) * keep;
+    // busy[N], touched (1 word; 4 for clusters over 64 devices), mem[N], util[K],
+    // util_mask, violations: the layout goes by the plan's N (ws_abi.h), not the instance
+    const int TW = wide_rec ? kW : 1;
+    const uint64_t sz = 16ull * N + 8ull * TW + 8 + 8ull * K + sizeof(ws_out_violation) * keep;
     unsigned long long off = 0;
     if (lane == 0) off = atomicAdd(A.arena_top, static_cast<unsigned long long>(sz));
     off = __shfl_sync(kFull, off, 0);
@@ -870,21 +922,24 @@ __global__ void __launch_bounds__(32 * kSimWarps, WS_SIM_MINB) k_sim(SimArgs A) 
     }
     uint8_t* base = A.arena + off;
     double* o_busy = reinterpret_cast<double*>(base);
-    double* o_mem = reinterpret_cast<double*>(base + 8ull * N + 8);
-    double* o_util = reinterpret_cast<double*>(base + 16ull * N + 8);
-    if (lane < N) o_busy[lane] = bc0, o_mem[lane] = mem0;
-    if (lane + 32 < N) o_busy[lane + 32] = bc1, o_mem[lane + 32] = mem1;
+    double* o_mem = reinterpret_cast<double*>(base + 8ull * N + 8ull * TW);
+    double* o_util = reinterpret_cast<double*>(base + 16ull * N + 8ull * TW);
+    #pragma unroll
+    for (int s = 0; s < DPL; ++s)
+        if (lane + 32 * s < N) o_busy[lane + 32 * s] = bc[s], o_mem[lane + 32 * s] = mem[s];
     for (int s = 0; s < 2; ++s) {
         const int k = lane + 32 * s;
         if (k < K)
             o_util[k] = (ds[s] > 0.0 && peak_rate > 0.0) ? (ls[s] / ds[s]) / peak_rate : 0.0;
     }
-    ws_out_violation* o_v = reinterpret_cast<ws_out_violation*>(base + 16ull * N + 16 + 8ull * K);
+    ws_out_violation* o_v = reinterpret_cast<ws_out_violation*>(base + 16ull * N + 8ull * TW + 8 + 8ull * K);
     #pragma unroll 1
     for (int i = lane; i < keep; i += 32) o_v[i] = vio[i];
     if (lane == 0) {
-        *reinterpret_cast<uint64_t*>(base + 8ull * N) = touched;
-        *reinterpret_cast<uint64_t*>(base + 16ull * N + 8 + 8ull * K) = util_mask;
+        #pragma unroll
+        for (int j = 0; j < kW; ++j)
+            if (j < TW) reinterpret_cast<uint64_t*>(base + 8ull * N)[j] = dm_word(touched, j);
+        *reinterpret_cast<uint64_t*>(base + 16ull * N + 8ull * TW + 8ull * K) = util_mask;
         ws_sim_result r{};
         r.status = WS_STATUS_OK;
         r.valid = nv == 0;

@@ -14,6 +14,10 @@ static inline uint64_t wsi_plan_arena_bound(const ws_plan_rec* r) {
 }
 
 /* evaluation record: busy/mem per device, utilization per entity, violations */
+// words of the busy_mask field of a simulation record (ws_abi.h ws_sim_result)
+static inline uint64_t sim_mask_words(uint64_t n_dev) { return n_dev > 64 ? 4 : 1; }
+
 static inline uint64_t wsi_plan_sim_bound(const ws_plan_rec* r) {
-    return 16ull * r->n_dev + 8ull * r->n_mod + 16 + sizeof(ws_out_violation) * WS_SIM_MAX_VIOLATIONS;
+    // a batch with a wider cluster evaluates every plan with 4-word masks
+    return 16ull * r->n_dev + 8ull * r->n_mod + 8 * 4 + 8 + sizeof(ws_out_violation) * WS_SIM_MAX_VIOLATIONS;
 }

@@ -24,6 +24,7 @@ struct Sections {
     const ws_out_entry* en;
     const ws_out_flow* fl;
     const ws_out_scope* sc;
+    const std::uint64_t* ext;  // device words 1..3 per entry (clusters of more than 64 devices)
 };
 
 Sections sections_of(const ws_plan_result& r, const std::uint8_t* arena) {
@@ -45,6 +46,8 @@ Sections sections_of(const ws_plan_result& r, const std::uint8_t* arena) {
     s.fl = reinterpret_cast<const ws_out_flow*>(base + off);
     off += al8(sizeof(ws_out_flow) * r.n_flows);
     s.sc = reinterpret_cast<const ws_out_scope*>(base + off);
+    off += al8(sizeof(ws_out_scope) * r.n_scopes);
+    s.ext = reinterpret_cast<const std::uint64_t*>(base + off);
     return s;
 }
 
@@ -82,17 +85,6 @@ std::string module_kind(const WorkloadSpec& spec, std::int64_t index) {
 // plan.devices list of an entry: ascending device index starting at `rot`
 // with wrap-around (the sequential ablation's rolling cursor order,
 // placement.hpp:351-357; rot = 0 for the locality placer's sorted sets)
-std::vector<int> device_list(const Problem& prob, const ws_out_entry& e) {
-    const auto& devs = prob.topo->devices;
-    const int N = static_cast<int>(devs.size());
-    std::vector<int> out;
-    for (int i = 0; i < N; ++i) {
-        const int d = (e.rot + i) % N;
-        if (e.devmask >> d & 1ull) out.push_back(devs[d]);
-    }
-    return out;
-}
-
 }  // namespace
 
 [[noreturn]] void throw_result_error(const Problem& prob, const ws_plan_result& r) {
@@ -198,9 +190,15 @@ PlannerResult decode_scoped(const Problem& prob, const ws_plan_result& r, const 
         wave.start = s.wv[w].start;
         wave.duration = s.wv[w].duration;
         for (int i = 0; i < s.wv[w].n_entries; ++i) {
-            const ws_out_entry& e = s.en[s.wv[w].entry_begin + i];
+            const int ei = s.wv[w].entry_begin + i;
+            const ws_out_entry& e = s.en[ei];
+            const std::uint64_t* ext = prob.topo->devices.size() > 64 ? s.ext + 3 * ei : nullptr;
             wave.entries.push_back({ids[e.metaop], e.n, e.layers, e.span});
-            if (e.devmask) plan.devices[{w, ids[e.metaop]}] = device_list(prob, e);
+            if (detail::entry_placed(e, ext)) {
+                std::vector<int> devs;
+                detail::entry_devices(prob.topo->devices, e, ext, devs);
+                plan.devices[{w, ids[e.metaop]}] = std::move(devs);
+            }
         }
         plan.schedule.waves.push_back(std::move(wave));
     }

@@ -103,7 +103,7 @@ struct PlanDocs {
             const ClusterTopology& topo = plan.topo;
             const int K = static_cast<int>(plan.entities.size());
             const int N = static_cast<int>(topo.devices.size());
-            if (N > WS_MAX_DEVICES) throw LimitExceeded("plan: more than 64 devices");
+            if (N > WS_MAX_DEVICES) throw LimitExceeded("plan: more than 256 devices");
             // index of the r-th id (std::map order) = the index whose "m<index>" has rank r
             std::vector<int> perm(K);
             std::iota(perm.begin(), perm.end(), 0);
@@ -184,6 +184,7 @@ struct PlanDocs {
             for (const auto& [a, b] : plan.deps) ed.push_back({idx(a), idx(b)});
             std::vector<ws_out_wave> wv;
             std::vector<ws_out_entry> en;
+            std::vector<std::uint64_t> ext;  // device words 1..3 per entry (N > 64, ws_abi.h)
             for (std::size_t w = 0; w < plan.schedule.waves.size(); ++w) {
                 const Wave& wave = plan.schedule.waves[w];
                 if (wave.index != static_cast<int>(w))
@@ -197,6 +198,7 @@ struct PlanDocs {
                 wv.push_back(x);
                 for (const WaveEntry& e : wave.entries) {
                     ws_out_entry y{};
+                    std::uint64_t w[4] = {0, 0, 0, 0};
                     y.span = e.span;
                     y.metaop = idx(e.metaop_id);
                     y.n = e.n;
@@ -208,13 +210,16 @@ struct PlanDocs {
                             if (di == dev_index.end())
                                 throw ParseError("plan: device " + std::to_string(it->second[i]) +
                                                  " not in the topology (unsupported)");
-                            if (y.devmask >> di->second & 1ull)
+                            const int d = di->second;
+                            if (w[d / 64] >> (d % 64) & 1ull)
                                 throw ParseError("plan: device listed twice in one entry (unsupported)");
-                            y.devmask |= 1ull << di->second;
-                            if (i == 0) y.rot = di->second;  // lists are ascending from their first device
+                            w[d / 64] |= 1ull << (d % 64);
+                            if (i == 0) y.rot = d;  // lists are ascending from their first device
                         }
                     }
+                    y.devmask = w[0];
                     en.push_back(y);
+                    if (N > 64) ext.insert(ext.end(), w + 1, w + 4);
                 }
             }
             std::vector<ws_out_flow> fl;
@@ -254,6 +259,7 @@ struct PlanDocs {
             put(wv.data(), sizeof(ws_out_wave) * wv.size());
             put(en.data(), sizeof(ws_out_entry) * en.size());
             put(fl.data(), sizeof(ws_out_flow) * fl.size());
+            put(ext.data(), sizeof(std::uint64_t) * ext.size());
             res.size = arena.size() - res.offset;
             im += K;
             id += N;

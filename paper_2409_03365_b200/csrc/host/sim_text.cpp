@@ -92,7 +92,8 @@ std::vector<std::string> violation_messages(const ClusterTopology& topo, const w
                                             const std::vector<std::string>& names) {
     std::vector<std::string> out;
     if (s.status != WS_STATUS_OK) return out;
-    const std::size_t o_viol = 16ull * topo.devices.size() + 16 + 8ull * r.n_metaops;
+    const std::size_t N = topo.devices.size();
+    const std::size_t o_viol = 16ull * N + 8ull * sim_mask_words(N) + 8 + 8ull * r.n_metaops;
     const int nv = std::min(s.n_violations, WS_SIM_MAX_VIOLATIONS);
     for (int i = 0; i < nv; ++i) {
         ws_out_violation v;
@@ -131,12 +132,14 @@ std::string sim_text_named(const ClusterTopology& topo, const ws_plan_result& r,
                       " transferred=" + fmt_exact(s.total_transferred_bytes) +
                       " inter=" + fmt_exact(s.total_inter_island_bytes) +
                       " timeline=" + std::to_string(s.timeline_items) + "\n";
-    const std::size_t o_busy = 0, o_bmask = 8ull * N, o_mem = 8ull * N + 8, o_util = 16ull * N + 8,
-                      o_umask = 16ull * N + 8 + 8ull * K;
-    const std::uint64_t bmask = u64(o_bmask), umask = u64(o_umask);
+    const std::size_t TW = sim_mask_words(N);  // busy_mask words
+    const std::size_t o_busy = 0, o_bmask = 8ull * N, o_mem = 8ull * N + 8 * TW, o_util = 16ull * N + 8 * TW,
+                      o_umask = 16ull * N + 8 * TW + 8ull * K;
+    const std::uint64_t umask = u64(o_umask);
     out += "busy";
     for (int d = 0; d < N; ++d)
-        if (bmask >> d & 1ull) out += " " + std::to_string(topo.devices[d]) + "=" + fmt_exact(f64(o_busy + 8ull * d));
+        if (u64(o_bmask + 8ull * (d / 64)) >> (d % 64) & 1ull)
+            out += " " + std::to_string(topo.devices[d]) + "=" + fmt_exact(f64(o_busy + 8ull * d));
     out += "\nmem";
     for (int d = 0; d < N; ++d) out += " " + std::to_string(topo.devices[d]) + "=" + fmt_exact(f64(o_mem + 8ull * d));
     out += "\nutil";

@@ -3,12 +3,15 @@
 container only).  The CPU oracle restatement keeps device sets in one u64
 (<= 64 devices), so these cases pin the device planner to the reference
 directly.  Writes wide_cases.json.gz: inputs + the reference outcome (plan
-text or "error <Class>: <what>") for
+text or "error <Class>: <what>") and the reference's evaluation of that plan
+(simulate_plan + validate_plan text, default simulation options; the same
+text as the reference's evaluation of the plan read back as a plan file) for
 
   * the paper's QWen-VAL on 256 GPUs and the other
     BASELINE families at 96, 128, 192 and 256 devices, several seeds;
   * option variants: sequential placement, no backtracking, drop floor,
-    the decoupled-sequential baseline (plan_for_strategy);
+    the three baselines (plan_for_strategy: decoupled-sequential, distmm-mt,
+    task-level-optimus);
   * tight memory (PlacementInfeasible / backtracking) and a hand-made
     topology with non-contiguous islands.
 
@@ -34,8 +37,12 @@ def main() -> None:
     def add(name, w, t, opts, strategy=None):
         expected = (po.ref_strategy_plan_text(w, t, strategy, **opts) if strategy
                     else po.ref_plan_text(w, t, **opts))
-        cases.append({"name": name, "workload": w, "topology": t, "options": opts, "strategy": strategy,
-                      "expected": expected})
+        so = dict(opts, strategy=strategy) if strategy else opts
+        case = {"name": name, "workload": w, "topology": t, "options": opts, "strategy": strategy,
+                "expected": expected, "sim_expected": po.ref_sim_text(w, t, {}, **so)}
+        if not expected.startswith("error"):  # the plan read back as a plan file evaluates the same
+            assert po.ref_sim_plan_text(expected) == case["sim_expected"], name
+        cases.append(case)
 
     for fam, tasks in (("qwen-val-like", 3), ("clip-like", 4), ("clip-like", 10), ("clip-like", 16),
                        ("ofasys-like", 7), ("ofasys-like", 12)):
@@ -48,6 +55,8 @@ def main() -> None:
                     add(f"wide-bt0/{fam}/{tasks}t/{devices}d", w, t, {"bt_depth": 0})
                     add(f"wide-drop/{fam}/{tasks}t/{devices}d", w, t, {"drop_floor": 0.05})
                     add(f"wide-decoupled/{fam}/{tasks}t/{devices}d", w, t, {}, "decoupled-sequential")
+                    add(f"wide-distmm/{fam}/{tasks}t/{devices}d", w, t, {}, "distmm-mt")
+                    add(f"wide-optimus/{fam}/{tasks}t/{devices}d", w, t, {}, "task-level-optimus")
     # tight memory: placement backtracking and PlacementInfeasible on wide clusters
     for fam, tasks in (("clip-like", 10), ("ofasys-like", 7)):
         w, t = po.ref_scenario(fam, tasks, 256, 0)
