@@ -1,5 +1,5 @@
 # e2e of ws_plan_batch_host (100k sweep) for several chunk weightings (WSGPU_HOST_WEIGHTS)
-for w in 1,3,3,1 1,4,4,2,1 1,2,2,1 1,3,1 1,5,5,1 1,3,3,3,1 2,3,3,2; do
+for w in ${WEIGHTS:-1,3,3,1 1,4,4,2,1 1,2,2,1 1,3,1 1,5,5,1 1,3,3,3,1 2,3,3,2}; do
 WSGPU_HOST_WEIGHTS=$w python -c "
 import sys,time; sys.path.insert(0,'.')
 import torch, paper_2409_03365_b200 as ws
