@@ -293,14 +293,17 @@ struct ws_ctx {
     // chunk's k_sched + k_place launch tail outweighs the hidden copies); two compute
     // streams (consecutive chunks fill each other's tails) with completion-order D2H:
     // weights 1,3,1 24.9, 1,3,3,1 22.8, 1,4,4,1 22.8, 1,3,3,3,1 22.8, 1,5,5,1 23.8
-    int host_chunks = 5;                     // $WSGPU_HOST_CHUNKS
+    int host_chunks = 4;                     // $WSGPU_HOST_CHUNKS
     int host_streams = 2;                    // $WSGPU_HOST_STREAMS (1 to 3)
     bool force_snap = false;                 // $WSGPU_FORCE_SNAP: k_place<true> for every batch (tuning)
     // k_sched launched programmatic-dependent on k_fit: its graph stage overlaps
     // k_fit (measured: single-plan latency -7..-10%, 100k throughput unchanged);
     // k_fit's time is then reported inside k_sched's.  $WSGPU_PDL=0 disables.
     bool pdl = true;
-    std::vector<double> host_weights{1, 4, 4, 2, 1};  // $WSGPU_HOST_WEIGHTS (sets the chunk count); measured r2: 1,3,3,1 16.3 ms, 1,4,4,2,1 15.3 ms per 100k
+    // $WSGPU_HOST_WEIGHTS (sets the chunk count).  Measured per 100k (profiles/
+    // r2h_host_weights.txt): 1,4,4,2,1 14.4 ms, 2,3,3,2 13.9 ms -- with the heavy
+    // backtracking tail gone (k_place attempt memo) a larger first chunk pays
+    std::vector<double> host_weights{2, 3, 3, 2};
     ws_plan_result* res_out() { return d_results ? d_results : results.as<ws_plan_result>(); }
     // small host batches stage their zeroed counters with the batch (one H2D copy)
     unsigned long long* small_counters = nullptr;
