@@ -1073,6 +1073,57 @@ int host_range(ws_ctx* ctx, const ws_batch* in, int P0, int P1, ws_plan_result* 
         pb[c + 1] = c + 1 == C ? P1
                                : P0 + std::max(pb[c] - P0 + 1, std::min(n - (C - 1 - c), static_cast<int>(n * (wacc / wsum))));
     }
+    // Chunk 0's input rows go out first: the DMA runs while the host makes its
+    // pass over the plan records below (which only the launch order and the
+    // arena bounds depend on)
+    auto* tops = ctx->chunk_tops.as<unsigned long long>();
+    cudaStream_t sh = ctx->stream2, sd = ctx->stream3;
+    cudaEvent_t* h2d = ctx->cev;               // [0, C)
+    cudaEvent_t* done = ctx->cev + kMaxHostChunks;  // [C, 2C)
+    CK(cudaEventRecord(ctx->ev[0], st));
+    CK(cudaStreamWaitEvent(sh, ctx->ev[0], 0));
+    const ws_batch& h = *in;
+    auto rows = [&](const void* hp, size_t esz, int64_t lo, int64_t hi) -> cudaError_t {
+        if (!hp || hi <= lo) return cudaSuccess;
+        const size_t off = static_cast<const char*>(hp) - static_cast<const char*>(in->blob) + lo * esz;
+        return cudaMemcpyAsync(dblob + off, static_cast<const char*>(hp) + lo * esz, (hi - lo) * esz,
+                               cudaMemcpyHostToDevice, sh);
+    };
+    auto first = [](const int32_t* a, int64_t i, int64_t n, int64_t total) { return i < n ? a[i] : total; };
+#define RK(x)                              \
+    do {                                   \
+        const cudaError_t e_ = (x);        \
+        if (e_ != cudaSuccess) return e_;  \
+    } while (0)
+    auto issue_rows = [&](int c) -> cudaError_t {  // chunk c's input rows (H2D side)
+        const int p0 = pb[c], p1 = pb[c + 1];
+        const int64_t m0 = h.plans[p0].mod_begin, m1 = p1 < P ? h.plans[p1].mod_begin : h.n_modules;
+        const int64_t t0 = h.plans[p0].task_begin, t1 = p1 < P ? h.plans[p1].task_begin : h.n_task_total;
+        const int64_t d0 = h.plans[p0].dev_begin, d1 = p1 < P ? h.plans[p1].dev_begin : h.n_devices;
+        const int64_t nm = h.n_modules, nt = h.n_task_total;
+        RK(rows(h.plans, sizeof(ws_plan_rec), p0, p1));
+        for (const int32_t* a : {h.mod_plan, h.mod_layers, h.mod_tp, h.mod_group, h.mod_alias, h.mod_name_off,
+                                 h.mod_name_len, h.mod_truth_off, h.mod_truth_n, h.mod_prof_off, h.mod_prof_n,
+                                 h.mod_bp_off, h.mod_bp_n, h.mod_pre_err})
+            RK(rows(a, 4, m0, m1));
+        for (const void* a : {static_cast<const void*>(h.mod_batch), static_cast<const void*>(h.mod_param),
+                              static_cast<const void*>(h.mod_act), static_cast<const void*>(h.mod_out),
+                              static_cast<const void*>(h.mod_w), static_cast<const void*>(h.mod_c)})
+            RK(rows(a, 8, m0, m1));
+        for (const int32_t* a : {h.task_tok_off, h.task_tok_n, h.task_rank}) RK(rows(a, 4, t0, t1));
+        RK(rows(h.tokens, 4, first(h.task_tok_off, t0, nt, h.n_tokens), first(h.task_tok_off, t1, nt, h.n_tokens)));
+        RK(rows(h.dev_island, 4, d0, d1));
+        RK(rows(h.truth, 40, first(h.mod_truth_off, m0, nm, h.n_pieces), first(h.mod_truth_off, m1, nm, h.n_pieces)));
+        const int64_t q0 = first(h.mod_prof_off, m0, nm, h.n_points), q1 = first(h.mod_prof_off, m1, nm, h.n_points);
+        RK(rows(h.prof_n, 4, q0, q1));
+        RK(rows(h.prof_t, 8, q0, q1));
+        RK(rows(h.bps, 4, first(h.mod_bp_off, m0, nm, h.n_bps), first(h.mod_bp_off, m1, nm, h.n_bps)));
+        RK(rows(h.names, 1, first(h.mod_name_off, m0, nm, h.n_name_bytes),
+                first(h.mod_name_off, m1, nm, h.n_name_bytes)));
+        return cudaSuccess;
+    };
+#undef RK
+    CK(issue_rows(0));
     // ONE pass over the plan records: launch maxima, per-chunk arena bounds, the
     // evaluation bound and per-chunk LPT key histograms; then one scatter pass
     // (the host work before the first copy is exposed in the end-to-end time)
@@ -1109,47 +1160,11 @@ int host_range(ws_ctx* ctx, const ws_batch* in, int P0, int P1, ws_plan_result* 
     FitOut fo;
     if (prepare_plan(ctx, fo, st)) return 1;
     auto* counters = ctx->counters_dev();
-    auto* tops = ctx->chunk_tops.as<unsigned long long>();
-    cudaStream_t sh = ctx->stream2, sd = ctx->stream3;
-    cudaEvent_t* h2d = ctx->cev;               // [0, C)
-    cudaEvent_t* done = ctx->cev + kMaxHostChunks;  // [C, 2C)
     t_prep = hclk::now();
-    CK(cudaEventRecord(ctx->ev[0], st));
-    CK(cudaStreamWaitEvent(sh, ctx->ev[0], 0));
     CK(cudaMemcpyAsync(tops, ctx->host_tops, 8ull * C, cudaMemcpyHostToDevice, sh));
-    const ws_batch& h = *in;
-    auto rows = [&](const void* hp, size_t esz, int64_t lo, int64_t hi) -> cudaError_t {
-        if (!hp || hi <= lo) return cudaSuccess;
-        const size_t off = static_cast<const char*>(hp) - static_cast<const char*>(in->blob) + lo * esz;
-        return cudaMemcpyAsync(dblob + off, static_cast<const char*>(hp) + lo * esz, (hi - lo) * esz,
-                               cudaMemcpyHostToDevice, sh);
-    };
-    auto first = [](const int32_t* a, int64_t i, int64_t n, int64_t total) { return i < n ? a[i] : total; };
-    for (int c = 0; c < C; ++c) {  // H2D side
+    for (int c = 0; c < C; ++c) {
         const int p0 = pb[c], p1 = pb[c + 1];
-        const int64_t m0 = h.plans[p0].mod_begin, m1 = p1 < P ? h.plans[p1].mod_begin : h.n_modules;
-        const int64_t t0 = h.plans[p0].task_begin, t1 = p1 < P ? h.plans[p1].task_begin : h.n_task_total;
-        const int64_t d0 = h.plans[p0].dev_begin, d1 = p1 < P ? h.plans[p1].dev_begin : h.n_devices;
-        const int64_t nm = h.n_modules, nt = h.n_task_total;
-        CK(rows(h.plans, sizeof(ws_plan_rec), p0, p1));
-        for (const int32_t* a : {h.mod_plan, h.mod_layers, h.mod_tp, h.mod_group, h.mod_alias, h.mod_name_off,
-                                 h.mod_name_len, h.mod_truth_off, h.mod_truth_n, h.mod_prof_off, h.mod_prof_n,
-                                 h.mod_bp_off, h.mod_bp_n, h.mod_pre_err})
-            CK(rows(a, 4, m0, m1));
-        for (const void* a : {static_cast<const void*>(h.mod_batch), static_cast<const void*>(h.mod_param),
-                              static_cast<const void*>(h.mod_act), static_cast<const void*>(h.mod_out),
-                              static_cast<const void*>(h.mod_w), static_cast<const void*>(h.mod_c)})
-            CK(rows(a, 8, m0, m1));
-        for (const int32_t* a : {h.task_tok_off, h.task_tok_n, h.task_rank}) CK(rows(a, 4, t0, t1));
-        CK(rows(h.tokens, 4, first(h.task_tok_off, t0, nt, h.n_tokens), first(h.task_tok_off, t1, nt, h.n_tokens)));
-        CK(rows(h.dev_island, 4, d0, d1));
-        CK(rows(h.truth, 40, first(h.mod_truth_off, m0, nm, h.n_pieces), first(h.mod_truth_off, m1, nm, h.n_pieces)));
-        const int64_t q0 = first(h.mod_prof_off, m0, nm, h.n_points), q1 = first(h.mod_prof_off, m1, nm, h.n_points);
-        CK(rows(h.prof_n, 4, q0, q1));
-        CK(rows(h.prof_t, 8, q0, q1));
-        CK(rows(h.bps, 4, first(h.mod_bp_off, m0, nm, h.n_bps), first(h.mod_bp_off, m1, nm, h.n_bps)));
-        CK(rows(h.names, 1, first(h.mod_name_off, m0, nm, h.n_name_bytes),
-                first(h.mod_name_off, m1, nm, h.n_name_bytes)));
+        if (c > 0) CK(issue_rows(c));
         CK(cudaMemcpyAsync(ctx->order.as<int32_t>() + p0, ctx->order_pinned + p0, 4ull * (p1 - p0),
                            cudaMemcpyHostToDevice, sh));
         CK(cudaEventRecord(h2d[c], sh));
