@@ -27,6 +27,12 @@ def golden_cases():
 
 
 @pytest.fixture(scope="session")
+def backtrack_cases():
+    with gzip.open(GOLDEN / "backtrack_cases.json.gz", "rt") as f:
+        return json.load(f)
+
+
+@pytest.fixture(scope="session")
 def sweep_hashes():
     with gzip.open(GOLDEN / "sweep_hashes.txt.gz", "rt") as f:
         return f.read().split()

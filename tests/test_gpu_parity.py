@@ -37,6 +37,18 @@ def test_gpu_matches_reference_golden_cases(planner, golden_cases):
     assert planner.launch_count >= 2
 
 
+def test_gpu_backtracking_options_match_reference(planner, backtrack_cases):
+    """The placement DFS under non-default (depth, branching), including the
+    attempt memo's skipped repeats and budget exhaustion at the reference's
+    wave, on the sweep's heaviest backtracking mixtures."""
+    ps, kept, _ = build_set(backtrack_cases)
+    ps.encode(pinned=True)
+    texts = planner.plan(ps).texts(ps)
+    bad = [c["name"] for c, t in zip(kept, texts) if t != c["expected"]]
+    assert not bad, bad[:10]
+    assert sum(1 for c in kept if "budget exhausted" in c["expected"]) >= 50
+
+
 def test_gpu_full_sweep_100k_matches_reference(planner, sweep_hashes):
     """BASELINE config 5 at full size: every mixture's plan text hashes to the
     reference planner's (217 PlacementInfeasible outcomes included)."""
