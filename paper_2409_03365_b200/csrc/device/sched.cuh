@@ -2018,6 +2018,28 @@ __device__ bool s_distmm(SCtx& C, char* rec, const RecLayout& RL, int& nW, int& 
 // Warp copy of a slot's shared working set to / from its global state slot
 // (16-byte words; SL.bytes is a multiple of 16) plus the control block and
 // the flags that live in registers between the phases.
+// Bytes of the working set that travel from phase 1 to phase 3: everything
+// before the wave-scheduling scratch (tk .. ord, written by phase 3 before it
+// is read) and the task-scoped arrays (the scoped baselines run unsplit).
+__host__ __device__ inline int sched_state_bytes(const SmLayout& L) { return (L.tk + 15) & ~15; }
+
+// The state slot's header: the warp's Ctl, the plan's ok flag and MetaOp count.
+__device__ __forceinline__ void sched_state_hdr(bool save, char* g, Ctl* ctl, int& ok, int& K, int lane) {
+    int* flags = reinterpret_cast<int*>(g + sizeof(Ctl));
+    if (save) {
+        if (lane == 0) {
+            *reinterpret_cast<Ctl*>(g) = *ctl;
+            flags[0] = ok;
+            flags[1] = K;
+        }
+    } else {
+        if (lane == 0) *ctl = *reinterpret_cast<const Ctl*>(g);
+        ok = flags[0];
+        K = flags[1];
+    }
+    __syncwarp();
+}
+
 __device__ __forceinline__ void sched_state_io(bool save, char* g, char* sm, int bytes, Ctl* ctl, int& ok, int& K,
                                                int lane) {
     int4* gs = reinterpret_cast<int4*>(g + kSchedStateHdr);
@@ -2035,18 +2057,28 @@ __device__ __forceinline__ void sched_state_io(bool save, char* g, char* sm, int
         }
         asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
     }
-    int* flags = reinterpret_cast<int*>(g + sizeof(Ctl));
+    sched_state_hdr(save, g, ctl, ok, K, lane);
+}
+
+// Bytes [lo, hi) of the working set (8-byte aligned layout offsets) to / from
+// the plan's state slot; restores are cp.async, waited for by sched_span_wait.
+__device__ __forceinline__ void sched_span_io(bool save, char* g, char* sm, int lo, int hi, int lane) {
+    uint64_t* gs = reinterpret_cast<uint64_t*>(g + kSchedStateHdr + lo);
+    uint64_t* ss = reinterpret_cast<uint64_t*>(sm + lo);
+    const int n = (hi - lo) / 8;
     if (save) {
-        if (lane == 0) {
-            *reinterpret_cast<Ctl*>(g) = *ctl;
-            flags[0] = ok;
-            flags[1] = K;
-        }
+        #pragma unroll 1
+        for (int i = lane; i < n; i += 32) gs[i] = ss[i];
     } else {
-        if (lane == 0) *ctl = *reinterpret_cast<const Ctl*>(g);
-        ok = flags[0];
-        K = flags[1];
+        #pragma unroll 1
+        for (int i = lane; i < n; i += 32) {
+            const unsigned dst = static_cast<unsigned>(__cvta_generic_to_shared(ss + i));
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(gs + i) : "memory");
+        }
     }
+}
+__device__ __forceinline__ void sched_span_wait() {
+    asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
     __syncwarp();
 }
 
@@ -2090,9 +2122,29 @@ __device__ __forceinline__ void sched_body(const SchedArgs& A, char* smem_dyn, C
     constexpr bool scoped = SCOPED;  // task-scoped baselines: distmm-mt, task-level-optimus
     bool ok = true;
     WS_PH_START(tg);
-    if constexpr (PHASE >= 2) {  // resume the plan where the previous phase left it
+    if constexpr (PHASE == 2) {
+        // The bisection phase moves only what it touches: it reads the valid
+        // sets, levels, level members and curve indices, and writes the
+        // discretized bi-points and per-level c*/errors; phase 3 then restores
+        // the whole slot (phase 1's state with these spans overwritten).
         int ok_i = 0;
-        sched_state_io(false, gstate, C.sm, A.SL.bytes, ctl, ok_i, C.K, lane);
+        sched_state_hdr(false, gstate, ctl, ok_i, C.K, lane);
+        ok = ok_i != 0;
+        if (ok && !decoupled && !scoped && C.K <= 32) {
+            const SmLayout& L = A.SL;
+            sched_span_io(false, gstate, C.sm, L.valid, L.credit, lane);
+            sched_span_io(false, gstate, C.sm, L.level, L.up_n, lane);
+            sched_span_io(false, gstate, C.sm, L.lvl_mem, L.absorb, lane);
+            sched_span_io(false, gstate, C.sm, L.lvl_begin, L.cstar_sm, lane);
+            sched_span_wait();
+            s_alloc_concurrent<DM>(C, ctl->i1);
+            sched_span_io(true, gstate, C.sm, L.up_n, L.sumlay, lane);
+            sched_span_io(true, gstate, C.sm, L.cstar_sm, L.tk, lane);
+        }
+        return;
+    } else if constexpr (PHASE == 3) {  // resume the plan where the previous phases left it
+        int ok_i = 0;
+        sched_state_io(false, gstate, C.sm, sched_state_bytes(A.SL), ctl, ok_i, C.K, lane);
         ok = ok_i != 0;
     } else {
     if (R.n_mod == 0 && R.n_tasks == 0) {
@@ -2129,12 +2181,12 @@ __device__ __forceinline__ void sched_body(const SchedArgs& A, char* smem_dyn, C
     WS_PH_STOP(tg, 11);
     }
     const bool conc = C.K <= 32;  // every level's bisection at once
-    if constexpr (PHASE == 0 || PHASE == 2) {
+    if constexpr (PHASE == 0) {
         if (ok && !decoupled && !scoped && conc) s_alloc_concurrent<DM>(C, ctl->i1);
     }
-    if constexpr (PHASE == 1 || PHASE == 2) {  // hand the plan to the next phase
+    if constexpr (PHASE == 1) {  // hand the plan to the next phase
         int ok_i = ok;
-        sched_state_io(true, gstate, C.sm, A.SL.bytes, ctl, ok_i, C.K, lane);
+        sched_state_io(true, gstate, C.sm, sched_state_bytes(A.SL), ctl, ok_i, C.K, lane);
         return;
     }
     int n_levels = 0, nW = 0, nE = 0, KE = 0, n_pg = 0;
