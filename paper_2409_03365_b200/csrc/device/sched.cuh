@@ -105,17 +105,12 @@ __host__ __device__ inline SmLayout make_sm_layout(int M, bool scoped = false, i
         return at;
     };
     const int T = 2 * M;
-    L.adj = take(8 * M);
-    L.tmask = take(8 * M);
-    L.predk = take(8 * M);
+    // the part phases 2 and 3 read (phase-split launches carry it between
+    // the phase kernels: sched_state_bytes) ...
     L.pred_r = take(8 * M);
     L.succ_r = take(8 * M);
     L.valid = take(mb * M);
     L.credit = take(8 * M);
-    L.indeg = take(4 * M);
-    L.keyrank = take(4 * M);
-    L.modat = take(4 * M);
-    L.kofm = take(4 * M);
     L.mod_of = take(4 * M);
     L.idrank = take(4 * M);
     L.by_rank = take(4 * M);
@@ -135,6 +130,16 @@ __host__ __device__ inline SmLayout make_sm_layout(int M, bool scoped = false, i
     L.aerr_x = take(8 * M);
     L.aerr_y = take(8 * M);
     L.aerr = take(4 * M);
+    // ... graph construction scratch and the task masks, read after phase 1
+    // only by the task-scoped baselines (which run unsplit) ...
+    L.adj = take(8 * M);
+    L.tmask = take(8 * M);
+    L.predk = take(8 * M);
+    L.indeg = take(4 * M);
+    L.keyrank = take(4 * M);
+    L.modat = take(4 * M);
+    L.kofm = take(4 * M);
+    // ... and the wave-scheduling scratch (written by phase 3 before it is read)
     L.tk = take(4 * T);
     L.tn = take(4 * T);
     L.tl = take(4 * T);
@@ -2018,10 +2023,9 @@ __device__ bool s_distmm(SCtx& C, char* rec, const RecLayout& RL, int& nW, int& 
 // Warp copy of a slot's shared working set to / from its global state slot
 // (16-byte words; SL.bytes is a multiple of 16) plus the control block and
 // the flags that live in registers between the phases.
-// Bytes of the working set that travel from phase 1 to phase 3: everything
-// before the wave-scheduling scratch (tk .. ord, written by phase 3 before it
-// is read) and the task-scoped arrays (the scoped baselines run unsplit).
-__host__ __device__ inline int sched_state_bytes(const SmLayout& L) { return (L.tk + 15) & ~15; }
+// Bytes of the working set that travel from phase 1 to phase 3: the layout's
+// leading part, up to the phase-1 scratch (make_sm_layout).
+__host__ __device__ inline int sched_state_bytes(const SmLayout& L) { return (L.adj + 15) & ~15; }
 
 // The state slot's header: the warp's Ctl, the plan's ok flag and MetaOp count.
 __device__ __forceinline__ void sched_state_hdr(bool save, char* g, Ctl* ctl, int& ok, int& K, int lane) {
@@ -2139,7 +2143,7 @@ __device__ __forceinline__ void sched_body(const SchedArgs& A, char* smem_dyn, C
             sched_span_wait();
             s_alloc_concurrent<DM>(C, ctl->i1);
             sched_span_io(true, gstate, C.sm, L.up_n, L.sumlay, lane);
-            sched_span_io(true, gstate, C.sm, L.cstar_sm, L.tk, lane);
+            sched_span_io(true, gstate, C.sm, L.cstar_sm, L.adj, lane);
         }
         return;
     } else if constexpr (PHASE == 3) {  // resume the plan where the previous phases left it
