@@ -459,6 +459,7 @@ int launch_pair(ws_ctx* ctx, cudaStream_t st, const LaunchCaps& lc, const FitOut
     const int mb = wide ? static_cast<int>(sizeof(DevMask<4>)) : 8;
     const int pw = wide ? 1 : kPlaceWarps;
     S.SL = make_sm_layout(lc.M, lc.scoped, lc.T, mb);
+    S.warp_smem = S.SL.bytes;
     // (a compile-time layout for k_sched, as k_place has, measured slower: the
     // fixed class's larger working set costs occupancy and phase-state traffic)
     S.scoped_ok = lc.scoped ? 1 : 0;
@@ -547,26 +548,31 @@ int launch_pair(ws_ctx* ctx, cudaStream_t st, const LaunchCaps& lc, const FitOut
         if (cnt <= 0) break;
         S.plan_ids = ids + base;
         S.n_launch = cnt;
+        SchedArgs S1 = S;  // the first k_sched kernel: the unsplit one, or phase 1
+        S1.warp_smem = split ? sched_phase_bytes(S.SL, 1) : S.SL.bytes;
         if (pdl && c == 0) {  // right behind k_fit: programmatic dependent launch
             cudaLaunchConfig_t cfg{};
             cfg.gridDim = dim3((cnt + kSchedWarps - 1) / kSchedWarps);
             cfg.blockDim = dim3(32 * kSchedWarps);
-            cfg.dynamicSmemBytes = kSchedWarps * S.SL.bytes;
+            cfg.dynamicSmemBytes = kSchedWarps * S1.warp_smem;
             cfg.stream = st;
             cudaLaunchAttribute attr[1];
             attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
             attr[0].val.programmaticStreamSerializationAllowed = 1;
             cfg.attrs = attr;
             cfg.numAttrs = 1;
-            CK(cudaLaunchKernelEx(&cfg, split ? ksched1 : ksched, S));
+            CK(cudaLaunchKernelEx(&cfg, split ? ksched1 : ksched, S1));
         } else {
             (split ? ksched1 : ksched)<<<(cnt + kSchedWarps - 1) / kSchedWarps, 32 * kSchedWarps,
-                                         kSchedWarps * S.SL.bytes, st>>>(S);
+                                         kSchedWarps * S1.warp_smem, st>>>(S1);
         }
         ctx->launches++;
         if (split) {
-            ksched2<<<(cnt + kSchedWarps - 1) / kSchedWarps, 32 * kSchedWarps, kSchedWarps * S.SL.bytes, st>>>(S);
-            ksched3<<<(cnt + kSchedWarps - 1) / kSchedWarps, 32 * kSchedWarps, kSchedWarps * S.SL.bytes, st>>>(S);
+            SchedArgs S2 = S1, S3 = S1;
+            S2.warp_smem = sched_phase_bytes(S.SL, 2);
+            S3.warp_smem = S.SL.bytes;
+            ksched2<<<(cnt + kSchedWarps - 1) / kSchedWarps, 32 * kSchedWarps, kSchedWarps * S2.warp_smem, st>>>(S2);
+            ksched3<<<(cnt + kSchedWarps - 1) / kSchedWarps, 32 * kSchedWarps, kSchedWarps * S3.warp_smem, st>>>(S3);
             ctx->launches += 2;
         }
         if (lc.scoped) {  // the batch's distmm-mt plans (each instance skips the other's plans)

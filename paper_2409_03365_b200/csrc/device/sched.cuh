@@ -197,6 +197,8 @@ struct SchedArgs {
     // shared working set, control block and flags between the phases
     char* state;
     long long state_stride;  // bytes per slot: SL.bytes + kSchedStateHdr
+    int warp_smem;           // dynamic shared bytes per warp of this launch (a phase kernel
+                             // gets only the layout prefix it touches: sched_phase_bytes)
 };
 
 // bytes before the saved shared working set of a phase-split slot: Ctl + flags
@@ -2027,6 +2029,14 @@ __device__ bool s_distmm(SCtx& C, char* rec, const RecLayout& RL, int& nW, int& 
 // leading part, up to the phase-1 scratch (make_sm_layout).
 __host__ __device__ inline int sched_state_bytes(const SmLayout& L) { return (L.adj + 15) & ~15; }
 
+// Shared bytes per warp a k_sched kernel needs: phase 1 works below the
+// wave-scheduling scratch, phase 2 inside the persistent part, phase 3 (and
+// the unsplit kernel) on the whole layout.  Smaller phase kernels fit more
+// blocks per SM where shared memory is their occupancy limit.
+__host__ __device__ inline int sched_phase_bytes(const SmLayout& L, int phase) {
+    return phase == 1 ? ((L.tk + 15) & ~15) : phase == 2 ? sched_state_bytes(L) : L.bytes;
+}
+
 // The state slot's header: the warp's Ctl, the plan's ok flag and MetaOp count.
 __device__ __forceinline__ void sched_state_hdr(bool save, char* g, Ctl* ctl, int& ok, int& K, int lane) {
     int* flags = reinterpret_cast<int*>(g + sizeof(Ctl));
@@ -2115,7 +2125,7 @@ __device__ __forceinline__ void sched_body(const SchedArgs& A, char* smem_dyn, C
     C.R = &R;
     C.F = &A.fit;
     C.L = &A.SL;
-    C.sm = smem_dyn + wid * A.SL.bytes;
+    C.sm = smem_dyn + wid * A.warp_smem;
     C.ctl = ctl;
     C.lane = lane;
     C.N = R.n_dev;
