@@ -2347,12 +2347,28 @@ __device__ __forceinline__ void sched_body(const SchedArgs& A, char* smem_dyn, C
 
 // DM: valid-allocation set type (uint64_t: N <= 64; DevMask<4>: N <= 256);
 // PHASE: 0 whole, 1..3 the phase-split launches (sched_body)
-template <class DM = uint64_t, int PHASE = 0>
-#ifdef WS_SCHED_MINB
-__global__ void __launch_bounds__(32 * kSchedWarps, WS_SCHED_MINB) k_sched(SchedArgs A) {
-#else
-__global__ void __launch_bounds__(32 * kSchedWarps) k_sched(SchedArgs A) {
+#ifndef WS_SCHED_MINB
+#define WS_SCHED_MINB 0  /* 0: no resident-block target (the compiler picks the register budget) */
 #endif
+#ifndef WS_SCHED1_MINB
+#define WS_SCHED1_MINB WS_SCHED_MINB
+#endif
+#ifndef WS_SCHED2_MINB
+// phase 2 (bisection): 7 blocks per SM (<= 72 registers) -- measured on the
+// 100k sweep: unbounded (90 registers, 5 blocks) 4.34 ms k_sched, 6 blocks
+// 4.20, 7 blocks 4.13, 8 blocks 4.13, 10 blocks 4.50 (spills)
+#define WS_SCHED2_MINB 7
+#endif
+#ifndef WS_SCHED3_MINB
+#define WS_SCHED3_MINB WS_SCHED_MINB
+#endif
+// resident-block targets per phase kernel (register budgets; tuning builds)
+template <int PHASE>
+constexpr int sched_minb() {
+    return PHASE == 1 ? WS_SCHED1_MINB : PHASE == 2 ? WS_SCHED2_MINB : PHASE == 3 ? WS_SCHED3_MINB : WS_SCHED_MINB;
+}
+template <class DM = uint64_t, int PHASE = 0>
+__global__ void __launch_bounds__(32 * kSchedWarps, sched_minb<PHASE>()) k_sched(SchedArgs A) {
     extern __shared__ __align__(16) char smem_dyn[];
     __shared__ Ctl ctl_s[kSchedWarps];
     sched_body<false, DM, PHASE>(A, smem_dyn, ctl_s);
