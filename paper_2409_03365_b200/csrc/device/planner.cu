@@ -1161,10 +1161,16 @@ int host_range(ws_ctx* ctx, const ws_batch* in, int P0, int P1, ws_plan_result* 
     ctx->caps_hard = caps_from(bm, true);
     ctx->sim_cap = sim_total + 4096;  // == ws_sim_arena_bound(in)
     ctx->arena_cap = abase[C];
-    if (ctx->arena_cap > arena_cap) return fail(ctx, "ws_plan_batch_host: arena buffer too small");
+    if (ctx->arena_cap > arena_cap) {
+        cudaStreamSynchronize(sh);  // chunk 0's copy reads the caller's buffers: done before returning
+        return fail(ctx, "ws_plan_batch_host: arena buffer too small");
+    }
     ctx->small_counters = nullptr;
     FitOut fo;
-    if (prepare_plan(ctx, fo, st)) return 1;
+    if (prepare_plan(ctx, fo, st)) {
+        cudaStreamSynchronize(sh);
+        return 1;
+    }
     auto* counters = ctx->counters_dev();
     t_prep = hclk::now();
     CK(cudaMemcpyAsync(tops, ctx->host_tops, 8ull * C, cudaMemcpyHostToDevice, sh));
